@@ -1,0 +1,213 @@
+/*
+ * esrnn_b200.h — C-ABI of the B200-native ES-RNN training / forecasting engine.
+ *
+ * This is the drop-in boundary for the reference's hot path: every entry point
+ * below replaces one member of `esrnn::Trainer`
+ * (/root/reference/proj/include/esrnn/trainer.hpp) or a free function it owns.
+ * The C++ class `esrnn::Trainer` in include/esrnn_b200/trainer.hpp (same API as
+ * the reference) is a thin header-only wrapper over these functions; Python
+ * binds them with ctypes (paper_1907_03329_b200/_native.py).
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; every buffer is caller-owned host memory,
+ *    copied in/out synchronously during the call (the engine owns all device
+ *    memory).  All real-valued buffers are fp64, like the reference's Matrix.
+ *  - Functions never throw across the ABI.  They return an `esrnn_status`
+ *    mirroring the reference's exception hierarchy (errors.hpp:9-67); the
+ *    message is available from esrnn_last_error(handle) (or NULL handle for
+ *    errors raised by esrnn_trainer_create).
+ *  - A handle is single-threaded, like the reference Trainer.
+ *
+ * The same ABI is implemented by three libraries:
+ *    libesrnn_b200.so          the product (CUDA sm_100a kernels)
+ *    oracle/liboracle_esrnn.so the plain-C restatement (test oracle only)
+ *    oracle/_ref/libesrnn_ref.so  the reference's own headers behind a shim
+ *                                 (test oracle / CPU baseline only)
+ */
+#ifndef ESRNN_B200_H
+#define ESRNN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ESRNN_ABI_VERSION 1
+#define ESRNN_MAX_BLOCKS 8
+#define ESRNN_MAX_LAYERS 16
+#define ESRNN_NUM_CATEGORIES 6      /* data.hpp:21 kNumCategories */
+
+/* Status codes: one per esrnn::Error subclass (errors.hpp:9-67) plus device errors. */
+typedef enum esrnn_status {
+    ESRNN_OK = 0,
+    ESRNN_ERROR = 1,                  /* esrnn::Error                   errors.hpp:9   */
+    ESRNN_PARSE_ERROR = 2,            /* ParseError                     errors.hpp:15  */
+    ESRNN_VALIDATION_ERROR = 3,       /* ValidationError                errors.hpp:22  */
+    ESRNN_SHAPE_ERROR = 4,            /* ShapeError                     errors.hpp:28  */
+    ESRNN_INSUFFICIENT_LENGTH = 5,    /* InsufficientLengthError        errors.hpp:34  */
+    ESRNN_NUMERIC_DOMAIN_ERROR = 6,   /* NumericDomainError             errors.hpp:40  */
+    ESRNN_CONFIG_ERROR = 7,           /* ConfigError                    errors.hpp:46  */
+    ESRNN_CONTRACT_ERROR = 8,         /* ContractError                  errors.hpp:52  */
+    ESRNN_EQUIVALENCE_ERROR = 9,      /* EquivalenceError               errors.hpp:58  */
+    ESRNN_CHECKPOINT_ERROR = 10,      /* CheckpointError                errors.hpp:64  */
+    ESRNN_CUDA_ERROR = 11,            /* device / driver failure (no reference analogue) */
+    ESRNN_NCCL_ERROR = 12             /* collective failure (no reference analogue)      */
+} esrnn_status;
+
+/* Compute precision of the device path (B200 extension; the reference is fp64). */
+enum { ESRNN_FP32 = 0, ESRNN_FP64 = 1 };
+
+/* esrnn::FrequencyProfile (data.hpp:60-118).  dilation_blocks is flattened:
+ * block b owns layers [sum(block_len[0..b)), +block_len[b]). */
+typedef struct esrnn_profile {
+    int32_t frequency;            /* 0 Yearly, 1 Quarterly, 2 Monthly (data.hpp:19) */
+    int32_t seasonality_length;   /* S */
+    int32_t horizon;              /* O */
+    int32_t input_window;         /* I */
+    int32_t hidden_size;          /* H */
+    int32_t min_length;           /* C */
+    int32_t n_blocks;
+    int32_t block_len[ESRNN_MAX_BLOCKS];
+    int32_t dilations[ESRNN_MAX_LAYERS];
+} esrnn_profile;
+
+/* esrnn::TrainConfig (trainer.hpp:22-44) plus B200 extensions at the end;
+ * zero-initialised extensions reproduce the reference's behaviour except
+ * `precision`, whose zero value selects the fp32 performance path. */
+typedef struct esrnn_train_config {
+    int32_t epochs;
+    int32_t batch_size;
+    double learning_rate_network;
+    double learning_rate_per_series;
+    double tau;
+    int32_t has_gradient_clip;    /* std::optional<double> gradient_clip */
+    double gradient_clip;
+    uint64_t seed;
+    int32_t attach_es_state;
+    int32_t patience;
+    double min_delta;
+    /* --- B200 extensions --- */
+    int32_t precision;            /* ESRNN_FP32 | ESRNN_FP64 */
+    int32_t max_batch_size;       /* 0 => 2048, the reference cap (trainer.hpp:36) */
+    int32_t device;               /* CUDA device ordinal */
+    int32_t use_graphs;           /* 0 => default (on); <0 => off (debug) */
+} esrnn_train_config;
+
+/* Series-sharded data parallelism (B200 extension).  Rank r owns
+ * dataset rows [floor(r*N/W), floor((r+1)*N/W)); per-series parameters live only
+ * on their owner; the shared-gradient buffer is all-reduced with NCCL. */
+typedef struct esrnn_dist {
+    int32_t rank;
+    int32_t world_size;
+    uint8_t nccl_unique_id[128];  /* from esrnn_nccl_unique_id() on rank 0 */
+} esrnn_dist;
+
+/* One named network array in StackWeights::for_each_param order (network.hpp:62-74). */
+typedef struct esrnn_param_info {
+    char name[32];
+    int32_t rows;
+    int32_t cols;
+    int64_t offset;               /* into the flat weight vector */
+} esrnn_param_info;
+
+typedef struct esrnn_trainer esrnn_trainer;
+
+const char* esrnn_version(void);
+int32_t esrnn_abi_version(void);
+/* Message of the last failing call on `t` (t == NULL: last failing create, per thread). */
+const char* esrnn_last_error(const esrnn_trainer* t);
+
+/* Trainer::Trainer(vector<SeriesRecord>, FrequencyProfile, TrainConfig)  trainer.hpp:159-200.
+ * values: n_series x length row-major; category: n_series entries in [0,6) or -1
+ * (unset -> Category::Other, trainer.hpp:186).  dist may be NULL (single GPU).
+ * In sharded mode every rank passes the full dataset; only the owned rows are
+ * uploaded.  Consumes the trainer RNG exactly like init_stack_weights
+ * (network.hpp:89-116). */
+esrnn_status esrnn_trainer_create(const esrnn_profile* profile, const esrnn_train_config* cfg,
+                                  int64_t n_series, int32_t length, const double* values,
+                                  const int32_t* category, const esrnn_dist* dist,
+                                  esrnn_trainer** out);
+void esrnn_trainer_destroy(esrnn_trainer* t);
+
+/* Rows owned by this rank (all rows when unsharded). */
+esrnn_status esrnn_trainer_shard(const esrnn_trainer* t, int64_t* row_begin, int64_t* row_end);
+
+/* StackWeights layout: number of arrays / values, and one array's info. */
+esrnn_status esrnn_trainer_param_count(const esrnn_trainer* t, int32_t* n_arrays, int64_t* n_values);
+esrnn_status esrnn_trainer_param_info(const esrnn_trainer* t, int32_t index, esrnn_param_info* out);
+
+/* Trainer::weights() (trainer.hpp:205-206) as a flat vector in for_each_param order. */
+esrnn_status esrnn_trainer_get_weights(esrnn_trainer* t, double* flat, int64_t count);
+/* Trainer::set_weights (trainer.hpp:415-432): count mismatch -> ESRNN_CHECKPOINT_ERROR. */
+esrnn_status esrnn_trainer_set_weights(esrnn_trainer* t, const double* flat, int64_t count);
+
+/* Trainer::per_series_params(i) (trainer.hpp:210-211) for rows [row_begin, row_begin+n)
+ * (global row numbers; must be owned).  seas_raw is n x S row-major. */
+esrnn_status esrnn_trainer_get_per_series(esrnn_trainer* t, int64_t row_begin, int64_t n,
+                                          double* alpha_raw, double* gamma_raw, double* seas_raw);
+/* Trainer::set_per_series (trainer.hpp:434-445), same addressing. */
+esrnn_status esrnn_trainer_set_per_series(esrnn_trainer* t, int64_t row_begin, int64_t n,
+                                          const double* alpha_raw, const double* gamma_raw,
+                                          const double* seas_raw);
+
+/* Trainer::train_epoch (trainer.hpp:234-243): shuffle (make_batches, trainer.hpp:82-102)
+ * with the trainer RNG, one step per batch with updates; returns the
+ * mask-weighted mean pinball loss. */
+esrnn_status esrnn_trainer_train_epoch(esrnn_trainer* t, double* mean_loss);
+
+/* One batch through build_graph (trainer.hpp:484-591) — the engine behind
+ * batch_loss (:338), batch_gradients (:308) and step (:593).
+ *   B, rows[B], anchors[B], mask[B*O] (NULL = all ones)         in
+ *   flags: ESRNN_BATCH_GRADS (backward), ESRNN_BATCH_UPDATE (apply_updates)
+ *   loss, mask_count                                            out (nullable)
+ *   inputs[B*(I+6)], targets[B*O], seasonality_slices[B*O], anchor_levels[B]
+ *                                                               out (nullable) — WindowBatch fields
+ *   net_grads[n_values] (for_each_param order, incl. the exact zeros)  out (nullable)
+ *   n_slots, slot_rows[B], ps_grads[B*(2+S)] (per slot: alpha_raw, gamma_raw, seas_raw[S])
+ *                                                               out (nullable; slots in first-appearance
+ *                                                               order, trainer.hpp:494-501)
+ * In sharded mode every rank passes the same global batch; the loss/network
+ * gradients are global, per-series outputs cover the local slots only. */
+enum { ESRNN_BATCH_GRADS = 1, ESRNN_BATCH_UPDATE = 2 };
+esrnn_status esrnn_trainer_run_batch(esrnn_trainer* t, int32_t B, const int32_t* rows,
+                                     const int32_t* anchors, const double* mask, int32_t flags,
+                                     double* loss, double* mask_count, double* inputs,
+                                     double* targets, double* seasonality_slices,
+                                     double* anchor_levels, double* net_grads, int32_t* n_slots,
+                                     int32_t* slot_rows, double* ps_grads);
+
+/* Trainer::forecast_at(drop_tail) (trainer.hpp:248-288): real-scale O-step
+ * forecasts for the owned rows, out is n_local x O row-major. */
+esrnn_status esrnn_trainer_forecast(esrnn_trainer* t, int64_t drop_tail, double* out);
+
+/* Trainer::validate (trainer.hpp:292-305): forecasts (nullable, n_local x O),
+ * per-series sMAPE (nullable, n_local) and the mean over ALL series (global). */
+esrnn_status esrnn_trainer_validate(esrnn_trainer* t, double* forecasts, double* smape_per_series,
+                                    double* mean_smape);
+
+/* HWState of hybrid_primer(values[0:t_len], per_series_params(row)) (holt_winters.hpp:66-97):
+ * levels[t_len], seasonalities[t_len + S].  Inspection hook for the scan KATs. */
+esrnn_status esrnn_trainer_hw_state(esrnn_trainer* t, int64_t row, int64_t t_len, double* levels,
+                                    double* seasonalities);
+
+/* Device time in ms of the last train_epoch / run_batch / forecast / validate
+ * call, measured with CUDA events on the engine's stream (0 for CPU builds). */
+esrnn_status esrnn_trainer_last_device_ms(const esrnn_trainer* t, double* ms);
+/* Number of kernels the engine launched since creation (graph nodes counted). */
+esrnn_status esrnn_trainer_kernel_launches(const esrnn_trainer* t, int64_t* n);
+
+/* NCCL bootstrap for esrnn_dist (returns ESRNN_NCCL_ERROR in builds without NCCL). */
+esrnn_status esrnn_nccl_unique_id(uint8_t out[128]);
+
+/* Synthetic M4-shaped data, bit-identical to the reference's
+ * testutil::make_multiplicative_series (tests/helpers.hpp:148-172) consumed in
+ * order from Rng(seed): values n x length, category n. */
+esrnn_status esrnn_make_synthetic(uint64_t seed, int64_t n, int32_t length, int32_t season_length,
+                                  double noise_sigma, double* values, int32_t* category);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ESRNN_B200_H */

@@ -1,0 +1,364 @@
+// TEST INFRASTRUCTURE — not product code.
+//
+// Exposes the UNMODIFIED reference implementation (/root/reference/proj/include,
+// header-only C++20) behind the engine's C-ABI (include/esrnn_b200.h) so tests and
+// bench.py's reference arm can drive the reference and the B200 engine through
+// the same calls.  Built by oracle/Makefile into oracle/_ref/libesrnn_ref.so; the
+// reference sources are compiled where they lie (never copied).
+//
+// `private` is widened only so build_graph/step (trainer.hpp:484-600) and the
+// tape's slot order (trainer.hpp:463-470) are reachable for slot-ordered gradient
+// dumps and for step(update=true) on a caller-supplied batch.
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <string>
+#include <vector>
+
+// every standard header the reference pulls in, parsed before the access hack
+#include <algorithm>
+#include <array>
+#include <bit>
+#include <charconv>
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <functional>
+#include <initializer_list>
+#include <istream>
+#include <limits>
+#include <map>
+#include <numeric>
+#include <optional>
+#include <ostream>
+#include <random>
+#include <set>
+#include <span>
+#include <sstream>
+#include <stdexcept>
+#include <string_view>
+#include <utility>
+
+#define private public
+#include "esrnn/trainer.hpp"
+#undef private
+#include "helpers.hpp"
+
+#include "esrnn_b200.h"
+
+using namespace esrnn;
+
+struct esrnn_trainer {
+    std::unique_ptr<Trainer> tr;
+    std::string err;
+    double last_ms = 0.0;
+};
+
+namespace {
+
+thread_local std::string g_create_err;
+
+template <class Fn>
+esrnn_status guarded(std::string& err, Fn&& fn) {
+    try {
+        fn();
+        return ESRNN_OK;
+    } catch (const ParseError& e) { err = e.what(); return ESRNN_PARSE_ERROR; }
+    catch (const ValidationError& e) { err = e.what(); return ESRNN_VALIDATION_ERROR; }
+    catch (const ShapeError& e) { err = e.what(); return ESRNN_SHAPE_ERROR; }
+    catch (const InsufficientLengthError& e) { err = e.what(); return ESRNN_INSUFFICIENT_LENGTH; }
+    catch (const NumericDomainError& e) { err = e.what(); return ESRNN_NUMERIC_DOMAIN_ERROR; }
+    catch (const ConfigError& e) { err = e.what(); return ESRNN_CONFIG_ERROR; }
+    catch (const ContractError& e) { err = e.what(); return ESRNN_CONTRACT_ERROR; }
+    catch (const EquivalenceError& e) { err = e.what(); return ESRNN_EQUIVALENCE_ERROR; }
+    catch (const CheckpointError& e) { err = e.what(); return ESRNN_CHECKPOINT_ERROR; }
+    catch (const Error& e) { err = e.what(); return ESRNN_ERROR; }
+    catch (const std::exception& e) { err = e.what(); return ESRNN_ERROR; }
+}
+
+FrequencyProfile to_profile(const esrnn_profile& p) {
+    FrequencyProfile f;
+    f.frequency = static_cast<Frequency>(p.frequency);
+    f.seasonality_length = p.seasonality_length;
+    f.horizon = p.horizon;
+    f.input_window = p.input_window;
+    f.hidden_size = p.hidden_size;
+    f.min_length = p.min_length;
+    f.dilation_blocks.clear();
+    int layer = 0;
+    for (int b = 0; b < p.n_blocks; ++b) {
+        std::vector<int> blk;
+        for (int j = 0; j < p.block_len[b]; ++j) blk.push_back(p.dilations[layer++]);
+        f.dilation_blocks.push_back(blk);
+    }
+    return f;
+}
+
+TrainConfig to_config(const esrnn_train_config& c) {
+    TrainConfig t;
+    t.epochs = c.epochs;
+    t.batch_size = c.batch_size;
+    t.learning_rate_network = c.learning_rate_network;
+    t.learning_rate_per_series = c.learning_rate_per_series;
+    t.tau = c.tau;
+    if (c.has_gradient_clip) t.gradient_clip = c.gradient_clip;
+    else t.gradient_clip.reset();
+    t.seed = c.seed;
+    t.attach_es_state = c.attach_es_state != 0;
+    t.patience = c.patience;
+    t.min_delta = c.min_delta;
+    return t;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* esrnn_version(void) { return "reference-shim (proj/include/esrnn, fp64 CPU)"; }
+int32_t esrnn_abi_version(void) { return ESRNN_ABI_VERSION; }
+
+const char* esrnn_last_error(const esrnn_trainer* t) {
+    return t ? t->err.c_str() : g_create_err.c_str();
+}
+
+esrnn_status esrnn_trainer_create(const esrnn_profile* profile, const esrnn_train_config* cfg,
+                                  int64_t n_series, int32_t length, const double* values,
+                                  const int32_t* category, const esrnn_dist* dist,
+                                  esrnn_trainer** out) {
+    *out = nullptr;
+    if (dist && dist->world_size > 1) {
+        g_create_err = "reference shim: no sharded mode (the reference is single-threaded)";
+        return ESRNN_CONFIG_ERROR;
+    }
+    auto h = std::make_unique<esrnn_trainer>();
+    esrnn_status st = guarded(g_create_err, [&] {
+        std::vector<SeriesRecord> recs(static_cast<std::size_t>(n_series));
+        for (int64_t i = 0; i < n_series; ++i) {
+            recs[i].id = "S" + std::to_string(i);
+            if (category && category[i] >= 0) recs[i].category = static_cast<Category>(category[i]);
+            recs[i].values.assign(values + i * length, values + (i + 1) * length);
+        }
+        h->tr = std::make_unique<Trainer>(std::move(recs), to_profile(*profile), to_config(*cfg));
+    });
+    if (st == ESRNN_OK) *out = h.release();
+    return st;
+}
+
+void esrnn_trainer_destroy(esrnn_trainer* t) { delete t; }
+
+esrnn_status esrnn_trainer_shard(const esrnn_trainer* t, int64_t* b, int64_t* e) {
+    *b = 0;
+    *e = static_cast<int64_t>(t->tr->series_count());
+    return ESRNN_OK;
+}
+
+esrnn_status esrnn_trainer_param_count(const esrnn_trainer* t, int32_t* n_arrays, int64_t* n_values) {
+    int32_t na = 0;
+    int64_t nv = 0;
+    t->tr->weights().for_each_param([&](const std::string&, const Matrix& m) {
+        ++na;
+        nv += static_cast<int64_t>(m.size());
+    });
+    *n_arrays = na;
+    *n_values = nv;
+    return ESRNN_OK;
+}
+
+esrnn_status esrnn_trainer_param_info(const esrnn_trainer* t, int32_t index, esrnn_param_info* out) {
+    int32_t i = 0;
+    int64_t off = 0;
+    bool found = false;
+    t->tr->weights().for_each_param([&](const std::string& name, const Matrix& m) {
+        if (i == index) {
+            std::memset(out, 0, sizeof *out);
+            std::strncpy(out->name, name.c_str(), sizeof(out->name) - 1);
+            out->rows = static_cast<int32_t>(m.rows());
+            out->cols = static_cast<int32_t>(m.cols());
+            out->offset = off;
+            found = true;
+        }
+        off += static_cast<int64_t>(m.size());
+        ++i;
+    });
+    return found ? ESRNN_OK : ESRNN_SHAPE_ERROR;
+}
+
+esrnn_status esrnn_trainer_get_weights(esrnn_trainer* t, double* flat, int64_t count) {
+    int64_t off = 0;
+    t->tr->weights().for_each_param([&](const std::string&, const Matrix& m) {
+        for (double v : m.data())
+            if (off < count) flat[off++] = v;
+    });
+    return ESRNN_OK;
+}
+
+esrnn_status esrnn_trainer_set_weights(esrnn_trainer* t, const double* flat, int64_t count) {
+    return guarded(t->err, [&] {
+        StackWeights w = t->tr->weights();
+        int64_t off = 0;
+        w.for_each_param([&](const std::string&, Matrix& m) {
+            for (double& v : m.data()) v = (off < count) ? flat[off] : 0.0, ++off;
+        });
+        if (off != count) throw CheckpointError("checkpoint network shapes incompatible with configuration");
+        t->tr->set_weights(std::move(w));
+    });
+}
+
+esrnn_status esrnn_trainer_get_per_series(esrnn_trainer* t, int64_t row_begin, int64_t n,
+                                          double* a, double* g, double* s) {
+    return guarded(t->err, [&] {
+        for (int64_t i = 0; i < n; ++i) {
+            const PerSeriesParams& p = t->tr->per_series_params(static_cast<std::size_t>(row_begin + i));
+            if (a) a[i] = p.alpha_raw;
+            if (g) g[i] = p.gamma_raw;
+            const int S = p.season_length();
+            if (s)
+                for (int j = 0; j < S; ++j) s[i * S + j] = p.init_seasonality_raw[j];
+        }
+    });
+}
+
+esrnn_status esrnn_trainer_set_per_series(esrnn_trainer* t, int64_t row_begin, int64_t n,
+                                          const double* a, const double* g, const double* s) {
+    return guarded(t->err, [&] {
+        for (int64_t i = 0; i < n; ++i) {
+            PerSeriesParams& p = t->tr->per_series_params(static_cast<std::size_t>(row_begin + i));
+            if (a) p.alpha_raw = a[i];
+            if (g) p.gamma_raw = g[i];
+            const int S = p.season_length();
+            if (s)
+                for (int j = 0; j < S; ++j) p.init_seasonality_raw[j] = s[i * S + j];
+        }
+    });
+}
+
+esrnn_status esrnn_trainer_train_epoch(esrnn_trainer* t, double* mean_loss) {
+    return guarded(t->err, [&] {
+        const auto t0 = std::chrono::steady_clock::now();
+        *mean_loss = t->tr->train_epoch();
+        t->last_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    });
+}
+
+esrnn_status esrnn_trainer_run_batch(esrnn_trainer* t, int32_t B, const int32_t* rows,
+                                     const int32_t* anchors, const double* mask, int32_t flags,
+                                     double* loss, double* mask_count, double* inputs,
+                                     double* targets, double* seas, double* levels,
+                                     double* net_grads, int32_t* n_slots, int32_t* slot_rows,
+                                     double* ps_grads) {
+    return guarded(t->err, [&] {
+        Trainer& tr = *t->tr;
+        const int O = tr.profile().horizon;
+        const int S = tr.profile().seasonality_length;
+        WindowBatch b;
+        for (int i = 0; i < B; ++i) {
+            b.series_rows.push_back(rows[i]);
+            b.anchors.push_back(anchors[i]);
+            b.ids.push_back("w");
+        }
+        b.mask = Matrix(static_cast<std::size_t>(B), static_cast<std::size_t>(O), 1.0);
+        if (mask) std::memcpy(b.mask.data().data(), mask, sizeof(double) * B * O);
+        const auto t0 = std::chrono::steady_clock::now();
+        double l;
+        if (flags & ESRNN_BATCH_GRADS) {
+            auto r = tr.step(b, (flags & ESRNN_BATCH_UPDATE) != 0);
+            l = r.loss;
+        } else {
+            l = tr.batch_loss(b);
+        }
+        t->last_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        auto& tb = tr.tape_build_;
+        if (loss) *loss = l;
+        if (mask_count) *mask_count = tb.mask_count;
+        if (inputs) std::memcpy(inputs, b.inputs.data().data(), sizeof(double) * b.inputs.size());
+        if (targets) std::memcpy(targets, b.targets.data().data(), sizeof(double) * b.targets.size());
+        if (seas) std::memcpy(seas, b.seasonality_slices.data().data(), sizeof(double) * b.seasonality_slices.size());
+        if (levels) std::memcpy(levels, b.anchor_levels.data(), sizeof(double) * b.anchor_levels.size());
+        const int k = static_cast<int>(tb.slot_series.size());
+        if (n_slots) *n_slots = k;
+        if (slot_rows)
+            for (int s = 0; s < k; ++s) slot_rows[s] = tb.slot_series[s];
+        if (flags & ESRNN_BATCH_GRADS) {
+            if (net_grads) {
+                int64_t off = 0;
+                for (const auto& leaf : tb.net_leaves)
+                    for (double v : leaf.grad().data()) net_grads[off++] = v;
+            }
+            if (ps_grads && tr.config().attach_es_state) {
+                for (int s = 0; s < k; ++s) {
+                    double* o = ps_grads + static_cast<int64_t>(s) * (2 + S);
+                    o[0] = tb.alpha_leaf.grad()(s, 0);
+                    o[1] = tb.gamma_leaf.grad()(s, 0);
+                    for (int j = 0; j < S; ++j) o[2 + j] = tb.seas_leaf.grad()(s, j);
+                }
+            }
+        }
+    });
+}
+
+esrnn_status esrnn_trainer_forecast(esrnn_trainer* t, int64_t drop_tail, double* out) {
+    return guarded(t->err, [&] {
+        const auto t0 = std::chrono::steady_clock::now();
+        ForecastResult fr = t->tr->forecast_at(static_cast<std::size_t>(drop_tail));
+        t->last_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        const int O = t->tr->profile().horizon;
+        for (std::size_t r = 0; r < fr.forecasts.size(); ++r)
+            for (int j = 0; j < O; ++j) out[r * O + j] = fr.forecasts[r][j];
+    });
+}
+
+esrnn_status esrnn_trainer_validate(esrnn_trainer* t, double* forecasts, double* smape_per_series,
+                                    double* mean_smape) {
+    return guarded(t->err, [&] {
+        const auto t0 = std::chrono::steady_clock::now();
+        ValidationResult v = t->tr->validate();
+        t->last_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        const int O = t->tr->profile().horizon;
+        for (std::size_t r = 0; r < v.forecasts.size(); ++r) {
+            if (forecasts)
+                for (int j = 0; j < O; ++j) forecasts[r * O + j] = v.forecasts[r][j];
+            if (smape_per_series) smape_per_series[r] = v.smape_per_series[r];
+        }
+        if (mean_smape) *mean_smape = v.mean_smape;
+    });
+}
+
+esrnn_status esrnn_trainer_hw_state(esrnn_trainer* t, int64_t row, int64_t t_len, double* levels,
+                                    double* seas) {
+    return guarded(t->err, [&] {
+        const auto& vals = t->tr->series(static_cast<std::size_t>(row)).values;
+        std::span<const double> ins(vals.data(), static_cast<std::size_t>(t_len));
+        HWState st = hybrid_primer(ins, t->tr->per_series_params(static_cast<std::size_t>(row)));
+        std::memcpy(levels, st.levels.data(), sizeof(double) * st.levels.size());
+        std::memcpy(seas, st.seasonalities.data(), sizeof(double) * st.seasonalities.size());
+    });
+}
+
+esrnn_status esrnn_trainer_last_device_ms(const esrnn_trainer* t, double* ms) {
+    *ms = t->last_ms;
+    return ESRNN_OK;
+}
+
+esrnn_status esrnn_trainer_kernel_launches(const esrnn_trainer*, int64_t* n) {
+    *n = 0;
+    return ESRNN_OK;
+}
+
+esrnn_status esrnn_nccl_unique_id(uint8_t*) {
+    g_create_err = "reference shim: no NCCL";
+    return ESRNN_NCCL_ERROR;
+}
+
+esrnn_status esrnn_make_synthetic(uint64_t seed, int64_t n, int32_t length, int32_t season_length,
+                                  double noise_sigma, double* values, int32_t* category) {
+    Rng rng(seed);
+    for (int64_t i = 0; i < n; ++i) {
+        SeriesRecord rec = testutil::make_multiplicative_series(rng, "S" + std::to_string(i), length,
+                                                                season_length, noise_sigma);
+        category[i] = static_cast<int32_t>(*rec.category);
+        for (int32_t t = 0; t < length; ++t) values[i * length + t] = rec.values[t];
+    }
+    return ESRNN_OK;
+}
+
+}  // extern "C"

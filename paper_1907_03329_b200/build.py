@@ -1,0 +1,86 @@
+"""In-tree build of the CUDA engine (sm_100a) and the test oracles.
+
+    python -m paper_1907_03329_b200.build      # or __graft_entry__.build()
+
+Outputs (git-ignored, travel to the GPU box with the snapshot):
+    paper_1907_03329_b200/libesrnn_b200.so     product: CUDA kernels + C-ABI
+    oracle/liboracle_esrnn.so                  test oracle (plain C)
+    oracle/_ref/libesrnn_ref.so                reference shim (only when /root/reference exists)
+    build/cpp_api_test                         C++ drop-in API test driver (tests/cpp)
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+PKG = ROOT / "paper_1907_03329_b200"
+CSRC = PKG / "csrc"
+INC = ROOT / "include"
+BUILD = ROOT / "build"
+LIB = PKG / "libesrnn_b200.so"
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+NVFLAGS = ["-std=c++17", "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC,-ffp-contract=off",
+           "-I" + str(INC), "-I" + str(CSRC)]
+
+
+def _run(cmd: list[str], cwd: Path | None = None) -> None:
+    print("+", " ".join(cmd), flush=True)
+    subprocess.run(cmd, check=True, cwd=cwd)
+
+
+def _stale(out: Path, deps: list[Path]) -> bool:
+    if not out.exists():
+        return True
+    t = out.stat().st_mtime
+    return any(d.stat().st_mtime > t for d in deps)
+
+
+def build_engine(force: bool = False) -> Path:
+    BUILD.mkdir(exist_ok=True)
+    deps = [*CSRC.glob("*.cu"), *CSRC.glob("*.cuh"), *CSRC.glob("*.cpp"), INC / "esrnn_b200.h"]
+    if not force and not _stale(LIB, deps):
+        return LIB
+    objs = []
+    for src in sorted(CSRC.glob("*.cu")):
+        obj = BUILD / (src.stem + ".o")
+        _run([NVCC, *NVFLAGS, "-Xptxas", "-v", "-c", str(src), "-o", str(obj)])
+        objs.append(str(obj))
+    for src in sorted(CSRC.glob("*.cpp")):
+        obj = BUILD / (src.stem + ".o")
+        _run(["g++", "-std=c++17", "-O2", "-fPIC", "-ffp-contract=off", "-I" + str(INC), "-c", str(src), "-o", str(obj)])
+        objs.append(str(obj))
+    _run([NVCC, *ARCH, "-shared", "-o", str(LIB), *objs, "-Xlinker", "-Bsymbolic",
+          "-L/usr/lib/x86_64-linux-gnu", "-lnccl"])
+    return LIB
+
+
+def build_oracle() -> None:
+    _run(["make", "-s", "all"], cwd=ROOT / "oracle")
+
+
+def build_cpp_tests() -> None:
+    src = ROOT / "tests" / "cpp" / "cpp_api_test.cpp"
+    if not src.exists():
+        return
+    out = BUILD / "cpp_api_test"
+    deps = [src, *(INC / "esrnn_b200").glob("*.hpp"), INC / "esrnn_b200.h"]
+    if not _stale(out, deps) and not _stale(out, [LIB]):
+        return
+    BUILD.mkdir(exist_ok=True)
+    _run(["g++", "-std=c++20", "-O2", "-I" + str(INC), str(src), "-o", str(out), "-L" + str(PKG), "-lesrnn_b200",
+          "-Wl,-rpath,$ORIGIN/../paper_1907_03329_b200"])
+
+
+def build_all(force: bool = False) -> None:
+    build_engine(force)
+    build_oracle()
+    build_cpp_tests()
+
+
+if __name__ == "__main__":
+    build_all(force="--force" in sys.argv)

@@ -1,0 +1,1161 @@
+// Host side of the B200 engine and the C-ABI (include/esrnn_b200.h).
+//
+// The host keeps everything the reference's Trainer keeps that is index/bookkeeping
+// work (profile, config, RNG stream, window lists, slot dedupe) and drives the device:
+// all arithmetic of the training step, forecast and validation runs in the sm_100a
+// kernels of kernels.cuh.  There is no CPU compute fallback: without a CUDA device the
+// create call fails with ESRNN_CUDA_ERROR.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <atomic>
+#include <climits>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "esrnn_b200.h"
+#include "kernels.cuh"
+
+using namespace esrnn_dev;
+
+namespace {
+
+// ------------------------------------------------------------------ errors
+struct ApiError : std::runtime_error {
+    esrnn_status code;
+    ApiError(esrnn_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] void raise(esrnn_status c, const char* fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    throw ApiError(c, buf);
+}
+
+#define CUDA_OK(expr)                                                                       \
+    do {                                                                                    \
+        cudaError_t e_ = (expr);                                                            \
+        if (e_ != cudaSuccess) raise(ESRNN_CUDA_ERROR, "%s: %s (%s:%d)", #expr,             \
+                                     cudaGetErrorString(e_), __FILE__, __LINE__);           \
+    } while (0)
+#define NCCL_OK(expr)                                                                       \
+    do {                                                                                    \
+        ncclResult_t r_ = (expr);                                                           \
+        if (r_ != ncclSuccess) raise(ESRNN_NCCL_ERROR, "%s: %s", #expr, ncclGetErrorString(r_)); \
+    } while (0)
+
+thread_local std::string g_create_err;
+
+// ------------------------------------------------------------------ host RNG
+// matrix.hpp:173-213: std::mt19937_64 with explicit bit draws.
+struct HostRng {
+    std::mt19937_64 gen;
+    explicit HostRng(uint64_t seed) : gen(seed) {}
+    double uniform() { return static_cast<double>(gen() >> 11) * 0x1.0p-53; }
+    double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
+    uint64_t below(uint64_t n) { return static_cast<uint64_t>((static_cast<unsigned __int128>(gen()) * n) >> 64); }
+};
+
+// ------------------------------------------------------------------ device buffer
+template <typename T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    void alloc(size_t count) {
+        free();
+        n = count;
+        if (count) CUDA_OK(cudaMalloc(&p, sizeof(T) * count));
+    }
+    void zero(cudaStream_t s) {
+        if (n) CUDA_OK(cudaMemsetAsync(p, 0, sizeof(T) * n, s));
+    }
+    void free() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    ~DBuf() { free(); }
+};
+
+template <typename T>
+struct PinnedBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    void reserve(size_t count) {
+        if (count <= n) return;
+        if (p) cudaFreeHost(p);
+        CUDA_OK(cudaMallocHost(&p, sizeof(T) * count));
+        n = count;
+    }
+    ~PinnedBuf() {
+        if (p) cudaFreeHost(p);
+    }
+};
+
+// One plan = ordered local windows + per-step slot lists + per-slot window CSR.
+struct HostPlan {
+    std::vector<int> w_row, w_anchor, w_slot, step_win_off, step_slot_off, slot_row, slot_win_off, slot_win;
+    std::vector<double> step_M;
+    int max_step_windows = 0, max_step_slots = 0;
+};
+
+struct DevPlan {
+    DBuf<int> w_row, w_anchor, w_slot, step_win_off, step_slot_off, slot_row, slot_win_off, slot_win;
+    DBuf<double> step_M;
+    DBuf<unsigned char> mask;
+    size_t cap_w = 0, cap_steps = 0, cap_slots = 0;
+    PlanDev view(bool with_mask) const {
+        PlanDev p;
+        p.w_row = w_row.p;
+        p.w_anchor = w_anchor.p;
+        p.w_slot = w_slot.p;
+        p.step_win_off = step_win_off.p;
+        p.step_slot_off = step_slot_off.p;
+        p.slot_row = slot_row.p;
+        p.slot_win_off = slot_win_off.p;
+        p.slot_win = slot_win.p;
+        p.step_M = step_M.p;
+        p.mask = with_mask ? mask.p : nullptr;
+        return p;
+    }
+};
+
+constexpr int kRows = 8;          // windows per K2 tile
+constexpr int kScanThreads = 64;  // K1 / K4 / K6 block
+
+// ------------------------------------------------------------------ engine
+struct EngineBase {
+    virtual ~EngineBase() = default;
+};
+
+}  // namespace
+
+struct esrnn_trainer {
+    // configuration (data.hpp:60-118, trainer.hpp:22-44)
+    esrnn_profile prof{};
+    esrnn_train_config cfg{};
+    int rank = 0, world = 1;
+    int N_global = 0, N = 0, row0 = 0, LEN = 0, T = 0, S = 0, I = 0, O = 0, H = 0, L = 0, in0 = 0;
+    int blen[ESRNN_MAX_BLOCKS] = {};
+    int layer_in[ESRNN_MAX_LAYERS] = {};
+    int64_t off_win[ESRNN_MAX_LAYERS] = {}, off_wrec[ESRNN_MAX_LAYERS] = {}, off_bias[ESRNN_MAX_LAYERS] = {};
+    int64_t off_nlw = 0, off_nlb = 0, off_outw = 0, off_outb = 0, P = 0;
+    NetLayout lay{};
+    std::vector<int64_t> live_flat;   // compact index -> flat index
+    std::vector<double> w_host;       // flat StackWeights mirror (dead entries live only here)
+    std::vector<int> cat_host;
+    std::vector<double> vals_host;    // local rows, row-major (for validate bookkeeping)
+    HostRng rng{0};
+    std::string err;
+    double last_ms = 0.0;
+    int64_t launches = 0;
+    bool fp64 = false;
+    size_t rsz = 4;
+
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    ncclComm_t comm = nullptr;
+
+    // device state (type-erased: Real = float or double, chosen by cfg.precision)
+    DBuf<unsigned char> vals, ps, ps_m, ps_v, theta, mW, vW;
+    DBuf<signed char> cat;
+    DBuf<int> ps_steps;
+    DBuf<unsigned char> lv, se, lbar, sbar, cI, cO, cl, part, gbuf, psg, d_inputs, d_targets, d_seas, d_levels;
+    DBuf<unsigned char> fX, fL, fS, dump_lv, dump_se;
+    DBuf<double> loss_part, es_sq_part, red_sq_part, scal, loss_hist, f_out, f_smape, smape_sum;
+    DBuf<unsigned int> done_ctr;
+    DBuf<long long> net_step;
+    DBuf<int> errw;
+    int Bcap = 0, kcap = 0, tiles_cap = 0, es_blocks = 0, red_blocks = 0, steps_cap = 0;
+
+    DevPlan epoch_plan, batch_plan;
+    HostPlan hp;
+    PinnedBuf<int> pin_i;
+    PinnedBuf<double> pin_d;
+
+    cudaGraphExec_t graph = nullptr;
+    int graph_steps = 0;
+    int graph_launch_nodes = 0;
+
+    ~esrnn_trainer() {
+        if (graph) cudaGraphExecDestroy(graph);
+        if (comm) ncclCommDestroy(comm);
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+        if (stream) cudaStreamDestroy(stream);
+    }
+
+    template <typename Real>
+    StateDev<Real> state() {
+        StateDev<Real> s{};
+        s.vals = reinterpret_cast<const Real*>(vals.p);
+        s.cat = cat.p;
+        s.N = N;
+        s.LEN = LEN;
+        s.kcap = kcap;
+        s.ps = reinterpret_cast<Real*>(ps.p);
+        s.ps_m = reinterpret_cast<Real*>(ps_m.p);
+        s.ps_v = reinterpret_cast<Real*>(ps_v.p);
+        s.ps_steps = ps_steps.p;
+        s.theta = reinterpret_cast<Real*>(theta.p);
+        s.mW = reinterpret_cast<Real*>(mW.p);
+        s.vW = reinterpret_cast<Real*>(vW.p);
+        s.lv = reinterpret_cast<Real*>(lv.p);
+        s.se = reinterpret_cast<Real*>(se.p);
+        s.lbar = reinterpret_cast<Real*>(lbar.p);
+        s.sbar = reinterpret_cast<Real*>(sbar.p);
+        s.cI = reinterpret_cast<Real*>(cI.p);
+        s.cO = reinterpret_cast<Real*>(cO.p);
+        s.cl = reinterpret_cast<Real*>(cl.p);
+        s.part = reinterpret_cast<Real*>(part.p);
+        s.loss_part = loss_part.p;
+        s.gbuf = reinterpret_cast<Real*>(gbuf.p);
+        s.psg = reinterpret_cast<Real*>(psg.p);
+        s.es_sq_part = es_sq_part.p;
+        s.red_sq_part = red_sq_part.p;
+        s.done_ctr = done_ctr.p;
+        s.scal = scal.p;
+        s.net_step = net_step.p;
+        s.loss_hist = loss_hist.p;
+        s.err = errw.p;
+        s.d_inputs = nullptr;
+        s.d_targets = nullptr;
+        s.d_seas = nullptr;
+        s.d_levels = nullptr;
+        s.tau = cfg.tau;
+        s.lr_net = cfg.learning_rate_network;
+        s.lr_ps = cfg.learning_rate_per_series;
+        s.clip = cfg.gradient_clip;
+        s.has_clip = cfg.has_gradient_clip ? 1 : 0;
+        s.attach = cfg.attach_es_state ? 1 : 0;
+        return s;
+    }
+};
+
+namespace {
+
+using Eng = esrnn_trainer;
+
+template <class Fn>
+esrnn_status guarded(std::string& err, Fn&& fn) {
+    try {
+        fn();
+        return ESRNN_OK;
+    } catch (const ApiError& e) {
+        err = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        err = "host allocation failed";
+        return ESRNN_ERROR;
+    } catch (const std::exception& e) {
+        err = e.what();
+        return ESRNN_ERROR;
+    }
+}
+
+// ------------------------------------------------------------------ validation
+void validate_config(const esrnn_profile& p, const esrnn_train_config& c) {
+    // data.hpp:101-114
+    if (p.seasonality_length < 1) raise(ESRNN_CONFIG_ERROR, "profile: seasonality must be >= 1");
+    if (p.horizon < 1) raise(ESRNN_CONFIG_ERROR, "profile: horizon must be >= 1");
+    if (p.input_window < p.seasonality_length)
+        raise(ESRNN_CONFIG_ERROR, "profile: input_window must cover at least one season");
+    if (p.n_blocks < 1) raise(ESRNN_CONFIG_ERROR, "profile: dilation blocks must be non-empty");
+    if (p.n_blocks > ESRNN_MAX_BLOCKS) raise(ESRNN_CONFIG_ERROR, "profile: at most %d dilation blocks", ESRNN_MAX_BLOCKS);
+    int layer = 0;
+    for (int b = 0; b < p.n_blocks; ++b) {
+        if (p.block_len[b] < 1) raise(ESRNN_CONFIG_ERROR, "profile: empty dilation block");
+        for (int j = 0; j < p.block_len[b]; ++j, ++layer) {
+            if (layer >= ESRNN_MAX_LAYERS) raise(ESRNN_CONFIG_ERROR, "profile: at most %d layers", ESRNN_MAX_LAYERS);
+            if (p.dilations[layer] < 1) raise(ESRNN_CONFIG_ERROR, "profile: dilations must be strictly positive");
+        }
+    }
+    if (p.hidden_size < 1) raise(ESRNN_CONFIG_ERROR, "profile: hidden_size must be >= 1");
+    if (p.min_length < 1) raise(ESRNN_CONFIG_ERROR, "profile: min_length must be >= 1");
+    // trainer.hpp:34-43 (+ the B200 batch cap extension)
+    const int cap = c.max_batch_size > 0 ? c.max_batch_size : 2048;
+    if (c.epochs < 0) raise(ESRNN_CONFIG_ERROR, "train: epochs must be >= 0");
+    if (c.batch_size < 1 || c.batch_size > cap) raise(ESRNN_CONFIG_ERROR, "train: batch_size must be in [1, %d]", cap);
+    if (!(c.tau > 0.0 && c.tau < 1.0)) raise(ESRNN_CONFIG_ERROR, "train: tau must be in (0, 1)");
+    if (c.learning_rate_network < 0.0 || c.learning_rate_per_series < 0.0)
+        raise(ESRNN_CONFIG_ERROR, "train: learning rates must be non-negative");
+    if (c.has_gradient_clip && c.gradient_clip <= 0.0) raise(ESRNN_CONFIG_ERROR, "train: gradient_clip must be positive");
+    // device-kernel limits (shared-memory tiles are sized from these)
+    if (p.hidden_size > 128) raise(ESRNN_CONFIG_ERROR, "profile: hidden_size > 128 unsupported by the B200 kernels");
+    if (p.seasonality_length > 64) raise(ESRNN_CONFIG_ERROR, "profile: seasonality > 64 unsupported by the B200 kernels");
+    if (p.input_window + ESRNN_NUM_CATEGORIES > 256 || p.horizon > 128)
+        raise(ESRNN_CONFIG_ERROR, "profile: window sizes unsupported by the B200 kernels");
+}
+
+void throw_device_error(Eng* e) {
+    int h[2];
+    CUDA_OK(cudaMemcpyAsync(h, e->errw.p, sizeof h, cudaMemcpyDeviceToHost, e->stream));
+    CUDA_OK(cudaStreamSynchronize(e->stream));
+    if (h[0] == 0) return;
+    const int reset[2] = {0, INT_MAX};
+    CUDA_OK(cudaMemcpyAsync(e->errw.p, reset, sizeof reset, cudaMemcpyHostToDevice, e->stream));
+    CUDA_OK(cudaStreamSynchronize(e->stream));
+    switch (h[0]) {
+        case kErrTrainLevel: raise(ESRNN_NUMERIC_DOMAIN_ERROR, "hybrid_primer_tape: non-positive level at t=%d", h[1]);
+        case kErrObs: raise(ESRNN_NUMERIC_DOMAIN_ERROR, "hybrid_primer: non-positive observation at t=%d", h[1]);
+        case kErrFcLevel: raise(ESRNN_NUMERIC_DOMAIN_ERROR, "hybrid_primer: non-positive level at t=%d", h[1]);
+        default: raise(ESRNN_NUMERIC_DOMAIN_ERROR, "deseasonalize_normalize: non-positive seasonality");
+    }
+}
+
+// ------------------------------------------------------------------ layout
+void build_layout(Eng* e) {
+    const int H = e->H, O = e->O;
+    int64_t off = 0, coff = 0;
+    NetLayout& lay = e->lay;
+    std::memset(&lay, 0, sizeof lay);
+    lay.L = e->L;
+    lay.nb = e->prof.n_blocks;
+    lay.H = H;
+    lay.O = O;
+    lay.I = e->I;
+    lay.S = e->S;
+    lay.in0 = e->in0;
+    lay.T = e->T;
+    e->live_flat.clear();
+    int layer = 0;
+    for (int b = 0; b < e->prof.n_blocks; ++b) {
+        const int first = layer;
+        for (int j = 0; j < e->prof.block_len[b]; ++j, ++layer) {
+            const int in = layer == 0 ? e->in0 : H;
+            e->layer_in[layer] = in;
+            lay.layer_in[layer] = in;
+            lay.res_src[layer] = -1;
+            lay.block_first[layer] = (b > 0 && layer == first) ? 1 : 0;
+            lay.block_last[layer] = (b > 0 && j == e->prof.block_len[b] - 1) ? 1 : 0;
+            if (lay.block_last[layer]) lay.res_src[layer] = first - 1;
+            // flat (for_each_param) layout: w_input, w_recur, bias
+            e->off_win[layer] = off;
+            off += static_cast<int64_t>(in) * 4 * H;
+            e->off_wrec[layer] = off;
+            off += static_cast<int64_t>(H) * 4 * H;
+            e->off_bias[layer] = off;
+            off += 4 * H;
+            // compact live layout: w_input columns [i | g | o] (forget gate dead), bias
+            lay.cw[layer] = coff;
+            for (int k = 0; k < in; ++k)
+                for (int q = 0; q < 3 * H; ++q) {
+                    const int col = q < H ? q : q + H;
+                    e->live_flat.push_back(e->off_win[layer] + static_cast<int64_t>(k) * 4 * H + col);
+                }
+            coff += static_cast<int64_t>(in) * 3 * H;
+            lay.cb[layer] = coff;
+            for (int q = 0; q < 3 * H; ++q) e->live_flat.push_back(e->off_bias[layer] + (q < H ? q : q + H));
+            coff += 3 * H;
+        }
+    }
+    e->off_nlw = off;
+    off += static_cast<int64_t>(H) * H;
+    e->off_nlb = off;
+    off += H;
+    e->off_outw = off;
+    off += static_cast<int64_t>(H) * O;
+    e->off_outb = off;
+    off += O;
+    e->P = off;
+    lay.c_nlw = coff;
+    for (int64_t i = 0; i < static_cast<int64_t>(H) * H; ++i) e->live_flat.push_back(e->off_nlw + i);
+    coff += static_cast<int64_t>(H) * H;
+    lay.c_nlb = coff;
+    for (int i = 0; i < H; ++i) e->live_flat.push_back(e->off_nlb + i);
+    coff += H;
+    lay.c_outw = coff;
+    for (int64_t i = 0; i < static_cast<int64_t>(H) * O; ++i) e->live_flat.push_back(e->off_outw + i);
+    coff += static_cast<int64_t>(H) * O;
+    lay.c_outb = coff;
+    for (int i = 0; i < O; ++i) e->live_flat.push_back(e->off_outb + i);
+    coff += O;
+    lay.P_live = coff;
+}
+
+// ------------------------------------------------------------------ conversions
+void to_real(Eng* e, const double* src, size_t n, void* host_tmp) {
+    if (e->fp64) {
+        std::memcpy(host_tmp, src, sizeof(double) * n);
+    } else {
+        float* f = static_cast<float*>(host_tmp);
+        for (size_t i = 0; i < n; ++i) f[i] = static_cast<float>(src[i]);
+    }
+}
+void from_real(Eng* e, const void* host_tmp, size_t n, double* dst) {
+    if (e->fp64) {
+        std::memcpy(dst, host_tmp, sizeof(double) * n);
+    } else {
+        const float* f = static_cast<const float*>(host_tmp);
+        for (size_t i = 0; i < n; ++i) dst[i] = static_cast<double>(f[i]);
+    }
+}
+
+void upload_real(Eng* e, void* dev, const double* src, size_t n) {
+    std::vector<double> tmp(n);
+    to_real(e, src, n, tmp.data());
+    CUDA_OK(cudaMemcpyAsync(dev, tmp.data(), e->rsz * n, cudaMemcpyHostToDevice, e->stream));
+    CUDA_OK(cudaStreamSynchronize(e->stream));
+}
+void download_real(Eng* e, const void* dev, size_t n, double* dst) {
+    std::vector<double> tmp(n);
+    CUDA_OK(cudaMemcpyAsync(tmp.data(), dev, e->rsz * n, cudaMemcpyDeviceToHost, e->stream));
+    CUDA_OK(cudaStreamSynchronize(e->stream));
+    from_real(e, tmp.data(), n, dst);
+}
+
+void upload_theta(Eng* e) {
+    std::vector<double> c(e->live_flat.size());
+    for (size_t i = 0; i < c.size(); ++i) c[i] = e->w_host[e->live_flat[i]];
+    upload_real(e, e->theta.p, c.data(), c.size());
+}
+
+void sync_weights_from_device(Eng* e) {
+    std::vector<double> c(e->live_flat.size());
+    download_real(e, e->theta.p, c.size(), c.data());
+    for (size_t i = 0; i < c.size(); ++i) e->w_host[e->live_flat[i]] = c[i];
+}
+
+// ------------------------------------------------------------------ capacity
+void ensure_capacity(Eng* e, int B) {
+    if (B <= e->Bcap) return;
+    if (e->graph) {
+        cudaGraphExecDestroy(e->graph);
+        e->graph = nullptr;
+    }
+    const int S = e->S, T = e->T, I = e->I, O = e->O;
+    const size_t r = e->rsz;
+    e->Bcap = B;
+    e->kcap = std::min(e->N > 0 ? e->N : 1, B);
+    const int kc = e->kcap;
+    e->tiles_cap = (B + kRows - 1) / kRows;
+    e->es_blocks = (kc + kScanThreads - 1) / kScanThreads;
+    e->lv.alloc(r * T * kc);
+    e->se.alloc(r * (T + S) * kc);
+    e->lbar.alloc(r * T * kc);
+    e->sbar.alloc(r * (T + S) * kc);
+    e->cI.alloc(r * static_cast<size_t>(B) * I);
+    e->cO.alloc(r * static_cast<size_t>(B) * O);
+    e->cl.alloc(r * B);
+    e->part.alloc(r * static_cast<size_t>(e->tiles_cap) * e->lay.P_live);
+    e->loss_part.alloc(e->tiles_cap);
+    e->psg.alloc(r * static_cast<size_t>(kc) * (2 + S));
+    e->es_sq_part.alloc(e->es_blocks);
+    e->d_inputs.alloc(r * static_cast<size_t>(B) * e->in0);
+    e->d_targets.alloc(r * static_cast<size_t>(B) * O);
+    e->d_seas.alloc(r * static_cast<size_t>(B) * O);
+    e->d_levels.alloc(r * B);
+}
+
+// ------------------------------------------------------------------ plans
+// trainer.hpp:493-501: slots in first-appearance order; per slot its windows in batch order.
+void append_step(Eng* e, HostPlan& hp, const int* rows, const int* anchors, int B, std::vector<int>& stamp,
+                 std::vector<int>& slot_id, int step) {
+    const int wbase = static_cast<int>(hp.w_row.size());
+    const int sbase = static_cast<int>(hp.slot_row.size());
+    for (int i = 0; i < B; ++i) {
+        const int r = rows[i] - e->row0;
+        if (r < 0 || r >= e->N) continue;
+        if (stamp[r] != step) {
+            stamp[r] = step;
+            slot_id[r] = static_cast<int>(hp.slot_row.size()) - sbase;
+            hp.slot_row.push_back(r);
+        }
+        hp.w_row.push_back(r);
+        hp.w_anchor.push_back(anchors[i]);
+        hp.w_slot.push_back(slot_id[r]);
+    }
+    const int nw = static_cast<int>(hp.w_row.size()) - wbase;
+    const int ns = static_cast<int>(hp.slot_row.size()) - sbase;
+    // CSR: count, prefix, fill in batch order
+    std::vector<int> cnt(ns + 1, 0);
+    for (int i = 0; i < nw; ++i) cnt[hp.w_slot[wbase + i] + 1]++;
+    for (int k = 0; k < ns; ++k) cnt[k + 1] += cnt[k];
+    const int cbase = static_cast<int>(hp.slot_win.size());
+    hp.slot_win.resize(cbase + nw);
+    std::vector<int> fill(cnt.begin(), cnt.end() - 1);
+    for (int i = 0; i < nw; ++i) hp.slot_win[cbase + fill[hp.w_slot[wbase + i]]++] = i;
+    for (int k = 0; k < ns; ++k) hp.slot_win_off.push_back(cbase + cnt[k + 1]);
+    hp.step_win_off.push_back(static_cast<int>(hp.w_row.size()));
+    hp.step_slot_off.push_back(static_cast<int>(hp.slot_row.size()));
+    hp.max_step_windows = std::max(hp.max_step_windows, nw);
+    hp.max_step_slots = std::max(hp.max_step_slots, ns);
+}
+
+void plan_begin(HostPlan& hp) {
+    hp.w_row.clear();
+    hp.w_anchor.clear();
+    hp.w_slot.clear();
+    hp.slot_row.clear();
+    hp.slot_win.clear();
+    hp.slot_win_off.assign(1, 0);
+    hp.step_win_off.assign(1, 0);
+    hp.step_slot_off.assign(1, 0);
+    hp.step_M.clear();
+    hp.max_step_windows = hp.max_step_slots = 0;
+}
+
+template <typename T>
+void upload_vec(Eng* e, DBuf<T>& d, const std::vector<T>& h, size_t cap) {
+    if (d.n < std::max<size_t>(cap, 1)) d.alloc(std::max<size_t>(cap, 1));
+    if (!h.empty()) CUDA_OK(cudaMemcpyAsync(d.p, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice, e->stream));
+}
+
+void upload_plan(Eng* e, const HostPlan& hp, DevPlan& dp, size_t cap_w, size_t cap_steps) {
+    const size_t cw = std::max(cap_w, hp.w_row.size());
+    const size_t cs = std::max(cap_steps, hp.step_M.size());
+    upload_vec(e, dp.w_row, hp.w_row, cw);
+    upload_vec(e, dp.w_anchor, hp.w_anchor, cw);
+    upload_vec(e, dp.w_slot, hp.w_slot, cw);
+    upload_vec(e, dp.slot_row, hp.slot_row, cw);
+    upload_vec(e, dp.slot_win, hp.slot_win, cw);
+    upload_vec(e, dp.slot_win_off, hp.slot_win_off, cw + 1);
+    upload_vec(e, dp.step_win_off, hp.step_win_off, cs + 1);
+    upload_vec(e, dp.step_slot_off, hp.step_slot_off, cs + 1);
+    upload_vec(e, dp.step_M, hp.step_M, cs);
+}
+
+// ------------------------------------------------------------------ step launch
+template <typename Real>
+size_t stack_smem(const NetLayout& lay) {
+    return sizeof(Real) * TileSmem::make(lay, kRows).total;
+}
+
+int stack_threads(const NetLayout& lay) {
+    int nt = ((3 * lay.H + 31) / 32) * 32;
+    return std::min(std::max(nt, 64), 256);
+}
+
+template <typename Real>
+void setup_kernel_attrs(Eng* e) {
+    const size_t sm = stack_smem<Real>(e->lay);
+    CUDA_OK(cudaFuncSetAttribute(k_stack<Real, kRows, kTrain>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    CUDA_OK(cudaFuncSetAttribute(k_stack<Real, kRows, kLossOnly>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    CUDA_OK(cudaFuncSetAttribute(k_stack<Real, kRows, kForecast>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+}
+
+// Launch one training step (K1..K5) for step `s` of plan `pv` on the engine stream.
+template <typename Real>
+void launch_step(Eng* e, const PlanDev& pv, int s, bool grads, bool update, StateDev<Real> st) {
+    const NetLayout& lay = e->lay;
+    const int kc = e->kcap;
+    const int scan_blocks = (kc + kScanThreads - 1) / kScanThreads;
+    k_scan_fwd<Real><<<scan_blocks, kScanThreads, sizeof(Real) * lay.S * kScanThreads, e->stream>>>(st, pv, lay, s);
+    ForecastArgs fa{};
+    const size_t sm = stack_smem<Real>(lay);
+    const int nt = stack_threads(lay);
+    if (grads)
+        k_stack<Real, kRows, kTrain><<<e->tiles_cap, nt, sm, e->stream>>>(st, pv, lay, s, fa);
+    else
+        k_stack<Real, kRows, kLossOnly><<<e->tiles_cap, nt, sm, e->stream>>>(st, pv, lay, s, fa);
+    e->launches += 2;
+    if (!grads) return;
+    k_es_bwd<Real><<<e->es_blocks, kScanThreads, 0, e->stream>>>(st, pv, lay, s);
+    const int rb = static_cast<int>((lay.P_live + 255) / 256);
+    const bool sharded = e->world > 1;
+    k_net_reduce<Real, kRows><<<rb, 256, 0, e->stream>>>(st, pv, lay, s, e->es_blocks, sharded ? 0 : 1);
+    e->launches += 2;
+    if (sharded) {
+        NCCL_OK(ncclAllReduce(st.gbuf, st.gbuf, lay.P_live + 2, e->fp64 ? ncclDouble : ncclFloat, ncclSum, e->comm,
+                              e->stream));
+        k_finalize<Real><<<rb, 256, 0, e->stream>>>(st, pv, lay, s);
+        e->launches += 1;
+    }
+    if (update) {
+        const long long n = lay.P_live + kc;
+        k_adam<Real><<<static_cast<int>((n + 255) / 256), 256, 0, e->stream>>>(st, pv, lay, s);
+        e->launches += 1;
+    }
+}
+
+template <typename Real>
+void alloc_state(Eng* e) {
+    const int N = e->N, S = e->S, LEN = e->LEN;
+    const size_t r = sizeof(Real);
+    e->vals.alloc(r * static_cast<size_t>(LEN) * std::max(N, 1));
+    e->ps.alloc(r * static_cast<size_t>(2 + S) * std::max(N, 1));
+    e->ps_m.alloc(r * static_cast<size_t>(2 + S) * std::max(N, 1));
+    e->ps_v.alloc(r * static_cast<size_t>(2 + S) * std::max(N, 1));
+    e->ps_steps.alloc(std::max(N, 1));
+    e->cat.alloc(std::max(N, 1));
+    e->theta.alloc(r * e->lay.P_live);
+    e->mW.alloc(r * e->lay.P_live);
+    e->vW.alloc(r * e->lay.P_live);
+    e->gbuf.alloc(r * (e->lay.P_live + 2));
+    e->red_blocks = static_cast<int>((e->lay.P_live + 255) / 256);
+    e->red_sq_part.alloc(e->red_blocks);
+    e->scal.alloc(4);
+    e->loss_hist.alloc(1);
+    e->done_ctr.alloc(2);
+    e->net_step.alloc(1);
+    e->errw.alloc(2);
+    for (auto* b : {&e->ps, &e->ps_m, &e->ps_v, &e->mW, &e->vW}) b->zero(e->stream);
+    e->ps_steps.zero(e->stream);
+    e->done_ctr.zero(e->stream);
+    e->net_step.zero(e->stream);
+    const int reset[2] = {0, INT_MAX};
+    CUDA_OK(cudaMemcpyAsync(e->errw.p, reset, sizeof reset, cudaMemcpyHostToDevice, e->stream));
+    setup_kernel_attrs<Real>(e);
+}
+
+template <typename Real>
+void upload_values(Eng* e, const double* values, const int32_t* category) {
+    const int N = e->N, LEN = e->LEN;
+    std::vector<Real> tm(static_cast<size_t>(LEN) * std::max(N, 1));
+    for (int r = 0; r < N; ++r)
+        for (int t = 0; t < LEN; ++t)
+            tm[static_cast<size_t>(t) * N + r] = static_cast<Real>(values[static_cast<size_t>(e->row0 + r) * LEN + t]);
+    CUDA_OK(cudaMemcpyAsync(e->vals.p, tm.data(), sizeof(Real) * tm.size(), cudaMemcpyHostToDevice, e->stream));
+    std::vector<signed char> c(std::max(N, 1), 5);
+    e->cat_host.assign(N, 5);
+    for (int r = 0; r < N; ++r) {
+        const int v = category ? category[e->row0 + r] : -1;
+        c[r] = static_cast<signed char>(v >= 0 && v < 6 ? v : 5);
+        e->cat_host[r] = c[r];
+    }
+    CUDA_OK(cudaMemcpyAsync(e->cat.p, c.data(), c.size(), cudaMemcpyHostToDevice, e->stream));
+    CUDA_OK(cudaStreamSynchronize(e->stream));
+}
+
+// ------------------------------------------------------------------ epoch
+template <typename Real>
+double train_epoch_impl(Eng* e) {
+    const int I = e->I, O = e->O, T = e->T;
+    const int per = T - O - I + 1;
+    const int64_t nw = static_cast<int64_t>(e->N_global) * per;
+    if (nw <= 0) raise(ESRNN_CONTRACT_ERROR, "make_batches: no windows");
+    // all_windows (trainer.hpp:214-223) + Rng::shuffle (matrix.hpp:203-205), global order
+    std::vector<int> wr(nw), wa(nw);
+    {
+        int64_t n = 0;
+        for (int r = 0; r < e->N_global; ++r)
+            for (int a = I - 1; a <= T - O - 1; ++a) {
+                wr[n] = r;
+                wa[n] = a;
+                ++n;
+            }
+        for (int64_t i = nw; i > 1; --i) {
+            const int64_t j = static_cast<int64_t>(e->rng.below(static_cast<uint64_t>(i)));
+            std::swap(wr[i - 1], wr[j]);
+            std::swap(wa[i - 1], wa[j]);
+        }
+    }
+    const int B = e->cfg.batch_size;
+    const int steps = static_cast<int>((nw + B - 1) / B);
+    HostPlan& hp = e->hp;
+    plan_begin(hp);
+    std::vector<int> stamp(std::max(e->N, 1), -1), slot_id(std::max(e->N, 1), 0);
+    for (int s = 0; s < steps; ++s) {
+        const int64_t start = static_cast<int64_t>(s) * B;
+        const int nb = static_cast<int>(std::min<int64_t>(nw, start + B) - start);
+        append_step(e, hp, wr.data() + start, wa.data() + start, nb, stamp, slot_id, s);
+        hp.step_M.push_back(static_cast<double>(nb) * O);
+    }
+    ensure_capacity(e, B);
+    const size_t local_w = static_cast<size_t>(e->N) * per;
+    upload_plan(e, hp, e->epoch_plan, local_w, steps);
+    if (e->steps_cap < steps) {
+        e->loss_hist.alloc(steps);
+        e->steps_cap = steps;
+        if (e->graph) {
+            cudaGraphExecDestroy(e->graph);
+            e->graph = nullptr;
+        }
+    }
+    const PlanDev pv = e->epoch_plan.view(false);
+    StateDev<Real> st = e->state<Real>();
+    const bool use_graph = e->cfg.use_graphs >= 0;
+    CUDA_OK(cudaEventRecord(e->ev0, e->stream));
+    if (use_graph) {
+        if (!e->graph || e->graph_steps != steps) {
+            if (e->graph) cudaGraphExecDestroy(e->graph);
+            e->graph = nullptr;
+            cudaGraph_t g;
+            const int64_t before = e->launches;
+            CUDA_OK(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
+            try {
+                for (int s = 0; s < steps; ++s) launch_step<Real>(e, pv, s, true, true, st);
+            } catch (...) {
+                cudaStreamEndCapture(e->stream, &g);
+                throw;
+            }
+            CUDA_OK(cudaStreamEndCapture(e->stream, &g));
+            CUDA_OK(cudaGraphInstantiate(&e->graph, g, 0));
+            CUDA_OK(cudaGraphDestroy(g));
+            e->graph_launch_nodes = static_cast<int>(e->launches - before);
+            e->launches = before;
+            e->graph_steps = steps;
+        }
+        CUDA_OK(cudaGraphLaunch(e->graph, e->stream));
+        e->launches += e->graph_launch_nodes;
+    } else {
+        for (int s = 0; s < steps; ++s) launch_step<Real>(e, pv, s, true, true, st);
+    }
+    CUDA_OK(cudaEventRecord(e->ev1, e->stream));
+    CUDA_OK(cudaGetLastError());
+    std::vector<double> lh(steps);
+    CUDA_OK(cudaMemcpyAsync(lh.data(), e->loss_hist.p, sizeof(double) * steps, cudaMemcpyDeviceToHost, e->stream));
+    CUDA_OK(cudaStreamSynchronize(e->stream));
+    float ms = 0.f;
+    CUDA_OK(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
+    e->last_ms = ms;
+    throw_device_error(e);
+    // trainer.hpp:236-242: acc += loss * count, in batch order
+    double acc = 0.0, weight = 0.0;
+    for (int s = 0; s < steps; ++s) {
+        acc += lh[s] * hp.step_M[s];
+        weight += hp.step_M[s];
+    }
+    return acc / weight;
+}
+
+// ------------------------------------------------------------------ single batch
+template <typename Real>
+void run_batch_impl(Eng* e, int32_t B, const int32_t* rows, const int32_t* anchors, const double* mask,
+                    int32_t flags, double* loss, double* mask_count, double* inputs, double* targets,
+                    double* seas, double* levels, double* net_grads, int32_t* n_slots, int32_t* slot_rows,
+                    double* ps_grads) {
+    const int O = e->O, I = e->I, T = e->T, S = e->S;
+    if (B <= 0) raise(ESRNN_CONTRACT_ERROR, "batch: empty");
+    for (int i = 0; i < B; ++i) {
+        if (rows[i] < 0 || rows[i] >= e->N_global) raise(ESRNN_SHAPE_ERROR, "batch: series row %d out of range", rows[i]);
+        if (anchors[i] < I - 1 || anchors[i] > T - O - 1) raise(ESRNN_SHAPE_ERROR, "batch: anchor %d out of range", anchors[i]);
+    }
+    double count = 0.0;
+    for (int64_t i = 0; i < static_cast<int64_t>(B) * O; ++i) count += (!mask || mask[i] != 0.0) ? 1.0 : 0.0;
+    if (count == 0.0) raise(ESRNN_CONTRACT_ERROR, "pinball: all-zero mask, mean undefined");
+    HostPlan bp;
+    plan_begin(bp);
+    std::vector<int> stamp(std::max(e->N, 1), -1), slot_id(std::max(e->N, 1), 0);
+    append_step(e, bp, rows, anchors, B, stamp, slot_id, 0);
+    bp.step_M.push_back(count);
+    const int Bl = static_cast<int>(bp.w_row.size());
+    ensure_capacity(e, std::max(Bl, 1));
+    upload_plan(e, bp, e->batch_plan, Bl, 1);
+    // local mask rows in local-window order
+    std::vector<unsigned char> m;
+    if (mask) {
+        m.reserve(static_cast<size_t>(Bl) * O);
+        for (int i = 0; i < B; ++i) {
+            const int r = rows[i] - e->row0;
+            if (r < 0 || r >= e->N) continue;
+            for (int j = 0; j < O; ++j) m.push_back(mask[static_cast<size_t>(i) * O + j] != 0.0 ? 1 : 0);
+        }
+        upload_vec(e, e->batch_plan.mask, m, std::max<size_t>(m.size(), 1));
+    }
+    const PlanDev pv = e->batch_plan.view(mask != nullptr);
+    StateDev<Real> st = e->state<Real>();
+    const bool want_dump = inputs || targets || seas || levels;
+    if (want_dump) {
+        st.d_inputs = reinterpret_cast<Real*>(e->d_inputs.p);
+        st.d_targets = reinterpret_cast<Real*>(e->d_targets.p);
+        st.d_seas = reinterpret_cast<Real*>(e->d_seas.p);
+        st.d_levels = reinterpret_cast<Real*>(e->d_levels.p);
+    }
+    const bool grads = (flags & ESRNN_BATCH_GRADS) != 0;
+    const bool update = grads && (flags & ESRNN_BATCH_UPDATE) != 0;
+    CUDA_OK(cudaEventRecord(e->ev0, e->stream));
+    if (Bl > 0 || e->world > 1) {
+        launch_step<Real>(e, pv, 0, grads, update, st);
+    }
+    CUDA_OK(cudaEventRecord(e->ev1, e->stream));
+    CUDA_OK(cudaGetLastError());
+    CUDA_OK(cudaStreamSynchronize(e->stream));
+    float ms = 0.f;
+    CUDA_OK(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
+    e->last_ms = ms;
+    throw_device_error(e);
+    // loss: sum of tile partials (single GPU) or all-reduced sum (sharded) / M
+    double lsum = 0.0;
+    if (grads && e->world > 1) {
+        Real g2[2];
+        CUDA_OK(cudaMemcpy(g2, reinterpret_cast<Real*>(e->gbuf.p) + e->lay.P_live, sizeof g2, cudaMemcpyDeviceToHost));
+        lsum = static_cast<double>(g2[1]);
+    } else {
+        const int nt = (Bl + kRows - 1) / kRows;
+        std::vector<double> lp(nt);
+        if (nt) CUDA_OK(cudaMemcpy(lp.data(), e->loss_part.p, sizeof(double) * nt, cudaMemcpyDeviceToHost));
+        for (double v : lp) lsum += v;
+        if (e->world > 1) raise(ESRNN_CONFIG_ERROR, "sharded batch_loss requires gradients (collective step)");
+    }
+    if (loss) *loss = lsum / count;
+    if (mask_count) *mask_count = count;
+    if (want_dump && Bl > 0) {
+        std::vector<double> tmp;
+        auto dl = [&](const DBuf<unsigned char>& d, size_t n, double* out) {
+            if (!out) return;
+            download_real(e, d.p, n, out);
+        };
+        dl(e->d_inputs, static_cast<size_t>(Bl) * e->in0, inputs);
+        dl(e->d_targets, static_cast<size_t>(Bl) * O, targets);
+        dl(e->d_seas, static_cast<size_t>(Bl) * O, seas);
+        dl(e->d_levels, Bl, levels);
+    }
+    const int k = static_cast<int>(bp.slot_row.size());
+    if (n_slots) *n_slots = k;
+    if (slot_rows)
+        for (int i = 0; i < k; ++i) slot_rows[i] = bp.slot_row[i] + e->row0;
+    if (grads) {
+        if (net_grads) {
+            std::vector<double> c(e->lay.P_live);
+            download_real(e, e->gbuf.p, c.size(), c.data());
+            std::fill(net_grads, net_grads + e->P, 0.0);
+            for (size_t i = 0; i < c.size(); ++i) net_grads[e->live_flat[i]] = c[i];
+        }
+        if (ps_grads && e->cfg.attach_es_state && k > 0) download_real(e, e->psg.p, static_cast<size_t>(k) * (2 + S), ps_grads);
+    }
+    if (update) sync_weights_from_device(e);
+}
+
+// ------------------------------------------------------------------ forecast
+template <typename Real>
+void forecast_impl(Eng* e, int64_t drop_tail, double* out, double* smape, double* mean, bool validate) {
+    const int I = e->I, O = e->O, S = e->S, N = e->N;
+    if (static_cast<int64_t>(e->LEN) < drop_tail + I) raise(ESRNN_INSUFFICIENT_LENGTH, "forecast_at: not enough in-sample data");
+    const int t_ins = static_cast<int>(e->LEN - drop_tail);
+    const size_t r = sizeof(Real);
+    if (e->fX.n < r * std::max(N, 1) * e->in0) {
+        e->fX.alloc(r * std::max(N, 1) * e->in0);
+        e->fL.alloc(r * std::max(N, 1));
+        e->fS.alloc(r * std::max(N, 1) * O);
+        e->f_out.alloc(static_cast<size_t>(std::max(N, 1)) * O);
+        e->f_smape.alloc(std::max(N, 1));
+    }
+    StateDev<Real> st = e->state<Real>();
+    const NetLayout& lay = e->lay;
+    CUDA_OK(cudaEventRecord(e->ev0, e->stream));
+    if (N > 0) {
+        const int sb = (N + kScanThreads - 1) / kScanThreads;
+        k_forecast_scan<Real><<<sb, kScanThreads, sizeof(Real) * (S + I) * kScanThreads, e->stream>>>(
+            st, lay, t_ins, reinterpret_cast<Real*>(e->fX.p), reinterpret_cast<Real*>(e->fL.p),
+            reinterpret_cast<Real*>(e->fS.p), nullptr, nullptr, -1);
+        ForecastArgs fa{};
+        fa.t_ins = t_ins;
+        fa.validate = validate ? 1 : 0;
+        fa.X = e->fX.p;
+        fa.lvl = e->fL.p;
+        fa.sout = e->fS.p;
+        fa.out = e->f_out.p;
+        fa.smape = e->f_smape.p;
+        const int tiles = (N + kRows - 1) / kRows;
+        k_stack<Real, kRows, kForecast><<<tiles, stack_threads(lay), stack_smem<Real>(lay), e->stream>>>(
+            st, e->batch_plan.view(false), lay, 0, fa);
+        e->launches += 2;
+    }
+    CUDA_OK(cudaEventRecord(e->ev1, e->stream));
+    CUDA_OK(cudaGetLastError());
+    CUDA_OK(cudaStreamSynchronize(e->stream));
+    float ms = 0.f;
+    CUDA_OK(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
+    e->last_ms = ms;
+    throw_device_error(e);
+    if (out && N > 0) CUDA_OK(cudaMemcpy(out, e->f_out.p, sizeof(double) * N * O, cudaMemcpyDeviceToHost));
+    if (validate) {
+        std::vector<double> sm(std::max(N, 1));
+        if (N > 0) CUDA_OK(cudaMemcpy(sm.data(), e->f_smape.p, sizeof(double) * N, cudaMemcpyDeviceToHost));
+        double acc = 0.0;
+        for (int i = 0; i < N; ++i) acc += sm[i];
+        if (smape)
+            for (int i = 0; i < N; ++i) smape[i] = sm[i];
+        if (e->world > 1) {
+            if (e->smape_sum.n < 1) e->smape_sum.alloc(1);
+            CUDA_OK(cudaMemcpy(e->smape_sum.p, &acc, sizeof acc, cudaMemcpyHostToDevice));
+            NCCL_OK(ncclAllReduce(e->smape_sum.p, e->smape_sum.p, 1, ncclDouble, ncclSum, e->comm, e->stream));
+            CUDA_OK(cudaMemcpyAsync(&acc, e->smape_sum.p, sizeof acc, cudaMemcpyDeviceToHost, e->stream));
+            CUDA_OK(cudaStreamSynchronize(e->stream));
+        }
+        if (mean) *mean = acc / static_cast<double>(e->N_global);
+    }
+}
+
+template <typename Real>
+void hw_state_impl(Eng* e, int64_t row, int64_t t_len, double* levels, double* seas) {
+    const int S = e->S;
+    const int lr = static_cast<int>(row - e->row0);
+    if (lr < 0 || lr >= e->N) raise(ESRNN_SHAPE_ERROR, "hw_state: row %lld not owned", static_cast<long long>(row));
+    if (t_len < S || t_len > e->LEN)
+        raise(ESRNN_INSUFFICIENT_LENGTH, "hybrid_primer: series length %lld shorter than season length %d",
+              static_cast<long long>(t_len), S);
+    const size_t r = sizeof(Real);
+    if (e->dump_lv.n < r * e->LEN) {
+        e->dump_lv.alloc(r * e->LEN);
+        e->dump_se.alloc(r * (e->LEN + S));
+    }
+    StateDev<Real> st = e->state<Real>();
+    const int sb = (e->N + kScanThreads - 1) / kScanThreads;
+    // the dump row's thread writes its full state; X == nullptr skips the window build
+    k_forecast_scan<Real><<<sb, kScanThreads, sizeof(Real) * (S + e->I) * kScanThreads, e->stream>>>(
+        st, e->lay, static_cast<int>(t_len), nullptr, nullptr, nullptr, reinterpret_cast<Real*>(e->dump_lv.p),
+        reinterpret_cast<Real*>(e->dump_se.p), lr);
+    e->launches += 1;
+    CUDA_OK(cudaGetLastError());
+    CUDA_OK(cudaStreamSynchronize(e->stream));
+    throw_device_error(e);
+    download_real(e, e->dump_lv.p, t_len, levels);
+    download_real(e, e->dump_se.p, t_len + S, seas);
+}
+
+}  // namespace
+
+// ======================================================================= C-ABI
+extern "C" {
+
+const char* esrnn_version(void) { return "esrnn-b200 0.1 (sm_100a CUDA engine)"; }
+int32_t esrnn_abi_version(void) { return ESRNN_ABI_VERSION; }
+const char* esrnn_last_error(const esrnn_trainer* t) { return t ? t->err.c_str() : g_create_err.c_str(); }
+
+esrnn_status esrnn_trainer_create(const esrnn_profile* profile, const esrnn_train_config* cfg, int64_t n_series,
+                                  int32_t length, const double* values, const int32_t* category,
+                                  const esrnn_dist* dist, esrnn_trainer** out) {
+    *out = nullptr;
+    std::unique_ptr<Eng> e(new Eng());
+    esrnn_status st = guarded(g_create_err, [&] {
+        validate_config(*profile, *cfg);
+        if (n_series <= 0) raise(ESRNN_CONTRACT_ERROR, "trainer: no series");
+        const int O = profile->horizon, S = profile->seasonality_length, I = profile->input_window;
+        if (length < 2 * O + 1)
+            raise(ESRNN_INSUFFICIENT_LENGTH, "split: need at least %d values, got %d", 2 * O + 1, length);
+        const int T = length - 2 * O;
+        if (T < I + O) raise(ESRNN_INSUFFICIENT_LENGTH, "trainer: train segment of %d cannot hold an input window plus horizon", T);
+        if (T < S) raise(ESRNN_INSUFFICIENT_LENGTH, "trainer: train segment shorter than one season");
+        e->prof = *profile;
+        e->cfg = *cfg;
+        e->fp64 = cfg->precision == ESRNN_FP64;
+        e->rsz = e->fp64 ? sizeof(double) : sizeof(float);
+        e->N_global = static_cast<int>(n_series);
+        if (dist && dist->world_size > 1) {
+            e->rank = dist->rank;
+            e->world = dist->world_size;
+            if (e->rank < 0 || e->rank >= e->world) raise(ESRNN_CONFIG_ERROR, "dist: rank out of range");
+        }
+        // contiguous row blocks
+        e->row0 = static_cast<int>((static_cast<int64_t>(e->rank) * n_series) / e->world);
+        const int row1 = static_cast<int>((static_cast<int64_t>(e->rank + 1) * n_series) / e->world);
+        e->N = row1 - e->row0;
+        e->LEN = length;
+        e->T = T;
+        e->S = S;
+        e->I = I;
+        e->O = O;
+        e->H = profile->hidden_size;
+        e->in0 = I + ESRNN_NUM_CATEGORIES;
+        e->L = 0;
+        for (int b = 0; b < profile->n_blocks; ++b) e->L += profile->block_len[b];
+        build_layout(e.get());
+
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+            raise(ESRNN_CUDA_ERROR, "no CUDA device visible: the B200 engine has no CPU fallback");
+        if (cfg->device < 0 || cfg->device >= ndev) raise(ESRNN_CUDA_ERROR, "device %d out of range", cfg->device);
+        CUDA_OK(cudaSetDevice(cfg->device));
+        CUDA_OK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+        CUDA_OK(cudaEventCreate(&e->ev0));
+        CUDA_OK(cudaEventCreate(&e->ev1));
+        if (e->world > 1) {
+            ncclUniqueId id;
+            static_assert(sizeof(id.internal) == 128, "nccl id size");
+            std::memcpy(id.internal, dist->nccl_unique_id, 128);
+            NCCL_OK(ncclCommInitRank(&e->comm, e->world, id, e->rank));
+        }
+
+        // network.hpp:89-116 init order on the trainer RNG (identical on every rank)
+        e->rng = HostRng(cfg->seed);
+        e->w_host.assign(e->P, 0.0);
+        const int H = e->H;
+        const double bound = 1.0 / std::sqrt(static_cast<double>(H));
+        for (int l = 0; l < e->L; ++l) {
+            for (int64_t i = 0; i < static_cast<int64_t>(e->layer_in[l]) * 4 * H; ++i)
+                e->w_host[e->off_win[l] + i] = e->rng.uniform(-bound, bound);
+            for (int64_t i = 0; i < static_cast<int64_t>(H) * 4 * H; ++i)
+                e->w_host[e->off_wrec[l] + i] = e->rng.uniform(-bound, bound);
+            for (int c = H; c < 2 * H; ++c) e->w_host[e->off_bias[l] + c] = 1.0;
+        }
+        for (int64_t i = 0; i < static_cast<int64_t>(H) * H; ++i) e->w_host[e->off_nlw + i] = e->rng.uniform(-bound, bound);
+        for (int64_t i = 0; i < static_cast<int64_t>(H) * e->O; ++i) e->w_host[e->off_outw + i] = e->rng.uniform(-bound, bound);
+
+        if (e->fp64) {
+            alloc_state<double>(e.get());
+            upload_values<double>(e.get(), values, category);
+        } else {
+            alloc_state<float>(e.get());
+            upload_values<float>(e.get(), values, category);
+        }
+        upload_theta(e.get());
+        ensure_capacity(e.get(), cfg->batch_size);
+        CUDA_OK(cudaStreamSynchronize(e->stream));
+    });
+    if (st == ESRNN_OK) *out = e.release();
+    return st;
+}
+
+void esrnn_trainer_destroy(esrnn_trainer* t) {
+    if (!t) return;
+    cudaSetDevice(t->cfg.device);
+    delete t;
+}
+
+esrnn_status esrnn_trainer_shard(const esrnn_trainer* t, int64_t* b, int64_t* e) {
+    *b = t->row0;
+    *e = t->row0 + t->N;
+    return ESRNN_OK;
+}
+
+esrnn_status esrnn_trainer_param_count(const esrnn_trainer* t, int32_t* n_arrays, int64_t* n_values) {
+    *n_arrays = 3 * t->L + 4;
+    *n_values = t->P;
+    return ESRNN_OK;
+}
+
+esrnn_status esrnn_trainer_param_info(const esrnn_trainer* t, int32_t idx, esrnn_param_info* o) {
+    std::memset(o, 0, sizeof *o);
+    const int H = t->H;
+    if (idx < 0 || idx >= 3 * t->L + 4) return ESRNN_SHAPE_ERROR;
+    if (idx < 3 * t->L) {
+        const int l = idx / 3, k = idx % 3;
+        if (k == 0) { std::snprintf(o->name, 32, "lstm%d.w_input", l); o->rows = t->layer_in[l]; o->cols = 4 * H; o->offset = t->off_win[l]; }
+        if (k == 1) { std::snprintf(o->name, 32, "lstm%d.w_recur", l); o->rows = H; o->cols = 4 * H; o->offset = t->off_wrec[l]; }
+        if (k == 2) { std::snprintf(o->name, 32, "lstm%d.bias", l); o->rows = 1; o->cols = 4 * H; o->offset = t->off_bias[l]; }
+        return ESRNN_OK;
+    }
+    switch (idx - 3 * t->L) {
+        case 0: std::snprintf(o->name, 32, "head.nl_w"); o->rows = H; o->cols = H; o->offset = t->off_nlw; break;
+        case 1: std::snprintf(o->name, 32, "head.nl_b"); o->rows = 1; o->cols = H; o->offset = t->off_nlb; break;
+        case 2: std::snprintf(o->name, 32, "head.out_w"); o->rows = H; o->cols = t->O; o->offset = t->off_outw; break;
+        default: std::snprintf(o->name, 32, "head.out_b"); o->rows = 1; o->cols = t->O; o->offset = t->off_outb; break;
+    }
+    return ESRNN_OK;
+}
+
+esrnn_status esrnn_trainer_get_weights(esrnn_trainer* t, double* flat, int64_t count) {
+    return guarded(t->err, [&] {
+        if (count != t->P) raise(ESRNN_SHAPE_ERROR, "get_weights: count %lld != %lld", (long long)count, (long long)t->P);
+        CUDA_OK(cudaSetDevice(t->cfg.device));
+        sync_weights_from_device(t);
+        std::memcpy(flat, t->w_host.data(), sizeof(double) * t->P);
+    });
+}
+
+esrnn_status esrnn_trainer_set_weights(esrnn_trainer* t, const double* flat, int64_t count) {
+    return guarded(t->err, [&] {
+        if (count != t->P) raise(ESRNN_CHECKPOINT_ERROR, "checkpoint network shapes incompatible with configuration");
+        CUDA_OK(cudaSetDevice(t->cfg.device));
+        std::memcpy(t->w_host.data(), flat, sizeof(double) * t->P);
+        upload_theta(t);
+    });
+}
+
+static void ps_io(esrnn_trainer* t, int64_t r0, int64_t n, double* a, double* g, double* s, bool get) {
+    const int S = t->S, N = t->N;
+    const int64_t lr0 = r0 - t->row0;
+    if (n < 0 || lr0 < 0 || lr0 + n > N) raise(ESRNN_SHAPE_ERROR, "per_series: rows [%lld, %lld) not owned by this rank", (long long)r0, (long long)(r0 + n));
+    if (n == 0) return;
+    CUDA_OK(cudaSetDevice(t->cfg.device));
+    std::vector<double> buf(n);
+    for (int j = 0; j < 2 + S; ++j) {
+        unsigned char* dev = t->ps.p + t->rsz * (static_cast<size_t>(j) * N + lr0);
+        double* dst = j == 0 ? a : (j == 1 ? g : nullptr);
+        if (get) {
+            download_real(t, dev, n, buf.data());
+            for (int64_t i = 0; i < n; ++i) {
+                if (j < 2) { if (dst) dst[i] = buf[i]; }
+                else if (s) s[i * S + (j - 2)] = buf[i];
+            }
+        } else {
+            const double* src = j == 0 ? a : (j == 1 ? g : nullptr);
+            if (j < 2 && !src) continue;
+            if (j >= 2 && !s) continue;
+            for (int64_t i = 0; i < n; ++i) buf[i] = j < 2 ? src[i] : s[i * S + (j - 2)];
+            upload_real(t, dev, buf.data(), n);
+        }
+    }
+}
+
+esrnn_status esrnn_trainer_get_per_series(esrnn_trainer* t, int64_t r0, int64_t n, double* a, double* g, double* s) {
+    return guarded(t->err, [&] { ps_io(t, r0, n, a, g, s, true); });
+}
+
+esrnn_status esrnn_trainer_set_per_series(esrnn_trainer* t, int64_t r0, int64_t n, const double* a, const double* g,
+                                          const double* s) {
+    return guarded(t->err, [&] {
+        ps_io(t, r0, n, const_cast<double*>(a), const_cast<double*>(g), const_cast<double*>(s), false);
+    });
+}
+
+esrnn_status esrnn_trainer_train_epoch(esrnn_trainer* t, double* mean_loss) {
+    return guarded(t->err, [&] {
+        CUDA_OK(cudaSetDevice(t->cfg.device));
+        const double l = t->fp64 ? train_epoch_impl<double>(t) : train_epoch_impl<float>(t);
+        *mean_loss = l;
+    });
+}
+
+esrnn_status esrnn_trainer_run_batch(esrnn_trainer* t, int32_t B, const int32_t* rows, const int32_t* anchors,
+                                     const double* mask, int32_t flags, double* loss, double* mask_count,
+                                     double* inputs, double* targets, double* seas, double* levels,
+                                     double* net_grads, int32_t* n_slots, int32_t* slot_rows, double* ps_grads) {
+    return guarded(t->err, [&] {
+        CUDA_OK(cudaSetDevice(t->cfg.device));
+        if (t->fp64)
+            run_batch_impl<double>(t, B, rows, anchors, mask, flags, loss, mask_count, inputs, targets, seas, levels,
+                                   net_grads, n_slots, slot_rows, ps_grads);
+        else
+            run_batch_impl<float>(t, B, rows, anchors, mask, flags, loss, mask_count, inputs, targets, seas, levels,
+                                  net_grads, n_slots, slot_rows, ps_grads);
+    });
+}
+
+esrnn_status esrnn_trainer_forecast(esrnn_trainer* t, int64_t drop_tail, double* out) {
+    return guarded(t->err, [&] {
+        CUDA_OK(cudaSetDevice(t->cfg.device));
+        if (t->fp64) forecast_impl<double>(t, drop_tail, out, nullptr, nullptr, false);
+        else forecast_impl<float>(t, drop_tail, out, nullptr, nullptr, false);
+    });
+}
+
+esrnn_status esrnn_trainer_validate(esrnn_trainer* t, double* forecasts, double* smape, double* mean) {
+    return guarded(t->err, [&] {
+        CUDA_OK(cudaSetDevice(t->cfg.device));
+        const int64_t dt = 2 * static_cast<int64_t>(t->O);
+        if (t->fp64) forecast_impl<double>(t, dt, forecasts, smape, mean, true);
+        else forecast_impl<float>(t, dt, forecasts, smape, mean, true);
+    });
+}
+
+esrnn_status esrnn_trainer_hw_state(esrnn_trainer* t, int64_t row, int64_t t_len, double* levels, double* seas) {
+    return guarded(t->err, [&] {
+        CUDA_OK(cudaSetDevice(t->cfg.device));
+        if (t->fp64) hw_state_impl<double>(t, row, t_len, levels, seas);
+        else hw_state_impl<float>(t, row, t_len, levels, seas);
+    });
+}
+
+esrnn_status esrnn_trainer_last_device_ms(const esrnn_trainer* t, double* ms) {
+    *ms = t->last_ms;
+    return ESRNN_OK;
+}
+
+esrnn_status esrnn_trainer_kernel_launches(const esrnn_trainer* t, int64_t* n) {
+    *n = t->launches;
+    return ESRNN_OK;
+}
+
+esrnn_status esrnn_nccl_unique_id(uint8_t out[128]) {
+    return guarded(g_create_err, [&] {
+        ncclUniqueId id;
+        NCCL_OK(ncclGetUniqueId(&id));
+        std::memcpy(out, id.internal, 128);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,530 @@
+"""Host-side mirror of the reference's hot-path API (reference trainer.hpp / data.hpp /
+holt_winters.hpp / network.hpp) over the engine C-ABI.
+
+Same names, argument meaning and error behaviour as the C++ reference, so parity tests
+read like the reference's own tests:
+
+    FrequencyProfile.defaults(Frequency.Quarterly)      data.hpp:69-99
+    TrainConfig(batch_size=..., seed=...)                trainer.hpp:22-44
+    Trainer(series, profile, cfg)                        trainer.hpp:159-200
+    .train_epoch() / .validate() / .forecast_at(k)       trainer.hpp:234-305
+    .batch_loss(b) / .batch_gradients(b)                 trainer.hpp:308-342
+    .benchmark_batched_vs_looped()                       trainer.hpp:351-413
+    make_batches / pinball_loss / early_stop_check        trainer.hpp:64-120
+
+All device work runs in the CUDA engine (libesrnn_b200.so); this module only marshals
+host buffers and reproduces host-side index logic (window lists, RNG shuffles) where the
+reference API exposes it.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import time
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _native as N
+from . import errors as E
+from .rng import Rng
+
+
+class Category(enum.IntEnum):  # data.hpp:18
+    Demographic = 0
+    Finance = 1
+    Industry = 2
+    Macro = 3
+    Micro = 4
+    Other = 5
+
+
+class Frequency(enum.IntEnum):  # data.hpp:19
+    Yearly = 0
+    Quarterly = 1
+    Monthly = 2
+
+
+@dataclass
+class SeriesRecord:  # data.hpp:52-57
+    id: str
+    values: np.ndarray
+    category: Optional[Category] = None
+    frequency: Optional[Frequency] = None
+
+
+@dataclass
+class FrequencyProfile:  # data.hpp:60-118
+    frequency: Frequency = Frequency.Quarterly
+    seasonality_length: int = 4
+    horizon: int = 8
+    input_window: int = 12
+    dilation_blocks: list = field(default_factory=lambda: [[1, 2], [4, 8]])
+    hidden_size: int = 40
+    min_length: int = 72
+
+    @staticmethod
+    def defaults(f: Frequency) -> "FrequencyProfile":
+        if f == Frequency.Yearly:
+            return FrequencyProfile(f, 1, 6, 6, [[1, 2], [2, 6]], 30, 13)
+        if f == Frequency.Quarterly:
+            return FrequencyProfile(f, 4, 8, 12, [[1, 2], [4, 8]], 40, 72)
+        return FrequencyProfile(f, 12, 18, 24, [[1, 3], [6, 12]], 50, 72)
+
+    def equalized_length(self) -> int:
+        return self.min_length + 2 * self.horizon
+
+    def to_c(self) -> N.Profile:
+        p = N.Profile()
+        p.frequency = int(self.frequency)
+        p.seasonality_length = self.seasonality_length
+        p.horizon = self.horizon
+        p.input_window = self.input_window
+        p.hidden_size = self.hidden_size
+        p.min_length = self.min_length
+        if len(self.dilation_blocks) > N.MAX_BLOCKS:
+            raise E.ConfigError("profile: too many dilation blocks")
+        p.n_blocks = len(self.dilation_blocks)
+        layer = 0
+        for b, blk in enumerate(self.dilation_blocks):
+            p.block_len[b] = len(blk)
+            for d in blk:
+                if layer >= N.MAX_LAYERS:
+                    raise E.ConfigError("profile: too many layers")
+                p.dilations[layer] = int(d)
+                layer += 1
+        return p
+
+
+@dataclass
+class TrainConfig:  # trainer.hpp:22-44 (+ B200 extensions)
+    epochs: int = 15
+    batch_size: int = 512
+    learning_rate_network: float = 1e-3
+    learning_rate_per_series: float = 1e-2
+    tau: float = 0.5
+    gradient_clip: Optional[float] = 20.0
+    seed: int = 0
+    attach_es_state: bool = True
+    patience: int = 0
+    min_delta: float = 0.0
+    # B200 extensions
+    precision: str = "fp32"          # "fp32" (performance) | "fp64" (parity mode)
+    max_batch_size: int = 0          # 0 -> 2048 reference cap
+    device: int = 0
+    use_graphs: bool = True
+
+    def to_c(self) -> N.TrainCfg:
+        c = N.TrainCfg()
+        c.epochs = self.epochs
+        c.batch_size = self.batch_size
+        c.learning_rate_network = self.learning_rate_network
+        c.learning_rate_per_series = self.learning_rate_per_series
+        c.tau = self.tau
+        c.has_gradient_clip = 0 if self.gradient_clip is None else 1
+        c.gradient_clip = 0.0 if self.gradient_clip is None else float(self.gradient_clip)
+        c.seed = int(self.seed) & 0xFFFFFFFFFFFFFFFF
+        c.attach_es_state = 1 if self.attach_es_state else 0
+        c.patience = self.patience
+        c.min_delta = self.min_delta
+        c.precision = N.FP64 if self.precision == "fp64" else N.FP32
+        c.max_batch_size = self.max_batch_size
+        c.device = self.device
+        c.use_graphs = 0 if self.use_graphs else -1
+        return c
+
+
+@dataclass
+class DatasetSplit:  # data.hpp:122-126
+    train: np.ndarray
+    validation: np.ndarray
+    test: np.ndarray
+
+
+def split_train_val_test(values: np.ndarray, horizon: int) -> DatasetSplit:  # data.hpp:128-140
+    n, o = len(values), horizon
+    if n < 2 * o + 1:
+        raise E.InsufficientLengthError(f"split: need at least {2 * o + 1} values, got {n}")
+    return DatasetSplit(values[: n - 2 * o], values[n - 2 * o: n - o], values[n - o:])
+
+
+@dataclass
+class PerSeriesParams:  # holt_winters.hpp:26-43
+    alpha_raw: float = 0.0
+    gamma_raw: float = 0.0
+    init_seasonality_raw: np.ndarray = field(default_factory=lambda: np.zeros(1))
+
+    def season_length(self) -> int:
+        return len(self.init_seasonality_raw)
+
+
+@dataclass
+class WindowBatch:  # trainer.hpp:50-61
+    series_rows: list
+    anchors: list
+    ids: list = field(default_factory=list)
+    mask: Optional[np.ndarray] = None           # (B, O); None -> ones
+    inputs: Optional[np.ndarray] = None         # (B, I+6) filled by the pass
+    targets: Optional[np.ndarray] = None        # (B, O)
+    anchor_levels: Optional[np.ndarray] = None  # (B,)
+    seasonality_slices: Optional[np.ndarray] = None  # (B, O)
+
+    def size(self) -> int:
+        return len(self.series_rows)
+
+
+@dataclass
+class ValidationResult:  # trainer.hpp:122-127
+    ids: list
+    forecasts: np.ndarray
+    smape_per_series: np.ndarray
+    mean_smape: float
+
+
+@dataclass
+class ForecastResult:  # trainer.hpp:129-132
+    ids: list
+    forecasts: np.ndarray
+
+
+@dataclass
+class BenchmarkReport:  # trainer.hpp:134-140
+    batched_s: float = 0.0
+    looped_s: float = 0.0
+    speedup: float = 0.0
+    batch_size: int = 0
+    n_series: int = 0
+
+
+@dataclass
+class PerSeriesGrad:  # trainer.hpp:146-150
+    alpha_raw: float
+    gamma_raw: float
+    init_seasonality_raw: np.ndarray
+
+
+@dataclass
+class BatchGradients:  # trainer.hpp:143-152
+    loss: float
+    network: dict
+    per_series: dict
+    slot_rows: list = field(default_factory=list)
+
+
+def pinball_loss(predicted, actual, tau: float, mask) -> float:  # trainer.hpp:64-78
+    predicted, actual, mask = (np.asarray(x, dtype=np.float64) for x in (predicted, actual, mask))
+    if predicted.shape != actual.shape:
+        raise E.ShapeError("pinball_loss: shape mismatch")
+    if predicted.shape != mask.shape:
+        raise E.ShapeError("pinball_loss mask: shape mismatch")
+    if not (0.0 < tau < 1.0):
+        raise E.ContractError("pinball_loss: tau must be in (0, 1)")
+    acc = 0.0
+    count = 0.0
+    for p, a, m in zip(predicted.ravel(), actual.ravel(), mask.ravel()):
+        if m == 0.0:
+            continue
+        d = a - p
+        acc += tau * d if d >= 0.0 else (tau - 1.0) * d
+        count += 1.0
+    if count == 0.0:
+        raise E.ContractError("pinball_loss: all-zero mask, mean undefined")
+    return acc / count
+
+
+def make_batches(windows, series_ids, batch_size: int, horizon: int, rng: Rng):  # trainer.hpp:82-102
+    windows = list(windows)
+    if not windows:
+        raise E.ContractError("make_batches: no windows")
+    if batch_size < 1:
+        raise E.ConfigError("make_batches: batch_size must be >= 1")
+    rng.shuffle(windows)
+    out = []
+    for start in range(0, len(windows), batch_size):
+        chunk = windows[start:start + batch_size]
+        out.append(WindowBatch([w[0] for w in chunk], [w[1] for w in chunk],
+                               [series_ids[w[0]] for w in chunk], np.ones((len(chunk), horizon))))
+    return out
+
+
+def early_stop_check(history: Sequence[float], patience: int, min_delta: float = 0.0) -> bool:  # :107-120
+    if len(history) == 0:
+        raise E.ContractError("early_stop_check: empty history")
+    if patience <= 0:
+        return False
+    best, last_improve = history[0], 0
+    for i in range(1, len(history)):
+        if best - history[i] > min_delta:
+            best, last_improve = history[i], i
+    return len(history) - 1 - last_improve >= patience
+
+
+class Trainer:
+    """esrnn::Trainer (trainer.hpp:157-673) backed by a native engine handle."""
+
+    def __init__(self, series, profile: FrequencyProfile, cfg: TrainConfig, *, api: N.NativeApi | None = None,
+                 dist: tuple[int, int, bytes] | None = None):
+        self.api = api if api is not None else N.product_api()
+        self._profile = profile
+        self._cfg = cfg
+        if isinstance(series, tuple):
+            values, cats = series
+            values = np.ascontiguousarray(values, dtype=np.float64)
+            cats = np.ascontiguousarray(cats, dtype=np.int32)
+            self._ids = [f"S{i}" for i in range(values.shape[0])]
+        else:
+            series = list(series)
+            if not series:
+                raise E.ContractError("trainer: no series")
+            n = len(series[0].values)
+            for s in series:
+                if len(s.values) != n:
+                    raise E.ConfigError(f'trainer: rectangular batching requires equal series lengths; "{s.id}" '
+                                        f"has {len(s.values)} values, expected {n}")
+            values = np.ascontiguousarray(np.stack([np.asarray(s.values, dtype=np.float64) for s in series]))
+            cats = np.array([-1 if s.category is None else int(s.category) for s in series], dtype=np.int32)
+            self._ids = [s.id for s in series]
+        self._values = values
+        self._cats = cats
+        c_dist = None
+        if dist is not None:
+            c_dist = N.Dist()
+            c_dist.rank, c_dist.world_size = dist[0], dist[1]
+            C.memmove(c_dist.nccl_unique_id, dist[2], 128)
+        h = C.c_void_p()
+        p_c, cfg_c = profile.to_c(), cfg.to_c()
+        self.api.check(self.api.lib.esrnn_trainer_create(
+            C.byref(p_c), C.byref(cfg_c), values.shape[0], values.shape[1], N.dptr(values), N.iptr(cats),
+            C.byref(c_dist) if c_dist is not None else None, C.byref(h)))
+        self._h = h
+        b, e = C.c_int64(), C.c_int64()
+        self._chk(self.api.lib.esrnn_trainer_shard(h, C.byref(b), C.byref(e)))
+        self.row_begin, self.row_end = b.value, e.value
+        na, nv = C.c_int32(), C.c_int64()
+        self._chk(self.api.lib.esrnn_trainer_param_count(h, C.byref(na), C.byref(nv)))
+        self.n_values = nv.value
+        self.param_layout = []
+        for i in range(na.value):
+            info = N.ParamInfo()
+            self._chk(self.api.lib.esrnn_trainer_param_info(h, i, C.byref(info)))
+            self.param_layout.append((info.name.decode(), info.rows, info.cols, info.offset))
+
+    # -- plumbing -------------------------------------------------------------------
+    def _chk(self, status):
+        self.api.check(status, self._h)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self.api.lib.esrnn_trainer_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    # -- accessors (trainer.hpp:202-211) ------------------------------------------------
+    def profile(self) -> FrequencyProfile:
+        return self._profile
+
+    def config(self) -> TrainConfig:
+        return self._cfg
+
+    def series_count(self) -> int:
+        return self._values.shape[0]
+
+    def series(self, i: int) -> SeriesRecord:
+        c = int(self._cats[i])
+        return SeriesRecord(self._ids[i], self._values[i].copy(), None if c < 0 else Category(c))
+
+    def split(self, i: int) -> DatasetSplit:
+        return split_train_val_test(self._values[i], self._profile.horizon)
+
+    def series_ids(self) -> list:
+        return list(self._ids)
+
+    def train_length(self) -> int:
+        return self._values.shape[1] - 2 * self._profile.horizon
+
+    def all_windows(self) -> list:  # trainer.hpp:214-223
+        I, O, T = self._profile.input_window, self._profile.horizon, self.train_length()
+        return [(r, a) for r in range(self.series_count()) for a in range(I - 1, T - O)]
+
+    def weights_flat(self) -> np.ndarray:
+        w = np.zeros(self.n_values)
+        self._chk(self.api.lib.esrnn_trainer_get_weights(self._h, N.dptr(w), self.n_values))
+        return w
+
+    def weights(self) -> dict:
+        """StackWeights by name (for_each_param order), as copies."""
+        flat = self.weights_flat()
+        return {n: flat[o:o + r * c].reshape(r, c).copy() for n, r, c, o in self.param_layout}
+
+    def set_weights(self, w) -> None:  # trainer.hpp:415-432
+        if isinstance(w, dict):
+            flat = np.zeros(self.n_values)
+            if set(w) != {n for n, *_ in self.param_layout}:
+                raise E.CheckpointError("checkpoint network shapes incompatible with configuration")
+            for n, r, c, o in self.param_layout:
+                a = np.asarray(w[n], dtype=np.float64)
+                if a.shape != (r, c):
+                    raise E.CheckpointError("checkpoint network shapes incompatible with configuration")
+                flat[o:o + r * c] = a.ravel()
+        else:
+            flat = np.ascontiguousarray(w, dtype=np.float64)
+        self._chk(self.api.lib.esrnn_trainer_set_weights(self._h, N.dptr(flat), flat.size))
+
+    def per_series_arrays(self):
+        n = self.row_end - self.row_begin
+        S = self._profile.seasonality_length
+        a, g, s = np.zeros(n), np.zeros(n), np.zeros((n, S))
+        self._chk(self.api.lib.esrnn_trainer_get_per_series(self._h, self.row_begin, n, N.dptr(a), N.dptr(g),
+                                                             N.dptr(s)))
+        return a, g, s
+
+    def set_per_series_arrays(self, a, g, s, row_begin=None):
+        a, g, s = (np.ascontiguousarray(x, dtype=np.float64) for x in (a, g, s))
+        rb = self.row_begin if row_begin is None else row_begin
+        self._chk(self.api.lib.esrnn_trainer_set_per_series(self._h, rb, a.shape[0], N.dptr(a), N.dptr(g),
+                                                             N.dptr(s)))
+
+    def per_series_params(self, i: int) -> PerSeriesParams:
+        S = self._profile.seasonality_length
+        a, g, s = np.zeros(1), np.zeros(1), np.zeros(S)
+        self._chk(self.api.lib.esrnn_trainer_get_per_series(self._h, i, 1, N.dptr(a), N.dptr(g), N.dptr(s)))
+        return PerSeriesParams(float(a[0]), float(g[0]), s)
+
+    def set_per_series_params(self, i: int, p: PerSeriesParams) -> None:
+        a, g = np.array([p.alpha_raw]), np.array([p.gamma_raw])
+        s = np.ascontiguousarray(p.init_seasonality_raw, dtype=np.float64)
+        self._chk(self.api.lib.esrnn_trainer_set_per_series(self._h, i, 1, N.dptr(a), N.dptr(g), N.dptr(s)))
+
+    def set_per_series(self, by_id: dict) -> None:  # trainer.hpp:434-445
+        S = self._profile.seasonality_length
+        for r in range(self.row_begin, self.row_end):
+            sid = self._ids[r]
+            if sid not in by_id:
+                raise E.CheckpointError(f'checkpoint missing per-series parameters for "{sid}"')
+            if by_id[sid].season_length() != S:
+                raise E.CheckpointError(f'checkpoint season length incompatible for "{sid}"')
+        for r in range(self.row_begin, self.row_end):
+            self.set_per_series_params(r, by_id[self._ids[r]])
+
+    def hw_state(self, row: int, t_len: int):
+        S = self._profile.seasonality_length
+        lv, se = np.zeros(t_len), np.zeros(t_len + S)
+        self._chk(self.api.lib.esrnn_trainer_hw_state(self._h, row, t_len, N.dptr(lv), N.dptr(se)))
+        return lv, se
+
+    # -- hot path ----------------------------------------------------------------------
+    def train_epoch(self) -> float:  # trainer.hpp:234-243
+        out = C.c_double()
+        self._chk(self.api.lib.esrnn_trainer_train_epoch(self._h, C.byref(out)))
+        return out.value
+
+    def _run_batch(self, batch: WindowBatch, flags: int, want_grads_out: bool):
+        B = batch.size()
+        O = self._profile.horizon
+        I, S = self._profile.input_window, self._profile.seasonality_length
+        rows = np.ascontiguousarray(batch.series_rows, dtype=np.int32)
+        anchors = np.ascontiguousarray(batch.anchors, dtype=np.int32)
+        mask = None
+        if batch.mask is not None:
+            mask = np.ascontiguousarray(batch.mask, dtype=np.float64)
+            if mask.shape != (B, O):
+                raise E.ShapeError(f"batch: mask shape ({mask.shape[0]}, {mask.shape[1] if mask.ndim > 1 else 1})")
+        loss, mc = C.c_double(), C.c_double()
+        inputs = np.zeros((B, I + N.NUM_CATEGORIES))
+        targets = np.zeros((B, O))
+        seas = np.zeros((B, O))
+        levels = np.zeros(B)
+        gnet = np.zeros(self.n_values) if want_grads_out else None
+        nslots = C.c_int32()
+        slot_rows = np.zeros(max(B, 1), dtype=np.int32)
+        gps = np.zeros((max(B, 1), 2 + S)) if want_grads_out else None
+        self._chk(self.api.lib.esrnn_trainer_run_batch(
+            self._h, B, N.iptr(rows), N.iptr(anchors), N.dptr(mask), flags, C.byref(loss), C.byref(mc),
+            N.dptr(inputs), N.dptr(targets), N.dptr(seas), N.dptr(levels), N.dptr(gnet), C.byref(nslots),
+            N.iptr(slot_rows), N.dptr(gps)))
+        batch.inputs, batch.targets, batch.seasonality_slices, batch.anchor_levels = inputs, targets, seas, levels
+        k = nslots.value
+        return loss.value, mc.value, gnet, slot_rows[:k].copy(), (gps[:k].copy() if gps is not None else None)
+
+    def batch_loss(self, batch: WindowBatch) -> float:  # trainer.hpp:338-342
+        return self._run_batch(batch, 0, False)[0]
+
+    def batch_gradients(self, batch: WindowBatch) -> BatchGradients:  # trainer.hpp:308-335
+        loss, _, gnet, slot_rows, gps = self._run_batch(batch, N.BATCH_GRADS, True)
+        net = {n: gnet[o:o + r * c].reshape(r, c).copy() for n, r, c, o in self.param_layout}
+        per = {}
+        if self._cfg.attach_es_state:
+            for s, row in enumerate(slot_rows):
+                per[self._ids[row]] = PerSeriesGrad(float(gps[s, 0]), float(gps[s, 1]), gps[s, 2:].copy())
+        return BatchGradients(loss, net, per, list(slot_rows))
+
+    def step(self, batch: WindowBatch, update: bool = True):
+        """trainer.hpp:593-600 (private in the reference; public here for tests/bench)."""
+        loss, mc, *_ = self._run_batch(batch, N.BATCH_GRADS | (N.BATCH_UPDATE if update else 0), False)
+        return loss, mc
+
+    def forecast_at(self, drop_tail: int) -> ForecastResult:  # trainer.hpp:248-288
+        n = self.row_end - self.row_begin
+        out = np.zeros((n, self._profile.horizon))
+        self._chk(self.api.lib.esrnn_trainer_forecast(self._h, drop_tail, N.dptr(out)))
+        return ForecastResult(self._ids[self.row_begin:self.row_end], out)
+
+    def validate(self) -> ValidationResult:  # trainer.hpp:292-305
+        n = self.row_end - self.row_begin
+        fc = np.zeros((n, self._profile.horizon))
+        sm = np.zeros(n)
+        mean = C.c_double()
+        self._chk(self.api.lib.esrnn_trainer_validate(self._h, N.dptr(fc), N.dptr(sm), C.byref(mean)))
+        return ValidationResult(self._ids[self.row_begin:self.row_end], fc, sm, mean.value)
+
+    def last_device_ms(self) -> float:
+        ms = C.c_double()
+        self._chk(self.api.lib.esrnn_trainer_last_device_ms(self._h, C.byref(ms)))
+        return ms.value
+
+    def kernel_launches(self) -> int:
+        n = C.c_int64()
+        self._chk(self.api.lib.esrnn_trainer_kernel_launches(self._h, C.byref(n)))
+        return n.value
+
+    def benchmark_batched_vs_looped(self) -> BenchmarkReport:  # trainer.hpp:351-413
+        windows = self.all_windows()
+        O = self._profile.horizon
+
+        def batches_of(bs):
+            return [WindowBatch([w[0] for w in windows[s:s + bs]], [w[1] for w in windows[s:s + bs]],
+                                ["w"] * len(windows[s:s + bs]), np.ones((len(windows[s:s + bs]), O)))
+                    for s in range(0, len(windows), bs)]
+
+        def timed_epoch(batches):
+            t0 = time.perf_counter()
+            acc = weight = 0.0
+            for b in batches:
+                loss, mc = self.step(b, update=False)
+                acc += loss * mc
+                weight += mc
+            return acc / weight, time.perf_counter() - t0
+
+        batched, looped = batches_of(self._cfg.batch_size), batches_of(1)
+        self.step(batched[0], update=False)
+        self.step(looped[0], update=False)
+        sb = sl = float("inf")
+        lb = ll = 0.0
+        for _ in range(3):
+            lb, t_b = timed_epoch(batched)
+            ll, t_l = timed_epoch(looped)
+            sb, sl = min(sb, t_b), min(sl, t_l)
+        rel = abs(lb - ll) / max(1e-30, abs(ll))
+        if rel > 1e-6:
+            raise E.EquivalenceError(f"benchmark: batched loss {lb} vs looped {ll} differ beyond 1e-6; timing withheld")
+        return BenchmarkReport(sb, sl, sl / sb, self._cfg.batch_size, self.series_count())

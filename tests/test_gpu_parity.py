@@ -1,0 +1,209 @@
+"""GPU parity: the CUDA engine (through the C-ABI) against the fp64 C oracle on identical
+seeded inputs.  fp64 mode must agree to ~1e-10; fp32 mode carries the north-star
+contract of 1e-4 relative per step (tensor-scaled, see tensor_err).
+
+Mirrors the reference's own checks: batched window elements / loss (acceptance.cpp:332-373),
+joint gradients (test_trainer.cpp:139-161), masking (acceptance.cpp:493-550), updates
+(test_trainer.cpp:96-137), forecast/validate (test_trainer.cpp:200-216), determinism
+(test_trainer.cpp:218-230).
+"""
+import numpy as np
+import pytest
+
+from conftest import PROFILES, dataset, max_rel, tensor_err
+from paper_1907_03329_b200 import errors as E
+from paper_1907_03329_b200.trainer import TrainConfig, Trainer, WindowBatch
+
+pytestmark = pytest.mark.gpu
+
+CASES = [("tiny", 3, 11, 16), ("quarterly", 12, 41, 64), ("yearly", 40, 5, 64), ("monthly", 9, 7, 64)]
+
+
+def pair(engine, oracle, name, n, seed, precision="fp64", **kw):
+    prof, vals, cats = dataset(oracle, name, n, seed)
+    cfg = TrainConfig(seed=7, precision=precision, **kw)
+    return (Trainer((vals, cats), prof, cfg, api=engine), Trainer((vals, cats), prof, cfg, api=oracle))
+
+
+def sample_batch(tr, B, seed, masked_rows=(), partial_row=None):
+    rng = np.random.default_rng(seed)
+    w = tr.all_windows()
+    idx = rng.integers(0, len(w), size=B)
+    O = tr.profile().horizon
+    mask = np.ones((B, O))
+    for r in masked_rows:
+        mask[r] = 0.0
+    if partial_row is not None:
+        mask[partial_row, ::2] = 0.0
+    return WindowBatch([w[i][0] for i in idx], [w[i][1] for i in idx], mask=mask)
+
+
+def copy_batch(b):
+    return WindowBatch(list(b.series_rows), list(b.anchors), mask=None if b.mask is None else b.mask.copy())
+
+
+@pytest.mark.parametrize("name,n,seed,B", CASES)
+def test_init_weights_identical(engine, oracle, name, n, seed, B):
+    g, o = pair(engine, oracle, name, n, seed)
+    assert np.array_equal(g.weights_flat(), o.weights_flat())  # same RNG consumption (network.hpp:89-116)
+
+
+@pytest.mark.parametrize("precision,tol", [("fp64", 1e-10), ("fp32", 1e-4)])
+@pytest.mark.parametrize("name,n,seed,B", CASES)
+def test_batch_gradients(engine, oracle, name, n, seed, B, precision, tol):
+    g, o = pair(engine, oracle, name, n, seed, precision)
+    b = sample_batch(o, B, seed, masked_rows=(1,), partial_row=2)
+    bg, bo = copy_batch(b), copy_batch(b)
+    gg, go = g.batch_gradients(bg), o.batch_gradients(bo)
+    assert max_rel(gg.loss, go.loss) < tol
+    for f in ("inputs", "targets", "seasonality_slices", "anchor_levels"):
+        assert tensor_err(getattr(bg, f), getattr(bo, f)) < tol, f
+    assert gg.slot_rows == go.slot_rows
+    for name_, arr in go.network.items():
+        assert tensor_err(gg.network[name_], arr) < tol * 10, name_
+        if name_.endswith("w_recur"):
+            assert not np.any(gg.network[name_])  # structurally zero at sequence length 1
+    for sid, ps in go.per_series.items():
+        pg = gg.per_series[sid]
+        v_g = np.r_[pg.alpha_raw, pg.gamma_raw, pg.init_seasonality_raw]
+        v_o = np.r_[ps.alpha_raw, ps.gamma_raw, ps.init_seasonality_raw]
+        scale = max(np.max(np.abs(v_o)), 1e-12)
+        assert np.max(np.abs(v_g - v_o)) / scale < tol * 100, sid
+
+
+@pytest.mark.parametrize("name,n,seed,B", CASES[:2])
+def test_loss_only_matches(engine, oracle, name, n, seed, B):
+    g, o = pair(engine, oracle, name, n, seed)
+    b = sample_batch(o, B, seed + 1)
+    assert max_rel(g.batch_loss(copy_batch(b)), o.batch_loss(copy_batch(b))) < 1e-12
+
+
+@pytest.mark.parametrize("name,n,seed,bs", [("tiny", 3, 11, 16), ("quarterly", 10, 41, 64),
+                                            ("yearly", 60, 5, 32), ("monthly", 6, 7, 48)])
+def test_train_epochs_fp64_trajectory(engine, oracle, name, n, seed, bs):
+    g, o = pair(engine, oracle, name, n, seed, batch_size=bs)
+    for _ in range(2):
+        lg, lo = g.train_epoch(), o.train_epoch()
+        assert max_rel(lg, lo) < 1e-8
+    assert tensor_err(g.weights_flat(), o.weights_flat()) < 1e-7
+    ag, gg_, sg = g.per_series_arrays()
+    ao, go_, so = o.per_series_arrays()
+    assert tensor_err(np.c_[ag, gg_, sg], np.c_[ao, go_, so]) < 1e-7
+    vg, vo = g.validate(), o.validate()
+    assert max_rel(vg.mean_smape, vo.mean_smape) < 1e-8
+    assert tensor_err(vg.forecasts, vo.forecasts) < 1e-8
+
+
+def test_train_epoch_fp32_tracks_oracle(engine, oracle):
+    g, o = pair(engine, oracle, "quarterly", 10, 41, "fp32", batch_size=64)
+    lg, lo = g.train_epoch(), o.train_epoch()
+    assert max_rel(lg, lo) < 1e-3
+    assert abs(g.validate().mean_smape - o.validate().mean_smape) < 0.1
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+@pytest.mark.parametrize("name", ["tiny", "quarterly", "yearly", "monthly"])
+def test_forecast_at(engine, oracle, name, precision):
+    prof = PROFILES[name][0]
+    g, o = pair(engine, oracle, name, 7, 3, precision)
+    tol = 1e-12 if precision == "fp64" else 1e-5
+    for drop in (0, prof.horizon, 2 * prof.horizon):
+        assert tensor_err(g.forecast_at(drop).forecasts, o.forecast_at(drop).forecasts) < tol
+
+
+def test_hw_state_matches_oracle(engine, oracle):
+    g, o = pair(engine, oracle, "monthly", 4, 3)
+    a = np.array([0.3, -0.7, 1.1, 2.0])
+    s = np.linspace(-0.2, 0.2, 4 * 12).reshape(4, 12)
+    for t in (g, o):
+        t.set_per_series_arrays(a, -a, s)
+    for row in range(4):
+        for tl in (12, 50, 108):
+            lg, sg = g.hw_state(row, tl)
+            lo, so = o.hw_state(row, tl)
+            assert max_rel(lg, lo) < 1e-13 and max_rel(sg, so) < 1e-13
+
+
+def test_masking_bit_zero(engine, oracle):
+    """acceptance.cpp:493-550: padded rows with mask 0 give bit-zero per-series gradients."""
+    g, _ = pair(engine, oracle, "quarterly", 6, 71)
+    I, O = 12, 8
+    small = WindowBatch([0, 1, 2, 3], [I - 1, I + 5, I + 9, I + 2], mask=np.ones((4, O)))
+    padded = WindowBatch([0, 1, 2, 3, 4, 5], [I - 1, I + 5, I + 9, I + 2, I + 7, I + 1], mask=np.ones((6, O)))
+    padded.mask[4:] = 0.0
+    gs, gp = g.batch_gradients(small), g.batch_gradients(padded)
+    assert abs(gs.loss - gp.loss) <= 1e-12
+    for k, v in gs.network.items():
+        assert np.max(np.abs(v - gp.network[k])) <= 1e-12
+    for sid in ("S4", "S5"):
+        p = gp.per_series[sid]
+        assert p.alpha_raw == 0.0 and p.gamma_raw == 0.0 and not np.any(p.init_seasonality_raw)
+
+
+def test_zero_learning_rates_bit_unchanged(engine, oracle):
+    """test_trainer.cpp:96-119"""
+    g, _ = pair(engine, oracle, "tiny", 3, 11, batch_size=16, learning_rate_network=0.0,
+                learning_rate_per_series=0.0)
+    w0 = g.weights_flat()
+    p0 = g.per_series_arrays()
+    assert np.isfinite(g.train_epoch())
+    assert np.array_equal(w0, g.weights_flat())
+    for a, b in zip(p0, g.per_series_arrays()):
+        assert np.array_equal(a, b)
+
+
+def test_detached_state_freezes_per_series(engine, oracle):
+    """test_trainer.cpp:274-282"""
+    g, o = pair(engine, oracle, "tiny", 2, 41, batch_size=16, attach_es_state=False)
+    p0 = g.per_series_arrays()
+    lg, lo = g.train_epoch(), o.train_epoch()
+    assert max_rel(lg, lo) < 1e-9
+    for a, b in zip(p0, g.per_series_arrays()):
+        assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_same_seed_bit_identical(engine, oracle, precision):
+    """test_trainer.cpp:218-230: same seed reproduces the loss trajectory bit for bit."""
+    a, _ = pair(engine, oracle, "quarterly", 20, 29, precision, batch_size=64)
+    b, _ = pair(engine, oracle, "quarterly", 20, 29, precision, batch_size=64)
+    for _ in range(3):
+        assert a.train_epoch() == b.train_epoch()
+    assert a.validate().mean_smape == b.validate().mean_smape
+
+
+def test_validate_zero_network(engine, oracle):
+    """test_trainer.cpp:200-216: zero weights -> forecasts 0, sMAPE 200, read-only."""
+    g, _ = pair(engine, oracle, "tiny", 3, 23)
+    g.set_weights(np.zeros(g.n_values))
+    v1, v2 = g.validate(), g.validate()
+    assert np.all(v1.forecasts == 0.0)
+    assert abs(v1.mean_smape - 200.0) < 1e-12
+    assert v1.mean_smape == v2.mean_smape
+
+
+def test_errors(engine, oracle):
+    g, _ = pair(engine, oracle, "tiny", 3, 11)
+    with pytest.raises(E.ShapeError):
+        g.batch_loss(WindowBatch([0], [100]))
+    with pytest.raises(E.ContractError):
+        g.batch_loss(WindowBatch([0], [7], mask=np.zeros((1, 4))))
+    with pytest.raises(E.ContractError):
+        g.batch_loss(WindowBatch([], []))
+    with pytest.raises(E.CheckpointError):
+        g.set_weights(np.zeros(3))
+    with pytest.raises(E.InsufficientLengthError):
+        g.forecast_at(1000)
+
+
+def test_numeric_domain_error(engine, oracle):
+    prof, vals, cats = dataset(oracle, "tiny", 2, 5)
+    vals[1, 3] = -vals[1, 3] * 50.0  # drives a level negative mid-scan
+    g = Trainer((vals, cats), prof, TrainConfig(seed=1, batch_size=16), api=engine)
+    o = Trainer((vals, cats), prof, TrainConfig(seed=1, batch_size=16), api=oracle)
+    with pytest.raises(E.NumericDomainError):
+        o.train_epoch()
+    with pytest.raises(E.NumericDomainError):
+        g.train_epoch()
+    with pytest.raises(E.NumericDomainError):
+        g.validate()
