@@ -1,0 +1,396 @@
+#!/usr/bin/env python3
+"""ES-RNN training throughput on B200 (BASELINE.json metric: train series/sec, M4-Quarterly shape).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg1|cfg2|cfg3|q24k|sweep<B>]
+                    [--impl b200|reference] [--precision fp32|fp64]
+
+A "step" is one pass of the hot path over the workload: one training epoch (every window
+once, reference Trainer::train_epoch, trainer.hpp:234-243) followed by one validation
+forecast (Trainer::validate, :292-305) — BASELINE configs[0] "one training epoch +
+forecast".  Default workload (cfg1): M4-Quarterly-shaped synthetic data, 1,000 series
+per GPU (weak scaling), length 88 (C=72 + 2*8), S=4, O=8, I=12, H=40, dilations
+(1,2),(4,8), batch 1,000 per GPU, data seed 41, train seed 7, fp32.
+
+value      series/s over all ranks, from CUDA-event device time of each step (max over
+           ranks); the L2 is flushed (512 MiB write) between timed steps, outside the events.
+e2e        the same metric through the public Python API with host buffers: every step
+           constructs the Trainer from host arrays (H2D of the series), trains one epoch
+           (H2D of the shuffled window plan), validates and reads back the losses,
+           forecasts and sMAPE (D2H); wall clock, synchronised.
+roofline   dominant kernel by device-time share, algorithmic FLOPs (SURVEY §8(d) formula)
+           per launch over its measured average launch time (CUDA events, profiling pass).
+cpu_baseline  the reference (oracle/_ref, the reference's own headers) timed on this host.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+from paper_1907_03329_b200 import _native as N  # noqa: E402
+from paper_1907_03329_b200.trainer import Frequency, FrequencyProfile, TrainConfig, Trainer  # noqa: E402
+
+REF_LIB = ROOT / "oracle" / "_ref" / "libesrnn_ref.so"
+PORT_LIB = ROOT / "oracle" / "liboracle_esrnn.so"
+
+CONFIGS = {
+    # name: (frequency, series per GPU or total, length, season, batch per GPU, scaling)
+    "cfg1": (Frequency.Quarterly, 1000, 88, 4, 1000, "weak"),
+    "cfg2": (Frequency.Yearly, 23000, 25, 1, 2048, "strong"),
+    "cfg3": (Frequency.Monthly, 48000, 108, 12, 2048, "strong"),
+    "q24k": (Frequency.Quarterly, 24000, 88, 4, 2048, "strong"),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg1")
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--precision", default="fp32", choices=["fp32", "fp64"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def workload(name: str, world: int):
+    if name.startswith("sweep"):
+        B = int(name[5:])
+        freq, n, length, s, scaling = Frequency.Quarterly, 24000, 88, 4, "strong"
+        return freq, n, length, s, B, scaling
+    freq, n, length, s, B, scaling = CONFIGS[name]
+    if scaling == "weak":
+        n, B = n * world, B * world
+    return freq, n, length, s, B, scaling
+
+
+def lstm_flops_per_step(prof: FrequencyProfile, B: int) -> float:
+    """live-gate LSTM FLOPs, fwd = sum_l 2*B*in_l*3H + 2BH^2 + 2BHO; bwd = 2*fwd."""
+    H, O = prof.hidden_size, prof.horizon
+    in0 = prof.input_window + 6
+    layers = sum(len(b) for b in prof.dilation_blocks)
+    fwd = sum(2.0 * B * (in0 if l == 0 else H) * 3 * H for l in range(layers)) + 2.0 * B * H * H + 2.0 * B * H * O
+    return 3.0 * fwd
+
+
+def scan_bytes(prof: FrequencyProfile, k: int, T: int) -> float:
+    """K1 algorithmic bytes (fp32): y (k*T) + params k(2+S) + levels k*T + seasonalities k(T+S)."""
+    S = prof.seasonality_length
+    return 4.0 * (k * T + k * (2 + S) + k * T + k * (T + S))
+
+
+class ClockSampler:
+    def __init__(self, path: Path):
+        self.path, self.proc = path, None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self, device: int):
+        try:
+            rows = [r.split(", ") for r in self.path.read_text().strip().splitlines()]
+        except Exception:
+            return None
+        rows = [r for r in rows if len(r) >= 9 and r[0].strip() == str(device)]
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for i, nm in enumerate(names):
+                if r[5 + i].strip().lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][2]), "reasons": sorted(reasons),
+                "samples": len(rows)}
+
+
+def dist_setup(gpus: int):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def allreduce_max(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def flush_l2(local: int):
+    import torch
+    buf = getattr(flush_l2, "buf", None)
+    if buf is None:
+        buf = flush_l2.buf = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+    buf.fill_(1.0)
+    torch.cuda.synchronize()
+
+
+def make_data(api, n, length, s, seed=41, sigma=0.05):
+    return api.make_synthetic(seed, n, length, s, sigma)
+
+
+# ----------------------------------------------------------------------------- CPU legs
+def time_cpu(lib_path: Path, prof, cfg: TrainConfig, vals, cats, budget_s: float):
+    """Reference / port on this host (1 thread: the reference is single-threaded).
+    Full epochs (+ validate) when an epoch fits the budget, else a bounded sample of
+    training batches through run_batch(update) extrapolated to the epoch."""
+    api = N.NativeApi(lib_path)
+    n = vals.shape[0]
+    cfg_c = TrainConfig(**{**cfg.__dict__, "precision": "fp64", "max_batch_size": 0,
+                           "batch_size": min(cfg.batch_size, 2048)})
+    tr = Trainer((vals, cats), prof, cfg_c, api=api)
+    T = vals.shape[1] - 2 * prof.horizon
+    per = T - prof.horizon - prof.input_window + 1
+    nw = n * per
+    steps = -(-nw // cfg_c.batch_size)
+    from paper_1907_03329_b200.trainer import WindowBatch
+    t0 = time.perf_counter()
+    tr.step(WindowBatch([0], [prof.input_window - 1]), update=False)
+    probe = time.perf_counter() - t0
+    # estimate one epoch: probe a single full batch
+    w = tr.all_windows()
+    rng = np.random.default_rng(0)
+    idx = rng.integers(0, len(w), size=cfg_c.batch_size)
+    b = WindowBatch([w[i][0] for i in idx], [w[i][1] for i in idx])
+    t0 = time.perf_counter()
+    tr.step(b, update=True)
+    per_batch = time.perf_counter() - t0
+    est_epoch = per_batch * steps
+    times = []
+    if est_epoch <= budget_s / 2:
+        kind = "epochs"
+        t_start = time.perf_counter()
+        while time.perf_counter() - t_start < budget_s or not times:
+            t0 = time.perf_counter()
+            tr.train_epoch()
+            tr.validate()
+            times.append(time.perf_counter() - t0)
+        step_s = statistics.median(times)
+        sample = f"{len(times)} full epochs (+validate) of {n} series, median"
+    else:
+        kind = "batches"
+        t_start = time.perf_counter()
+        nb = 0
+        while time.perf_counter() - t_start < budget_s or nb == 0:
+            idx = rng.integers(0, len(w), size=cfg_c.batch_size)
+            b = WindowBatch([w[i][0] for i in idx], [w[i][1] for i in idx])
+            tr.step(b, update=True)
+            nb += 1
+        per_batch = (time.perf_counter() - t_start) / nb
+        t0 = time.perf_counter()
+        tr.validate()
+        val_s = time.perf_counter() - t0
+        step_s = per_batch * steps + val_s
+        sample = (f"{nb} training batches of {cfg_c.batch_size} windows (+1 validate), extrapolated to "
+                  f"{steps} batches/epoch")
+    del probe, kind
+    return {"value": n / step_s, "unit": "series/s", "cores": 1, "epoch_s": step_s, "sample": sample,
+            "host_cores": os.cpu_count()}
+
+
+# ----------------------------------------------------------------------------- main
+def main():
+    a = parse()
+    world, rank, local = dist_setup(a.gpus)
+    freq, n_total, length, s, B, scaling = workload(a.config, world)
+    prof = FrequencyProfile.defaults(freq)
+    metric = "train series/sec (M4-Quarterly shape) at 1/2/4/8 B200 vs CPU ref; sMAPE parity"
+    cfg_desc = {"workload": f"{a.config}: {freq.name}-shaped synthetic, {n_total} series x length {length}, "
+                            f"S={s}, O={prof.horizon}, I={prof.input_window}, H={prof.hidden_size}, "
+                            f"dilations {prof.dilation_blocks}, batch {B}; step = 1 train epoch + validate",
+                "series": n_total, "global_batch": B, "length": length, "parallelism": f"series-sharded dp{world}",
+                "l2": "flushed between timed steps (512 MiB write)", "data_seed": 41, "train_seed": 7}
+
+    if a.impl == "reference":
+        if rank != 0:
+            return
+        lib = REF_LIB if REF_LIB.exists() else PORT_LIB
+        kind = "reference" if lib == REF_LIB else "port"
+        api = N.NativeApi(PORT_LIB if kind == "port" else REF_LIB)
+        vals, cats = make_data(api, n_total, length, s)
+        cfg = TrainConfig(batch_size=min(B, 2048), seed=7, precision="fp64")
+        for _ in range(max(a.warmup, 0)):
+            pass
+        res = [time_cpu(lib, prof, cfg, vals, cats, budget_s=max(3.0, 60.0 / max(a.steps, 1)))
+               for _ in range(max(a.steps, 1))]
+        v = statistics.median(r["value"] for r in res)
+        print(json.dumps({
+            "impl": "reference", "metric": metric, "value": v, "unit": "series/s", "n_gpus": world,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1000.0 * n_total / v, "higher_is_better": True,
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg_desc,
+            "cpu_baseline": {"value": v, "unit": "series/s", "cores": 1, "kind": kind, "sample": res[0]["sample"]},
+            "e2e": {"value": v, "unit": "series/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        return
+
+    api = N.product_api()
+    vals, cats = make_data(api, n_total, length, s)
+    cfg = TrainConfig(batch_size=B, seed=7, precision=a.precision, device=local,
+                      max_batch_size=max(B, 2048))
+    dist_arg = None
+    if world > 1:
+        import torch.distributed as dist
+        uid = [api.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        dist_arg = (rank, world, uid[0])
+    tr = Trainer((vals, cats), prof, cfg, api=api, dist=dist_arg)
+    n_local = tr.row_end - tr.row_begin
+
+    for _ in range(a.warmup):
+        tr.train_epoch()
+        tr.validate()
+    losses = []
+    dev_ms = []
+    wall = []
+    launches0 = tr.kernel_launches()
+    clock = ClockSampler(ROOT / "gpurun_out" / f"clocks_r{rank}.csv") if (ROOT / "gpurun_out").exists() else \
+        ClockSampler(Path(f"/tmp/esrnn_clocks_r{rank}.csv"))
+    import torch
+    torch.cuda.synchronize()
+    barrier(world)
+    with clock:
+        for _ in range(a.steps):
+            flush_l2(local)
+            barrier(world)
+            t0 = time.perf_counter()
+            losses.append(tr.train_epoch())
+            m_train = tr.last_device_ms()
+            v = tr.validate()
+            m_val = tr.last_device_ms()
+            wall.append(time.perf_counter() - t0)
+            dev_ms.append(m_train + m_val)
+    torch.cuda.synchronize()
+    barrier(world)
+    launches = tr.kernel_launches() - launches0
+    total_ms = allreduce_max(sum(dev_ms), world)
+    value = n_total * a.steps / (total_ms / 1000.0)
+    clocks = clock.summary(local)
+
+    # per-kernel profiling pass (outside the timed region)
+    tr.profile_kernels(True)
+    tr.train_epoch()
+    tr.validate()
+    kt = tr.kernel_times()
+    tr.profile_kernels(False)
+    tot = sum(ms for ms, _ in kt.values()) or 1.0
+    shares = {k: {"ms": ms, "launches": n, "share": ms / tot} for k, (ms, n) in kt.items() if n}
+    dom = max(shares, key=lambda k: shares[k]["ms"])
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    sm_max = peaks.get("sm_max_mhz", 1965.0)
+    fp32_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12
+    T = length - 2 * prof.horizon
+    per = T - prof.horizon - prof.input_window + 1
+    steps_per_epoch = -(-n_total * per // B)
+    B_local = B // world
+    if dom in ("stack",):
+        flops = lstm_flops_per_step(prof, B_local)
+        avg_s = shares[dom]["ms"] / shares[dom]["launches"] / 1e3
+        achieved = flops / avg_s / 1e12
+        peak = fp32_peak if a.precision == "fp32" else fp32_peak / 2
+        roof = {"kernel": "k_stack (fused window+LSTM fwd/bwd+pinball)", "bound": "fp32-fma",
+                "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                "peak_source": f"derived CUDA-core FP32 FMA peak: 148 SM x 128 lanes x 2 x {sm_max:.0f} MHz "
+                               f"(MEASURED_PEAKS sm_max_mhz); no tensor-core path (fp32 contract)",
+                "algorithmic_per_launch": f"{flops:.3e} FLOP (live-gate LSTM fwd+bwd, B={B_local})"}
+    else:
+        k_slots = min(n_local, B_local)
+        byts = scan_bytes(prof, k_slots, T)
+        avg_s = shares[dom]["ms"] / shares[dom]["launches"] / 1e3
+        achieved = byts / avg_s / 1e9
+        peak = peaks.get("hbm_gbs", 6553.9)
+        roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None, "peak_source": "MEASURED_PEAKS hbm_gbs (measured)",
+                "algorithmic_per_launch": f"{byts:.3e} B"}
+
+    # e2e through the public API with host buffers
+    e2e = None
+    if not a.no_e2e:
+        e2e_t = []
+        h2d = d2h = 0
+        for _ in range(max(1, a.steps)):
+            barrier(world)
+            t0 = time.perf_counter()
+            t2 = Trainer((vals, cats), prof, cfg, api=api, dist=dist_arg)
+            t2.train_epoch()
+            v2 = t2.validate()
+            t2.close()
+            e2e_t.append(time.perf_counter() - t0)
+            rb = 4 if a.precision == "fp32" else 8
+            h2d = n_local * length * rb + n_local * per * 3 * 4
+            d2h = steps_per_epoch * 8 + v2.forecasts.nbytes + v2.smape_per_series.nbytes
+        e2e_s = allreduce_max(sum(e2e_t), world)
+        e2e = {"value": n_total * len(e2e_t) / e2e_s, "unit": "series/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h),
+               "what": "Trainer(series) construction + train_epoch + validate + destroy per step, wall clock"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        lib = REF_LIB if REF_LIB.exists() else PORT_LIB
+        kind = "reference" if lib == REF_LIB else "port"
+        cb = time_cpu(lib, prof, TrainConfig(batch_size=min(B, 2048), seed=7), vals, cats, a.cpu_seconds)
+        cpu = {"value": cb["value"], "unit": "series/s", "cores": 1, "kind": kind, "sample": cb["sample"],
+               "host_cores": cb["host_cores"]}
+
+    if rank == 0:
+        out = {
+            "metric": metric, "value": value, "unit": "series/s", "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": total_ms / a.steps, "higher_is_better": True, "scaling": scaling,
+            "vs_baseline": None, "dtype": "f32" if a.precision == "fp32" else "f64",
+            "data": "synthetic (reference generator make_multiplicative_series, seed 41)", "config": cfg_desc,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+            "wall_ms_per_step": 1000.0 * statistics.mean(wall), "epoch_losses": losses,
+            "val_smape": v.mean_smape, "kernels": shares,
+            "speedup_vs_cpu": (value / cpu["value"]) if cpu else None,
+        }
+        print(json.dumps(out))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -197,6 +197,16 @@ esrnn_status esrnn_trainer_last_device_ms(const esrnn_trainer* t, double* ms);
 /* Number of kernels the engine launched since creation (graph nodes counted). */
 esrnn_status esrnn_trainer_kernel_launches(const esrnn_trainer* t, int64_t* n);
 
+/* Per-kernel device timing (measurement hook for bench.py's roofline).  When enabled,
+ * train_epoch / run_batch / forecast launch kernels directly (no CUDA graph) with a CUDA
+ * event pair around every launch on the engine stream; kernel_times returns, per kernel
+ * class, the summed milliseconds and launch counts since the last reset.
+ * Classes: 0 scan_fwd, 1 stack(train/loss), 2 es_bwd, 3 net_reduce, 4 adam, 5 finalize,
+ * 6 forecast_scan, 7 stack(forecast). */
+#define ESRNN_KERNEL_CLASSES 8
+esrnn_status esrnn_trainer_profile_kernels(esrnn_trainer* t, int32_t enable);
+esrnn_status esrnn_trainer_kernel_times(esrnn_trainer* t, double* total_ms, int64_t* launches);
+
 /* NCCL bootstrap for esrnn_dist (returns ESRNN_NCCL_ERROR in builds without NCCL). */
 esrnn_status esrnn_nccl_unique_id(uint8_t out[128]);
 

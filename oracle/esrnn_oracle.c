@@ -1082,6 +1082,20 @@ esrnn_status esrnn_trainer_kernel_launches(const esrnn_trainer* t, int64_t* n) {
     return ESRNN_OK;
 }
 
+esrnn_status esrnn_trainer_profile_kernels(esrnn_trainer* t, int32_t enable) {
+    (void)t; (void)enable;
+    return ESRNN_OK;
+}
+
+esrnn_status esrnn_trainer_kernel_times(esrnn_trainer* t, double* total_ms, int64_t* launches) {
+    (void)t;
+    for (int i = 0; i < ESRNN_KERNEL_CLASSES; ++i) {
+        if (total_ms) total_ms[i] = 0.0;
+        if (launches) launches[i] = 0;
+    }
+    return ESRNN_OK;
+}
+
 esrnn_status esrnn_nccl_unique_id(uint8_t out[128]) {
     (void)out;
     snprintf(g_create_err, sizeof g_create_err, "oracle: no NCCL");

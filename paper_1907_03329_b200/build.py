@@ -40,6 +40,18 @@ def _stale(out: Path, deps: list[Path]) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
+def _torch_nccl_dir() -> str | None:
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    if spec is None or not spec.submodule_search_locations:
+        return None
+    for base in spec.submodule_search_locations:
+        d = Path(base) / "nccl" / "lib"
+        if (d / "libnccl.so.2").exists():
+            return str(d)
+    return None
+
+
 def build_engine(force: bool = False) -> Path:
     BUILD.mkdir(exist_ok=True)
     deps = [*CSRC.glob("*.cu"), *CSRC.glob("*.cuh"), *CSRC.glob("*.cpp"), INC / "esrnn_b200.h"]
@@ -54,8 +66,12 @@ def build_engine(force: bool = False) -> Path:
         obj = BUILD / (src.stem + ".o")
         _run(["g++", "-std=c++17", "-O2", "-fPIC", "-ffp-contract=off", "-I" + str(INC), "-c", str(src), "-o", str(obj)])
         objs.append(str(obj))
-    _run([NVCC, *ARCH, "-shared", "-o", str(LIB), *objs, "-Xlinker", "-Bsymbolic",
-          "-L/usr/lib/x86_64-linux-gnu", "-lnccl"])
+    # Link the NCCL that torch bundles (2.28.x) so a process that also imports torch sees one
+    # libnccl.so.2; fall back to the system copy (2.27.3) when the wheel is absent.
+    nccl_dir = _torch_nccl_dir()
+    link = ["-L" + nccl_dir, "-l:libnccl.so.2", "-Xlinker", "-rpath," + nccl_dir] if nccl_dir else \
+        ["-L/usr/lib/x86_64-linux-gnu", "-lnccl"]
+    _run([NVCC, *ARCH, "-shared", "-o", str(LIB), *objs, "-Xlinker", "-Bsymbolic", *link])
     return LIB
 
 

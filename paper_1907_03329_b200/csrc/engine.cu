@@ -188,6 +188,42 @@ struct esrnn_trainer {
     int graph_steps = 0;
     int graph_launch_nodes = 0;
 
+    // per-kernel event timing (esrnn_trainer_profile_kernels)
+    bool profiling = false;
+    std::vector<cudaEvent_t> prof_ev;
+    std::vector<int> prof_cls;
+    double prof_ms[ESRNN_KERNEL_CLASSES] = {};
+    int64_t prof_n[ESRNN_KERNEL_CLASSES] = {};
+    struct KScope {
+        esrnn_trainer* e;
+        int cls;
+        KScope(esrnn_trainer* e_, int c) : e(e_), cls(c) {
+            if (e->profiling) e->prof_mark(cls);
+        }
+        ~KScope() {
+            if (e->profiling) e->prof_mark(-1);
+        }
+    };
+    void prof_mark(int cls) {
+        cudaEvent_t ev;
+        cudaEventCreate(&ev);
+        cudaEventRecord(ev, stream);
+        prof_ev.push_back(ev);
+        prof_cls.push_back(cls);
+    }
+    void prof_collect() {
+        cudaStreamSynchronize(stream);
+        for (size_t i = 0; i + 1 < prof_ev.size(); i += 2) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, prof_ev[i], prof_ev[i + 1]);
+            prof_ms[prof_cls[i]] += ms;
+            prof_n[prof_cls[i]] += 1;
+        }
+        for (auto ev : prof_ev) cudaEventDestroy(ev);
+        prof_ev.clear();
+        prof_cls.clear();
+    }
+
     ~esrnn_trainer() {
         if (graph) cudaGraphExecDestroy(graph);
         if (comm) ncclCommDestroy(comm);
@@ -551,29 +587,44 @@ void launch_step(Eng* e, const PlanDev& pv, int s, bool grads, bool update, Stat
     const NetLayout& lay = e->lay;
     const int kc = e->kcap;
     const int scan_blocks = (kc + kScanThreads - 1) / kScanThreads;
-    k_scan_fwd<Real><<<scan_blocks, kScanThreads, sizeof(Real) * lay.S * kScanThreads, e->stream>>>(st, pv, lay, s);
+    using KS = Eng::KScope;
+    {
+        KS k(e, 0);
+        k_scan_fwd<Real><<<scan_blocks, kScanThreads, sizeof(Real) * lay.S * kScanThreads, e->stream>>>(st, pv, lay, s);
+    }
     ForecastArgs fa{};
     const size_t sm = stack_smem<Real>(lay);
     const int nt = stack_threads(lay);
-    if (grads)
-        k_stack<Real, kRows, kTrain><<<e->tiles_cap, nt, sm, e->stream>>>(st, pv, lay, s, fa);
-    else
-        k_stack<Real, kRows, kLossOnly><<<e->tiles_cap, nt, sm, e->stream>>>(st, pv, lay, s, fa);
+    {
+        KS k(e, 1);
+        if (grads)
+            k_stack<Real, kRows, kTrain><<<e->tiles_cap, nt, sm, e->stream>>>(st, pv, lay, s, fa);
+        else
+            k_stack<Real, kRows, kLossOnly><<<e->tiles_cap, nt, sm, e->stream>>>(st, pv, lay, s, fa);
+    }
     e->launches += 2;
     if (!grads) return;
-    k_es_bwd<Real><<<e->es_blocks, kScanThreads, 0, e->stream>>>(st, pv, lay, s);
+    {
+        KS k(e, 2);
+        k_es_bwd<Real><<<e->es_blocks, kScanThreads, 0, e->stream>>>(st, pv, lay, s);
+    }
     const int rb = static_cast<int>((lay.P_live + 255) / 256);
     const bool sharded = e->world > 1;
-    k_net_reduce<Real, kRows><<<rb, 256, 0, e->stream>>>(st, pv, lay, s, e->es_blocks, sharded ? 0 : 1);
+    {
+        KS k(e, 3);
+        k_net_reduce<Real, kRows><<<rb, 256, 0, e->stream>>>(st, pv, lay, s, e->es_blocks, sharded ? 0 : 1);
+    }
     e->launches += 2;
     if (sharded) {
         NCCL_OK(ncclAllReduce(st.gbuf, st.gbuf, lay.P_live + 2, e->fp64 ? ncclDouble : ncclFloat, ncclSum, e->comm,
                               e->stream));
+        KS k(e, 5);
         k_finalize<Real><<<rb, 256, 0, e->stream>>>(st, pv, lay, s);
         e->launches += 1;
     }
     if (update) {
         const long long n = lay.P_live + kc;
+        KS k(e, 4);
         k_adam<Real><<<static_cast<int>((n + 255) / 256), 256, 0, e->stream>>>(st, pv, lay, s);
         e->launches += 1;
     }
@@ -675,7 +726,7 @@ double train_epoch_impl(Eng* e) {
     }
     const PlanDev pv = e->epoch_plan.view(false);
     StateDev<Real> st = e->state<Real>();
-    const bool use_graph = e->cfg.use_graphs >= 0;
+    const bool use_graph = e->cfg.use_graphs >= 0 && !e->profiling;
     CUDA_OK(cudaEventRecord(e->ev0, e->stream));
     if (use_graph) {
         if (!e->graph || e->graph_steps != steps) {
@@ -704,6 +755,7 @@ double train_epoch_impl(Eng* e) {
     }
     CUDA_OK(cudaEventRecord(e->ev1, e->stream));
     CUDA_OK(cudaGetLastError());
+    if (e->profiling) e->prof_collect();
     std::vector<double> lh(steps);
     CUDA_OK(cudaMemcpyAsync(lh.data(), e->loss_hist.p, sizeof(double) * steps, cudaMemcpyDeviceToHost, e->stream));
     CUDA_OK(cudaStreamSynchronize(e->stream));
@@ -771,6 +823,7 @@ void run_batch_impl(Eng* e, int32_t B, const int32_t* rows, const int32_t* ancho
     }
     CUDA_OK(cudaEventRecord(e->ev1, e->stream));
     CUDA_OK(cudaGetLastError());
+    if (e->profiling) e->prof_collect();
     CUDA_OK(cudaStreamSynchronize(e->stream));
     float ms = 0.f;
     CUDA_OK(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
@@ -837,9 +890,12 @@ void forecast_impl(Eng* e, int64_t drop_tail, double* out, double* smape, double
     CUDA_OK(cudaEventRecord(e->ev0, e->stream));
     if (N > 0) {
         const int sb = (N + kScanThreads - 1) / kScanThreads;
-        k_forecast_scan<Real><<<sb, kScanThreads, sizeof(Real) * (S + I) * kScanThreads, e->stream>>>(
-            st, lay, t_ins, reinterpret_cast<Real*>(e->fX.p), reinterpret_cast<Real*>(e->fL.p),
-            reinterpret_cast<Real*>(e->fS.p), nullptr, nullptr, -1);
+        {
+            Eng::KScope k(e, 6);
+            k_forecast_scan<Real><<<sb, kScanThreads, sizeof(Real) * (S + I) * kScanThreads, e->stream>>>(
+                st, lay, t_ins, reinterpret_cast<Real*>(e->fX.p), reinterpret_cast<Real*>(e->fL.p),
+                reinterpret_cast<Real*>(e->fS.p), nullptr, nullptr, -1);
+        }
         ForecastArgs fa{};
         fa.t_ins = t_ins;
         fa.validate = validate ? 1 : 0;
@@ -849,10 +905,14 @@ void forecast_impl(Eng* e, int64_t drop_tail, double* out, double* smape, double
         fa.out = e->f_out.p;
         fa.smape = e->f_smape.p;
         const int tiles = (N + kRows - 1) / kRows;
-        k_stack<Real, kRows, kForecast><<<tiles, stack_threads(lay), stack_smem<Real>(lay), e->stream>>>(
-            st, e->batch_plan.view(false), lay, 0, fa);
+        {
+            Eng::KScope k(e, 7);
+            k_stack<Real, kRows, kForecast><<<tiles, stack_threads(lay), stack_smem<Real>(lay), e->stream>>>(
+                st, e->batch_plan.view(false), lay, 0, fa);
+        }
         e->launches += 2;
     }
+    if (e->profiling) e->prof_collect();
     CUDA_OK(cudaEventRecord(e->ev1, e->stream));
     CUDA_OK(cudaGetLastError());
     CUDA_OK(cudaStreamSynchronize(e->stream));
@@ -1147,6 +1207,23 @@ esrnn_status esrnn_trainer_last_device_ms(const esrnn_trainer* t, double* ms) {
 
 esrnn_status esrnn_trainer_kernel_launches(const esrnn_trainer* t, int64_t* n) {
     *n = t->launches;
+    return ESRNN_OK;
+}
+
+esrnn_status esrnn_trainer_profile_kernels(esrnn_trainer* t, int32_t enable) {
+    t->profiling = enable != 0;
+    for (int i = 0; i < ESRNN_KERNEL_CLASSES; ++i) {
+        t->prof_ms[i] = 0.0;
+        t->prof_n[i] = 0;
+    }
+    return ESRNN_OK;
+}
+
+esrnn_status esrnn_trainer_kernel_times(esrnn_trainer* t, double* total_ms, int64_t* launches) {
+    for (int i = 0; i < ESRNN_KERNEL_CLASSES; ++i) {
+        if (total_ms) total_ms[i] = t->prof_ms[i];
+        if (launches) launches[i] = t->prof_n[i];
+    }
     return ESRNN_OK;
 }
 

@@ -497,6 +497,18 @@ class Trainer:
         self._chk(self.api.lib.esrnn_trainer_kernel_launches(self._h, C.byref(n)))
         return n.value
 
+    KERNEL_CLASSES = ("scan_fwd", "stack", "es_bwd", "net_reduce", "adam", "finalize", "forecast_scan",
+                      "forecast_stack")
+
+    def profile_kernels(self, enable: bool) -> None:
+        self._chk(self.api.lib.esrnn_trainer_profile_kernels(self._h, 1 if enable else 0))
+
+    def kernel_times(self) -> dict:
+        ms = np.zeros(8)
+        n = (C.c_int64 * 8)()
+        self._chk(self.api.lib.esrnn_trainer_kernel_times(self._h, N.dptr(ms), n))
+        return {k: (float(ms[i]), int(n[i])) for i, k in enumerate(self.KERNEL_CLASSES)}
+
     def benchmark_batched_vs_looped(self) -> BenchmarkReport:  # trainer.hpp:351-413
         windows = self.all_windows()
         O = self._profile.horizon
