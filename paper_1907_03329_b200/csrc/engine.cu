@@ -171,7 +171,7 @@ struct esrnn_trainer {
     DBuf<unsigned char> vals, ps, ps_m, ps_v, theta, mW, vW;
     DBuf<signed char> cat;
     DBuf<int> ps_steps;
-    DBuf<unsigned char> lv, se, lbar, sbar, cI, cO, cl, part, gbuf, psg, d_inputs, d_targets, d_seas, d_levels;
+    DBuf<unsigned char> lv, se, cI, cO, cl, part, gbuf, psg, d_inputs, d_targets, d_seas, d_levels;
     DBuf<unsigned char> fX, fL, fS, dump_lv, dump_se;
     DBuf<double> loss_part, es_sq_part, red_sq_part, scal, loss_hist, f_out, f_smape, smape_sum;
     DBuf<unsigned int> done_ctr;
@@ -249,8 +249,6 @@ struct esrnn_trainer {
         s.vW = reinterpret_cast<Real*>(vW.p);
         s.lv = reinterpret_cast<Real*>(lv.p);
         s.se = reinterpret_cast<Real*>(se.p);
-        s.lbar = reinterpret_cast<Real*>(lbar.p);
-        s.sbar = reinterpret_cast<Real*>(sbar.p);
         s.cI = reinterpret_cast<Real*>(cI.p);
         s.cO = reinterpret_cast<Real*>(cO.p);
         s.cl = reinterpret_cast<Real*>(cl.p);
@@ -364,7 +362,16 @@ void build_layout(Eng* e) {
     lay.S = e->S;
     lay.in0 = e->in0;
     lay.T = e->T;
+    lay.ldx = (e->in0 + 3) & ~3;
+    lay.ldh = (H + 3) & ~3;
     e->live_flat.clear();
+    // compact segments start on 4-element boundaries; padding slots map to -1
+    auto pad4 = [&]() {
+        while (coff % 4) {
+            e->live_flat.push_back(-1);
+            ++coff;
+        }
+    };
     int layer = 0;
     for (int b = 0; b < e->prof.n_blocks; ++b) {
         const int first = layer;
@@ -391,9 +398,11 @@ void build_layout(Eng* e) {
                     e->live_flat.push_back(e->off_win[layer] + static_cast<int64_t>(k) * 4 * H + col);
                 }
             coff += static_cast<int64_t>(in) * 3 * H;
+            pad4();
             lay.cb[layer] = coff;
             for (int q = 0; q < 3 * H; ++q) e->live_flat.push_back(e->off_bias[layer] + (q < H ? q : q + H));
             coff += 3 * H;
+            pad4();
         }
     }
     e->off_nlw = off;
@@ -408,16 +417,22 @@ void build_layout(Eng* e) {
     lay.c_nlw = coff;
     for (int64_t i = 0; i < static_cast<int64_t>(H) * H; ++i) e->live_flat.push_back(e->off_nlw + i);
     coff += static_cast<int64_t>(H) * H;
+    pad4();
     lay.c_nlb = coff;
     for (int i = 0; i < H; ++i) e->live_flat.push_back(e->off_nlb + i);
     coff += H;
+    pad4();
     lay.c_outw = coff;
     for (int64_t i = 0; i < static_cast<int64_t>(H) * O; ++i) e->live_flat.push_back(e->off_outw + i);
     coff += static_cast<int64_t>(H) * O;
+    pad4();
     lay.c_outb = coff;
     for (int i = 0; i < O; ++i) e->live_flat.push_back(e->off_outb + i);
     coff += O;
-    lay.P_live = coff;
+    pad4();
+    lay.P_pad = coff;
+    lay.P_live = 0;
+    for (int64_t f : e->live_flat) lay.P_live += f >= 0 ? 1 : 0;
 }
 
 // ------------------------------------------------------------------ conversions
@@ -452,15 +467,17 @@ void download_real(Eng* e, const void* dev, size_t n, double* dst) {
 }
 
 void upload_theta(Eng* e) {
-    std::vector<double> c(e->live_flat.size());
-    for (size_t i = 0; i < c.size(); ++i) c[i] = e->w_host[e->live_flat[i]];
+    std::vector<double> c(e->live_flat.size(), 0.0);
+    for (size_t i = 0; i < c.size(); ++i)
+        if (e->live_flat[i] >= 0) c[i] = e->w_host[e->live_flat[i]];
     upload_real(e, e->theta.p, c.data(), c.size());
 }
 
 void sync_weights_from_device(Eng* e) {
     std::vector<double> c(e->live_flat.size());
     download_real(e, e->theta.p, c.size(), c.data());
-    for (size_t i = 0; i < c.size(); ++i) e->w_host[e->live_flat[i]] = c[i];
+    for (size_t i = 0; i < c.size(); ++i)
+        if (e->live_flat[i] >= 0) e->w_host[e->live_flat[i]] = c[i];
 }
 
 // ------------------------------------------------------------------ capacity
@@ -476,15 +493,15 @@ void ensure_capacity(Eng* e, int B) {
     e->kcap = std::min(e->N > 0 ? e->N : 1, B);
     const int kc = e->kcap;
     e->tiles_cap = (B + kRows - 1) / kRows;
-    e->es_blocks = (kc + kScanThreads - 1) / kScanThreads;
+    e->es_blocks = (kc + kFinishThreads - 1) / kFinishThreads;
     e->lv.alloc(r * T * kc);
     e->se.alloc(r * (T + S) * kc);
-    e->lbar.alloc(r * T * kc);
-    e->sbar.alloc(r * (T + S) * kc);
     e->cI.alloc(r * static_cast<size_t>(B) * I);
     e->cO.alloc(r * static_cast<size_t>(B) * O);
     e->cl.alloc(r * B);
-    e->part.alloc(r * static_cast<size_t>(e->tiles_cap) * e->lay.P_live);
+    // padding slots of the tile partials are never written: zero them once
+    e->part.alloc(r * static_cast<size_t>(e->tiles_cap) * e->lay.P_pad);
+    e->part.zero(e->stream);
     e->loss_part.alloc(e->tiles_cap);
     e->psg.alloc(r * static_cast<size_t>(kc) * (2 + S));
     e->es_sq_part.alloc(e->es_blocks);
@@ -564,8 +581,17 @@ void upload_plan(Eng* e, const HostPlan& hp, DevPlan& dp, size_t cap_w, size_t c
 
 // ------------------------------------------------------------------ step launch
 template <typename Real>
-size_t stack_smem(const NetLayout& lay) {
-    return sizeof(Real) * TileSmem::make(lay, kRows).total;
+size_t stack_smem(const NetLayout& lay, bool resident) {
+    return sizeof(Real) * TileSmem::make(lay, kRows, resident).total;
+}
+
+// Resident mode keeps every live weight in shared memory for the whole tile (one TMA
+// bulk copy); larger fp64 networks stage one layer at a time.
+int g_smem_optin = 227 * 1024;  // cudaDevAttrMaxSharedMemoryPerBlockOptin, set at create
+
+template <typename Real>
+bool stack_resident(const NetLayout& lay) {
+    return stack_smem<Real>(lay, true) + 4096 <= static_cast<size_t>(g_smem_optin);
 }
 
 int stack_threads(const NetLayout& lay) {
@@ -574,11 +600,39 @@ int stack_threads(const NetLayout& lay) {
 }
 
 template <typename Real>
+size_t finish_smem(const NetLayout& lay) {
+    return sizeof(Real) * static_cast<size_t>(2 * lay.T + lay.S) * kFinishThreads;
+}
+
+template <typename Real, int MODE>
+void set_stack_attr(const NetLayout& lay) {
+    if (stack_resident<Real>(lay))
+        CUDA_OK(cudaFuncSetAttribute(k_stack<Real, kRows, MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)stack_smem<Real>(lay, true)));
+    CUDA_OK(cudaFuncSetAttribute(k_stack<Real, kRows, MODE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)stack_smem<Real>(lay, false)));
+}
+
+template <typename Real>
 void setup_kernel_attrs(Eng* e) {
-    const size_t sm = stack_smem<Real>(e->lay);
-    CUDA_OK(cudaFuncSetAttribute(k_stack<Real, kRows, kTrain>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    CUDA_OK(cudaFuncSetAttribute(k_stack<Real, kRows, kLossOnly>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    CUDA_OK(cudaFuncSetAttribute(k_stack<Real, kRows, kForecast>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    set_stack_attr<Real, kTrain>(e->lay);
+    set_stack_attr<Real, kLossOnly>(e->lay);
+    set_stack_attr<Real, kForecast>(e->lay);
+    CUDA_OK(cudaFuncSetAttribute(k_grad_finish<Real, kRows>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)finish_smem<Real>(e->lay)));
+    if (stack_smem<Real>(e->lay, false) > static_cast<size_t>(g_smem_optin) ||
+        finish_smem<Real>(e->lay) > static_cast<size_t>(g_smem_optin))
+        raise(ESRNN_CONFIG_ERROR, "profile too large for the B200 kernels' shared-memory tiles");
+}
+
+template <typename Real, int MODE>
+void launch_stack(Eng* e, int grid, const StateDev<Real>& st, const PlanDev& pv, int s, const ForecastArgs& fa) {
+    const NetLayout& lay = e->lay;
+    const int nt = stack_threads(lay);
+    if (stack_resident<Real>(lay))
+        k_stack<Real, kRows, MODE, true><<<grid, nt, stack_smem<Real>(lay, true), e->stream>>>(st, pv, lay, s, fa);
+    else
+        k_stack<Real, kRows, MODE, false><<<grid, nt, stack_smem<Real>(lay, false), e->stream>>>(st, pv, lay, s, fa);
 }
 
 // Launch one training step (K1..K5) for step `s` of plan `pv` on the engine stream.
@@ -586,44 +640,39 @@ template <typename Real>
 void launch_step(Eng* e, const PlanDev& pv, int s, bool grads, bool update, StateDev<Real> st) {
     const NetLayout& lay = e->lay;
     const int kc = e->kcap;
-    const int scan_blocks = (kc + kScanThreads - 1) / kScanThreads;
+    const int scan_blocks = (kc + kScanThreads - 1) / kScanThreads;  // 64-thread blocks: more SMs busy
     using KS = Eng::KScope;
     {
         KS k(e, 0);
         k_scan_fwd<Real><<<scan_blocks, kScanThreads, sizeof(Real) * lay.S * kScanThreads, e->stream>>>(st, pv, lay, s);
     }
     ForecastArgs fa{};
-    const size_t sm = stack_smem<Real>(lay);
-    const int nt = stack_threads(lay);
     {
         KS k(e, 1);
         if (grads)
-            k_stack<Real, kRows, kTrain><<<e->tiles_cap, nt, sm, e->stream>>>(st, pv, lay, s, fa);
+            launch_stack<Real, kTrain>(e, e->tiles_cap, st, pv, s, fa);
         else
-            k_stack<Real, kRows, kLossOnly><<<e->tiles_cap, nt, sm, e->stream>>>(st, pv, lay, s, fa);
+            launch_stack<Real, kLossOnly>(e, e->tiles_cap, st, pv, s, fa);
     }
     e->launches += 2;
     if (!grads) return;
-    {
-        KS k(e, 2);
-        k_es_bwd<Real><<<e->es_blocks, kScanThreads, 0, e->stream>>>(st, pv, lay, s);
-    }
-    const int rb = static_cast<int>((lay.P_live + 255) / 256);
     const bool sharded = e->world > 1;
     {
-        KS k(e, 3);
-        k_net_reduce<Real, kRows><<<rb, 256, 0, e->stream>>>(st, pv, lay, s, e->es_blocks, sharded ? 0 : 1);
+        KS k(e, 2);
+        k_grad_finish<Real, kRows><<<e->es_blocks + e->red_blocks, kFinishThreads, finish_smem<Real>(lay), e->stream>>>(
+            st, pv, lay, s, e->es_blocks, sharded ? 0 : 1);
     }
-    e->launches += 2;
+    e->launches += 1;
     if (sharded) {
-        NCCL_OK(ncclAllReduce(st.gbuf, st.gbuf, lay.P_live + 2, e->fp64 ? ncclDouble : ncclFloat, ncclSum, e->comm,
+        NCCL_OK(ncclAllReduce(st.gbuf, st.gbuf, lay.P_pad + 2, e->fp64 ? ncclDouble : ncclFloat, ncclSum, e->comm,
                               e->stream));
         KS k(e, 5);
+        const int rb = static_cast<int>((lay.P_pad + 255) / 256);
         k_finalize<Real><<<rb, 256, 0, e->stream>>>(st, pv, lay, s);
         e->launches += 1;
     }
     if (update) {
-        const long long n = lay.P_live + kc;
+        const long long n = lay.P_pad + kc;
         KS k(e, 4);
         k_adam<Real><<<static_cast<int>((n + 255) / 256), 256, 0, e->stream>>>(st, pv, lay, s);
         e->launches += 1;
@@ -640,12 +689,12 @@ void alloc_state(Eng* e) {
     e->ps_v.alloc(r * static_cast<size_t>(2 + S) * std::max(N, 1));
     e->ps_steps.alloc(std::max(N, 1));
     e->cat.alloc(std::max(N, 1));
-    e->theta.alloc(r * e->lay.P_live);
-    e->mW.alloc(r * e->lay.P_live);
-    e->vW.alloc(r * e->lay.P_live);
-    e->gbuf.alloc(r * (e->lay.P_live + 2));
-    e->red_blocks = static_cast<int>((e->lay.P_live + 255) / 256);
-    e->red_sq_part.alloc(e->red_blocks);
+    e->theta.alloc(r * e->lay.P_pad);
+    e->mW.alloc(r * e->lay.P_pad);
+    e->vW.alloc(r * e->lay.P_pad);
+    e->gbuf.alloc(r * (e->lay.P_pad + 2));
+    e->red_blocks = static_cast<int>((e->lay.P_pad + 32 * kRedChunks - 1) / (32 * kRedChunks));
+    e->red_sq_part.alloc(std::max<int>(e->red_blocks, static_cast<int>((e->lay.P_pad + 255) / 256)));
     e->scal.alloc(4);
     e->loss_hist.alloc(1);
     e->done_ctr.alloc(2);
@@ -833,7 +882,7 @@ void run_batch_impl(Eng* e, int32_t B, const int32_t* rows, const int32_t* ancho
     double lsum = 0.0;
     if (grads && e->world > 1) {
         Real g2[2];
-        CUDA_OK(cudaMemcpy(g2, reinterpret_cast<Real*>(e->gbuf.p) + e->lay.P_live, sizeof g2, cudaMemcpyDeviceToHost));
+        CUDA_OK(cudaMemcpy(g2, reinterpret_cast<Real*>(e->gbuf.p) + e->lay.P_pad, sizeof g2, cudaMemcpyDeviceToHost));
         lsum = static_cast<double>(g2[1]);
     } else {
         const int nt = (Bl + kRows - 1) / kRows;
@@ -861,10 +910,11 @@ void run_batch_impl(Eng* e, int32_t B, const int32_t* rows, const int32_t* ancho
         for (int i = 0; i < k; ++i) slot_rows[i] = bp.slot_row[i] + e->row0;
     if (grads) {
         if (net_grads) {
-            std::vector<double> c(e->lay.P_live);
+            std::vector<double> c(e->lay.P_pad);
             download_real(e, e->gbuf.p, c.size(), c.data());
             std::fill(net_grads, net_grads + e->P, 0.0);
-            for (size_t i = 0; i < c.size(); ++i) net_grads[e->live_flat[i]] = c[i];
+            for (size_t i = 0; i < c.size(); ++i)
+                if (e->live_flat[i] >= 0) net_grads[e->live_flat[i]] = c[i];
         }
         if (ps_grads && e->cfg.attach_es_state && k > 0) download_real(e, e->psg.p, static_cast<size_t>(k) * (2 + S), ps_grads);
     }
@@ -907,8 +957,7 @@ void forecast_impl(Eng* e, int64_t drop_tail, double* out, double* smape, double
         const int tiles = (N + kRows - 1) / kRows;
         {
             Eng::KScope k(e, 7);
-            k_stack<Real, kRows, kForecast><<<tiles, stack_threads(lay), stack_smem<Real>(lay), e->stream>>>(
-                st, e->batch_plan.view(false), lay, 0, fa);
+            launch_stack<Real, kForecast>(e, tiles, st, e->batch_plan.view(false), 0, fa);
         }
         e->launches += 2;
     }
@@ -1019,6 +1068,7 @@ esrnn_status esrnn_trainer_create(const esrnn_profile* profile, const esrnn_trai
             raise(ESRNN_CUDA_ERROR, "no CUDA device visible: the B200 engine has no CPU fallback");
         if (cfg->device < 0 || cfg->device >= ndev) raise(ESRNN_CUDA_ERROR, "device %d out of range", cfg->device);
         CUDA_OK(cudaSetDevice(cfg->device));
+        CUDA_OK(cudaDeviceGetAttribute(&g_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, cfg->device));
         CUDA_OK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
         CUDA_OK(cudaEventCreate(&e->ev0));
         CUDA_OK(cudaEventCreate(&e->ev1));
