@@ -1,0 +1,225 @@
+// Shared device-side types and helpers of the ES-RNN B200 kernels.
+//
+// Layout in HBM: series values time-major y[t][N] (coalesced across series), per-series
+// parameters and Adam moments SoA [(2+S)][N], scan state [t][slot], and the shared
+// network parameters in a compact "live" vector that drops the structurally-dead
+// forget-gate columns and recurrent matrices (their gradients are exactly zero at
+// sequence length 1).  Every weight matrix is stored transposed, [out][in]
+// with an odd row stride, so both the forward product (threads over outputs) and the
+// input adjoint (threads over inputs) read shared memory without bank conflicts, and
+// the whole vector moves into shared memory with one TMA bulk copy.
+#pragma once
+#include <cstdint>
+
+#include "devmath.cuh"
+
+namespace esrnn_dev {
+
+constexpr int kMaxLayers = 16;
+
+struct NetLayout {
+    int L, nb, H, O, I, S, in0, T;
+    int ldx, ldh, ldg, ldo;      // padded (multiple of 4) row strides: x, hidden, 3H gates, horizon
+    int ldkh;                    // odd row stride of the transposed head matrices (>= H)
+    int layer_in[kMaxLayers];
+    int ldk[kMaxLayers];         // odd row stride of layer l's transposed input matrix (>= in_l)
+    int res_src[kMaxLayers];     // >=0: layer output added as residual after this layer
+    int block_first[kMaxLayers]; // 1 if layer is the first of a block b>0 (adjoint joins the residual)
+    int block_last[kMaxLayers];  // 1 if layer is the last of a block b>0 (residual added here)
+    long long cw[kMaxLayers], cb[kMaxLayers];  // WT_l [3H][ldk_l], bias_l [3H]
+    long long c_nlw, c_nlb, c_outw, c_outb;     // nl_w^T [H][ldkh], nl_b [H], out_w^T [O][ldkh], out_b [O]
+    long long P_live, P_pad;
+};
+
+// Per-epoch (or single-batch) plan: windows in global batch order, filtered to the
+// rows this rank owns, with per-step slot lists and per-slot window CSR.
+struct PlanDev {
+    const int* w_row;         // local row of each window
+    const int* w_anchor;
+    const int* w_slot;        // slot within its step
+    const int* step_win_off;  // [steps+1]
+    const int* step_slot_off; // [steps+1]
+    const int* slot_row;      // local row of each slot
+    const int* slot_win_off;  // [total_slots+1] into slot_win
+    const int* slot_win;      // window index relative to its step's first window
+    const int* w_csr;         // step-local CSR position of each window (slot-major order)
+    const int* csr_anchor;    // anchor of each CSR entry
+    const double* step_M;     // global mask count per step
+    const unsigned char* mask;// [window][O] or nullptr (all ones)
+};
+
+template <typename Real>
+struct StateDev {
+    const Real* vals;       // [LEN][N] time-major, local rows (series-parallel readers)
+    const Real* vrm;        // [N][ldv] row-major copy (slot-parallel readers: random rows)
+    int ldv;
+    const signed char* cat; // [N]
+    int N, LEN, kcap;
+    Real* ps;               // [(2+S)][N]: alpha_raw, gamma_raw, seas_raw[S]
+    Real* ps_m;
+    Real* ps_v;
+    int* ps_steps;
+    Real* theta;            // [P_pad]
+    Real* mW;
+    Real* vW;
+    // scratch
+    Real* lv;               // [T][kcap]
+    Real* se;               // [T+S][kcap]
+    Real* contrib;          // [Bcap][cwp] ES adjoint contributions per window, in slot-major
+                            // CSR order: [0,O) target seasonalities, [O,O+I) input
+                            // seasonalities, [O+I] anchor level
+    int cwp;                // row stride of contrib (multiple of 4 >= I+O+1)
+    Real* part;             // [tiles][P_pad]
+    double* loss_part;      // [tiles]
+    Real* gbuf;             // [P_pad + 2]  (comm buffer: grads | ps sq-norm | loss sum)
+    Real* psg;              // [kcap][2+S]
+    double* es_sq_part;     // [es blocks]
+    double* red_sq_part;    // [reduce blocks]
+    unsigned int* done_ctr; // [2]
+    double* scal;           // [4] scale, bc1, bc2, loss
+    long long* net_step;
+    double* loss_hist;      // [steps]
+    int* err;               // [2] code, min t
+    // optional dumps (run_batch): WindowBatch matrices, step-local window order
+    Real* d_inputs;
+    Real* d_targets;
+    Real* d_seas;
+    Real* d_levels;
+    double tau, lr_net, lr_ps, clip;
+    int has_clip, attach;
+    long long* dbg_clk;     // optional phase timestamps (ESRNN_DEBUG_CLOCKS), block 0 thread 0
+};
+
+enum ErrCode { kErrNone = 0, kErrTrainLevel = 1, kErrObs = 2, kErrFcLevel = 3, kErrSeas = 4 };
+
+__device__ __forceinline__ void flag_error(int* err, int code, int t) {
+    atomicMin(err + 1, t);
+    atomicCAS(err, 0, code);
+}
+
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T* red) {
+    // fixed-order block reduction (warp shuffles then warp 0), deterministic
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    T r = 0;
+    if (threadIdx.x == 0)
+        for (int w = 0; w < nw; ++w) r += red[w];
+    __syncthreads();
+    return r;  // valid in thread 0
+}
+
+#define DBG_CLK(st, i)                                                              \
+    do {                                                                            \
+        if ((st).dbg_clk && blockIdx.x == 0 && threadIdx.x == 0 && _dbg < 64) (st).dbg_clk[_dbg] = clock64(); \
+        ++_dbg;                                                                     \
+    } while (0)
+
+// ------------------------------------------------------------------ TMA bulk copy
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+    unsigned ok = 0;
+    do {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(ok)
+            : "r"(smem_addr(bar)), "r"(phase)
+            : "memory");
+    } while (!ok);
+}
+
+// 4-wide shared-memory vector (16 B for fp32, 2 x 16 B for fp64); p must be 4-aligned
+template <typename Real>
+struct V4 {
+    Real x, y, z, w;
+};
+template <typename Real>
+__device__ __forceinline__ V4<Real> lds4(const Real* p) {
+    if constexpr (sizeof(Real) == 4) {
+        const float4 v = *reinterpret_cast<const float4*>(p);
+        return {v.x, v.y, v.z, v.w};
+    } else {
+        const double2 a = *reinterpret_cast<const double2*>(p);
+        const double2 b = *reinterpret_cast<const double2*>(p + 2);
+        return {a.x, a.y, b.x, b.y};
+    }
+}
+
+template <typename Real>
+__device__ __forceinline__ V4<Real> ldg4(const Real* p) {
+    if constexpr (sizeof(Real) == 4) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+        return {v.x, v.y, v.z, v.w};
+    } else {
+        const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+        const double2 b = __ldg(reinterpret_cast<const double2*>(p + 2));
+        return {a.x, a.y, b.x, b.y};
+    }
+}
+
+// Asynchronous global->shared element copies (LDGSTS): every load of a scattered
+// column is in flight at once without staging through registers.
+template <typename Real>
+__device__ __forceinline__ void cp_async_elem(Real* smem, const Real* gmem) {
+    if constexpr (sizeof(Real) == 4)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(smem)), "l"(gmem) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(smem)), "l"(gmem) : "memory");
+}
+
+// Row stride (elements) for per-thread rows staged with 16-byte copies: a multiple of
+// 16 bytes, and an odd number of 16-byte units so a warp's same-column reads spread over
+// 8 bank groups.
+template <typename Real>
+__host__ __device__ __forceinline__ int row_pad(int n) {
+    constexpr int e = 16 / static_cast<int>(sizeof(Real));
+    int p = (n + e - 1) / e * e;
+    if (((p / e) & 1) == 0) p += e;
+    return p;
+}
+
+// Stage this thread's contiguous row src[0:n) (16-byte aligned) into dst[0:n) with
+// 16-byte cp.async copies; caller waits with cp_async_wait_all().
+template <typename Real>
+__device__ __forceinline__ void stage_row_async(Real* dst, const Real* __restrict__ src, int n) {
+    constexpr int e = 16 / static_cast<int>(sizeof(Real));
+#pragma unroll 4
+    for (int t = 0; t < n; t += e) cp_async16(dst + t, src + t);
+}
+
+__host__ __device__ __forceinline__ int log2_ceil(int w) {
+    int l = 0;
+    while ((1 << l) < w) ++l;
+    return l;
+}
+
+// fp32 performance mode divides with the SFU reciprocal path; fp64 keeps IEEE division
+template <typename Real>
+__device__ __forceinline__ Real fdiv(Real a, Real b) {
+    if constexpr (sizeof(Real) == 4) return __fdividef(a, b);
+    else return a / b;
+}
+
+}  // namespace esrnn_dev

@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <random>
@@ -22,7 +23,9 @@
 #include <vector>
 
 #include "esrnn_b200.h"
-#include "kernels.cuh"
+#include "finish.cuh"
+#include "scan.cuh"
+#include "stack.cuh"
 
 using namespace esrnn_dev;
 
@@ -105,13 +108,14 @@ struct PinnedBuf {
 
 // One plan = ordered local windows + per-step slot lists + per-slot window CSR.
 struct HostPlan {
-    std::vector<int> w_row, w_anchor, w_slot, step_win_off, step_slot_off, slot_row, slot_win_off, slot_win;
+    std::vector<int> w_row, w_anchor, w_slot, step_win_off, step_slot_off, slot_row, slot_win_off, slot_win, w_csr,
+        csr_anchor;
     std::vector<double> step_M;
     int max_step_windows = 0, max_step_slots = 0;
 };
 
 struct DevPlan {
-    DBuf<int> w_row, w_anchor, w_slot, step_win_off, step_slot_off, slot_row, slot_win_off, slot_win;
+    DBuf<int> w_row, w_anchor, w_slot, step_win_off, step_slot_off, slot_row, slot_win_off, slot_win, w_csr, csr_anchor;
     DBuf<double> step_M;
     DBuf<unsigned char> mask;
     size_t cap_w = 0, cap_steps = 0, cap_slots = 0;
@@ -125,6 +129,8 @@ struct DevPlan {
         p.slot_row = slot_row.p;
         p.slot_win_off = slot_win_off.p;
         p.slot_win = slot_win.p;
+        p.w_csr = w_csr.p;
+        p.csr_anchor = csr_anchor.p;
         p.step_M = step_M.p;
         p.mask = with_mask ? mask.p : nullptr;
         return p;
@@ -132,12 +138,6 @@ struct DevPlan {
 };
 
 constexpr int kRows = 8;          // windows per K2 tile
-constexpr int kScanThreads = 64;  // K1 / K4 / K6 block
-
-// ------------------------------------------------------------------ engine
-struct EngineBase {
-    virtual ~EngineBase() = default;
-};
 
 }  // namespace
 
@@ -168,14 +168,16 @@ struct esrnn_trainer {
     ncclComm_t comm = nullptr;
 
     // device state (type-erased: Real = float or double, chosen by cfg.precision)
-    DBuf<unsigned char> vals, ps, ps_m, ps_v, theta, mW, vW;
+    DBuf<unsigned char> vals, vrm, ps, ps_m, ps_v, theta, mW, vW;
+    int ldv = 0;  // row stride of the row-major value copy (16-byte multiple)
     DBuf<signed char> cat;
     DBuf<int> ps_steps;
-    DBuf<unsigned char> lv, se, cI, cO, cl, part, gbuf, psg, d_inputs, d_targets, d_seas, d_levels;
+    DBuf<unsigned char> lv, se, contrib, part, gbuf, psg, d_inputs, d_targets, d_seas, d_levels;
     DBuf<unsigned char> fX, fL, fS, dump_lv, dump_se;
     DBuf<double> loss_part, es_sq_part, red_sq_part, scal, loss_hist, f_out, f_smape, smape_sum;
     DBuf<unsigned int> done_ctr;
     DBuf<long long> net_step;
+    DBuf<long long> dbg_clk;  // ESRNN_DEBUG_CLOCKS: per-phase clock64 stamps of tile 0
     DBuf<int> errw;
     int Bcap = 0, kcap = 0, tiles_cap = 0, es_blocks = 0, red_blocks = 0, steps_cap = 0;
 
@@ -236,6 +238,8 @@ struct esrnn_trainer {
     StateDev<Real> state() {
         StateDev<Real> s{};
         s.vals = reinterpret_cast<const Real*>(vals.p);
+        s.vrm = reinterpret_cast<const Real*>(vrm.p);
+        s.ldv = ldv;
         s.cat = cat.p;
         s.N = N;
         s.LEN = LEN;
@@ -249,9 +253,8 @@ struct esrnn_trainer {
         s.vW = reinterpret_cast<Real*>(vW.p);
         s.lv = reinterpret_cast<Real*>(lv.p);
         s.se = reinterpret_cast<Real*>(se.p);
-        s.cI = reinterpret_cast<Real*>(cI.p);
-        s.cO = reinterpret_cast<Real*>(cO.p);
-        s.cl = reinterpret_cast<Real*>(cl.p);
+        s.contrib = reinterpret_cast<Real*>(contrib.p);
+        s.cwp = (I + O + 1 + 3) & ~3;
         s.part = reinterpret_cast<Real*>(part.p);
         s.loss_part = loss_part.p;
         s.gbuf = reinterpret_cast<Real*>(gbuf.p);
@@ -273,6 +276,7 @@ struct esrnn_trainer {
         s.clip = cfg.gradient_clip;
         s.has_clip = cfg.has_gradient_clip ? 1 : 0;
         s.attach = cfg.attach_es_state ? 1 : 0;
+        s.dbg_clk = dbg_clk.p;
         return s;
     }
 };
@@ -326,7 +330,7 @@ void validate_config(const esrnn_profile& p, const esrnn_train_config& c) {
         raise(ESRNN_CONFIG_ERROR, "train: learning rates must be non-negative");
     if (c.has_gradient_clip && c.gradient_clip <= 0.0) raise(ESRNN_CONFIG_ERROR, "train: gradient_clip must be positive");
     // device-kernel limits (shared-memory tiles are sized from these)
-    if (p.hidden_size > 128) raise(ESRNN_CONFIG_ERROR, "profile: hidden_size > 128 unsupported by the B200 kernels");
+    if (p.hidden_size > 80) raise(ESRNN_CONFIG_ERROR, "profile: hidden_size > 80 unsupported by the B200 kernels");
     if (p.seasonality_length > 64) raise(ESRNN_CONFIG_ERROR, "profile: seasonality > 64 unsupported by the B200 kernels");
     if (p.input_window + ESRNN_NUM_CATEGORIES > 256 || p.horizon > 128)
         raise(ESRNN_CONFIG_ERROR, "profile: window sizes unsupported by the B200 kernels");
@@ -390,21 +394,26 @@ void build_layout(Eng* e) {
             off += static_cast<int64_t>(H) * 4 * H;
             e->off_bias[layer] = off;
             off += 4 * H;
-            // compact live layout: w_input columns [i | g | o] (forget gate dead), bias
-            lay.cw[layer] = coff;
-            for (int k = 0; k < in; ++k)
-                for (int q = 0; q < 3 * H; ++q) {
-                    const int col = q < H ? q : q + H;
-                    e->live_flat.push_back(e->off_win[layer] + static_cast<int64_t>(k) * 4 * H + col);
-                }
-            coff += static_cast<int64_t>(in) * 3 * H;
+            // compact live layout: W^T over the live gate columns [i | g | o] (forget gate
+            // dead) with an odd row stride ldk >= in (pad columns -> -1), then the bias
             pad4();
+            const int ldk = in | 1;
+            lay.ldk[layer] = ldk;
+            lay.cw[layer] = coff;
+            for (int q = 0; q < 3 * H; ++q) {
+                const int col = q < H ? q : q + H;
+                for (int k = 0; k < ldk; ++k)
+                    e->live_flat.push_back(k < in ? e->off_win[layer] + static_cast<int64_t>(k) * 4 * H + col : -1);
+            }
+            coff += static_cast<int64_t>(3 * H) * ldk;
             lay.cb[layer] = coff;
             for (int q = 0; q < 3 * H; ++q) e->live_flat.push_back(e->off_bias[layer] + (q < H ? q : q + H));
             coff += 3 * H;
-            pad4();
         }
     }
+    lay.ldg = (3 * H + 3) & ~3;
+    lay.ldo = (O + 3) & ~3;
+    lay.ldkh = H | 1;
     e->off_nlw = off;
     off += static_cast<int64_t>(H) * H;
     e->off_nlb = off;
@@ -414,18 +423,20 @@ void build_layout(Eng* e) {
     e->off_outb = off;
     off += O;
     e->P = off;
-    lay.c_nlw = coff;
-    for (int64_t i = 0; i < static_cast<int64_t>(H) * H; ++i) e->live_flat.push_back(e->off_nlw + i);
-    coff += static_cast<int64_t>(H) * H;
+    // head: nl_w^T [H][ldkh], nl_b [H], out_w^T [O][ldkh], out_b [O] (one contiguous segment)
     pad4();
+    const int ldkh = lay.ldkh;
+    lay.c_nlw = coff;
+    for (int j = 0; j < H; ++j)
+        for (int k = 0; k < ldkh; ++k) e->live_flat.push_back(k < H ? e->off_nlw + static_cast<int64_t>(k) * H + j : -1);
+    coff += static_cast<int64_t>(H) * ldkh;
     lay.c_nlb = coff;
     for (int i = 0; i < H; ++i) e->live_flat.push_back(e->off_nlb + i);
     coff += H;
-    pad4();
     lay.c_outw = coff;
-    for (int64_t i = 0; i < static_cast<int64_t>(H) * O; ++i) e->live_flat.push_back(e->off_outw + i);
-    coff += static_cast<int64_t>(H) * O;
-    pad4();
+    for (int o = 0; o < O; ++o)
+        for (int k = 0; k < ldkh; ++k) e->live_flat.push_back(k < H ? e->off_outw + static_cast<int64_t>(k) * O + o : -1);
+    coff += static_cast<int64_t>(O) * ldkh;
     lay.c_outb = coff;
     for (int i = 0; i < O; ++i) e->live_flat.push_back(e->off_outb + i);
     coff += O;
@@ -493,12 +504,10 @@ void ensure_capacity(Eng* e, int B) {
     e->kcap = std::min(e->N > 0 ? e->N : 1, B);
     const int kc = e->kcap;
     e->tiles_cap = (B + kRows - 1) / kRows;
-    e->es_blocks = (kc + kFinishThreads - 1) / kFinishThreads;
+    e->es_blocks = (kc + kEsSlotsPerBlock - 1) / kEsSlotsPerBlock;
     e->lv.alloc(r * T * kc);
     e->se.alloc(r * (T + S) * kc);
-    e->cI.alloc(r * static_cast<size_t>(B) * I);
-    e->cO.alloc(r * static_cast<size_t>(B) * O);
-    e->cl.alloc(r * B);
+    e->contrib.alloc(r * static_cast<size_t>(B) * ((I + O + 1 + 3) & ~3));
     // padding slots of the tile partials are never written: zero them once
     e->part.alloc(r * static_cast<size_t>(e->tiles_cap) * e->lay.P_pad);
     e->part.zero(e->stream);
@@ -539,6 +548,15 @@ void append_step(Eng* e, HostPlan& hp, const int* rows, const int* anchors, int 
     hp.slot_win.resize(cbase + nw);
     std::vector<int> fill(cnt.begin(), cnt.end() - 1);
     for (int i = 0; i < nw; ++i) hp.slot_win[cbase + fill[hp.w_slot[wbase + i]]++] = i;
+    // slot-major CSR position of each window (K2 writes its ES contributions there) and the
+    // anchor of each CSR entry (K3 reads a slot's windows contiguously)
+    hp.w_csr.resize(wbase + nw);
+    hp.csr_anchor.resize(cbase + nw);
+    for (int c = 0; c < nw; ++c) {
+        const int i = hp.slot_win[cbase + c];
+        hp.w_csr[wbase + i] = c;
+        hp.csr_anchor[cbase + c] = hp.w_anchor[wbase + i];
+    }
     for (int k = 0; k < ns; ++k) hp.slot_win_off.push_back(cbase + cnt[k + 1]);
     hp.step_win_off.push_back(static_cast<int>(hp.w_row.size()));
     hp.step_slot_off.push_back(static_cast<int>(hp.slot_row.size()));
@@ -550,6 +568,8 @@ void plan_begin(HostPlan& hp) {
     hp.w_row.clear();
     hp.w_anchor.clear();
     hp.w_slot.clear();
+    hp.w_csr.clear();
+    hp.csr_anchor.clear();
     hp.slot_row.clear();
     hp.slot_win.clear();
     hp.slot_win_off.assign(1, 0);
@@ -571,6 +591,8 @@ void upload_plan(Eng* e, const HostPlan& hp, DevPlan& dp, size_t cap_w, size_t c
     upload_vec(e, dp.w_row, hp.w_row, cw);
     upload_vec(e, dp.w_anchor, hp.w_anchor, cw);
     upload_vec(e, dp.w_slot, hp.w_slot, cw);
+    upload_vec(e, dp.w_csr, hp.w_csr, cw);
+    upload_vec(e, dp.csr_anchor, hp.csr_anchor, cw);
     upload_vec(e, dp.slot_row, hp.slot_row, cw);
     upload_vec(e, dp.slot_win, hp.slot_win, cw);
     upload_vec(e, dp.slot_win_off, hp.slot_win_off, cw + 1);
@@ -594,14 +616,17 @@ bool stack_resident(const NetLayout& lay) {
     return stack_smem<Real>(lay, true) + 4096 <= static_cast<size_t>(g_smem_optin);
 }
 
-int stack_threads(const NetLayout& lay) {
-    int nt = ((3 * lay.H + 31) / 32) * 32;
-    return std::min(std::max(nt, 64), 256);
-}
+int stack_threads(const NetLayout& lay) { return stack_threads_for(lay); }
 
 template <typename Real>
 size_t finish_smem(const NetLayout& lay) {
-    return sizeof(Real) * static_cast<size_t>(2 * lay.T + lay.S) * kFinishThreads;
+    // lb, sb, forward l and s columns [.][bd] + one staged observation row per slot
+    return sizeof(Real) * (static_cast<size_t>(4 * lay.T + lay.S) + row_pad<Real>(lay.T)) * kEsSlotsPerBlock;
+}
+
+template <typename Real>
+size_t scan_smem(const NetLayout& lay) {
+    return sizeof(Real) * (static_cast<size_t>(lay.S) + row_pad<Real>(lay.T)) * kScanThreads;
 }
 
 template <typename Real, int MODE>
@@ -613,16 +638,61 @@ void set_stack_attr(const NetLayout& lay) {
                                  (int)stack_smem<Real>(lay, false)));
 }
 
+// The scans are specialised for the M4 seasonalities (S = 1, 4, 12: seasonal ring in
+// registers); any other S runs the generic shared-memory-ring variant.
+template <typename Real, int SC>
+void set_scan_attrs(const NetLayout& lay) {
+    CUDA_OK(cudaFuncSetAttribute(k_scan_fwd<Real, SC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)scan_smem<Real>(lay)));
+    CUDA_OK(cudaFuncSetAttribute(k_grad_finish<Real, kRows, SC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)finish_smem<Real>(lay)));
+}
+
 template <typename Real>
 void setup_kernel_attrs(Eng* e) {
     set_stack_attr<Real, kTrain>(e->lay);
     set_stack_attr<Real, kLossOnly>(e->lay);
     set_stack_attr<Real, kForecast>(e->lay);
-    CUDA_OK(cudaFuncSetAttribute(k_grad_finish<Real, kRows>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)finish_smem<Real>(e->lay)));
+    switch (e->S) {
+        case 1: set_scan_attrs<Real, 1>(e->lay); break;
+        case 4: set_scan_attrs<Real, 4>(e->lay); break;
+        case 12: set_scan_attrs<Real, 12>(e->lay); break;
+        default: set_scan_attrs<Real, 0>(e->lay); break;
+    }
+    const size_t fsm = sizeof(Real) * static_cast<size_t>(e->LEN + e->S + e->I) * kScanThreads;
+    CUDA_OK(cudaFuncSetAttribute(k_forecast_scan<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
     if (stack_smem<Real>(e->lay, false) > static_cast<size_t>(g_smem_optin) ||
-        finish_smem<Real>(e->lay) > static_cast<size_t>(g_smem_optin))
+        finish_smem<Real>(e->lay) > static_cast<size_t>(g_smem_optin) || fsm > static_cast<size_t>(g_smem_optin))
         raise(ESRNN_CONFIG_ERROR, "profile too large for the B200 kernels' shared-memory tiles");
+}
+
+template <typename Real, int SC>
+void launch_scan_sc(Eng* e, int blocks, const StateDev<Real>& st, const PlanDev& pv, int s) {
+    k_scan_fwd<Real, SC><<<blocks, kScanThreads, scan_smem<Real>(e->lay), e->stream>>>(st, pv, e->lay, s);
+}
+template <typename Real>
+void launch_scan(Eng* e, int blocks, const StateDev<Real>& st, const PlanDev& pv, int s) {
+    switch (e->S) {
+        case 1: launch_scan_sc<Real, 1>(e, blocks, st, pv, s); break;
+        case 4: launch_scan_sc<Real, 4>(e, blocks, st, pv, s); break;
+        case 12: launch_scan_sc<Real, 12>(e, blocks, st, pv, s); break;
+        default: launch_scan_sc<Real, 0>(e, blocks, st, pv, s); break;
+    }
+}
+
+template <typename Real, int SC>
+void launch_finish_sc(Eng* e, const StateDev<Real>& st, const PlanDev& pv, int s, int finalize) {
+    k_grad_finish<Real, kRows, SC><<<e->es_blocks + e->red_blocks, kFinishThreads, finish_smem<Real>(e->lay),
+                                     e->stream>>>(st, pv, e->lay, s, e->es_blocks, finalize);
+}
+template <typename Real>
+void launch_finish(Eng* e, const StateDev<Real>& st, const PlanDev& pv, int s, int finalize) {
+    switch (e->S) {
+        case 1: launch_finish_sc<Real, 1>(e, st, pv, s, finalize); break;
+        case 4: launch_finish_sc<Real, 4>(e, st, pv, s, finalize); break;
+        case 12: launch_finish_sc<Real, 12>(e, st, pv, s, finalize); break;
+        default: launch_finish_sc<Real, 0>(e, st, pv, s, finalize); break;
+    }
 }
 
 template <typename Real, int MODE>
@@ -644,13 +714,18 @@ void launch_step(Eng* e, const PlanDev& pv, int s, bool grads, bool update, Stat
     using KS = Eng::KScope;
     {
         KS k(e, 0);
-        k_scan_fwd<Real><<<scan_blocks, kScanThreads, sizeof(Real) * lay.S * kScanThreads, e->stream>>>(st, pv, lay, s);
+        launch_scan<Real>(e, scan_blocks, st, pv, s);
     }
     ForecastArgs fa{};
     {
         KS k(e, 1);
         if (grads)
+        {
+            // ESRNN_DEBUG_TWICE: re-run the (idempotent) tile kernel so the stamps show a
+            // warm instruction cache
+            if (e->dbg_clk.p && std::getenv("ESRNN_DEBUG_TWICE")) launch_stack<Real, kTrain>(e, e->tiles_cap, st, pv, s, fa);
             launch_stack<Real, kTrain>(e, e->tiles_cap, st, pv, s, fa);
+        }
         else
             launch_stack<Real, kLossOnly>(e, e->tiles_cap, st, pv, s, fa);
     }
@@ -659,8 +734,7 @@ void launch_step(Eng* e, const PlanDev& pv, int s, bool grads, bool update, Stat
     const bool sharded = e->world > 1;
     {
         KS k(e, 2);
-        k_grad_finish<Real, kRows><<<e->es_blocks + e->red_blocks, kFinishThreads, finish_smem<Real>(lay), e->stream>>>(
-            st, pv, lay, s, e->es_blocks, sharded ? 0 : 1);
+        launch_finish<Real>(e, st, pv, s, sharded ? 0 : 1);
     }
     e->launches += 1;
     if (sharded) {
@@ -684,6 +758,8 @@ void alloc_state(Eng* e) {
     const int N = e->N, S = e->S, LEN = e->LEN;
     const size_t r = sizeof(Real);
     e->vals.alloc(r * static_cast<size_t>(LEN) * std::max(N, 1));
+    e->ldv = (LEN + 3) & ~3;
+    e->vrm.alloc(r * static_cast<size_t>(e->ldv) * std::max(N, 1));
     e->ps.alloc(r * static_cast<size_t>(2 + S) * std::max(N, 1));
     e->ps_m.alloc(r * static_cast<size_t>(2 + S) * std::max(N, 1));
     e->ps_v.alloc(r * static_cast<size_t>(2 + S) * std::max(N, 1));
@@ -700,6 +776,10 @@ void alloc_state(Eng* e) {
     e->done_ctr.alloc(2);
     e->net_step.alloc(1);
     e->errw.alloc(2);
+    if (std::getenv("ESRNN_DEBUG_CLOCKS")) {
+        e->dbg_clk.alloc(64);
+        e->dbg_clk.zero(e->stream);
+    }
     for (auto* b : {&e->ps, &e->ps_m, &e->ps_v, &e->mW, &e->vW}) b->zero(e->stream);
     e->ps_steps.zero(e->stream);
     e->done_ctr.zero(e->stream);
@@ -717,6 +797,11 @@ void upload_values(Eng* e, const double* values, const int32_t* category) {
         for (int t = 0; t < LEN; ++t)
             tm[static_cast<size_t>(t) * N + r] = static_cast<Real>(values[static_cast<size_t>(e->row0 + r) * LEN + t]);
     CUDA_OK(cudaMemcpyAsync(e->vals.p, tm.data(), sizeof(Real) * tm.size(), cudaMemcpyHostToDevice, e->stream));
+    std::vector<Real> rm(static_cast<size_t>(e->ldv) * std::max(N, 1), Real(0));
+    for (int r = 0; r < N; ++r)
+        for (int t = 0; t < LEN; ++t)
+            rm[static_cast<size_t>(r) * e->ldv + t] = static_cast<Real>(values[static_cast<size_t>(e->row0 + r) * LEN + t]);
+    CUDA_OK(cudaMemcpyAsync(e->vrm.p, rm.data(), sizeof(Real) * rm.size(), cudaMemcpyHostToDevice, e->stream));
     std::vector<signed char> c(std::max(N, 1), 5);
     e->cat_host.assign(N, 5);
     for (int r = 0; r < N; ++r) {
@@ -812,6 +897,17 @@ double train_epoch_impl(Eng* e) {
     CUDA_OK(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
     e->last_ms = ms;
     throw_device_error(e);
+    if (e->dbg_clk.p) {
+        long long c[64];
+        CUDA_OK(cudaMemcpy(c, e->dbg_clk.p, sizeof c, cudaMemcpyDeviceToHost));
+        std::fprintf(stderr, "[esrnn dbg] k_stack tile0 phase cycles:");
+        for (int i = 1; i < 32 && c[i] > 0; ++i) std::fprintf(stderr, " %lld", c[i] - c[i - 1]);
+        std::fprintf(stderr, "\n[esrnn dbg] grad_finish ES block0:");
+        for (int i = 33; i < 48 && c[i] > 0; ++i) std::fprintf(stderr, " %lld", c[i] - c[i - 1]);
+        std::fprintf(stderr, "\n[esrnn dbg] grad_finish reduce block0:");
+        for (int i = 49; i < 64 && c[i] > 0; ++i) std::fprintf(stderr, " %lld", c[i] - c[i - 1]);
+        std::fprintf(stderr, "\n[esrnn dbg] reduce block0 start - ES block0 start: %lld\n", c[48] - c[32]);
+    }
     // trainer.hpp:236-242: acc += loss * count, in batch order
     double acc = 0.0, weight = 0.0;
     for (int s = 0; s < steps; ++s) {
@@ -942,7 +1038,7 @@ void forecast_impl(Eng* e, int64_t drop_tail, double* out, double* smape, double
         const int sb = (N + kScanThreads - 1) / kScanThreads;
         {
             Eng::KScope k(e, 6);
-            k_forecast_scan<Real><<<sb, kScanThreads, sizeof(Real) * (S + I) * kScanThreads, e->stream>>>(
+            k_forecast_scan<Real><<<sb, kScanThreads, sizeof(Real) * (t_ins + S + I) * kScanThreads, e->stream>>>(
                 st, lay, t_ins, reinterpret_cast<Real*>(e->fX.p), reinterpret_cast<Real*>(e->fL.p),
                 reinterpret_cast<Real*>(e->fS.p), nullptr, nullptr, -1);
         }
@@ -1004,7 +1100,7 @@ void hw_state_impl(Eng* e, int64_t row, int64_t t_len, double* levels, double* s
     StateDev<Real> st = e->state<Real>();
     const int sb = (e->N + kScanThreads - 1) / kScanThreads;
     // the dump row's thread writes its full state; X == nullptr skips the window build
-    k_forecast_scan<Real><<<sb, kScanThreads, sizeof(Real) * (S + e->I) * kScanThreads, e->stream>>>(
+    k_forecast_scan<Real><<<sb, kScanThreads, sizeof(Real) * (t_len + S + e->I) * kScanThreads, e->stream>>>(
         st, e->lay, static_cast<int>(t_len), nullptr, nullptr, nullptr, reinterpret_cast<Real*>(e->dump_lv.p),
         reinterpret_cast<Real*>(e->dump_se.p), lr);
     e->launches += 1;

@@ -1,0 +1,352 @@
+// K3 k_grad_finish: per-slot ES backward + fixed-order reduction of the tile partials,
+//                   last CTA finalises the step scalars (single GPU).
+// K3' k_finalize:   post-all-reduce finalisation (sharded mode).
+// K4 k_adam:        Adam over the compact shared vector and the step's per-series slots.
+//
+// Reference: Gather adjoint (autodiff.hpp:603-610), the HW recursion adjoint through the
+// tape (holt_winters.hpp:266-277, Logistic :483, Exp :501), apply_updates
+// (trainer.hpp:602-655).
+#pragma once
+#include "common.cuh"
+
+namespace esrnn_dev {
+
+constexpr int kFinishThreads = 256;
+constexpr int kEsSlotsPerBlock = 64;  // ES blocks use warps 0-1 (64 slots), shared columns (2T+S)*64
+constexpr int kRedGroups = 8;         // tile groups per reduce block
+constexpr int kRedChunks = 2;         // 32-parameter chunks per reduce block
+
+// clip scale (trainer.hpp:603-615), global Adam step and bias corrections (:617-620),
+// step loss (masked mean, autodiff.hpp:392)
+template <typename Real>
+__device__ void finalize_scalars(StateDev<Real>& st, const PlanDev& pl, int s, double sq, double loss_sum) {
+    double scale = 1.0;
+    if (st.has_clip) {
+        const double norm = sqrt(sq);
+        if (norm > st.clip) scale = st.clip / norm;
+    }
+    st.scal[0] = scale;
+    st.scal[3] = loss_sum / pl.step_M[s];
+    st.loss_hist[s] = loss_sum / pl.step_M[s];
+    if (st.err[0] == 0) {
+        const long long step = ++(*st.net_step);
+        st.scal[1] = 1.0 - pow(0.9, static_cast<double>(step));
+        st.scal[2] = 1.0 - pow(0.999, static_cast<double>(step));
+    }
+}
+
+template <typename Real, int R, int SC>
+__global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> st, PlanDev pl, NetLayout lay, int s,
+                                                                int es_blocks, int finalize) {
+    using M = Math<Real>;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    __shared__ double red[32];
+    __shared__ Real gsum[kRedGroups][32];
+    __shared__ bool last;
+    const int tid = threadIdx.x;
+    double sq = 0.0;
+    // ESRNN_DEBUG_CLOCKS: ES block 0 stamps at [32, 40), reduce block 0 at [48, 56)
+    const int dbg_base = blockIdx.x == 0 ? 32 : (static_cast<int>(blockIdx.x) == es_blocks ? 48 : -1);
+    int fdbg = 0;
+    auto FCLK = [&]() {
+        if (st.dbg_clk && dbg_base >= 0 && tid == 0) st.dbg_clk[dbg_base + fdbg] = clock64();
+        ++fdbg;
+    };
+    FCLK();
+    if (static_cast<int>(blockIdx.x) < es_blocks) {
+        // ---------------- per-slot window-adjoint gather + reverse HW scan ---------------
+        const int k0 = pl.step_slot_off[s];
+        const int k = pl.step_slot_off[s + 1] - k0;
+        const int slot = blockIdx.x * kEsSlotsPerBlock + tid;
+        if (tid < kEsSlotsPerBlock && slot < k && st.attach) {
+            const int N = st.N, S = SC > 0 ? SC : lay.S, T = lay.T, I = lay.I, O = lay.O, kc = st.kcap;
+            const int bd = kEsSlotsPerBlock, tp = row_pad<Real>(T);
+            Real* lb = reinterpret_cast<Real*>(smem_raw) + tid;  // [T][bd]    level adjoint (window part)
+            Real* sb = lb + T * bd;                               // [T+S][bd]  seasonality adjoint
+            Real* lvs = sb + (T + S) * bd;                        // [T][bd]    forward levels
+            Real* ses = lvs + T * bd;                             // [T][bd]    forward seasonalities
+            Real* ys = reinterpret_cast<Real*>(smem_raw) + (4 * T + S) * bd + tid * tp;  // row
+            const int row = pl.slot_row[k0 + slot];
+            FCLK();
+            for (int t = 0; t < T; ++t) lb[t * bd] = 0;
+            for (int t = 0; t < T + S; ++t) sb[t * bd] = 0;
+            FCLK();
+            // this slot's windows are contiguous in the CSR-ordered contribution table:
+            // whole rows arrive as 16-byte loads, 16 values in flight at a time
+            const int cb0 = pl.slot_win_off[k0];
+            const int wb = pl.slot_win_off[k0 + slot], we = pl.slot_win_off[k0 + slot + 1];
+            const int cwp = st.cwp, nv = O + I + 1;
+            for (int w = wb; w < we; ++w) {
+                const int a = __ldg(pl.csr_anchor + w);
+                const Real* __restrict__ cr = st.contrib + (size_t)(w - cb0) * cwp;
+                for (int j0 = 0; j0 < nv; j0 += 16) {
+                    Real v[16];
+#pragma unroll
+                    for (int u = 0; u < 16; u += 4) {
+                        if (j0 + u < cwp) {
+                            const V4<Real> x = ldg4(cr + j0 + u);
+                            v[u] = x.x; v[u + 1] = x.y; v[u + 2] = x.z; v[u + 3] = x.w;
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 16; ++u) {
+                        const int j = j0 + u;
+                        if (j < O) sb[(a + 1 + j) * bd] += v[u];
+                        else if (j < O + I) sb[(a - I + 1 + (j - O)) * bd] += v[u];
+                        else if (j == O + I) lb[a * bd] += v[u];
+                    }
+                }
+            }
+            // the forward state this reverse scan needs, all in flight at once
+            stage_row_async(ys, st.vrm + (size_t)row * st.ldv, T);
+#pragma unroll 4
+            for (int t = 0; t < T; ++t) {
+                cp_async_elem(lvs + t * bd, st.lv + (size_t)t * kc + slot);
+                cp_async_elem(ses + t * bd, st.se + (size_t)t * kc + slot);
+            }
+            const Real alpha = M::logistic_ps(st.ps[row]);
+            const Real gamma = M::logistic_ps(st.ps[N + row]);
+            const Real oma = Real(1) - alpha, omg = Real(1) - gamma;
+            FCLK();
+            cp_async_wait_all();
+            FCLK();
+            Real l0 = 0;
+            for (int j = 0; j < S; ++j) l0 += ys[j];
+            l0 = l0 / Real(S);
+            Real abar = 0, gbar = 0, omab = 0, omgb = 0;
+            Real lbn = lb[(T - 1) * bd];  // running adjoint of l[t]
+            // one reverse step: Sb = final adjoint of s[t+S], returns the final adjoint of s[t]
+            auto step = [&](int t, Real Sb) -> Real {
+                const Real yt = ys[t];
+                const Real lp = t > 0 ? lvs[(t - 1) * bd] : l0;
+                const Real s_t = ses[t * bd];
+                Real sbt = sb[t * bd];
+                // s_{t+S} = gamma*(y/lp) + (1-gamma)*s_t
+                omgb += Sb * s_t;
+                sbt += Sb * omg;
+                const Real d2 = fdiv(yt, lp);
+                gbar += Sb * d2;
+                const Real d2b = Sb * gamma;
+                Real lpb = t > 0 ? lb[(t - 1) * bd] : Real(0);
+                if (t > 0) lpb -= fdiv(d2b * d2, lp);
+                // l_t = alpha*(y/s_t) + (1-alpha)*lp
+                const Real Lb = lbn;
+                omab += Lb * lp;
+                if (t > 0) lpb += Lb * oma;
+                const Real d1 = fdiv(yt, s_t);
+                abar += Lb * d1;
+                sbt -= fdiv((Lb * alpha) * d1, s_t);
+                lbn = lpb;
+                return sbt;
+            };
+            Real sfin[SC > 0 ? SC : 1];
+            if constexpr (SC > 0) {
+                // register ring: rg[j] holds the final adjoint of the latest s index = j (mod S)
+                Real rg[SC];
+#pragma unroll
+                for (int j = 0; j < SC; ++j) rg[j] = 0;  // s[T..T+S) receive no adjoint
+                for (int base = ((T + SC - 1) / SC - 1) * SC; base >= 0; base -= SC) {
+#pragma unroll
+                    for (int jj = SC - 1; jj >= 0; --jj) {
+                        const int t = base + jj;
+                        if (t < T) rg[jj] = step(t, rg[jj]);
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < SC; ++j) sfin[j] = rg[j];
+            } else {
+#pragma unroll 4
+                for (int t = T - 1; t >= 0; --t) sb[t * bd] = step(t, sb[(t + S) * bd]);
+            }
+            FCLK();
+            abar -= omab;
+            gbar -= omgb;
+            Real* o = st.psg + (size_t)slot * (2 + S);
+            const Real ga = abar * alpha * (Real(1) - alpha);
+            const Real gg = gbar * gamma * (Real(1) - gamma);
+            o[0] = ga;
+            o[1] = gg;
+            sq += static_cast<double>(ga) * ga + static_cast<double>(gg) * gg;
+            for (int j = 0; j < S; ++j) {
+                const Real sj = M::exp_ps(st.ps[(2 + j) * N + row]);
+                Real sbj;
+                if constexpr (SC > 0) {
+                    sbj = 0;
+#pragma unroll
+                    for (int jj = 0; jj < SC; ++jj)
+                        if (jj == j) sbj = sfin[jj];
+                } else {
+                    sbj = sb[j * bd];
+                }
+                const Real g = sbj * sj;
+                o[2 + j] = g;
+                sq += static_cast<double>(g) * g;
+            }
+        }
+        const double tot = block_sum(sq, red);
+        if (tid == 0) st.es_sq_part[blockIdx.x] = tot;
+    } else {
+        // ------- tile-partial reduction: kRedChunks x 32 params, kRedGroups tile groups ---
+        const int rb = blockIdx.x - es_blocks;
+        const int w0 = pl.step_win_off[s];
+        const int nt = (pl.step_win_off[s + 1] - w0 + R - 1) / R;
+        const int lane = tid & 31, grp = tid >> 5;
+        const size_t P = lay.P_pad;
+        FCLK();
+        for (int ch = 0; ch < kRedChunks; ++ch) {
+            FCLK();
+            const long long q = ((long long)rb * kRedChunks + ch) * 32 + lane;
+            Real g = 0;
+            if (q < lay.P_pad) {
+                const Real* __restrict__ p = st.part + q;
+                Real a[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) a[u] = 0;
+                int t = grp;
+                for (; t + 7 * kRedGroups < nt; t += 8 * kRedGroups) {
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) a[u] += p[(size_t)(t + u * kRedGroups) * P];
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int tt = t + u * kRedGroups;
+                    if (tt < nt) a[u] += p[(size_t)tt * P];
+                }
+                g = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+            }
+            gsum[grp][lane] = g;
+            __syncthreads();
+            if (grp == 0) {
+                Real tot = gsum[0][lane];
+#pragma unroll
+                for (int gi = 1; gi < kRedGroups; ++gi) tot += gsum[gi][lane];
+                if (q < lay.P_pad) {
+                    st.gbuf[q] = tot;
+                    sq += static_cast<double>(tot) * tot;
+                }
+            }
+            __syncthreads();
+        }
+        const double tot = block_sum(sq, red);
+        if (tid == 0) st.red_sq_part[rb] = tot;
+    }
+    FCLK();
+    // ---------------- last CTA finalises ------------------------------------------------
+    if (tid == 0) {
+        __threadfence();
+        const unsigned ticket = atomicAdd(st.done_ctr, 1u);
+        last = (ticket == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!last || tid != 0) return;
+    __threadfence();
+    const int nrb = gridDim.x - es_blocks;
+    const int w0 = pl.step_win_off[s];
+    const int nt = (pl.step_win_off[s + 1] - w0 + R - 1) / R;
+    double es = 0.0;
+    if (st.attach)
+        for (int b = 0; b < es_blocks; ++b) es += *reinterpret_cast<volatile double*>(st.es_sq_part + b);
+    double ls = 0.0;
+    for (int t = 0; t < nt; ++t) ls += st.loss_part[t];
+    st.gbuf[lay.P_pad] = static_cast<Real>(es);
+    st.gbuf[lay.P_pad + 1] = static_cast<Real>(ls);
+    if (finalize) {
+        double all = 0.0;
+        for (int b = 0; b < nrb; ++b) all += *reinterpret_cast<volatile double*>(st.red_sq_part + b);
+        finalize_scalars(st, pl, s, all + es, ls);
+    }
+    *st.done_ctr = 0;
+}
+
+// After the NCCL all-reduce of gbuf (sharded mode): global squared norm + scalars.
+template <typename Real>
+__global__ void __launch_bounds__(256) k_finalize(StateDev<Real> st, PlanDev pl, NetLayout lay, int s) {
+    __shared__ double red[32];
+    __shared__ bool last;
+    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    double sq = 0.0;
+    if (q < lay.P_pad) {
+        const double g = st.gbuf[q];
+        sq = g * g;
+    }
+    const double tot = block_sum(sq, red);
+    if (threadIdx.x == 0) {
+        st.red_sq_part[blockIdx.x] = tot;
+        __threadfence();
+        last = atomicAdd(st.done_ctr + 1, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last || threadIdx.x != 0) return;
+    __threadfence();
+    double all = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) all += *reinterpret_cast<volatile double*>(st.red_sq_part + b);
+    const double es = st.attach ? static_cast<double>(st.gbuf[lay.P_pad]) : 0.0;
+    finalize_scalars(st, pl, s, all + es, static_cast<double>(st.gbuf[lay.P_pad + 1]));
+    st.done_ctr[1] = 0;
+}
+
+// ------------------------------------------------------------------------------ K4
+__device__ __forceinline__ void adam_update(double& theta, double& m, double& v, double g, double lr, double c1,
+                                            double c2) {
+    // trainer.hpp:626-630 / :642-647
+    m = 0.9 * m + (1.0 - 0.9) * g;
+    v = 0.999 * v + (1.0 - 0.999) * g * g;
+    theta -= lr * (m / c1) / (sqrt(v / c2) + 1e-8);
+}
+
+template <typename Real>
+__global__ void __launch_bounds__(256) k_adam(StateDev<Real> st, PlanDev pl, NetLayout lay, int s) {
+    if (st.err[0] != 0) return;  // the reference throws before apply_updates
+    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < lay.P_pad) {
+        const Real g0 = st.gbuf[q], m0 = st.mW[q], v0 = st.vW[q], t0 = st.theta[q];
+        const double scale = st.scal[0], bc1 = st.scal[1], bc2 = st.scal[2];
+        double th = t0, m = m0, v = v0;
+        adam_update(th, m, v, static_cast<double>(g0) * scale, st.lr_net, bc1, bc2);
+        st.mW[q] = static_cast<Real>(m);
+        st.vW[q] = static_cast<Real>(v);
+        st.theta[q] = static_cast<Real>(th);
+        return;
+    }
+    if (!st.attach) return;
+    const int k0 = pl.step_slot_off[s];
+    const int k = pl.step_slot_off[s + 1] - k0;
+    const long long slot = q - lay.P_pad;
+    if (slot >= k) return;
+    const int N = st.N, S = lay.S;
+    const int row = pl.slot_row[k0 + slot];
+    const int steps = st.ps_steps[row] + 1;
+    st.ps_steps[row] = steps;
+    const double scale = st.scal[0];
+    const double sc1 = 1.0 - pow(0.9, static_cast<double>(steps));
+    const double sc2 = 1.0 - pow(0.999, static_cast<double>(steps));
+    const Real* g = st.psg + (size_t)slot * (2 + S);
+    for (int j0 = 0; j0 < 2 + S; j0 += 4) {
+        Real pv[4], mv[4], vv[4], gv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int j = j0 + u;
+            if (j < 2 + S) {
+                const size_t e = (size_t)j * N + row;
+                pv[u] = st.ps[e];
+                mv[u] = st.ps_m[e];
+                vv[u] = st.ps_v[e];
+                gv[u] = g[j];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int j = j0 + u;
+            if (j < 2 + S) {
+                const size_t e = (size_t)j * N + row;
+                double th = pv[u], m = mv[u], v = vv[u];
+                adam_update(th, m, v, static_cast<double>(gv[u]) * scale, st.lr_ps, sc1, sc2);
+                st.ps_m[e] = static_cast<Real>(m);
+                st.ps_v[e] = static_cast<Real>(v);
+                st.ps[e] = static_cast<Real>(th);
+            }
+        }
+    }
+}
+
+}  // namespace esrnn_dev

@@ -1,0 +1,184 @@
+// Holt-Winters scans (the per-series sequential part of the step).
+//
+//   K1 k_scan_fwd       training scan for the slots of one step (holt_winters.hpp:236-283)
+//   K6 k_forecast_scan  forecast scan over values[0:t_ins) + window build (holt_winters.hpp:66-97,
+//                       deseasonalize_normalize :153-166, HWState::seasonal_at :55-59)
+//
+// One thread per series.  The whole observation column is first staged into shared
+// memory with every load in flight at once, the last S seasonalities live in a
+// shared-memory ring, so the recurrence waits only on its own FMA chain
+// (l_t = a*y/s_t + (1-a)*l_{t-1}; the division feeding s_{t+S} has S steps of slack).
+#pragma once
+#include "common.cuh"
+
+namespace esrnn_dev {
+
+constexpr int kScanThreads = 64;
+
+// Stage y[0:n) of this thread's series (stride N in global) into ys[t*bd] (shared).
+// All n element copies are issued back to back as cp.async (LDGSTS) and waited once.
+template <typename Real>
+__device__ __forceinline__ void stage_column(Real* ys, const Real* __restrict__ y, int n, int N, int bd) {
+#pragma unroll 8
+    for (int t = 0; t < n; ++t) cp_async_elem(ys + t * bd, y + (size_t)t * N);
+    cp_async_wait_all();
+}
+
+// ------------------------------------------------------------------------------ K1
+// smem: ring [S][bd] | ys rows [bd][row_pad(T)]  (row-major observations, 16-byte copies)
+// SC > 0: the seasonal ring is a register array (S == SC known at compile time); SC == 0:
+// generic S, ring in shared memory.
+template <typename Real, int SC>
+__global__ void __launch_bounds__(kScanThreads) k_scan_fwd(StateDev<Real> st, PlanDev pl, NetLayout lay, int s) {
+    using M = Math<Real>;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int k0 = pl.step_slot_off[s];
+    const int k = pl.step_slot_off[s + 1] - k0;
+    const int slot = blockIdx.x * blockDim.x + threadIdx.x;
+    if (slot >= k) return;
+    const int bd = blockDim.x, tid = threadIdx.x;
+    const int N = st.N, S = SC > 0 ? SC : lay.S, T = lay.T, kc = st.kcap;
+    const int tp = row_pad<Real>(T);
+    Real* ring = reinterpret_cast<Real*>(smem_raw) + tid;
+    Real* ys = reinterpret_cast<Real*>(smem_raw) + S * bd + tid * tp;
+    const int row = pl.slot_row[k0 + slot];
+    // the observation row and the per-series parameters, all in flight at once
+    stage_row_async(ys, st.vrm + (size_t)row * st.ldv, T);
+    for (int j = 0; j < S; ++j) cp_async_elem(ring + j * bd, st.ps + (size_t)(2 + j) * N + row);
+    const Real alpha = M::logistic_ps(st.ps[row]);
+    const Real gamma = M::logistic_ps(st.ps[N + row]);
+    const Real oma = Real(1) - alpha, omg = Real(1) - gamma;
+    cp_async_wait_all();
+    Real* __restrict__ se = st.se + slot;
+    Real* __restrict__ lv = st.lv + slot;
+    Real lp = 0;
+    int bad = -1;
+    if constexpr (SC > 0) {
+        Real rg[SC];
+#pragma unroll
+        for (int j = 0; j < SC; ++j) {
+            rg[j] = M::exp_ps(ring[j * bd]);
+            se[j * kc] = rg[j];
+            lp += ys[j];
+        }
+        lp = lp / Real(SC);
+        for (int t0 = 0; t0 < T; t0 += SC) {
+#pragma unroll
+            for (int j = 0; j < SC; ++j) {
+                const int t = t0 + j;
+                if (t < T) {
+                    const Real yt = ys[t];
+                    const Real l = alpha * fdiv(yt, rg[j]) + oma * lp;
+                    if (!(l > Real(0)) || !isfinite(l)) bad = bad < 0 ? t : bad;
+                    rg[j] = gamma * fdiv(yt, lp) + omg * rg[j];
+                    se[(t + SC) * kc] = rg[j];
+                    lv[t * kc] = l;
+                    lp = l;
+                }
+            }
+        }
+    } else {
+        for (int j = 0; j < S; ++j) {
+            const Real s0 = M::exp_ps(ring[j * bd]);
+            ring[j * bd] = s0;
+            se[j * kc] = s0;
+            lp += ys[j];
+        }
+        lp = lp / Real(S);
+        int j = 0;
+#pragma unroll 4
+        for (int t = 0; t < T; ++t) {
+            const Real yt = ys[t];
+            const Real s_t = ring[j * bd];
+            const Real l = alpha * fdiv(yt, s_t) + oma * lp;
+            if (!(l > Real(0)) || !isfinite(l)) bad = bad < 0 ? t : bad;
+            const Real sn = gamma * fdiv(yt, lp) + omg * s_t;
+            ring[j * bd] = sn;
+            se[(t + S) * kc] = sn;
+            lv[t * kc] = l;
+            lp = l;
+            j = (j + 1 == S) ? 0 : j + 1;
+        }
+    }
+    if (bad >= 0) flag_error(st.err, kErrTrainLevel, bad);
+}
+
+// ------------------------------------------------------------------------------ K6
+// smem: ys [t_ins][bd] | ring [S][bd] | win [I][bd]
+template <typename Real>
+__global__ void __launch_bounds__(kScanThreads) k_forecast_scan(StateDev<Real> st, NetLayout lay, int t_ins, Real* X,
+                                                                Real* FL, Real* FS, Real* dump_lv, Real* dump_se,
+                                                                int dump_row) {
+    using M = Math<Real>;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int S = lay.S, I = lay.I, O = lay.O, in0 = lay.in0, N = st.N;
+    const int row = blockIdx.x * blockDim.x + threadIdx.x;
+    if (row >= N) return;
+    const int bd = blockDim.x, tid = threadIdx.x;
+    Real* ys = reinterpret_cast<Real*>(smem_raw) + tid;
+    Real* ring = reinterpret_cast<Real*>(smem_raw) + t_ins * bd + tid;
+    Real* win = ring + S * bd;
+    for (int j = 0; j < S; ++j) cp_async_elem(ring + j * bd, st.ps + (size_t)(2 + j) * N + row);
+    const Real a_raw = st.ps[row], g_raw = st.ps[N + row];
+    stage_column(ys, st.vals + row, t_ins, N, bd);
+    for (int t = 0; t < t_ins; ++t)
+        if (!(ys[t * bd] > Real(0))) {
+            flag_error(st.err, kErrObs, t);
+            return;
+        }
+    const bool dump = row == dump_row;
+    const Real alpha = M::logistic_ps(a_raw);
+    const Real gamma = M::logistic_ps(g_raw);
+    const Real oma = Real(1) - alpha, omg = Real(1) - gamma;
+    Real lp = 0;
+    for (int j = 0; j < S; ++j) {
+        const Real s0 = M::exp_ps(ring[j * bd]);
+        ring[j * bd] = s0;
+        if (dump) dump_se[j] = s0;
+        lp += ys[j * bd];
+    }
+    lp = lp / Real(S);
+    // seasonality index u is produced at step u-S; the window needs u in [t_ins-I, t_ins)
+    for (int u = t_ins - I; u < S && u < t_ins; ++u)
+        if (u >= 0) win[(u - (t_ins - I)) * bd] = ring[u * bd];
+    int j = 0;
+    for (int t = 0; t < t_ins; ++t) {
+        const Real yt = ys[t * bd];
+        const Real s_t = ring[j * bd];
+        const Real l = alpha * fdiv(yt, s_t) + oma * lp;
+        if (!(l > Real(0)) || !isfinite(l)) {
+            flag_error(st.err, kErrFcLevel, t);
+            return;
+        }
+        const Real sn = gamma * fdiv(yt, lp) + omg * s_t;
+        ring[j * bd] = sn;
+        const int uu = t + S;
+        if (uu >= t_ins - I && uu < t_ins) win[(uu - (t_ins - I)) * bd] = sn;
+        if (dump) {
+            dump_lv[t] = l;
+            dump_se[uu] = sn;
+        }
+        lp = l;
+        j = (j + 1 == S) ? 0 : j + 1;
+    }
+    if (X == nullptr) return;
+    const Real level = lp;
+    for (int c = 0; c < I; ++c) {
+        const Real sv = win[c * bd];
+        if (!(sv > Real(0))) {
+            flag_error(st.err, kErrSeas, t_ins);
+            return;
+        }
+        X[(size_t)row * in0 + c] = fdiv(ys[(t_ins - I + c) * bd], level * sv);
+    }
+    for (int c = 0; c < 6; ++c) X[(size_t)row * in0 + I + c] = (st.cat[row] == c) ? Real(1) : Real(0);
+    FL[row] = level;
+    // seasonal_at(t_ins + o): indices [t_ins, t_ins+S) sit in ring slot (index mod S)
+    for (int o = 0; o < O; ++o) {
+        int idx = t_ins + o;
+        while (idx >= t_ins + S) idx -= S;
+        FS[(size_t)row * O + o] = ring[(idx % S) * bd];
+    }
+}
+
+}  // namespace esrnn_dev
