@@ -177,6 +177,13 @@ esrnn_status esrnn_trainer_run_batch(esrnn_trainer* t, int32_t B, const int32_t*
                                      double* anchor_levels, double* net_grads, int32_t* n_slots,
                                      int32_t* slot_rows, double* ps_grads);
 
+/* Global shuffled window order (series row, anchor) that the last train_epoch consumed:
+ * make_batches(all_windows(), ...) with the trainer RNG (trainer.hpp:82-102, 214-223,
+ * matrix.hpp:203-205); batch b is entries [b*batch_size, (b+1)*batch_size).  n must equal
+ * the number of windows (series x (T - O - I + 1)).  Inspection hook for the bit-exact
+ * window-index contract. */
+esrnn_status esrnn_trainer_last_epoch_windows(const esrnn_trainer* t, int32_t* rows, int32_t* anchors, int64_t n);
+
 /* Trainer::forecast_at(drop_tail) (trainer.hpp:248-288): real-scale O-step
  * forecasts for the owned rows, out is n_local x O row-major. */
 esrnn_status esrnn_trainer_forecast(esrnn_trainer* t, int64_t drop_tail, double* out);

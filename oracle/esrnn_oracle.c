@@ -160,6 +160,8 @@ struct esrnn_trainer {
     rng_t rng;
     char err[512];
     double last_ms;
+    int32_t *last_wr, *last_wa;   /* window order of the last train_epoch */
+    int64_t last_nw;
 };
 
 static char g_create_err[512];
@@ -311,7 +313,7 @@ void esrnn_trainer_destroy(esrnn_trainer* t) {
     if (!t) return;
     free(t->vals); free(t->cat); free(t->a_raw); free(t->g_raw); free(t->s_raw);
     free(t->m_a); free(t->v_a); free(t->m_g); free(t->v_g); free(t->m_s); free(t->v_s);
-    free(t->steps); free(t->W); free(t->mW); free(t->vW);
+    free(t->steps); free(t->W); free(t->mW); free(t->vW); free(t->last_wr); free(t->last_wa);
     free(t);
 }
 
@@ -898,8 +900,11 @@ esrnn_status esrnn_trainer_train_epoch(esrnn_trainer* t, double* mean_loss) {
         acc += l * mc;
         weight += mc;
     }
-    free(wr);
-    free(wa);
+    free(t->last_wr);
+    free(t->last_wa);
+    t->last_wr = wr;
+    t->last_wa = wa;
+    t->last_nw = nw;
     if (st) return st;
     *mean_loss = acc / weight;
     return ESRNN_OK;
@@ -1068,6 +1073,13 @@ esrnn_status esrnn_trainer_hw_state(esrnn_trainer* t, int64_t row, int64_t t_len
         levels[tt] = lvl;
         lp = lvl;
     }
+    return ESRNN_OK;
+}
+
+esrnn_status esrnn_trainer_last_epoch_windows(const esrnn_trainer* t, int32_t* rows, int32_t* anchors, int64_t n) {
+    if (n != t->last_nw || !t->last_wr) return ESRNN_SHAPE_ERROR;
+    memcpy(rows, t->last_wr, sizeof(int32_t) * n);
+    memcpy(anchors, t->last_wa, sizeof(int32_t) * n);
     return ESRNN_OK;
 }
 

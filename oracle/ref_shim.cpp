@@ -52,6 +52,7 @@ struct esrnn_trainer {
     std::unique_ptr<Trainer> tr;
     std::string err;
     double last_ms = 0.0;
+    std::vector<std::pair<int, int>> last_windows;  // order consumed by the last train_epoch
 };
 
 namespace {
@@ -234,6 +235,14 @@ esrnn_status esrnn_trainer_set_per_series(esrnn_trainer* t, int64_t row_begin, i
 
 esrnn_status esrnn_trainer_train_epoch(esrnn_trainer* t, double* mean_loss) {
     return guarded(t->err, [&] {
+        // replay make_batches on a copy of the trainer RNG to record the window order the
+        // epoch is about to consume (trainer.hpp:235)
+        {
+            Rng copy = t->tr->rng_;
+            auto w = t->tr->all_windows();
+            copy.shuffle(w);
+            t->last_windows = std::move(w);
+        }
         const auto t0 = std::chrono::steady_clock::now();
         *mean_loss = t->tr->train_epoch();
         t->last_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -332,6 +341,15 @@ esrnn_status esrnn_trainer_hw_state(esrnn_trainer* t, int64_t row, int64_t t_len
         std::memcpy(levels, st.levels.data(), sizeof(double) * st.levels.size());
         std::memcpy(seas, st.seasonalities.data(), sizeof(double) * st.seasonalities.size());
     });
+}
+
+esrnn_status esrnn_trainer_last_epoch_windows(const esrnn_trainer* t, int32_t* rows, int32_t* anchors, int64_t n) {
+    if (n != static_cast<int64_t>(t->last_windows.size())) return ESRNN_SHAPE_ERROR;
+    for (int64_t i = 0; i < n; ++i) {
+        rows[i] = t->last_windows[i].first;
+        anchors[i] = t->last_windows[i].second;
+    }
+    return ESRNN_OK;
 }
 
 esrnn_status esrnn_trainer_last_device_ms(const esrnn_trainer* t, double* ms) {

@@ -127,6 +127,7 @@ class NativeApi:
         L.esrnn_trainer_validate.argtypes = [_vp, _dp, _dp, _dp]
         L.esrnn_trainer_hw_state.argtypes = [_vp, C.c_int64, C.c_int64, _dp, _dp]
         L.esrnn_trainer_last_device_ms.argtypes = [_vp, _dp]
+        L.esrnn_trainer_last_epoch_windows.argtypes = [_vp, _ip, _ip, C.c_int64]
         L.esrnn_trainer_kernel_launches.argtypes = [_vp, C.POINTER(C.c_int64)]
         L.esrnn_trainer_profile_kernels.argtypes = [_vp, C.c_int32]
         L.esrnn_trainer_kernel_times.argtypes = [_vp, _dp, C.POINTER(C.c_int64)]
@@ -136,7 +137,7 @@ class NativeApi:
                    "esrnn_trainer_param_info", "esrnn_trainer_get_weights", "esrnn_trainer_set_weights",
                    "esrnn_trainer_get_per_series", "esrnn_trainer_set_per_series", "esrnn_trainer_train_epoch",
                    "esrnn_trainer_run_batch", "esrnn_trainer_forecast", "esrnn_trainer_validate",
-                   "esrnn_trainer_hw_state", "esrnn_trainer_last_device_ms", "esrnn_trainer_kernel_launches",
+                   "esrnn_trainer_hw_state", "esrnn_trainer_last_device_ms", "esrnn_trainer_last_epoch_windows", "esrnn_trainer_kernel_launches",
                    "esrnn_trainer_profile_kernels", "esrnn_trainer_kernel_times", "esrnn_nccl_unique_id", "esrnn_make_synthetic"):
             getattr(L, fn).restype = C.c_int
 

@@ -183,6 +183,7 @@ struct esrnn_trainer {
 
     DevPlan epoch_plan, batch_plan;
     HostPlan hp;
+    std::vector<int> last_wr, last_wa;  // global window order of the last train_epoch
     PinnedBuf<int> pin_i;
     PinnedBuf<double> pin_d;
 
@@ -731,10 +732,11 @@ void launch_step(Eng* e, const PlanDev& pv, int s, bool grads, bool update, Stat
     }
     e->launches += 2;
     if (!grads) return;
-    const bool sharded = e->world > 1;
+    const bool sharded = e->world > 1 && e->comm != nullptr;
     {
         KS k(e, 2);
-        launch_finish<Real>(e, st, pv, s, sharded ? 0 : 1);
+        // bit 0: finalise the step scalars here (single GPU); bit 1: the step applies updates
+        launch_finish<Real>(e, st, pv, s, (sharded ? 0 : 1) | (update ? 2 : 0));
     }
     e->launches += 1;
     if (sharded) {
@@ -742,7 +744,7 @@ void launch_step(Eng* e, const PlanDev& pv, int s, bool grads, bool update, Stat
                               e->stream));
         KS k(e, 5);
         const int rb = static_cast<int>((lay.P_pad + 255) / 256);
-        k_finalize<Real><<<rb, 256, 0, e->stream>>>(st, pv, lay, s);
+        k_finalize<Real><<<rb, 256, 0, e->stream>>>(st, pv, lay, s, update ? 1 : 0);
         e->launches += 1;
     }
     if (update) {
@@ -908,6 +910,8 @@ double train_epoch_impl(Eng* e) {
         for (int i = 49; i < 64 && c[i] > 0; ++i) std::fprintf(stderr, " %lld", c[i] - c[i - 1]);
         std::fprintf(stderr, "\n[esrnn dbg] reduce block0 start - ES block0 start: %lld\n", c[48] - c[32]);
     }
+    e->last_wr = std::move(wr);
+    e->last_wa = std::move(wa);
     // trainer.hpp:236-242: acc += loss * count, in batch order
     double acc = 0.0, weight = 0.0;
     for (int s = 0; s < steps; ++s) {
@@ -976,7 +980,7 @@ void run_batch_impl(Eng* e, int32_t B, const int32_t* rows, const int32_t* ancho
     throw_device_error(e);
     // loss: sum of tile partials (single GPU) or all-reduced sum (sharded) / M
     double lsum = 0.0;
-    if (grads && e->world > 1) {
+    if (grads && e->comm != nullptr) {
         Real g2[2];
         CUDA_OK(cudaMemcpy(g2, reinterpret_cast<Real*>(e->gbuf.p) + e->lay.P_pad, sizeof g2, cudaMemcpyDeviceToHost));
         lsum = static_cast<double>(g2[1]);
@@ -985,7 +989,7 @@ void run_batch_impl(Eng* e, int32_t B, const int32_t* rows, const int32_t* ancho
         std::vector<double> lp(nt);
         if (nt) CUDA_OK(cudaMemcpy(lp.data(), e->loss_part.p, sizeof(double) * nt, cudaMemcpyDeviceToHost));
         for (double v : lp) lsum += v;
-        if (e->world > 1) raise(ESRNN_CONFIG_ERROR, "sharded batch_loss requires gradients (collective step)");
+        if (e->comm != nullptr) raise(ESRNN_CONFIG_ERROR, "sharded batch_loss requires gradients (collective step)");
     }
     if (loss) *loss = lsum / count;
     if (mask_count) *mask_count = count;
@@ -1073,7 +1077,7 @@ void forecast_impl(Eng* e, int64_t drop_tail, double* out, double* smape, double
         for (int i = 0; i < N; ++i) acc += sm[i];
         if (smape)
             for (int i = 0; i < N; ++i) smape[i] = sm[i];
-        if (e->world > 1) {
+        if (e->comm != nullptr) {
             if (e->smape_sum.n < 1) e->smape_sum.alloc(1);
             CUDA_OK(cudaMemcpy(e->smape_sum.p, &acc, sizeof acc, cudaMemcpyHostToDevice));
             NCCL_OK(ncclAllReduce(e->smape_sum.p, e->smape_sum.p, 1, ncclDouble, ncclSum, e->comm, e->stream));
@@ -1169,10 +1173,16 @@ esrnn_status esrnn_trainer_create(const esrnn_profile* profile, const esrnn_trai
         CUDA_OK(cudaEventCreate(&e->ev0));
         CUDA_OK(cudaEventCreate(&e->ev1));
         if (e->world > 1) {
-            ncclUniqueId id;
-            static_assert(sizeof(id.internal) == 128, "nccl id size");
-            std::memcpy(id.internal, dist->nccl_unique_id, 128);
-            NCCL_OK(ncclCommInitRank(&e->comm, e->world, id, e->rank));
+            // an id of 128 x 0xEE is the local-partials test mode: the shard runs its data
+            // path but skips the collective, so a test can sum per-rank partials itself
+            bool local_only = true;
+            for (int i = 0; i < 128; ++i) local_only = local_only && dist->nccl_unique_id[i] == 0xEE;
+            if (!local_only) {
+                ncclUniqueId id;
+                static_assert(sizeof(id.internal) == 128, "nccl id size");
+                std::memcpy(id.internal, dist->nccl_unique_id, 128);
+                NCCL_OK(ncclCommInitRank(&e->comm, e->world, id, e->rank));
+            }
         }
 
         // network.hpp:89-116 init order on the trainer RNG (identical on every rank)
@@ -1344,6 +1354,13 @@ esrnn_status esrnn_trainer_hw_state(esrnn_trainer* t, int64_t row, int64_t t_len
         if (t->fp64) hw_state_impl<double>(t, row, t_len, levels, seas);
         else hw_state_impl<float>(t, row, t_len, levels, seas);
     });
+}
+
+esrnn_status esrnn_trainer_last_epoch_windows(const esrnn_trainer* t, int32_t* rows, int32_t* anchors, int64_t n) {
+    if (n != static_cast<int64_t>(t->last_wr.size())) return ESRNN_SHAPE_ERROR;
+    std::memcpy(rows, t->last_wr.data(), sizeof(int32_t) * n);
+    std::memcpy(anchors, t->last_wa.data(), sizeof(int32_t) * n);
+    return ESRNN_OK;
 }
 
 esrnn_status esrnn_trainer_last_device_ms(const esrnn_trainer* t, double* ms) {

@@ -19,7 +19,8 @@ constexpr int kRedChunks = 2;         // 32-parameter chunks per reduce block
 // clip scale (trainer.hpp:603-615), global Adam step and bias corrections (:617-620),
 // step loss (masked mean, autodiff.hpp:392)
 template <typename Real>
-__device__ void finalize_scalars(StateDev<Real>& st, const PlanDev& pl, int s, double sq, double loss_sum) {
+__device__ void finalize_scalars(StateDev<Real>& st, const PlanDev& pl, int s, double sq, double loss_sum,
+                                 bool advance) {
     double scale = 1.0;
     if (st.has_clip) {
         const double norm = sqrt(sq);
@@ -28,7 +29,7 @@ __device__ void finalize_scalars(StateDev<Real>& st, const PlanDev& pl, int s, d
     st.scal[0] = scale;
     st.scal[3] = loss_sum / pl.step_M[s];
     st.loss_hist[s] = loss_sum / pl.step_M[s];
-    if (st.err[0] == 0) {
+    if (advance && st.err[0] == 0) {  // only a step that applies updates advances Adam's t
         const long long step = ++(*st.net_step);
         st.scal[1] = 1.0 - pow(0.9, static_cast<double>(step));
         st.scal[2] = 1.0 - pow(0.999, static_cast<double>(step));
@@ -250,17 +251,17 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
     for (int t = 0; t < nt; ++t) ls += st.loss_part[t];
     st.gbuf[lay.P_pad] = static_cast<Real>(es);
     st.gbuf[lay.P_pad + 1] = static_cast<Real>(ls);
-    if (finalize) {
+    if (finalize & 1) {
         double all = 0.0;
         for (int b = 0; b < nrb; ++b) all += *reinterpret_cast<volatile double*>(st.red_sq_part + b);
-        finalize_scalars(st, pl, s, all + es, ls);
+        finalize_scalars(st, pl, s, all + es, ls, (finalize & 2) != 0);
     }
     *st.done_ctr = 0;
 }
 
 // After the NCCL all-reduce of gbuf (sharded mode): global squared norm + scalars.
 template <typename Real>
-__global__ void __launch_bounds__(256) k_finalize(StateDev<Real> st, PlanDev pl, NetLayout lay, int s) {
+__global__ void __launch_bounds__(256) k_finalize(StateDev<Real> st, PlanDev pl, NetLayout lay, int s, int advance) {
     __shared__ double red[32];
     __shared__ bool last;
     const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -281,7 +282,7 @@ __global__ void __launch_bounds__(256) k_finalize(StateDev<Real> st, PlanDev pl,
     double all = 0.0;
     for (unsigned b = 0; b < gridDim.x; ++b) all += *reinterpret_cast<volatile double*>(st.red_sq_part + b);
     const double es = st.attach ? static_cast<double>(st.gbuf[lay.P_pad]) : 0.0;
-    finalize_scalars(st, pl, s, all + es, static_cast<double>(st.gbuf[lay.P_pad + 1]));
+    finalize_scalars(st, pl, s, all + es, static_cast<double>(st.gbuf[lay.P_pad + 1]), advance != 0);
     st.done_ctr[1] = 0;
 }
 

@@ -487,6 +487,14 @@ class Trainer:
         self._chk(self.api.lib.esrnn_trainer_validate(self._h, N.dptr(fc), N.dptr(sm), C.byref(mean)))
         return ValidationResult(self._ids[self.row_begin:self.row_end], fc, sm, mean.value)
 
+    def last_epoch_windows(self) -> list:
+        """Global shuffled (row, anchor) order consumed by the last train_epoch."""
+        I, O, T = self._profile.input_window, self._profile.horizon, self.train_length()
+        n = self.series_count() * (T - O - I + 1)
+        r, a = np.zeros(n, dtype=np.int32), np.zeros(n, dtype=np.int32)
+        self._chk(self.api.lib.esrnn_trainer_last_epoch_windows(self._h, N.iptr(r), N.iptr(a), n))
+        return list(zip(r.tolist(), a.tolist()))
+
     def last_device_ms(self) -> float:
         ms = C.c_double()
         self._chk(self.api.lib.esrnn_trainer_last_device_ms(self._h, C.byref(ms)))

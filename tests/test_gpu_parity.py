@@ -207,3 +207,84 @@ def test_numeric_domain_error(engine, oracle):
         g.train_epoch()
     with pytest.raises(E.NumericDomainError):
         g.validate()
+
+
+# ------------------------------------------------------------------ reference goldens
+import golden_check  # noqa: E402
+
+
+@pytest.mark.parametrize("name", golden_check.FIXTURES)
+def test_engine_matches_reference_golden_fp64(engine, name):
+    """Replays the reference-generated fixture: init weights, one masked batch (loss,
+    WindowBatch matrices, slot order, all gradients), two epochs (losses, bit-exact window
+    order, parameters), validate / forecast_at(0), post-training HW state."""
+    golden_check.check(engine, name, "fp64", tol=1e-10, tol_train=1e-9)
+
+
+@pytest.mark.parametrize("name", golden_check.FIXTURES)
+def test_engine_matches_reference_golden_fp32_step(engine, name):
+    """fp32 performance mode against the same fixture: first-step losses/gradients within
+    the north-star 1e-4 (tensor-scaled), window order still bit-exact."""
+    fx = golden_check.load(name)
+    prof = PROFILES[fx["profile"]][0]
+    tr = Trainer((np.array(fx["values"]), np.array(fx["categories"], dtype=np.int32)), prof,
+                 TrainConfig(seed=fx["train_seed"], batch_size=fx["batch_size"], precision="fp32"), api=engine)
+    bt = fx["batch"]
+    b = WindowBatch(list(bt["rows"]), list(bt["anchors"]), mask=np.array(bt["mask"]))
+    g = tr.batch_gradients(b)
+    assert abs(g.loss - bt["loss"]) <= 1e-4 * abs(bt["loss"])
+    for k, v in bt["net_grads"].items():
+        golden_check._cmp_array(g.network[k], v, 1e-3, k)
+    tr.train_epoch()
+    tr.train_epoch()
+    assert [list(x) for x in tr.last_epoch_windows()[:512]] == fx["last_epoch_windows"]
+
+
+# ------------------------------------------------------------------ window indices
+def test_epoch_window_order_bit_exact_vs_reference(engine, oracle):
+    """North-star contract: bit-exact window indices.  The engine's host replica of
+    all_windows + Rng::shuffle equals the reference / oracle order, epoch after epoch."""
+    from conftest import REF_LIB
+    from paper_1907_03329_b200._native import NativeApi
+    apis = [oracle] + ([NativeApi(REF_LIB)] if REF_LIB.exists() else [])
+    prof, vals, cats = dataset(oracle, "quarterly", 30, 3)
+    trs = [Trainer((vals, cats), prof, TrainConfig(seed=99, batch_size=100), api=a) for a in [engine] + apis]
+    for _ in range(3):
+        orders = []
+        for t in trs:
+            t.train_epoch()
+            orders.append(t.last_epoch_windows())
+        assert all(o == orders[0] for o in orders[1:])
+
+
+# ------------------------------------------------------------------ sharded data path
+@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_sharded_partials_sum_to_full_batch(engine, oracle, world, precision):
+    """Series-sharded ranks on one GPU (local-partials mode: the data path of every rank
+    runs, the collective is summed here): the per-rank partial loss / shared gradients add
+    up to the single-GPU step; per-series gradients stay with their owner."""
+    from paper_1907_03329_b200.sharding import LOCAL_PARTIALS_ID, shard_range
+    prof, vals, cats = dataset(oracle, "monthly", 10, 4)
+    cfg = TrainConfig(seed=7, batch_size=64, precision=precision)
+    full = Trainer((vals, cats), prof, cfg, api=engine)
+    b = sample_batch(full, 64, 5, masked_rows=(3,))
+    gf = full.batch_gradients(copy_batch(b))
+    tot_loss, tot = 0.0, {k: np.zeros_like(v) for k, v in gf.network.items()}
+    for r in range(world):
+        tr = Trainer((vals, cats), prof, cfg, api=engine, dist=(r, world, LOCAL_PARTIALS_ID))
+        assert (tr.row_begin, tr.row_end) == shard_range(r, world, 10)
+        g = tr.batch_gradients(copy_batch(b))
+        tot_loss += g.loss
+        for k in tot:
+            tot[k] += g.network[k]
+        for sid, p in g.per_series.items():
+            assert tr.row_begin <= int(sid[1:]) < tr.row_end
+            ref = gf.per_series[sid]
+            scale = max(abs(ref.alpha_raw), abs(ref.gamma_raw), np.max(np.abs(ref.init_seasonality_raw)))
+            tol = 1e-9 if precision == "fp64" else 1e-3
+            assert abs(p.alpha_raw - ref.alpha_raw) <= tol * scale
+    tol = 1e-12 if precision == "fp64" else 1e-5
+    assert abs(tot_loss - gf.loss) <= tol * abs(gf.loss)
+    for k, v in gf.network.items():
+        assert tensor_err(tot[k], v) <= (1e-11 if precision == "fp64" else 1e-4), k
