@@ -605,7 +605,7 @@ void upload_plan(Eng* e, const HostPlan& hp, DevPlan& dp, size_t cap_w, size_t c
 // ------------------------------------------------------------------ step launch
 template <typename Real>
 size_t stack_smem(const NetLayout& lay, bool resident) {
-    return sizeof(Real) * TileSmem::make(lay, kRows, resident).total;
+    return sizeof(Real) * TileSmem::make(lay, kRows, stack_threads_for_r<kRows>(lay), resident).total;
 }
 
 // Resident mode keeps every live weight in shared memory for the whole tile (one TMA
@@ -617,7 +617,7 @@ bool stack_resident(const NetLayout& lay) {
     return stack_smem<Real>(lay, true) + 4096 <= static_cast<size_t>(g_smem_optin);
 }
 
-int stack_threads(const NetLayout& lay) { return stack_threads_for(lay); }
+int stack_threads(const NetLayout& lay) { return stack_threads_for_r<kRows>(lay); }
 
 template <typename Real>
 size_t finish_smem(const NetLayout& lay) {

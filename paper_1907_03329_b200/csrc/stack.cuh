@@ -9,14 +9,18 @@
 //
 // A CTA owns R windows.  Weights: in resident mode the whole compact vector arrives in
 // shared memory by one TMA bulk copy (cp.async.bulk + mbarrier) overlapped with the window
-// gather; otherwise (fp64 nets that do not fit) one layer is staged at a time.  All
-// products are register-blocked FFMA on shared memory:
-//   forward   pre[r][q] = sum_k u[r][k] W^T[q][k]   thread (row group, q), 4 rows x 4 k per step
-//   backward  W_bar^T[q][k] = sum_r u[r][k] a[r][q]  and  u_bar[r][k] = sum_q a[r][q] W^T[q][k]
-//             in one pass, thread (q group, k): W_bar partials go to global coalesced over k,
-//             u_bar partials over q groups are summed in a fixed order.
+// gather; otherwise (fp64 nets that do not fit) one layer is staged at a time.
+//
+// The tile is a chain of barrier-separated phases, so the phase count is the latency:
+//   forward   one phase per layer: thread (row pair, hidden unit) accumulates the three
+//             live gate pre-activations (i, g, o) over the input and applies the cell
+//             nonlinearities in registers (no separate gate phase);
+//   backward  per layer: [combine input-adjoint partials + residual + gate adjoints] and
+//             [input adjoint u_bar = pre_bar . W^T over q groups]; the weight-gradient
+//             partials (not on the dependency chain) are produced afterwards for every
+//             layer and the head in one barrier-free tail, coalesced over k.
 // Thread mappings use power-of-two strides (shift/mask, no runtime integer division)
-// and the two GEMM helpers are out-of-line so the kernel body stays i-cache resident.
+// and the product helpers are out-of-line so the kernel body stays i-cache resident.
 #pragma once
 #include "common.cuh"
 
@@ -34,16 +38,17 @@ struct ForecastArgs {
     double* smape;       // [N]
 };
 
-constexpr int kRowGroups = 2;
+constexpr int kRowsPerThread = 2;  // forward: 2 rows x 1 hidden unit (3 gates) per thread
 
-__host__ __device__ inline int stack_threads_for(const NetLayout& lay) {
-    const int nt = kRowGroups << log2_ceil(3 * lay.H);
+template <int R>
+__host__ __device__ inline int stack_threads_for_r(const NetLayout& lay) {
+    const int nt = (R / kRowsPerThread) << log2_ceil(lay.H);
     return nt < 64 ? 64 : (nt > 512 ? 512 : nt);
 }
 
 // Shared-memory carve-up of one row tile (Real units; every offset a multiple of 4).
 struct TileSmem {
-    int w, xin, sin, sout, lvl, tgt, msk, act, gates, z, pred, pbar, pre, hbar, resid, ubar, upart, total;
+    int w, xin, sin, sout, lvl, tgt, msk, act, gates, z, zb, pred, pbar, preb, hbar, resid, ubar, upart, total;
     int wsize;
     __host__ __device__ static int r4(int x) { return (x + 3) & ~3; }
     __host__ __device__ static long long stage_size(const NetLayout& lay) {
@@ -54,10 +59,9 @@ struct TileSmem {
         }
         return m;
     }
-    __host__ __device__ static TileSmem make(const NetLayout& lay, int R, bool resident) {
+    __host__ __device__ static TileSmem make(const NetLayout& lay, int R, int NT, bool resident) {
         TileSmem t;
         const int H = lay.H, I = lay.I, L = lay.L;
-        const int NT = stack_threads_for(lay);
         int o = 0;
         t.wsize = resident ? static_cast<int>(lay.P_pad) : r4(static_cast<int>(stage_size(lay)));
         t.w = o; o += t.wsize;
@@ -70,9 +74,10 @@ struct TileSmem {
         t.act = o; o += r4(L * R * lay.ldh);
         t.gates = o; o += r4(4 * L * R * H);
         t.z = o; o += r4(R * lay.ldh);
+        t.zb = o; o += r4(R * lay.ldh);
         t.pred = o; o += r4(R * lay.ldo);
         t.pbar = o; o += r4(R * lay.ldo);
-        t.pre = o; o += r4(R * lay.ldg);
+        t.preb = o; o += r4(L * R * lay.ldg);
         t.hbar = o; o += r4(R * lay.ldh);
         t.resid = o; o += r4(R * lay.ldh);
         t.ubar = o; o += r4(R * (lay.ldx > lay.ldh ? lay.ldx : lay.ldh));
@@ -114,8 +119,82 @@ __device__ __forceinline__ void stage_segment(Real* __restrict__ dst, const Real
     }
 }
 
-// out[r][q] = act(sum_k u[r][k] * WT[q][k] + bias[q]) for r < R, q < G.
-// Thread (row group rg, column q): RPT rows per thread, 4 k per step.
+// One LSTM layer at sequence length 1 (lstm_cell, network.hpp:148-163), fused:
+// pre = u . W_in + b for the live gates of hidden unit hh, then i, g, o, c = i*g,
+// h = o*tanh(c) (+ residual).  Thread (row group, hh), RPT rows each.
+template <typename Real, int R, int RPT>
+__device__ __noinline__ void fwd_layer(Real* __restrict__ gates, Real* __restrict__ out, const Real* __restrict__ radd,
+                                       const Real* __restrict__ u, int ldu, const Real* __restrict__ WT, int ldk,
+                                       const Real* __restrict__ bias, int in, int H, int ldh) {
+    using M = Math<Real>;
+    const int lh = log2_ceil(H);
+    constexpr int NG = R / RPT;
+    for (int idx = threadIdx.x; idx < (NG << lh); idx += blockDim.x) {
+        const int hh = idx & ((1 << lh) - 1), rg = idx >> lh;
+        if (hh >= H) continue;
+        const Real* wi = WT + hh * ldk;
+        const Real* wg = WT + (H + hh) * ldk;
+        const Real* wo = WT + (2 * H + hh) * ldk;
+        const Real* ub = u + rg * RPT * ldu;
+        Real ai[RPT], ag[RPT], ao[RPT];
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) ai[j] = ag[j] = ao[j] = 0;
+        int k = 0;
+#pragma unroll 1
+        for (; k + 4 <= in; k += 4) {
+            Real vi[4], vg[4], vo[4];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                vi[c] = wi[k + c];
+                vg[c] = wg[k + c];
+                vo[c] = wo[k + c];
+            }
+#pragma unroll
+            for (int j = 0; j < RPT; ++j) {
+                const V4<Real> x = lds4(ub + j * ldu + k);
+                const Real xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    ai[j] += xs[c] * vi[c];
+                    ag[j] += xs[c] * vg[c];
+                    ao[j] += xs[c] * vo[c];
+                }
+            }
+        }
+#pragma unroll 1
+        for (; k < in; ++k) {
+            const Real a = wi[k], b = wg[k], c = wo[k];
+#pragma unroll
+            for (int j = 0; j < RPT; ++j) {
+                const Real x = ub[j * ldu + k];
+                ai[j] += x * a;
+                ag[j] += x * b;
+                ao[j] += x * c;
+            }
+        }
+        const Real bi = bias[hh], bg = bias[H + hh], bo = bias[2 * H + hh];
+        const int RH = R * H;
+#pragma unroll
+        for (int j = 0; j < RPT; ++j) {
+            const int r = rg * RPT + j;
+            const Real i = M::logistic(ai[j] + bi);
+            const Real g = M::tanh(ag[j] + bg);
+            const Real o = M::logistic(ao[j] + bo);
+            const Real c = i * g;
+            const Real tc = M::tanh(c);
+            Real h = o * tc;
+            if (radd) h = h + radd[r * ldh + hh];
+            const int e = r * H + hh;
+            gates[e] = i;
+            gates[RH + e] = g;
+            gates[2 * RH + e] = o;
+            gates[3 * RH + e] = tc;
+            out[r * ldh + hh] = h;
+        }
+    }
+}
+
+// out[r][q] = act(sum_k u[r][k] * WT[q][k] + bias[q]) for the head (q < G).
 template <typename Real, int R, int RPT>
 __device__ __noinline__ void gemm_fwd(Real* __restrict__ out, int ldo, const Real* __restrict__ u, int ldu,
                                       const Real* __restrict__ WT, int ldk, const Real* __restrict__ bias, int in, int G,
@@ -159,35 +238,75 @@ __device__ __noinline__ void gemm_fwd(Real* __restrict__ out, int ldo, const Rea
     }
 }
 
-// One pass over (q group g, input k):
-//   part_w[q*ldk + k] = sum_r u[r][k] * a[r][q]            (weight-gradient partial, global)
-//   upart[g][r][k]    = sum_{q in group} a[r][q] * WT[q][k] (input-adjoint partial, shared)
-// Returns the number of q groups used (upart slices to combine).
-template <typename Real, int R>
-__device__ __noinline__ int gemm_bwd(Real* __restrict__ part_w, const Real* __restrict__ u, int ldu,
-                                     const Real* __restrict__ a, int lda, const Real* __restrict__ WT, int ldk, int in,
-                                     int G, Real* __restrict__ upart) {
-    const int li = log2_ceil(in);
-    int QG = static_cast<int>(blockDim.x) >> li;
+// q groups for the adjoint products: thread (group, k) with lanes over k.
+__device__ __forceinline__ void q_groups(int in, int G, int& li, int& QG, int& qs) {
+    li = log2_ceil(in);
+    QG = static_cast<int>(blockDim.x) >> li;
     QG = QG < 1 ? 1 : QG;
-    int qs = (G + QG - 1) / QG;
+    qs = (G + QG - 1) / QG;
     qs = (qs + 3) & ~3;
     QG = (G + qs - 1) / qs;
+}
+
+// Input adjoint partials: upart[g][r][k] = sum_{q in group g} a[r][q] * WT[q][k].
+// Returns the number of groups (QG) the caller sums in a fixed order.
+template <typename Real, int R>
+__device__ __noinline__ int gemm_adj(Real* __restrict__ upart, const Real* __restrict__ a, int lda,
+                                     const Real* __restrict__ WT, int ldk, int in, int G) {
+    int li, QG, qs;
+    q_groups(in, G, li, QG, qs);
     for (int idx = threadIdx.x; idx < (QG << li); idx += blockDim.x) {
         const int k = idx & ((1 << li) - 1), g = idx >> li;
         if (k >= in) continue;
         const int q0 = g * qs, q1 = min(G, q0 + qs);
-        Real uk[R], au[R];
+        Real au[R];
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            uk[r] = u[r * ldu + k];
-            au[r] = 0;
-        }
+        for (int r = 0; r < R; ++r) au[r] = 0;
         int q = q0;
 #pragma unroll 1
         for (; q + 4 <= q1; q += 4) {
             const Real w0 = WT[(q + 0) * ldk + k], w1 = WT[(q + 1) * ldk + k];
             const Real w2 = WT[(q + 2) * ldk + k], w3 = WT[(q + 3) * ldk + k];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const V4<Real> x = lds4(a + r * lda + q);
+                au[r] += x.x * w0;
+                au[r] += x.y * w1;
+                au[r] += x.z * w2;
+                au[r] += x.w * w3;
+            }
+        }
+#pragma unroll 1
+        for (; q < q1; ++q) {
+            const Real w = WT[q * ldk + k];
+#pragma unroll
+            for (int r = 0; r < R; ++r) au[r] += a[r * lda + q] * w;
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) upart[(g * R + r) * in + k] = au[r];
+    }
+    return QG;
+}
+
+// Weight-gradient partials of one matrix, part_w[q*ldk + k] = sum_r u[r][k] * a[r][q]
+// (rows summed in order), plus the bias partial part_b[q] = sum_r a[r][q].  Reads only
+// shared memory that is final by now and writes disjoint global ranges: consecutive calls
+// need no barrier.
+template <typename Real, int R>
+__device__ __noinline__ void gemm_wgrad(Real* __restrict__ part_w, Real* __restrict__ part_b, const Real* __restrict__ u,
+                                        int ldu, const Real* __restrict__ a, int lda, int ldk, int in, int G) {
+    int li, QG, qs;
+    q_groups(in, G, li, QG, qs);
+    for (int idx = threadIdx.x; idx < (QG << li); idx += blockDim.x) {
+        const int k = idx & ((1 << li) - 1), g = idx >> li;
+        if (k >= in) continue;
+        const int q0 = g * qs, q1 = min(G, q0 + qs);
+        Real uk[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) uk[r] = u[r * ldu + k];
+        int q = q0;
+#pragma unroll 1
+        for (; q + 4 <= q1; q += 4) {
             Real g0 = 0, g1 = 0, g2 = 0, g3 = 0;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -196,10 +315,6 @@ __device__ __noinline__ int gemm_bwd(Real* __restrict__ part_w, const Real* __re
                 g1 += uk[r] * x.y;
                 g2 += uk[r] * x.z;
                 g3 += uk[r] * x.w;
-                au[r] += x.x * w0;
-                au[r] += x.y * w1;
-                au[r] += x.z * w2;
-                au[r] += x.w * w3;
             }
             part_w[(q + 0) * ldk + k] = g0;
             part_w[(q + 1) * ldk + k] = g1;
@@ -208,25 +323,12 @@ __device__ __noinline__ int gemm_bwd(Real* __restrict__ part_w, const Real* __re
         }
 #pragma unroll 1
         for (; q < q1; ++q) {
-            const Real w = WT[q * ldk + k];
             Real g0 = 0;
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const Real x = a[r * lda + q];
-                g0 += uk[r] * x;
-                au[r] += x * w;
-            }
+            for (int r = 0; r < R; ++r) g0 += uk[r] * a[r * lda + q];
             part_w[q * ldk + k] = g0;
         }
-#pragma unroll
-        for (int r = 0; r < R; ++r) upart[(g * R + r) * in + k] = au[r];
     }
-    return QG;
-}
-
-// bias-gradient partial: part_b[q] = sum_r a[r][q]
-template <typename Real, int R>
-__device__ __forceinline__ void colsum(Real* __restrict__ part_b, const Real* __restrict__ a, int lda, int G) {
     for (int q = threadIdx.x; q < G; q += blockDim.x) {
         Real acc = 0;
 #pragma unroll
@@ -239,21 +341,20 @@ __device__ __forceinline__ void colsum(Real* __restrict__ part_b, const Real* __
 template <typename Real, int R, int MODE, bool RESIDENT>
 __global__ void __launch_bounds__(512) k_stack(StateDev<Real> st, PlanDev pl, NetLayout lay_p, int s, ForecastArgs fa) {
     using M = Math<Real>;
-    constexpr int RPT = R / kRowGroups;
+    constexpr int RPT = kRowsPerThread;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Real* sm = reinterpret_cast<Real*>(smem_raw);
     __shared__ double red[32];
     __shared__ __align__(8) uint64_t wbar;
-    // the layout is read with dynamic layer indices in every phase: one shared copy up front
-    // instead of constant-bank misses scattered over the phases
+    // the layout is read with dynamic layer indices in every phase: one shared copy
     __shared__ NetLayout lay_s;
     if (threadIdx.x == 0) lay_s = lay_p;
     __syncthreads();
     const NetLayout& lay = lay_s;
-    const TileSmem ts = TileSmem::make(lay, R, RESIDENT);
+    const int tid = threadIdx.x, NT = blockDim.x;
+    const TileSmem ts = TileSmem::make(lay, R, NT, RESIDENT);
     const int H = lay.H, O = lay.O, I = lay.I, in0 = lay.in0, L = lay.L, G = 3 * H;
     const int ldx = lay.ldx, ldh = lay.ldh, ldg = lay.ldg, ldo = lay.ldo, ldkh = lay.ldkh;
-    const int tid = threadIdx.x, NT = blockDim.x;
     const int tile = blockIdx.x;
     const Real* __restrict__ th = st.theta;
 
@@ -267,10 +368,10 @@ __global__ void __launch_bounds__(512) k_stack(StateDev<Real> st, PlanDev pl, Ne
     Real* act = sm + ts.act;
     Real* gates = sm + ts.gates;
     Real* z = sm + ts.z;
+    Real* zb = sm + ts.zb;
     Real* pred = sm + ts.pred;
     Real* pbar = sm + ts.pbar;
-    Real* pre = sm + ts.pre;
-    Real* hbar = sm + ts.hbar;
+    Real* preb = sm + ts.preb;
     Real* resid = sm + ts.resid;
     Real* ubar = sm + ts.ubar;
     Real* upart = sm + ts.upart;
@@ -368,49 +469,24 @@ __global__ void __launch_bounds__(512) k_stack(StateDev<Real> st, PlanDev pl, Ne
 
     // ---- forward through the stack (network.hpp:148-210, sequence length 1) --------
     for (int l = 0; l < L; ++l) {
-        const int in = lay.layer_in[l];
         const Real* u = l == 0 ? xin : act + (l - 1) * R * ldh;
-        const int ldu = l == 0 ? ldx : ldh;
         if (!RESIDENT) {
             stage_segment(wsm, th + lay.cw[l], lay.cb[l] - lay.cw[l] + G);
             __syncthreads();
-            DBG_CLK(st, 2);
         }
         const Real* WT = RESIDENT ? wsm + lay.cw[l] : wsm;
         const Real* bias = RESIDENT ? wsm + lay.cb[l] : wsm + (lay.cb[l] - lay.cw[l]);
-        gemm_fwd<Real, R, RPT>(pre, ldg, u, ldu, WT, lay.ldk[l], bias, in, G, false);
-        __syncthreads();
-        DBG_CLK(st, 3);
-        Real* gi = gates + (4 * l + 0) * R * H;
-        Real* gg = gates + (4 * l + 1) * R * H;
-        Real* go = gates + (4 * l + 2) * R * H;
-        Real* gt = gates + (4 * l + 3) * R * H;
-        Real* out = act + l * R * ldh;
         const Real* radd = lay.block_last[l] ? act + lay.res_src[l] * R * ldh : nullptr;
-        for_rc(R, H, [&](int r, int hh) {
-            const Real i = M::logistic(pre[r * ldg + hh]);
-            const Real g = M::tanh(pre[r * ldg + H + hh]);
-            const Real o = M::logistic(pre[r * ldg + 2 * H + hh]);
-            const Real c = i * g;
-            const Real tc = M::tanh(c);
-            Real h = o * tc;
-            if (radd) h = h + radd[r * ldh + hh];
-            const int e = r * H + hh;
-            gi[e] = i;
-            gg[e] = g;
-            go[e] = o;
-            gt[e] = tc;
-            out[r * ldh + hh] = h;
-        });
+        fwd_layer<Real, R, RPT>(gates + 4 * l * R * H, act + l * R * ldh, radd, u, l == 0 ? ldx : ldh, WT, lay.ldk[l],
+                                bias, lay.layer_in[l], H, ldh);
         __syncthreads();
-        DBG_CLK(st, 4);
+        DBG_CLK(st, 2);
     }
     // head (network.hpp:207-209)
     const Real* cur = act + (L - 1) * R * ldh;
     if (!RESIDENT) {
         stage_segment(wsm, th + lay.c_nlw, lay.P_pad - lay.c_nlw);
         __syncthreads();
-        DBG_CLK(st, 5);
     }
     const long long hb0 = RESIDENT ? 0 : lay.c_nlw;
     const Real* nlwT = wsm + (lay.c_nlw - hb0);
@@ -419,17 +495,15 @@ __global__ void __launch_bounds__(512) k_stack(StateDev<Real> st, PlanDev pl, Ne
     const Real* obias = wsm + (lay.c_outb - hb0);
     gemm_fwd<Real, R, RPT>(z, ldh, cur, ldh, nlwT, ldkh, nlb, H, H, true);
     __syncthreads();
-    DBG_CLK(st, 6);
     gemm_fwd<Real, R, RPT>(pred, ldo, z, ldh, owT, ldkh, obias, H, O, false);
     __syncthreads();
-    DBG_CLK(st, 7);
+    DBG_CLK(st, 3);
     if (MODE == kForecast) {
         for_rc(nrows, O, [&](int r, int o) {
             fa.out[(size_t)(tile * R + r) * O + o] = static_cast<double>(pred[r * ldo + o] * lvl[r] * s_out[r * ldo + o]);
         });
         if (fa.validate) {
             __syncthreads();
-            DBG_CLK(st, 8);
             // sMAPE against the validation block (metrics.hpp:17-28)
             for (int r = tid; r < nrows; r += NT) {
                 const int row = tile * R + r;
@@ -460,79 +534,69 @@ __global__ void __launch_bounds__(512) k_stack(StateDev<Real> st, PlanDev pl, Ne
         }
         pbar[e] = pb;
     });
-    const double ltot = block_sum(lsum, red);
+    const double ltot = block_sum(lsum, red);  // its barriers also publish pbar
     if (tid == 0) st.loss_part[tile] = ltot;
     if (MODE == kLossOnly) return;
+    DBG_CLK(st, 4);
 
-    // ---- backward: head ------------------------------------------------------------
-    Real* __restrict__ part = st.part + (size_t)tile * lay.P_pad;
-    colsum<Real, R>(part + lay.c_outb, pbar, ldo, O);
-    int QG = gemm_bwd<Real, R>(part + lay.c_outw, z, ldh, pbar, ldo, owT, ldkh, H, O, upart);
+    // ---- backward: the dependency chain (input adjoints only) -----------------------
+    int QG = gemm_adj<Real, R>(upart, pbar, ldo, owT, ldkh, H, O);
     __syncthreads();
-    DBG_CLK(st, 9);
-    Real* zb = ubar;  // z adjoint through tanh
-    for_rc(R, H, [&](int r, int k) {
+    for_rc(R, H, [&](int r, int k) {  // z adjoint through tanh
         Real acc = 0;
         for (int g = 0; g < QG; ++g) acc += upart[(g * R + r) * H + k];
         const Real zz = z[r * ldh + k];
         zb[r * ldh + k] = acc * (Real(1) - zz * zz);
     });
     __syncthreads();
-    DBG_CLK(st, 10);
-    colsum<Real, R>(part + lay.c_nlb, zb, ldh, H);
-    QG = gemm_bwd<Real, R>(part + lay.c_nlw, cur, ldh, zb, ldh, nlwT, ldkh, H, H, upart);
+    QG = gemm_adj<Real, R>(upart, zb, ldh, nlwT, ldkh, H, H);
     __syncthreads();
-    DBG_CLK(st, 11);
-    for_rc(R, H, [&](int r, int k) {
-        Real acc = 0;
-        for (int g = 0; g < QG; ++g) acc += upart[(g * R + r) * H + k];
-        hbar[r * ldh + k] = acc;
-    });
-    __syncthreads();
-    DBG_CLK(st, 12);
-
-    // ---- backward: layers (reverse) ------------------------------------------------
+    DBG_CLK(st, 5);
     for (int l = L - 1; l >= 0; --l) {
-        const int in = lay.layer_in[l];
-        const Real* u = l == 0 ? xin : act + (l - 1) * R * ldh;
-        const int ldu = l == 0 ? ldx : ldh;
-        if (lay.block_last[l])
-            for (int e = tid; e < R * ldh; e += NT) resid[e] = hbar[e];
-        if (!RESIDENT) stage_segment(wsm, th + lay.cw[l], lay.cb[l] - lay.cw[l]);
-        const Real* WT = RESIDENT ? wsm + lay.cw[l] : wsm;
-        const Real* gi = gates + (4 * l + 0) * R * H;
-        const Real* gg = gates + (4 * l + 1) * R * H;
-        const Real* go = gates + (4 * l + 2) * R * H;
-        const Real* gt = gates + (4 * l + 3) * R * H;
+        // h_bar of layer l = input adjoint of the layer above (+ the block residual adjoint
+        // when layer l+1 opens a block b>0); the gate adjoints follow in the same phase
+        const bool add_res = (l + 1 < L) && lay.block_first[l + 1];
+        const bool save_res = lay.block_last[l] != 0;
+        const Real* gl = gates + 4 * l * R * H;
+        Real* pb = preb + l * R * ldg;
+        const int QGc = QG;
         for_rc(R, H, [&](int r, int hh) {
-            const int e = r * H + hh;
-            const Real hb = hbar[r * ldh + hh];
-            const Real i = gi[e], g = gg[e], o = go[e], tc = gt[e];
+            Real hb = 0;
+            for (int g = 0; g < QGc; ++g) hb += upart[(g * R + r) * H + hh];
+            if (add_res) hb = hb + resid[r * ldh + hh];
+            if (save_res) resid[r * ldh + hh] = hb;
+            const int e = r * H + hh, RH = R * H;
+            const Real i = gl[e], g = gl[RH + e], o = gl[2 * RH + e], tc = gl[3 * RH + e];
             const Real ob = hb * tc;
             const Real cb = (hb * o) * (Real(1) - tc * tc);
             const Real ib = cb * g, gb = cb * i;
-            pre[r * ldg + hh] = ib * i * (Real(1) - i);
-            pre[r * ldg + H + hh] = gb * (Real(1) - g * g);
-            pre[r * ldg + 2 * H + hh] = ob * o * (Real(1) - o);
+            pb[r * ldg + hh] = ib * i * (Real(1) - i);
+            pb[r * ldg + H + hh] = gb * (Real(1) - g * g);
+            pb[r * ldg + 2 * H + hh] = ob * o * (Real(1) - o);
         });
+        if (!RESIDENT) stage_segment(wsm, th + lay.cw[l], lay.cb[l] - lay.cw[l]);
         __syncthreads();
-        DBG_CLK(st, 13);
-        colsum<Real, R>(part + lay.cb[l], pre, ldg, G);
-        QG = gemm_bwd<Real, R>(part + lay.cw[l], u, ldu, pre, ldg, WT, lay.ldk[l], in, G, upart);
+        const Real* WT = RESIDENT ? wsm + lay.cw[l] : wsm;
+        QG = gemm_adj<Real, R>(upart, pb, ldg, WT, lay.ldk[l], lay.layer_in[l], G);
         __syncthreads();
-        DBG_CLK(st, 14);
-        const int ldub = l == 0 ? ldx : ldh;
-        for_rc(R, in, [&](int r, int k) {
-            Real acc = 0;
-            for (int g = 0; g < QG; ++g) acc += upart[(g * R + r) * in + k];
-            if (l > 0)
-                hbar[r * ldh + k] = lay.block_first[l] ? acc + resid[r * ldh + k] : acc;
-            else
-                ubar[r * ldub + k] = acc;
-        });
-        __syncthreads();
-        DBG_CLK(st, 15);
+        DBG_CLK(st, 6);
     }
+    // x_bar (layer 0's input adjoint) for the ES contributions
+    for_rc(R, in0, [&](int r, int k) {
+        Real acc = 0;
+        for (int g = 0; g < QG; ++g) acc += upart[(g * R + r) * in0 + k];
+        ubar[r * ldx + k] = acc;
+    });
+
+    // ---- weight-gradient partials: every matrix of the tile, no barriers in between ----
+    Real* __restrict__ part = st.part + (size_t)tile * lay.P_pad;
+    gemm_wgrad<Real, R>(part + lay.c_outw, part + lay.c_outb, z, ldh, pbar, ldo, ldkh, H, O);
+    gemm_wgrad<Real, R>(part + lay.c_nlw, part + lay.c_nlb, cur, ldh, zb, ldh, ldkh, H, H);
+    for (int l = L - 1; l >= 0; --l)
+        gemm_wgrad<Real, R>(part + lay.cw[l], part + lay.cb[l], l == 0 ? xin : act + (l - 1) * R * ldh,
+                            l == 0 ? ldx : ldh, preb + l * R * ldg, ldg, lay.ldk[l], lay.layer_in[l], G);
+    __syncthreads();
+    DBG_CLK(st, 7);
 
     // ---- ES adjoint contributions per window (Div / Mul / BroadcastCol adjoints) ----
     // written in slot-major CSR order so each slot's windows are contiguous for K3
