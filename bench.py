@@ -351,20 +351,21 @@ def main():
     if not a.no_e2e:
         e2e_t = []
         h2d = d2h = 0
-        for _ in range(max(1, a.steps)):
+        for it in range(max(1, a.warmup) + max(1, a.steps)):
             barrier(world)
             t0 = time.perf_counter()
             t2 = Trainer((vals, cats), prof, cfg, api=api, dist=dist_arg)
             t2.train_epoch()
             v2 = t2.validate()
             t2.close()
-            e2e_t.append(time.perf_counter() - t0)
+            if it >= max(1, a.warmup):
+                e2e_t.append(time.perf_counter() - t0)
             rb = 4 if a.precision == "fp32" else 8
             h2d = n_local * length * rb + n_local * per * 3 * 4
             d2h = steps_per_epoch * 8 + v2.forecasts.nbytes + v2.smape_per_series.nbytes
         e2e_s = allreduce_max(sum(e2e_t), world)
         e2e = {"value": n_total * len(e2e_t) / e2e_s, "unit": "series/s", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": [1000 * x for x in e2e_t],
                "what": "Trainer(series) construction + train_epoch + validate + destroy per step, wall clock"}
 
     cpu = None

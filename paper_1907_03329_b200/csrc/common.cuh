@@ -10,6 +10,9 @@
 // the whole vector moves into shared memory with one TMA bulk copy.
 #pragma once
 #include <cstdint>
+#include <cfloat>
+#include <climits>
+#include <type_traits>
 
 #include "devmath.cuh"
 
@@ -66,9 +69,9 @@ struct StateDev {
     Real* lv;               // [T][kcap]
     Real* se;               // [T+S][kcap]
     Real* contrib;          // [Bcap][cwp] ES adjoint contributions per window, in slot-major
-                            // CSR order: [0,O) target seasonalities, [O,O+I) input
-                            // seasonalities, [O+I] anchor level
-    int cwp;                // row stride of contrib (multiple of 4 >= I+O+1)
+                            // CSR order: [0,I) input seasonalities, [I,I+O) target
+                            // seasonalities, [I+O] anchor level, [I+O+1] the anchor
+    int cwp;                // row stride of contrib (multiple of 4 >= I+O+2)
     Real* part;             // [tiles][P_pad]
     double* loss_part;      // [tiles]
     Real* gbuf;             // [P_pad + 2]  (comm buffer: grads | ps sq-norm | loss sum)
@@ -111,6 +114,17 @@ __device__ __forceinline__ T block_sum(T v, T* red) {
     __syncthreads();
     return r;  // valid in thread 0
 }
+
+// global-timer stamp (ns) into dbg_clk[80 + i], block 0 thread 0 (kernel start/end timeline)
+__device__ __forceinline__ long long gtimer() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define DBG_GT(st, i)                                                               \
+    do {                                                                            \
+        if ((st).dbg_clk && blockIdx.x == 0 && threadIdx.x == 0) (st).dbg_clk[80 + (i)] = gtimer(); \
+    } while (0)
 
 #define DBG_CLK(st, i)                                                              \
     do {                                                                            \
@@ -215,10 +229,28 @@ __host__ __device__ __forceinline__ int log2_ceil(int w) {
     return l;
 }
 
-// fp32 performance mode divides with the SFU reciprocal path; fp64 keeps IEEE division
+// fp32 performance mode divides with the SFU reciprocal (MUFU.RCP, <= 1 ulp, flush-to-zero;
+// the path's operands are positive levels/seasonalities of O(1e-3..1e6)); fp64 keeps IEEE
+// division, as the reference does
+__device__ __forceinline__ float rcp_fast(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
 template <typename Real>
 __device__ __forceinline__ Real fdiv(Real a, Real b) {
-    if constexpr (sizeof(Real) == 4) return __fdividef(a, b);
+    if constexpr (sizeof(Real) == 4) return a * rcp_fast(b);
+    else return a / b;
+}
+// a / b with a reciprocal the caller computed once (rb = rcp(b)); IEEE a / b in fp64
+template <typename Real>
+__device__ __forceinline__ Real rcp_of(Real b) {
+    if constexpr (sizeof(Real) == 4) return rcp_fast(b);
+    else return Real(1) / b;
+}
+template <typename Real>
+__device__ __forceinline__ Real fdiv_r(Real a, Real b, Real rb) {
+    if constexpr (sizeof(Real) == 4) return a * rb;
     else return a / b;
 }
 

@@ -255,7 +255,7 @@ struct esrnn_trainer {
         s.lv = reinterpret_cast<Real*>(lv.p);
         s.se = reinterpret_cast<Real*>(se.p);
         s.contrib = reinterpret_cast<Real*>(contrib.p);
-        s.cwp = (I + O + 1 + 3) & ~3;
+        s.cwp = (I + O + 2 + 3) & ~3;
         s.part = reinterpret_cast<Real*>(part.p);
         s.loss_part = loss_part.p;
         s.gbuf = reinterpret_cast<Real*>(gbuf.p);
@@ -508,7 +508,7 @@ void ensure_capacity(Eng* e, int B) {
     e->es_blocks = (kc + kEsSlotsPerBlock - 1) / kEsSlotsPerBlock;
     e->lv.alloc(r * T * kc);
     e->se.alloc(r * (T + S) * kc);
-    e->contrib.alloc(r * static_cast<size_t>(B) * ((I + O + 1 + 3) & ~3));
+    e->contrib.alloc(r * static_cast<size_t>(B) * ((I + O + 2 + 3) & ~3));
     // padding slots of the tile partials are never written: zero them once
     e->part.alloc(r * static_cast<size_t>(e->tiles_cap) * e->lay.P_pad);
     e->part.zero(e->stream);
@@ -622,7 +622,10 @@ int stack_threads(const NetLayout& lay) { return stack_threads_for_r<kRows>(lay)
 template <typename Real>
 size_t finish_smem(const NetLayout& lay) {
     // lb, sb, forward l and s columns [.][bd] + one staged observation row per slot
-    return sizeof(Real) * (static_cast<size_t>(4 * lay.T + lay.S) + row_pad<Real>(lay.T)) * kEsSlotsPerBlock;
+    // + one chunk of staged contribution rows
+    const size_t cwp = (lay.I + lay.O + 2 + 3) & ~3;
+    return sizeof(Real) * ((static_cast<size_t>(4 * lay.T + lay.S + 2) + row_pad<Real>(lay.T)) * kEsSlotsPerBlock +
+                           kEsChunk * cwp);
 }
 
 template <typename Real>
@@ -683,7 +686,8 @@ void launch_scan(Eng* e, int blocks, const StateDev<Real>& st, const PlanDev& pv
 
 template <typename Real, int SC>
 void launch_finish_sc(Eng* e, const StateDev<Real>& st, const PlanDev& pv, int s, int finalize) {
-    k_grad_finish<Real, kRows, SC><<<e->es_blocks + e->red_blocks, kFinishThreads, finish_smem<Real>(e->lay),
+    static const bool nored = std::getenv("ESRNN_DEBUG_NORED") != nullptr;  // timing experiments only
+    k_grad_finish<Real, kRows, SC><<<e->es_blocks + (nored ? 0 : e->red_blocks), kFinishThreads, finish_smem<Real>(e->lay),
                                      e->stream>>>(st, pv, e->lay, s, e->es_blocks, finalize);
 }
 template <typename Real>
@@ -779,7 +783,7 @@ void alloc_state(Eng* e) {
     e->net_step.alloc(1);
     e->errw.alloc(2);
     if (std::getenv("ESRNN_DEBUG_CLOCKS")) {
-        e->dbg_clk.alloc(64);
+        e->dbg_clk.alloc(96);
         e->dbg_clk.zero(e->stream);
     }
     for (auto* b : {&e->ps, &e->ps_m, &e->ps_v, &e->mW, &e->vW}) b->zero(e->stream);
@@ -900,7 +904,7 @@ double train_epoch_impl(Eng* e) {
     e->last_ms = ms;
     throw_device_error(e);
     if (e->dbg_clk.p) {
-        long long c[64];
+        long long c[96];
         CUDA_OK(cudaMemcpy(c, e->dbg_clk.p, sizeof c, cudaMemcpyDeviceToHost));
         std::fprintf(stderr, "[esrnn dbg] k_stack tile0 phase cycles:");
         for (int i = 1; i < 32 && c[i] > 0; ++i) std::fprintf(stderr, " %lld", c[i] - c[i - 1]);
@@ -909,6 +913,12 @@ double train_epoch_impl(Eng* e) {
         std::fprintf(stderr, "\n[esrnn dbg] grad_finish reduce block0:");
         for (int i = 49; i < 64 && c[i] > 0; ++i) std::fprintf(stderr, " %lld", c[i] - c[i - 1]);
         std::fprintf(stderr, "\n[esrnn dbg] reduce block0 start - ES block0 start: %lld\n", c[48] - c[32]);
+        std::fprintf(stderr, "[esrnn dbg] scan block0:");
+        for (int i = 65; i < 80 && c[i] > 0; ++i) std::fprintf(stderr, " %lld", c[i] - c[i - 1]);
+        std::fprintf(stderr, "\n[esrnn dbg] timeline ns (scan0 start, scan0 end, stack0 start, stack0 end, "
+                             "finish0 start, finish last, adam0 start) rel. scan start:");
+        for (int i = 80; i < 87; ++i) std::fprintf(stderr, " %lld", c[i] - c[80]);
+        std::fprintf(stderr, "\n");
     }
     e->last_wr = std::move(wr);
     e->last_wa = std::move(wa);

@@ -12,7 +12,8 @@
 namespace esrnn_dev {
 
 constexpr int kFinishThreads = 256;
-constexpr int kEsSlotsPerBlock = 64;  // ES blocks use warps 0-1 (64 slots), shared columns (2T+S)*64
+constexpr int kEsSlotsPerBlock = 32;  // ES blocks: warp 0 owns 32 slots; all warps stage the windows
+constexpr int kEsChunk = 128;         // contribution rows staged per round
 constexpr int kRedGroups = 8;         // tile groups per reduce block
 constexpr int kRedChunks = 2;         // 32-parameter chunks per reduce block
 
@@ -54,134 +55,183 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
         ++fdbg;
     };
     FCLK();
+    DBG_GT(st, 4);
     if (static_cast<int>(blockIdx.x) < es_blocks) {
         // ---------------- per-slot window-adjoint gather + reverse HW scan ---------------
         const int k0 = pl.step_slot_off[s];
         const int k = pl.step_slot_off[s + 1] - k0;
-        const int slot = blockIdx.x * kEsSlotsPerBlock + tid;
-        if (tid < kEsSlotsPerBlock && slot < k && st.attach) {
+        const int sl0 = blockIdx.x * kEsSlotsPerBlock;
+        const int sl1 = min(k, sl0 + kEsSlotsPerBlock);
+        if (sl0 < sl1 && st.attach) {  // uniform per block
             const int N = st.N, S = SC > 0 ? SC : lay.S, T = lay.T, I = lay.I, O = lay.O, kc = st.kcap;
-            const int bd = kEsSlotsPerBlock, tp = row_pad<Real>(T);
-            Real* lb = reinterpret_cast<Real*>(smem_raw) + tid;  // [T][bd]    level adjoint (window part)
-            Real* sb = lb + T * bd;                               // [T+S][bd]  seasonality adjoint
-            Real* lvs = sb + (T + S) * bd;                        // [T][bd]    forward levels
-            Real* ses = lvs + T * bd;                             // [T][bd]    forward seasonalities
-            Real* ys = reinterpret_cast<Real*>(smem_raw) + (4 * T + S) * bd + tid * tp;  // row
-            const int row = pl.slot_row[k0 + slot];
+            const int bd = kEsSlotsPerBlock, tp = row_pad<Real>(T), cwp = st.cwp;
+            const int slot = sl0 + tid;
+            const bool mine = tid < bd && slot < sl1;
+            const int lane = tid & 31;                                         // slot lane (bd == 32)
+            // window adjoints row-major per slot (odd strides: the per-slot reverse scan reads
+            // them conflict-free; the per-window warp scatter writes consecutive words)
+            const int ldl = T | 1, lds = (T + S) | 1;
+            Real* LB = reinterpret_cast<Real*>(smem_raw);                      // [bd][ldl] level adjoint
+            Real* SB = LB + bd * ldl;                                          // [bd][lds] seasonality adjoint
+            Real* LV = SB + bd * lds;                                          // [T][bd]   forward levels
+            Real* SE = LV + T * bd;                                            // [T][bd]   forward seasonalities
+            Real* YS = SE + T * bd;                                            // [bd][tp]  observation rows
+            Real* cbuf = YS + bd * tp;                                         // [kEsChunk][cwp]
+            Real* lb = LB + tid * ldl;
+            Real* sb = SB + tid * lds;
+            Real* lvs = LV + tid;
+            Real* ses = SE + tid;
+            Real* ys = YS + tid * tp;
             FCLK();
-            for (int t = 0; t < T; ++t) lb[t * bd] = 0;
-            for (int t = 0; t < T + S; ++t) sb[t * bd] = 0;
-            FCLK();
-            // this slot's windows are contiguous in the CSR-ordered contribution table:
-            // whole rows arrive as 16-byte loads, 16 values in flight at a time
+            // ---- stage the forward state with the whole block (every copy in flight at once) ----
+            const bool lane_ok = sl0 + lane < sl1;
+            const int lrow = lane_ok ? pl.slot_row[k0 + sl0 + lane] : 0;
+            Real a_raw = 0, g_raw = 0;
+            if (mine) {
+                a_raw = st.ps[lrow];
+                g_raw = st.ps[N + lrow];
+            }
+            constexpr int e16 = 16 / static_cast<int>(sizeof(Real));
+            if (lane_ok) {
+                for (int ch = tid >> 5; ch * e16 < tp; ch += kFinishThreads / 32)
+                    cp_async16(YS + lane * tp + ch * e16, st.vrm + (size_t)lrow * st.ldv + ch * e16);
+                for (int t = tid >> 5; t < T; t += kFinishThreads / 32) {
+                    cp_async_elem(LV + t * bd + lane, st.lv + (size_t)t * kc + sl0 + lane);
+                    cp_async_elem(SE + t * bd + lane, st.se + (size_t)t * kc + sl0 + lane);
+                }
+            }
+            // ---- window adjoints: this block's windows are one contiguous range of the
+            // CSR-ordered contribution table, staged in chunks of kEsChunk rows; then one warp
+            // per slot adds the slot's windows in CSR order, lanes over the window's
+            // contiguous run of seasonality indices [a-I+1, a+O] ----
             const int cb0 = pl.slot_win_off[k0];
-            const int wb = pl.slot_win_off[k0 + slot], we = pl.slot_win_off[k0 + slot + 1];
-            const int cwp = st.cwp, nv = O + I + 1;
-            for (int w = wb; w < we; ++w) {
-                const int a = __ldg(pl.csr_anchor + w);
-                const Real* __restrict__ cr = st.contrib + (size_t)(w - cb0) * cwp;
-                for (int j0 = 0; j0 < nv; j0 += 16) {
-                    Real v[16];
+            const int blo = pl.slot_win_off[k0 + sl0], bhi = pl.slot_win_off[k0 + sl1];
+            const int nio = I + O;
+            const int wq = tid >> 5;
+            for (int sl = wq; sl < bd; sl += kFinishThreads / 32) {
+                for (int t = lane; t < lds; t += 32) SB[sl * lds + t] = 0;
+                for (int t = lane; t < ldl; t += 32) LB[sl * ldl + t] = 0;
+            }
+            FCLK();
+            for (int clo = blo; clo < bhi; clo += kEsChunk) {
+                const int chi = min(bhi, clo + kEsChunk);
+                const Real* src = st.contrib + (size_t)(clo - cb0) * cwp;
+                const int nel = (chi - clo) * cwp;
+                for (int i = tid * e16; i < nel; i += kFinishThreads * e16) cp_async16(cbuf + i, src + i);
+                cp_async_wait_all();
+                __syncthreads();
+                FCLK();
+                for (int sl = wq; sl0 + sl < sl1 && sl < bd; sl += kFinishThreads / 32) {
+                    const int w_lo = max(pl.slot_win_off[k0 + sl0 + sl], clo);
+                    const int w_hi = min(pl.slot_win_off[k0 + sl0 + sl + 1], chi);
+                    Real* sbr = SB + sl * lds;
+                    for (int w = w_lo; w < w_hi; ++w) {
+                        const Real* c = cbuf + (w - clo) * cwp;
+                        const int a = static_cast<int>(c[nio + 1]);
+                        for (int j = lane; j < nio; j += 32) sbr[a - I + 1 + j] += c[j];
+                        if (lane == 0) LB[sl * ldl + a] += c[nio];
+                        __syncwarp();
+                    }
+                }
+                __syncthreads();
+            }
+            if (blo == bhi) {  // no windows (cannot happen for a slot in the step; kept total)
+                cp_async_wait_all();
+                __syncthreads();
+            }
+            FCLK();
+            if (mine) {
+                const Real alpha = M::logistic_ps(a_raw);
+                const Real gamma = M::logistic_ps(g_raw);
+                const Real oma = Real(1) - alpha, omg = Real(1) - gamma;
+                const int row = lrow;
+                cp_async_wait_all();
+                FCLK();
+                Real l0 = 0;
+                for (int j = 0; j < S; ++j) l0 += ys[j];
+                l0 = l0 / Real(S);
+                Real abar = 0, gbar = 0, omab = 0, omgb = 0;
+                Real lbn = lb[T - 1];  // running adjoint of l[t]
+                // one reverse step (t > 0 unless FIRST): Sb = final adjoint of s[t+S],
+                // returns the final adjoint of s[t]
+                auto step = [&](int t, Real Sb, auto first) -> Real {
+                    constexpr bool kFirst = decltype(first)::value;
+                    const Real yt = ys[t];
+                    const Real lp = kFirst ? l0 : lvs[(t - 1) * bd];
+                    const Real s_t = ses[t * bd];
+                    const Real rlp = rcp_of(lp), rst = rcp_of(s_t);
+                    Real sbt = sb[t];
+                    // s_{t+S} = gamma*(y/lp) + (1-gamma)*s_t
+                    omgb += Sb * s_t;
+                    sbt += Sb * omg;
+                    const Real d2 = fdiv_r(yt, lp, rlp);
+                    gbar += Sb * d2;
+                    // l_t = alpha*(y/s_t) + (1-alpha)*lp
+                    const Real Lb = lbn;
+                    omab += Lb * lp;
+                    const Real d1 = fdiv_r(yt, s_t, rst);
+                    abar += Lb * d1;
+                    sbt -= fdiv_r((Lb * alpha) * d1, s_t, rst);
+                    if constexpr (!kFirst) {
+                        const Real d2b = Sb * gamma;
+                        lbn = lb[t - 1] - fdiv_r(d2b * d2, lp, rlp) + Lb * oma;
+                    }
+                    return sbt;
+                };
+                using Mid = std::integral_constant<bool, false>;
+                using First = std::integral_constant<bool, true>;
+                Real sfin[SC > 0 ? SC : 1];
+                if constexpr (SC > 0) {
+                    // register ring: rg[j] holds the final adjoint of the latest s index = j (mod S);
+                    // full groups of SC steps are branch-free so consecutive steps interleave
+                    Real rg[SC];
 #pragma unroll
-                    for (int u = 0; u < 16; u += 4) {
-                        if (j0 + u < cwp) {
-                            const V4<Real> x = ldg4(cr + j0 + u);
-                            v[u] = x.x; v[u + 1] = x.y; v[u + 2] = x.z; v[u + 3] = x.w;
+                    for (int j = 0; j < SC; ++j) rg[j] = 0;  // s[T..T+S) receive no adjoint
+                    int base = ((T - 1) / SC) * SC;
+                    if (base > 0) {
+#pragma unroll
+                        for (int jj = SC - 1; jj >= 0; --jj)
+                            if (base + jj < T) rg[jj] = step(base + jj, rg[jj], Mid{});
+                        for (base -= SC; base > 0; base -= SC) {
+#pragma unroll
+                            for (int jj = SC - 1; jj >= 0; --jj) rg[jj] = step(base + jj, rg[jj], Mid{});
                         }
                     }
 #pragma unroll
-                    for (int u = 0; u < 16; ++u) {
-                        const int j = j0 + u;
-                        if (j < O) sb[(a + 1 + j) * bd] += v[u];
-                        else if (j < O + I) sb[(a - I + 1 + (j - O)) * bd] += v[u];
-                        else if (j == O + I) lb[a * bd] += v[u];
-                    }
-                }
-            }
-            // the forward state this reverse scan needs, all in flight at once
-            stage_row_async(ys, st.vrm + (size_t)row * st.ldv, T);
-#pragma unroll 4
-            for (int t = 0; t < T; ++t) {
-                cp_async_elem(lvs + t * bd, st.lv + (size_t)t * kc + slot);
-                cp_async_elem(ses + t * bd, st.se + (size_t)t * kc + slot);
-            }
-            const Real alpha = M::logistic_ps(st.ps[row]);
-            const Real gamma = M::logistic_ps(st.ps[N + row]);
-            const Real oma = Real(1) - alpha, omg = Real(1) - gamma;
-            FCLK();
-            cp_async_wait_all();
-            FCLK();
-            Real l0 = 0;
-            for (int j = 0; j < S; ++j) l0 += ys[j];
-            l0 = l0 / Real(S);
-            Real abar = 0, gbar = 0, omab = 0, omgb = 0;
-            Real lbn = lb[(T - 1) * bd];  // running adjoint of l[t]
-            // one reverse step: Sb = final adjoint of s[t+S], returns the final adjoint of s[t]
-            auto step = [&](int t, Real Sb) -> Real {
-                const Real yt = ys[t];
-                const Real lp = t > 0 ? lvs[(t - 1) * bd] : l0;
-                const Real s_t = ses[t * bd];
-                Real sbt = sb[t * bd];
-                // s_{t+S} = gamma*(y/lp) + (1-gamma)*s_t
-                omgb += Sb * s_t;
-                sbt += Sb * omg;
-                const Real d2 = fdiv(yt, lp);
-                gbar += Sb * d2;
-                const Real d2b = Sb * gamma;
-                Real lpb = t > 0 ? lb[(t - 1) * bd] : Real(0);
-                if (t > 0) lpb -= fdiv(d2b * d2, lp);
-                // l_t = alpha*(y/s_t) + (1-alpha)*lp
-                const Real Lb = lbn;
-                omab += Lb * lp;
-                if (t > 0) lpb += Lb * oma;
-                const Real d1 = fdiv(yt, s_t);
-                abar += Lb * d1;
-                sbt -= fdiv((Lb * alpha) * d1, s_t);
-                lbn = lpb;
-                return sbt;
-            };
-            Real sfin[SC > 0 ? SC : 1];
-            if constexpr (SC > 0) {
-                // register ring: rg[j] holds the final adjoint of the latest s index = j (mod S)
-                Real rg[SC];
+                    for (int jj = SC - 1; jj >= 1; --jj)
+                        if (jj < T) rg[jj] = step(jj, rg[jj], Mid{});
+                    rg[0] = step(0, rg[0], First{});
 #pragma unroll
-                for (int j = 0; j < SC; ++j) rg[j] = 0;  // s[T..T+S) receive no adjoint
-                for (int base = ((T + SC - 1) / SC - 1) * SC; base >= 0; base -= SC) {
-#pragma unroll
-                    for (int jj = SC - 1; jj >= 0; --jj) {
-                        const int t = base + jj;
-                        if (t < T) rg[jj] = step(t, rg[jj]);
-                    }
-                }
-#pragma unroll
-                for (int j = 0; j < SC; ++j) sfin[j] = rg[j];
-            } else {
-#pragma unroll 4
-                for (int t = T - 1; t >= 0; --t) sb[t * bd] = step(t, sb[(t + S) * bd]);
-            }
-            FCLK();
-            abar -= omab;
-            gbar -= omgb;
-            Real* o = st.psg + (size_t)slot * (2 + S);
-            const Real ga = abar * alpha * (Real(1) - alpha);
-            const Real gg = gbar * gamma * (Real(1) - gamma);
-            o[0] = ga;
-            o[1] = gg;
-            sq += static_cast<double>(ga) * ga + static_cast<double>(gg) * gg;
-            for (int j = 0; j < S; ++j) {
-                const Real sj = M::exp_ps(st.ps[(2 + j) * N + row]);
-                Real sbj;
-                if constexpr (SC > 0) {
-                    sbj = 0;
-#pragma unroll
-                    for (int jj = 0; jj < SC; ++jj)
-                        if (jj == j) sbj = sfin[jj];
+                    for (int j = 0; j < SC; ++j) sfin[j] = rg[j];
                 } else {
-                    sbj = sb[j * bd];
+#pragma unroll 4
+                    for (int t = T - 1; t >= 1; --t) sb[t] = step(t, sb[t + S], Mid{});
+                    sb[0] = step(0, sb[S], First{});
                 }
-                const Real g = sbj * sj;
-                o[2 + j] = g;
-                sq += static_cast<double>(g) * g;
+                FCLK();
+                abar -= omab;
+                gbar -= omgb;
+                Real* o = st.psg + (size_t)slot * (2 + S);
+                const Real ga = abar * alpha * (Real(1) - alpha);
+                const Real gg = gbar * gamma * (Real(1) - gamma);
+                o[0] = ga;
+                o[1] = gg;
+                sq += static_cast<double>(ga) * ga + static_cast<double>(gg) * gg;
+                for (int j = 0; j < S; ++j) {
+                    const Real sj = M::exp_ps(st.ps[(2 + j) * N + row]);
+                    Real sbj;
+                    if constexpr (SC > 0) {
+                        sbj = 0;
+#pragma unroll
+                        for (int jj = 0; jj < SC; ++jj)
+                            if (jj == j) sbj = sfin[jj];
+                    } else {
+                        sbj = sb[j];
+                    }
+                    const Real g = sbj * sj;
+                    o[2 + j] = g;
+                    sq += static_cast<double>(g) * g;
+                }
             }
         }
         const double tot = block_sum(sq, red);
@@ -239,23 +289,25 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
         last = (ticket == gridDim.x - 1);
     }
     __syncthreads();
-    if (!last || tid != 0) return;
+    if (!last) return;
     __threadfence();
+    if (tid == 0 && st.dbg_clk) st.dbg_clk[85] = gtimer();
+    // all threads sum the per-block parts (strided, then a fixed tree): L2 loads in flight at once
     const int nrb = gridDim.x - es_blocks;
     const int w0 = pl.step_win_off[s];
     const int nt = (pl.step_win_off[s + 1] - w0 + R - 1) / R;
-    double es = 0.0;
+    double es = 0.0, ls = 0.0, all = 0.0;
     if (st.attach)
-        for (int b = 0; b < es_blocks; ++b) es += *reinterpret_cast<volatile double*>(st.es_sq_part + b);
-    double ls = 0.0;
-    for (int t = 0; t < nt; ++t) ls += st.loss_part[t];
+        for (int b = tid; b < es_blocks; b += kFinishThreads) es += __ldcg(st.es_sq_part + b);
+    for (int t = tid; t < nt; t += kFinishThreads) ls += __ldcg(st.loss_part + t);
+    for (int b = tid; b < nrb; b += kFinishThreads) all += __ldcg(st.red_sq_part + b);
+    es = block_sum(es, red);
+    ls = block_sum(ls, red);
+    all = block_sum(all, red);
+    if (tid != 0) return;
     st.gbuf[lay.P_pad] = static_cast<Real>(es);
     st.gbuf[lay.P_pad + 1] = static_cast<Real>(ls);
-    if (finalize & 1) {
-        double all = 0.0;
-        for (int b = 0; b < nrb; ++b) all += *reinterpret_cast<volatile double*>(st.red_sq_part + b);
-        finalize_scalars(st, pl, s, all + es, ls, (finalize & 2) != 0);
-    }
+    if (finalize & 1) finalize_scalars(st, pl, s, all + es, ls, (finalize & 2) != 0);
     *st.done_ctr = 0;
 }
 
@@ -277,10 +329,12 @@ __global__ void __launch_bounds__(256) k_finalize(StateDev<Real> st, PlanDev pl,
         last = atomicAdd(st.done_ctr + 1, 1u) == gridDim.x - 1;
     }
     __syncthreads();
-    if (!last || threadIdx.x != 0) return;
+    if (!last) return;
     __threadfence();
     double all = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) all += *reinterpret_cast<volatile double*>(st.red_sq_part + b);
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) all += __ldcg(st.red_sq_part + b);
+    all = block_sum(all, red);
+    if (threadIdx.x != 0) return;
     const double es = st.attach ? static_cast<double>(st.gbuf[lay.P_pad]) : 0.0;
     finalize_scalars(st, pl, s, all + es, static_cast<double>(st.gbuf[lay.P_pad + 1]), advance != 0);
     st.done_ctr[1] = 0;
@@ -297,6 +351,7 @@ __device__ __forceinline__ void adam_update(double& theta, double& m, double& v,
 
 template <typename Real>
 __global__ void __launch_bounds__(256) k_adam(StateDev<Real> st, PlanDev pl, NetLayout lay, int s) {
+    DBG_GT(st, 6);
     if (st.err[0] != 0) return;  // the reference throws before apply_updates
     const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (q < lay.P_pad) {

@@ -32,6 +32,13 @@ template <typename Real, int SC>
 __global__ void __launch_bounds__(kScanThreads) k_scan_fwd(StateDev<Real> st, PlanDev pl, NetLayout lay, int s) {
     using M = Math<Real>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
+    int sdbg = 64;
+    auto SCLK = [&]() {
+        if (st.dbg_clk && blockIdx.x == 0 && threadIdx.x == 0) st.dbg_clk[sdbg] = clock64();
+        ++sdbg;
+    };
+    SCLK();
+    DBG_GT(st, 0);
     const int k0 = pl.step_slot_off[s];
     const int k = pl.step_slot_off[s + 1] - k0;
     const int slot = blockIdx.x * blockDim.x + threadIdx.x;
@@ -42,17 +49,20 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_fwd(StateDev<Real> st, Pl
     Real* ring = reinterpret_cast<Real*>(smem_raw) + tid;
     Real* ys = reinterpret_cast<Real*>(smem_raw) + S * bd + tid * tp;
     const int row = pl.slot_row[k0 + slot];
+    SCLK();
     // the observation row and the per-series parameters, all in flight at once
     stage_row_async(ys, st.vrm + (size_t)row * st.ldv, T);
     for (int j = 0; j < S; ++j) cp_async_elem(ring + j * bd, st.ps + (size_t)(2 + j) * N + row);
     const Real alpha = M::logistic_ps(st.ps[row]);
     const Real gamma = M::logistic_ps(st.ps[N + row]);
     const Real oma = Real(1) - alpha, omg = Real(1) - gamma;
+    SCLK();
     cp_async_wait_all();
+    SCLK();
     Real* __restrict__ se = st.se + slot;
     Real* __restrict__ lv = st.lv + slot;
     Real lp = 0;
-    int bad = -1;
+    int bad = INT_MAX;  // first step with a non-positive / non-finite level (branch-free min)
     if constexpr (SC > 0) {
         Real rg[SC];
 #pragma unroll
@@ -62,21 +72,26 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_fwd(StateDev<Real> st, Pl
             lp += ys[j];
         }
         lp = lp / Real(SC);
-        for (int t0 = 0; t0 < T; t0 += SC) {
+        // one step: l_t = a*y/s_t + (1-a)*l_{t-1};  s_{t+S} = g*y/l_{t-1} + (1-g)*s_t
+        auto step = [&](int t, Real& sj) {
+            const Real yt = ys[t];
+            const Real l = alpha * fdiv(yt, sj) + oma * lp;
+            const bool ok = (l > Real(0)) & (l <= (sizeof(Real) == 4 ? Real(FLT_MAX) : Real(DBL_MAX)));
+            bad = min(bad, ok ? INT_MAX : t);
+            sj = gamma * fdiv(yt, lp) + omg * sj;
+            se[(t + SC) * kc] = sj;
+            lv[t * kc] = l;
+            lp = l;
+        };
+        // full groups of SC steps are branch-free, so consecutive steps interleave
+        int t0 = 0;
+        for (; t0 + SC <= T; t0 += SC) {
 #pragma unroll
-            for (int j = 0; j < SC; ++j) {
-                const int t = t0 + j;
-                if (t < T) {
-                    const Real yt = ys[t];
-                    const Real l = alpha * fdiv(yt, rg[j]) + oma * lp;
-                    if (!(l > Real(0)) || !isfinite(l)) bad = bad < 0 ? t : bad;
-                    rg[j] = gamma * fdiv(yt, lp) + omg * rg[j];
-                    se[(t + SC) * kc] = rg[j];
-                    lv[t * kc] = l;
-                    lp = l;
-                }
-            }
+            for (int j = 0; j < SC; ++j) step(t0 + j, rg[j]);
         }
+#pragma unroll
+        for (int j = 0; j < SC; ++j)
+            if (t0 + j < T) step(t0 + j, rg[j]);
     } else {
         for (int j = 0; j < S; ++j) {
             const Real s0 = M::exp_ps(ring[j * bd]);
@@ -91,7 +106,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_fwd(StateDev<Real> st, Pl
             const Real yt = ys[t];
             const Real s_t = ring[j * bd];
             const Real l = alpha * fdiv(yt, s_t) + oma * lp;
-            if (!(l > Real(0)) || !isfinite(l)) bad = bad < 0 ? t : bad;
+            if (!(l > Real(0)) || !isfinite(l)) bad = min(bad, t);
             const Real sn = gamma * fdiv(yt, lp) + omg * s_t;
             ring[j * bd] = sn;
             se[(t + S) * kc] = sn;
@@ -100,7 +115,9 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_fwd(StateDev<Real> st, Pl
             j = (j + 1 == S) ? 0 : j + 1;
         }
     }
-    if (bad >= 0) flag_error(st.err, kErrTrainLevel, bad);
+    SCLK();
+    DBG_GT(st, 1);
+    if (bad != INT_MAX) flag_error(st.err, kErrTrainLevel, bad);
 }
 
 // ------------------------------------------------------------------------------ K6

@@ -386,6 +386,7 @@ __global__ void __launch_bounds__(512) k_stack(StateDev<Real> st, PlanDev pl, Ne
     }
     if (nrows <= 0) return;
     int _dbg = 0;
+    if (MODE == kTrain) DBG_GT(st, 2);
     DBG_CLK(st, 0);
 
     // ---- weights: TMA bulk copy of the compact parameter vector (resident mode) ----
@@ -599,29 +600,32 @@ __global__ void __launch_bounds__(512) k_stack(StateDev<Real> st, PlanDev pl, Ne
     DBG_CLK(st, 7);
 
     // ---- ES adjoint contributions per window (Div / Mul / BroadcastCol adjoints) ----
-    // written in slot-major CSR order so each slot's windows are contiguous for K3
+    // written in slot-major CSR order so each slot's windows are contiguous for K3;
+    // row = [inputs (s index a-I+1..a) | targets (a+1..a+O) | level a | anchor a]
     if (st.attach) {
         for (int r = tid; r < nrows; r += NT) {
             Real* __restrict__ cr = st.contrib + (size_t)pl.w_csr[w0 + tile * R + r] * st.cwp;
+            cr[I + O + 1] = static_cast<Real>(pl.w_anchor[w0 + tile * R + r]);  // exact (< 2^24)
             const Real lv = lvl[r];
             Real acc_o = 0;
             for (int j = 0; j < O; ++j) {
                 const Real tb = -pbar[r * ldo + j];
                 const Real den = s_out[r * ldo + j] * lv;
                 const Real denb = -fdiv(tb * tgt[r * ldo + j], den);
-                cr[j] = denb * lv;
+                cr[I + j] = denb * lv;
                 acc_o += denb * s_out[r * ldo + j];
             }
             Real acc_i = 0;
             for (int j = 0; j < I; ++j) {
                 const Real den = s_in[r * I + j] * lv;
                 const Real denb = -fdiv(ubar[r * ldx + j] * xin[r * ldx + j], den);
-                cr[O + j] = denb * lv;
+                cr[j] = denb * lv;
                 acc_i += denb * s_in[r * I + j];
             }
             cr[O + I] = acc_o + acc_i;
         }
     }
+    if (MODE == kTrain) DBG_GT(st, 3);
 }
 
 }  // namespace esrnn_dev
