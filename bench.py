@@ -326,12 +326,12 @@ def main():
     per = T - prof.horizon - prof.input_window + 1
     steps_per_epoch = -(-n_total * per // B)
     B_local = B // world
-    if dom in ("stack",):
+    if dom in ("tile",):
         flops = lstm_flops_per_step(prof, B_local)
         avg_s = shares[dom]["ms"] / shares[dom]["launches"] / 1e3
         achieved = flops / avg_s / 1e12
         peak = fp32_peak if a.precision == "fp32" else fp32_peak / 2
-        roof = {"kernel": "k_stack (fused window+LSTM fwd/bwd+pinball)", "bound": "fp32-fma",
+        roof = {"kernel": "k_tile (fused HW scan + window + LSTM fwd/bwd + pinball)", "bound": "fp32-fma",
                 "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
                 "peak_source": f"derived CUDA-core FP32 FMA peak: 148 SM x 128 lanes x 2 x {sm_max:.0f} MHz "
                                f"(MEASURED_PEAKS sm_max_mhz); no tensor-core path (fp32 contract)",

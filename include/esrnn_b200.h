@@ -208,11 +208,18 @@ esrnn_status esrnn_trainer_kernel_launches(const esrnn_trainer* t, int64_t* n);
  * train_epoch / run_batch / forecast launch kernels directly (no CUDA graph) with a CUDA
  * event pair around every launch on the engine stream; kernel_times returns, per kernel
  * class, the summed milliseconds and launch counts since the last reset.
- * Classes: 0 scan_fwd, 1 stack(train/loss), 2 es_bwd, 3 net_reduce, 4 adam, 5 finalize,
- * 6 forecast_scan, 7 stack(forecast). */
+ * Classes: 0 (unused: the training scan runs inside the tile kernel), 1 tile (scan +
+ * window + stack fwd/bwd + loss), 2 finish (ES backward + weight-gradient contraction),
+ * 3 (unused), 4 adam, 5 finalize, 6 forecast_scan, 7 tile (forecast). */
 #define ESRNN_KERNEL_CLASSES 8
 esrnn_status esrnn_trainer_profile_kernels(esrnn_trainer* t, int32_t enable);
 esrnn_status esrnn_trainer_kernel_times(esrnn_trainer* t, double* total_ms, int64_t* launches);
+
+/* The engine keeps freed device / pinned-host blocks and instantiated epoch graphs in
+ * process-wide caches so that re-creating a trainer of the same configuration allocates
+ * and captures nothing; this returns every cached block to CUDA and drops the cached
+ * graphs (live trainers keep theirs).  No-op in the CPU oracles. */
+esrnn_status esrnn_release_cached_memory(void);
 
 /* NCCL bootstrap for esrnn_dist (returns ESRNN_NCCL_ERROR in builds without NCCL). */
 esrnn_status esrnn_nccl_unique_id(uint8_t out[128]);

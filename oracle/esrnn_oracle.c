@@ -1108,6 +1108,8 @@ esrnn_status esrnn_trainer_kernel_times(esrnn_trainer* t, double* total_ms, int6
     return ESRNN_OK;
 }
 
+esrnn_status esrnn_release_cached_memory(void) { return ESRNN_OK; }
+
 esrnn_status esrnn_nccl_unique_id(uint8_t out[128]) {
     (void)out;
     snprintf(g_create_err, sizeof g_create_err, "oracle: no NCCL");

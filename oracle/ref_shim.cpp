@@ -372,6 +372,8 @@ esrnn_status esrnn_trainer_kernel_times(esrnn_trainer*, double* total_ms, int64_
     return ESRNN_OK;
 }
 
+esrnn_status esrnn_release_cached_memory(void) { return ESRNN_OK; }
+
 esrnn_status esrnn_nccl_unique_id(uint8_t*) {
     g_create_err = "reference shim: no NCCL";
     return ESRNN_NCCL_ERROR;

@@ -132,13 +132,15 @@ class NativeApi:
         L.esrnn_trainer_profile_kernels.argtypes = [_vp, C.c_int32]
         L.esrnn_trainer_kernel_times.argtypes = [_vp, _dp, C.POINTER(C.c_int64)]
         L.esrnn_nccl_unique_id.argtypes = [C.POINTER(C.c_uint8)]
+        L.esrnn_release_cached_memory.argtypes = []
         L.esrnn_make_synthetic.argtypes = [C.c_uint64, C.c_int64, C.c_int32, C.c_int32, C.c_double, _dp, _ip]
         for fn in ("esrnn_trainer_create", "esrnn_trainer_shard", "esrnn_trainer_param_count",
                    "esrnn_trainer_param_info", "esrnn_trainer_get_weights", "esrnn_trainer_set_weights",
                    "esrnn_trainer_get_per_series", "esrnn_trainer_set_per_series", "esrnn_trainer_train_epoch",
                    "esrnn_trainer_run_batch", "esrnn_trainer_forecast", "esrnn_trainer_validate",
                    "esrnn_trainer_hw_state", "esrnn_trainer_last_device_ms", "esrnn_trainer_last_epoch_windows", "esrnn_trainer_kernel_launches",
-                   "esrnn_trainer_profile_kernels", "esrnn_trainer_kernel_times", "esrnn_nccl_unique_id", "esrnn_make_synthetic"):
+                   "esrnn_trainer_profile_kernels", "esrnn_trainer_kernel_times", "esrnn_nccl_unique_id", "esrnn_make_synthetic",
+                   "esrnn_release_cached_memory"):
             getattr(L, fn).restype = C.c_int
 
     @property
@@ -157,6 +159,10 @@ class NativeApi:
         cats = np.zeros(n, dtype=np.int32)
         self.check(self.lib.esrnn_make_synthetic(seed, n, length, season_length, noise_sigma, dptr(vals), iptr(cats)))
         return vals, cats
+
+    def release_cached_memory(self) -> None:
+        """Return the engine's cached device / pinned blocks and epoch graphs to CUDA."""
+        self.check(self.lib.esrnn_release_cached_memory())
 
     def nccl_unique_id(self) -> bytes:
         buf = (C.c_uint8 * 128)()

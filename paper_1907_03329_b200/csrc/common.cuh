@@ -19,19 +19,35 @@
 namespace esrnn_dev {
 
 constexpr int kMaxLayers = 16;
+constexpr int kMaxMats = kMaxLayers + 2;
+
+// One weight matrix of the K3 gradient contraction G[q][k] = sum_b A[b][q] * U[b][k]
+// (A, U: columns of the row store), written into W^T at cw (row stride ldk) and its bias
+// gradient sum_b A[b][q] at cb.
+struct MatDesc {
+    int a_off, Q, u_off, K, ldk, pad_;
+    long long cw, cb;
+};
 
 struct NetLayout {
     int L, nb, H, O, I, S, in0, T;
     int ldx, ldh, ldg, ldo;      // padded (multiple of 4) row strides: x, hidden, 3H gates, horizon
-    int ldkh;                    // odd row stride of the transposed head matrices (>= H)
+    int ldkh;                    // row stride of the transposed head matrices (8 * odd >= H)
     int layer_in[kMaxLayers];
-    int ldk[kMaxLayers];         // odd row stride of layer l's transposed input matrix (>= in_l)
+    int ldk[kMaxLayers];         // row stride of layer l's transposed input matrix (8 * odd >= in_l)
     int res_src[kMaxLayers];     // >=0: layer output added as residual after this layer
     int block_first[kMaxLayers]; // 1 if layer is the first of a block b>0 (adjoint joins the residual)
     int block_last[kMaxLayers];  // 1 if layer is the last of a block b>0 (residual added here)
     long long cw[kMaxLayers], cb[kMaxLayers];  // WT_l [3H][ldk_l], bias_l [3H]
     long long c_nlw, c_nlb, c_outw, c_outb;     // nl_w^T [H][ldkh], nl_b [H], out_w^T [O][ldkh], out_b [O]
     long long P_live, P_pad;
+    // per-window row store written by K2 for K3 (Real units, offsets multiples of 4):
+    // x | h_0..h_{L-1} | z | pre_bar_0..pre_bar_{L-1} (i, g, o) | z_bar | pred_bar
+    int rs_ld, rs_x, rs_z, rs_zb, rs_pb;
+    int rs_h[kMaxLayers], rs_pr[kMaxLayers];
+    int nmat;                      // L + 2 (layers, nl head, out head)
+    int mat_blk0[kMaxMats + 1];    // prefix of K3 GEMM blocks per matrix
+    MatDesc mats[kMaxMats];
 };
 
 // Per-epoch (or single-batch) plan: windows in global batch order, filtered to the
@@ -40,6 +56,7 @@ struct PlanDev {
     const int* w_row;         // local row of each window
     const int* w_anchor;
     const int* w_slot;        // slot within its step
+    const int* w_first;       // 1 if the window is its slot's first in batch order
     const int* step_win_off;  // [steps+1]
     const int* step_slot_off; // [steps+1]
     const int* slot_row;      // local row of each slot
@@ -72,7 +89,7 @@ struct StateDev {
                             // CSR order: [0,I) input seasonalities, [I,I+O) target
                             // seasonalities, [I+O] anchor level, [I+O+1] the anchor
     int cwp;                // row stride of contrib (multiple of 4 >= I+O+2)
-    Real* part;             // [tiles][P_pad]
+    Real* rowstore;         // [Bcap][rs_ld] per-window K3 operands (NetLayout rs_*)
     double* loss_part;      // [tiles]
     Real* gbuf;             // [P_pad + 2]  (comm buffer: grads | ps sq-norm | loss sum)
     Real* psg;              // [kcap][2+S]
@@ -199,6 +216,11 @@ __device__ __forceinline__ void cp_async_elem(Real* smem, const Real* gmem) {
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(smem)), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(smem)), "l"(gmem) : "memory");
 }

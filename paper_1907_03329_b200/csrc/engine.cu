@@ -16,16 +16,22 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
+#include <chrono>
+#include <list>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "esrnn_b200.h"
 #include "finish.cuh"
 #include "scan.cuh"
-#include "stack.cuh"
+#include "tile.cuh"
 
 using namespace esrnn_dev;
 
@@ -70,21 +76,71 @@ struct HostRng {
     uint64_t below(uint64_t n) { return static_cast<uint64_t>((static_cast<unsigned __int128>(gen()) * n) >> 64); }
 };
 
+// ------------------------------------------------------------------ caching allocator
+// Process-wide free lists of device and pinned-host blocks, keyed by (device, size class).
+// A freed buffer is kept for the next request of its class, so re-creating a trainer of
+// the same configuration costs no cudaMalloc / cudaFree (which synchronise the device and
+// can take milliseconds) and gets the same addresses back (which lets the epoch graph be
+// reused, see GraphCache).  esrnn_release_cached_memory() returns the blocks to CUDA.
+struct BlockCache {
+    std::mutex mu;
+    std::map<std::pair<int, size_t>, std::vector<void*>> dev, host;
+};
+BlockCache& block_cache() {
+    static BlockCache* c = new BlockCache;  // never destroyed: no CUDA calls at exit
+    return *c;
+}
+size_t size_class(size_t bytes) { return (bytes + 4095) & ~static_cast<size_t>(4095); }
+int current_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d;
+}
+void* cache_get(bool host, size_t cls) {
+    BlockCache& c = block_cache();
+    const int dev = host ? -1 : current_device();
+    {
+        std::lock_guard<std::mutex> g(c.mu);
+        auto& m = host ? c.host : c.dev;
+        auto it = m.find({dev, cls});
+        if (it != m.end() && !it->second.empty()) {
+            void* p = it->second.back();
+            it->second.pop_back();
+            return p;
+        }
+    }
+    void* p = nullptr;
+    if (host)
+        CUDA_OK(cudaMallocHost(&p, cls));
+    else
+        CUDA_OK(cudaMalloc(&p, cls));
+    return p;
+}
+void cache_put(bool host, void* p, size_t cls) {
+    BlockCache& c = block_cache();
+    std::lock_guard<std::mutex> g(c.mu);
+    (host ? c.host : c.dev)[{host ? -1 : current_device(), cls}].push_back(p);
+}
+
 // ------------------------------------------------------------------ device buffer
+std::atomic<uint64_t> g_alloc_seq{0};
+
 template <typename T>
 struct DBuf {
     T* p = nullptr;
     size_t n = 0;
+    uint64_t seq = 0;  // allocation order (the owner frees in reverse, see release_buffers)
     void alloc(size_t count) {
         free();
         n = count;
-        if (count) CUDA_OK(cudaMalloc(&p, sizeof(T) * count));
+        seq = ++g_alloc_seq;
+        if (count) p = static_cast<T*>(cache_get(false, size_class(sizeof(T) * count)));
     }
     void zero(cudaStream_t s) {
         if (n) CUDA_OK(cudaMemsetAsync(p, 0, sizeof(T) * n, s));
     }
     void free() {
-        if (p) cudaFree(p);
+        if (p) cache_put(false, p, size_class(sizeof(T) * n));
         p = nullptr;
         n = 0;
     }
@@ -97,33 +153,88 @@ struct PinnedBuf {
     size_t n = 0;
     void reserve(size_t count) {
         if (count <= n) return;
-        if (p) cudaFreeHost(p);
-        CUDA_OK(cudaMallocHost(&p, sizeof(T) * count));
-        n = count;
+        release();
+        p = static_cast<T*>(cache_get(true, size_class(sizeof(T) * count)));
+        n = size_class(sizeof(T) * count) / sizeof(T);
     }
-    ~PinnedBuf() {
-        if (p) cudaFreeHost(p);
+    void release() {
+        if (p) cache_put(true, p, size_class(sizeof(T) * n));
+        p = nullptr;
+        n = 0;
+    }
+    ~PinnedBuf() { release(); }
+};
+
+// ------------------------------------------------------------------ graph cache
+// Epoch graphs keyed by the exact bytes of every launch argument they capture.  With the
+// caching allocator a re-created trainer of the same configuration reproduces the key, and
+// its first epoch replays the instantiated graph instead of capturing a new one.
+struct GraphExec {
+    cudaGraphExec_t g = nullptr;
+    int launch_nodes = 0;
+    ~GraphExec() {
+        if (g) cudaGraphExecDestroy(g);
     }
 };
+struct GraphCache {
+    std::mutex mu;
+    std::list<std::pair<std::string, std::shared_ptr<GraphExec>>> lru;  // front = newest
+    static constexpr size_t kMax = 16;
+    std::shared_ptr<GraphExec> find(const std::string& key) {
+        std::lock_guard<std::mutex> g(mu);
+        for (auto it = lru.begin(); it != lru.end(); ++it)
+            if (it->first == key) {
+                lru.splice(lru.begin(), lru, it);
+                return it->second;
+            }
+        return nullptr;
+    }
+    void insert(const std::string& key, std::shared_ptr<GraphExec> ge) {
+        std::lock_guard<std::mutex> g(mu);
+        lru.emplace_front(key, std::move(ge));
+        if (lru.size() > kMax) lru.pop_back();  // live trainers keep their own reference
+    }
+    void clear() {
+        std::lock_guard<std::mutex> g(mu);
+        lru.clear();
+    }
+};
+GraphCache& graph_cache() {
+    static GraphCache* c = new GraphCache;  // never destroyed: no CUDA calls at exit
+    return *c;
+}
+template <typename T>
+void key_append(std::string& k, const T& v) {
+    k.append(reinterpret_cast<const char*>(&v), sizeof v);
+}
 
 // One plan = ordered local windows + per-step slot lists + per-slot window CSR.
 struct HostPlan {
-    std::vector<int> w_row, w_anchor, w_slot, step_win_off, step_slot_off, slot_row, slot_win_off, slot_win, w_csr,
+    std::vector<int> w_row, w_anchor, w_slot, w_first, step_win_off, step_slot_off, slot_row, slot_win_off, slot_win, w_csr,
         csr_anchor;
     std::vector<double> step_M;
     int max_step_windows = 0, max_step_slots = 0;
 };
 
+// One epoch's host plan: the global shuffled window order and this rank's step plan.
+struct EpochPlan {
+    std::vector<int> wr, wa;
+    HostPlan hp;
+    int steps = 0;
+    bool ready = false;
+};
+
 struct DevPlan {
-    DBuf<int> w_row, w_anchor, w_slot, step_win_off, step_slot_off, slot_row, slot_win_off, slot_win, w_csr, csr_anchor;
+    DBuf<int> w_row, w_anchor, w_slot, w_first, step_win_off, step_slot_off, slot_row, slot_win_off, slot_win, w_csr, csr_anchor;
     DBuf<double> step_M;
     DBuf<unsigned char> mask;
     size_t cap_w = 0, cap_steps = 0, cap_slots = 0;
     PlanDev view(bool with_mask) const {
-        PlanDev p;
+        PlanDev p{};
         p.w_row = w_row.p;
         p.w_anchor = w_anchor.p;
         p.w_slot = w_slot.p;
+        p.w_first = w_first.p;
         p.step_win_off = step_win_off.p;
         p.step_slot_off = step_slot_off.p;
         p.slot_row = slot_row.p;
@@ -137,7 +248,7 @@ struct DevPlan {
     }
 };
 
-constexpr int kRows = 8;          // windows per K2 tile
+constexpr int kRows = kR;         // windows per K2 tile
 
 }  // namespace
 
@@ -172,7 +283,7 @@ struct esrnn_trainer {
     int ldv = 0;  // row stride of the row-major value copy (16-byte multiple)
     DBuf<signed char> cat;
     DBuf<int> ps_steps;
-    DBuf<unsigned char> lv, se, contrib, part, gbuf, psg, d_inputs, d_targets, d_seas, d_levels;
+    DBuf<unsigned char> lv, se, contrib, rowstore, gbuf, psg, d_inputs, d_targets, d_seas, d_levels;
     DBuf<unsigned char> fX, fL, fS, dump_lv, dump_se;
     DBuf<double> loss_part, es_sq_part, red_sq_part, scal, loss_hist, f_out, f_smape, smape_sum;
     DBuf<unsigned int> done_ctr;
@@ -182,14 +293,14 @@ struct esrnn_trainer {
     int Bcap = 0, kcap = 0, tiles_cap = 0, es_blocks = 0, red_blocks = 0, steps_cap = 0;
 
     DevPlan epoch_plan, batch_plan;
-    HostPlan hp;
+    EpochPlan cur_plan, next_plan;
+    std::thread plan_thread;  // builds the first epoch's plan while create finishes
     std::vector<int> last_wr, last_wa;  // global window order of the last train_epoch
     PinnedBuf<int> pin_i;
     PinnedBuf<double> pin_d;
 
-    cudaGraphExec_t graph = nullptr;
-    int graph_steps = 0;
-    int graph_launch_nodes = 0;
+    std::shared_ptr<GraphExec> graph;  // epoch graph (shared with the process-wide cache)
+    std::string graph_key;
 
     // per-kernel event timing (esrnn_trainer_profile_kernels)
     bool profiling = false;
@@ -227,8 +338,36 @@ struct esrnn_trainer {
         prof_cls.clear();
     }
 
+    // Return every device buffer to the block cache in reverse allocation order: the cache is
+    // LIFO per size class, so a trainer that repeats this one's allocation sequence gets the
+    // same addresses back (and with them the cached epoch graph).
+    void release_buffers() {
+        std::vector<std::pair<uint64_t, std::function<void()>>> v;
+        auto add = [&](auto&... bs) {
+            (([&](auto& b) {
+                 if (b.p) v.emplace_back(b.seq, [&b] { b.free(); });
+             }(bs)),
+             ...);
+        };
+        add(vals, vrm, ps, ps_m, ps_v, theta, mW, vW, cat, ps_steps, lv, se, contrib, rowstore, gbuf, psg, d_inputs,
+            d_targets, d_seas, d_levels, fX, fL, fS, dump_lv, dump_se, loss_part, es_sq_part, red_sq_part, scal,
+            loss_hist, f_out, f_smape, smape_sum, done_ctr, net_step, dbg_clk, errw);
+        for (DevPlan* d : {&epoch_plan, &batch_plan})
+            add(d->w_row, d->w_anchor, d->w_slot, d->w_first, d->step_win_off, d->step_slot_off, d->slot_row,
+                d->slot_win_off, d->slot_win, d->w_csr, d->csr_anchor, d->step_M, d->mask);
+        std::sort(v.begin(), v.end(), [](const auto& a, const auto& b) { return a.first > b.first; });
+        for (auto& kv : v) kv.second();
+    }
+
+    void join_plan() {
+        if (plan_thread.joinable()) plan_thread.join();
+    }
+
     ~esrnn_trainer() {
-        if (graph) cudaGraphExecDestroy(graph);
+        join_plan();
+        if (stream) cudaStreamSynchronize(stream);  // buffers go back to the block cache below
+        release_buffers();
+        graph.reset();
         if (comm) ncclCommDestroy(comm);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
@@ -256,7 +395,7 @@ struct esrnn_trainer {
         s.se = reinterpret_cast<Real*>(se.p);
         s.contrib = reinterpret_cast<Real*>(contrib.p);
         s.cwp = (I + O + 2 + 3) & ~3;
-        s.part = reinterpret_cast<Real*>(part.p);
+        s.rowstore = reinterpret_cast<Real*>(rowstore.p);
         s.loss_part = loss_part.p;
         s.gbuf = reinterpret_cast<Real*>(gbuf.p);
         s.psg = reinterpret_cast<Real*>(psg.p);
@@ -354,6 +493,13 @@ void throw_device_error(Eng* e) {
 }
 
 // ------------------------------------------------------------------ layout
+// W^T row stride: a multiple of 8 with an odd quotient (conflict-free for both K2 products)
+int ld8odd(int n) {
+    int p = (n + 7) & ~7;
+    if (((p >> 3) & 1) == 0) p += 8;
+    return p;
+}
+
 void build_layout(Eng* e) {
     const int H = e->H, O = e->O;
     int64_t off = 0, coff = 0;
@@ -396,9 +542,9 @@ void build_layout(Eng* e) {
             e->off_bias[layer] = off;
             off += 4 * H;
             // compact live layout: W^T over the live gate columns [i | g | o] (forget gate
-            // dead) with an odd row stride ldk >= in (pad columns -> -1), then the bias
+            // dead) with row stride ldk = 8 * odd >= in (pad columns -> -1), then the bias
             pad4();
-            const int ldk = in | 1;
+            const int ldk = ld8odd(in);
             lay.ldk[layer] = ldk;
             lay.cw[layer] = coff;
             for (int q = 0; q < 3 * H; ++q) {
@@ -414,7 +560,7 @@ void build_layout(Eng* e) {
     }
     lay.ldg = (3 * H + 3) & ~3;
     lay.ldo = (O + 3) & ~3;
-    lay.ldkh = H | 1;
+    lay.ldkh = ld8odd(H);
     e->off_nlw = off;
     off += static_cast<int64_t>(H) * H;
     e->off_nlb = off;
@@ -445,6 +591,40 @@ void build_layout(Eng* e) {
     lay.P_pad = coff;
     lay.P_live = 0;
     for (int64_t f : e->live_flat) lay.P_live += f >= 0 ? 1 : 0;
+
+    // row store of one window (K2 -> K3): x | h_l | z | pre_bar_l | z_bar | pred_bar, plus 16
+    // columns of tail slack for K3's fixed-width strip copies
+    auto r4 = [](int x) { return (x + 3) & ~3; };
+    int o = 0;
+    lay.rs_x = o;
+    o += r4(e->in0);
+    for (int l = 0; l < lay.L; ++l) {
+        lay.rs_h[l] = o;
+        o += r4(H);
+    }
+    lay.rs_z = o;
+    o += r4(H);
+    for (int l = 0; l < lay.L; ++l) {
+        lay.rs_pr[l] = o;
+        o += r4(3 * H);
+    }
+    lay.rs_zb = o;
+    o += r4(H);
+    lay.rs_pb = o;
+    o += r4(O);
+    lay.rs_ld = o + 16;
+    // K3 contraction matrices: the layers, then the head (nl_w, out_w)
+    lay.nmat = lay.L + 2;
+    for (int l = 0; l < lay.L; ++l)
+        lay.mats[l] = MatDesc{lay.rs_pr[l], 3 * H, l == 0 ? lay.rs_x : lay.rs_h[l - 1], lay.layer_in[l], lay.ldk[l], 0,
+                              lay.cw[l], lay.cb[l]};
+    lay.mats[lay.L] = MatDesc{lay.rs_zb, H, lay.rs_h[lay.L - 1], H, lay.ldkh, 0, lay.c_nlw, lay.c_nlb};
+    lay.mats[lay.L + 1] = MatDesc{lay.rs_pb, O, lay.rs_z, H, lay.ldkh, 0, lay.c_outw, lay.c_outb};
+    lay.mat_blk0[0] = 0;
+    for (int m = 0; m < lay.nmat; ++m) {
+        const MatDesc& d = lay.mats[m];
+        lay.mat_blk0[m + 1] = lay.mat_blk0[m] + ((d.Q + kGq - 1) / kGq) * ((d.K + kGk - 1) / kGk);
+    }
 }
 
 // ------------------------------------------------------------------ conversions
@@ -495,10 +675,6 @@ void sync_weights_from_device(Eng* e) {
 // ------------------------------------------------------------------ capacity
 void ensure_capacity(Eng* e, int B) {
     if (B <= e->Bcap) return;
-    if (e->graph) {
-        cudaGraphExecDestroy(e->graph);
-        e->graph = nullptr;
-    }
     const int S = e->S, T = e->T, I = e->I, O = e->O;
     const size_t r = e->rsz;
     e->Bcap = B;
@@ -509,9 +685,8 @@ void ensure_capacity(Eng* e, int B) {
     e->lv.alloc(r * T * kc);
     e->se.alloc(r * (T + S) * kc);
     e->contrib.alloc(r * static_cast<size_t>(B) * ((I + O + 2 + 3) & ~3));
-    // padding slots of the tile partials are never written: zero them once
-    e->part.alloc(r * static_cast<size_t>(e->tiles_cap) * e->lay.P_pad);
-    e->part.zero(e->stream);
+    // row store: K2 writes every column of a live window's row; rows are read only by K3
+    e->rowstore.alloc(r * static_cast<size_t>(e->tiles_cap * kRows) * e->lay.rs_ld);
     e->loss_part.alloc(e->tiles_cap);
     e->psg.alloc(r * static_cast<size_t>(kc) * (2 + S));
     e->es_sq_part.alloc(e->es_blocks);
@@ -527,56 +702,85 @@ void append_step(Eng* e, HostPlan& hp, const int* rows, const int* anchors, int 
                  std::vector<int>& slot_id, int step) {
     const int wbase = static_cast<int>(hp.w_row.size());
     const int sbase = static_cast<int>(hp.slot_row.size());
-    for (int i = 0; i < B; ++i) {
-        const int r = rows[i] - e->row0;
-        if (r < 0 || r >= e->N) continue;
-        if (stamp[r] != step) {
-            stamp[r] = step;
-            slot_id[r] = static_cast<int>(hp.slot_row.size()) - sbase;
-            hp.slot_row.push_back(r);
-        }
-        hp.w_row.push_back(r);
-        hp.w_anchor.push_back(anchors[i]);
-        hp.w_slot.push_back(slot_id[r]);
-    }
-    const int nw = static_cast<int>(hp.w_row.size()) - wbase;
-    const int ns = static_cast<int>(hp.slot_row.size()) - sbase;
-    // CSR: count, prefix, fill in batch order
-    std::vector<int> cnt(ns + 1, 0);
-    for (int i = 0; i < nw; ++i) cnt[hp.w_slot[wbase + i] + 1]++;
-    for (int k = 0; k < ns; ++k) cnt[k + 1] += cnt[k];
     const int cbase = static_cast<int>(hp.slot_win.size());
+    const int row0 = e->row0, N = e->N;
+    // this rank's windows of the batch, slots in first-appearance order
+    hp.w_row.resize(wbase + B);
+    hp.w_anchor.resize(wbase + B);
+    hp.w_slot.resize(wbase + B);
+    hp.w_first.resize(wbase + B);
+    hp.slot_row.resize(sbase + B);
+    int* __restrict__ wrow = hp.w_row.data() + wbase;
+    int* __restrict__ wanc = hp.w_anchor.data() + wbase;
+    int* __restrict__ wslot = hp.w_slot.data() + wbase;
+    int* __restrict__ wfirst = hp.w_first.data() + wbase;
+    int* __restrict__ srow = hp.slot_row.data() + sbase;
+    int* __restrict__ stp = stamp.data();
+    int* __restrict__ sid = slot_id.data();
+    int nw = 0, ns = 0;
+    for (int i = 0; i < B; ++i) {
+        const int r = rows[i] - row0;
+        if (r < 0 || r >= N) continue;
+        const bool first = stp[r] != step;
+        if (first) {
+            stp[r] = step;
+            sid[r] = ns;
+            srow[ns++] = r;
+        }
+        wfirst[nw] = first ? 1 : 0;
+        wrow[nw] = r;
+        wanc[nw] = anchors[i];
+        wslot[nw] = sid[r];
+        ++nw;
+    }
+    hp.w_row.resize(wbase + nw);
+    hp.w_anchor.resize(wbase + nw);
+    hp.w_slot.resize(wbase + nw);
+    hp.w_first.resize(wbase + nw);
+    hp.slot_row.resize(sbase + ns);
+    // CSR: count, prefix, fill in batch order
+    static thread_local std::vector<int> cnt;
+    cnt.assign(ns + 1, 0);
+    int* __restrict__ c = cnt.data();
+    for (int i = 0; i < nw; ++i) c[wslot[i] + 1]++;
+    for (int k = 0; k < ns; ++k) c[k + 1] += c[k];
     hp.slot_win.resize(cbase + nw);
-    std::vector<int> fill(cnt.begin(), cnt.end() - 1);
-    for (int i = 0; i < nw; ++i) hp.slot_win[cbase + fill[hp.w_slot[wbase + i]]++] = i;
-    // slot-major CSR position of each window (K2 writes its ES contributions there) and the
-    // anchor of each CSR entry (K3 reads a slot's windows contiguously)
     hp.w_csr.resize(wbase + nw);
     hp.csr_anchor.resize(cbase + nw);
-    for (int c = 0; c < nw; ++c) {
-        const int i = hp.slot_win[cbase + c];
-        hp.w_csr[wbase + i] = c;
-        hp.csr_anchor[cbase + c] = hp.w_anchor[wbase + i];
+    hp.slot_win_off.resize(hp.slot_win_off.size() + ns);
+    int* __restrict__ soff = hp.slot_win_off.data() + (hp.slot_win_off.size() - ns);
+    for (int k = 0; k < ns; ++k) soff[k] = cbase + c[k + 1];
+    // slot-major CSR position of each window (K2 writes its ES contributions there) and the
+    // anchor of each CSR entry (K3 reads a slot's windows contiguously)
+    int* __restrict__ swin = hp.slot_win.data() + cbase;
+    int* __restrict__ wcsr = hp.w_csr.data() + wbase;
+    int* __restrict__ canc = hp.csr_anchor.data() + cbase;
+    for (int i = 0; i < nw; ++i) {
+        const int pos = c[wslot[i]]++;
+        swin[pos] = i;
+        wcsr[i] = pos;
+        canc[pos] = wanc[i];
     }
-    for (int k = 0; k < ns; ++k) hp.slot_win_off.push_back(cbase + cnt[k + 1]);
-    hp.step_win_off.push_back(static_cast<int>(hp.w_row.size()));
-    hp.step_slot_off.push_back(static_cast<int>(hp.slot_row.size()));
+    hp.step_win_off.push_back(wbase + nw);
+    hp.step_slot_off.push_back(sbase + ns);
     hp.max_step_windows = std::max(hp.max_step_windows, nw);
     hp.max_step_slots = std::max(hp.max_step_slots, ns);
 }
 
-void plan_begin(HostPlan& hp) {
-    hp.w_row.clear();
-    hp.w_anchor.clear();
-    hp.w_slot.clear();
-    hp.w_csr.clear();
-    hp.csr_anchor.clear();
-    hp.slot_row.clear();
-    hp.slot_win.clear();
+void plan_begin(HostPlan& hp, size_t windows = 0, int steps = 0) {
+    for (auto* v : {&hp.w_row, &hp.w_anchor, &hp.w_slot, &hp.w_first, &hp.w_csr, &hp.csr_anchor, &hp.slot_row,
+                    &hp.slot_win}) {
+        v->clear();
+        v->reserve(windows);
+    }
     hp.slot_win_off.assign(1, 0);
+    hp.slot_win_off.reserve(windows + 1);
     hp.step_win_off.assign(1, 0);
+    hp.step_win_off.reserve(steps + 1);
     hp.step_slot_off.assign(1, 0);
+    hp.step_slot_off.reserve(steps + 1);
     hp.step_M.clear();
+    hp.step_M.reserve(steps);
     hp.max_step_windows = hp.max_step_slots = 0;
 }
 
@@ -592,6 +796,7 @@ void upload_plan(Eng* e, const HostPlan& hp, DevPlan& dp, size_t cap_w, size_t c
     upload_vec(e, dp.w_row, hp.w_row, cw);
     upload_vec(e, dp.w_anchor, hp.w_anchor, cw);
     upload_vec(e, dp.w_slot, hp.w_slot, cw);
+    upload_vec(e, dp.w_first, hp.w_first, cw);
     upload_vec(e, dp.w_csr, hp.w_csr, cw);
     upload_vec(e, dp.csr_anchor, hp.csr_anchor, cw);
     upload_vec(e, dp.slot_row, hp.slot_row, cw);
@@ -605,7 +810,7 @@ void upload_plan(Eng* e, const HostPlan& hp, DevPlan& dp, size_t cap_w, size_t c
 // ------------------------------------------------------------------ step launch
 template <typename Real>
 size_t stack_smem(const NetLayout& lay, bool resident) {
-    return sizeof(Real) * TileSmem::make(lay, kRows, stack_threads_for_r<kRows>(lay), resident).total;
+    return sizeof(Real) * TileSmem::make<Real>(lay, resident).total;
 }
 
 // Resident mode keeps every live weight in shared memory for the whole tile (one TMA
@@ -617,51 +822,46 @@ bool stack_resident(const NetLayout& lay) {
     return stack_smem<Real>(lay, true) + 4096 <= static_cast<size_t>(g_smem_optin);
 }
 
-int stack_threads(const NetLayout& lay) { return stack_threads_for_r<kRows>(lay); }
+int stack_threads(const NetLayout& lay) { return tile_threads(lay); }
 
 template <typename Real>
 size_t finish_smem(const NetLayout& lay) {
     // lb, sb, forward l and s columns [.][bd] + one staged observation row per slot
     // + one chunk of staged contribution rows
     const size_t cwp = (lay.I + lay.O + 2 + 3) & ~3;
-    return sizeof(Real) * ((static_cast<size_t>(4 * lay.T + lay.S + 2) + row_pad<Real>(lay.T)) * kEsSlotsPerBlock +
-                           kEsChunk * cwp);
+    const size_t es = (static_cast<size_t>(4 * lay.T + lay.S + 2) + row_pad<Real>(lay.T)) * kEsSlotsPerBlock +
+                      kEsChunk * cwp;
+    const size_t gemm = static_cast<size_t>(kGBuf * kGChunk) * (kGq + kGk) + (kFinishThreads / 32) * 32 * 6;
+    return sizeof(Real) * std::max(es, gemm);
 }
 
-template <typename Real>
-size_t scan_smem(const NetLayout& lay) {
-    return sizeof(Real) * (static_cast<size_t>(lay.S) + row_pad<Real>(lay.T)) * kScanThreads;
-}
-
-template <typename Real, int MODE>
-void set_stack_attr(const NetLayout& lay) {
+// The tile kernel's scans are specialised for the M4 seasonalities (S = 1, 4, 12: seasonal
+// ring in registers); any other S runs the generic variant.
+template <typename Real, int MODE, int SC>
+void set_tile_attr(const NetLayout& lay) {
     if (stack_resident<Real>(lay))
-        CUDA_OK(cudaFuncSetAttribute(k_stack<Real, kRows, MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CUDA_OK(cudaFuncSetAttribute(k_tile<Real, MODE, true, SC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)stack_smem<Real>(lay, true)));
-    CUDA_OK(cudaFuncSetAttribute(k_stack<Real, kRows, MODE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CUDA_OK(cudaFuncSetAttribute(k_tile<Real, MODE, false, SC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)stack_smem<Real>(lay, false)));
 }
 
-// The scans are specialised for the M4 seasonalities (S = 1, 4, 12: seasonal ring in
-// registers); any other S runs the generic shared-memory-ring variant.
 template <typename Real, int SC>
-void set_scan_attrs(const NetLayout& lay) {
-    CUDA_OK(cudaFuncSetAttribute(k_scan_fwd<Real, SC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)scan_smem<Real>(lay)));
-    CUDA_OK(cudaFuncSetAttribute(k_grad_finish<Real, kRows, SC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+void set_sc_attrs(const NetLayout& lay) {
+    set_tile_attr<Real, kTrain, SC>(lay);
+    set_tile_attr<Real, kLossOnly, SC>(lay);
+    CUDA_OK(cudaFuncSetAttribute(k_grad_finish<Real, SC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)finish_smem<Real>(lay)));
 }
 
 template <typename Real>
 void setup_kernel_attrs(Eng* e) {
-    set_stack_attr<Real, kTrain>(e->lay);
-    set_stack_attr<Real, kLossOnly>(e->lay);
-    set_stack_attr<Real, kForecast>(e->lay);
+    set_tile_attr<Real, kForecast, 0>(e->lay);
     switch (e->S) {
-        case 1: set_scan_attrs<Real, 1>(e->lay); break;
-        case 4: set_scan_attrs<Real, 4>(e->lay); break;
-        case 12: set_scan_attrs<Real, 12>(e->lay); break;
-        default: set_scan_attrs<Real, 0>(e->lay); break;
+        case 1: set_sc_attrs<Real, 1>(e->lay); break;
+        case 4: set_sc_attrs<Real, 4>(e->lay); break;
+        case 12: set_sc_attrs<Real, 12>(e->lay); break;
+        default: set_sc_attrs<Real, 0>(e->lay); break;
     }
     const size_t fsm = sizeof(Real) * static_cast<size_t>(e->LEN + e->S + e->I) * kScanThreads;
     CUDA_OK(cudaFuncSetAttribute(k_forecast_scan<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
@@ -671,23 +871,9 @@ void setup_kernel_attrs(Eng* e) {
 }
 
 template <typename Real, int SC>
-void launch_scan_sc(Eng* e, int blocks, const StateDev<Real>& st, const PlanDev& pv, int s) {
-    k_scan_fwd<Real, SC><<<blocks, kScanThreads, scan_smem<Real>(e->lay), e->stream>>>(st, pv, e->lay, s);
-}
-template <typename Real>
-void launch_scan(Eng* e, int blocks, const StateDev<Real>& st, const PlanDev& pv, int s) {
-    switch (e->S) {
-        case 1: launch_scan_sc<Real, 1>(e, blocks, st, pv, s); break;
-        case 4: launch_scan_sc<Real, 4>(e, blocks, st, pv, s); break;
-        case 12: launch_scan_sc<Real, 12>(e, blocks, st, pv, s); break;
-        default: launch_scan_sc<Real, 0>(e, blocks, st, pv, s); break;
-    }
-}
-
-template <typename Real, int SC>
 void launch_finish_sc(Eng* e, const StateDev<Real>& st, const PlanDev& pv, int s, int finalize) {
     static const bool nored = std::getenv("ESRNN_DEBUG_NORED") != nullptr;  // timing experiments only
-    k_grad_finish<Real, kRows, SC><<<e->es_blocks + (nored ? 0 : e->red_blocks), kFinishThreads, finish_smem<Real>(e->lay),
+    k_grad_finish<Real, SC><<<e->es_blocks + (nored ? 0 : e->red_blocks), kFinishThreads, finish_smem<Real>(e->lay),
                                      e->stream>>>(st, pv, e->lay, s, e->es_blocks, finalize);
 }
 template <typename Real>
@@ -700,14 +886,27 @@ void launch_finish(Eng* e, const StateDev<Real>& st, const PlanDev& pv, int s, i
     }
 }
 
-template <typename Real, int MODE>
-void launch_stack(Eng* e, int grid, const StateDev<Real>& st, const PlanDev& pv, int s, const ForecastArgs& fa) {
+template <typename Real, int MODE, int SC>
+void launch_tile_sc(Eng* e, int grid, const StateDev<Real>& st, const PlanDev& pv, int s, const ForecastArgs& fa) {
     const NetLayout& lay = e->lay;
     const int nt = stack_threads(lay);
     if (stack_resident<Real>(lay))
-        k_stack<Real, kRows, MODE, true><<<grid, nt, stack_smem<Real>(lay, true), e->stream>>>(st, pv, lay, s, fa);
+        k_tile<Real, MODE, true, SC><<<grid, nt, stack_smem<Real>(lay, true), e->stream>>>(st, pv, lay, s, fa);
     else
-        k_stack<Real, kRows, MODE, false><<<grid, nt, stack_smem<Real>(lay, false), e->stream>>>(st, pv, lay, s, fa);
+        k_tile<Real, MODE, false, SC><<<grid, nt, stack_smem<Real>(lay, false), e->stream>>>(st, pv, lay, s, fa);
+}
+template <typename Real, int MODE>
+void launch_stack(Eng* e, int grid, const StateDev<Real>& st, const PlanDev& pv, int s, const ForecastArgs& fa) {
+    if (MODE == kForecast) {
+        launch_tile_sc<Real, kForecast, 0>(e, grid, st, pv, s, fa);
+        return;
+    }
+    switch (e->S) {
+        case 1: launch_tile_sc<Real, MODE, 1>(e, grid, st, pv, s, fa); break;
+        case 4: launch_tile_sc<Real, MODE, 4>(e, grid, st, pv, s, fa); break;
+        case 12: launch_tile_sc<Real, MODE, 12>(e, grid, st, pv, s, fa); break;
+        default: launch_tile_sc<Real, MODE, 0>(e, grid, st, pv, s, fa); break;
+    }
 }
 
 // Launch one training step (K1..K5) for step `s` of plan `pv` on the engine stream.
@@ -715,12 +914,7 @@ template <typename Real>
 void launch_step(Eng* e, const PlanDev& pv, int s, bool grads, bool update, StateDev<Real> st) {
     const NetLayout& lay = e->lay;
     const int kc = e->kcap;
-    const int scan_blocks = (kc + kScanThreads - 1) / kScanThreads;  // 64-thread blocks: more SMs busy
     using KS = Eng::KScope;
-    {
-        KS k(e, 0);
-        launch_scan<Real>(e, scan_blocks, st, pv, s);
-    }
     ForecastArgs fa{};
     {
         KS k(e, 1);
@@ -734,7 +928,7 @@ void launch_step(Eng* e, const PlanDev& pv, int s, bool grads, bool update, Stat
         else
             launch_stack<Real, kLossOnly>(e, e->tiles_cap, st, pv, s, fa);
     }
-    e->launches += 2;
+    e->launches += 1;
     if (!grads) return;
     const bool sharded = e->world > 1 && e->comm != nullptr;
     {
@@ -775,10 +969,17 @@ void alloc_state(Eng* e) {
     e->mW.alloc(r * e->lay.P_pad);
     e->vW.alloc(r * e->lay.P_pad);
     e->gbuf.alloc(r * (e->lay.P_pad + 2));
-    e->red_blocks = static_cast<int>((e->lay.P_pad + 32 * kRedChunks - 1) / (32 * kRedChunks));
+    e->gbuf.zero(e->stream);  // padding slots of the compact vector are never written
+    e->red_blocks = e->lay.mat_blk0[e->lay.nmat];
     e->red_sq_part.alloc(std::max<int>(e->red_blocks, static_cast<int>((e->lay.P_pad + 255) / 256)));
     e->scal.alloc(4);
-    e->loss_hist.alloc(1);
+    {
+        // one loss slot per training step of an epoch (make_batches, trainer.hpp:82-102)
+        const int64_t nw = static_cast<int64_t>(e->N_global) * std::max(0, e->T - e->O - e->I + 1);
+        const int B = std::max(1, e->cfg.batch_size);
+        e->steps_cap = static_cast<int>(std::max<int64_t>(1, (nw + B - 1) / B));
+        e->loss_hist.alloc(e->steps_cap);
+    }
     e->done_ctr.alloc(2);
     e->net_step.alloc(1);
     e->errw.alloc(2);
@@ -820,85 +1021,131 @@ void upload_values(Eng* e, const double* values, const int32_t* category) {
 }
 
 // ------------------------------------------------------------------ epoch
+// all_windows (trainer.hpp:214-223) + Rng::shuffle (matrix.hpp:203-205) in global order,
+// cut into batches (make_batches, trainer.hpp:82-102) and planned per step.
+void build_epoch_plan(Eng* e, EpochPlan& ep) {
+    const int I = e->I, O = e->O, T = e->T;
+    const int per = T - O - I + 1;
+    const int64_t nw = static_cast<int64_t>(e->N_global) * per;
+    ep.wr.resize(nw);
+    ep.wa.resize(nw);
+    {
+        // shuffle (row, anchor) pairs together: one random access per swap
+        std::vector<uint64_t> w(nw);
+        int64_t n = 0;
+        for (int r = 0; r < e->N_global; ++r)
+            for (int a = I - 1; a <= T - O - 1; ++a) w[n++] = (static_cast<uint64_t>(r) << 32) | static_cast<uint32_t>(a);
+        for (int64_t i = nw; i > 1; --i) {
+            const int64_t j = static_cast<int64_t>(e->rng.below(static_cast<uint64_t>(i)));
+            std::swap(w[i - 1], w[j]);
+        }
+        for (int64_t i = 0; i < nw; ++i) {
+            ep.wr[i] = static_cast<int>(w[i] >> 32);
+            ep.wa[i] = static_cast<int>(static_cast<uint32_t>(w[i]));
+        }
+    }
+    const int B = e->cfg.batch_size;
+    ep.steps = static_cast<int>((nw + B - 1) / B);
+    HostPlan& hp = ep.hp;
+    plan_begin(hp, static_cast<size_t>(std::min<int64_t>(nw, static_cast<int64_t>(e->N) * per)), ep.steps);
+    std::vector<int> stamp(std::max(e->N, 1), -1), slot_id(std::max(e->N, 1), 0);
+    for (int s = 0; s < ep.steps; ++s) {
+        const int64_t start = static_cast<int64_t>(s) * B;
+        const int nb = static_cast<int>(std::min<int64_t>(nw, start + B) - start);
+        append_step(e, hp, ep.wr.data() + start, ep.wa.data() + start, nb, stamp, slot_id, s);
+        hp.step_M.push_back(static_cast<double>(nb) * O);
+    }
+    ep.ready = true;
+}
+
 template <typename Real>
 double train_epoch_impl(Eng* e) {
     const int I = e->I, O = e->O, T = e->T;
     const int per = T - O - I + 1;
     const int64_t nw = static_cast<int64_t>(e->N_global) * per;
     if (nw <= 0) raise(ESRNN_CONTRACT_ERROR, "make_batches: no windows");
-    // all_windows (trainer.hpp:214-223) + Rng::shuffle (matrix.hpp:203-205), global order
-    std::vector<int> wr(nw), wa(nw);
-    {
-        int64_t n = 0;
-        for (int r = 0; r < e->N_global; ++r)
-            for (int a = I - 1; a <= T - O - 1; ++a) {
-                wr[n] = r;
-                wa[n] = a;
-                ++n;
-            }
-        for (int64_t i = nw; i > 1; --i) {
-            const int64_t j = static_cast<int64_t>(e->rng.below(static_cast<uint64_t>(i)));
-            std::swap(wr[i - 1], wr[j]);
-            std::swap(wa[i - 1], wa[j]);
-        }
-    }
+    using clk = std::chrono::steady_clock;
+    static const bool dbg_host = std::getenv("ESRNN_DEBUG_HOST") != nullptr;
+    const auto h0 = clk::now();
+    // this epoch's plan: built ahead (during create / while the previous epoch ran on the
+    // device), else now
+    e->join_plan();
+    if (!e->next_plan.ready) build_epoch_plan(e, e->next_plan);
+    std::swap(e->cur_plan, e->next_plan);
+    e->next_plan.ready = false;
     const int B = e->cfg.batch_size;
-    const int steps = static_cast<int>((nw + B - 1) / B);
-    HostPlan& hp = e->hp;
-    plan_begin(hp);
-    std::vector<int> stamp(std::max(e->N, 1), -1), slot_id(std::max(e->N, 1), 0);
-    for (int s = 0; s < steps; ++s) {
-        const int64_t start = static_cast<int64_t>(s) * B;
-        const int nb = static_cast<int>(std::min<int64_t>(nw, start + B) - start);
-        append_step(e, hp, wr.data() + start, wa.data() + start, nb, stamp, slot_id, s);
-        hp.step_M.push_back(static_cast<double>(nb) * O);
-    }
+    const int steps = e->cur_plan.steps;
+    HostPlan& hp = e->cur_plan.hp;
+    const auto h1 = clk::now();
     ensure_capacity(e, B);
     const size_t local_w = static_cast<size_t>(e->N) * per;
     upload_plan(e, hp, e->epoch_plan, local_w, steps);
+    const auto h2 = clk::now();
     if (e->steps_cap < steps) {
         e->loss_hist.alloc(steps);
         e->steps_cap = steps;
-        if (e->graph) {
-            cudaGraphExecDestroy(e->graph);
-            e->graph = nullptr;
-        }
     }
     const PlanDev pv = e->epoch_plan.view(false);
     StateDev<Real> st = e->state<Real>();
     const bool use_graph = e->cfg.use_graphs >= 0 && !e->profiling;
     CUDA_OK(cudaEventRecord(e->ev0, e->stream));
     if (use_graph) {
-        if (!e->graph || e->graph_steps != steps) {
-            if (e->graph) cudaGraphExecDestroy(e->graph);
-            e->graph = nullptr;
-            cudaGraph_t g;
-            const int64_t before = e->launches;
-            CUDA_OK(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
-            try {
-                for (int s = 0; s < steps; ++s) launch_step<Real>(e, pv, s, true, true, st);
-            } catch (...) {
-                cudaStreamEndCapture(e->stream, &g);
-                throw;
+        // the graph captures exactly these arguments: same bytes -> same graph
+        std::string key;
+        key_append(key, st);
+        key_append(key, pv);
+        key_append(key, e->lay);
+        const long long dims[8] = {steps, e->tiles_cap, e->es_blocks, e->red_blocks, e->kcap, e->S, e->rank,
+                                   e->world};
+        key_append(key, dims);
+        key_append(key, e->comm);
+        key_append(key, e->stream == nullptr);
+        if (!e->graph || e->graph_key != key) {
+            e->graph = graph_cache().find(key);
+            if (!e->graph) {
+                auto ge = std::make_shared<GraphExec>();
+                cudaGraph_t g;
+                const int64_t before = e->launches;
+                CUDA_OK(cudaStreamBeginCapture(e->stream, cudaStreamCaptureModeThreadLocal));
+                try {
+                    for (int s = 0; s < steps; ++s) launch_step<Real>(e, pv, s, true, true, st);
+                } catch (...) {
+                    cudaStreamEndCapture(e->stream, &g);
+                    throw;
+                }
+                CUDA_OK(cudaStreamEndCapture(e->stream, &g));
+                CUDA_OK(cudaGraphInstantiate(&ge->g, g, 0));
+                CUDA_OK(cudaGraphDestroy(g));
+                ge->launch_nodes = static_cast<int>(e->launches - before);
+                e->launches = before;
+                graph_cache().insert(key, ge);
+                e->graph = ge;
             }
-            CUDA_OK(cudaStreamEndCapture(e->stream, &g));
-            CUDA_OK(cudaGraphInstantiate(&e->graph, g, 0));
-            CUDA_OK(cudaGraphDestroy(g));
-            e->graph_launch_nodes = static_cast<int>(e->launches - before);
-            e->launches = before;
-            e->graph_steps = steps;
+            e->graph_key = key;
         }
-        CUDA_OK(cudaGraphLaunch(e->graph, e->stream));
-        e->launches += e->graph_launch_nodes;
+        CUDA_OK(cudaGraphLaunch(e->graph->g, e->stream));
+        e->launches += e->graph->launch_nodes;
     } else {
         for (int s = 0; s < steps; ++s) launch_step<Real>(e, pv, s, true, true, st);
     }
     CUDA_OK(cudaEventRecord(e->ev1, e->stream));
     CUDA_OK(cudaGetLastError());
+    const auto h3 = clk::now();
+    // the next epoch's shuffle + plan overlap this epoch's device time (the trainer RNG is
+    // consumed in the same order as building it at the next call would)
+    if (!e->profiling) build_epoch_plan(e, e->next_plan);
     if (e->profiling) e->prof_collect();
     std::vector<double> lh(steps);
     CUDA_OK(cudaMemcpyAsync(lh.data(), e->loss_hist.p, sizeof(double) * steps, cudaMemcpyDeviceToHost, e->stream));
     CUDA_OK(cudaStreamSynchronize(e->stream));
+    if (dbg_host) {
+        const auto h4 = clk::now();
+        auto us = [](clk::time_point a, clk::time_point b) {
+            return std::chrono::duration<double, std::micro>(b - a).count();
+        };
+        std::fprintf(stderr, "[esrnn host] epoch: shuffle+plan %.0f us, upload %.0f us, launch %.0f us, wait %.0f us\n",
+                     us(h0, h1), us(h1, h2), us(h2, h3), us(h3, h4));
+    }
     float ms = 0.f;
     CUDA_OK(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
     e->last_ms = ms;
@@ -906,7 +1153,7 @@ double train_epoch_impl(Eng* e) {
     if (e->dbg_clk.p) {
         long long c[96];
         CUDA_OK(cudaMemcpy(c, e->dbg_clk.p, sizeof c, cudaMemcpyDeviceToHost));
-        std::fprintf(stderr, "[esrnn dbg] k_stack tile0 phase cycles:");
+        std::fprintf(stderr, "[esrnn dbg] k_tile tile0 phase cycles:");
         for (int i = 1; i < 32 && c[i] > 0; ++i) std::fprintf(stderr, " %lld", c[i] - c[i - 1]);
         std::fprintf(stderr, "\n[esrnn dbg] grad_finish ES block0:");
         for (int i = 33; i < 48 && c[i] > 0; ++i) std::fprintf(stderr, " %lld", c[i] - c[i - 1]);
@@ -920,8 +1167,8 @@ double train_epoch_impl(Eng* e) {
         for (int i = 80; i < 87; ++i) std::fprintf(stderr, " %lld", c[i] - c[80]);
         std::fprintf(stderr, "\n");
     }
-    e->last_wr = std::move(wr);
-    e->last_wa = std::move(wa);
+    e->last_wr = e->cur_plan.wr;
+    e->last_wa = e->cur_plan.wa;
     // trainer.hpp:236-242: acc += loss * count, in batch order
     double acc = 0.0, weight = 0.0;
     for (int s = 0; s < steps; ++s) {
@@ -1210,6 +1457,18 @@ esrnn_status esrnn_trainer_create(const esrnn_profile* profile, const esrnn_trai
         for (int64_t i = 0; i < static_cast<int64_t>(H) * H; ++i) e->w_host[e->off_nlw + i] = e->rng.uniform(-bound, bound);
         for (int64_t i = 0; i < static_cast<int64_t>(H) * e->O; ++i) e->w_host[e->off_outw + i] = e->rng.uniform(-bound, bound);
 
+        // the first epoch's shuffle is the next consumer of the trainer RNG: build its plan
+        // on a helper thread while the device state is set up
+        if (std::max(0, T - e->O - e->I + 1) > 0) {
+            Eng* ep = e.get();
+            ep->plan_thread = std::thread([ep] {
+                try {
+                    build_epoch_plan(ep, ep->next_plan);
+                } catch (...) {
+                    ep->next_plan.ready = false;  // rebuilt (from a fresh shuffle) by train_epoch
+                }
+            });
+        }
         if (e->fp64) {
             alloc_state<double>(e.get());
             upload_values<double>(e.get(), values, category);
@@ -1398,6 +1657,25 @@ esrnn_status esrnn_trainer_kernel_times(esrnn_trainer* t, double* total_ms, int6
         if (launches) launches[i] = t->prof_n[i];
     }
     return ESRNN_OK;
+}
+
+esrnn_status esrnn_release_cached_memory(void) {
+    std::string err;
+    return guarded(err, [&] {
+        graph_cache().clear();
+        BlockCache& c = block_cache();
+        std::lock_guard<std::mutex> g(c.mu);
+        int dev0 = current_device();
+        for (auto& kv : c.dev) {
+            cudaSetDevice(kv.first.first);
+            for (void* p : kv.second) cudaFree(p);
+        }
+        cudaSetDevice(dev0);
+        for (auto& kv : c.host)
+            for (void* p : kv.second) cudaFreeHost(p);
+        c.dev.clear();
+        c.host.clear();
+    });
 }
 
 esrnn_status esrnn_nccl_unique_id(uint8_t out[128]) {

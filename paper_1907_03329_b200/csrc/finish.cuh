@@ -1,5 +1,6 @@
-// K3 k_grad_finish: per-slot ES backward + fixed-order reduction of the tile partials,
-//                   last CTA finalises the step scalars (single GPU).
+// K3 k_grad_finish: per-slot ES backward + the weight-gradient contraction over the step's
+//                   windows (row store written by K2), last CTA finalises the step scalars
+//                   (single GPU).
 // K3' k_finalize:   post-all-reduce finalisation (sharded mode).
 // K4 k_adam:        Adam over the compact shared vector and the step's per-series slots.
 //
@@ -8,14 +9,16 @@
 // (trainer.hpp:602-655).
 #pragma once
 #include "common.cuh"
+#include "tile.cuh"
 
 namespace esrnn_dev {
 
 constexpr int kFinishThreads = 256;
 constexpr int kEsSlotsPerBlock = 32;  // ES blocks: warp 0 owns 32 slots; all warps stage the windows
 constexpr int kEsChunk = 128;         // contribution rows staged per round
-constexpr int kRedGroups = 8;         // tile groups per reduce block
-constexpr int kRedChunks = 2;         // 32-parameter chunks per reduce block
+constexpr int kGq = 16, kGk = 8;      // K3 GEMM output block (gate rows x input features)
+constexpr int kGChunk = 128;          // row-store rows staged per round
+constexpr int kGBuf = 6;              // staging ring depth (kGBuf - 1 chunks in flight)
 
 // clip scale (trainer.hpp:603-615), global Adam step and bias corrections (:617-620),
 // step loss (masked mean, autodiff.hpp:392)
@@ -37,13 +40,12 @@ __device__ void finalize_scalars(StateDev<Real>& st, const PlanDev& pl, int s, d
     }
 }
 
-template <typename Real, int R, int SC>
+template <typename Real, int SC>
 __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> st, PlanDev pl, NetLayout lay, int s,
                                                                 int es_blocks, int finalize) {
     using M = Math<Real>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ double red[32];
-    __shared__ Real gsum[kRedGroups][32];
     __shared__ bool last;
     const int tid = threadIdx.x;
     double sq = 0.0;
@@ -237,49 +239,103 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
         const double tot = block_sum(sq, red);
         if (tid == 0) st.es_sq_part[blockIdx.x] = tot;
     } else {
-        // ------- tile-partial reduction: kRedChunks x 32 params, kRedGroups tile groups ---
-        const int rb = blockIdx.x - es_blocks;
-        const int w0 = pl.step_win_off[s];
-        const int nt = (pl.step_win_off[s + 1] - w0 + R - 1) / R;
-        const int lane = tid & 31, grp = tid >> 5;
-        const size_t P = lay.P_pad;
-        FCLK();
-        for (int ch = 0; ch < kRedChunks; ++ch) {
-            FCLK();
-            const long long q = ((long long)rb * kRedChunks + ch) * 32 + lane;
-            Real g = 0;
-            if (q < lay.P_pad) {
-                const Real* __restrict__ p = st.part + q;
-                Real a[8];
-#pragma unroll
-                for (int u = 0; u < 8; ++u) a[u] = 0;
-                int t = grp;
-                for (; t + 7 * kRedGroups < nt; t += 8 * kRedGroups) {
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) a[u] += p[(size_t)(t + u * kRedGroups) * P];
-                }
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int tt = t + u * kRedGroups;
-                    if (tt < nt) a[u] += p[(size_t)tt * P];
-                }
-                g = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+        // ------- weight gradients: G[q][k] = sum_b A[b][q] U[b][k] over the step's windows ----
+        // block -> (matrix, 16 q x 8 k output block); warp w sums rows b = w (mod 8) in order,
+        // warps are combined in order: a fixed summation order, no atomics
+        const int gb = blockIdx.x - es_blocks;
+        int m = 0;
+        while (m + 1 < lay.nmat && gb >= lay.mat_blk0[m + 1]) ++m;
+        const MatDesc md = lay.mats[m];
+        const int local = gb - lay.mat_blk0[m];
+        const int nkb = (md.K + kGk - 1) / kGk;
+        const int q0 = (local / nkb) * kGq, k0 = (local % nkb) * kGk;
+        const int wb0 = pl.step_win_off[s];
+        const int Bl = pl.step_win_off[s + 1] - wb0;
+        const int lane = tid & 31, warp = tid >> 5;
+        const int qp = lane >> 2, kp = lane & 3;
+        Real* As = reinterpret_cast<Real*>(smem_raw);       // [kGBuf][kGChunk][kGq]
+        Real* Us = As + kGBuf * kGChunk * kGq;               // [kGBuf][kGChunk][kGk]
+        Real* Rd = Us + kGBuf * kGChunk * kGk;               // [8 warps][32 lanes][6]
+        constexpr int e16 = 16 / static_cast<int>(sizeof(Real));
+        constexpr int ca = kGq / e16, cu = kGk / e16;
+        const int rs_ld = lay.rs_ld;
+        // one cp.async group per chunk (possibly empty, so the group count stays uniform)
+        auto stage = [&](int c) {
+            const int c0 = c * kGChunk, buf = c % kGBuf;
+            const int nb = min(kGChunk, Bl - c0);
+            for (int i = tid; i < nb * (ca + cu); i += kFinishThreads) {
+                const int row = i / (ca + cu), part = i - row * (ca + cu);
+                const Real* src = st.rowstore + (size_t)(c0 + row) * rs_ld;
+                if (part < ca)
+                    cp_async16(As + (buf * kGChunk + row) * kGq + part * e16, src + md.a_off + q0 + part * e16);
+                else
+                    cp_async16(Us + (buf * kGChunk + row) * kGk + (part - ca) * e16,
+                               src + md.u_off + k0 + (part - ca) * e16);
             }
-            gsum[grp][lane] = g;
-            __syncthreads();
-            if (grp == 0) {
-                Real tot = gsum[0][lane];
+            cp_async_commit();
+        };
+        Real acc[2][2] = {{0, 0}, {0, 0}}, bacc[2] = {0, 0};
+        const int nch = (Bl + kGChunk - 1) / kGChunk;
+        // kGBuf - 1 chunks in flight ahead of the one being summed
 #pragma unroll
-                for (int gi = 1; gi < kRedGroups; ++gi) tot += gsum[gi][lane];
-                if (q < lay.P_pad) {
-                    st.gbuf[q] = tot;
-                    sq += static_cast<double>(tot) * tot;
+        for (int c = 0; c < kGBuf - 1; ++c) stage(c);
+        for (int c = 0; c < nch; ++c) {
+            stage(c + kGBuf - 1);  // empty group past the end
+            cp_async_wait<kGBuf - 1>();
+            __syncthreads();
+            const int nb = min(kGChunk, Bl - c * kGChunk);
+            const Real* Ab = As + (c % kGBuf) * kGChunk * kGq + 2 * qp;
+            const Real* Ub = Us + (c % kGBuf) * kGChunk * kGk + 2 * kp;
+#pragma unroll 4
+            for (int b = warp; b < nb; b += kFinishThreads / 32) {
+                const Real a0 = Ab[b * kGq], a1 = Ab[b * kGq + 1];
+                const Real u0 = Ub[b * kGk], u1 = Ub[b * kGk + 1];
+                acc[0][0] += a0 * u0;
+                acc[0][1] += a0 * u1;
+                acc[1][0] += a1 * u0;
+                acc[1][1] += a1 * u1;
+                bacc[0] += a0;
+                bacc[1] += a1;
+            }
+            __syncthreads();  // buffer c % kGBuf is restaged next round
+        }
+        cp_async_wait<0>();
+        Real* rd = Rd + (warp * 32 + lane) * 6;
+        rd[0] = acc[0][0];
+        rd[1] = acc[0][1];
+        rd[2] = acc[1][0];
+        rd[3] = acc[1][1];
+        rd[4] = bacc[0];
+        rd[5] = bacc[1];
+        __syncthreads();
+        if (warp == 0) {
+            Real t[6];
+#pragma unroll
+            for (int j = 0; j < 6; ++j) t[j] = Rd[lane * 6 + j];
+            for (int w = 1; w < kFinishThreads / 32; ++w)
+#pragma unroll
+                for (int j = 0; j < 6; ++j) t[j] += Rd[(w * 32 + lane) * 6 + j];
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const int q = q0 + 2 * qp + i;
+                if (q >= md.Q) continue;
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const int k = k0 + 2 * kp + j;
+                    if (k >= md.K) continue;
+                    const Real g = t[2 * i + j];
+                    st.gbuf[md.cw + (long long)q * md.ldk + k] = g;
+                    sq += static_cast<double>(g) * g;
+                }
+                if (k0 == 0 && kp == 0) {
+                    const Real g = t[4 + i];
+                    st.gbuf[md.cb + q] = g;
+                    sq += static_cast<double>(g) * g;
                 }
             }
-            __syncthreads();
         }
         const double tot = block_sum(sq, red);
-        if (tid == 0) st.red_sq_part[rb] = tot;
+        if (tid == 0) st.red_sq_part[gb] = tot;
     }
     FCLK();
     // ---------------- last CTA finalises ------------------------------------------------
@@ -295,7 +351,7 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
     // all threads sum the per-block parts (strided, then a fixed tree): L2 loads in flight at once
     const int nrb = gridDim.x - es_blocks;
     const int w0 = pl.step_win_off[s];
-    const int nt = (pl.step_win_off[s + 1] - w0 + R - 1) / R;
+    const int nt = (pl.step_win_off[s + 1] - w0 + kR - 1) / kR;
     double es = 0.0, ls = 0.0, all = 0.0;
     if (st.attach)
         for (int b = tid; b < es_blocks; b += kFinishThreads) es += __ldcg(st.es_sq_part + b);

@@ -1,6 +1,5 @@
-// Holt-Winters scans (the per-series sequential part of the step).
+// Forecast-side Holt-Winters scan (the training scan runs in K2's prologue, tile.cuh).
 //
-//   K1 k_scan_fwd       training scan for the slots of one step (holt_winters.hpp:236-283)
 //   K6 k_forecast_scan  forecast scan over values[0:t_ins) + window build (holt_winters.hpp:66-97,
 //                       deseasonalize_normalize :153-166, HWState::seasonal_at :55-59)
 //
@@ -22,102 +21,6 @@ __device__ __forceinline__ void stage_column(Real* ys, const Real* __restrict__ 
 #pragma unroll 8
     for (int t = 0; t < n; ++t) cp_async_elem(ys + t * bd, y + (size_t)t * N);
     cp_async_wait_all();
-}
-
-// ------------------------------------------------------------------------------ K1
-// smem: ring [S][bd] | ys rows [bd][row_pad(T)]  (row-major observations, 16-byte copies)
-// SC > 0: the seasonal ring is a register array (S == SC known at compile time); SC == 0:
-// generic S, ring in shared memory.
-template <typename Real, int SC>
-__global__ void __launch_bounds__(kScanThreads) k_scan_fwd(StateDev<Real> st, PlanDev pl, NetLayout lay, int s) {
-    using M = Math<Real>;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    int sdbg = 64;
-    auto SCLK = [&]() {
-        if (st.dbg_clk && blockIdx.x == 0 && threadIdx.x == 0) st.dbg_clk[sdbg] = clock64();
-        ++sdbg;
-    };
-    SCLK();
-    DBG_GT(st, 0);
-    const int k0 = pl.step_slot_off[s];
-    const int k = pl.step_slot_off[s + 1] - k0;
-    const int slot = blockIdx.x * blockDim.x + threadIdx.x;
-    if (slot >= k) return;
-    const int bd = blockDim.x, tid = threadIdx.x;
-    const int N = st.N, S = SC > 0 ? SC : lay.S, T = lay.T, kc = st.kcap;
-    const int tp = row_pad<Real>(T);
-    Real* ring = reinterpret_cast<Real*>(smem_raw) + tid;
-    Real* ys = reinterpret_cast<Real*>(smem_raw) + S * bd + tid * tp;
-    const int row = pl.slot_row[k0 + slot];
-    SCLK();
-    // the observation row and the per-series parameters, all in flight at once
-    stage_row_async(ys, st.vrm + (size_t)row * st.ldv, T);
-    for (int j = 0; j < S; ++j) cp_async_elem(ring + j * bd, st.ps + (size_t)(2 + j) * N + row);
-    const Real alpha = M::logistic_ps(st.ps[row]);
-    const Real gamma = M::logistic_ps(st.ps[N + row]);
-    const Real oma = Real(1) - alpha, omg = Real(1) - gamma;
-    SCLK();
-    cp_async_wait_all();
-    SCLK();
-    Real* __restrict__ se = st.se + slot;
-    Real* __restrict__ lv = st.lv + slot;
-    Real lp = 0;
-    int bad = INT_MAX;  // first step with a non-positive / non-finite level (branch-free min)
-    if constexpr (SC > 0) {
-        Real rg[SC];
-#pragma unroll
-        for (int j = 0; j < SC; ++j) {
-            rg[j] = M::exp_ps(ring[j * bd]);
-            se[j * kc] = rg[j];
-            lp += ys[j];
-        }
-        lp = lp / Real(SC);
-        // one step: l_t = a*y/s_t + (1-a)*l_{t-1};  s_{t+S} = g*y/l_{t-1} + (1-g)*s_t
-        auto step = [&](int t, Real& sj) {
-            const Real yt = ys[t];
-            const Real l = alpha * fdiv(yt, sj) + oma * lp;
-            const bool ok = (l > Real(0)) & (l <= (sizeof(Real) == 4 ? Real(FLT_MAX) : Real(DBL_MAX)));
-            bad = min(bad, ok ? INT_MAX : t);
-            sj = gamma * fdiv(yt, lp) + omg * sj;
-            se[(t + SC) * kc] = sj;
-            lv[t * kc] = l;
-            lp = l;
-        };
-        // full groups of SC steps are branch-free, so consecutive steps interleave
-        int t0 = 0;
-        for (; t0 + SC <= T; t0 += SC) {
-#pragma unroll
-            for (int j = 0; j < SC; ++j) step(t0 + j, rg[j]);
-        }
-#pragma unroll
-        for (int j = 0; j < SC; ++j)
-            if (t0 + j < T) step(t0 + j, rg[j]);
-    } else {
-        for (int j = 0; j < S; ++j) {
-            const Real s0 = M::exp_ps(ring[j * bd]);
-            ring[j * bd] = s0;
-            se[j * kc] = s0;
-            lp += ys[j];
-        }
-        lp = lp / Real(S);
-        int j = 0;
-#pragma unroll 4
-        for (int t = 0; t < T; ++t) {
-            const Real yt = ys[t];
-            const Real s_t = ring[j * bd];
-            const Real l = alpha * fdiv(yt, s_t) + oma * lp;
-            if (!(l > Real(0)) || !isfinite(l)) bad = min(bad, t);
-            const Real sn = gamma * fdiv(yt, lp) + omg * s_t;
-            ring[j * bd] = sn;
-            se[(t + S) * kc] = sn;
-            lv[t * kc] = l;
-            lp = l;
-            j = (j + 1 == S) ? 0 : j + 1;
-        }
-    }
-    SCLK();
-    DBG_GT(st, 1);
-    if (bad != INT_MAX) flag_error(st.err, kErrTrainLevel, bad);
 }
 
 // ------------------------------------------------------------------------------ K6

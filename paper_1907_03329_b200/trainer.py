@@ -505,8 +505,8 @@ class Trainer:
         self._chk(self.api.lib.esrnn_trainer_kernel_launches(self._h, C.byref(n)))
         return n.value
 
-    KERNEL_CLASSES = ("scan_fwd", "stack", "es_bwd", "net_reduce", "adam", "finalize", "forecast_scan",
-                      "forecast_stack")
+    KERNEL_CLASSES = ("unused0", "tile", "finish", "unused3", "adam", "finalize", "forecast_scan",
+                      "forecast_tile")
 
     def profile_kernels(self, enable: bool) -> None:
         self._chk(self.api.lib.esrnn_trainer_profile_kernels(self._h, 1 if enable else 0))

@@ -10,7 +10,7 @@ api = N.product_api()
 prof = FrequencyProfile.defaults(Frequency.Quarterly)
 vals, cats = api.make_synthetic(41, 1000, 88, 4, 0.05)
 cfg = TrainConfig(seed=7, batch_size=1000, precision="fp32")
-for it in range(4):
+for it in range(6):
     t = [time.perf_counter()]
     tr = Trainer((vals, cats), prof, cfg, api=api); t.append(time.perf_counter())
     tr.train_epoch(); t.append(time.perf_counter())

@@ -1,4 +1,4 @@
-"""Print per-phase clock64 stamps of k_stack tile 0 (ESRNN_DEBUG_CLOCKS=1, no graphs)."""
+"""Print per-phase clock64 stamps of k_tile tile 0 (ESRNN_DEBUG_CLOCKS=1, no graphs)."""
 import os, sys
 from pathlib import Path
 os.environ["ESRNN_DEBUG_CLOCKS"] = "1"
