@@ -193,6 +193,18 @@ esrnn_status esrnn_trainer_forecast(esrnn_trainer* t, int64_t drop_tail, double*
 esrnn_status esrnn_trainer_validate(esrnn_trainer* t, double* forecasts, double* smape_per_series,
                                     double* mean_smape);
 
+/* Scoring behind cmd_evaluate (commands.hpp:312-338) and detail::score_forecasts
+ * (commands.hpp:285-308), fused into the forecast pass.  against_test != 0: model forecasts
+ * are forecast_at(O), actual = the test block, in-sample = train + validation;
+ * against_test == 0: forecast_at(2*O), actual = the validation block, in-sample = train.
+ * Per owned series (all nullable): forecasts [n_local x O], smape (metrics.hpp:17-28),
+ * mase (metrics.hpp:33-49; NaN where the in-sample seasonal-naive MAE is 0, the reference's
+ * std::nullopt), and the same two scores of seasonal_naive (metrics.hpp:52-59) over the same
+ * in-sample span.  totals[8] (nullable) are sums over ALL ranks: {smape, mase, mase count,
+ * naive smape, naive mase, naive mase count, series, 0}. */
+esrnn_status esrnn_trainer_evaluate(esrnn_trainer* t, int32_t against_test, double* forecasts, double* smape,
+                                    double* mase, double* naive_smape, double* naive_mase, double* totals);
+
 /* HWState of hybrid_primer(values[0:t_len], per_series_params(row)) (holt_winters.hpp:66-97):
  * levels[t_len], seasonalities[t_len + S].  Inspection hook for the scan KATs. */
 esrnn_status esrnn_trainer_hw_state(esrnn_trainer* t, int64_t row, int64_t t_len, double* levels,

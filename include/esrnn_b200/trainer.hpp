@@ -140,6 +140,19 @@ struct ForecastResult {
     std::vector<std::string> ids;
     std::vector<std::vector<double>> forecasts;
 };
+// cmd_evaluate's scored rows (commands.hpp:285-338; metrics.hpp:17-59), model and seasonal
+// naive, computed on the device (B200 extension of the Trainer surface; the reference scores
+// on the host in detail::score_forecasts).  MASE entries are std::nullopt where the in-sample
+// seasonal-naive MAE is zero, exactly like metrics.hpp:46.
+struct EvaluationScores {
+    std::vector<std::string> ids;
+    std::vector<std::vector<double>> forecasts;
+    std::vector<double> smape, naive_smape;
+    std::vector<std::optional<double>> mase, naive_mase;
+    double mean_smape = 0.0, naive_mean_smape = 0.0;  // over all series (all ranks)
+    std::optional<double> mean_mase, naive_mean_mase;  // over series with a defined MASE
+    std::size_t mase_undefined_count = 0;
+};
 struct BenchmarkReport {
     double batched_s = 0.0, looped_s = 0.0, speedup = 0.0;
     int batch_size = 0, n_series = 0;
@@ -294,6 +307,35 @@ public:
         }
         v.smape_per_series = std::move(sm);
         return v;
+    }
+
+    // cmd_evaluate (commands.hpp:312-338): forecast_at(O) against the test block when
+    // against_test, else forecast_at(2*O) against the validation block.
+    EvaluationScores evaluate(bool against_test = true) const {
+        push();
+        const int O = profile_.horizon;
+        const std::size_t n = row_end_ - row_begin_;
+        std::vector<double> fc(n * static_cast<std::size_t>(O)), sm(n), ma(n), ns(n), nm(n);
+        double tot[8] = {};
+        detail::check(esrnn_trainer_evaluate(h_.get(), against_test ? 1 : 0, fc.data(), sm.data(), ma.data(), ns.data(),
+                                             nm.data(), tot),
+                      h_.get());
+        EvaluationScores e;
+        auto opt = [](double v) { return std::isnan(v) ? std::optional<double>() : std::optional<double>(v); };
+        for (std::size_t r = 0; r < n; ++r) {
+            e.ids.push_back(series_[row_begin_ + r].id);
+            e.forecasts.emplace_back(fc.data() + r * static_cast<std::size_t>(O), fc.data() + (r + 1) * static_cast<std::size_t>(O));
+            e.mase.push_back(opt(ma[r]));
+            e.naive_mase.push_back(opt(nm[r]));
+        }
+        e.smape = std::move(sm);
+        e.naive_smape = std::move(ns);
+        e.mean_smape = tot[0] / tot[6];
+        e.naive_mean_smape = tot[3] / tot[6];
+        if (tot[2] > 0) e.mean_mase = tot[1] / tot[2];
+        if (tot[5] > 0) e.naive_mean_mase = tot[4] / tot[5];
+        e.mase_undefined_count = static_cast<std::size_t>(tot[6] - tot[2]);
+        return e;
     }
 
     BatchGradients batch_gradients(WindowBatch& batch) {  // trainer.hpp:308-335

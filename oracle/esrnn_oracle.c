@@ -1049,6 +1049,54 @@ esrnn_status esrnn_trainer_validate(esrnn_trainer* t, double* forecasts, double*
     return st;
 }
 
+/* metrics.hpp:33-49 mase: forecast MAE over the in-sample seasonal-naive MAE; returns NAN for
+ * the reference's std::nullopt (zero denominator) */
+static double mase(const double* ins, int n_ins, const double* a, const double* f, int n, int S) {
+    double den = 0.0;
+    for (int t = S; t < n_ins; ++t) den += fabs(ins[t] - ins[t - S]);
+    den /= (double)(n_ins - S);
+    if (den == 0.0) return NAN;
+    double num = 0.0;
+    for (int i = 0; i < n; ++i) num += fabs(a[i] - f[i]);
+    num /= (double)n;
+    return num / den;
+}
+
+/* commands.hpp:285-338 score_forecasts / cmd_evaluate with metrics.hpp:52-59 seasonal_naive */
+esrnn_status esrnn_trainer_evaluate(esrnn_trainer* t, int32_t against_test, double* forecasts, double* smape_o,
+                                    double* mase_o, double* naive_smape, double* naive_mase, double* totals) {
+    const int O = t->O, N = t->N, S = t->S;
+    const int t_ins = against_test ? t->T + O : t->T;
+    if (t_ins <= S) return fail(t->err, ESRNN_INSUFFICIENT_LENGTH, "mase: in-sample length must exceed season length");
+    double* fc = (double*)xcalloc((size_t)N * O, sizeof(double));
+    double* nv = (double*)xcalloc((size_t)O, sizeof(double));
+    esrnn_status st = esrnn_trainer_forecast(t, against_test ? O : 2 * O, fc);
+    if (!st) {
+        double tot[8] = {0, 0, 0, 0, 0, 0, (double)N, 0};
+        for (int r = 0; r < N; ++r) {
+            const double* v = t->vals + (size_t)r * t->LEN;
+            const double* act = v + t_ins;
+            const double* f = fc + (size_t)r * O;
+            for (int i = 0; i < O; ++i) nv[i] = v[t_ins - S + (i % S)];
+            const double s = smape(act, f, O), m = mase(v, t_ins, act, f, O, S);
+            const double ns = smape(act, nv, O), nm = mase(v, t_ins, act, nv, O, S);
+            if (smape_o) smape_o[r] = s;
+            if (mase_o) mase_o[r] = m;
+            if (naive_smape) naive_smape[r] = ns;
+            if (naive_mase) naive_mase[r] = nm;
+            tot[0] += s;
+            if (!isnan(m)) { tot[1] += m; tot[2] += 1; }
+            tot[3] += ns;
+            if (!isnan(nm)) { tot[4] += nm; tot[5] += 1; }
+        }
+        if (forecasts) memcpy(forecasts, fc, sizeof(double) * (size_t)N * O);
+        if (totals) memcpy(totals, tot, sizeof tot);
+    }
+    free(nv);
+    free(fc);
+    return st;
+}
+
 /* holt_winters.hpp:66-97 hybrid_primer on values[0:t_len] of one series */
 esrnn_status esrnn_trainer_hw_state(esrnn_trainer* t, int64_t row, int64_t t_len, double* levels,
                                     double* seas) {

@@ -332,6 +332,41 @@ esrnn_status esrnn_trainer_validate(esrnn_trainer* t, double* forecasts, double*
     });
 }
 
+// cmd_evaluate / detail::score_forecasts (commands.hpp:285-338) restated over the reference's
+// own metrics.hpp smape / mase / seasonal_naive (commands.hpp needs the absent vendored json)
+esrnn_status esrnn_trainer_evaluate(esrnn_trainer* t, int32_t against_test, double* forecasts, double* smape_o,
+                                    double* mase_o, double* naive_smape, double* naive_mase, double* totals) {
+    return guarded(t->err, [&] {
+        const auto t0 = std::chrono::steady_clock::now();
+        const int O = t->tr->profile().horizon, S = t->tr->profile().seasonality_length;
+        ForecastResult fr = t->tr->forecast_at(static_cast<std::size_t>(against_test ? O : 2 * O));
+        double tot[8] = {0, 0, 0, 0, 0, 0, static_cast<double>(t->tr->series_count()), 0};
+        for (std::size_t i = 0; i < t->tr->series_count(); ++i) {
+            const DatasetSplit& sp = t->tr->split(i);
+            const std::vector<double>& actual = against_test ? sp.test : sp.validation;
+            std::vector<double> insample = sp.train;
+            if (against_test) insample.insert(insample.end(), sp.validation.begin(), sp.validation.end());
+            const std::vector<double> nv = seasonal_naive(insample, S, O);
+            const double s = smape(actual, fr.forecasts[i]);
+            const std::optional<double> m = mase(insample, actual, fr.forecasts[i], S);
+            const double ns = smape(actual, nv);
+            const std::optional<double> nm = mase(insample, actual, nv, S);
+            if (forecasts)
+                for (int j = 0; j < O; ++j) forecasts[i * O + j] = fr.forecasts[i][j];
+            if (smape_o) smape_o[i] = s;
+            if (mase_o) mase_o[i] = m ? *m : NAN;
+            if (naive_smape) naive_smape[i] = ns;
+            if (naive_mase) naive_mase[i] = nm ? *nm : NAN;
+            tot[0] += s;
+            if (m) { tot[1] += *m; tot[2] += 1; }
+            tot[3] += ns;
+            if (nm) { tot[4] += *nm; tot[5] += 1; }
+        }
+        if (totals) std::memcpy(totals, tot, sizeof tot);
+        t->last_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    });
+}
+
 esrnn_status esrnn_trainer_hw_state(esrnn_trainer* t, int64_t row, int64_t t_len, double* levels,
                                     double* seas) {
     return guarded(t->err, [&] {

@@ -285,7 +285,7 @@ struct esrnn_trainer {
     DBuf<int> ps_steps;
     DBuf<unsigned char> lv, se, contrib, rowstore, gbuf, psg, d_inputs, d_targets, d_seas, d_levels;
     DBuf<unsigned char> fX, fL, fS, dump_lv, dump_se;
-    DBuf<double> loss_part, es_sq_part, red_sq_part, scal, loss_hist, f_out, f_smape, smape_sum;
+    DBuf<double> loss_part, es_sq_part, red_sq_part, scal, loss_hist, f_out, f_smape, f_score, smape_sum;
     DBuf<unsigned int> done_ctr;
     DBuf<long long> net_step;
     DBuf<long long> dbg_clk;  // ESRNN_DEBUG_CLOCKS: per-phase clock64 stamps of tile 0
@@ -351,7 +351,7 @@ struct esrnn_trainer {
         };
         add(vals, vrm, ps, ps_m, ps_v, theta, mW, vW, cat, ps_steps, lv, se, contrib, rowstore, gbuf, psg, d_inputs,
             d_targets, d_seas, d_levels, fX, fL, fS, dump_lv, dump_se, loss_part, es_sq_part, red_sq_part, scal,
-            loss_hist, f_out, f_smape, smape_sum, done_ctr, net_step, dbg_clk, errw);
+            loss_hist, f_out, f_smape, f_score, smape_sum, done_ctr, net_step, dbg_clk, errw);
         for (DevPlan* d : {&epoch_plan, &batch_plan})
             add(d->w_row, d->w_anchor, d->w_slot, d->w_first, d->step_win_off, d->step_slot_off, d->slot_row,
                 d->slot_win_off, d->slot_win, d->w_csr, d->csr_anchor, d->step_M, d->mask);
@@ -1279,11 +1279,23 @@ void run_batch_impl(Eng* e, int32_t B, const int32_t* rows, const int32_t* ancho
 }
 
 // ------------------------------------------------------------------ forecast
+// Host outputs of one forecast pass (all nullable).  mode 0: forecast_at; 1: validate (sMAPE);
+// 2: evaluate (sMAPE + MASE + seasonal-naive scores, commands.hpp:285-338).
+struct ScoreOut {
+    double* smape = nullptr;        // [n_local]
+    double* mase = nullptr;         // [n_local], NaN = undefined (std::nullopt)
+    double* naive_smape = nullptr;  // [n_local]
+    double* naive_mase = nullptr;   // [n_local]
+    double* totals = nullptr;       // [8] global sums (see esrnn_trainer_evaluate)
+    double* mean = nullptr;         // validate: global mean sMAPE
+};
+
 template <typename Real>
-void forecast_impl(Eng* e, int64_t drop_tail, double* out, double* smape, double* mean, bool validate) {
+void forecast_impl(Eng* e, int64_t drop_tail, double* out, int mode, const ScoreOut& so) {
     const int I = e->I, O = e->O, S = e->S, N = e->N;
     if (static_cast<int64_t>(e->LEN) < drop_tail + I) raise(ESRNN_INSUFFICIENT_LENGTH, "forecast_at: not enough in-sample data");
     const int t_ins = static_cast<int>(e->LEN - drop_tail);
+    if (mode == 2 && t_ins <= S) raise(ESRNN_INSUFFICIENT_LENGTH, "mase: in-sample length must exceed season length");
     const size_t r = sizeof(Real);
     if (e->fX.n < r * std::max(N, 1) * e->in0) {
         e->fX.alloc(r * std::max(N, 1) * e->in0);
@@ -1292,6 +1304,7 @@ void forecast_impl(Eng* e, int64_t drop_tail, double* out, double* smape, double
         e->f_out.alloc(static_cast<size_t>(std::max(N, 1)) * O);
         e->f_smape.alloc(std::max(N, 1));
     }
+    if (mode == 2 && e->f_score.n < 4 * static_cast<size_t>(std::max(N, 1))) e->f_score.alloc(4 * std::max(N, 1));
     StateDev<Real> st = e->state<Real>();
     const NetLayout& lay = e->lay;
     CUDA_OK(cudaEventRecord(e->ev0, e->stream));
@@ -1301,16 +1314,18 @@ void forecast_impl(Eng* e, int64_t drop_tail, double* out, double* smape, double
             Eng::KScope k(e, 6);
             k_forecast_scan<Real><<<sb, kScanThreads, sizeof(Real) * (t_ins + S + I) * kScanThreads, e->stream>>>(
                 st, lay, t_ins, reinterpret_cast<Real*>(e->fX.p), reinterpret_cast<Real*>(e->fL.p),
-                reinterpret_cast<Real*>(e->fS.p), nullptr, nullptr, -1);
+                reinterpret_cast<Real*>(e->fS.p), nullptr, nullptr, -1, mode == 2 ? e->f_score.p : nullptr);
         }
         ForecastArgs fa{};
         fa.t_ins = t_ins;
-        fa.validate = validate ? 1 : 0;
+        fa.validate = mode != 0 ? 1 : 0;
         fa.X = e->fX.p;
         fa.lvl = e->fL.p;
         fa.sout = e->fS.p;
         fa.out = e->f_out.p;
         fa.smape = e->f_smape.p;
+        fa.mase = mode == 2 ? e->f_score.p + 3 * static_cast<size_t>(N) : nullptr;
+        fa.score = mode == 2 ? e->f_score.p : nullptr;
         const int tiles = (N + kRows - 1) / kRows;
         {
             Eng::KScope k(e, 7);
@@ -1327,22 +1342,37 @@ void forecast_impl(Eng* e, int64_t drop_tail, double* out, double* smape, double
     e->last_ms = ms;
     throw_device_error(e);
     if (out && N > 0) CUDA_OK(cudaMemcpy(out, e->f_out.p, sizeof(double) * N * O, cudaMemcpyDeviceToHost));
-    if (validate) {
-        std::vector<double> sm(std::max(N, 1));
-        if (N > 0) CUDA_OK(cudaMemcpy(sm.data(), e->f_smape.p, sizeof(double) * N, cudaMemcpyDeviceToHost));
-        double acc = 0.0;
-        for (int i = 0; i < N; ++i) acc += sm[i];
-        if (smape)
-            for (int i = 0; i < N; ++i) smape[i] = sm[i];
-        if (e->comm != nullptr) {
-            if (e->smape_sum.n < 1) e->smape_sum.alloc(1);
-            CUDA_OK(cudaMemcpy(e->smape_sum.p, &acc, sizeof acc, cudaMemcpyHostToDevice));
-            NCCL_OK(ncclAllReduce(e->smape_sum.p, e->smape_sum.p, 1, ncclDouble, ncclSum, e->comm, e->stream));
-            CUDA_OK(cudaMemcpyAsync(&acc, e->smape_sum.p, sizeof acc, cudaMemcpyDeviceToHost, e->stream));
-            CUDA_OK(cudaStreamSynchronize(e->stream));
+    if (mode == 0) return;
+    std::vector<double> sm(std::max(N, 1));
+    if (N > 0) CUDA_OK(cudaMemcpy(sm.data(), e->f_smape.p, sizeof(double) * N, cudaMemcpyDeviceToHost));
+    if (so.smape)
+        for (int i = 0; i < N; ++i) so.smape[i] = sm[i];
+    // global sums: [smape, mase, mase count, naive smape, naive mase, naive mase count, series, 0]
+    double tot[8] = {0, 0, 0, 0, 0, 0, static_cast<double>(N), 0};
+    for (int i = 0; i < N; ++i) tot[0] += sm[i];
+    if (mode == 2) {
+        std::vector<double> sc(4 * static_cast<size_t>(std::max(N, 1)));
+        if (N > 0) CUDA_OK(cudaMemcpy(sc.data(), e->f_score.p, sizeof(double) * 4 * N, cudaMemcpyDeviceToHost));
+        for (int i = 0; i < N; ++i) {
+            const double ns = sc[N + i], nm = sc[2 * N + i], m = sc[3 * N + i];
+            if (so.mase) so.mase[i] = m;
+            if (so.naive_smape) so.naive_smape[i] = ns;
+            if (so.naive_mase) so.naive_mase[i] = nm;
+            if (!std::isnan(m)) { tot[1] += m; tot[2] += 1; }
+            tot[3] += ns;
+            if (!std::isnan(nm)) { tot[4] += nm; tot[5] += 1; }
         }
-        if (mean) *mean = acc / static_cast<double>(e->N_global);
     }
+    if (e->comm != nullptr) {
+        if (e->smape_sum.n < 8) e->smape_sum.alloc(8);
+        CUDA_OK(cudaMemcpy(e->smape_sum.p, tot, sizeof tot, cudaMemcpyHostToDevice));
+        NCCL_OK(ncclAllReduce(e->smape_sum.p, e->smape_sum.p, 8, ncclDouble, ncclSum, e->comm, e->stream));
+        CUDA_OK(cudaMemcpyAsync(tot, e->smape_sum.p, sizeof tot, cudaMemcpyDeviceToHost, e->stream));
+        CUDA_OK(cudaStreamSynchronize(e->stream));
+    }
+    if (so.mean) *so.mean = tot[0] / static_cast<double>(e->N_global);
+    if (so.totals)
+        for (int i = 0; i < 8; ++i) so.totals[i] = tot[i];
 }
 
 template <typename Real>
@@ -1363,7 +1393,7 @@ void hw_state_impl(Eng* e, int64_t row, int64_t t_len, double* levels, double* s
     // the dump row's thread writes its full state; X == nullptr skips the window build
     k_forecast_scan<Real><<<sb, kScanThreads, sizeof(Real) * (t_len + S + e->I) * kScanThreads, e->stream>>>(
         st, e->lay, static_cast<int>(t_len), nullptr, nullptr, nullptr, reinterpret_cast<Real*>(e->dump_lv.p),
-        reinterpret_cast<Real*>(e->dump_se.p), lr);
+        reinterpret_cast<Real*>(e->dump_se.p), lr, nullptr);
     e->launches += 1;
     CUDA_OK(cudaGetLastError());
     CUDA_OK(cudaStreamSynchronize(e->stream));
@@ -1603,8 +1633,8 @@ esrnn_status esrnn_trainer_run_batch(esrnn_trainer* t, int32_t B, const int32_t*
 esrnn_status esrnn_trainer_forecast(esrnn_trainer* t, int64_t drop_tail, double* out) {
     return guarded(t->err, [&] {
         CUDA_OK(cudaSetDevice(t->cfg.device));
-        if (t->fp64) forecast_impl<double>(t, drop_tail, out, nullptr, nullptr, false);
-        else forecast_impl<float>(t, drop_tail, out, nullptr, nullptr, false);
+        if (t->fp64) forecast_impl<double>(t, drop_tail, out, 0, ScoreOut{});
+        else forecast_impl<float>(t, drop_tail, out, 0, ScoreOut{});
     });
 }
 
@@ -1612,8 +1642,27 @@ esrnn_status esrnn_trainer_validate(esrnn_trainer* t, double* forecasts, double*
     return guarded(t->err, [&] {
         CUDA_OK(cudaSetDevice(t->cfg.device));
         const int64_t dt = 2 * static_cast<int64_t>(t->O);
-        if (t->fp64) forecast_impl<double>(t, dt, forecasts, smape, mean, true);
-        else forecast_impl<float>(t, dt, forecasts, smape, mean, true);
+        ScoreOut so;
+        so.smape = smape;
+        so.mean = mean;
+        if (t->fp64) forecast_impl<double>(t, dt, forecasts, 1, so);
+        else forecast_impl<float>(t, dt, forecasts, 1, so);
+    });
+}
+
+esrnn_status esrnn_trainer_evaluate(esrnn_trainer* t, int32_t against_test, double* forecasts, double* smape,
+                                    double* mase, double* naive_smape, double* naive_mase, double* totals) {
+    return guarded(t->err, [&] {
+        CUDA_OK(cudaSetDevice(t->cfg.device));
+        const int64_t dt = (against_test ? 1 : 2) * static_cast<int64_t>(t->O);
+        ScoreOut so;
+        so.smape = smape;
+        so.mase = mase;
+        so.naive_smape = naive_smape;
+        so.naive_mase = naive_mase;
+        so.totals = totals;
+        if (t->fp64) forecast_impl<double>(t, dt, forecasts, 2, so);
+        else forecast_impl<float>(t, dt, forecasts, 2, so);
     });
 }
 

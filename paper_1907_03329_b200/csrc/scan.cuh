@@ -1,7 +1,9 @@
 // Forecast-side Holt-Winters scan (the training scan runs in K2's prologue, tile.cuh).
 //
 //   K6 k_forecast_scan  forecast scan over values[0:t_ins) + window build (holt_winters.hpp:66-97,
-//                       deseasonalize_normalize :153-166, HWState::seasonal_at :55-59)
+//                       deseasonalize_normalize :153-166, HWState::seasonal_at :55-59); with
+//                       `score`, also the series' MASE scale and the seasonal-naive scores
+//                       (metrics.hpp:33-59, commands.hpp:285-308) from the staged column
 //
 // One thread per series.  The whole observation column is first staged into shared
 // memory with every load in flight at once, the last S seasonalities live in a
@@ -28,7 +30,7 @@ __device__ __forceinline__ void stage_column(Real* ys, const Real* __restrict__ 
 template <typename Real>
 __global__ void __launch_bounds__(kScanThreads) k_forecast_scan(StateDev<Real> st, NetLayout lay, int t_ins, Real* X,
                                                                 Real* FL, Real* FS, Real* dump_lv, Real* dump_se,
-                                                                int dump_row) {
+                                                                int dump_row, double* score) {
     using M = Math<Real>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int S = lay.S, I = lay.I, O = lay.O, in0 = lay.in0, N = st.N;
@@ -46,6 +48,26 @@ __global__ void __launch_bounds__(kScanThreads) k_forecast_scan(StateDev<Real> s
             flag_error(st.err, kErrObs, t);
             return;
         }
+    if (score != nullptr) {
+        // mase(): in-sample seasonal-naive MAE over y[0:t_ins) (metrics.hpp:40-44); the
+        // seasonal-naive forecast y[t_ins-S+(o mod S)] (metrics.hpp:52-59) scored with
+        // smape() (:17-28) and mase() against the held-out block y[t_ins:t_ins+O)
+        double den = 0.0;
+        for (int t = S; t < t_ins; ++t)
+            den += fabs(static_cast<double>(ys[t * bd]) - static_cast<double>(ys[(t - S) * bd]));
+        den /= static_cast<double>(t_ins - S);
+        double acc = 0.0, mae = 0.0;
+        for (int o = 0; o < O; ++o) {
+            const double f = static_cast<double>(ys[(t_ins - S + o % S) * bd]);
+            const double a = static_cast<double>(st.vals[(size_t)(t_ins + o) * N + row]);
+            const double d = fabs(a) + fabs(f);
+            if (d > 0.0) acc += fabs(a - f) / d;
+            mae += fabs(a - f);
+        }
+        score[row] = den;
+        score[N + row] = 200.0 * acc / static_cast<double>(O);
+        score[2 * N + row] = den == 0.0 ? NAN : (mae / static_cast<double>(O)) / den;
+    }
     const bool dump = row == dump_row;
     const Real alpha = M::logistic_ps(a_raw);
     const Real gamma = M::logistic_ps(g_raw);

@@ -38,6 +38,8 @@ struct ForecastArgs {
     const void* sout;    // [N][O] Real
     double* out;         // [N][O]
     double* smape;       // [N]
+    double* mase;        // [N] or nullptr (evaluate)
+    const double* score; // [N] MASE scale from k_forecast_scan (evaluate)
 };
 
 constexpr int kR = 8;  // windows per tile = the reduce-scatter fan-in
@@ -572,17 +574,23 @@ __global__ void __launch_bounds__(512) k_tile(StateDev<Real> st, PlanDev pl, Net
         }
         if (fa.validate) {
             __syncthreads();
-            // sMAPE against the validation block (metrics.hpp:17-28)
+            // sMAPE (metrics.hpp:17-28) and MASE (:33-49) against the held-out block
+            // y[t_ins : t_ins+O) (validate: the validation block; evaluate: the test block)
             for (int r = tid; r < nrows; r += NT) {
                 const int row = tile * R + r;
-                double acc = 0.0;
+                double acc = 0.0, mae = 0.0;
                 for (int o = 0; o < O; ++o) {
-                    const double a = static_cast<double>(st.vals[(size_t)(lay.T + o) * st.N + row]);
+                    const double a = static_cast<double>(st.vals[(size_t)(fa.t_ins + o) * st.N + row]);
                     const double f = fa.out[(size_t)row * O + o];
                     const double den = fabs(a) + fabs(f);
                     if (den > 0.0) acc += fabs(a - f) / den;
+                    mae += fabs(a - f);
                 }
                 fa.smape[row] = 200.0 * acc / static_cast<double>(O);
+                if (fa.mase) {
+                    const double d = fa.score[row];
+                    fa.mase[row] = d == 0.0 ? NAN : (mae / static_cast<double>(O)) / d;
+                }
             }
         }
         return;

@@ -183,6 +183,75 @@ class ValidationResult:  # trainer.hpp:122-127
 
 
 @dataclass
+class MeanCount:  # metrics.hpp:75-78
+    mean: float = 0.0
+    count: int = 0
+
+
+@dataclass
+class ReportAggregates:  # metrics.hpp:82-91
+    smape_by_category: dict
+    smape_by_frequency: dict
+    mase_by_category: dict
+    mase_by_frequency: dict
+    overall_smape: float
+    overall_mase: Optional[float]
+    total_series: int
+    mase_undefined_count: int
+
+
+def aggregate(categories, frequency: str, smape, mase) -> ReportAggregates:  # metrics.hpp:106-137
+    """Per-category / per-frequency running means in row order (the reference's fold), the
+    count-weighted overall means (weighted_mean, metrics.hpp:94-104); NaN MASE = nullopt."""
+    if len(smape) == 0:
+        raise E.ContractError("aggregate: no rows")
+    sc, sf, mc, mf = {}, {}, {}, {}
+    undefined = 0
+
+    def fold(m, key, v):
+        x = m.setdefault(key, MeanCount())
+        x.mean = (x.mean * x.count + v) / (x.count + 1)
+        x.count += 1
+
+    for c, s_, m_ in zip(categories, smape, mase):
+        cname = Category(c).name if c >= 0 else Category.Other.name
+        fold(sc, cname, float(s_))
+        fold(sf, frequency, float(s_))
+        if np.isnan(m_):
+            undefined += 1
+        else:
+            fold(mc, cname, float(m_))
+            fold(mf, frequency, float(m_))
+
+    def wmean(m):
+        tot = sum(x.count for x in m.values())
+        return sum(x.mean * x.count for x in m.values()) / tot
+
+    return ReportAggregates(sc, sf, mc, mf, wmean(sf), wmean(mf) if mf else None, len(smape), undefined)
+
+
+@dataclass
+class EvaluationResult:  # cmd_evaluate's scored rows (commands.hpp:285-338) for model and seasonal-naive
+    ids: list
+    forecasts: np.ndarray
+    smape: np.ndarray
+    mase: np.ndarray            # NaN where metrics.hpp:46 returns nullopt
+    naive_smape: np.ndarray
+    naive_mase: np.ndarray
+    totals: np.ndarray          # global sums over ranks (esrnn_trainer_evaluate)
+    model: ReportAggregates = None
+    naive: ReportAggregates = None
+
+    @property
+    def mean_smape(self) -> float:
+        return float(self.totals[0] / self.totals[6])
+
+    @property
+    def mean_mase(self) -> float:
+        return float(self.totals[1] / self.totals[2]) if self.totals[2] else float("nan")
+
+
+@dataclass
 class ForecastResult:  # trainer.hpp:129-132
     ids: list
     forecasts: np.ndarray
@@ -486,6 +555,24 @@ class Trainer:
         mean = C.c_double()
         self._chk(self.api.lib.esrnn_trainer_validate(self._h, N.dptr(fc), N.dptr(sm), C.byref(mean)))
         return ValidationResult(self._ids[self.row_begin:self.row_end], fc, sm, mean.value)
+
+    def evaluate(self, against_test: bool = True) -> EvaluationResult:
+        """cmd_evaluate (commands.hpp:312-338): forecast_at(O) scored against the test block
+        (against_test) or forecast_at(2*O) against the validation block, with sMAPE, MASE and
+        the seasonal-naive baseline's scores computed on the device."""
+        n = self.row_end - self.row_begin
+        fc = np.zeros((n, self._profile.horizon))
+        arrs = [np.zeros(n) for _ in range(4)]
+        tot = np.zeros(8)
+        self._chk(self.api.lib.esrnn_trainer_evaluate(self._h, 1 if against_test else 0, N.dptr(fc),
+                                                      *[N.dptr(a) for a in arrs], N.dptr(tot)))
+        cats = self._cats[self.row_begin:self.row_end]
+        fname = self._profile.frequency.name
+        res = EvaluationResult(self._ids[self.row_begin:self.row_end], fc, *arrs, tot)
+        if n:
+            res.model = aggregate(cats, fname, arrs[0], arrs[1])
+            res.naive = aggregate(cats, fname, arrs[2], arrs[3])
+        return res
 
     def last_epoch_windows(self) -> list:
         """Global shuffled (row, anchor) order consumed by the last train_epoch."""

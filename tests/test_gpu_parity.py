@@ -12,7 +12,7 @@ import pytest
 
 from conftest import PROFILES, dataset, max_rel, tensor_err
 from paper_1907_03329_b200 import errors as E
-from paper_1907_03329_b200.trainer import TrainConfig, Trainer, WindowBatch
+from paper_1907_03329_b200.trainer import Frequency, FrequencyProfile, TrainConfig, Trainer, WindowBatch
 
 pytestmark = pytest.mark.gpu
 
@@ -288,3 +288,39 @@ def test_sharded_partials_sum_to_full_batch(engine, oracle, world, precision):
     assert abs(tot_loss - gf.loss) <= tol * abs(gf.loss)
     for k, v in gf.network.items():
         assert tensor_err(tot[k], v) <= (1e-11 if precision == "fp64" else 1e-4), k
+
+
+@pytest.mark.parametrize("precision,tol", [("fp64", 1e-10), ("fp32", 1e-5)])
+@pytest.mark.parametrize("name", ["quarterly", "yearly", "monthly"])
+@pytest.mark.parametrize("against_test", [True, False])
+def test_evaluate_scores(engine, oracle, name, precision, tol, against_test):
+    """Device-side cmd_evaluate scoring (sMAPE, MASE, seasonal-naive) vs the oracle."""
+    g, o = pair(engine, oracle, name, 37, 4, precision, batch_size=64)
+    for tr in (g, o):
+        tr.train_epoch()
+    eg, eo = g.evaluate(against_test), o.evaluate(against_test)
+    for f in ("forecasts", "smape", "mase", "naive_smape", "naive_mase"):
+        a, b = getattr(eg, f), getattr(eo, f)
+        assert np.array_equal(np.isnan(a), np.isnan(b)), f
+        assert tensor_err(np.nan_to_num(a), np.nan_to_num(b)) < (tol if "naive" not in f else 1e-6), f
+    assert abs(eg.mean_smape - eo.mean_smape) < 100 * tol
+    assert abs(eg.mean_mase - eo.mean_mase) < 100 * tol
+
+
+def test_quality_parity_cfg1_15_epochs(engine, ref):
+    """North-star quality contract: after the same 15 epochs and seeds on cfg1 (Quarterly,
+    1,000 series, B=1,000), the fp32 engine's holdout sMAPE and MASE are within 0.1 of the
+    reference's own fp64 CPU run (oracle/_ref).  Trajectories diverge chaotically at fp32
+    (SURVEY §7 hard parts), so only end-of-run quality is compared."""
+    prof = FrequencyProfile.defaults(Frequency.Quarterly)
+    vals, cats = ref.make_synthetic(41, 1000, 88, 4, 0.05)
+    scores = {}
+    for key, api, prec in (("gpu", engine, "fp32"), ("ref", ref, "fp64")):
+        tr = Trainer((vals, cats), prof, TrainConfig(seed=7, batch_size=1000, precision=prec), api=api)
+        for _ in range(15):
+            tr.train_epoch()
+        v = tr.evaluate(False)
+        t = tr.evaluate(True)
+        scores[key] = (v.mean_smape, v.mean_mase, t.mean_smape, t.mean_mase)
+    g, r = scores["gpu"], scores["ref"]
+    assert all(abs(a - b) < 0.1 for a, b in zip(g, r)), (g, r)

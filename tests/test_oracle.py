@@ -149,3 +149,36 @@ def test_config_validation(oracle):
             Trainer((vals, cats), prof, TrainConfig(**bad), api=oracle)
     with pytest.raises(E.InsufficientLengthError):
         Trainer((vals[:, :10], cats), prof, TrainConfig(), api=oracle)
+
+
+@pytest.mark.parametrize("name,n,seed", [("quarterly", 8, 9), ("yearly", 20, 2), ("monthly", 5, 3)])
+@pytest.mark.parametrize("against_test", [True, False])
+def test_oracle_evaluate_matches_reference(oracle, ref, name, n, seed, against_test):
+    """cmd_evaluate scoring (commands.hpp:285-338): model and seasonal-naive sMAPE / MASE per
+    series, the oracle restatement against the reference's own metrics.hpp functions."""
+    prof, vals, cats = dataset(ref, name, n, seed)
+    cfg = TrainConfig(seed=seed, batch_size=32)
+    o, r = (Trainer((vals, cats), prof, cfg, api=a) for a in (oracle, ref))
+    o.train_epoch(), r.train_epoch()
+    eo, er = o.evaluate(against_test), r.evaluate(against_test)
+    for f in ("forecasts", "smape", "mase", "naive_smape", "naive_mase", "totals"):
+        a, b = getattr(eo, f), getattr(er, f)
+        assert np.array_equal(np.isnan(a), np.isnan(b)), f
+        assert tensor_err(np.nan_to_num(a), np.nan_to_num(b)) < 1e-11, f
+    assert eo.model.smape_by_category.keys() == er.model.smape_by_category.keys()
+    if not against_test:
+        assert max_rel(eo.mean_smape, o.validate().mean_smape) < 1e-14  # validate == evaluate(validation)
+
+
+def test_mase_undefined_for_periodic_insample(oracle, ref):
+    """metrics.hpp:46: a perfectly periodic in-sample span has a zero seasonal-naive MAE, so
+    MASE is undefined (std::nullopt -> NaN) and excluded from the aggregates."""
+    prof = FrequencyProfile.defaults(Frequency.Quarterly)
+    cyc = [10.0, 12.0, 9.0, 11.0]
+    vals = np.array([cyc * 22, [v * (1 + 0.01 * i) for i, v in enumerate(cyc * 22)]])
+    for api in (oracle, ref):
+        tr = Trainer((vals, np.array([0, 1], dtype=np.int32)), prof, TrainConfig(seed=1), api=api)
+        ev = tr.evaluate(True)
+        assert np.isnan(ev.naive_mase[0]) and np.isnan(ev.mase[0]) and not np.isnan(ev.mase[1])
+        assert ev.naive_smape[0] == 0.0  # the naive forecast repeats the exact cycle
+        assert ev.model.mase_undefined_count == 1 and ev.totals[2] == 1
