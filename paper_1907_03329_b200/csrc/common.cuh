@@ -149,6 +149,16 @@ __device__ __forceinline__ long long gtimer() {
         ++_dbg;                                                                     \
     } while (0)
 
+// ------------------------------------------------------------------ programmatic dependent launch
+// Kernels of a training step are launched with programmatic stream serialisation: each
+// kernel lets its dependent launch as soon as every CTA has started (pdl_trigger) and
+// waits for its predecessor grid's completion and memory (pdl_wait) before touching data
+// the predecessor writes -- or data the predecessor reads that this kernel overwrites.
+// Before the wait a kernel may only read epoch-constant data (observations, plan).  Both
+// are no-ops for a kernel launched without the attribute.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ------------------------------------------------------------------ TMA bulk copy
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
     return static_cast<unsigned>(__cvta_generic_to_shared(p));

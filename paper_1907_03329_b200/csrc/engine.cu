@@ -291,6 +291,7 @@ struct esrnn_trainer {
     DBuf<long long> dbg_clk;  // ESRNN_DEBUG_CLOCKS: per-phase clock64 stamps of tile 0
     DBuf<int> errw;
     int Bcap = 0, kcap = 0, tiles_cap = 0, es_blocks = 0, red_blocks = 0, steps_cap = 0;
+    bool pdl = std::getenv("ESRNN_NO_PDL") == nullptr;  // programmatic dependent launch between step kernels
 
     DevPlan epoch_plan, batch_plan;
     EpochPlan cur_plan, next_plan;
@@ -870,42 +871,61 @@ void setup_kernel_attrs(Eng* e) {
         raise(ESRNN_CONFIG_ERROR, "profile too large for the B200 kernels' shared-memory tiles");
 }
 
+// Kernel launch on the engine stream; with `pdl`, programmatic stream serialisation lets
+// the kernel launch while its predecessor drains (common.cuh pdl_trigger / pdl_wait).
+template <typename... KArgs, typename... Args>
+void launch_k(Eng* e, bool pdl, void (*kern)(KArgs...), int grid, int block, size_t smem, Args&&... args) {
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(block);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = e->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = (pdl && e->pdl && !e->profiling) ? 1 : 0;
+    CUDA_OK(cudaLaunchKernelEx(&lc, kern, std::forward<Args>(args)...));
+}
+
 template <typename Real, int SC>
-void launch_finish_sc(Eng* e, const StateDev<Real>& st, const PlanDev& pv, int s, int finalize) {
+void launch_finish_sc(Eng* e, const StateDev<Real>& st, const PlanDev& pv, int s, int finalize, bool pdl) {
     static const bool nored = std::getenv("ESRNN_DEBUG_NORED") != nullptr;  // timing experiments only
-    k_grad_finish<Real, SC><<<e->es_blocks + (nored ? 0 : e->red_blocks), kFinishThreads, finish_smem<Real>(e->lay),
-                                     e->stream>>>(st, pv, e->lay, s, e->es_blocks, finalize);
+    launch_k(e, pdl, k_grad_finish<Real, SC>, e->es_blocks + (nored ? 0 : e->red_blocks), kFinishThreads,
+             finish_smem<Real>(e->lay), st, pv, e->lay, s, e->es_blocks, finalize);
 }
 template <typename Real>
-void launch_finish(Eng* e, const StateDev<Real>& st, const PlanDev& pv, int s, int finalize) {
+void launch_finish(Eng* e, const StateDev<Real>& st, const PlanDev& pv, int s, int finalize, bool pdl = false) {
     switch (e->S) {
-        case 1: launch_finish_sc<Real, 1>(e, st, pv, s, finalize); break;
-        case 4: launch_finish_sc<Real, 4>(e, st, pv, s, finalize); break;
-        case 12: launch_finish_sc<Real, 12>(e, st, pv, s, finalize); break;
-        default: launch_finish_sc<Real, 0>(e, st, pv, s, finalize); break;
+        case 1: launch_finish_sc<Real, 1>(e, st, pv, s, finalize, pdl); break;
+        case 4: launch_finish_sc<Real, 4>(e, st, pv, s, finalize, pdl); break;
+        case 12: launch_finish_sc<Real, 12>(e, st, pv, s, finalize, pdl); break;
+        default: launch_finish_sc<Real, 0>(e, st, pv, s, finalize, pdl); break;
     }
 }
 
 template <typename Real, int MODE, int SC>
-void launch_tile_sc(Eng* e, int grid, const StateDev<Real>& st, const PlanDev& pv, int s, const ForecastArgs& fa) {
+void launch_tile_sc(Eng* e, int grid, const StateDev<Real>& st, const PlanDev& pv, int s, const ForecastArgs& fa,
+                    bool pdl) {
     const NetLayout& lay = e->lay;
     const int nt = stack_threads(lay);
     if (stack_resident<Real>(lay))
-        k_tile<Real, MODE, true, SC><<<grid, nt, stack_smem<Real>(lay, true), e->stream>>>(st, pv, lay, s, fa);
+        launch_k(e, pdl, k_tile<Real, MODE, true, SC>, grid, nt, stack_smem<Real>(lay, true), st, pv, lay, s, fa);
     else
-        k_tile<Real, MODE, false, SC><<<grid, nt, stack_smem<Real>(lay, false), e->stream>>>(st, pv, lay, s, fa);
+        launch_k(e, pdl, k_tile<Real, MODE, false, SC>, grid, nt, stack_smem<Real>(lay, false), st, pv, lay, s, fa);
 }
 template <typename Real, int MODE>
-void launch_stack(Eng* e, int grid, const StateDev<Real>& st, const PlanDev& pv, int s, const ForecastArgs& fa) {
+void launch_stack(Eng* e, int grid, const StateDev<Real>& st, const PlanDev& pv, int s, const ForecastArgs& fa,
+                  bool pdl = false) {
     if (MODE == kForecast) {
-        launch_tile_sc<Real, kForecast, 0>(e, grid, st, pv, s, fa);
+        launch_tile_sc<Real, kForecast, 0>(e, grid, st, pv, s, fa, false);
         return;
     }
     switch (e->S) {
-        case 1: launch_tile_sc<Real, MODE, 1>(e, grid, st, pv, s, fa); break;
-        case 4: launch_tile_sc<Real, MODE, 4>(e, grid, st, pv, s, fa); break;
-        case 12: launch_tile_sc<Real, MODE, 12>(e, grid, st, pv, s, fa); break;
-        default: launch_tile_sc<Real, MODE, 0>(e, grid, st, pv, s, fa); break;
+        case 1: launch_tile_sc<Real, MODE, 1>(e, grid, st, pv, s, fa, pdl); break;
+        case 4: launch_tile_sc<Real, MODE, 4>(e, grid, st, pv, s, fa, pdl); break;
+        case 12: launch_tile_sc<Real, MODE, 12>(e, grid, st, pv, s, fa, pdl); break;
+        default: launch_tile_sc<Real, MODE, 0>(e, grid, st, pv, s, fa, pdl); break;
     }
 }
 
@@ -923,7 +943,7 @@ void launch_step(Eng* e, const PlanDev& pv, int s, bool grads, bool update, Stat
             // ESRNN_DEBUG_TWICE: re-run the (idempotent) tile kernel so the stamps show a
             // warm instruction cache
             if (e->dbg_clk.p && std::getenv("ESRNN_DEBUG_TWICE")) launch_stack<Real, kTrain>(e, e->tiles_cap, st, pv, s, fa);
-            launch_stack<Real, kTrain>(e, e->tiles_cap, st, pv, s, fa);
+            launch_stack<Real, kTrain>(e, e->tiles_cap, st, pv, s, fa, s > 0);
         }
         else
             launch_stack<Real, kLossOnly>(e, e->tiles_cap, st, pv, s, fa);
@@ -934,7 +954,7 @@ void launch_step(Eng* e, const PlanDev& pv, int s, bool grads, bool update, Stat
     {
         KS k(e, 2);
         // bit 0: finalise the step scalars here (single GPU); bit 1: the step applies updates
-        launch_finish<Real>(e, st, pv, s, (sharded ? 0 : 1) | (update ? 2 : 0));
+        launch_finish<Real>(e, st, pv, s, (sharded ? 0 : 1) | (update ? 2 : 0), true);
     }
     e->launches += 1;
     if (sharded) {
@@ -948,7 +968,9 @@ void launch_step(Eng* e, const PlanDev& pv, int s, bool grads, bool update, Stat
     if (update) {
         const long long n = lay.P_pad + kc;
         KS k(e, 4);
-        k_adam<Real><<<static_cast<int>((n + 255) / 256), 256, 0, e->stream>>>(st, pv, lay, s);
+        // K4 waits for K3 the ordinary way: launched early under PDL its CTAs measured slower
+        // (cfg1 +6%), while the next tile's early launch after K4 (and K3's after K2) pays
+        launch_k(e, false, k_adam<Real>, static_cast<int>((n + 255) / 256), 256, 0, st, pv, lay, s);
         e->launches += 1;
     }
 }

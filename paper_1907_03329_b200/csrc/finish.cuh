@@ -47,6 +47,7 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ double red[32];
     __shared__ bool last;
+    pdl_trigger();
     const int tid = threadIdx.x;
     double sq = 0.0;
     // ESRNN_DEBUG_CLOCKS: ES block 0 stamps at [32, 40), reduce block 0 at [48, 56)
@@ -88,15 +89,18 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
             // ---- stage the forward state with the whole block (every copy in flight at once) ----
             const bool lane_ok = sl0 + lane < sl1;
             const int lrow = lane_ok ? pl.slot_row[k0 + sl0 + lane] : 0;
+            constexpr int e16 = 16 / static_cast<int>(sizeof(Real));
+            // observation rows are epoch constants: staged before the dependency wait
+            if (lane_ok)
+                for (int ch = tid >> 5; ch * e16 < tp; ch += kFinishThreads / 32)
+                    cp_async16(YS + lane * tp + ch * e16, st.vrm + (size_t)lrow * st.ldv + ch * e16);
+            pdl_wait();
             Real a_raw = 0, g_raw = 0;
             if (mine) {
                 a_raw = st.ps[lrow];
                 g_raw = st.ps[N + lrow];
             }
-            constexpr int e16 = 16 / static_cast<int>(sizeof(Real));
             if (lane_ok) {
-                for (int ch = tid >> 5; ch * e16 < tp; ch += kFinishThreads / 32)
-                    cp_async16(YS + lane * tp + ch * e16, st.vrm + (size_t)lrow * st.ldv + ch * e16);
                 for (int t = tid >> 5; t < T; t += kFinishThreads / 32) {
                     cp_async_elem(LV + t * bd + lane, st.lv + (size_t)t * kc + sl0 + lane);
                     cp_async_elem(SE + t * bd + lane, st.se + (size_t)t * kc + sl0 + lane);
@@ -235,10 +239,13 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
                     sq += static_cast<double>(g) * g;
                 }
             }
+        } else {
+            pdl_wait();
         }
         const double tot = block_sum(sq, red);
         if (tid == 0) st.es_sq_part[blockIdx.x] = tot;
     } else {
+        pdl_wait();
         // ------- weight gradients: G[q][k] = sum_b A[b][q] U[b][k] over the step's windows ----
         // block -> (matrix, 16 q x 8 k output block); warp w sums rows b = w (mod 8) in order,
         // warps are combined in order: a fixed summation order, no atomics
@@ -407,6 +414,8 @@ __device__ __forceinline__ void adam_update(double& theta, double& m, double& v,
 
 template <typename Real>
 __global__ void __launch_bounds__(256) k_adam(StateDev<Real> st, PlanDev pl, NetLayout lay, int s) {
+    pdl_trigger();
+    pdl_wait();
     DBG_GT(st, 6);
     if (st.err[0] != 0) return;  // the reference throws before apply_updates
     const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;

@@ -307,6 +307,7 @@ template <typename Real, int MODE, bool RESIDENT, int SC>
 __global__ void __launch_bounds__(512) k_tile(StateDev<Real> st, PlanDev pl, NetLayout lay_p, int s, ForecastArgs fa) {
     using M = Math<Real>;
     constexpr int R = kR, LD = ldr<Real>();
+    pdl_trigger();  // dependents may launch; they wait for this grid's completion themselves
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Real* sm = reinterpret_cast<Real*>(smem_raw);
     __shared__ double red[32];
@@ -353,8 +354,10 @@ __global__ void __launch_bounds__(512) k_tile(StateDev<Real> st, PlanDev pl, Net
     // row store of this tile's windows (K3 operands): [b][rs_ld], b = step-local window
     Real* __restrict__ rs = (MODE == kTrain) ? st.rowstore + (size_t)(tile * R) * lay.rs_ld : nullptr;
 
-    // ---- weights: TMA bulk copy of the compact parameter vector (resident mode) ----
-    if (RESIDENT && tid == 0) {
+    // ---- weights: TMA bulk copy of the compact parameter vector (resident mode), issued
+    // once the previous step's Adam has completed (after pdl_wait) ----
+    auto weights_tma = [&]() {
+        if (!(RESIDENT && tid == 0)) return;
         mbar_init(&wbar, 1);
         const unsigned total = static_cast<unsigned>(lay.P_pad * sizeof(Real));
         mbar_expect_tx(&wbar, total);
@@ -364,25 +367,31 @@ __global__ void __launch_bounds__(512) k_tile(StateDev<Real> st, PlanDev pl, Net
             bulk_g2s(reinterpret_cast<unsigned char*>(wsm) + off, reinterpret_cast<const unsigned char*>(th) + off, n,
                      &wbar);
         }
-    }
+    };
 
     // ---- prologue: Holt-Winters scan of each window's series (K1 fused here) ---------
     Real* LVR = sm + ts.lvr;
     Real* SER = sm + ts.ser;
+    Real* YS = sm + ts.ys;
     if (MODE != kForecast) {
-        Real* YS = sm + ts.ys;
         Real* PSM = sm + ts.psm;
         const int T = lay.T, S = lay.S, np = 2 + S;
         constexpr int e16 = 16 / static_cast<int>(sizeof(Real));
         const int nch = (T + e16 - 1) / e16;
-        // observation rows and per-series parameters, every copy in flight at once
-        for (int e = tid; e < nrows * (nch + np); e += NT) {
-            const int r = e / (nch + np), c = e - r * (nch + np);
+        // observation rows (constant for the epoch: staged before the dependency wait, so
+        // the copies overlap the previous kernel's tail under programmatic dependent
+        // launch), then the per-series parameters the previous step's Adam wrote
+        for (int e = tid; e < nrows * nch; e += NT) {
+            const int r = e / nch, c = e - r * nch;
             const int row = pl.w_row[w0 + tile * R + r];
-            if (c < nch)
-                cp_async16(YS + r * ts.tp + c * e16, st.vrm + (size_t)row * st.ldv + c * e16);
-            else
-                cp_async_elem(PSM + r * np + (c - nch), st.ps + (size_t)(c - nch) * st.N + row);
+            cp_async16(YS + r * ts.tp + c * e16, st.vrm + (size_t)row * st.ldv + c * e16);
+        }
+        pdl_wait();
+        weights_tma();
+        for (int e = tid; e < nrows * np; e += NT) {
+            const int r = e / np, c = e - r * np;
+            const int row = pl.w_row[w0 + tile * R + r];
+            cp_async_elem(PSM + r * np + c, st.ps + (size_t)c * st.N + row);
         }
         cp_async_wait_all();
         __syncthreads();
@@ -415,6 +424,8 @@ __global__ void __launch_bounds__(512) k_tile(StateDev<Real> st, PlanDev pl, Net
     DBG_CLK(st, 0);
     // ---- window gather + normalisation (trainer.hpp:532-566) --------------------------
     if (MODE == kForecast) {
+        pdl_wait();
+        weights_tma();
         const Real* X = reinterpret_cast<const Real*>(fa.X);
         const Real* FL = reinterpret_cast<const Real*>(fa.lvl);
         const Real* FS = reinterpret_cast<const Real*>(fa.sout);
@@ -461,14 +472,14 @@ __global__ void __launch_bounds__(512) k_tile(StateDev<Real> st, PlanDev pl, Net
             if (c < I) {
                 const int idx = a - I + 1 + c;
                 const Real sv = SER[r * ts.lds + idx];
-                const Real v = fdiv(st.vrm[(size_t)row * st.ldv + idx], sv * l);
+                const Real v = fdiv(YS[r * ts.tp + idx], sv * l);
                 XT[c * LD + r] = v;
                 if (rs) rs[r * lay.rs_ld + lay.rs_x + c] = v;
                 s_in[r * I + c] = sv;
             } else if (c < I + O) {
                 const int j = c - I, idx = a + 1 + j;
                 const Real sv = SER[r * ts.lds + idx];
-                tgt[r * ldo + j] = fdiv(st.vrm[(size_t)row * st.ldv + idx], sv * l);
+                tgt[r * ldo + j] = fdiv(YS[r * ts.tp + idx], sv * l);
                 s_out[r * ldo + j] = sv;
                 msk[r * ldo + j] = (pl.mask == nullptr || pl.mask[(size_t)wb * O + j] != 0) ? Real(1) : Real(0);
             } else {
