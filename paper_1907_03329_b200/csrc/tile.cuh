@@ -353,6 +353,28 @@ __global__ void __launch_bounds__(512) k_tile(StateDev<Real> st, PlanDev pl, Net
     DBG_CLK(st, 0);
     // row store of this tile's windows (K3 operands): [b][rs_ld], b = step-local window
     Real* __restrict__ rs = (MODE == kTrain) ? st.rowstore + (size_t)(tile * R) * lay.rs_ld : nullptr;
+    // the tile's windows' plan entries (epoch constants), one load per thread, all in flight:
+    // series row, anchor, publishing slot (-1 unless the window is its slot's first), CSR
+    // position, category
+    __shared__ int w_info[5][kR];
+    if (MODE != kForecast) {
+        if (tid < 4 * R) {
+            const int q = tid / R, r = tid - q * R;
+            int v = 0;
+            if (r < nrows) {
+                const int wb = w0 + tile * R + r;
+                if (q == 0) v = pl.w_row[wb];
+                else if (q == 1) v = pl.w_anchor[wb];
+                else if (q == 2) v = (MODE == kTrain && pl.w_first[wb] != 0) ? pl.w_slot[wb] : -1;
+                else v = MODE == kTrain ? pl.w_csr[wb] : 0;
+            }
+            w_info[q][r] = v;
+        }
+        __syncthreads();
+        if (tid < nrows) w_info[4][tid] = st.cat[w_info[0][tid]];
+    }
+    const int* w_rowv = w_info[0];
+    const int* w_ancv = w_info[1];
 
     // ---- weights: TMA bulk copy of the compact parameter vector (resident mode), issued
     // once the previous step's Adam has completed (after pdl_wait) ----
@@ -383,24 +405,20 @@ __global__ void __launch_bounds__(512) k_tile(StateDev<Real> st, PlanDev pl, Net
         // launch), then the per-series parameters the previous step's Adam wrote
         for (int e = tid; e < nrows * nch; e += NT) {
             const int r = e / nch, c = e - r * nch;
-            const int row = pl.w_row[w0 + tile * R + r];
-            cp_async16(YS + r * ts.tp + c * e16, st.vrm + (size_t)row * st.ldv + c * e16);
+            cp_async16(YS + r * ts.tp + c * e16, st.vrm + (size_t)w_rowv[r] * st.ldv + c * e16);
         }
         pdl_wait();
         weights_tma();
         for (int e = tid; e < nrows * np; e += NT) {
             const int r = e / np, c = e - r * np;
-            const int row = pl.w_row[w0 + tile * R + r];
-            cp_async_elem(PSM + r * np + c, st.ps + (size_t)c * st.N + row);
+            cp_async_elem(PSM + r * np + c, st.ps + (size_t)c * st.N + w_rowv[r]);
         }
         cp_async_wait_all();
         __syncthreads();
         DBG_CLK(st, 0);
-        __shared__ int pub_slot[kR];
+        // the tile holding a slot's first window (batch order) publishes the slot's states
+        const int* pub_slot = w_info[2];
         if (tid < nrows) {
-            const int wb = w0 + tile * R + tid;
-            // the tile holding a slot's first window (batch order) publishes the slot's states
-            pub_slot[tid] = (MODE == kTrain && pl.w_first[wb] != 0) ? pl.w_slot[wb] : -1;
             const int bad = hw_scan_row<Real, SC>(YS + tid * ts.tp, PSM + tid * np, T, S, LVR + tid * ts.ldl,
                                                   SER + tid * ts.lds);
             if (bad != INT_MAX) flag_error(st.err, kErrTrainLevel, bad);
@@ -459,15 +477,14 @@ __global__ void __launch_bounds__(512) k_tile(StateDev<Real> st, PlanDev pl, Net
                 }
                 continue;
             }
-            const int row = pl.w_row[wb];
             if (c > I + O) {
                 const int cc = c - O - 1;  // x column in [I, in0)
-                const Real v = (st.cat[row] == cc - I) ? Real(1) : Real(0);
+                const Real v = (w_info[4][r] == cc - I) ? Real(1) : Real(0);
                 XT[cc * LD + r] = v;
                 if (rs) rs[r * lay.rs_ld + lay.rs_x + cc] = v;
                 continue;
             }
-            const int a = pl.w_anchor[wb];
+            const int a = w_ancv[r];
             const Real l = LVR[r * ts.ldl + a];
             if (c < I) {
                 const int idx = a - I + 1 + c;
@@ -711,26 +728,32 @@ __global__ void __launch_bounds__(512) k_tile(StateDev<Real> st, PlanDev pl, Net
     // written in slot-major CSR order so each slot's windows are contiguous for K3;
     // row = [inputs (s index a-I+1..a) | targets (a+1..a+O) | level a | anchor a]
     if (st.attach) {
-        for (int r = tid; r < nrows; r += NT) {
-            Real* __restrict__ cr = st.contrib + (size_t)pl.w_csr[w0 + tile * R + r] * st.cwp;
-            cr[I + O + 1] = static_cast<Real>(pl.w_anchor[w0 + tile * R + r]);  // exact (< 2^24)
+        // one warp per window, lanes over its I + O normalised entries; fixed-order warp sum
+        const int nio = I + O;
+        for (int r = warp; r < nrows; r += NW) {
+            Real* __restrict__ cr = st.contrib + (size_t)w_info[3][r] * st.cwp;
             const Real lv = lvl[r];
-            Real acc_o = 0;
-            for (int j = 0; j < O; ++j) {
-                const Real tb = -PBT[j * LD + r];
-                const Real den = s_out[r * ldo + j] * lv;
-                const Real denb = -fdiv(tb * tgt[r * ldo + j], den);
-                cr[I + j] = denb * lv;
-                acc_o += denb * s_out[r * ldo + j];
-            }
-            Real acc_i = 0;
-            for (int j = 0; j < I; ++j) {
-                const Real den = s_in[r * I + j] * lv;
-                const Real denb = -fdiv(UBT[j * LD + r] * XT[j * LD + r], den);
+            Real acc = 0;
+            for (int j = lane; j < nio; j += 32) {
+                Real v, sv;
+                if (j < I) {
+                    sv = s_in[r * I + j];
+                    v = UBT[j * LD + r] * XT[j * LD + r];
+                } else {
+                    const int o = j - I;
+                    sv = s_out[r * ldo + o];
+                    v = -PBT[o * LD + r] * tgt[r * ldo + o];
+                }
+                const Real denb = -fdiv(v, sv * lv);
                 cr[j] = denb * lv;
-                acc_i += denb * s_in[r * I + j];
+                acc += denb * sv;
             }
-            cr[O + I] = acc_o + acc_i;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (lane == 0) {
+                cr[nio] = acc;
+                cr[nio + 1] = static_cast<Real>(w_ancv[r]);  // exact (< 2^24)
+            }
         }
     }
     if (MODE == kTrain) DBG_GT(st, 3);
