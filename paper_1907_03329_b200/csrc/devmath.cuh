@@ -70,10 +70,26 @@ struct Math<float> {
     static __device__ __forceinline__ float exp(float x) {
         return __expf(fminf(fmaxf(x, -87.0f), 88.0f));
     }
-    // libdevice tanhf: <= 2 ulp, MUFU.EX2 + RCP inside
-    static __device__ __forceinline__ float tanh(float x) { return tanhf(x); }
+    static __device__ __forceinline__ float rcp(float x) {
+        float r;
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+        return r;
+    }
+    // Branch-free tanh, the single-precision Cephes scheme: odd polynomial below 0.625
+    // (relative error ~1e-7), else 1 - 2 / (exp(2|x|) + 1) from MUFU.EX2 + MUFU.RCP (no
+    // cancellation there: the result is >= 0.55); saturates to +-1 past 9.
+    static __device__ __forceinline__ float tanh(float x) {
+        const float ax = fabsf(x);
+        const float z = x * x;
+        const float p = ((((-5.70498872745e-3f * z + 2.06390887954e-2f) * z - 5.37397155531e-2f) * z +
+                          1.33314422036e-1f) * z - 3.33332819422e-1f) * z * x + x;
+        const float e = __expf(2.0f * fminf(ax, 9.0f));
+        const float t = copysignf(1.0f - 2.0f * rcp(e + 1.0f), x);
+        return ax < 0.625f ? p : t;
+    }
+    // fastmath.hpp:70-75 with the SFU reciprocal (<= 1 ulp) in place of the IEEE division
     static __device__ __forceinline__ float logistic(float x) {
-        const float y = __frcp_rn(1.0f + exp(-x));
+        const float y = rcp(1.0f + exp(-x));
         const float lo = FLT_MIN, hi = 1.0f - FLT_EPSILON / 2.0f;
         return y < lo ? lo : (y > hi ? hi : y);
     }
