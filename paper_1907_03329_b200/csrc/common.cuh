@@ -99,6 +99,9 @@ struct StateDev {
     double* scal;           // [4] scale, bc1, bc2, loss
     long long* net_step;
     double* loss_hist;      // [steps]
+    const double* bc;       // [2 * bc_n] Adam bias corrections {1 - 0.9^t, 1 - 0.999^t} by step t,
+                            // host std::pow like trainer.hpp:617-620 / :640-641
+    long long bc_n;         // table length; both corrections are exactly 1.0 from t = bc_n on
     int* err;               // [2] code, min t
     // optional dumps (run_batch): WindowBatch matrices, step-local window order
     Real* d_inputs;
@@ -109,6 +112,16 @@ struct StateDev {
     int has_clip, attach;
     long long* dbg_clk;     // optional phase timestamps (ESRNN_DEBUG_CLOCKS), block 0 thread 0
 };
+
+// Adam bias corrections of step t (StateDev::bc; exactly 1.0 past the table)
+template <typename Real>
+__device__ __forceinline__ double bias_c1(const StateDev<Real>& st, long long t) {
+    return t < st.bc_n ? st.bc[2 * t] : 1.0;
+}
+template <typename Real>
+__device__ __forceinline__ double bias_c2(const StateDev<Real>& st, long long t) {
+    return t < st.bc_n ? st.bc[2 * t + 1] : 1.0;
+}
 
 enum ErrCode { kErrNone = 0, kErrTrainLevel = 1, kErrObs = 2, kErrFcLevel = 3, kErrSeas = 4 };
 
@@ -141,6 +154,19 @@ __device__ __forceinline__ long long gtimer() {
 #define DBG_GT(st, i)                                                               \
     do {                                                                            \
         if ((st).dbg_clk && blockIdx.x == 0 && threadIdx.x == 0) (st).dbg_clk[80 + (i)] = gtimer(); \
+    } while (0)
+
+// step-5 kernel spans (ESRNN_DEBUG_CLOCKS): earliest / latest global-timer stamp over all
+// blocks in dbg_clk[100 + i] (the host seeds min slots with LLONG_MAX, max slots with 0)
+#define DBG_SPAN_MIN(st, step, i)                                                   \
+    do {                                                                            \
+        if ((st).dbg_clk && (step) == 5 && threadIdx.x == 0)                        \
+            atomicMin(reinterpret_cast<long long*>((st).dbg_clk) + 100 + (i), gtimer()); \
+    } while (0)
+#define DBG_SPAN_MAX(st, step, i)                                                   \
+    do {                                                                            \
+        if ((st).dbg_clk && (step) == 5 && threadIdx.x == 0)                        \
+            atomicMax(reinterpret_cast<long long*>((st).dbg_clk) + 100 + (i), gtimer()); \
     } while (0)
 
 #define DBG_CLK(st, i)                                                              \

@@ -249,6 +249,7 @@ struct DevPlan {
 };
 
 constexpr int kRows = kR;         // windows per K2 tile
+constexpr int64_t kBcSteps = 40960;  // Adam bias-correction table length (bc_table)
 
 }  // namespace
 
@@ -287,6 +288,7 @@ struct esrnn_trainer {
     DBuf<unsigned char> fX, fL, fS, dump_lv, dump_se;
     DBuf<double> loss_part, es_sq_part, red_sq_part, scal, loss_hist, f_out, f_smape, f_score, smape_sum;
     DBuf<unsigned int> done_ctr;
+    const double* bc_tab = nullptr;  // process-wide bias-correction table of this GPU (StateDev::bc)
     DBuf<long long> net_step;
     DBuf<long long> dbg_clk;  // ESRNN_DEBUG_CLOCKS: per-phase clock64 stamps of tile 0
     DBuf<int> errw;
@@ -406,6 +408,8 @@ struct esrnn_trainer {
         s.scal = scal.p;
         s.net_step = net_step.p;
         s.loss_hist = loss_hist.p;
+        s.bc = bc_tab;
+        s.bc_n = kBcSteps;
         s.err = errw.p;
         s.d_inputs = nullptr;
         s.d_targets = nullptr;
@@ -679,7 +683,9 @@ void ensure_capacity(Eng* e, int B) {
     const int S = e->S, T = e->T, I = e->I, O = e->O;
     const size_t r = e->rsz;
     e->Bcap = B;
-    e->kcap = std::min(e->N > 0 ? e->N : 1, B);
+    // slot capacity = the scan-state row stride, a multiple of K3's slots per block so every
+    // ES block stages whole 16-byte rows of its slots
+    e->kcap = (std::min(e->N > 0 ? e->N : 1, B) + kEsSlotsPerBlock - 1) / kEsSlotsPerBlock * kEsSlotsPerBlock;
     const int kc = e->kcap;
     e->tiles_cap = (B + kRows - 1) / kRows;
     e->es_blocks = (kc + kEsSlotsPerBlock - 1) / kEsSlotsPerBlock;
@@ -695,6 +701,28 @@ void ensure_capacity(Eng* e, int B) {
     e->d_targets.alloc(r * static_cast<size_t>(B) * O);
     e->d_seas.alloc(r * static_cast<size_t>(B) * O);
     e->d_levels.alloc(r * B);
+}
+
+// Adam bias corrections {1 - 0.9^t, 1 - 0.999^t} (trainer.hpp:617-620, :640-641) with the
+// host's std::pow, like the reference.  From t = kBcSteps on both are exactly 1.0 in double
+// (0.999^t < 2^-53 past t ~ 37,000), so one process-wide device table per GPU of kBcSteps
+// entries serves every trainer (kernels read 1.0 beyond it).
+const double* bc_table(int device) {
+    static std::mutex mu;
+    static std::map<int, double*> tabs;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = tabs.find(device);
+    if (it != tabs.end()) return it->second;
+    std::vector<double> h(2 * static_cast<size_t>(kBcSteps));
+    for (int64_t t = 0; t < kBcSteps; ++t) {
+        h[2 * t] = 1.0 - std::pow(0.9, static_cast<double>(t));
+        h[2 * t + 1] = 1.0 - std::pow(0.999, static_cast<double>(t));
+    }
+    double* d = nullptr;
+    CUDA_OK(cudaMalloc(&d, sizeof(double) * h.size()));
+    CUDA_OK(cudaMemcpy(d, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice));
+    tabs[device] = d;
+    return d;
 }
 
 // ------------------------------------------------------------------ plans
@@ -953,8 +981,11 @@ void launch_step(Eng* e, const PlanDev& pv, int s, bool grads, bool update, Stat
     const bool sharded = e->world > 1 && e->comm != nullptr;
     {
         KS k(e, 2);
-        // bit 0: finalise the step scalars here (single GPU); bit 1: the step applies updates
-        launch_finish<Real>(e, st, pv, s, (sharded ? 0 : 1) | (update ? 2 : 0), true);
+        // bit 0: a last CTA finalises the step scalars (single GPU, no update: K4 does not
+        // run); bit 1: the step applies updates; bit 2: single GPU updating step -- K4
+        // derives the scalars and K3 only advances Adam's step
+        const int fin = sharded ? (update ? 2 : 0) : (update ? 2 | 4 : 1);
+        launch_finish<Real>(e, st, pv, s, fin, true);
     }
     e->launches += 1;
     if (sharded) {
@@ -970,7 +1001,8 @@ void launch_step(Eng* e, const PlanDev& pv, int s, bool grads, bool update, Stat
         KS k(e, 4);
         // K4 waits for K3 the ordinary way: launched early under PDL its CTAs measured slower
         // (cfg1 +6%), while the next tile's early launch after K4 (and K3's after K2) pays
-        launch_k(e, false, k_adam<Real>, static_cast<int>((n + 255) / 256), 256, 0, st, pv, lay, s);
+        launch_k(e, false, k_adam<Real>, static_cast<int>((n + 255) / 256), 256, 0, st, pv, lay, s,
+                 sharded ? -1 : e->es_blocks, e->red_blocks);
         e->launches += 1;
     }
 }
@@ -1006,7 +1038,7 @@ void alloc_state(Eng* e) {
     e->net_step.alloc(1);
     e->errw.alloc(2);
     if (std::getenv("ESRNN_DEBUG_CLOCKS")) {
-        e->dbg_clk.alloc(96);
+        e->dbg_clk.alloc(128);
         e->dbg_clk.zero(e->stream);
     }
     for (auto* b : {&e->ps, &e->ps_m, &e->ps_v, &e->mW, &e->vW}) b->zero(e->stream);
@@ -1110,6 +1142,11 @@ double train_epoch_impl(Eng* e) {
     const PlanDev pv = e->epoch_plan.view(false);
     StateDev<Real> st = e->state<Real>();
     const bool use_graph = e->cfg.use_graphs >= 0 && !e->profiling;
+    if (e->dbg_clk.p) {
+        long long seed[16];
+        for (int i = 0; i < 16; ++i) seed[i] = (i == 2 || i == 5 || i == 6 || i == 8) ? 0 : LLONG_MAX;
+        CUDA_OK(cudaMemcpyAsync(e->dbg_clk.p + 100, seed, sizeof seed, cudaMemcpyHostToDevice, e->stream));
+    }
     CUDA_OK(cudaEventRecord(e->ev0, e->stream));
     if (use_graph) {
         // the graph captures exactly these arguments: same bytes -> same graph
@@ -1188,6 +1225,13 @@ double train_epoch_impl(Eng* e) {
                              "finish0 start, finish last, adam0 start) rel. scan start:");
         for (int i = 80; i < 87; ++i) std::fprintf(stderr, " %lld", c[i] - c[80]);
         std::fprintf(stderr, "\n");
+        long long sp[16];
+        CUDA_OK(cudaMemcpy(sp, e->dbg_clk.p + 100, sizeof sp, cudaMemcpyDeviceToHost));
+        std::fprintf(stderr, "[esrnn dbg] step-5 spans ns rel. tile launch: tile waited %lld end %lld | finish launch "
+                             "%lld waited %lld blocks-end %lld last-CTA-end %lld | adam start %lld end %lld | next tile "
+                             "waited %lld\n",
+                     sp[1] - sp[0], sp[2] - sp[0], sp[3] - sp[0], sp[4] - sp[0], sp[5] - sp[0], sp[6] - sp[0],
+                     sp[7] - sp[0], sp[8] - sp[0], sp[9] - sp[0]);
     }
     e->last_wr = e->cur_plan.wr;
     e->last_wa = e->cur_plan.wa;
@@ -1521,6 +1565,7 @@ esrnn_status esrnn_trainer_create(const esrnn_profile* profile, const esrnn_trai
                 }
             });
         }
+        e->bc_tab = bc_table(e->cfg.device);
         if (e->fp64) {
             alloc_state<double>(e.get());
             upload_values<double>(e.get(), values, category);

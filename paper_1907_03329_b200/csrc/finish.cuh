@@ -35,8 +35,8 @@ __device__ void finalize_scalars(StateDev<Real>& st, const PlanDev& pl, int s, d
     st.loss_hist[s] = loss_sum / pl.step_M[s];
     if (advance && st.err[0] == 0) {  // only a step that applies updates advances Adam's t
         const long long step = ++(*st.net_step);
-        st.scal[1] = 1.0 - pow(0.9, static_cast<double>(step));
-        st.scal[2] = 1.0 - pow(0.999, static_cast<double>(step));
+        st.scal[1] = bias_c1(st, step);
+        st.scal[2] = bias_c2(st, step);
     }
 }
 
@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
     };
     FCLK();
     DBG_GT(st, 4);
+    DBG_SPAN_MIN(st, s, 3);
     if (static_cast<int>(blockIdx.x) < es_blocks) {
         // ---------------- per-slot window-adjoint gather + reverse HW scan ---------------
         const int k0 = pl.step_slot_off[s];
@@ -95,16 +96,18 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
                 for (int ch = tid >> 5; ch * e16 < tp; ch += kFinishThreads / 32)
                     cp_async16(YS + lane * tp + ch * e16, st.vrm + (size_t)lrow * st.ldv + ch * e16);
             pdl_wait();
+            DBG_SPAN_MIN(st, s, 4);
             Real a_raw = 0, g_raw = 0;
             if (mine) {
                 a_raw = st.ps[lrow];
                 g_raw = st.ps[N + lrow];
             }
-            if (lane_ok) {
-                for (int t = tid >> 5; t < T; t += kFinishThreads / 32) {
-                    cp_async_elem(LV + t * bd + lane, st.lv + (size_t)t * kc + sl0 + lane);
-                    cp_async_elem(SE + t * bd + lane, st.se + (size_t)t * kc + sl0 + lane);
-                }
+            // forward levels / seasonalities of the block's slots: whole 16-byte pieces of the
+            // [t][kcap] rows (kcap and sl0 are multiples of kEsSlotsPerBlock)
+            for (int e = tid; e < 2 * T * (bd / e16); e += kFinishThreads) {
+                const int half = e / (T * (bd / e16)), r = e - half * T * (bd / e16);
+                const int t = r / (bd / e16), ch = r - t * (bd / e16);
+                cp_async16((half ? SE : LV) + t * bd + ch * e16, (half ? st.se : st.lv) + (size_t)t * kc + sl0 + ch * e16);
             }
             // ---- window adjoints: this block's windows are one contiguous range of the
             // CSR-ordered contribution table, staged in chunks of kEsChunk rows; then one warp
@@ -345,6 +348,15 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
         if (tid == 0) st.red_sq_part[gb] = tot;
     }
     FCLK();
+    DBG_SPAN_MAX(st, s, 5);
+    if (finalize & 4) {
+        // single GPU, updating step: K4 derives the step scalars from the partials itself
+        // (no last-CTA ticket on this kernel's tail); only a step that applies updates
+        // advances Adam's t (trainer.hpp:617) -- every block has passed pdl_wait, so the
+        // tile's error word is final
+        if (blockIdx.x == 0 && tid == 0 && st.err[0] == 0) ++(*st.net_step);
+        return;
+    }
     // ---------------- last CTA finalises ------------------------------------------------
     if (tid == 0) {
         __threadfence();
@@ -372,6 +384,7 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
     st.gbuf[lay.P_pad + 1] = static_cast<Real>(ls);
     if (finalize & 1) finalize_scalars(st, pl, s, all + es, ls, (finalize & 2) != 0);
     *st.done_ctr = 0;
+    DBG_SPAN_MAX(st, s, 6);
 }
 
 // After the NCCL all-reduce of gbuf (sharded mode): global squared norm + scalars.
@@ -412,35 +425,86 @@ __device__ __forceinline__ void adam_update(double& theta, double& m, double& v,
     theta -= lr * (m / c1) / (sqrt(v / c2) + 1e-8);
 }
 
+// es_blocks >= 0 (single GPU): every block first derives the step scalars -- clip scale
+// (trainer.hpp:603-615), bias corrections at the step K3 advanced (:617-620), step loss --
+// from K3's per-block partials with the same loads, order and tree as the last-CTA
+// finalisation, so all blocks hold bit-identical values and K3 needs no serial tail;
+// block 0 publishes them.  es_blocks < 0 (sharded): k_finalize already wrote st.scal.
 template <typename Real>
-__global__ void __launch_bounds__(256) k_adam(StateDev<Real> st, PlanDev pl, NetLayout lay, int s) {
+__global__ void __launch_bounds__(256) k_adam(StateDev<Real> st, PlanDev pl, NetLayout lay, int s, int es_blocks,
+                                              int red_blocks) {
+    __shared__ double red[32];
+    __shared__ double sc[3];
     pdl_trigger();
     pdl_wait();
     DBG_GT(st, 6);
+    DBG_SPAN_MIN(st, s, 7);
+    const int tid = threadIdx.x;
+    if (es_blocks >= 0) {
+        const int w0 = pl.step_win_off[s];
+        const int nt = (pl.step_win_off[s + 1] - w0 + kR - 1) / kR;
+        double es = 0.0, ls = 0.0, all = 0.0;
+        if (st.attach)
+            for (int b = tid; b < es_blocks; b += blockDim.x) es += __ldcg(st.es_sq_part + b);
+        for (int t = tid; t < nt; t += blockDim.x) ls += __ldcg(st.loss_part + t);
+        for (int b = tid; b < red_blocks; b += blockDim.x) all += __ldcg(st.red_sq_part + b);
+        es = block_sum(es, red);
+        ls = block_sum(ls, red);
+        all = block_sum(all, red);
+        if (tid == 0) {
+            double scale = 1.0;
+            if (st.has_clip) {
+                const double norm = sqrt(all + es);
+                if (norm > st.clip) scale = st.clip / norm;
+            }
+            const long long step = *st.net_step;
+            sc[0] = scale;
+            sc[1] = bias_c1(st, step);
+            sc[2] = bias_c2(st, step);
+            if (blockIdx.x == 0) {
+                st.gbuf[lay.P_pad] = static_cast<Real>(es);
+                st.gbuf[lay.P_pad + 1] = static_cast<Real>(ls);
+                st.scal[0] = scale;
+                st.scal[3] = ls / pl.step_M[s];
+                st.loss_hist[s] = ls / pl.step_M[s];
+                if (st.err[0] == 0) {
+                    st.scal[1] = sc[1];
+                    st.scal[2] = sc[2];
+                }
+            }
+        }
+    } else if (tid == 0) {
+        sc[0] = st.scal[0];
+        sc[1] = st.scal[1];
+        sc[2] = st.scal[2];
+    }
+    __syncthreads();
     if (st.err[0] != 0) return;  // the reference throws before apply_updates
     const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (q < lay.P_pad) {
         const Real g0 = st.gbuf[q], m0 = st.mW[q], v0 = st.vW[q], t0 = st.theta[q];
-        const double scale = st.scal[0], bc1 = st.scal[1], bc2 = st.scal[2];
+        const double scale = sc[0], bc1 = sc[1], bc2 = sc[2];
         double th = t0, m = m0, v = v0;
         adam_update(th, m, v, static_cast<double>(g0) * scale, st.lr_net, bc1, bc2);
         st.mW[q] = static_cast<Real>(m);
         st.vW[q] = static_cast<Real>(v);
         st.theta[q] = static_cast<Real>(th);
+        DBG_SPAN_MAX(st, s, 8);
         return;
     }
     if (!st.attach) return;
     const int k0 = pl.step_slot_off[s];
     const int k = pl.step_slot_off[s + 1] - k0;
     const long long slot = q - lay.P_pad;
+    DBG_SPAN_MAX(st, s, 8);
     if (slot >= k) return;
     const int N = st.N, S = lay.S;
     const int row = pl.slot_row[k0 + slot];
     const int steps = st.ps_steps[row] + 1;
     st.ps_steps[row] = steps;
-    const double scale = st.scal[0];
-    const double sc1 = 1.0 - pow(0.9, static_cast<double>(steps));
-    const double sc2 = 1.0 - pow(0.999, static_cast<double>(steps));
+    const double scale = sc[0];
+    const double sc1 = bias_c1(st, steps);
+    const double sc2 = bias_c2(st, steps);
     const Real* g = st.psg + (size_t)slot * (2 + S);
     for (int j0 = 0; j0 < 2 + S; j0 += 4) {
         Real pv[4], mv[4], vv[4], gv[4];

@@ -350,6 +350,7 @@ __global__ void __launch_bounds__(512) k_tile(StateDev<Real> st, PlanDev pl, Net
     if (nrows <= 0) return;
     int _dbg = 0;
     if (MODE == kTrain) DBG_GT(st, 2);
+    if (MODE == kTrain) DBG_SPAN_MIN(st, s, 0);
     DBG_CLK(st, 0);
     // row store of this tile's windows (K3 operands): [b][rs_ld], b = step-local window
     Real* __restrict__ rs = (MODE == kTrain) ? st.rowstore + (size_t)(tile * R) * lay.rs_ld : nullptr;
@@ -408,6 +409,10 @@ __global__ void __launch_bounds__(512) k_tile(StateDev<Real> st, PlanDev pl, Net
             cp_async16(YS + r * ts.tp + c * e16, st.vrm + (size_t)w_rowv[r] * st.ldv + c * e16);
         }
         pdl_wait();
+        if (MODE == kTrain) {
+            DBG_SPAN_MIN(st, s, 1);
+            DBG_SPAN_MIN(st, s - 1, 9);
+        }
         weights_tma();
         for (int e = tid; e < nrows * np; e += NT) {
             const int r = e / np, c = e - r * np;
@@ -757,6 +762,7 @@ __global__ void __launch_bounds__(512) k_tile(StateDev<Real> st, PlanDev pl, Net
         }
     }
     if (MODE == kTrain) DBG_GT(st, 3);
+    if (MODE == kTrain) DBG_SPAN_MAX(st, s, 2);
 }
 
 }  // namespace esrnn_dev
