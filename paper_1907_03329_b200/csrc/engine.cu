@@ -20,6 +20,7 @@
 #include <chrono>
 #include <list>
 #include <map>
+#include <condition_variable>
 #include <memory>
 #include <mutex>
 #include <random>
@@ -129,6 +130,9 @@ template <typename T>
 struct DBuf {
     T* p = nullptr;
     size_t n = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
     uint64_t seq = 0;  // allocation order (the owner frees in reverse, see release_buffers)
     void alloc(size_t count) {
         free();
@@ -151,6 +155,18 @@ template <typename T>
 struct PinnedBuf {
     T* p = nullptr;
     size_t n = 0;
+    PinnedBuf() = default;
+    PinnedBuf(const PinnedBuf&) = delete;
+    PinnedBuf& operator=(const PinnedBuf&) = delete;
+    PinnedBuf(PinnedBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr, o.n = 0; }
+    PinnedBuf& operator=(PinnedBuf&& o) noexcept {
+        if (this != &o) {
+            release();
+            p = o.p, n = o.n;
+            o.p = nullptr, o.n = 0;
+        }
+        return *this;
+    }
     void reserve(size_t count) {
         if (count <= n) return;
         release();
@@ -164,6 +180,57 @@ struct PinnedBuf {
     }
     ~PinnedBuf() { release(); }
 };
+
+// ------------------------------------------------------------------ host worker pool
+// Persistent host threads for the epoch plan (parallel over step ranges); the calling
+// thread takes tasks too.  One job at a time (run() is serialised).
+struct WorkerPool {
+    std::mutex run_mu, mu;
+    std::condition_variable cv, done_cv;
+    std::function<void(int)> job;
+    int n_tasks = 0, next = 0, done = 0;
+    uint64_t gen = 0;
+    std::vector<std::thread> th;
+    explicit WorkerPool(int n) {
+        for (int i = 0; i < n; ++i) th.emplace_back([this] { loop(); });
+    }
+    void drain(std::unique_lock<std::mutex>& lk) {
+        while (next < n_tasks) {
+            const int i = next++;
+            lk.unlock();
+            job(i);
+            lk.lock();
+            if (++done == n_tasks) done_cv.notify_all();
+        }
+    }
+    void loop() {
+        uint64_t seen = 0;
+        std::unique_lock<std::mutex> lk(mu);
+        for (;;) {
+            cv.wait(lk, [&] { return gen != seen; });
+            seen = gen;
+            drain(lk);
+        }
+    }
+    void run(int n, const std::function<void(int)>& f) {
+        std::lock_guard<std::mutex> serial(run_mu);
+        std::unique_lock<std::mutex> lk(mu);
+        job = f;
+        n_tasks = n;
+        next = done = 0;
+        ++gen;
+        cv.notify_all();
+        drain(lk);
+        done_cv.wait(lk, [&] { return done == n_tasks; });
+    }
+};
+WorkerPool& worker_pool() {
+    static WorkerPool* p = new WorkerPool(3);  // never destroyed (threads park in cv.wait)
+    return *p;
+}
+// stamp ids for slot dedupe: unique per planned step across the process (no re-init of
+// the per-row stamp arrays between steps / epochs)
+std::atomic<int64_t> g_stamp_id{1};
 
 // ------------------------------------------------------------------ graph cache
 // Epoch graphs keyed by the exact bytes of every launch argument they capture.  With the
@@ -216,12 +283,21 @@ struct HostPlan {
     int max_step_windows = 0, max_step_slots = 0;
 };
 
-// One epoch's host plan: the global shuffled window order and this rank's step plan.
+// One epoch's host plan: the global shuffled window order and this rank's step plan, built
+// in step-range chunks on the worker pool and packed (with offset fix-ups) into a pinned
+// buffer in upload order, so the epoch's plan goes to the device as a few async copies.
 struct EpochPlan {
     std::vector<int> wr, wa;
-    HostPlan hp;
+    std::vector<HostPlan> chunks;
     int steps = 0;
     bool ready = false;
+    // packed arrays: 11 int arrays then step_M (doubles), each at off[i] (bytes)
+    enum { kWRow, kWAnchor, kWSlot, kWFirst, kWCsr, kCsrAnchor, kSlotRow, kSlotWin, kSlotWinOff, kStepWinOff,
+           kStepSlotOff, kStepM, kArrays };
+    PinnedBuf<unsigned char> pin;
+    size_t off[kArrays + 1] = {};
+    size_t n_w = 0, n_slots = 0;
+    int max_step_windows = 0, max_step_slots = 0;
 };
 
 struct DevPlan {
@@ -298,7 +374,7 @@ struct esrnn_trainer {
     DevPlan epoch_plan, batch_plan;
     EpochPlan cur_plan, next_plan;
     std::thread plan_thread;  // builds the first epoch's plan while create finishes
-    std::vector<int> last_wr, last_wa;  // global window order of the last train_epoch
+    bool have_last = false;  // cur_plan holds the global window order of the last train_epoch
     PinnedBuf<int> pin_i;
     PinnedBuf<double> pin_d;
 
@@ -727,8 +803,8 @@ const double* bc_table(int device) {
 
 // ------------------------------------------------------------------ plans
 // trainer.hpp:493-501: slots in first-appearance order; per slot its windows in batch order.
-void append_step(Eng* e, HostPlan& hp, const int* rows, const int* anchors, int B, std::vector<int>& stamp,
-                 std::vector<int>& slot_id, int step) {
+void append_step(Eng* e, HostPlan& hp, const int* rows, const int* anchors, int B, std::vector<int64_t>& stamp,
+                 std::vector<int>& slot_id, int64_t step) {
     const int wbase = static_cast<int>(hp.w_row.size());
     const int sbase = static_cast<int>(hp.slot_row.size());
     const int cbase = static_cast<int>(hp.slot_win.size());
@@ -744,7 +820,7 @@ void append_step(Eng* e, HostPlan& hp, const int* rows, const int* anchors, int 
     int* __restrict__ wslot = hp.w_slot.data() + wbase;
     int* __restrict__ wfirst = hp.w_first.data() + wbase;
     int* __restrict__ srow = hp.slot_row.data() + sbase;
-    int* __restrict__ stp = stamp.data();
+    int64_t* __restrict__ stp = stamp.data();
     int* __restrict__ sid = slot_id.data();
     int nw = 0, ns = 0;
     for (int i = 0; i < B; ++i) {
@@ -1078,6 +1154,9 @@ void upload_values(Eng* e, const double* values, const int32_t* category) {
 // all_windows (trainer.hpp:214-223) + Rng::shuffle (matrix.hpp:203-205) in global order,
 // cut into batches (make_batches, trainer.hpp:82-102) and planned per step.
 void build_epoch_plan(Eng* e, EpochPlan& ep) {
+    using clk = std::chrono::steady_clock;
+    static const bool dbg_host = std::getenv("ESRNN_DEBUG_HOST") != nullptr;
+    const auto p0 = clk::now();
     const int I = e->I, O = e->O, T = e->T;
     const int per = T - O - I + 1;
     const int64_t nw = static_cast<int64_t>(e->N_global) * per;
@@ -1085,7 +1164,8 @@ void build_epoch_plan(Eng* e, EpochPlan& ep) {
     ep.wa.resize(nw);
     {
         // shuffle (row, anchor) pairs together: one random access per swap
-        std::vector<uint64_t> w(nw);
+        static thread_local std::vector<uint64_t> w;
+        w.resize(nw);
         int64_t n = 0;
         for (int r = 0; r < e->N_global; ++r)
             for (int a = I - 1; a <= T - O - 1; ++a) w[n++] = (static_cast<uint64_t>(r) << 32) | static_cast<uint32_t>(a);
@@ -1098,18 +1178,115 @@ void build_epoch_plan(Eng* e, EpochPlan& ep) {
             ep.wa[i] = static_cast<int>(static_cast<uint32_t>(w[i]));
         }
     }
+    const auto p1 = clk::now();
     const int B = e->cfg.batch_size;
-    ep.steps = static_cast<int>((nw + B - 1) / B);
-    HostPlan& hp = ep.hp;
-    plan_begin(hp, static_cast<size_t>(std::min<int64_t>(nw, static_cast<int64_t>(e->N) * per)), ep.steps);
-    std::vector<int> stamp(std::max(e->N, 1), -1), slot_id(std::max(e->N, 1), 0);
-    for (int s = 0; s < ep.steps; ++s) {
-        const int64_t start = static_cast<int64_t>(s) * B;
-        const int nb = static_cast<int>(std::min<int64_t>(nw, start + B) - start);
-        append_step(e, hp, ep.wr.data() + start, ep.wa.data() + start, nb, stamp, slot_id, s);
-        hp.step_M.push_back(static_cast<double>(nb) * O);
+    const int steps = static_cast<int>((nw + B - 1) / B);
+    ep.steps = steps;
+    // step-range chunks, planned in parallel (each with its own dedupe stamps)
+    const int nchunk = std::max(1, std::min(4, steps / 8));
+    ep.chunks.resize(nchunk);
+    const int64_t id0 = g_stamp_id.fetch_add(steps);
+    auto chunk_range = [&](int c, int& s0, int& s1) {
+        s0 = static_cast<int>(static_cast<int64_t>(steps) * c / nchunk);
+        s1 = static_cast<int>(static_cast<int64_t>(steps) * (c + 1) / nchunk);
+    };
+    worker_pool().run(nchunk, [&](int c) {
+        int s0, s1;
+        chunk_range(c, s0, s1);
+        HostPlan& hp = ep.chunks[c];
+        const size_t wcap = static_cast<size_t>(std::min<int64_t>(nw, static_cast<int64_t>(s1 - s0) * B));
+        plan_begin(hp, wcap, s1 - s0);
+        static thread_local std::vector<int64_t> stamp;
+        static thread_local std::vector<int> slot_id;
+        if (stamp.size() < static_cast<size_t>(std::max(e->N, 1))) {
+            stamp.assign(std::max(e->N, 1), -1);
+            slot_id.assign(std::max(e->N, 1), 0);
+        }
+        for (int s = s0; s < s1; ++s) {
+            const int64_t start = static_cast<int64_t>(s) * B;
+            const int nb = static_cast<int>(std::min<int64_t>(nw, start + B) - start);
+            append_step(e, hp, ep.wr.data() + start, ep.wa.data() + start, nb, stamp, slot_id, id0 + s);
+            hp.step_M.push_back(static_cast<double>(nb) * O);
+        }
+    });
+    const auto p2 = clk::now();
+    // pack into the pinned upload buffer (device layout order), chunks in parallel
+    std::vector<size_t> wb(nchunk + 1, 0), sb(nchunk + 1, 0);
+    ep.max_step_windows = ep.max_step_slots = 0;
+    for (int c = 0; c < nchunk; ++c) {
+        wb[c + 1] = wb[c] + ep.chunks[c].w_row.size();
+        sb[c + 1] = sb[c] + ep.chunks[c].slot_row.size();
+        ep.max_step_windows = std::max(ep.max_step_windows, ep.chunks[c].max_step_windows);
+        ep.max_step_slots = std::max(ep.max_step_slots, ep.chunks[c].max_step_slots);
     }
+    ep.n_w = wb[nchunk];
+    ep.n_slots = sb[nchunk];
+    const size_t cnt[EpochPlan::kArrays] = {ep.n_w, ep.n_w, ep.n_w, ep.n_w, ep.n_w, ep.n_w, ep.n_slots, ep.n_w,
+                                            ep.n_slots + 1, static_cast<size_t>(steps) + 1,
+                                            static_cast<size_t>(steps) + 1, static_cast<size_t>(steps)};
+    ep.off[0] = 0;
+    for (int i = 0; i < EpochPlan::kArrays; ++i) {
+        const size_t el = i == EpochPlan::kStepM ? sizeof(double) : sizeof(int);
+        ep.off[i + 1] = (ep.off[i] + cnt[i] * el + 15) & ~static_cast<size_t>(15);
+    }
+    ep.pin.reserve(ep.off[EpochPlan::kArrays]);
+    unsigned char* base = ep.pin.p;
+    auto arr = [&](int i) { return reinterpret_cast<int*>(base + ep.off[i]); };
+    arr(EpochPlan::kSlotWinOff)[0] = 0;
+    arr(EpochPlan::kStepWinOff)[0] = 0;
+    arr(EpochPlan::kStepSlotOff)[0] = 0;
+    worker_pool().run(nchunk, [&](int c) {
+        const HostPlan& hp = ep.chunks[c];
+        int s0, s1;
+        chunk_range(c, s0, s1);
+        auto put = [&](int i, const std::vector<int>& v, size_t at) {
+            if (!v.empty()) std::memcpy(arr(i) + at, v.data(), sizeof(int) * v.size());
+        };
+        put(EpochPlan::kWRow, hp.w_row, wb[c]);
+        put(EpochPlan::kWAnchor, hp.w_anchor, wb[c]);
+        put(EpochPlan::kWSlot, hp.w_slot, wb[c]);
+        put(EpochPlan::kWFirst, hp.w_first, wb[c]);
+        put(EpochPlan::kWCsr, hp.w_csr, wb[c]);
+        put(EpochPlan::kCsrAnchor, hp.csr_anchor, wb[c]);
+        put(EpochPlan::kSlotRow, hp.slot_row, sb[c]);
+        put(EpochPlan::kSlotWin, hp.slot_win, wb[c]);
+        const int wo = static_cast<int>(wb[c]), so = static_cast<int>(sb[c]);
+        int* swo = arr(EpochPlan::kSlotWinOff) + sb[c] + 1;
+        for (size_t k = 1; k < hp.slot_win_off.size(); ++k) swo[k - 1] = hp.slot_win_off[k] + wo;
+        int* stw = arr(EpochPlan::kStepWinOff) + s0 + 1;
+        int* sts = arr(EpochPlan::kStepSlotOff) + s0 + 1;
+        for (int k = 1; k <= s1 - s0; ++k) {
+            stw[k - 1] = hp.step_win_off[k] + wo;
+            sts[k - 1] = hp.step_slot_off[k] + so;
+        }
+        std::memcpy(reinterpret_cast<double*>(base + ep.off[EpochPlan::kStepM]) + s0, hp.step_M.data(),
+                    sizeof(double) * hp.step_M.size());
+    });
     ep.ready = true;
+    if (dbg_host)
+        std::fprintf(stderr, "[esrnn host] plan: shuffle %.0f us, steps %.0f us (%d chunks), pack %.0f us\n",
+                     std::chrono::duration<double, std::micro>(p1 - p0).count(),
+                     std::chrono::duration<double, std::micro>(p2 - p1).count(), nchunk,
+                     std::chrono::duration<double, std::micro>(clk::now() - p2).count());
+}
+
+// Async copies of a packed epoch plan (pinned) into the epoch DevPlan (capacity-sized, so
+// the pointers -- and the captured epoch graph -- stay stable across epochs).
+void upload_epoch_plan(Eng* e, const EpochPlan& ep, DevPlan& dp, size_t cap_w, size_t cap_steps) {
+    const size_t cw = std::max(cap_w, ep.n_w), cs = std::max(cap_steps, static_cast<size_t>(ep.steps));
+    DBuf<int>* dst[EpochPlan::kStepM] = {&dp.w_row, &dp.w_anchor, &dp.w_slot, &dp.w_first, &dp.w_csr,
+                                         &dp.csr_anchor, &dp.slot_row, &dp.slot_win, &dp.slot_win_off,
+                                         &dp.step_win_off, &dp.step_slot_off};
+    const size_t cap[EpochPlan::kStepM] = {cw, cw, cw, cw, cw, cw, cw, cw, cw + 1, cs + 1, cs + 1};
+    for (int i = 0; i < EpochPlan::kStepM; ++i) {
+        if (dst[i]->n < std::max<size_t>(cap[i], 1)) dst[i]->alloc(std::max<size_t>(cap[i], 1));
+        const size_t bytes = ep.off[i + 1] - ep.off[i];
+        const size_t used = std::min(bytes, sizeof(int) * dst[i]->n);
+        CUDA_OK(cudaMemcpyAsync(dst[i]->p, ep.pin.p + ep.off[i], used, cudaMemcpyHostToDevice, e->stream));
+    }
+    if (dp.step_M.n < std::max<size_t>(cs, 1)) dp.step_M.alloc(std::max<size_t>(cs, 1));
+    CUDA_OK(cudaMemcpyAsync(dp.step_M.p, ep.pin.p + ep.off[EpochPlan::kStepM], sizeof(double) * ep.steps,
+                            cudaMemcpyHostToDevice, e->stream));
 }
 
 template <typename Real>
@@ -1129,11 +1306,10 @@ double train_epoch_impl(Eng* e) {
     e->next_plan.ready = false;
     const int B = e->cfg.batch_size;
     const int steps = e->cur_plan.steps;
-    HostPlan& hp = e->cur_plan.hp;
     const auto h1 = clk::now();
     ensure_capacity(e, B);
     const size_t local_w = static_cast<size_t>(e->N) * per;
-    upload_plan(e, hp, e->epoch_plan, local_w, steps);
+    upload_epoch_plan(e, e->cur_plan, e->epoch_plan, local_w, steps);
     const auto h2 = clk::now();
     if (e->steps_cap < steps) {
         e->loss_hist.alloc(steps);
@@ -1233,13 +1409,13 @@ double train_epoch_impl(Eng* e) {
                      sp[1] - sp[0], sp[2] - sp[0], sp[3] - sp[0], sp[4] - sp[0], sp[5] - sp[0], sp[6] - sp[0],
                      sp[7] - sp[0], sp[8] - sp[0], sp[9] - sp[0]);
     }
-    e->last_wr = e->cur_plan.wr;
-    e->last_wa = e->cur_plan.wa;
+    e->have_last = true;
     // trainer.hpp:236-242: acc += loss * count, in batch order
+    const double* sm = reinterpret_cast<const double*>(e->cur_plan.pin.p + e->cur_plan.off[EpochPlan::kStepM]);
     double acc = 0.0, weight = 0.0;
     for (int s = 0; s < steps; ++s) {
-        acc += lh[s] * hp.step_M[s];
-        weight += hp.step_M[s];
+        acc += lh[s] * sm[s];
+        weight += sm[s];
     }
     return acc / weight;
 }
@@ -1261,7 +1437,8 @@ void run_batch_impl(Eng* e, int32_t B, const int32_t* rows, const int32_t* ancho
     if (count == 0.0) raise(ESRNN_CONTRACT_ERROR, "pinball: all-zero mask, mean undefined");
     HostPlan bp;
     plan_begin(bp);
-    std::vector<int> stamp(std::max(e->N, 1), -1), slot_id(std::max(e->N, 1), 0);
+    std::vector<int64_t> stamp(std::max(e->N, 1), -1);
+    std::vector<int> slot_id(std::max(e->N, 1), 0);
     append_step(e, bp, rows, anchors, B, stamp, slot_id, 0);
     bp.step_M.push_back(count);
     const int Bl = static_cast<int>(bp.w_row.size());
@@ -1482,6 +1659,11 @@ esrnn_status esrnn_trainer_create(const esrnn_profile* profile, const esrnn_trai
                                   const esrnn_dist* dist, esrnn_trainer** out) {
     *out = nullptr;
     std::unique_ptr<Eng> e(new Eng());
+    using clk = std::chrono::steady_clock;
+    static const bool dbg_host = std::getenv("ESRNN_DEBUG_HOST") != nullptr;
+    clk::time_point c[8];
+    int nc = 0;
+    c[nc++] = clk::now();
     esrnn_status st = guarded(g_create_err, [&] {
         validate_config(*profile, *cfg);
         if (n_series <= 0) raise(ESRNN_CONTRACT_ERROR, "trainer: no series");
@@ -1525,6 +1707,7 @@ esrnn_status esrnn_trainer_create(const esrnn_profile* profile, const esrnn_trai
         CUDA_OK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
         CUDA_OK(cudaEventCreate(&e->ev0));
         CUDA_OK(cudaEventCreate(&e->ev1));
+        c[nc++] = clk::now();
         if (e->world > 1) {
             // an id of 128 x 0xEE is the local-partials test mode: the shard runs its data
             // path but skips the collective, so a test can sum per-rank partials itself
@@ -1553,6 +1736,7 @@ esrnn_status esrnn_trainer_create(const esrnn_profile* profile, const esrnn_trai
         for (int64_t i = 0; i < static_cast<int64_t>(H) * H; ++i) e->w_host[e->off_nlw + i] = e->rng.uniform(-bound, bound);
         for (int64_t i = 0; i < static_cast<int64_t>(H) * e->O; ++i) e->w_host[e->off_outw + i] = e->rng.uniform(-bound, bound);
 
+        c[nc++] = clk::now();
         // the first epoch's shuffle is the next consumer of the trainer RNG: build its plan
         // on a helper thread while the device state is set up
         if (std::max(0, T - e->O - e->I + 1) > 0) {
@@ -1565,6 +1749,7 @@ esrnn_status esrnn_trainer_create(const esrnn_profile* profile, const esrnn_trai
                 }
             });
         }
+        c[nc++] = clk::now();
         e->bc_tab = bc_table(e->cfg.device);
         if (e->fp64) {
             alloc_state<double>(e.get());
@@ -1573,9 +1758,17 @@ esrnn_status esrnn_trainer_create(const esrnn_profile* profile, const esrnn_trai
             alloc_state<float>(e.get());
             upload_values<float>(e.get(), values, category);
         }
+        c[nc++] = clk::now();
         upload_theta(e.get());
         ensure_capacity(e.get(), cfg->batch_size);
         CUDA_OK(cudaStreamSynchronize(e->stream));
+        c[nc++] = clk::now();
+        if (dbg_host) {
+            std::fprintf(stderr, "[esrnn host] create:");
+            for (int i = 1; i < nc; ++i)
+                std::fprintf(stderr, " %.0f", std::chrono::duration<double, std::micro>(c[i] - c[i - 1]).count());
+            std::fprintf(stderr, " us (setup+stream, rng init, plan thread, alloc+values, theta+capacity+sync)\n");
+        }
     });
     if (st == ESRNN_OK) *out = e.release();
     return st;
@@ -1742,9 +1935,10 @@ esrnn_status esrnn_trainer_hw_state(esrnn_trainer* t, int64_t row, int64_t t_len
 }
 
 esrnn_status esrnn_trainer_last_epoch_windows(const esrnn_trainer* t, int32_t* rows, int32_t* anchors, int64_t n) {
-    if (n != static_cast<int64_t>(t->last_wr.size())) return ESRNN_SHAPE_ERROR;
-    std::memcpy(rows, t->last_wr.data(), sizeof(int32_t) * n);
-    std::memcpy(anchors, t->last_wa.data(), sizeof(int32_t) * n);
+    const std::vector<int>& wr = t->cur_plan.wr;
+    if (!t->have_last || n != static_cast<int64_t>(wr.size())) return ESRNN_SHAPE_ERROR;
+    std::memcpy(rows, wr.data(), sizeof(int32_t) * n);
+    std::memcpy(anchors, t->cur_plan.wa.data(), sizeof(int32_t) * n);
     return ESRNN_OK;
 }
 

@@ -324,3 +324,19 @@ def test_quality_parity_cfg1_15_epochs(engine, ref):
         scores[key] = (v.mean_smape, v.mean_mase, t.mean_smape, t.mean_mase)
     g, r = scores["gpu"], scores["ref"]
     assert all(abs(a - b) < 0.1 for a, b in zip(g, r)), (g, r)
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_two_live_trainers_interleaved_bit_identical(engine, oracle, precision):
+    """Two trainers of the same configuration alive at once, epochs interleaved: the shared
+    process-wide caches (device / pinned blocks, epoch graphs, plan worker pool) must not
+    couple them (test_trainer.cpp:218-230 determinism, with the C++ API's usage pattern)."""
+    prof, vals, cats = dataset(oracle, "quarterly", 9, 29)
+    cfg = TrainConfig(seed=42, batch_size=32, precision=precision)
+    t1 = Trainer((vals, cats), prof, cfg, api=engine)
+    t2 = Trainer((vals, cats), prof, cfg, api=engine)
+    for _ in range(4):
+        assert t1.train_epoch() == t2.train_epoch()
+        assert t1.last_epoch_windows() == t2.last_epoch_windows()
+    assert np.array_equal(t1.weights_flat(), t2.weights_flat())
+    assert t1.validate().mean_smape == t2.validate().mean_smape

@@ -1,6 +1,6 @@
 #!/bin/bash
 # quick GPU iteration: gpu tests, then bench summaries (args: bench configs, default cfg1)
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+echo "TESTS: $(timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -1)"
 for c in ${@:-cfg1}; do
   timeout 300 python bench.py --config $c --no-cpu-baseline > gpurun_out/chk_$c.json 2> gpurun_out/chk_$c.err || tail -5 gpurun_out/chk_$c.err
   python - "$c" <<'PY'
