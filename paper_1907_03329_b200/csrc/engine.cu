@@ -9,6 +9,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <climits>
 #include <cmath>
@@ -86,6 +87,8 @@ struct HostRng {
 struct BlockCache {
     std::mutex mu;
     std::map<std::pair<int, size_t>, std::vector<void*>> dev, host;
+    // (stream, event, event) triples per device: stream / event creation costs ~100 us
+    std::map<int, std::vector<std::array<void*, 3>>> streams;
 };
 BlockCache& block_cache() {
     static BlockCache* c = new BlockCache;  // never destroyed: no CUDA calls at exit
@@ -121,6 +124,31 @@ void cache_put(bool host, void* p, size_t cls) {
     BlockCache& c = block_cache();
     std::lock_guard<std::mutex> g(c.mu);
     (host ? c.host : c.dev)[{host ? -1 : current_device(), cls}].push_back(p);
+}
+
+// A trainer's stream and timing events, from the process-wide pool (created on a miss).
+void stream_get(cudaStream_t& st, cudaEvent_t& a, cudaEvent_t& b) {
+    BlockCache& c = block_cache();
+    const int dev = current_device();
+    {
+        std::lock_guard<std::mutex> g(c.mu);
+        auto& v = c.streams[dev];
+        if (!v.empty()) {
+            st = static_cast<cudaStream_t>(v.back()[0]);
+            a = static_cast<cudaEvent_t>(v.back()[1]);
+            b = static_cast<cudaEvent_t>(v.back()[2]);
+            v.pop_back();
+            return;
+        }
+    }
+    CUDA_OK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    CUDA_OK(cudaEventCreate(&a));
+    CUDA_OK(cudaEventCreate(&b));
+}
+void stream_put(cudaStream_t st, cudaEvent_t a, cudaEvent_t b) {
+    BlockCache& c = block_cache();
+    std::lock_guard<std::mutex> g(c.mu);
+    c.streams[current_device()].push_back({static_cast<void*>(st), static_cast<void*>(a), static_cast<void*>(b)});
 }
 
 // ------------------------------------------------------------------ device buffer
@@ -448,9 +476,7 @@ struct esrnn_trainer {
         release_buffers();
         graph.reset();
         if (comm) ncclCommDestroy(comm);
-        if (ev0) cudaEventDestroy(ev0);
-        if (ev1) cudaEventDestroy(ev1);
-        if (stream) cudaStreamDestroy(stream);
+        if (stream) stream_put(stream, ev0, ev1);  // idle: synchronised above
     }
 
     template <typename Real>
@@ -1126,28 +1152,42 @@ void alloc_state(Eng* e) {
     setup_kernel_attrs<Real>(e);
 }
 
+// Series values: the caller's row-major fp64 block goes to the device once; a layout kernel
+// converts it to Real and writes both device copies (time-major vals, padded row-major vrm).
+template <typename Real>
+__global__ void k_layout_values(const double* __restrict__ raw, int N, int LEN, int ldv, Real* __restrict__ vals,
+                                Real* __restrict__ vrm) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= static_cast<long long>(N) * ldv) return;
+    const int r = static_cast<int>(i / ldv), t = static_cast<int>(i - static_cast<long long>(r) * ldv);
+    const Real v = t < LEN ? static_cast<Real>(raw[static_cast<size_t>(r) * LEN + t]) : Real(0);
+    vrm[i] = v;
+    if (t < LEN) vals[static_cast<size_t>(t) * N + r] = v;
+}
+
 template <typename Real>
 void upload_values(Eng* e, const double* values, const int32_t* category) {
     const int N = e->N, LEN = e->LEN;
-    std::vector<Real> tm(static_cast<size_t>(LEN) * std::max(N, 1));
-    for (int r = 0; r < N; ++r)
-        for (int t = 0; t < LEN; ++t)
-            tm[static_cast<size_t>(t) * N + r] = static_cast<Real>(values[static_cast<size_t>(e->row0 + r) * LEN + t]);
-    CUDA_OK(cudaMemcpyAsync(e->vals.p, tm.data(), sizeof(Real) * tm.size(), cudaMemcpyHostToDevice, e->stream));
-    std::vector<Real> rm(static_cast<size_t>(e->ldv) * std::max(N, 1), Real(0));
-    for (int r = 0; r < N; ++r)
-        for (int t = 0; t < LEN; ++t)
-            rm[static_cast<size_t>(r) * e->ldv + t] = static_cast<Real>(values[static_cast<size_t>(e->row0 + r) * LEN + t]);
-    CUDA_OK(cudaMemcpyAsync(e->vrm.p, rm.data(), sizeof(Real) * rm.size(), cudaMemcpyHostToDevice, e->stream));
-    std::vector<signed char> c(std::max(N, 1), 5);
-    e->cat_host.assign(N, 5);
-    for (int r = 0; r < N; ++r) {
-        const int v = category ? category[e->row0 + r] : -1;
-        c[r] = static_cast<signed char>(v >= 0 && v < 6 ? v : 5);
-        e->cat_host[r] = c[r];
+    if (N > 0) {
+        DBuf<double> raw;
+        raw.alloc(static_cast<size_t>(N) * LEN);
+        CUDA_OK(cudaMemcpyAsync(raw.p, values + static_cast<size_t>(e->row0) * LEN, sizeof(double) * raw.n,
+                                cudaMemcpyHostToDevice, e->stream));
+        const long long n = static_cast<long long>(N) * e->ldv;
+        k_layout_values<Real><<<static_cast<int>((n + 255) / 256), 256, 0, e->stream>>>(
+            raw.p, N, LEN, e->ldv, reinterpret_cast<Real*>(e->vals.p), reinterpret_cast<Real*>(e->vrm.p));
+        e->launches += 1;
+        CUDA_OK(cudaGetLastError());
+        std::vector<signed char> c(N, 5);
+        e->cat_host.assign(N, 5);
+        for (int r = 0; r < N; ++r) {
+            const int v = category ? category[e->row0 + r] : -1;
+            c[r] = static_cast<signed char>(v >= 0 && v < 6 ? v : 5);
+            e->cat_host[r] = c[r];
+        }
+        CUDA_OK(cudaMemcpyAsync(e->cat.p, c.data(), c.size(), cudaMemcpyHostToDevice, e->stream));
+        CUDA_OK(cudaStreamSynchronize(e->stream));  // raw goes back to the block cache
     }
-    CUDA_OK(cudaMemcpyAsync(e->cat.p, c.data(), c.size(), cudaMemcpyHostToDevice, e->stream));
-    CUDA_OK(cudaStreamSynchronize(e->stream));
 }
 
 // ------------------------------------------------------------------ epoch
@@ -1704,9 +1744,7 @@ esrnn_status esrnn_trainer_create(const esrnn_profile* profile, const esrnn_trai
         if (cfg->device < 0 || cfg->device >= ndev) raise(ESRNN_CUDA_ERROR, "device %d out of range", cfg->device);
         CUDA_OK(cudaSetDevice(cfg->device));
         CUDA_OK(cudaDeviceGetAttribute(&g_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, cfg->device));
-        CUDA_OK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
-        CUDA_OK(cudaEventCreate(&e->ev0));
-        CUDA_OK(cudaEventCreate(&e->ev1));
+        stream_get(e->stream, e->ev0, e->ev1);
         c[nc++] = clk::now();
         if (e->world > 1) {
             // an id of 128 x 0xEE is the local-partials test mode: the shard runs its data
@@ -1980,11 +2018,20 @@ esrnn_status esrnn_release_cached_memory(void) {
             cudaSetDevice(kv.first.first);
             for (void* p : kv.second) cudaFree(p);
         }
+        for (auto& kv : c.streams) {
+            cudaSetDevice(kv.first);
+            for (auto& t : kv.second) {
+                cudaEventDestroy(static_cast<cudaEvent_t>(t[1]));
+                cudaEventDestroy(static_cast<cudaEvent_t>(t[2]));
+                cudaStreamDestroy(static_cast<cudaStream_t>(t[0]));
+            }
+        }
         cudaSetDevice(dev0);
         for (auto& kv : c.host)
             for (void* p : kv.second) cudaFreeHost(p);
         c.dev.clear();
         c.host.clear();
+        c.streams.clear();
     });
 }
 
