@@ -151,6 +151,28 @@ esrnn_status esrnn_trainer_set_per_series(esrnn_trainer* t, int64_t row_begin, i
                                           const double* alpha_raw, const double* gamma_raw,
                                           const double* seas_raw);
 
+/* Training state for exact resume (B200 extension).  The reference's checkpoint v1
+ * (checkpoint.hpp:37-46, :64-88) stores weights and per-series parameters only, so a
+ * reloaded trainer restarts Adam and the shuffle RNG; these two calls export / import the
+ * rest of what apply_updates and make_batches consume:
+ *   adam_m, adam_v [n_values]  network Adam moments in for_each_param order (trainer.hpp:625-631)
+ *   net_step                   the global Adam step (trainer.hpp:617)
+ *   ps_m, ps_v [n x (2+S)]     per-series moments for rows [row_begin, row_begin+n), each row
+ *                              {alpha, gamma, seas[S]} like PerSeriesParams (trainer.hpp:638-650)
+ *   ps_steps [n]               per-series Adam steps (trainer.hpp:639)
+ *   rng_text                   the trainer RNG (matrix.hpp:173-213) as std::mt19937_64's text
+ *                              form, taken before the next epoch's shuffle; NUL-terminated, at
+ *                              most ESRNN_RNG_TEXT_MAX bytes
+ * Every pointer is nullable (that part is skipped); rows must be owned by this rank. */
+#define ESRNN_RNG_TEXT_MAX 8192
+esrnn_status esrnn_trainer_get_train_state(esrnn_trainer* t, double* adam_m, double* adam_v, int64_t n_values,
+                                           int64_t row_begin, int64_t n, double* ps_m, double* ps_v,
+                                           int64_t* ps_steps, int64_t* net_step, char* rng_text, int64_t rng_cap);
+esrnn_status esrnn_trainer_set_train_state(esrnn_trainer* t, const double* adam_m, const double* adam_v,
+                                           int64_t n_values, int64_t row_begin, int64_t n, const double* ps_m,
+                                           const double* ps_v, const int64_t* ps_steps, int64_t net_step,
+                                           const char* rng_text);
+
 /* Trainer::train_epoch (trainer.hpp:234-243): shuffle (make_batches, trainer.hpp:82-102)
  * with the trainer RNG, one step per batch with updates; returns the
  * mask-weighted mean pinball loss. */

@@ -153,6 +153,19 @@ struct EvaluationScores {
     std::optional<double> mean_mase, naive_mean_mase;  // over series with a defined MASE
     std::size_t mase_undefined_count = 0;
 };
+// Exact-resume training state (B200 extension; the reference's Checkpoint, checkpoint.hpp:37-46,
+// stores weights and per-series parameters only): network Adam moments in for_each_param
+// order, the global Adam step, per-series moments {alpha, gamma, seas[S]} and steps for the
+// owned rows, and the trainer RNG in std::mt19937_64's text form before the next shuffle.
+// Serialise it next to a reference checkpoint (paper_1907_03329_b200/checkpoint.py writes it
+// as the file's "training_state" object).
+struct TrainState {
+    std::vector<double> adam_m, adam_v;
+    long long net_step = 0;
+    std::vector<double> ps_m, ps_v;  // (owned rows) x (2 + S), row-major
+    std::vector<long long> ps_steps;
+    std::string rng;
+};
 struct BenchmarkReport {
     double batched_s = 0.0, looped_s = 0.0, speedup = 0.0;
     int batch_size = 0, n_series = 0;
@@ -307,6 +320,39 @@ public:
         }
         v.smape_per_series = std::move(sm);
         return v;
+    }
+
+    TrainState train_state() const {
+        const std::size_t n = row_end_ - row_begin_, w = 2 + static_cast<std::size_t>(profile_.seasonality_length);
+        TrainState ts;
+        ts.adam_m.resize(static_cast<std::size_t>(n_values_));
+        ts.adam_v.resize(static_cast<std::size_t>(n_values_));
+        ts.ps_m.resize(n * w);
+        ts.ps_v.resize(n * w);
+        std::vector<std::int64_t> steps(n);
+        std::int64_t net = 0;
+        std::string rng(ESRNN_RNG_TEXT_MAX, '\0');
+        detail::check(esrnn_trainer_get_train_state(h_.get(), ts.adam_m.data(), ts.adam_v.data(), n_values_,
+                                                    static_cast<std::int64_t>(row_begin_), static_cast<std::int64_t>(n),
+                                                    ts.ps_m.data(), ts.ps_v.data(), steps.data(), &net, rng.data(),
+                                                    ESRNN_RNG_TEXT_MAX),
+                      h_.get());
+        ts.net_step = net;
+        ts.ps_steps.assign(steps.begin(), steps.end());
+        ts.rng = rng.c_str();
+        return ts;
+    }
+    void set_train_state(const TrainState& ts) {
+        const std::size_t n = row_end_ - row_begin_, w = 2 + static_cast<std::size_t>(profile_.seasonality_length);
+        if (ts.ps_m.size() != n * w || ts.ps_v.size() != n * w || ts.ps_steps.size() != n)
+            throw CheckpointError("train state: per-series state does not match the owned rows");
+        std::vector<std::int64_t> steps(ts.ps_steps.begin(), ts.ps_steps.end());
+        detail::check(esrnn_trainer_set_train_state(h_.get(), ts.adam_m.data(), ts.adam_v.data(),
+                                                    static_cast<std::int64_t>(ts.adam_m.size()),
+                                                    static_cast<std::int64_t>(row_begin_), static_cast<std::int64_t>(n),
+                                                    ts.ps_m.data(), ts.ps_v.data(), steps.data(), ts.net_step,
+                                                    ts.rng.c_str()),
+                      h_.get());
     }
 
     // cmd_evaluate (commands.hpp:312-338): forecast_at(O) against the test block when

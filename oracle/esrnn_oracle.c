@@ -1049,6 +1049,90 @@ esrnn_status esrnn_trainer_validate(esrnn_trainer* t, double* forecasts, double*
     return st;
 }
 
+/* Exact-resume training state (B200 extension of the ABI): the Adam moments / steps of
+ * apply_updates (trainer.hpp:602-655) and the trainer RNG in std::mt19937_64's text form
+ * (the 312 state words, then the position), which this MT19937-64 restatement shares. */
+esrnn_status esrnn_trainer_get_train_state(esrnn_trainer* t, double* adam_m, double* adam_v, int64_t n_values,
+                                           int64_t row_begin, int64_t n, double* ps_m, double* ps_v,
+                                           int64_t* ps_steps, int64_t* net_step, char* rng_text, int64_t rng_cap) {
+    const int S = t->S;
+    if ((adam_m || adam_v) && n_values != t->P)
+        return fail(t->err, ESRNN_CHECKPOINT_ERROR, "train state: %lld network values, expected %lld", (long long)n_values, (long long)t->P);
+    if (n < 0 || row_begin < 0 || row_begin + n > t->N) return fail(t->err, ESRNN_SHAPE_ERROR, "train state: rows out of range");
+    if (adam_m) memcpy(adam_m, t->mW, sizeof(double) * (size_t)t->P);
+    if (adam_v) memcpy(adam_v, t->vW, sizeof(double) * (size_t)t->P);
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t r = row_begin + i;
+        if (ps_m) {
+            ps_m[i * (2 + S)] = t->m_a[r];
+            ps_m[i * (2 + S) + 1] = t->m_g[r];
+            for (int j = 0; j < S; ++j) ps_m[i * (2 + S) + 2 + j] = t->m_s[(size_t)r * S + j];
+        }
+        if (ps_v) {
+            ps_v[i * (2 + S)] = t->v_a[r];
+            ps_v[i * (2 + S) + 1] = t->v_g[r];
+            for (int j = 0; j < S; ++j) ps_v[i * (2 + S) + 2 + j] = t->v_s[(size_t)r * S + j];
+        }
+        if (ps_steps) ps_steps[i] = t->steps[r];
+    }
+    if (net_step) *net_step = t->net_step;
+    if (rng_text) {
+        int64_t at = 0;
+        for (int i = 0; i <= MT_N; ++i) {
+            char buf[32];
+            const int k = i < MT_N ? snprintf(buf, sizeof buf, "%llu ", (unsigned long long)t->rng.mt[i])
+                                   : snprintf(buf, sizeof buf, "%d", t->rng.mti);
+            if (at + k + 1 > rng_cap) return fail(t->err, ESRNN_SHAPE_ERROR, "train state: rng buffer too small");
+            memcpy(rng_text + at, buf, (size_t)k);
+            at += k;
+        }
+        rng_text[at] = 0;
+    }
+    return ESRNN_OK;
+}
+
+esrnn_status esrnn_trainer_set_train_state(esrnn_trainer* t, const double* adam_m, const double* adam_v,
+                                           int64_t n_values, int64_t row_begin, int64_t n, const double* ps_m,
+                                           const double* ps_v, const int64_t* ps_steps, int64_t net_step,
+                                           const char* rng_text) {
+    const int S = t->S;
+    if ((adam_m || adam_v) && n_values != t->P)
+        return fail(t->err, ESRNN_CHECKPOINT_ERROR, "train state: %lld network values, expected %lld", (long long)n_values, (long long)t->P);
+    if (n < 0 || row_begin < 0 || row_begin + n > t->N) return fail(t->err, ESRNN_SHAPE_ERROR, "train state: rows out of range");
+    if (net_step < 0) return fail(t->err, ESRNN_CHECKPOINT_ERROR, "train state: negative Adam step");
+    rng_t g = t->rng;
+    if (rng_text) {
+        const char* p = rng_text;
+        for (int i = 0; i <= MT_N; ++i) {
+            char* end = NULL;
+            const unsigned long long v = strtoull(p, &end, 10);
+            if (end == p) return fail(t->err, ESRNN_CHECKPOINT_ERROR, "train state: malformed rng state");
+            if (i < MT_N) g.mt[i] = (uint64_t)v;
+            else g.mti = (int)v;
+            p = end;
+        }
+    }
+    if (adam_m) memcpy(t->mW, adam_m, sizeof(double) * (size_t)t->P);
+    if (adam_v) memcpy(t->vW, adam_v, sizeof(double) * (size_t)t->P);
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t r = row_begin + i;
+        if (ps_m) {
+            t->m_a[r] = ps_m[i * (2 + S)];
+            t->m_g[r] = ps_m[i * (2 + S) + 1];
+            for (int j = 0; j < S; ++j) t->m_s[(size_t)r * S + j] = ps_m[i * (2 + S) + 2 + j];
+        }
+        if (ps_v) {
+            t->v_a[r] = ps_v[i * (2 + S)];
+            t->v_g[r] = ps_v[i * (2 + S) + 1];
+            for (int j = 0; j < S; ++j) t->v_s[(size_t)r * S + j] = ps_v[i * (2 + S) + 2 + j];
+        }
+        if (ps_steps) t->steps[r] = (long)ps_steps[i];
+    }
+    t->net_step = (long)net_step;
+    t->rng = g;
+    return ESRNN_OK;
+}
+
 /* metrics.hpp:33-49 mase: forecast MAE over the in-sample seasonal-naive MAE; returns NAN for
  * the reference's std::nullopt (zero denominator) */
 static double mase(const double* ins, int n_ins, const double* a, const double* f, int n, int S) {

@@ -332,6 +332,96 @@ esrnn_status esrnn_trainer_validate(esrnn_trainer* t, double* forecasts, double*
     });
 }
 
+// Exact-resume training state straight from the reference Trainer's private members
+// (adam_net_, net_step_, adam_series_, rng_.gen_; trainer.hpp:446-457, :655-672).
+esrnn_status esrnn_trainer_get_train_state(esrnn_trainer* t, double* adam_m, double* adam_v, int64_t n_values,
+                                           int64_t row_begin, int64_t n, double* ps_m, double* ps_v,
+                                           int64_t* ps_steps, int64_t* net_step, char* rng_text, int64_t rng_cap) {
+    return guarded(t->err, [&] {
+        Trainer& tr = *t->tr;
+        const int S = tr.profile().seasonality_length;
+        int64_t off = 0;
+        tr.weights_.for_each_param([&](const std::string& name, const Matrix& m) {
+            const auto& st = tr.adam_net_.at(name);
+            for (std::size_t e = 0; e < m.size(); ++e, ++off) {
+                if (off >= n_values) continue;
+                if (adam_m) adam_m[off] = st.m.data()[e];
+                if (adam_v) adam_v[off] = st.v.data()[e];
+            }
+        });
+        if ((adam_m || adam_v) && off != n_values) throw CheckpointError("train state: network size mismatch");
+        if (row_begin < 0 || n < 0 || row_begin + n > static_cast<int64_t>(tr.series_count()))
+            throw ShapeError("train state: rows out of range");
+        for (int64_t i = 0; i < n; ++i) {
+            const auto& sa = tr.adam_series_[static_cast<std::size_t>(row_begin + i)];
+            if (ps_m) {
+                ps_m[i * (2 + S)] = sa.m_alpha;
+                ps_m[i * (2 + S) + 1] = sa.m_gamma;
+                for (int j = 0; j < S; ++j) ps_m[i * (2 + S) + 2 + j] = sa.m_seas[j];
+            }
+            if (ps_v) {
+                ps_v[i * (2 + S)] = sa.v_alpha;
+                ps_v[i * (2 + S) + 1] = sa.v_gamma;
+                for (int j = 0; j < S; ++j) ps_v[i * (2 + S) + 2 + j] = sa.v_seas[j];
+            }
+            if (ps_steps) ps_steps[i] = sa.steps;
+        }
+        if (net_step) *net_step = tr.net_step_;
+        if (rng_text) {
+            std::ostringstream os;
+            os << tr.rng_.gen_;
+            const std::string txt = os.str();
+            if (static_cast<int64_t>(txt.size()) + 1 > rng_cap) throw ShapeError("train state: rng buffer too small");
+            std::memcpy(rng_text, txt.c_str(), txt.size() + 1);
+        }
+    });
+}
+
+esrnn_status esrnn_trainer_set_train_state(esrnn_trainer* t, const double* adam_m, const double* adam_v,
+                                           int64_t n_values, int64_t row_begin, int64_t n, const double* ps_m,
+                                           const double* ps_v, const int64_t* ps_steps, int64_t net_step,
+                                           const char* rng_text) {
+    return guarded(t->err, [&] {
+        Trainer& tr = *t->tr;
+        const int S = tr.profile().seasonality_length;
+        int64_t total = 0;
+        tr.weights_.for_each_param([&](const std::string&, const Matrix& m) { total += static_cast<int64_t>(m.size()); });
+        if ((adam_m || adam_v) && total != n_values) throw CheckpointError("train state: network size mismatch");
+        if (row_begin < 0 || n < 0 || row_begin + n > static_cast<int64_t>(tr.series_count()))
+            throw ShapeError("train state: rows out of range");
+        std::mt19937_64 g = tr.rng_.gen_;
+        if (rng_text) {
+            std::istringstream is(rng_text);
+            is >> g;
+            if (is.fail()) throw CheckpointError("train state: malformed rng state");
+        }
+        int64_t off = 0;
+        tr.weights_.for_each_param([&](const std::string& name, const Matrix& m) {
+            auto& st = tr.adam_net_.at(name);
+            for (std::size_t e = 0; e < m.size(); ++e, ++off) {
+                if (adam_m) st.m.data()[e] = adam_m[off];
+                if (adam_v) st.v.data()[e] = adam_v[off];
+            }
+        });
+        for (int64_t i = 0; i < n; ++i) {
+            auto& sa = tr.adam_series_[static_cast<std::size_t>(row_begin + i)];
+            if (ps_m) {
+                sa.m_alpha = ps_m[i * (2 + S)];
+                sa.m_gamma = ps_m[i * (2 + S) + 1];
+                for (int j = 0; j < S; ++j) sa.m_seas[j] = ps_m[i * (2 + S) + 2 + j];
+            }
+            if (ps_v) {
+                sa.v_alpha = ps_v[i * (2 + S)];
+                sa.v_gamma = ps_v[i * (2 + S) + 1];
+                for (int j = 0; j < S; ++j) sa.v_seas[j] = ps_v[i * (2 + S) + 2 + j];
+            }
+            if (ps_steps) sa.steps = static_cast<long>(ps_steps[i]);
+        }
+        tr.net_step_ = static_cast<long>(net_step);
+        tr.rng_.gen_ = g;
+    });
+}
+
 // cmd_evaluate / detail::score_forecasts (commands.hpp:285-338) restated over the reference's
 // own metrics.hpp smape / mase / seasonal_naive (commands.hpp needs the absent vendored json)
 esrnn_status esrnn_trainer_evaluate(esrnn_trainer* t, int32_t against_test, double* forecasts, double* smape_o,

@@ -24,6 +24,7 @@
 #include <condition_variable>
 #include <memory>
 #include <mutex>
+#include <sstream>
 #include <random>
 #include <stdexcept>
 #include <string>
@@ -315,6 +316,7 @@ struct HostPlan {
 // in step-range chunks on the worker pool and packed (with offset fix-ups) into a pinned
 // buffer in upload order, so the epoch's plan goes to the device as a few async copies.
 struct EpochPlan {
+    std::mt19937_64 rng_before;  // trainer RNG before this epoch's shuffle (exact-resume state)
     std::vector<int> wr, wa;
     std::vector<HostPlan> chunks;
     int steps = 0;
@@ -677,7 +679,8 @@ void build_layout(Eng* e) {
     e->off_outb = off;
     off += O;
     e->P = off;
-    // head: nl_w^T [H][ldkh], nl_b [H], out_w^T [O][ldkh], out_b [O] (one contiguous segment)
+    // head: nl_w^T [H][ldkh], nl_b [H], out_w^T [O][ldkh], out_b [O] (one contiguous segment,
+    // 4-aligned matrices)
     pad4();
     const int ldkh = lay.ldkh;
     lay.c_nlw = coff;
@@ -687,6 +690,7 @@ void build_layout(Eng* e) {
     lay.c_nlb = coff;
     for (int i = 0; i < H; ++i) e->live_flat.push_back(e->off_nlb + i);
     coff += H;
+    pad4();  // out_w^T rows are read 16 bytes at a time
     lay.c_outw = coff;
     for (int o = 0; o < O; ++o)
         for (int k = 0; k < ldkh; ++k) e->live_flat.push_back(k < H ? e->off_outw + static_cast<int64_t>(k) * O + o : -1);
@@ -1200,6 +1204,7 @@ void build_epoch_plan(Eng* e, EpochPlan& ep) {
     const int I = e->I, O = e->O, T = e->T;
     const int per = T - O - I + 1;
     const int64_t nw = static_cast<int64_t>(e->N_global) * per;
+    ep.rng_before = e->rng.gen;
     ep.wr.resize(nw);
     ep.wa.resize(nw);
     {
@@ -1902,6 +1907,112 @@ esrnn_status esrnn_trainer_set_per_series(esrnn_trainer* t, int64_t r0, int64_t 
                                           const double* s) {
     return guarded(t->err, [&] {
         ps_io(t, r0, n, const_cast<double*>(a), const_cast<double*>(g), const_cast<double*>(s), false);
+    });
+}
+
+// ---- exact-resume training state (B200 extension; checkpoint.hpp:37-46 saves neither) ----
+esrnn_status esrnn_trainer_get_train_state(esrnn_trainer* t, double* adam_m, double* adam_v, int64_t n_values,
+                                           int64_t row_begin, int64_t n, double* ps_m, double* ps_v,
+                                           int64_t* ps_steps, int64_t* net_step, char* rng_text, int64_t rng_cap) {
+    return guarded(t->err, [&] {
+        CUDA_OK(cudaSetDevice(t->cfg.device));
+        if (adam_m || adam_v) {
+            if (n_values != t->P) raise(ESRNN_CHECKPOINT_ERROR, "train state: %lld network values, expected %lld", (long long)n_values, (long long)t->P);
+            const size_t np = static_cast<size_t>(t->lay.P_pad);
+            std::vector<double> c(np);
+            for (int which = 0; which < 2; ++which) {
+                double* dst = which ? adam_v : adam_m;
+                if (!dst) continue;
+                download_real(t, (which ? t->vW : t->mW).p, np, c.data());
+                std::fill(dst, dst + t->P, 0.0);  // structurally dead entries: m = v = 0 (zero gradients)
+                for (size_t i = 0; i < np; ++i)
+                    if (t->live_flat[i] >= 0) dst[t->live_flat[i]] = c[i];
+            }
+        }
+        const int S = t->S, N = t->N;
+        const int64_t lr0 = row_begin - t->row0;
+        if (n < 0 || lr0 < 0 || lr0 + n > N) raise(ESRNN_SHAPE_ERROR, "train state: rows not owned by this rank");
+        if (n > 0 && (ps_m || ps_v || ps_steps)) {
+            std::vector<double> buf(n);
+            for (int which = 0; which < 2; ++which) {
+                double* dst = which ? ps_v : ps_m;
+                if (!dst) continue;
+                for (int j = 0; j < 2 + S; ++j) {
+                    download_real(t, (which ? t->ps_v : t->ps_m).p + t->rsz * (static_cast<size_t>(j) * N + lr0), n, buf.data());
+                    for (int64_t i = 0; i < n; ++i) dst[i * (2 + S) + j] = buf[i];
+                }
+            }
+            if (ps_steps) {
+                std::vector<int> st(n);
+                CUDA_OK(cudaMemcpy(st.data(), t->ps_steps.p + lr0, sizeof(int) * n, cudaMemcpyDeviceToHost));
+                for (int64_t i = 0; i < n; ++i) ps_steps[i] = st[i];
+            }
+        }
+        if (net_step) {
+            long long v = 0;
+            CUDA_OK(cudaMemcpy(&v, t->net_step.p, sizeof v, cudaMemcpyDeviceToHost));
+            *net_step = v;
+        }
+        if (rng_text) {
+            // the trainer RNG before the next epoch's shuffle (the engine plans epochs ahead)
+            t->join_plan();
+            std::ostringstream os;
+            os << (t->next_plan.ready ? t->next_plan.rng_before : t->rng.gen);
+            const std::string txt = os.str();
+            if (static_cast<int64_t>(txt.size()) + 1 > rng_cap) raise(ESRNN_SHAPE_ERROR, "train state: rng buffer too small (%zu)", txt.size() + 1);
+            std::memcpy(rng_text, txt.c_str(), txt.size() + 1);
+        }
+    });
+}
+
+esrnn_status esrnn_trainer_set_train_state(esrnn_trainer* t, const double* adam_m, const double* adam_v,
+                                           int64_t n_values, int64_t row_begin, int64_t n, const double* ps_m,
+                                           const double* ps_v, const int64_t* ps_steps, int64_t net_step,
+                                           const char* rng_text) {
+    return guarded(t->err, [&] {
+        CUDA_OK(cudaSetDevice(t->cfg.device));
+        if (adam_m || adam_v) {
+            if (n_values != t->P) raise(ESRNN_CHECKPOINT_ERROR, "train state: %lld network values, expected %lld", (long long)n_values, (long long)t->P);
+            const size_t np = static_cast<size_t>(t->lay.P_pad);
+            std::vector<double> c(np);
+            for (int which = 0; which < 2; ++which) {
+                const double* src = which ? adam_v : adam_m;
+                if (!src) continue;
+                for (size_t i = 0; i < np; ++i) c[i] = t->live_flat[i] >= 0 ? src[t->live_flat[i]] : 0.0;
+                upload_real(t, (which ? t->vW : t->mW).p, c.data(), np);
+            }
+        }
+        const int S = t->S, N = t->N;
+        const int64_t lr0 = row_begin - t->row0;
+        if (n < 0 || lr0 < 0 || lr0 + n > N) raise(ESRNN_SHAPE_ERROR, "train state: rows not owned by this rank");
+        if (n > 0) {
+            std::vector<double> buf(n);
+            for (int which = 0; which < 2; ++which) {
+                const double* src = which ? ps_v : ps_m;
+                if (!src) continue;
+                for (int j = 0; j < 2 + S; ++j) {
+                    for (int64_t i = 0; i < n; ++i) buf[i] = src[i * (2 + S) + j];
+                    upload_real(t, (which ? t->ps_v : t->ps_m).p + t->rsz * (static_cast<size_t>(j) * N + lr0), buf.data(), n);
+                }
+            }
+            if (ps_steps) {
+                std::vector<int> st(n);
+                for (int64_t i = 0; i < n; ++i) st[i] = static_cast<int>(ps_steps[i]);
+                CUDA_OK(cudaMemcpy(t->ps_steps.p + lr0, st.data(), sizeof(int) * n, cudaMemcpyHostToDevice));
+            }
+        }
+        if (net_step < 0) raise(ESRNN_CHECKPOINT_ERROR, "train state: negative Adam step");
+        const long long v = net_step;
+        CUDA_OK(cudaMemcpy(t->net_step.p, &v, sizeof v, cudaMemcpyHostToDevice));
+        if (rng_text) {
+            std::istringstream is(rng_text);
+            std::mt19937_64 g;
+            is >> g;
+            if (is.fail()) raise(ESRNN_CHECKPOINT_ERROR, "train state: malformed rng state");
+            t->join_plan();
+            t->rng.gen = g;
+            t->next_plan.ready = false;  // re-planned from the restored RNG at the next epoch
+        }
     });
 }
 

@@ -252,6 +252,22 @@ class EvaluationResult:  # cmd_evaluate's scored rows (commands.hpp:285-338) for
 
 
 @dataclass
+class TrainState:
+    """What the reference's checkpoint v1 leaves out (checkpoint.hpp:37-46) and apply_updates /
+    make_batches consume: network Adam moments (for_each_param order, trainer.hpp:625-631),
+    the global Adam step (:617), per-series moments and steps (:638-650; rows {alpha, gamma,
+    seas[S]}), and the trainer RNG (matrix.hpp:173-213) before the next epoch's shuffle."""
+    adam_m: np.ndarray
+    adam_v: np.ndarray
+    net_step: int
+    ps_m: np.ndarray      # (n, 2 + S), rows [row_begin, row_begin + n)
+    ps_v: np.ndarray
+    ps_steps: np.ndarray  # (n,) int64
+    rng: str              # std::mt19937_64 text form
+    row_begin: int = 0
+
+
+@dataclass
 class ForecastResult:  # trainer.hpp:129-132
     ids: list
     forecasts: np.ndarray
@@ -573,6 +589,31 @@ class Trainer:
             res.model = aggregate(cats, fname, arrs[0], arrs[1])
             res.naive = aggregate(cats, fname, arrs[2], arrs[3])
         return res
+
+    def train_state(self) -> TrainState:
+        n = self.row_end - self.row_begin
+        S = self._profile.seasonality_length
+        m, v = np.zeros(self.n_values), np.zeros(self.n_values)
+        pm, pv = np.zeros((n, 2 + S)), np.zeros((n, 2 + S))
+        steps = np.zeros(n, dtype=np.int64)
+        net = C.c_int64()
+        buf = C.create_string_buffer(N.RNG_TEXT_MAX)
+        lp = C.POINTER(C.c_int64)
+        self._chk(self.api.lib.esrnn_trainer_get_train_state(
+            self._h, N.dptr(m), N.dptr(v), self.n_values, self.row_begin, n, N.dptr(pm), N.dptr(pv),
+            steps.ctypes.data_as(lp), C.byref(net), buf, N.RNG_TEXT_MAX))
+        return TrainState(m, v, int(net.value), pm, pv, steps, buf.value.decode(), self.row_begin)
+
+    def set_train_state(self, ts: TrainState) -> None:
+        S = self._profile.seasonality_length
+        pm = np.ascontiguousarray(ts.ps_m, dtype=np.float64).reshape(-1, 2 + S)
+        pv = np.ascontiguousarray(ts.ps_v, dtype=np.float64).reshape(-1, 2 + S)
+        steps = np.ascontiguousarray(ts.ps_steps, dtype=np.int64)
+        m = np.ascontiguousarray(ts.adam_m, dtype=np.float64)
+        v = np.ascontiguousarray(ts.adam_v, dtype=np.float64)
+        self._chk(self.api.lib.esrnn_trainer_set_train_state(
+            self._h, N.dptr(m), N.dptr(v), m.size, ts.row_begin, pm.shape[0], N.dptr(pm), N.dptr(pv),
+            steps.ctypes.data_as(C.POINTER(C.c_int64)), int(ts.net_step), ts.rng.encode()))
 
     def last_epoch_windows(self) -> list:
         """Global shuffled (row, anchor) order consumed by the last train_epoch."""

@@ -167,6 +167,25 @@ int main() {
             auto v2 = tr.validate();
             CHECK(v1.mean_smape == v2.mean_smape);
         }
+        // exact resume: weights + per-series (the reference's checkpoint) + TrainState
+        {
+            Trainer a(dataset(5, 17, 28, 4, 0.03), tiny_profile(), tiny_config(4, prec));
+            a.train_epoch();
+            const StackWeights w = a.weights();
+            std::map<std::string, PerSeriesParams> ps;
+            for (std::size_t i = 0; i < a.series_count(); ++i) ps.emplace(a.series(i).id, a.per_series_params(i));
+            const TrainState ts = a.train_state();
+            CHECK(ts.net_step > 0 && !ts.rng.empty());
+            const double la = a.train_epoch();
+            Trainer b(dataset(5, 17, 28, 4, 0.03), tiny_profile(), tiny_config(99, prec));
+            b.set_weights(w);
+            b.set_per_series(ps);
+            b.set_train_state(ts);
+            CHECK(b.train_epoch() == la);
+            TrainState bad = ts;
+            bad.rng = "not a state";
+            CHECK(throws<CheckpointError>([&] { b.set_train_state(bad); }));
+        }
         // same seed reproduces the loss trajectory bit for bit (test_trainer.cpp:218-230)
         {
             Trainer t1(dataset(3, 29, 28, 4, 0.03), tiny_profile(), tiny_config(42, prec));
