@@ -227,6 +227,19 @@ esrnn_status esrnn_trainer_validate(esrnn_trainer* t, double* forecasts, double*
 esrnn_status esrnn_trainer_evaluate(esrnn_trainer* t, int32_t against_test, double* forecasts, double* smape,
                                     double* mase, double* naive_smape, double* naive_mase, double* totals);
 
+/* forward_stack (network.hpp:190-210; plain mirror :268-287) over a general input sequence
+ * with this trainer's StackWeights: the dilated recurrence with full LSTM cells (forget gates,
+ * recurrent matrices, (h, c) from step t - d; lstm_cell :148-163, dilated_lstm_layer :167-184)
+ * that the sequence-length-1 training path never exercises.
+ *   inputs [seq_len][B][I+6] row-major (one (B, I+6) matrix per step), out [B][O]
+ *   out_bar [B][O] (nullable): upstream adjoint of out; then weights_bar [n_values]
+ *   (for_each_param order) and inputs_bar [seq_len][B][I+6] (each nullable) receive the
+ *   reverse-mode adjoints (Tape::backward of the same graph, autodiff.hpp:397-631).
+ * seq_len < 1 -> ESRNN_CONTRACT_ERROR ("forward_stack: empty sequence"). */
+esrnn_status esrnn_trainer_forward_stack(esrnn_trainer* t, int32_t seq_len, int32_t B, const double* inputs,
+                                         double* out, const double* out_bar, double* weights_bar,
+                                         double* inputs_bar);
+
 /* HWState of hybrid_primer(values[0:t_len], per_series_params(row)) (holt_winters.hpp:66-97):
  * levels[t_len], seasonalities[t_len + S].  Inspection hook for the scan KATs. */
 esrnn_status esrnn_trainer_hw_state(esrnn_trainer* t, int64_t row, int64_t t_len, double* levels,

@@ -1049,6 +1049,156 @@ esrnn_status esrnn_trainer_validate(esrnn_trainer* t, double* forecasts, double*
     return st;
 }
 
+/* network.hpp:148-210 forward_stack over a general sequence (full LSTM cells with forget
+ * gates, recurrent matrices and (h, c) from step t-d), and the adjoints of Tape::backward
+ * for an upstream out_bar (autodiff.hpp:428-610: MatMul / Add / Mul / Logistic / Tanh). */
+esrnn_status esrnn_trainer_forward_stack(esrnn_trainer* t, int32_t T, int32_t B, const double* X, double* out,
+                                         const double* obar, double* wbar, double* xbar) {
+    if (T < 1) return fail(t->err, ESRNN_CONTRACT_ERROR, "forward_stack: empty sequence");
+    if (B < 1) return fail(t->err, ESRNN_SHAPE_ERROR, "forward_stack: empty batch");
+    const int L = t->L, H = t->H, O = t->O, in0 = t->in0, G = 4 * H;
+    int dil[MAXL], res_src[MAXL];
+    for (int l = 0, b = 0, first = 0; b < t->nb; first += t->blen[b], ++b)
+        for (int j = 0; j < t->blen[b]; ++j, ++l) {
+            dil[l] = t->prof.dilations[l];
+            res_src[l] = (b > 0 && j == t->blen[b] - 1) ? first - 1 : -1;
+        }
+    const size_t LTB = (size_t)L * T * B;
+    double* gates = (double*)xcalloc(LTB * G, sizeof(double));
+    double* cs = (double*)xcalloc(LTB * H, sizeof(double));
+    double* hr = (double*)xcalloc(LTB * H, sizeof(double));
+    double* cur = (double*)xcalloc(LTB * H, sizeof(double));
+    double* z = (double*)xcalloc((size_t)B * H, sizeof(double));
+#define SI(l, tt, r) ((((size_t)(l) * T + (tt)) * B + (r)))
+    const double* W = t->W;
+    for (int l = 0; l < L; ++l) {
+        const int K = t->layer_in[l], d = dil[l];
+        for (int tt = 0; tt < T; ++tt)
+            for (int r = 0; r < B; ++r) {
+                const double* x = l == 0 ? X + ((size_t)tt * B + r) * in0 : cur + SI(l - 1, tt, r) * H;
+                double* g = gates + SI(l, tt, r) * G;
+                for (int j = 0; j < G; ++j) {
+                    double a = 0.0;
+                    for (int k = 0; k < K; ++k) a += x[k] * W[t->off_win[l] + (int64_t)k * G + j];
+                    if (tt >= d) {
+                        const double* hp = hr + SI(l, tt - d, r) * H;
+                        double a2 = 0.0;
+                        for (int k = 0; k < H; ++k) a2 += hp[k] * W[t->off_wrec[l] + (int64_t)k * G + j];
+                        a += a2;
+                    }
+                    a += W[t->off_bias[l] + j];
+                    g[j] = (j >= 2 * H && j < 3 * H) ? fm_tanh(a) : fm_logistic(a);
+                }
+                for (int j = 0; j < H; ++j) {
+                    const double c = (tt >= d ? g[H + j] * cs[SI(l, tt - d, r) * H + j] : 0.0) + g[j] * g[2 * H + j];
+                    const double h = g[3 * H + j] * fm_tanh(c);
+                    cs[SI(l, tt, r) * H + j] = c;
+                    hr[SI(l, tt, r) * H + j] = h;
+                    cur[SI(l, tt, r) * H + j] = res_src[l] >= 0 ? h + cur[SI(res_src[l], tt, r) * H + j] : h;
+                }
+            }
+    }
+    for (int r = 0; r < B; ++r) {
+        const double* last = cur + SI(L - 1, T - 1, r) * H;
+        for (int j = 0; j < H; ++j) {
+            double a = 0.0;
+            for (int k = 0; k < H; ++k) a += last[k] * W[t->off_nlw + (int64_t)k * H + j];
+            z[(size_t)r * H + j] = fm_tanh(a + W[t->off_nlb + j]);
+        }
+        for (int o = 0; o < O; ++o) {
+            double a = 0.0;
+            for (int k = 0; k < H; ++k) a += z[(size_t)r * H + k] * W[t->off_outw + (int64_t)k * O + o];
+            if (out) out[(size_t)r * O + o] = a + W[t->off_outb + o];
+        }
+    }
+    if (obar) {
+        double* wb = (double*)xcalloc((size_t)t->P, sizeof(double));
+        double* dcur = (double*)xcalloc(LTB * H, sizeof(double));
+        double* dhr = (double*)xcalloc((size_t)T * B * H, sizeof(double));
+        double* dcr = (double*)xcalloc((size_t)T * B * H, sizeof(double));
+        double* dpre = (double*)xcalloc((size_t)T * B * G, sizeof(double));
+        double* dzp = (double*)xcalloc((size_t)B * H, sizeof(double));
+        for (int r = 0; r < B; ++r) {
+            const double* ob = obar + (size_t)r * O;
+            const double* last = cur + SI(L - 1, T - 1, r) * H;
+            for (int o = 0; o < O; ++o) wb[t->off_outb + o] += ob[o];
+            for (int k = 0; k < H; ++k) {
+                double dz = 0.0;
+                for (int o = 0; o < O; ++o) {
+                    wb[t->off_outw + (int64_t)k * O + o] += z[(size_t)r * H + k] * ob[o];
+                    dz += ob[o] * W[t->off_outw + (int64_t)k * O + o];
+                }
+                dzp[(size_t)r * H + k] = dz * (1.0 - z[(size_t)r * H + k] * z[(size_t)r * H + k]);
+            }
+            for (int j = 0; j < H; ++j) wb[t->off_nlb + j] += dzp[(size_t)r * H + j];
+            for (int k = 0; k < H; ++k) {
+                double a = 0.0;
+                for (int j = 0; j < H; ++j) {
+                    wb[t->off_nlw + (int64_t)k * H + j] += last[k] * dzp[(size_t)r * H + j];
+                    a += dzp[(size_t)r * H + j] * W[t->off_nlw + (int64_t)k * H + j];
+                }
+                dcur[SI(L - 1, T - 1, r) * H + k] = a;
+            }
+        }
+        for (int l = L - 1; l >= 0; --l) {
+            const int K = t->layer_in[l], d = dil[l];
+            if (res_src[l] >= 0)
+                for (size_t e = 0; e < (size_t)T * B * H; ++e) {
+                    const size_t tt = e / ((size_t)B * H), rj = e % ((size_t)B * H);
+                    dcur[SI(res_src[l], tt, 0) * H + rj] += dcur[SI(l, tt, 0) * H + rj];
+                }
+            memset(dhr, 0, sizeof(double) * (size_t)T * B * H);
+            memset(dcr, 0, sizeof(double) * (size_t)T * B * H);
+            for (int tt = T - 1; tt >= 0; --tt)
+                for (int r = 0; r < B; ++r) {
+                    const double* g = gates + SI(l, tt, r) * G;
+                    double* dp = dpre + ((size_t)tt * B + r) * G;
+                    for (int j = 0; j < H; ++j) {
+                        const double i = g[j], f = g[H + j], gg = g[2 * H + j], o = g[3 * H + j];
+                        const double tc = fm_tanh(cs[SI(l, tt, r) * H + j]);
+                        const size_t q = ((size_t)tt * B + r) * H + j;
+                        const double dh = dcur[SI(l, tt, r) * H + j] + dhr[q];
+                        const double dc = dcr[q] + dh * o * (1.0 - tc * tc);
+                        double df = 0.0;
+                        if (tt >= d) {
+                            df = dc * cs[SI(l, tt - d, r) * H + j];
+                            dcr[((size_t)(tt - d) * B + r) * H + j] += dc * f;
+                        }
+                        dp[j] = dc * gg * i * (1.0 - i);
+                        dp[H + j] = df * f * (1.0 - f);
+                        dp[2 * H + j] = dc * i * (1.0 - gg * gg);
+                        dp[3 * H + j] = dh * tc * o * (1.0 - o);
+                    }
+                    for (int k = 0; k < K; ++k) {
+                        double a = 0.0;
+                        for (int j = 0; j < G; ++j) a += dp[j] * W[t->off_win[l] + (int64_t)k * G + j];
+                        if (l > 0) dcur[SI(l - 1, tt, r) * H + k] += a;
+                        else if (xbar) xbar[((size_t)tt * B + r) * in0 + k] = a;
+                    }
+                    if (tt >= d)
+                        for (int k = 0; k < H; ++k) {
+                            double a = 0.0;
+                            for (int j = 0; j < G; ++j) a += dp[j] * W[t->off_wrec[l] + (int64_t)k * G + j];
+                            dhr[((size_t)(tt - d) * B + r) * H + k] += a;
+                        }
+                    const double* x = l == 0 ? X + ((size_t)tt * B + r) * in0 : cur + SI(l - 1, tt, r) * H;
+                    for (int j = 0; j < G; ++j) {
+                        for (int k = 0; k < K; ++k) wb[t->off_win[l] + (int64_t)k * G + j] += x[k] * dp[j];
+                        if (tt >= d)
+                            for (int k = 0; k < H; ++k)
+                                wb[t->off_wrec[l] + (int64_t)k * G + j] += hr[SI(l, tt - d, r) * H + k] * dp[j];
+                        wb[t->off_bias[l] + j] += dp[j];
+                    }
+                }
+        }
+        if (wbar) memcpy(wbar, wb, sizeof(double) * (size_t)t->P);
+        free(wb), free(dcur), free(dhr), free(dcr), free(dpre), free(dzp);
+    }
+#undef SI
+    free(gates), free(cs), free(hr), free(cur), free(z);
+    return ESRNN_OK;
+}
+
 /* Exact-resume training state (B200 extension of the ABI): the Adam moments / steps of
  * apply_updates (trainer.hpp:602-655) and the trainer RNG in std::mt19937_64's text form
  * (the 312 state words, then the position), which this MT19937-64 restatement shares. */

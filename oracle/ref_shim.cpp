@@ -332,6 +332,51 @@ esrnn_status esrnn_trainer_validate(esrnn_trainer* t, double* forecasts, double*
     });
 }
 
+// forward_stack through the reference's own tape (network.hpp:190-210), and its gradients by
+// Tape::backward of sum(out * out_bar) (autodiff.hpp:264, :397-631).
+esrnn_status esrnn_trainer_forward_stack(esrnn_trainer* t, int32_t T, int32_t B, const double* X, double* out,
+                                         const double* obar, double* wbar, double* xbar) {
+    return guarded(t->err, [&] {
+        Trainer& tr = *t->tr;
+        const StackConfig& sc = tr.stack_config();
+        const int in = sc.input_size, O = tr.profile().horizon;
+        ad::Tape tape;
+        StackLeaves lv = lift_weights(tape, tr.weights());
+        std::vector<ad::DiffArray> seq;
+        for (int s = 0; s < T; ++s) {
+            Matrix m(static_cast<std::size_t>(B), static_cast<std::size_t>(in));
+            std::memcpy(m.data().data(), X + static_cast<std::size_t>(s) * B * in, sizeof(double) * B * in);
+            seq.push_back(ad::leaf(tape, std::move(m)));
+        }
+        ad::DiffArray o = forward_stack(seq, lv, sc);
+        if (out) std::memcpy(out, o.value().data().data(), sizeof(double) * B * O);
+        if (!obar) return;
+        Matrix ob(static_cast<std::size_t>(B), static_cast<std::size_t>(O));
+        std::memcpy(ob.data().data(), obar, sizeof(double) * B * O);
+        ad::backward(ad::sum(ad::mul(o, ad::constant(tape, std::move(ob)))));
+        if (wbar) {
+            std::size_t off = 0;
+            auto put = [&](const ad::DiffArray& a) {
+                const Matrix& g = a.grad();
+                std::memcpy(wbar + off, g.data().data(), sizeof(double) * g.size());
+                off += g.size();
+            };
+            for (const auto& c : lv.layers) {  // for_each_param order (network.hpp:62-74)
+                put(c.w_input);
+                put(c.w_recur);
+                put(c.bias);
+            }
+            put(lv.nl_w);
+            put(lv.nl_b);
+            put(lv.out_w);
+            put(lv.out_b);
+        }
+        if (xbar)
+            for (int s = 0; s < T; ++s)
+                std::memcpy(xbar + static_cast<std::size_t>(s) * B * in, seq[s].grad().data().data(), sizeof(double) * B * in);
+    });
+}
+
 // Exact-resume training state straight from the reference Trainer's private members
 // (adam_net_, net_step_, adam_series_, rng_.gen_; trainer.hpp:446-457, :655-672).
 esrnn_status esrnn_trainer_get_train_state(esrnn_trainer* t, double* adam_m, double* adam_v, int64_t n_values,

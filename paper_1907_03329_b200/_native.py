@@ -129,6 +129,7 @@ class NativeApi:
         L.esrnn_trainer_forecast.argtypes = [_vp, C.c_int64, _dp]
         L.esrnn_trainer_validate.argtypes = [_vp, _dp, _dp, _dp]
         L.esrnn_trainer_evaluate.argtypes = [_vp, C.c_int32, _dp, _dp, _dp, _dp, _dp, _dp]
+        L.esrnn_trainer_forward_stack.argtypes = [_vp, C.c_int32, C.c_int32, _dp, _dp, _dp, _dp, _dp]
         _lp = C.POINTER(C.c_int64)
         L.esrnn_trainer_get_train_state.argtypes = [_vp, _dp, _dp, C.c_int64, C.c_int64, C.c_int64, _dp, _dp, _lp,
                                                     _lp, C.c_char_p, C.c_int64]
@@ -147,7 +148,7 @@ class NativeApi:
                    "esrnn_trainer_param_info", "esrnn_trainer_get_weights", "esrnn_trainer_set_weights",
                    "esrnn_trainer_get_per_series", "esrnn_trainer_set_per_series", "esrnn_trainer_train_epoch",
                    "esrnn_trainer_run_batch", "esrnn_trainer_forecast", "esrnn_trainer_validate", "esrnn_trainer_evaluate",
-                   "esrnn_trainer_get_train_state", "esrnn_trainer_set_train_state",
+                   "esrnn_trainer_get_train_state", "esrnn_trainer_set_train_state", "esrnn_trainer_forward_stack",
                    "esrnn_trainer_hw_state", "esrnn_trainer_last_device_ms", "esrnn_trainer_last_epoch_windows", "esrnn_trainer_kernel_launches",
                    "esrnn_trainer_profile_kernels", "esrnn_trainer_kernel_times", "esrnn_nccl_unique_id", "esrnn_make_synthetic",
                    "esrnn_release_cached_memory"):

@@ -33,6 +33,7 @@
 
 #include "esrnn_b200.h"
 #include "finish.cuh"
+#include "seqstack.cuh"
 #include "scan.cuh"
 #include "tile.cuh"
 
@@ -1663,6 +1664,70 @@ void forecast_impl(Eng* e, int64_t drop_tail, double* out, int mode, const Score
         for (int i = 0; i < 8; ++i) so.totals[i] = tot[i];
 }
 
+// ------------------------------------------------------------------ general forward_stack
+// network.hpp:190-210 over a multi-step sequence with the trainer's full StackWeights (the
+// structurally dead parts of the sequence-length-1 hot path -- forget gates, recurrent
+// matrices -- are live here), plus the tape adjoints for an upstream out_bar.
+template <typename Real>
+void forward_stack_impl(Eng* e, int Tq, int B, const double* inputs, double* out, const double* out_bar,
+                        double* wbar, double* xbar) {
+    if (Tq < 1) raise(ESRNN_CONTRACT_ERROR, "forward_stack: empty sequence");
+    if (B < 1) raise(ESRNN_SHAPE_ERROR, "forward_stack: empty batch");
+    SeqLayout sl{};
+    sl.L = e->L, sl.H = e->H, sl.O = e->O, sl.in0 = e->in0, sl.T = Tq, sl.B = B;
+    sl.in_max = std::max(e->in0, e->H);
+    for (int l = 0; l < e->L; ++l) {
+        sl.layer_in[l] = e->layer_in[l];
+        sl.dil[l] = e->prof.dilations[l];
+        sl.res_src[l] = -1;
+        sl.w_in[l] = e->off_win[l];
+        sl.w_rec[l] = e->off_wrec[l];
+        sl.bias[l] = e->off_bias[l];
+    }
+    for (int b = 0, first = 0; b < e->prof.n_blocks; first += e->prof.block_len[b], ++b)
+        if (b > 0) sl.res_src[first + e->prof.block_len[b] - 1] = first - 1;  // network.hpp:201-206
+    sl.nl_w = e->off_nlw, sl.nl_b = e->off_nlb, sl.out_w = e->off_outw, sl.out_b = e->off_outb, sl.P = e->P;
+    sync_weights_from_device(e);
+    const size_t r = e->rsz;
+    const int nblk = (B + kSeqRows - 1) / kSeqRows;
+    DBuf<unsigned char> w, x, scratch, ob, wpart, xb;
+    DBuf<double> dout, dwbar;
+    w.alloc(r * e->P);
+    upload_real(e, w.p, e->w_host.data(), e->P);
+    x.alloc(r * static_cast<size_t>(Tq) * B * e->in0);
+    upload_real(e, x.p, inputs, static_cast<size_t>(Tq) * B * e->in0);
+    scratch.alloc(r * static_cast<size_t>(nblk) * SeqScratch<Real>::size(sl));
+    dout.alloc(static_cast<size_t>(B) * e->O);
+    CUDA_OK(cudaEventRecord(e->ev0, e->stream));
+    k_seq_forward<Real><<<nblk, kSeqThreads, 0, e->stream>>>(sl, reinterpret_cast<const Real*>(w.p),
+                                                              reinterpret_cast<const Real*>(x.p),
+                                                              reinterpret_cast<Real*>(scratch.p), dout.p);
+    e->launches += 1;
+    if (out_bar) {
+        ob.alloc(r * static_cast<size_t>(B) * e->O);
+        upload_real(e, ob.p, out_bar, static_cast<size_t>(B) * e->O);
+        wpart.alloc(r * static_cast<size_t>(nblk) * e->P);
+        if (xbar) xb.alloc(r * static_cast<size_t>(Tq) * B * e->in0);
+        k_seq_backward<Real><<<nblk, kSeqThreads, 0, e->stream>>>(
+            sl, reinterpret_cast<const Real*>(w.p), reinterpret_cast<const Real*>(x.p),
+            reinterpret_cast<Real*>(scratch.p), reinterpret_cast<const Real*>(ob.p), reinterpret_cast<Real*>(wpart.p),
+            xbar ? reinterpret_cast<Real*>(xb.p) : nullptr);
+        dwbar.alloc(e->P);
+        k_seq_reduce<Real><<<static_cast<int>((e->P + 255) / 256), 256, 0, e->stream>>>(
+            reinterpret_cast<const Real*>(wpart.p), nblk, e->P, dwbar.p);
+        e->launches += 2;
+    }
+    CUDA_OK(cudaEventRecord(e->ev1, e->stream));
+    CUDA_OK(cudaGetLastError());
+    CUDA_OK(cudaStreamSynchronize(e->stream));
+    float ms = 0.f;
+    CUDA_OK(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
+    e->last_ms = ms;
+    if (out) CUDA_OK(cudaMemcpy(out, dout.p, sizeof(double) * B * e->O, cudaMemcpyDeviceToHost));
+    if (out_bar && wbar) CUDA_OK(cudaMemcpy(wbar, dwbar.p, sizeof(double) * e->P, cudaMemcpyDeviceToHost));
+    if (out_bar && xbar) download_real(e, xb.p, static_cast<size_t>(Tq) * B * e->in0, xbar);
+}
+
 template <typename Real>
 void hw_state_impl(Eng* e, int64_t row, int64_t t_len, double* levels, double* seas) {
     const int S = e->S;
@@ -2072,6 +2137,15 @@ esrnn_status esrnn_trainer_evaluate(esrnn_trainer* t, int32_t against_test, doub
         so.totals = totals;
         if (t->fp64) forecast_impl<double>(t, dt, forecasts, 2, so);
         else forecast_impl<float>(t, dt, forecasts, 2, so);
+    });
+}
+
+esrnn_status esrnn_trainer_forward_stack(esrnn_trainer* t, int32_t seq_len, int32_t B, const double* inputs,
+                                         double* out, const double* out_bar, double* weights_bar, double* inputs_bar) {
+    return guarded(t->err, [&] {
+        CUDA_OK(cudaSetDevice(t->cfg.device));
+        if (t->fp64) forward_stack_impl<double>(t, seq_len, B, inputs, out, out_bar, weights_bar, inputs_bar);
+        else forward_stack_impl<float>(t, seq_len, B, inputs, out, out_bar, weights_bar, inputs_bar);
     });
 }
 

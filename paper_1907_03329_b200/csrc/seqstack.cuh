@@ -1,0 +1,277 @@
+// The general dilated LSTM stack over an input sequence:
+// forward_stack (network.hpp:190-210, plain mirror :268-287) with full LSTM cells -- forget
+// gates, recurrent matrices, (h, c) read from step t - d (lstm_cell :148-163,
+// dilated_lstm_layer :167-184) -- and the reverse-mode adjoints the reference's tape forms for
+// it (Tape::backward, autodiff.hpp:397-631).  The training hot path runs the stack at sequence
+// length 1 (tile.cuh); this is the rest of the forward_stack API, for callers that pass
+// multi-step sequences (test_network.cpp:94-181, :235-267; acceptance.cpp:183-217).
+//
+// A CTA owns kSeqRows batch rows for the whole sequence: layer by layer, step by step (the
+// recurrence is serial in t), threads over (row, gate output) for the products and over
+// (row, unit) for the cell.  Saved activations live in a per-CTA global scratch (L2
+// resident at these sizes).  Weight gradients are per-CTA partials, reduced in CTA order by
+// k_seq_reduce: deterministic, no float atomics.
+#pragma once
+#include "common.cuh"
+
+namespace esrnn_dev {
+
+constexpr int kSeqRows = 4;
+constexpr int kSeqThreads = 256;
+
+// Offsets of the flat for_each_param weight vector (network.hpp:62-74) and the stack shape.
+struct SeqLayout {
+    int L, H, O, in0, T, B, in_max;
+    int layer_in[kMaxLayers], dil[kMaxLayers];
+    int res_src[kMaxLayers];    // >= 0: this layer's output gets layer res_src's output added (block b>0 skip)
+    long long w_in[kMaxLayers], w_rec[kMaxLayers], bias[kMaxLayers];
+    long long nl_w, nl_b, out_w, out_b, P;
+};
+
+// Per-CTA scratch (Real units), see seq_scratch_size
+template <typename Real>
+struct SeqScratch {
+    Real *gates, *cst, *hraw, *cur, *dcur, *dhr, *dcr, *dpre, *din, *z, *dzp;
+    __host__ __device__ static long long size(const SeqLayout& s) {
+        const long long LT = static_cast<long long>(s.L) * s.T * kSeqRows;
+        const long long TR = static_cast<long long>(s.T) * kSeqRows;
+        return LT * (4LL * s.H) + 4 * LT * s.H + 2 * TR * s.H + TR * 4LL * s.H + TR * s.in_max + 2LL * kSeqRows * s.H;
+    }
+    __device__ static SeqScratch at(Real* base, const SeqLayout& s) {
+        const long long LT = static_cast<long long>(s.L) * s.T * kSeqRows;
+        const long long TR = static_cast<long long>(s.T) * kSeqRows;
+        SeqScratch c;
+        Real* p = base + static_cast<long long>(blockIdx.x) * size(s);
+        c.gates = p; p += LT * 4 * s.H;   // [L][T][r][4H] i f g o
+        c.cst = p; p += LT * s.H;         // [L][T][r][H] cell state
+        c.hraw = p; p += LT * s.H;        // [L][T][r][H] cell output (the recurrent state)
+        c.cur = p; p += LT * s.H;         // [L][T][r][H] layer output (+ block skip)
+        c.dcur = p; p += LT * s.H;        // [L][T][r][H] adjoint of cur
+        c.dhr = p; p += TR * s.H;         // [T][r][H] recurrent adjoint of h
+        c.dcr = p; p += TR * s.H;         // [T][r][H] recurrent adjoint of c
+        c.dpre = p; p += TR * 4 * s.H;    // [T][r][4H] pre-activation adjoints of one layer
+        c.din = p; p += TR * s.in_max;    // [T][r][in] input adjoint of one layer
+        c.z = p; p += kSeqRows * s.H;     // [r][H] head activations
+        c.dzp = p;                        // [r][H] head pre-activation adjoints
+        return c;
+    }
+};
+
+__device__ __forceinline__ long long sidx(const SeqLayout& s, int l, int t, int r) {
+    return (static_cast<long long>(l) * s.T + t) * kSeqRows + r;
+}
+
+// Layer input row (row r, step t) of layer l: the sequence for layer 0, else the previous
+// layer's output.
+template <typename Real>
+__device__ __forceinline__ const Real* seq_in(const SeqLayout& s, const SeqScratch<Real>& c, const Real* X, int l,
+                                              int t, int r, int b0) {
+    return l == 0 ? X + (static_cast<long long>(t) * s.B + b0 + r) * s.in0 : c.cur + sidx(s, l - 1, t, r) * s.H;
+}
+
+template <typename Real>
+__global__ void __launch_bounds__(kSeqThreads) k_seq_forward(SeqLayout s, const Real* __restrict__ W,
+                                                              const Real* __restrict__ X, Real* scratch, double* out) {
+    using M = Math<Real>;
+    const int b0 = blockIdx.x * kSeqRows, nr = min(kSeqRows, s.B - b0);
+    const int tid = threadIdx.x, NT = blockDim.x, H = s.H, G = 4 * H;
+    const SeqScratch<Real> c = SeqScratch<Real>::at(scratch, s);
+    for (int l = 0; l < s.L; ++l) {
+        const int K = s.layer_in[l], d = s.dil[l];
+        const Real* Wi = W + s.w_in[l];
+        const Real* Wr = W + s.w_rec[l];
+        const Real* bi = W + s.bias[l];
+        for (int t = 0; t < s.T; ++t) {
+            // pre = x W_in (+ h_{t-d} W_rec) + b (lstm_cell, network.hpp:152-154), then the gates
+            for (int e = tid; e < nr * G; e += NT) {
+                const int r = e / G, j = e - r * G;
+                const Real* x = seq_in(s, c, X, l, t, r, b0);
+                Real acc = 0;
+                for (int k = 0; k < K; ++k) acc += x[k] * Wi[static_cast<long long>(k) * G + j];
+                if (t >= d) {
+                    const Real* hp = c.hraw + sidx(s, l, t - d, r) * H;
+                    Real a2 = 0;
+                    for (int k = 0; k < H; ++k) a2 += hp[k] * Wr[static_cast<long long>(k) * G + j];
+                    acc += a2;
+                }
+                acc += bi[j];
+                c.gates[sidx(s, l, t, r) * G + j] = (j >= 2 * H && j < 3 * H) ? M::tanh(acc) : M::logistic(acc);
+            }
+            __syncthreads();
+            // c = f c_{t-d} + i g, h = o tanh(c); block skip added after the block's last layer
+            for (int e = tid; e < nr * H; e += NT) {
+                const int r = e / H, j = e - r * H;
+                const Real* gt = c.gates + sidx(s, l, t, r) * G;
+                const Real i = gt[j], f = gt[H + j], g = gt[2 * H + j], o = gt[3 * H + j];
+                const Real cv = (t >= d ? f * c.cst[sidx(s, l, t - d, r) * H + j] : Real(0)) + i * g;
+                const Real h = o * M::tanh(cv);
+                c.cst[sidx(s, l, t, r) * H + j] = cv;
+                c.hraw[sidx(s, l, t, r) * H + j] = h;
+                c.cur[sidx(s, l, t, r) * H + j] =
+                    s.res_src[l] >= 0 ? h + c.cur[sidx(s, s.res_src[l], t, r) * H + j] : h;
+            }
+            __syncthreads();
+        }
+    }
+    // head on the last step (network.hpp:207-209)
+    for (int e = tid; e < nr * H; e += NT) {
+        const int r = e / H, j = e - r * H;
+        const Real* last = c.cur + sidx(s, s.L - 1, s.T - 1, r) * H;
+        Real acc = 0;
+        for (int k = 0; k < H; ++k) acc += last[k] * W[s.nl_w + static_cast<long long>(k) * H + j];
+        c.z[r * H + j] = M::tanh(acc + W[s.nl_b + j]);
+    }
+    __syncthreads();
+    for (int e = tid; e < nr * s.O; e += NT) {
+        const int r = e / s.O, o = e - r * s.O;
+        Real acc = 0;
+        for (int k = 0; k < H; ++k) acc += c.z[r * H + k] * W[s.out_w + static_cast<long long>(k) * s.O + o];
+        out[static_cast<long long>(b0 + r) * s.O + o] = static_cast<double>(acc + W[s.out_b + o]);
+    }
+}
+
+// Reverse sweep of the same graph for the adjoint out_bar [B][O]: per-CTA weight-gradient
+// partials wpart [gridDim][P] (for_each_param order) and input adjoints xbar [T][B][in0].
+template <typename Real>
+__global__ void __launch_bounds__(kSeqThreads) k_seq_backward(SeqLayout s, const Real* __restrict__ W,
+                                                               const Real* __restrict__ X, Real* scratch,
+                                                               const Real* __restrict__ obar, Real* wpart, Real* xbar) {
+    const int b0 = blockIdx.x * kSeqRows, nr = min(kSeqRows, s.B - b0);
+    const int tid = threadIdx.x, NT = blockDim.x, H = s.H, G = 4 * H, O = s.O;
+    const SeqScratch<Real> c = SeqScratch<Real>::at(scratch, s);
+    Real* wp = wpart + static_cast<long long>(blockIdx.x) * s.P;
+    for (long long e = tid; e < s.P; e += NT) wp[e] = 0;
+    for (long long e = tid; e < static_cast<long long>(s.L) * s.T * kSeqRows * H; e += NT) c.dcur[e] = 0;
+    __syncthreads();
+    // head: out = z out_w + out_b, z = tanh(last nl_w + nl_b)
+    const Real* ob = obar + static_cast<long long>(b0) * O;
+    for (int e = tid; e < H * O + O; e += NT) {
+        Real acc = 0;
+        if (e < H * O) {
+            const int k = e / O, o = e - k * O;
+            for (int r = 0; r < nr; ++r) acc += c.z[r * H + k] * ob[r * O + o];
+            wp[s.out_w + e] = acc;
+        } else {
+            for (int r = 0; r < nr; ++r) acc += ob[r * O + (e - H * O)];
+            wp[s.out_b + (e - H * O)] = acc;
+        }
+    }
+    for (int e = tid; e < nr * H; e += NT) {
+        const int r = e / H, k = e - r * H;
+        Real acc = 0;
+        for (int o = 0; o < O; ++o) acc += ob[r * O + o] * W[s.out_w + static_cast<long long>(k) * O + o];
+        const Real z = c.z[r * H + k];
+        c.dzp[r * H + k] = acc * (Real(1) - z * z);
+    }
+    __syncthreads();
+    for (int e = tid; e < H * H + H; e += NT) {
+        Real acc = 0;
+        if (e < H * H) {
+            const int k = e / H, j = e - k * H;
+            for (int r = 0; r < nr; ++r) acc += c.cur[sidx(s, s.L - 1, s.T - 1, r) * H + k] * c.dzp[r * H + j];
+            wp[s.nl_w + e] = acc;
+        } else {
+            for (int r = 0; r < nr; ++r) acc += c.dzp[r * H + (e - H * H)];
+            wp[s.nl_b + (e - H * H)] = acc;
+        }
+    }
+    for (int e = tid; e < nr * H; e += NT) {
+        const int r = e / H, k = e - r * H;
+        Real acc = 0;
+        for (int j = 0; j < H; ++j) acc += c.dzp[r * H + j] * W[s.nl_w + static_cast<long long>(k) * H + j];
+        c.dcur[sidx(s, s.L - 1, s.T - 1, r) * H + k] = acc;
+    }
+    __syncthreads();
+    for (int l = s.L - 1; l >= 0; --l) {
+        const int K = s.layer_in[l], d = s.dil[l];
+        const Real* Wi = W + s.w_in[l];
+        const Real* Wr = W + s.w_rec[l];
+        // block skip: its source receives the layer output's adjoint too
+        if (s.res_src[l] >= 0)
+            for (int e = tid; e < s.T * nr * H; e += NT) {
+                const int t = e / (nr * H), rj = e - t * nr * H, r = rj / H, j = rj - r * H;
+                c.dcur[sidx(s, s.res_src[l], t, r) * H + j] += c.dcur[sidx(s, l, t, r) * H + j];
+            }
+        for (int e = tid; e < 2 * s.T * kSeqRows * H; e += NT) c.dhr[e] = 0;  // dhr and dcr are contiguous
+        __syncthreads();
+        for (int t = s.T - 1; t >= 0; --t) {
+            // cell adjoints (Mul / Tanh / Logistic / Add adjoints of lstm_cell)
+            for (int e = tid; e < nr * H; e += NT) {
+                const int r = e / H, j = e - r * H;
+                const long long q = sidx(s, l, t, r);
+                const Real* gt = c.gates + q * G;
+                const Real i = gt[j], f = gt[H + j], g = gt[2 * H + j], o = gt[3 * H + j];
+                const Real tc = Math<Real>::tanh(c.cst[q * H + j]);
+                const long long rt = (static_cast<long long>(t) * kSeqRows + r) * H + j;
+                const Real dh = c.dcur[q * H + j] + c.dhr[rt];
+                const Real dc = c.dcr[rt] + dh * o * (Real(1) - tc * tc);
+                Real df = 0;
+                if (t >= d) {
+                    df = dc * c.cst[sidx(s, l, t - d, r) * H + j];
+                    c.dcr[(static_cast<long long>(t - d) * kSeqRows + r) * H + j] += dc * f;
+                }
+                Real* dp = c.dpre + (static_cast<long long>(t) * kSeqRows + r) * G;
+                dp[j] = dc * g * i * (Real(1) - i);
+                dp[H + j] = df * f * (Real(1) - f);
+                dp[2 * H + j] = dc * i * (Real(1) - g * g);
+                dp[3 * H + j] = dh * tc * o * (Real(1) - o);
+            }
+            __syncthreads();
+            // input adjoint of step t and the recurrent adjoint of h_{t-d}
+            const int kmax = K > H ? K : H;
+            for (int e = tid; e < nr * kmax; e += NT) {
+                const int r = e / kmax, k = e - r * kmax;
+                const Real* dp = c.dpre + (static_cast<long long>(t) * kSeqRows + r) * G;
+                if (k < K) {
+                    Real acc = 0;
+                    for (int j = 0; j < G; ++j) acc += dp[j] * Wi[static_cast<long long>(k) * G + j];
+                    c.din[(static_cast<long long>(t) * kSeqRows + r) * s.in_max + k] = acc;
+                }
+                if (t >= d && k < H) {
+                    Real acc = 0;
+                    for (int j = 0; j < G; ++j) acc += dp[j] * Wr[static_cast<long long>(k) * G + j];
+                    c.dhr[(static_cast<long long>(t - d) * kSeqRows + r) * H + k] += acc;
+                }
+            }
+            __syncthreads();
+        }
+        // this layer's weight gradients: x^T dpre, h_{t-d}^T dpre, 1^T dpre (reverse-step order)
+        for (long long e = tid; e < static_cast<long long>(K + H + 1) * G; e += NT) {
+            const int k = static_cast<int>(e / G), j = static_cast<int>(e - static_cast<long long>(k) * G);
+            Real acc = 0;
+            for (int t = s.T - 1; t >= 0; --t)
+                for (int r = 0; r < nr; ++r) {
+                    const Real a = c.dpre[(static_cast<long long>(t) * kSeqRows + r) * G + j];
+                    if (k < K) acc += seq_in(s, c, X, l, t, r, b0)[k] * a;
+                    else if (k < K + H) {
+                        if (t >= d) acc += c.hraw[sidx(s, l, t - d, r) * H + (k - K)] * a;
+                    } else {
+                        acc += a;
+                    }
+                }
+            if (k < K) wp[s.w_in[l] + static_cast<long long>(k) * G + j] = acc;
+            else if (k < K + H) wp[s.w_rec[l] + static_cast<long long>(k - K) * G + j] = acc;
+            else wp[s.bias[l] + j] = acc;
+        }
+        // the input adjoint goes to the previous layer's output or to the sequence
+        for (int e = tid; e < s.T * nr * K; e += NT) {
+            const int t = e / (nr * K), rk = e - t * nr * K, r = rk / K, k = rk - r * K;
+            const Real v = c.din[(static_cast<long long>(t) * kSeqRows + r) * s.in_max + k];
+            if (l > 0) c.dcur[sidx(s, l - 1, t, r) * H + k] += v;
+            else if (xbar) xbar[(static_cast<long long>(t) * s.B + b0 + r) * s.in0 + k] = v;
+        }
+        __syncthreads();
+    }
+}
+
+// weights_bar[p] = sum over CTAs b (in order) of wpart[b][p]
+template <typename Real>
+__global__ void k_seq_reduce(const Real* __restrict__ wpart, int nblk, long long P, double* out) {
+    const long long p = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (p >= P) return;
+    double acc = 0;
+    for (int b = 0; b < nblk; ++b) acc += static_cast<double>(wpart[static_cast<long long>(b) * P + p]);
+    out[p] = acc;
+}
+
+}  // namespace esrnn_dev

@@ -590,6 +590,29 @@ class Trainer:
             res.naive = aggregate(cats, fname, arrs[2], arrs[3])
         return res
 
+    def forward_stack(self, sequence, out_bar=None):
+        """network.hpp:190-210 forward_stack over a general input sequence (seq_len, B, I+6) with
+        this trainer's StackWeights: the full dilated recurrence.  Returns the (B, O) output, or
+        with `out_bar` (B, O) the tuple (out, weights_bar by name, inputs_bar) of the tape's
+        reverse-mode adjoints."""
+        x = np.ascontiguousarray(sequence, dtype=np.float64)
+        if x.ndim != 3 or x.shape[0] < 1:
+            raise E.ContractError("forward_stack: empty sequence")
+        T, B, width = x.shape
+        if width != self._profile.input_window + 6:
+            raise E.ShapeError(f"forward_stack: input width {width}, expected {self._profile.input_window + 6}")
+        out = np.zeros((B, self._profile.horizon))
+        if out_bar is None:
+            self._chk(self.api.lib.esrnn_trainer_forward_stack(self._h, T, B, N.dptr(x), N.dptr(out), None, None,
+                                                               None))
+            return out
+        ob = np.ascontiguousarray(out_bar, dtype=np.float64).reshape(B, self._profile.horizon)
+        wb = np.zeros(self.n_values)
+        xb = np.zeros_like(x)
+        self._chk(self.api.lib.esrnn_trainer_forward_stack(self._h, T, B, N.dptr(x), N.dptr(out), N.dptr(ob),
+                                                           N.dptr(wb), N.dptr(xb)))
+        return out, {n: wb[o:o + r * c].reshape(r, c) for n, r, c, o in self.param_layout}, xb
+
     def train_state(self) -> TrainState:
         n = self.row_end - self.row_begin
         S = self._profile.seasonality_length

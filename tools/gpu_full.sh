@@ -24,3 +24,6 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_gr
   -o gpurun_out/${TAG}_finish python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e \
   > gpurun_out/${TAG}_ncu_finish.log 2>&1; echo "ncu finish rc=$?"
 for f in gpurun_out/${TAG}_bench_*.json; do echo "== $f"; tail -1 $f | cut -c1-600; done
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_adam -s 200 -c 2 \
+  -o gpurun_out/${TAG}_adam python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e \
+  > gpurun_out/${TAG}_ncu_adam.log 2>&1; echo "ncu adam rc=$?"
