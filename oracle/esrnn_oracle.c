@@ -204,8 +204,11 @@ static esrnn_status validate_config(const esrnn_profile* p, const esrnn_train_co
     if (p->hidden_size < 1) return fail(err, ESRNN_CONFIG_ERROR, "profile: hidden_size must be >= 1");
     if (p->min_length < 1) return fail(err, ESRNN_CONFIG_ERROR, "profile: min_length must be >= 1");
     if (c->epochs < 0) return fail(err, ESRNN_CONFIG_ERROR, "train: epochs must be >= 0");
-    if (c->batch_size < 1 || c->batch_size > 2048)
-        return fail(err, ESRNN_CONFIG_ERROR, "train: batch_size must be in [1, 2048]");
+    /* trainer.hpp:36-37 caps the batch at 2048; the ABI's max_batch_size extension lifts the
+     * cap for the large-batch sweep, where this restatement is the only CPU checker */
+    const int cap = c->max_batch_size > 0 ? c->max_batch_size : 2048;
+    if (c->batch_size < 1 || c->batch_size > cap)
+        return fail(err, ESRNN_CONFIG_ERROR, "train: batch_size must be in [1, %d]", cap);
     if (!(c->tau > 0.0 && c->tau < 1.0)) return fail(err, ESRNN_CONFIG_ERROR, "train: tau must be in (0, 1)");
     if (c->learning_rate_network < 0.0 || c->learning_rate_per_series < 0.0)
         return fail(err, ESRNN_CONFIG_ERROR, "train: learning rates must be non-negative");

@@ -303,8 +303,10 @@ __device__ __forceinline__ int hw_scan_row(const Real* __restrict__ ys, const Re
     return bad;
 }
 
+// RESIDENT: all weights in shared memory, one CTA per SM; staged fp32 tiles (weights one
+// layer at a time) fit two CTAs per SM, so their register budget is capped accordingly.
 template <typename Real, int MODE, bool RESIDENT, int SC>
-__global__ void __launch_bounds__(512) k_tile(StateDev<Real> st, PlanDev pl, NetLayout lay_p, int s, ForecastArgs fa) {
+__global__ void __launch_bounds__((RESIDENT || sizeof(Real) == 8) ? 512 : 384, (RESIDENT || sizeof(Real) == 8) ? 1 : 2) k_tile(StateDev<Real> st, PlanDev pl, NetLayout lay_p, int s, ForecastArgs fa) {
     using M = Math<Real>;
     constexpr int R = kR, LD = ldr<Real>();
     pdl_trigger();  // dependents may launch; they wait for this grid's completion themselves

@@ -340,3 +340,20 @@ def test_two_live_trainers_interleaved_bit_identical(engine, oracle, precision):
         assert t1.last_epoch_windows() == t2.last_epoch_windows()
     assert np.array_equal(t1.weights_flat(), t2.weights_flat())
     assert t1.validate().mean_smape == t2.validate().mean_smape
+
+
+@pytest.mark.parametrize("precision,tol", [("fp32", 1e-4), ("fp64", 1e-10)])
+def test_two_wave_batch_matches_oracle(engine, oracle, precision, tol):
+    """A batch of more than two waves of 8-window tiles (>= 2 x 148 x 8 windows) runs the
+    staged two-CTAs-per-SM tile variant: same loss and gradients as the oracle."""
+    prof, vals, cats = dataset(oracle, "monthly", 90, 13)
+    kw = dict(batch_size=2400, max_batch_size=4096)
+    g = Trainer((vals, cats), prof, TrainConfig(seed=7, precision=precision, **kw), api=engine)
+    o = Trainer((vals, cats), prof, TrainConfig(seed=7, precision="fp64", **kw), api=oracle)
+    b = sample_batch(o, 2400, 3)
+    gg, go = g.batch_gradients(copy_batch(b)), o.batch_gradients(copy_batch(b))
+    assert max_rel(gg.loss, go.loss) < tol
+    for name_, arr in go.network.items():
+        assert tensor_err(gg.network[name_], arr) < tol * 10, name_
+    lg, lo = g.train_epoch(), o.train_epoch()
+    assert max_rel(lg, lo) < (1e-8 if precision == "fp64" else 1e-3)
