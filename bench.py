@@ -326,13 +326,22 @@ def main():
     per = T - prof.horizon - prof.input_window + 1
     steps_per_epoch = -(-n_total * per // B)
     B_local = B // world
+    # DRAM traffic per launch of the dominant kernel, from the committed ncu --set full capture
+    # of this workload (tools/ncu_summary.py traffic), when there is one
+    traffic = None
+    tf = ROOT / "profiles" / "ncu_traffic.json"
+    if tf.exists():
+        doc = json.loads(tf.read_text())
+        kname = {"tile": "k_tile", "finish": "k_grad_finish", "adam": "k_adam"}.get(dom)
+        if doc.get("config") == a.config and kname in doc.get("kernels", {}):
+            traffic = doc["kernels"][kname]
     if dom in ("tile",):
         flops = lstm_flops_per_step(prof, B_local)
         avg_s = shares[dom]["ms"] / shares[dom]["launches"] / 1e3
         achieved = flops / avg_s / 1e12
         peak = fp32_peak if a.precision == "fp32" else fp32_peak / 2
         roof = {"kernel": "k_tile (fused HW scan + window + LSTM fwd/bwd + pinball)", "bound": "fp32-fma",
-                "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                 "peak_source": f"derived CUDA-core FP32 FMA peak: 148 SM x 128 lanes x 2 x {sm_max:.0f} MHz "
                                f"(MEASURED_PEAKS sm_max_mhz); no tensor-core path (fp32 contract)",
                 "algorithmic_per_launch": f"{flops:.3e} FLOP (live-gate LSTM fwd+bwd, B={B_local})"}
@@ -343,7 +352,7 @@ def main():
         achieved = byts / avg_s / 1e9
         peak = peaks.get("hbm_gbs", 6553.9)
         roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": None, "peak_source": "MEASURED_PEAKS hbm_gbs (measured)",
+                "frac": achieved / peak, "traffic": traffic, "peak_source": "MEASURED_PEAKS hbm_gbs (measured)",
                 "algorithmic_per_launch": f"{byts:.3e} B"}
 
     # e2e through the public API with host buffers

@@ -3,6 +3,8 @@
 
     python tools/ncu_summary.py full  <rep.ncu-rep> [...]   # --set full capture: SOL, DRAM bytes, stalls
     python tools/ncu_summary.py launches <launches.csv>       # per-kernel launch list: count, mean, share
+    python tools/ncu_summary.py traffic <out.json> <config> <rep.ncu-rep> [...]
+        # per-kernel DRAM bytes per launch (read + write) for bench.py's roofline.traffic
 """
 import collections
 import csv
@@ -66,7 +68,31 @@ def launches(path):
         print(f"{k:80s} {len(v):8d} {sum(v) / len(v):12.1f} {sum(v) / tot * 100:6.1f}%")
 
 
+def traffic(out, config, paths):
+    import json
+    res = {}
+    for path in paths:
+        raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        rows = list(csv.reader(io.StringIO(raw)))
+        hdr, units = rows[0], rows[1]
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        for v in rows[2:]:
+            d, u = dict(zip(hdr, v)), dict(zip(hdr, units))
+            name = d["Kernel Name"].split("(")[0].split("<")[0].split("::")[-1].split()[-1]
+            b = sum(float(d[k].replace(",", "")) * scale[u[k]] for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+            res.setdefault(name, []).append(b)
+    doc = {"config": config, "source": [str(p) for p in paths],
+           "what": "dram__bytes_read.sum + dram__bytes_write.sum per launch, ncu --set full",
+           "kernels": {k: sum(v) / len(v) for k, v in res.items()}}
+    with open(out, "w") as f:
+        json.dump(doc, f, indent=1)
+    print(json.dumps(doc))
+
+
 if __name__ == "__main__":
     mode, *paths = sys.argv[1:]
-    for p in paths:
-        (full if mode == "full" else launches)(p)
+    if mode == "traffic":
+        traffic(paths[0], paths[1], paths[2:])
+    else:
+        for p in paths:
+            (full if mode == "full" else launches)(p)
