@@ -255,7 +255,9 @@ struct WorkerPool {
     }
 };
 WorkerPool& worker_pool() {
-    static WorkerPool* p = new WorkerPool(3);  // never destroyed (threads park in cv.wait)
+    // never destroyed (threads park in cv.wait); sized to the host, at most 7 helpers
+    static WorkerPool* p = new WorkerPool(static_cast<int>(
+        std::max(1u, std::min(7u, std::thread::hardware_concurrency() > 1 ? std::thread::hardware_concurrency() - 1 : 1u))));
     return *p;
 }
 // stamp ids for slot dedupe: unique per planned step across the process (no re-init of
@@ -1237,7 +1239,7 @@ void build_epoch_plan(Eng* e, EpochPlan& ep) {
     const int steps = static_cast<int>((nw + B - 1) / B);
     ep.steps = steps;
     // step-range chunks, planned in parallel (each with its own dedupe stamps)
-    const int nchunk = std::max(1, std::min(4, steps / 8));
+    const int nchunk = std::max(1, std::min(static_cast<int>(worker_pool().th.size()) + 1, steps / 6));
     ep.chunks.resize(nchunk);
     const int64_t id0 = g_stamp_id.fetch_add(steps);
     auto chunk_range = [&](int c, int& s0, int& s1) {
