@@ -1444,8 +1444,11 @@ double train_epoch_impl(Eng* e) {
     if (e->dbg_clk.p) {
         long long c[96];
         CUDA_OK(cudaMemcpy(c, e->dbg_clk.p, sizeof c, cudaMemcpyDeviceToHost));
+        static const char* kPh[] = {"stage+wait", "scan", "publish", "gather", "fwd0", "fwd1", "fwd2", "fwd3", "head",
+                                    "loss", "zbar", "bwd3", "bwd2", "bwd1", "bwd0", "xbar"};
         std::fprintf(stderr, "[esrnn dbg] k_tile tile0 phase cycles:");
-        for (int i = 1; i < 32 && c[i] > 0; ++i) std::fprintf(stderr, " %lld", c[i] - c[i - 1]);
+        for (int i = 1; i < 32 && c[i] > 0; ++i)
+            std::fprintf(stderr, " %s=%lld", i - 1 < 16 ? kPh[i - 1] : "?", c[i] - c[i - 1]);
         std::fprintf(stderr, "\n[esrnn dbg] grad_finish ES block0:");
         for (int i = 33; i < 48 && c[i] > 0; ++i) std::fprintf(stderr, " %lld", c[i] - c[i - 1]);
         std::fprintf(stderr, "\n[esrnn dbg] grad_finish reduce block0:");

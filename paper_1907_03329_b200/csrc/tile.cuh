@@ -434,15 +434,11 @@ __global__ void __launch_bounds__((RESIDENT || sizeof(Real) == 8) ? 512 : 384, (
         __syncthreads();
         // published states for K3's reverse scan: lv [T][kcap], se [T+S][kcap]
         if (MODE == kTrain) {
-            const int per = 2 * T + S;
-            for (int e = tid; e < nrows * per; e += NT) {
-                const int r = e / per, t = e - r * per;
+            for (int r = warp; r < nrows; r += NW) {  // a warp per window row, lanes over t
                 const int slot = pub_slot[r];
                 if (slot < 0) continue;
-                if (t < T)
-                    st.lv[(size_t)t * st.kcap + slot] = LVR[r * ts.ldl + t];
-                else
-                    st.se[(size_t)(t - T) * st.kcap + slot] = SER[r * ts.lds + (t - T)];
+                for (int t = lane; t < T; t += 32) st.lv[(size_t)t * st.kcap + slot] = LVR[r * ts.ldl + t];
+                for (int t = lane; t < T + S; t += 32) st.se[(size_t)t * st.kcap + slot] = SER[r * ts.lds + t];
             }
         }
     }
@@ -646,8 +642,17 @@ __global__ void __launch_bounds__((RESIDENT || sizeof(Real) == 8) ? 512 : 384, (
         PBT[o * LD + r] = pb;
         if (rs && r < nrows) rs[r * lay.rs_ld + lay.rs_pb + o] = pb;
     }
-    const double ltot = block_sum(lsum, red);  // its barriers also publish PBT
-    if (tid == 0) st.loss_part[tile] = ltot;
+    // block sum in block_sum's fixed order (warp shuffles, then warps in order), with the one
+    // barrier that also publishes PBT
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) lsum += __shfl_down_sync(0xffffffffu, lsum, o);
+    if (lane == 0) red[warp] = lsum;
+    __syncthreads();
+    if (tid == 0) {
+        double ltot = 0.0;
+        for (int w = 0; w < NW; ++w) ltot += red[w];
+        st.loss_part[tile] = ltot;
+    }
     if (MODE == kLossOnly) return;
     DBG_CLK(st, 4);
 
