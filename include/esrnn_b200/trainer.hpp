@@ -384,6 +384,18 @@ public:
         return e;
     }
 
+    // forward_stack (network.hpp:190-210; plain::forward_stack :268-287) over a general
+    // sequence with this trainer's weights -- the full dilated recurrence -- on the device.
+    // With out_bar, also the tape adjoints (Tape::backward, autodiff.hpp:397-631): network
+    // gradients by name and one input adjoint per step.
+    Matrix forward_stack(const std::vector<Matrix>& sequence) const {
+        return forward_stack_impl(sequence, nullptr, nullptr, nullptr);
+    }
+    Matrix forward_stack(const std::vector<Matrix>& sequence, const Matrix& out_bar,
+                         std::map<std::string, Matrix>& weights_bar, std::vector<Matrix>& inputs_bar) const {
+        return forward_stack_impl(sequence, &out_bar, &weights_bar, &inputs_bar);
+    }
+
     BatchGradients batch_gradients(WindowBatch& batch) {  // trainer.hpp:308-335
         BatchGradients out;
         std::vector<double> gnet(static_cast<std::size_t>(n_values_));
@@ -605,6 +617,55 @@ private:
     }
 
     // host mirrors -> device before any device call
+    Matrix forward_stack_impl(const std::vector<Matrix>& seq, const Matrix* out_bar,
+                              std::map<std::string, Matrix>* wbar, std::vector<Matrix>* xbar) const {
+        push();
+        if (seq.empty()) throw ContractError("forward_stack: empty sequence");
+        const std::size_t B = seq[0].rows(), in = static_cast<std::size_t>(stack_cfg_.input_size);
+        const int O = profile_.horizon;
+        std::vector<double> x;
+        x.reserve(seq.size() * B * in);
+        for (const Matrix& m : seq) {
+            if (m.rows() != B || m.cols() != in)
+                throw ShapeError("forward_stack: input width " + std::to_string(m.cols()) + ", expected " +
+                                 std::to_string(in));
+            x.insert(x.end(), m.data().begin(), m.data().end());
+        }
+        Matrix out(B, static_cast<std::size_t>(O));
+        std::vector<double> wb, xb;
+        if (out_bar) {
+            if (out_bar->rows() != B || out_bar->cols() != static_cast<std::size_t>(O))
+                throw ShapeError("forward_stack: out_bar shape");
+            wb.resize(static_cast<std::size_t>(n_values_));
+            xb.resize(x.size());
+        }
+        detail::check(esrnn_trainer_forward_stack(h_.get(), static_cast<std::int32_t>(seq.size()),
+                                                  static_cast<std::int32_t>(B), x.data(), out.data().data(),
+                                                  out_bar ? out_bar->data().data() : nullptr,
+                                                  out_bar ? wb.data() : nullptr, out_bar ? xb.data() : nullptr),
+                      h_.get());
+        if (out_bar) {
+            wbar->clear();
+            std::size_t off = 0;
+            StackWeights shape = weights_;
+            shape.for_each_param([&](const std::string& name, Matrix& m) {
+                Matrix g(m.rows(), m.cols());
+                std::copy(wb.begin() + static_cast<std::ptrdiff_t>(off),
+                          wb.begin() + static_cast<std::ptrdiff_t>(off + m.size()), g.data().begin());
+                off += m.size();
+                wbar->emplace(name, std::move(g));
+            });
+            xbar->clear();
+            for (std::size_t t = 0; t < seq.size(); ++t) {
+                Matrix g(B, in);
+                std::copy(xb.begin() + static_cast<std::ptrdiff_t>(t * B * in),
+                          xb.begin() + static_cast<std::ptrdiff_t>((t + 1) * B * in), g.data().begin());
+                xbar->push_back(std::move(g));
+            }
+        }
+        return out;
+    }
+
     void push() const {
         if (weights_tainted_) {
             std::vector<double> flat;

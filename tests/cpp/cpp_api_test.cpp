@@ -186,6 +186,42 @@ int main() {
             bad.rng = "not a state";
             CHECK(throws<CheckpointError>([&] { b.set_train_state(bad); }));
         }
+        // general dilated stack: forward_stack over a sequence, gradients vs central differences
+        // (test_network.cpp:235-267), with live recurrent matrices and forget gates
+        if (prec == Precision::FP64) {
+            Trainer tr(dataset(3, 23, 28, 4, 0.03), tiny_profile(), tiny_config(5, prec));
+            StackWeights w = tr.weights();
+            Rng rng(77);
+            w.for_each_param([&](const std::string&, Matrix& m) {
+                for (double& v : m.data()) v = rng.uniform(-0.5, 0.5);
+            });
+            tr.set_weights(w);
+            std::vector<Matrix> seq;
+            for (int t = 0; t < 4; ++t) {
+                Matrix m(2, 14);
+                for (double& v : m.data()) v = rng.uniform(-1.0, 1.0);
+                seq.push_back(m);
+            }
+            Matrix ob(2, 4, 1.0);
+            std::map<std::string, Matrix> wb;
+            std::vector<Matrix> xb;
+            const Matrix out = tr.forward_stack(seq, ob, wb, xb);
+            CHECK(out.rows() == 2 && out.cols() == 4 && xb.size() == 4);
+            auto total = [&](const std::vector<Matrix>& s) {
+                const Matrix o = tr.forward_stack(s);
+                double acc = 0.0;
+                for (double v : o.data()) acc += v;
+                return acc;
+            };
+            const double h = 1e-6;
+            std::vector<Matrix> sp = seq, sm = seq;
+            sp[1](0, 3) += h;
+            sm[1](0, 3) -= h;
+            const double fd = (total(sp) - total(sm)) / (2 * h);
+            CHECK(std::abs(fd - xb[1](0, 3)) < 1e-6 + 1e-5 * std::abs(fd));
+            CHECK(std::abs(wb.at("lstm0.w_recur")(1, 2)) > 0.0);  // the recurrence is live
+            CHECK(throws<ContractError>([&] { tr.forward_stack(std::vector<Matrix>{}); }));
+        }
         // same seed reproduces the loss trajectory bit for bit (test_trainer.cpp:218-230)
         {
             Trainer t1(dataset(3, 29, 28, 4, 0.03), tiny_profile(), tiny_config(42, prec));
