@@ -1114,12 +1114,14 @@ void launch_step(Eng* e, const PlanDev& pv, int s, bool grads, bool update, Stat
         e->launches += 1;
     }
     if (update) {
-        const long long n = lay.P_pad + kc;
         KS k(e, 4);
         // K4 waits for K3 the ordinary way: launched early under PDL its CTAs measured slower
         // (cfg1 +6%), while the next tile's early launch after K4 (and K3's after K2) pays
-        launch_k(e, false, k_adam<Real>, static_cast<int>((n + 255) / 256), 256, 0, st, pv, lay, s,
-                 sharded ? -1 : e->es_blocks, e->red_blocks);
+        const int net_blocks = static_cast<int>((lay.P_pad + 255) / 256);
+        const int spb = 256 / (2 + e->S);  // slots per per-series block (a thread per parameter)
+        const int slot_blocks = (kc + spb - 1) / spb;
+        launch_k(e, false, k_adam<Real>, net_blocks + slot_blocks, 256, 0, st, pv, lay, s,
+                 sharded ? -1 : e->es_blocks, e->red_blocks, net_blocks);
         e->launches += 1;
     }
 }
@@ -1376,7 +1378,7 @@ double train_epoch_impl(Eng* e) {
     const bool use_graph = e->cfg.use_graphs >= 0 && !e->profiling;
     if (e->dbg_clk.p) {
         long long seed[16];
-        for (int i = 0; i < 16; ++i) seed[i] = (i == 2 || i == 5 || i == 6 || i == 8) ? 0 : LLONG_MAX;
+        for (int i = 0; i < 16; ++i) seed[i] = (i == 2 || i == 5 || i == 6 || i == 8 || i == 10 || i == 11) ? 0 : LLONG_MAX;
         CUDA_OK(cudaMemcpyAsync(e->dbg_clk.p + 100, seed, sizeof seed, cudaMemcpyHostToDevice, e->stream));
     }
     CUDA_OK(cudaEventRecord(e->ev0, e->stream));
@@ -1467,6 +1469,8 @@ double train_epoch_impl(Eng* e) {
                              "waited %lld\n",
                      sp[1] - sp[0], sp[2] - sp[0], sp[3] - sp[0], sp[4] - sp[0], sp[5] - sp[0], sp[6] - sp[0],
                      sp[7] - sp[0], sp[8] - sp[0], sp[9] - sp[0]);
+        std::fprintf(stderr, "[esrnn dbg] step-5 K3 ES blocks end %lld, GEMM blocks end %lld\n", sp[10] - sp[0],
+                     sp[11] - sp[0]);
     }
     e->have_last = true;
     // trainer.hpp:236-242: acc += loss * count, in batch order

@@ -349,6 +349,8 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
     }
     FCLK();
     DBG_SPAN_MAX(st, s, 5);
+    if (static_cast<int>(blockIdx.x) < es_blocks) DBG_SPAN_MAX(st, s, 10);
+    else DBG_SPAN_MAX(st, s, 11);
     if (finalize & 4) {
         // single GPU, updating step: K4 derives the step scalars from the partials itself
         // (no last-CTA ticket on this kernel's tail); only a step that applies updates
@@ -432,7 +434,7 @@ __device__ __forceinline__ void adam_update(double& theta, double& m, double& v,
 // block 0 publishes them.  es_blocks < 0 (sharded): k_finalize already wrote st.scal.
 template <typename Real>
 __global__ void __launch_bounds__(256) k_adam(StateDev<Real> st, PlanDev pl, NetLayout lay, int s, int es_blocks,
-                                              int red_blocks) {
+                                              int red_blocks, int net_blocks) {
     __shared__ double red[32];
     __shared__ double sc[3];
     pdl_trigger();
@@ -480,8 +482,9 @@ __global__ void __launch_bounds__(256) k_adam(StateDev<Real> st, PlanDev pl, Net
     }
     __syncthreads();
     if (st.err[0] != 0) return;  // the reference throws before apply_updates
-    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (q < lay.P_pad) {
+    if (static_cast<int>(blockIdx.x) < net_blocks) {
+        const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+        if (q >= lay.P_pad) return;
         const Real g0 = st.gbuf[q], m0 = st.mW[q], v0 = st.vW[q], t0 = st.theta[q];
         const double scale = sc[0], bc1 = sc[1], bc2 = sc[2];
         double th = t0, m = m0, v = v0;
@@ -493,45 +496,29 @@ __global__ void __launch_bounds__(256) k_adam(StateDev<Real> st, PlanDev pl, Net
         return;
     }
     if (!st.attach) return;
+    // per-series Adam (trainer.hpp:636-650): one thread per (slot, parameter), a slot's 2+S
+    // threads in one block so the step counter is read before it is advanced
+    const int N = st.N, S = lay.S, np = 2 + S;
+    const int spb = static_cast<int>(blockDim.x) / np;
     const int k0 = pl.step_slot_off[s];
     const int k = pl.step_slot_off[s + 1] - k0;
-    const long long slot = q - lay.P_pad;
-    DBG_SPAN_MAX(st, s, 8);
-    if (slot >= k) return;
-    const int N = st.N, S = lay.S;
-    const int row = pl.slot_row[k0 + slot];
-    const int steps = st.ps_steps[row] + 1;
-    st.ps_steps[row] = steps;
-    const double scale = sc[0];
+    const int ls = threadIdx.x / np, j = threadIdx.x - ls * np;
+    const int slot = (static_cast<int>(blockIdx.x) - net_blocks) * spb + ls;
+    const bool mine = ls < spb && slot < k;
+    const int row = mine ? pl.slot_row[k0 + slot] : 0;
+    const int steps = mine ? st.ps_steps[row] + 1 : 0;
+    __syncthreads();
+    if (!mine) return;
+    if (j == 0) st.ps_steps[row] = steps;
     const double sc1 = bias_c1(st, steps);
     const double sc2 = bias_c2(st, steps);
-    const Real* g = st.psg + (size_t)slot * (2 + S);
-    for (int j0 = 0; j0 < 2 + S; j0 += 4) {
-        Real pv[4], mv[4], vv[4], gv[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int j = j0 + u;
-            if (j < 2 + S) {
-                const size_t e = (size_t)j * N + row;
-                pv[u] = st.ps[e];
-                mv[u] = st.ps_m[e];
-                vv[u] = st.ps_v[e];
-                gv[u] = g[j];
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int j = j0 + u;
-            if (j < 2 + S) {
-                const size_t e = (size_t)j * N + row;
-                double th = pv[u], m = mv[u], v = vv[u];
-                adam_update(th, m, v, static_cast<double>(gv[u]) * scale, st.lr_ps, sc1, sc2);
-                st.ps_m[e] = static_cast<Real>(m);
-                st.ps_v[e] = static_cast<Real>(v);
-                st.ps[e] = static_cast<Real>(th);
-            }
-        }
-    }
+    const size_t e = (size_t)j * N + row;
+    double th = st.ps[e], m = st.ps_m[e], v = st.ps_v[e];
+    adam_update(th, m, v, static_cast<double>(st.psg[(size_t)slot * np + j]) * sc[0], st.lr_ps, sc1, sc2);
+    st.ps_m[e] = static_cast<Real>(m);
+    st.ps_v[e] = static_cast<Real>(v);
+    st.ps[e] = static_cast<Real>(th);
+    DBG_SPAN_MAX(st, s, 8);
 }
 
 }  // namespace esrnn_dev
