@@ -296,10 +296,18 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
             const int nb = min(kGChunk, Bl - c * kGChunk);
             const Real* Ab = As + (c % kGBuf) * kGChunk * kGq + 2 * qp;
             const Real* Ub = Us + (c % kGBuf) * kGChunk * kGk + 2 * kp;
-#pragma unroll 4
+#pragma unroll 8
             for (int b = warp; b < nb; b += kFinishThreads / 32) {
-                const Real a0 = Ab[b * kGq], a1 = Ab[b * kGq + 1];
-                const Real u0 = Ub[b * kGk], u1 = Ub[b * kGk + 1];
+                Real a0, a1, u0, u1;
+                if constexpr (sizeof(Real) == 4) {  // 8-byte pairs (2*qp, 2*kp are even)
+                    const float2 a = *reinterpret_cast<const float2*>(Ab + b * kGq);
+                    const float2 u = *reinterpret_cast<const float2*>(Ub + b * kGk);
+                    a0 = a.x, a1 = a.y, u0 = u.x, u1 = u.y;
+                } else {
+                    const double2 a = *reinterpret_cast<const double2*>(Ab + b * kGq);
+                    const double2 u = *reinterpret_cast<const double2*>(Ub + b * kGk);
+                    a0 = a.x, a1 = a.y, u0 = u.x, u1 = u.y;
+                }
                 acc[0][0] += a0 * u0;
                 acc[0][1] += a0 * u1;
                 acc[1][0] += a1 * u0;
