@@ -145,6 +145,25 @@ __device__ __forceinline__ T block_sum(T v, T* red) {
     return r;  // valid in thread 0
 }
 
+// Three block sums at once, each in block_sum's fixed order (bit-identical results), with
+// one barrier pair instead of three.  Valid in thread 0.
+__device__ __forceinline__ void block_sum3(double& a, double& b, double& c, double* red /*[3 * 32]*/) {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_down_sync(0xffffffffu, a, o);
+        b += __shfl_down_sync(0xffffffffu, b, o);
+        c += __shfl_down_sync(0xffffffffu, c, o);
+    }
+    if (lane == 0) red[wid] = a, red[32 + wid] = b, red[64 + wid] = c;
+    __syncthreads();
+    double ra = 0, rb = 0, rc = 0;
+    if (threadIdx.x == 0)
+        for (int w = 0; w < nw; ++w) ra += red[w], rb += red[32 + w], rc += red[64 + w];
+    __syncthreads();
+    a = ra, b = rb, c = rc;
+}
+
 // global-timer stamp (ns) into dbg_clk[80 + i], block 0 thread 0 (kernel start/end timeline)
 __device__ __forceinline__ long long gtimer() {
     long long t;

@@ -443,14 +443,50 @@ __device__ __forceinline__ void adam_update(double& theta, double& m, double& v,
 template <typename Real>
 __global__ void __launch_bounds__(256) k_adam(StateDev<Real> st, PlanDev pl, NetLayout lay, int s, int es_blocks,
                                               int red_blocks, int net_blocks) {
-    __shared__ double red[32];
+    __shared__ double red[96];
     __shared__ double sc[3];
     pdl_trigger();
     pdl_wait();
     DBG_GT(st, 6);
     DBG_SPAN_MIN(st, s, 7);
     const int tid = threadIdx.x;
+    // this thread's Adam operands first: their L2 latency overlaps the scalar reduction
+    // below.  Network blocks: one live parameter; per-series blocks (trainer.hpp:636-650):
+    // one (slot, parameter), a slot's 2+S threads in one block so its step counter is read
+    // before it is advanced.
+    const bool net = static_cast<int>(blockIdx.x) < net_blocks;
+    const int N = st.N, np = 2 + lay.S;
+    const long long q = (long long)blockIdx.x * blockDim.x + tid;
+    bool mine = false;
+    int row = 0, steps = 0, j = 0, slot = 0;
+    size_t e = 0;
+    Real g0 = 0, m0 = 0, v0 = 0, t0 = 0;
+    double c1 = 1.0, c2 = 1.0;
+    if (net) {
+        mine = q < lay.P_pad;
+        if (mine) g0 = st.gbuf[q], m0 = st.mW[q], v0 = st.vW[q], t0 = st.theta[q];
+    } else if (st.attach) {
+        const int spb = static_cast<int>(blockDim.x) / np;
+        const int k0 = pl.step_slot_off[s];
+        const int k = pl.step_slot_off[s + 1] - k0;
+        const int ls = tid / np;
+        j = tid - ls * np;
+        slot = (static_cast<int>(blockIdx.x) - net_blocks) * spb + ls;
+        mine = ls < spb && slot < k;
+        if (mine) {
+            row = pl.slot_row[k0 + slot];
+            steps = st.ps_steps[row] + 1;
+            e = (size_t)j * N + row;
+            g0 = st.psg[(size_t)slot * np + j], m0 = st.ps_m[e], v0 = st.ps_v[e], t0 = st.ps[e];
+            c1 = bias_c1(st, steps);
+            c2 = bias_c2(st, steps);
+        }
+    }
     if (es_blocks >= 0) {
+        // single GPU: the step scalars from K3's partials -- clip scale (trainer.hpp:603-615),
+        // bias corrections at the step K3 advanced (:617-620), step loss -- with the same
+        // loads, order and tree as the last-CTA finalisation, so every block holds identical
+        // values; block 0 publishes them
         const int w0 = pl.step_win_off[s];
         const int nt = (pl.step_win_off[s + 1] - w0 + kR - 1) / kR;
         double es = 0.0, ls = 0.0, all = 0.0;
@@ -458,9 +494,7 @@ __global__ void __launch_bounds__(256) k_adam(StateDev<Real> st, PlanDev pl, Net
             for (int b = tid; b < es_blocks; b += blockDim.x) es += __ldcg(st.es_sq_part + b);
         for (int t = tid; t < nt; t += blockDim.x) ls += __ldcg(st.loss_part + t);
         for (int b = tid; b < red_blocks; b += blockDim.x) all += __ldcg(st.red_sq_part + b);
-        es = block_sum(es, red);
-        ls = block_sum(ls, red);
-        all = block_sum(all, red);
+        block_sum3(es, ls, all, red);
         if (tid == 0) {
             double scale = 1.0;
             if (st.has_clip) {
@@ -483,49 +517,26 @@ __global__ void __launch_bounds__(256) k_adam(StateDev<Real> st, PlanDev pl, Net
                 }
             }
         }
-    } else if (tid == 0) {
+    } else if (tid == 0) {  // sharded: k_finalize already wrote them
         sc[0] = st.scal[0];
         sc[1] = st.scal[1];
         sc[2] = st.scal[2];
     }
     __syncthreads();
-    if (st.err[0] != 0) return;  // the reference throws before apply_updates
-    if (static_cast<int>(blockIdx.x) < net_blocks) {
-        const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-        if (q >= lay.P_pad) return;
-        const Real g0 = st.gbuf[q], m0 = st.mW[q], v0 = st.vW[q], t0 = st.theta[q];
-        const double scale = sc[0], bc1 = sc[1], bc2 = sc[2];
-        double th = t0, m = m0, v = v0;
-        adam_update(th, m, v, static_cast<double>(g0) * scale, st.lr_net, bc1, bc2);
+    if (!mine || st.err[0] != 0) return;  // the reference throws before apply_updates
+    double th = t0, m = m0, v = v0;
+    if (net) {
+        adam_update(th, m, v, static_cast<double>(g0) * sc[0], st.lr_net, sc[1], sc[2]);
         st.mW[q] = static_cast<Real>(m);
         st.vW[q] = static_cast<Real>(v);
         st.theta[q] = static_cast<Real>(th);
-        DBG_SPAN_MAX(st, s, 8);
-        return;
+    } else {
+        if (j == 0) st.ps_steps[row] = steps;
+        adam_update(th, m, v, static_cast<double>(g0) * sc[0], st.lr_ps, c1, c2);
+        st.ps_m[e] = static_cast<Real>(m);
+        st.ps_v[e] = static_cast<Real>(v);
+        st.ps[e] = static_cast<Real>(th);
     }
-    if (!st.attach) return;
-    // per-series Adam (trainer.hpp:636-650): one thread per (slot, parameter), a slot's 2+S
-    // threads in one block so the step counter is read before it is advanced
-    const int N = st.N, S = lay.S, np = 2 + S;
-    const int spb = static_cast<int>(blockDim.x) / np;
-    const int k0 = pl.step_slot_off[s];
-    const int k = pl.step_slot_off[s + 1] - k0;
-    const int ls = threadIdx.x / np, j = threadIdx.x - ls * np;
-    const int slot = (static_cast<int>(blockIdx.x) - net_blocks) * spb + ls;
-    const bool mine = ls < spb && slot < k;
-    const int row = mine ? pl.slot_row[k0 + slot] : 0;
-    const int steps = mine ? st.ps_steps[row] + 1 : 0;
-    __syncthreads();
-    if (!mine) return;
-    if (j == 0) st.ps_steps[row] = steps;
-    const double sc1 = bias_c1(st, steps);
-    const double sc2 = bias_c2(st, steps);
-    const size_t e = (size_t)j * N + row;
-    double th = st.ps[e], m = st.ps_m[e], v = st.ps_v[e];
-    adam_update(th, m, v, static_cast<double>(st.psg[(size_t)slot * np + j]) * sc[0], st.lr_ps, sc1, sc2);
-    st.ps_m[e] = static_cast<Real>(m);
-    st.ps_v[e] = static_cast<Real>(v);
-    st.ps[e] = static_cast<Real>(th);
     DBG_SPAN_MAX(st, s, 8);
 }
 
