@@ -98,9 +98,14 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
             pdl_wait();
             DBG_SPAN_MIN(st, s, 4);
             Real a_raw = 0, g_raw = 0;
+            Real s0[SC > 0 ? SC : 1];  // exp(seas_raw) for the output's chain rule, loaded up front
             if (mine) {
                 a_raw = st.ps[lrow];
                 g_raw = st.ps[N + lrow];
+                if constexpr (SC > 0) {
+#pragma unroll
+                    for (int j = 0; j < SC; ++j) s0[j] = st.ps[(size_t)(2 + j) * N + lrow];
+                }
             }
             // forward levels / seasonalities of the block's slots: whole 16-byte pieces of the
             // [t][kcap] rows (kcap and sl0 are multiples of kEsSlotsPerBlock)
@@ -226,20 +231,19 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
                 o[0] = ga;
                 o[1] = gg;
                 sq += static_cast<double>(ga) * ga + static_cast<double>(gg) * gg;
-                for (int j = 0; j < S; ++j) {
-                    const Real sj = M::exp_ps(st.ps[(2 + j) * N + row]);
-                    Real sbj;
-                    if constexpr (SC > 0) {
-                        sbj = 0;
+                if constexpr (SC > 0) {
 #pragma unroll
-                        for (int jj = 0; jj < SC; ++jj)
-                            if (jj == j) sbj = sfin[jj];
-                    } else {
-                        sbj = sb[j];
+                    for (int j = 0; j < SC; ++j) {
+                        const Real g = sfin[j] * M::exp_ps(s0[j]);
+                        o[2 + j] = g;
+                        sq += static_cast<double>(g) * g;
                     }
-                    const Real g = sbj * sj;
-                    o[2 + j] = g;
-                    sq += static_cast<double>(g) * g;
+                } else {
+                    for (int j = 0; j < S; ++j) {
+                        const Real g = sb[j] * M::exp_ps(st.ps[(2 + j) * N + row]);
+                        o[2 + j] = g;
+                        sq += static_cast<double>(g) * g;
+                    }
                 }
             }
         } else {
