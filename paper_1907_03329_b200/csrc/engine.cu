@@ -376,7 +376,6 @@ struct esrnn_trainer {
     std::vector<int64_t> live_flat;   // compact index -> flat index
     std::vector<double> w_host;       // flat StackWeights mirror (dead entries live only here)
     std::vector<int> cat_host;
-    std::vector<double> vals_host;    // local rows, row-major (for validate bookkeeping)
     HostRng rng{0};
     std::string err;
     double last_ms = 0.0;
@@ -1029,8 +1028,7 @@ void launch_k(Eng* e, bool pdl, void (*kern)(KArgs...), int grid, int block, siz
 
 template <typename Real, int SC>
 void launch_finish_sc(Eng* e, const StateDev<Real>& st, const PlanDev& pv, int s, int finalize, bool pdl) {
-    static const bool nored = std::getenv("ESRNN_DEBUG_NORED") != nullptr;  // timing experiments only
-    launch_k(e, pdl, k_grad_finish<Real, SC>, e->es_blocks + (nored ? 0 : e->red_blocks), kFinishThreads,
+    launch_k(e, pdl, k_grad_finish<Real, SC>, e->es_blocks + e->red_blocks, kFinishThreads,
              finish_smem<Real>(e->lay), st, pv, e->lay, s, e->es_blocks, finalize);
 }
 template <typename Real>
