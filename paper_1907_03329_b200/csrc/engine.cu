@@ -1640,23 +1640,34 @@ void forecast_impl(Eng* e, int64_t drop_tail, double* out, int mode, const Score
     if (e->profiling) e->prof_collect();
     CUDA_OK(cudaEventRecord(e->ev1, e->stream));
     CUDA_OK(cudaGetLastError());
+    // results into pinned staging on the same stream: one synchronisation for everything
+    const size_t nfo = static_cast<size_t>(N) * O, nsc = mode == 2 ? 4 * static_cast<size_t>(N) : 0;
+    e->pin_d.reserve(nfo + N + nsc + 1);
+    double* pf = e->pin_d.p;
+    double* psm = pf + nfo;
+    double* psc = psm + N;
+    if (N > 0) {
+        if (out) CUDA_OK(cudaMemcpyAsync(pf, e->f_out.p, sizeof(double) * nfo, cudaMemcpyDeviceToHost, e->stream));
+        if (mode != 0)
+            CUDA_OK(cudaMemcpyAsync(psm, e->f_smape.p, sizeof(double) * N, cudaMemcpyDeviceToHost, e->stream));
+        if (mode == 2)
+            CUDA_OK(cudaMemcpyAsync(psc, e->f_score.p, sizeof(double) * nsc, cudaMemcpyDeviceToHost, e->stream));
+    }
     CUDA_OK(cudaStreamSynchronize(e->stream));
     float ms = 0.f;
     CUDA_OK(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
     e->last_ms = ms;
     throw_device_error(e);
-    if (out && N > 0) CUDA_OK(cudaMemcpy(out, e->f_out.p, sizeof(double) * N * O, cudaMemcpyDeviceToHost));
+    if (out && N > 0) std::memcpy(out, pf, sizeof(double) * nfo);
     if (mode == 0) return;
-    std::vector<double> sm(std::max(N, 1));
-    if (N > 0) CUDA_OK(cudaMemcpy(sm.data(), e->f_smape.p, sizeof(double) * N, cudaMemcpyDeviceToHost));
+    const double* sm = psm;
     if (so.smape)
         for (int i = 0; i < N; ++i) so.smape[i] = sm[i];
     // global sums: [smape, mase, mase count, naive smape, naive mase, naive mase count, series, 0]
     double tot[8] = {0, 0, 0, 0, 0, 0, static_cast<double>(N), 0};
     for (int i = 0; i < N; ++i) tot[0] += sm[i];
     if (mode == 2) {
-        std::vector<double> sc(4 * static_cast<size_t>(std::max(N, 1)));
-        if (N > 0) CUDA_OK(cudaMemcpy(sc.data(), e->f_score.p, sizeof(double) * 4 * N, cudaMemcpyDeviceToHost));
+        const double* sc = psc;
         for (int i = 0; i < N; ++i) {
             const double ns = sc[N + i], nm = sc[2 * N + i], m = sc[3 * N + i];
             if (so.mase) so.mase[i] = m;
