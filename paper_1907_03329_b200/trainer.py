@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import functools
 import time
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
@@ -345,6 +346,12 @@ def early_stop_check(history: Sequence[float], patience: int, min_delta: float =
     return len(history) - 1 - last_improve >= patience
 
 
+@functools.lru_cache(maxsize=8)
+def _default_ids(n: int) -> list:
+    """Ids of array-constructed datasets ("S0", "S1", ...; the synthetic generator's ids)."""
+    return [f"S{i}" for i in range(n)]
+
+
 class Trainer:
     """esrnn::Trainer (trainer.hpp:157-673) backed by a native engine handle."""
 
@@ -357,7 +364,7 @@ class Trainer:
             values, cats = series
             values = np.ascontiguousarray(values, dtype=np.float64)
             cats = np.ascontiguousarray(cats, dtype=np.int32)
-            self._ids = [f"S{i}" for i in range(values.shape[0])]
+            self._ids_list = None  # "S{i}" ids, built on first use (_ids)
         else:
             series = list(series)
             if not series:
@@ -369,7 +376,7 @@ class Trainer:
                                         f"has {len(s.values)} values, expected {n}")
             values = np.ascontiguousarray(np.stack([np.asarray(s.values, dtype=np.float64) for s in series]))
             cats = np.array([-1 if s.category is None else int(s.category) for s in series], dtype=np.int32)
-            self._ids = [s.id for s in series]
+            self._ids_list = [s.id for s in series]
         self._values = values
         self._cats = cats
         c_dist = None
@@ -396,6 +403,12 @@ class Trainer:
             self.param_layout.append((info.name.decode(), info.rows, info.cols, info.offset))
 
     # -- plumbing -------------------------------------------------------------------
+    @property
+    def _ids(self) -> list:
+        if self._ids_list is None:
+            self._ids_list = _default_ids(self._values.shape[0])  # shared, read-only by convention
+        return self._ids_list
+
     def _chk(self, status):
         self.api.check(status, self._h)
 
