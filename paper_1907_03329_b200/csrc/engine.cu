@@ -18,6 +18,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <future>
 #include <chrono>
 #include <list>
 #include <map>
@@ -320,6 +321,7 @@ struct HostPlan {
 // buffer in upload order, so the epoch's plan goes to the device as a few async copies.
 struct EpochPlan {
     std::mt19937_64 rng_before;  // trainer RNG before this epoch's shuffle (exact-resume state)
+    std::vector<uint64_t> wbuf;  // shuffle scratch: (row, anchor) pairs
     std::vector<int> wr, wa;
     std::vector<HostPlan> chunks;
     int steps = 0;
@@ -332,6 +334,31 @@ struct EpochPlan {
     size_t n_w = 0, n_slots = 0;
     int max_step_windows = 0, max_step_slots = 0;
 };
+
+// Released trainers' epoch plans (host vectors + pinned upload buffer), reused by the next
+// trainer so its first plan writes to warm memory instead of faulting in fresh pages.
+struct PlanPool {
+    std::mutex mu;
+    std::vector<EpochPlan> free;
+};
+PlanPool& plan_pool() {
+    static PlanPool* p = new PlanPool;  // never destroyed
+    return *p;
+}
+EpochPlan plan_pool_get() {
+    PlanPool& p = plan_pool();
+    std::lock_guard<std::mutex> g(p.mu);
+    if (p.free.empty()) return EpochPlan{};
+    EpochPlan e = std::move(p.free.back());
+    p.free.pop_back();
+    e.ready = false;
+    return e;
+}
+void plan_pool_put(EpochPlan&& e) {
+    PlanPool& p = plan_pool();
+    std::lock_guard<std::mutex> g(p.mu);
+    if (p.free.size() < 8) p.free.push_back(std::move(e));
+}
 
 struct DevPlan {
     DBuf<int> w_row, w_anchor, w_slot, w_first, step_win_off, step_slot_off, slot_row, slot_win_off, slot_win, w_csr, csr_anchor;
@@ -476,6 +503,8 @@ struct esrnn_trainer {
 
     ~esrnn_trainer() {
         join_plan();
+        plan_pool_put(std::move(cur_plan));
+        plan_pool_put(std::move(next_plan));
         if (stream) cudaStreamSynchronize(stream);  // buffers go back to the block cache below
         release_buffers();
         graph.reset();
@@ -1220,7 +1249,7 @@ void build_epoch_plan(Eng* e, EpochPlan& ep) {
     ep.wa.resize(nw);
     {
         // shuffle (row, anchor) pairs together: one random access per swap
-        static thread_local std::vector<uint64_t> w;
+        std::vector<uint64_t>& w = ep.wbuf;
         w.resize(nw);
         int64_t n = 0;
         for (int r = 0; r < e->N_global; ++r)
@@ -1857,33 +1886,45 @@ esrnn_status esrnn_trainer_create(const esrnn_profile* profile, const esrnn_trai
             }
         }
 
-        // network.hpp:89-116 init order on the trainer RNG (identical on every rank)
+        // network.hpp:89-116 init order on the trainer RNG (identical on every rank).  The
+        // first epoch's shuffle is the RNG's next consumer, so one helper thread draws the
+        // weights, then shuffles and plans epoch 1, while this thread sets up the device
+        // state; the weights are uploaded once the helper has drawn them.
         e->rng = HostRng(cfg->seed);
         e->w_host.assign(e->P, 0.0);
-        const int H = e->H;
-        const double bound = 1.0 / std::sqrt(static_cast<double>(H));
-        for (int l = 0; l < e->L; ++l) {
-            for (int64_t i = 0; i < static_cast<int64_t>(e->layer_in[l]) * 4 * H; ++i)
-                e->w_host[e->off_win[l] + i] = e->rng.uniform(-bound, bound);
-            for (int64_t i = 0; i < static_cast<int64_t>(H) * 4 * H; ++i)
-                e->w_host[e->off_wrec[l] + i] = e->rng.uniform(-bound, bound);
-            for (int c = H; c < 2 * H; ++c) e->w_host[e->off_bias[l] + c] = 1.0;
-        }
-        for (int64_t i = 0; i < static_cast<int64_t>(H) * H; ++i) e->w_host[e->off_nlw + i] = e->rng.uniform(-bound, bound);
-        for (int64_t i = 0; i < static_cast<int64_t>(H) * e->O; ++i) e->w_host[e->off_outw + i] = e->rng.uniform(-bound, bound);
-
+        e->cur_plan = plan_pool_get();
+        e->next_plan = plan_pool_get();
+        Eng* ep = e.get();
+        auto init_weights = [ep] {
+            const int H = ep->H;
+            const double bound = 1.0 / std::sqrt(static_cast<double>(H));
+            for (int l = 0; l < ep->L; ++l) {
+                for (int64_t i = 0; i < static_cast<int64_t>(ep->layer_in[l]) * 4 * H; ++i)
+                    ep->w_host[ep->off_win[l] + i] = ep->rng.uniform(-bound, bound);
+                for (int64_t i = 0; i < static_cast<int64_t>(H) * 4 * H; ++i)
+                    ep->w_host[ep->off_wrec[l] + i] = ep->rng.uniform(-bound, bound);
+                for (int c2 = H; c2 < 2 * H; ++c2) ep->w_host[ep->off_bias[l] + c2] = 1.0;
+            }
+            for (int64_t i = 0; i < static_cast<int64_t>(H) * H; ++i) ep->w_host[ep->off_nlw + i] = ep->rng.uniform(-bound, bound);
+            for (int64_t i = 0; i < static_cast<int64_t>(H) * ep->O; ++i)
+                ep->w_host[ep->off_outw + i] = ep->rng.uniform(-bound, bound);
+        };
+        std::promise<void> weights_drawn;
+        std::future<void> weights_ready = weights_drawn.get_future();
         c[nc++] = clk::now();
-        // the first epoch's shuffle is the next consumer of the trainer RNG: build its plan
-        // on a helper thread while the device state is set up
         if (std::max(0, T - e->O - e->I + 1) > 0) {
-            Eng* ep = e.get();
-            ep->plan_thread = std::thread([ep] {
+            ep->plan_thread = std::thread([ep, init_weights, p = std::move(weights_drawn)]() mutable {
+                init_weights();
+                p.set_value();
                 try {
                     build_epoch_plan(ep, ep->next_plan);
                 } catch (...) {
                     ep->next_plan.ready = false;  // rebuilt (from a fresh shuffle) by train_epoch
                 }
             });
+        } else {
+            init_weights();
+            weights_drawn.set_value();
         }
         c[nc++] = clk::now();
         e->bc_tab = bc_table(e->cfg.device);
@@ -1894,6 +1935,7 @@ esrnn_status esrnn_trainer_create(const esrnn_profile* profile, const esrnn_trai
             alloc_state<float>(e.get());
             upload_values<float>(e.get(), values, category);
         }
+        weights_ready.wait();
         c[nc++] = clk::now();
         upload_theta(e.get());
         ensure_capacity(e.get(), cfg->batch_size);
@@ -1903,7 +1945,7 @@ esrnn_status esrnn_trainer_create(const esrnn_profile* profile, const esrnn_trai
             std::fprintf(stderr, "[esrnn host] create:");
             for (int i = 1; i < nc; ++i)
                 std::fprintf(stderr, " %.0f", std::chrono::duration<double, std::micro>(c[i] - c[i - 1]).count());
-            std::fprintf(stderr, " us (setup+stream, rng init, plan thread, alloc+values, theta+capacity+sync)\n");
+            std::fprintf(stderr, " us (setup+stream, plan thread start, alloc+values, weights wait, theta+capacity+sync)\n");
         }
     });
     if (st == ESRNN_OK) *out = e.release();
