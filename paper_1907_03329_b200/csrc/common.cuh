@@ -94,7 +94,10 @@ struct StateDev {
     Real* gbuf;             // [P_pad + 2]  (comm buffer: grads | ps sq-norm | loss sum)
     Real* psg;              // [kcap][2+S]
     double* es_sq_part;     // [es blocks]
-    double* red_sq_part;    // [reduce blocks]
+    double* red_sq_part;    // [weight-gradient tiles]
+    Real* gpart;            // [gsplit][tiles][32 lanes][6]: row-part tile partials (large steps)
+    unsigned* gtile_ctr;    // [tiles] arrival tickets of a tile's row parts
+    int red_tiles;          // K3 weight-gradient output tiles
     unsigned int* done_ctr; // [2]
     double* scal;           // [4] scale, bc1, bc2, loss
     long long* net_step;

@@ -422,7 +422,9 @@ struct esrnn_trainer {
     DBuf<unsigned char> lv, se, contrib, rowstore, gbuf, psg, d_inputs, d_targets, d_seas, d_levels;
     DBuf<unsigned char> fX, fL, fS, dump_lv, dump_se;
     DBuf<double> loss_part, es_sq_part, red_sq_part, scal, loss_hist, f_out, f_smape, f_score, smape_sum;
-    DBuf<unsigned int> done_ctr;
+    DBuf<unsigned int> done_ctr, gtile_ctr;
+    DBuf<unsigned char> gpart;
+    int gsplit = 1;  // K3 weight-gradient row parts per output tile (large steps)
     const double* bc_tab = nullptr;  // process-wide bias-correction table of this GPU (StateDev::bc)
     DBuf<long long> net_step;
     DBuf<long long> dbg_clk;  // ESRNN_DEBUG_CLOCKS: per-phase clock64 stamps of tile 0
@@ -489,7 +491,7 @@ struct esrnn_trainer {
         };
         add(vals, vrm, ps, ps_m, ps_v, theta, mW, vW, cat, ps_steps, lv, se, contrib, rowstore, gbuf, psg, d_inputs,
             d_targets, d_seas, d_levels, fX, fL, fS, dump_lv, dump_se, loss_part, es_sq_part, red_sq_part, scal,
-            loss_hist, f_out, f_smape, f_score, smape_sum, done_ctr, net_step, dbg_clk, errw);
+            loss_hist, f_out, f_smape, f_score, smape_sum, done_ctr, gtile_ctr, gpart, net_step, dbg_clk, errw);
         for (DevPlan* d : {&epoch_plan, &batch_plan})
             add(d->w_row, d->w_anchor, d->w_slot, d->w_first, d->step_win_off, d->step_slot_off, d->slot_row,
                 d->slot_win_off, d->slot_win, d->w_csr, d->csr_anchor, d->step_M, d->mask);
@@ -539,6 +541,9 @@ struct esrnn_trainer {
         s.psg = reinterpret_cast<Real*>(psg.p);
         s.es_sq_part = es_sq_part.p;
         s.red_sq_part = red_sq_part.p;
+        s.gpart = reinterpret_cast<Real*>(gpart.p);
+        s.gtile_ctr = gtile_ctr.p;
+        s.red_tiles = red_blocks;
         s.done_ctr = done_ctr.p;
         s.scal = scal.p;
         s.net_step = net_step.p;
@@ -826,6 +831,14 @@ void ensure_capacity(Eng* e, int B) {
     const int kc = e->kcap;
     e->tiles_cap = (B + kRows - 1) / kRows;
     e->es_blocks = (kc + kEsSlotsPerBlock - 1) / kEsSlotsPerBlock;
+    // Row parts per weight-gradient tile: at B <= 4,096 one block per tile is fastest (a
+    // two-part split measured +6.8 us at cfg1); beyond, one part per 4,096 rows (<= 16)
+    e->gsplit = std::max(1, std::min(16, B / 4096));
+    e->gpart.alloc(e->rsz * static_cast<size_t>(e->gsplit) * std::max(e->red_blocks, 1) * 32 * 6);
+    if (e->gtile_ctr.n < static_cast<size_t>(std::max(e->red_blocks, 1))) {
+        e->gtile_ctr.alloc(std::max(e->red_blocks, 1));
+        e->gtile_ctr.zero(e->stream);
+    }
     e->lv.alloc(r * T * kc);
     e->se.alloc(r * (T + S) * kc);
     e->contrib.alloc(r * static_cast<size_t>(B) * ((I + O + 2 + 3) & ~3));
@@ -1057,8 +1070,8 @@ void launch_k(Eng* e, bool pdl, void (*kern)(KArgs...), int grid, int block, siz
 
 template <typename Real, int SC>
 void launch_finish_sc(Eng* e, const StateDev<Real>& st, const PlanDev& pv, int s, int finalize, bool pdl) {
-    launch_k(e, pdl, k_grad_finish<Real, SC>, e->es_blocks + e->red_blocks, kFinishThreads,
-             finish_smem<Real>(e->lay), st, pv, e->lay, s, e->es_blocks, finalize);
+    launch_k(e, pdl, k_grad_finish<Real, SC>, e->es_blocks + e->red_blocks * e->gsplit, kFinishThreads,
+             finish_smem<Real>(e->lay), st, pv, e->lay, s, e->es_blocks, finalize, e->gsplit);
 }
 template <typename Real>
 void launch_finish(Eng* e, const StateDev<Real>& st, const PlanDev& pv, int s, int finalize, bool pdl = false) {

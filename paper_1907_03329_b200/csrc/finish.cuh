@@ -42,7 +42,7 @@ __device__ void finalize_scalars(StateDev<Real>& st, const PlanDev& pl, int s, d
 
 template <typename Real, int SC>
 __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> st, PlanDev pl, NetLayout lay, int s,
-                                                                int es_blocks, int finalize) {
+                                                                int es_blocks, int finalize, int gsplit) {
     using M = Math<Real>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ double red[32];
@@ -254,9 +254,12 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
     } else {
         pdl_wait();
         // ------- weight gradients: G[q][k] = sum_b A[b][q] U[b][k] over the step's windows ----
-        // block -> (matrix, 16 q x 8 k output block); warp w sums rows b = w (mod 8) in order,
-        // warps are combined in order: a fixed summation order, no atomics
-        const int gb = blockIdx.x - es_blocks;
+        // block -> (matrix, 16 q x 8 k output block, row part); warp w sums rows b = w (mod 8)
+        // of its part in order, warps are combined in order, and for large steps (gsplit > 1
+        // row parts) the last-arriving part adds the parts' tiles in part order: a fixed
+        // summation order, no float atomics
+        const int gbp = blockIdx.x - es_blocks;
+        const int gb = gbp / gsplit, part = gbp - gb * gsplit;
         int m = 0;
         while (m + 1 < lay.nmat && gb >= lay.mat_blk0[m + 1]) ++m;
         const MatDesc md = lay.mats[m];
@@ -264,7 +267,11 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
         const int nkb = (md.K + kGk - 1) / kGk;
         const int q0 = (local / nkb) * kGq, k0 = (local % nkb) * kGk;
         const int wb0 = pl.step_win_off[s];
-        const int Bl = pl.step_win_off[s + 1] - wb0;
+        const int Bstep = pl.step_win_off[s + 1] - wb0;
+        // this part's rows [r0, r0 + Bl) of the step's row store (chunk-aligned split)
+        const int span = ((Bstep + gsplit - 1) / gsplit + kGChunk - 1) / kGChunk * kGChunk;
+        const int r0 = min(Bstep, part * span);
+        const int Bl = min(Bstep, r0 + span) - r0;
         const int lane = tid & 31, warp = tid >> 5;
         const int qp = lane >> 2, kp = lane & 3;
         Real* As = reinterpret_cast<Real*>(smem_raw);       // [kGBuf][kGChunk][kGq]
@@ -279,7 +286,7 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
             const int nb = min(kGChunk, Bl - c0);
             for (int i = tid; i < nb * (ca + cu); i += kFinishThreads) {
                 const int row = i / (ca + cu), part = i - row * (ca + cu);
-                const Real* src = st.rowstore + (size_t)(c0 + row) * rs_ld;
+                const Real* src = st.rowstore + (size_t)(r0 + c0 + row) * rs_ld;
                 if (part < ca)
                     cp_async16(As + (buf * kGChunk + row) * kGq + part * e16, src + md.a_off + q0 + part * e16);
                 else
@@ -330,13 +337,39 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
         rd[4] = bacc[0];
         rd[5] = bacc[1];
         __syncthreads();
+        __shared__ bool last_part;
+        Real t[6];
         if (warp == 0) {
-            Real t[6];
 #pragma unroll
             for (int j = 0; j < 6; ++j) t[j] = Rd[lane * 6 + j];
             for (int w = 1; w < kFinishThreads / 32; ++w)
 #pragma unroll
                 for (int j = 0; j < 6; ++j) t[j] += Rd[(w * 32 + lane) * 6 + j];
+            if (gsplit > 1) {
+                // publish this part's tile; the last part to arrive combines them
+                Real* mine = st.gpart + ((size_t)part * st.red_tiles + gb) * 32 * 6 + lane * 6;
+#pragma unroll
+                for (int j = 0; j < 6; ++j) mine[j] = t[j];
+                __threadfence();
+                __syncwarp();
+                if (lane == 0) last_part = atomicAdd(st.gtile_ctr + gb, 1u) == static_cast<unsigned>(gsplit - 1);
+                __syncwarp();
+            }
+        }
+        __syncthreads();
+        const bool writer = gsplit == 1 || last_part;  // else another part writes this tile
+        if (warp == 0 && writer) {
+            if (gsplit > 1) {
+                __threadfence();
+                if (lane == 0) st.gtile_ctr[gb] = 0;
+#pragma unroll
+                for (int j = 0; j < 6; ++j) {
+                    Real a = 0;
+                    for (int p = 0; p < gsplit; ++p)
+                        a += __ldcg(st.gpart + ((size_t)p * st.red_tiles + gb) * 32 * 6 + lane * 6 + j);
+                    t[j] = a;
+                }
+            }
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
                 const int q = q0 + 2 * qp + i;
@@ -357,7 +390,7 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
             }
         }
         const double tot = block_sum(sq, red);
-        if (tid == 0) st.red_sq_part[gb] = tot;
+        if (tid == 0 && writer) st.red_sq_part[gb] = tot;
     }
     FCLK();
     DBG_SPAN_MAX(st, s, 5);
@@ -382,7 +415,7 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
     __threadfence();
     if (tid == 0 && st.dbg_clk) st.dbg_clk[85] = gtimer();
     // all threads sum the per-block parts (strided, then a fixed tree): L2 loads in flight at once
-    const int nrb = gridDim.x - es_blocks;
+    const int nrb = st.red_tiles;
     const int w0 = pl.step_win_off[s];
     const int nt = (pl.step_win_off[s + 1] - w0 + kR - 1) / kR;
     double es = 0.0, ls = 0.0, all = 0.0;

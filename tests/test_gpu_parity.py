@@ -357,3 +357,23 @@ def test_two_wave_batch_matches_oracle(engine, oracle, precision, tol):
         assert tensor_err(gg.network[name_], arr) < tol * 10, name_
     lg, lo = g.train_epoch(), o.train_epoch()
     assert max_rel(lg, lo) < (1e-8 if precision == "fp64" else 1e-3)
+
+
+@pytest.mark.parametrize("precision,tol", [("fp32", 1e-4), ("fp64", 1e-10)])
+def test_large_step_split_gradient_tiles(engine, oracle, precision, tol):
+    """A step of >= 8,192 windows splits each weight-gradient tile's rows over several blocks
+    (ticketed, fixed-order combine): gradients still match the oracle."""
+    prof, vals, cats = dataset(oracle, "monthly", 300, 17)
+    kw = dict(batch_size=8500, max_batch_size=16384)
+    g = Trainer((vals, cats), prof, TrainConfig(seed=7, precision=precision, **kw), api=engine)
+    o = Trainer((vals, cats), prof, TrainConfig(seed=7, precision="fp64", **kw), api=oracle)
+    b = sample_batch(o, 8500, 5)
+    gg, go = g.batch_gradients(copy_batch(b)), o.batch_gradients(copy_batch(b))
+    assert max_rel(gg.loss, go.loss) < tol
+    for name_, arr in go.network.items():
+        assert tensor_err(gg.network[name_], arr) < tol * 10, name_
+    # determinism of the split combine
+    g2 = Trainer((vals, cats), prof, TrainConfig(seed=7, precision=precision, **kw), api=engine)
+    gg2 = g2.batch_gradients(copy_batch(b))
+    for name_ in go.network:
+        assert np.array_equal(gg.network[name_], gg2.network[name_]), name_
