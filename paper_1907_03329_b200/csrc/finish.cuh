@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
                 __syncwarp();
             }
         }
-        __syncthreads();
+        if (gsplit > 1) __syncthreads();  // last_part (block-uniform branch)
         const bool writer = gsplit == 1 || last_part;  // else another part writes this tile
         if (warp == 0 && writer) {
             if (gsplit > 1) {
