@@ -26,6 +26,9 @@
 #pragma once
 #include "common.cuh"
 
+// k_tile<kLossOnly> returns after the loss; its backward half is statically unreachable
+#pragma nv_diag_suppress 128
+
 namespace esrnn_dev {
 
 enum StackMode { kTrain = 0, kLossOnly = 1, kForecast = 2 };
