@@ -346,6 +346,9 @@ def early_stop_check(history: Sequence[float], patience: int, min_delta: float =
     return len(history) - 1 - last_improve >= patience
 
 
+_LAYOUTS: dict = {}  # (library, profile shape) -> (n_values, [(name, rows, cols, offset)])
+
+
 @functools.lru_cache(maxsize=8)
 def _default_ids(n: int) -> list:
     """Ids of array-constructed datasets ("S0", "S1", ...; the synthetic generator's ids)."""
@@ -393,14 +396,21 @@ class Trainer:
         b, e = C.c_int64(), C.c_int64()
         self._chk(self.api.lib.esrnn_trainer_shard(h, C.byref(b), C.byref(e)))
         self.row_begin, self.row_end = b.value, e.value
-        na, nv = C.c_int32(), C.c_int64()
-        self._chk(self.api.lib.esrnn_trainer_param_count(h, C.byref(na), C.byref(nv)))
-        self.n_values = nv.value
-        self.param_layout = []
-        for i in range(na.value):
-            info = N.ParamInfo()
-            self._chk(self.api.lib.esrnn_trainer_param_info(h, i, C.byref(info)))
-            self.param_layout.append((info.name.decode(), info.rows, info.cols, info.offset))
+        # StackWeights layout (network.hpp:62-74) depends only on the profile: asked once per
+        # library and profile
+        key = (id(self.api), p_c.input_window, p_c.hidden_size, p_c.horizon,
+               tuple(p_c.block_len[:p_c.n_blocks]))
+        cached = _LAYOUTS.get(key)
+        if cached is None:
+            na, nv = C.c_int32(), C.c_int64()
+            self._chk(self.api.lib.esrnn_trainer_param_count(h, C.byref(na), C.byref(nv)))
+            layout = []
+            for i in range(na.value):
+                info = N.ParamInfo()
+                self._chk(self.api.lib.esrnn_trainer_param_info(h, i, C.byref(info)))
+                layout.append((info.name.decode(), info.rows, info.cols, info.offset))
+            cached = _LAYOUTS[key] = (nv.value, layout)
+        self.n_values, self.param_layout = cached[0], list(cached[1])
 
     # -- plumbing -------------------------------------------------------------------
     @property
