@@ -17,9 +17,10 @@
 //            inputs k = ks (mod 8); 8 row accumulators per gate; three xor-shuffle levels
 //            (16, 8, 4) fold the 8 k-slices and leave lane ks owning row r = ks, so the cell
 //            nonlinearities run right after the product, no extra phase;
-//   backward (outputs = input features) lane = (qs = lane>>3, c = lane&7): feature c, gate
-//            rows q = qs (mod 4); two shuffle levels (16, 8) leave rows 2qs, 2qs+1, and the
-//            lane immediately forms the gate adjoints of the layer below.
+//   backward (outputs = input features) lane = (qs = lane>>2, c = lane&3): feature c of the
+//            warp's 4, gate rows q = qs (mod 8); the same three shuffle levels leave lane qs
+//            owning row r = qs, and the lane immediately forms the gate adjoints of the layer
+//            below.
 //
 // W^T rows have stride ldk = 8 * odd (NetLayout), which makes both access patterns
 // bank-conflict free.  One barrier per layer forward and one per layer backward.
@@ -55,7 +56,7 @@ __host__ __device__ constexpr int ldr() {
 
 __host__ __device__ inline int tile_threads(const NetLayout& lay) {
     int w = (lay.H + 3) / 4;                                        // forward: 4 units per warp
-    const int wb = ((lay.in0 > lay.H ? lay.in0 : lay.H) + 7) / 8;  // backward: 8 features per warp
+    const int wb = ((lay.in0 > lay.H ? lay.in0 : lay.H) + 3) / 4;  // backward: 4 features per warp
     w = w > wb ? w : wb;
     w = w < 4 ? 4 : (w > 16 ? 16 : w);
     return 32 * w;
@@ -119,30 +120,10 @@ __device__ __forceinline__ void ld_rows(Real (&x)[kR], const Real* p) {
     x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
 }
 
-// Forward-type product for the lane's U output units (W^T rows wrow[u]): returns in out[u]
-// the full sum over k < K for row r = lane>>2.  All 32 lanes must call (shuffles).
+// Reduce-scatter of per-lane partial sums acc[u][row] (8 rows) over the warp's 8 slices (lane
+// bits 4, 3, 2): afterwards lane keeps in out[u] the full sum of row lane>>2.
 template <typename Real, int U>
-__device__ __forceinline__ void fwd_prod(Real (&out)[U], const Real* __restrict__ XT, const Real* const (&wrow)[U],
-                                         int K) {
-    constexpr int LD = ldr<Real>();
-    const int lane = threadIdx.x & 31, ks = lane >> 2;
-    Real acc[U][kR];
-#pragma unroll
-    for (int u = 0; u < U; ++u)
-#pragma unroll
-        for (int r = 0; r < kR; ++r) acc[u][r] = 0;
-#pragma unroll 2
-    for (int k = ks; k < K; k += 8) {
-        Real x[kR];
-        ld_rows(x, XT + k * LD);
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const Real w = wrow[u][k];
-#pragma unroll
-            for (int r = 0; r < kR; ++r) acc[u][r] += x[r] * w;
-        }
-    }
-    // reduce-scatter over the 8 k-slices (lane bits 4, 3, 2): lane keeps row ks
+__device__ __forceinline__ void reduce_scatter8(Real (&out)[U], Real (&acc)[U][kR], int lane) {
     const bool b2 = lane & 16, b1 = lane & 8, b0 = lane & 4;
     Real a4[U][4];
 #pragma unroll
@@ -170,39 +151,54 @@ __device__ __forceinline__ void fwd_prod(Real (&out)[U], const Real* __restrict_
     }
 }
 
-// Backward-type product: out[j] = sum_{q < Q} AT[q][r_j] * WT[q*ldk + k] for the lane's
-// rows r_j = 2*(lane>>3) + j.  All 32 lanes must call.
-template <typename Real>
-__device__ __forceinline__ void bwd_prod(Real (&out)[2], const Real* __restrict__ AT, const Real* __restrict__ WT, int ldk,
-                                         int Q, int k) {
+// Forward-type product for the lane's U output units (W^T rows wrow[u]): returns in out[u]
+// the full sum over k < K for row r = lane>>2.  All 32 lanes must call (shuffles).
+template <typename Real, int U>
+__device__ __forceinline__ void fwd_prod(Real (&out)[U], const Real* __restrict__ XT, const Real* const (&wrow)[U],
+                                         int K) {
     constexpr int LD = ldr<Real>();
-    const int lane = threadIdx.x & 31, qs = lane >> 3;
-    Real acc[kR];
+    const int lane = threadIdx.x & 31, ks = lane >> 2;
+    Real acc[U][kR];
 #pragma unroll
-    for (int r = 0; r < kR; ++r) acc[r] = 0;
-    const Real* wp = WT + k;
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int r = 0; r < kR; ++r) acc[u][r] = 0;
 #pragma unroll 2
-    for (int q = qs; q < Q; q += 4) {
+    for (int k = ks; k < K; k += 8) {
+        Real x[kR];
+        ld_rows(x, XT + k * LD);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const Real w = wrow[u][k];
+#pragma unroll
+            for (int r = 0; r < kR; ++r) acc[u][r] += x[r] * w;
+        }
+    }
+    reduce_scatter8<Real, U>(out, acc, lane);
+}
+
+// Backward-type product for one input feature k per lane quad (column wcol = WT + k):
+// returns the full sum over q < Q of AT[q][r] * WT[q*ldk + k] for row r = lane>>2.  Eight
+// q-slices per warp (lane bits 4, 3, 2) and the forward's reduce-scatter, so a warp covers 4
+// features and a layer's input adjoint spreads over all warps.  All 32 lanes must call.
+template <typename Real>
+__device__ __forceinline__ Real bwd_prod(const Real* __restrict__ AT, const Real* __restrict__ wcol, int ldk, int Q) {
+    constexpr int LD = ldr<Real>();
+    const int lane = threadIdx.x & 31, qs = lane >> 2;
+    Real acc[1][kR];
+#pragma unroll
+    for (int r = 0; r < kR; ++r) acc[0][r] = 0;
+#pragma unroll 2
+    for (int q = qs; q < Q; q += 8) {
         Real a[kR];
         ld_rows(a, AT + q * LD);
-        const Real w = wp[q * ldk];
+        const Real w = wcol[q * ldk];
 #pragma unroll
-        for (int r = 0; r < kR; ++r) acc[r] += a[r] * w;
+        for (int r = 0; r < kR; ++r) acc[0][r] += a[r] * w;
     }
-    const bool b1 = lane & 16, b0 = lane & 8;
-    Real a4[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-        const Real send = b1 ? acc[j] : acc[j + 4];
-        const Real keep = b1 ? acc[j + 4] : acc[j];
-        a4[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-    }
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-        const Real send = b0 ? a4[j] : a4[j + 2];
-        const Real keep = b0 ? a4[j + 2] : a4[j];
-        out[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-    }
+    Real out[1];
+    reduce_scatter8<Real, 1>(out, acc, lane);
+    return out[0];
 }
 
 // Vectorised global->shared copy of one contiguous segment (non-resident mode).
@@ -660,22 +656,18 @@ __global__ void __launch_bounds__((RESIDENT || sizeof(Real) == 8) ? 512 : 384, (
     DBG_CLK(st, 4);
 
     // ---- backward: input adjoints, each fused with the epilogue of the layer below ----
-    const int rb0 = 2 * (lane >> 3);  // the two rows a backward lane owns
+    // backward lanes: feature k0 + (lane & 3) of the warp's 4, row rf = lane >> 2
     // z_bar = pbar . out_w^T, then through tanh
-    for (int k0 = warp * 8; k0 < H; k0 += NW * 8) {
-        const int k = k0 + (lane & 7);
+    for (int k0 = warp * 4; k0 < H; k0 += NW * 4) {
+        const int k = k0 + (lane & 3);
         const int kc = k < H ? k : H - 1;
-        Real v[2];
-        bwd_prod<Real>(v, PBT, owT, ldkh, O, kc);
+        const Real v = bwd_prod<Real>(PBT, owT + kc, ldkh, O);
         if (k < H) {
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-                const int r = rb0 + j;
-                const Real zz = ZT[k * LD + r];
-                const Real zb = v[j] * (Real(1) - zz * zz);
-                ZBT[k * LD + r] = zb;
-                if (rs && r < nrows) rs[r * lay.rs_ld + lay.rs_zb + k] = zb;
-            }
+            const int r = rf;
+            const Real zz = ZT[k * LD + r];
+            const Real zb = v * (Real(1) - zz * zz);
+            ZBT[k * LD + r] = zb;
+            if (rs && r < nrows) rs[r * lay.rs_ld + lay.rs_zb + k] = zb;
         }
     }
     __syncthreads();
@@ -692,20 +684,16 @@ __global__ void __launch_bounds__((RESIDENT || sizeof(Real) == 8) ? 512 : 384, (
         const bool save_res = l >= 0 && lay.block_last[l] != 0;
         Real* PR = sm + ((l & 1) ? ts.prt1 : ts.prt0);
         const Real* gl = GT + 4 * (l >= 0 ? l : 0) * H * R;
-        for (int k0 = warp * 8; k0 < Kout; k0 += NW * 8) {
-            const int k = k0 + (lane & 7);
+        for (int k0 = warp * 4; k0 < Kout; k0 += NW * 4) {
+            const int k = k0 + (lane & 3);
             const int kc = k < Kout ? k : Kout - 1;
-            Real v[2];
-            bwd_prod<Real>(v, AT, WA, lda, QA, kc);
+            const Real v = bwd_prod<Real>(AT, WA + kc, lda, QA);
             if (k < Kout) {
-#pragma unroll
-                for (int j = 0; j < 2; ++j) {
-                    const int r = rb0 + j;
-                    if (l < 0) {
-                        UBT[k * LD + r] = v[j];  // x_bar: the ES contributions read it
-                        continue;
-                    }
-                    Real hb = v[j];
+                const int r = rf;
+                if (l < 0) {
+                    UBT[k * LD + r] = v;  // x_bar: the ES contributions read it
+                } else {
+                    Real hb = v;
                     if (add_res) hb = hb + RES[k * LD + r];
                     if (save_res) RES[k * LD + r] = hb;
                     const int e = k * R + r;
