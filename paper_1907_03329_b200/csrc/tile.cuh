@@ -377,6 +377,8 @@ __global__ void __launch_bounds__((RESIDENT || sizeof(Real) == 8) ? 512 : 384, (
     }
     const int* w_rowv = w_info[0];
     const int* w_ancv = w_info[1];
+    // the step's global mask count (epoch constant): loaded now, used by the pinball adjoint
+    const double step_m = MODE == kForecast ? 1.0 : pl.step_M[s];
 
     // ---- weights: TMA bulk copy of the compact parameter vector (resident mode), issued
     // once the previous step's Adam has completed (after pdl_wait) ----
@@ -627,7 +629,7 @@ __global__ void __launch_bounds__((RESIDENT || sizeof(Real) == 8) ? 512 : 384, (
     }
     // masked pinball (autodiff.hpp:384-392) and its adjoint (:620-626)
     double lsum = 0.0;
-    const Real gscale = static_cast<Real>(1.0 / pl.step_M[s]);
+    const Real gscale = static_cast<Real>(1.0 / step_m);
     const Real tau = static_cast<Real>(st.tau);
     for (int e = tid; e < O * R; e += NT) {
         const int o = e >> 3, r = e & 7;
