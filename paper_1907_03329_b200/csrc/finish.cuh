@@ -17,8 +17,8 @@ constexpr int kFinishThreads = 256;
 constexpr int kEsSlotsPerBlock = 32;  // ES blocks: warp 0 owns 32 slots; all warps stage the windows
 constexpr int kEsChunk = 128;         // contribution rows staged per round
 constexpr int kGq = 16, kGk = 8;      // K3 GEMM output block (gate rows x input features)
-constexpr int kGChunk = 128;          // row-store rows staged per round
-constexpr int kGBuf = 6;              // staging ring depth (kGBuf - 1 chunks in flight)
+constexpr int kGChunk = 256;          // row-store rows staged per round
+constexpr int kGBuf = 3;              // staging ring depth (kGBuf - 1 chunks in flight)
 
 // clip scale (trainer.hpp:603-615), global Adam step and bias corrections (:617-620),
 // step loss (masked mean, autodiff.hpp:392)
