@@ -1876,33 +1876,10 @@ esrnn_status esrnn_trainer_create(const esrnn_profile* profile, const esrnn_trai
         for (int b = 0; b < profile->n_blocks; ++b) e->L += profile->block_len[b];
         build_layout(e.get());
 
-        int ndev = 0;
-        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
-            raise(ESRNN_CUDA_ERROR, "no CUDA device visible: the B200 engine has no CPU fallback");
-        if (cfg->device < 0 || cfg->device >= ndev) raise(ESRNN_CUDA_ERROR, "device %d out of range", cfg->device);
-        CUDA_OK(cudaSetDevice(cfg->device));
-        CUDA_OK(cudaDeviceGetAttribute(&g_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, cfg->device));
-        CUDA_OK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, cfg->device));
-        CUDA_OK(cudaDeviceGetAttribute(&g_smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, cfg->device));
-        stream_get(e->stream, e->ev0, e->ev1);
-        c[nc++] = clk::now();
-        if (e->world > 1) {
-            // an id of 128 x 0xEE is the local-partials test mode: the shard runs its data
-            // path but skips the collective, so a test can sum per-rank partials itself
-            bool local_only = true;
-            for (int i = 0; i < 128; ++i) local_only = local_only && dist->nccl_unique_id[i] == 0xEE;
-            if (!local_only) {
-                ncclUniqueId id;
-                static_assert(sizeof(id.internal) == 128, "nccl id size");
-                std::memcpy(id.internal, dist->nccl_unique_id, 128);
-                NCCL_OK(ncclCommInitRank(&e->comm, e->world, id, e->rank));
-            }
-        }
-
         // network.hpp:89-116 init order on the trainer RNG (identical on every rank).  The
         // first epoch's shuffle is the RNG's next consumer, so one helper thread draws the
         // weights, then shuffles and plans epoch 1, while this thread sets up the device
-        // state; the weights are uploaded once the helper has drawn them.
+        // (and the NCCL communicator); the weights are uploaded once the helper has drawn them.
         e->rng = HostRng(cfg->seed);
         e->w_host.assign(e->P, 0.0);
         e->cur_plan = plan_pool_get();
@@ -1939,6 +1916,30 @@ esrnn_status esrnn_trainer_create(const esrnn_profile* profile, const esrnn_trai
             init_weights();
             weights_drawn.set_value();
         }
+
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+            raise(ESRNN_CUDA_ERROR, "no CUDA device visible: the B200 engine has no CPU fallback");
+        if (cfg->device < 0 || cfg->device >= ndev) raise(ESRNN_CUDA_ERROR, "device %d out of range", cfg->device);
+        CUDA_OK(cudaSetDevice(cfg->device));
+        CUDA_OK(cudaDeviceGetAttribute(&g_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, cfg->device));
+        CUDA_OK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, cfg->device));
+        CUDA_OK(cudaDeviceGetAttribute(&g_smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, cfg->device));
+        stream_get(e->stream, e->ev0, e->ev1);
+        c[nc++] = clk::now();
+        if (e->world > 1) {
+            // an id of 128 x 0xEE is the local-partials test mode: the shard runs its data
+            // path but skips the collective, so a test can sum per-rank partials itself
+            bool local_only = true;
+            for (int i = 0; i < 128; ++i) local_only = local_only && dist->nccl_unique_id[i] == 0xEE;
+            if (!local_only) {
+                ncclUniqueId id;
+                static_assert(sizeof(id.internal) == 128, "nccl id size");
+                std::memcpy(id.internal, dist->nccl_unique_id, 128);
+                NCCL_OK(ncclCommInitRank(&e->comm, e->world, id, e->rank));
+            }
+        }
+
         c[nc++] = clk::now();
         e->bc_tab = bc_table(e->cfg.device);
         if (e->fp64) {
