@@ -589,13 +589,39 @@ __global__ void __launch_bounds__((RESIDENT || sizeof(Real) == 8) ? 512 : 384, (
         }
     }
     __syncthreads();
+    // adapter output, fused with the masked pinball (autodiff.hpp:384-392) and its adjoint
+    // (:620-626): the lane owning (output oo, row rf) forms its loss term and pred_bar
+    double lsum = 0.0;
+    const Real gscale = static_cast<Real>(1.0 / step_m);
+    const Real tau = static_cast<Real>(st.tau);
     for (int o0 = warp * 4; o0 < O; o0 += NW * 4) {
         const int oo = o0 + (lane & 3);
         const int oc = oo < O ? oo : O - 1;
         const Real* wr[1] = {owT + oc * ldkh};
         Real v[1];
         fwd_prod<Real, 1>(v, ZT, wr, H);
-        if (oo < O) PT[oo * LD + rf] = v[0] + obias[oc];
+        if (oo < O) {
+            const Real p = v[0] + obias[oc];
+            PT[oo * LD + rf] = p;
+            if (MODE != kForecast) {
+                Real pb = 0;
+                if (msk[rf * ldo + oo] != Real(0)) {
+                    const Real t = tgt[rf * ldo + oo];
+                    const Real d = t - p;
+                    lsum += (d >= Real(0)) ? st.tau * static_cast<double>(d) : (st.tau - 1.0) * static_cast<double>(d);
+                    pb = gscale * ((t >= p) ? -tau : Real(1) - tau);
+                }
+                PBT[oo * LD + rf] = pb;
+                if (rs && rf < nrows) rs[rf * lay.rs_ld + lay.rs_pb + oo] = pb;
+            }
+        }
+    }
+    if (MODE != kForecast) {
+        // fixed-order block sum (warp shuffles, then warps in order); the barrier below also
+        // publishes PT and PBT
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) lsum += __shfl_down_sync(0xffffffffu, lsum, o);
+        if (lane == 0) red[warp] = lsum;
     }
     __syncthreads();
     DBG_CLK(st, 3);
@@ -627,28 +653,6 @@ __global__ void __launch_bounds__((RESIDENT || sizeof(Real) == 8) ? 512 : 384, (
         }
         return;
     }
-    // masked pinball (autodiff.hpp:384-392) and its adjoint (:620-626)
-    double lsum = 0.0;
-    const Real gscale = static_cast<Real>(1.0 / step_m);
-    const Real tau = static_cast<Real>(st.tau);
-    for (int e = tid; e < O * R; e += NT) {
-        const int o = e >> 3, r = e & 7;
-        Real pb = 0;
-        if (msk[r * ldo + o] != Real(0)) {
-            const Real p = PT[o * LD + r], t = tgt[r * ldo + o];
-            const Real d = t - p;
-            lsum += (d >= Real(0)) ? st.tau * static_cast<double>(d) : (st.tau - 1.0) * static_cast<double>(d);
-            pb = gscale * ((t >= p) ? -tau : Real(1) - tau);
-        }
-        PBT[o * LD + r] = pb;
-        if (rs && r < nrows) rs[r * lay.rs_ld + lay.rs_pb + o] = pb;
-    }
-    // block sum in block_sum's fixed order (warp shuffles, then warps in order), with the one
-    // barrier that also publishes PBT
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) lsum += __shfl_down_sync(0xffffffffu, lsum, o);
-    if (lane == 0) red[warp] = lsum;
-    __syncthreads();
     if (tid == 0) {
         double ltot = 0.0;
         for (int w = 0; w < NW; ++w) ltot += red[w];
