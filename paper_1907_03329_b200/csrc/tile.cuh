@@ -113,6 +113,27 @@ struct TileSmem {
     }
 };
 
+// acc[r] += x[r] * w over the 8 rows; fp32 pairs rows into Blackwell's paired FMA (FFMA2,
+// two independent round-to-nearest FMAs: bit-identical to the scalar form)
+template <typename Real>
+__device__ __forceinline__ void fma_rows(Real (&acc)[kR], const Real (&x)[kR], Real w) {
+    if constexpr (sizeof(Real) == 4) {
+#pragma unroll
+        for (int r = 0; r < kR; r += 2)
+            asm("{ .reg .b64 a, x, w;\n\t"
+                "mov.b64 a, {%0, %1};\n\t"
+                "mov.b64 x, {%2, %3};\n\t"
+                "mov.b64 w, {%4, %4};\n\t"
+                "fma.rn.f32x2 a, x, w, a;\n\t"
+                "mov.b64 {%0, %1}, a; }"
+                : "+f"(acc[r]), "+f"(acc[r + 1])
+                : "f"(x[r]), "f"(x[r + 1]), "f"(w));
+    } else {
+#pragma unroll
+        for (int r = 0; r < kR; ++r) acc[r] += x[r] * w;
+    }
+}
+
 template <typename Real>
 __device__ __forceinline__ void ld_rows(Real (&x)[kR], const Real* p) {
     const V4<Real> a = lds4(p), b = lds4(p + 4);
@@ -168,11 +189,7 @@ __device__ __forceinline__ void fwd_prod(Real (&out)[U], const Real* __restrict_
         Real x[kR];
         ld_rows(x, XT + k * LD);
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const Real w = wrow[u][k];
-#pragma unroll
-            for (int r = 0; r < kR; ++r) acc[u][r] += x[r] * w;
-        }
+        for (int u = 0; u < U; ++u) fma_rows<Real>(acc[u], x, wrow[u][k]);
     }
     reduce_scatter8<Real, U>(out, acc, lane);
 }
@@ -192,9 +209,7 @@ __device__ __forceinline__ Real bwd_prod(const Real* __restrict__ AT, const Real
     for (int q = qs; q < Q; q += 8) {
         Real a[kR];
         ld_rows(a, AT + q * LD);
-        const Real w = wcol[q * ldk];
-#pragma unroll
-        for (int r = 0; r < kR; ++r) acc[0][r] += a[r] * w;
+        fma_rows<Real>(acc[0], a, wcol[q * ldk]);
     }
     Real out[1];
     reduce_scatter8<Real, 1>(out, acc, lane);
