@@ -319,12 +319,33 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
                     const double2 u = *reinterpret_cast<const double2*>(Ub + b * kGk);
                     a0 = a.x, a1 = a.y, u0 = u.x, u1 = u.y;
                 }
-                acc[0][0] += a0 * u0;
-                acc[0][1] += a0 * u1;
-                acc[1][0] += a1 * u0;
-                acc[1][1] += a1 * u1;
-                bacc[0] += a0;
-                bacc[1] += a1;
+                if constexpr (sizeof(Real) == 4) {
+                    // paired FMAs / adds (FFMA2, FADD2): bit-identical to the scalar form
+                    asm("{ .reg .b64 p, q, u, a0, a1, b;\n\t"
+                        "mov.b64 u, {%6, %7};\n\t"
+                        "mov.b64 a0, {%8, %8};\n\t"
+                        "mov.b64 a1, {%9, %9};\n\t"
+                        "mov.b64 p, {%0, %1};\n\t"
+                        "mov.b64 q, {%2, %3};\n\t"
+                        "mov.b64 b, {%4, %5};\n\t"
+                        "fma.rn.f32x2 p, a0, u, p;\n\t"
+                        "fma.rn.f32x2 q, a1, u, q;\n\t"
+                        "mov.b64 u, {%8, %9};\n\t"
+                        "add.rn.f32x2 b, b, u;\n\t"
+                        "mov.b64 {%0, %1}, p;\n\t"
+                        "mov.b64 {%2, %3}, q;\n\t"
+                        "mov.b64 {%4, %5}, b; }"
+                        : "+f"(acc[0][0]), "+f"(acc[0][1]), "+f"(acc[1][0]), "+f"(acc[1][1]), "+f"(bacc[0]),
+                          "+f"(bacc[1])
+                        : "f"(u0), "f"(u1), "f"(a0), "f"(a1));
+                } else {
+                    acc[0][0] += a0 * u0;
+                    acc[0][1] += a0 * u1;
+                    acc[1][0] += a1 * u0;
+                    acc[1][1] += a1 * u1;
+                    bacc[0] += a0;
+                    bacc[1] += a1;
+                }
             }
             __syncthreads();  // buffer c % kGBuf is restaged next round
         }
