@@ -134,27 +134,30 @@ __device__ __forceinline__ void fma_rows(Real (&acc)[kR], const Real (&x)[kR], R
     }
 }
 
+// Offsets of the two 4-row halves a lane loads first / second: lanes with bit 4 set load the
+// halves swapped (reduce_scatter8's first level then needs no selects)
+__device__ __forceinline__ int row_half0(int lane) { return (lane & 16) ? 4 : 0; }
+
 template <typename Real>
-__device__ __forceinline__ void ld_rows(Real (&x)[kR], const Real* p) {
-    const V4<Real> a = lds4(p), b = lds4(p + 4);
+__device__ __forceinline__ void ld_rows(Real (&x)[kR], const Real* p0, const Real* p1) {
+    const V4<Real> a = lds4(p0), b = lds4(p1);
     x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
     x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
 }
 
-// Reduce-scatter of per-lane partial sums acc[u][row] (8 rows) over the warp's 8 slices (lane
-// bits 4, 3, 2): afterwards lane keeps in out[u] the full sum of row lane>>2.
+
+// Reduce-scatter of per-lane partial sums over the warp's 8 slices (lane bits 4, 3, 2):
+// afterwards lane keeps in out[u] the full sum of row lane>>2.  acc[u][j] holds row j, except
+// that lanes with bit 4 set hold row j ^ 4 (their row halves are loaded swapped, see
+// row_halves), so the first level exchanges acc[j + 4] for acc[j] without selects.
 template <typename Real, int U>
 __device__ __forceinline__ void reduce_scatter8(Real (&out)[U], Real (&acc)[U][kR], int lane) {
-    const bool b2 = lane & 16, b1 = lane & 8, b0 = lane & 4;
+    const bool b1 = lane & 8, b0 = lane & 4;
     Real a4[U][4];
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const Real send = b2 ? acc[u][j] : acc[u][j + 4];
-            const Real keep = b2 ? acc[u][j + 4] : acc[u][j];
-            a4[u][j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-        }
+        for (int j = 0; j < 4; ++j) a4[u][j] = acc[u][j] + __shfl_xor_sync(0xffffffffu, acc[u][j + 4], 16);
     Real a2[U][2];
 #pragma unroll
     for (int u = 0; u < U; ++u)
@@ -184,10 +187,12 @@ __device__ __forceinline__ void fwd_prod(Real (&out)[U], const Real* __restrict_
     for (int u = 0; u < U; ++u)
 #pragma unroll
         for (int r = 0; r < kR; ++r) acc[u][r] = 0;
+    const Real* X0 = XT + row_half0(lane);
+    const Real* X1 = XT + (4 - row_half0(lane));
 #pragma unroll 2
     for (int k = ks; k < K; k += 8) {
         Real x[kR];
-        ld_rows(x, XT + k * LD);
+        ld_rows(x, X0 + k * LD, X1 + k * LD);
 #pragma unroll
         for (int u = 0; u < U; ++u) fma_rows<Real>(acc[u], x, wrow[u][k]);
     }
@@ -205,10 +210,12 @@ __device__ __forceinline__ Real bwd_prod(const Real* __restrict__ AT, const Real
     Real acc[1][kR];
 #pragma unroll
     for (int r = 0; r < kR; ++r) acc[0][r] = 0;
+    const Real* A0 = AT + row_half0(lane);
+    const Real* A1 = AT + (4 - row_half0(lane));
 #pragma unroll 2
     for (int q = qs; q < Q; q += 8) {
         Real a[kR];
-        ld_rows(a, AT + q * LD);
+        ld_rows(a, A0 + q * LD, A1 + q * LD);
         fma_rows<Real>(acc[0], a, wcol[q * ldk]);
     }
     Real out[1];
