@@ -97,20 +97,37 @@ class ClockSampler:
     def __init__(self, path: Path):
         self.path, self.proc = path, None
 
+    def _lines(self) -> int:
+        try:
+            return self.path.read_text().count("\n")
+        except OSError:
+            return 0
+
     def __enter__(self):
+        # nvidia-smi takes ~100 ms to start: wait for its first sample so the (short) timed
+        # region is covered, then sample every 20 ms
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
                  "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except FileNotFoundError:
             self.proc = None
+            return self
+        t0 = time.time()
+        while self._lines() < 1 and time.time() - t0 < 5.0:
+            time.sleep(0.01)
+        self.start_lines = self._lines()
         return self
 
     def __exit__(self, *a):
         if self.proc:
+            # at least one sample taken after the timed region began
+            t0 = time.time()
+            while self._lines() <= self.start_lines and time.time() - t0 < 2.0:
+                time.sleep(0.01)
             self.proc.terminate()
             self.proc.wait()
 
