@@ -54,7 +54,7 @@ def _torch_nccl_dir() -> str | None:
 
 def build_engine(force: bool = False) -> Path:
     BUILD.mkdir(exist_ok=True)
-    deps = [*CSRC.glob("*.cu"), *CSRC.glob("*.cuh"), *CSRC.glob("*.cpp"), INC / "esrnn_b200.h"]
+    deps = [*CSRC.glob("*.cu"), *CSRC.glob("*.cuh"), *CSRC.glob("*.h"), *CSRC.glob("*.cpp"), INC / "esrnn_b200.h"]
     if not force and not _stale(LIB, deps):
         return LIB
     objs = []
