@@ -57,9 +57,10 @@ struct HostPlan {
 // in step-range chunks on the worker pool and packed (with offset fix-ups) into a pinned
 // buffer in upload order, so the epoch's plan goes to the device as a few async copies.
 struct EpochPlan {
-    std::mt19937_64 rng_before;  // trainer RNG before this epoch's shuffle (exact-resume state)
+    Mt64 rng_before;  // trainer RNG before this epoch's shuffle (exact-resume state)
     std::vector<uint64_t> wbuf;  // shuffle scratch: (row, anchor) pairs
-    std::vector<int> wr, wa;
+    std::vector<uint64_t> rnd;   // the shuffle's raw draws
+    int64_t n_windows = 0;
     std::vector<HostPlan> chunks;
     int steps = 0;
     bool ready = false;
@@ -139,6 +140,7 @@ struct esrnn_trainer {
     NetLayout lay{};
     std::vector<int64_t> live_flat;   // compact index -> flat index
     std::vector<double> w_host;       // flat StackWeights mirror (dead entries live only here)
+    std::vector<uint64_t> w_raw;      // creation: the weight init's raw draws
     std::vector<int> cat_host;
     HostRng rng{0};
     std::string err;
@@ -171,7 +173,7 @@ struct esrnn_trainer {
 
     DevPlan epoch_plan, batch_plan;
     EpochPlan cur_plan, next_plan;
-    std::thread plan_thread;  // builds the first epoch's plan while create finishes
+    std::future<void> plan_done;  // the first epoch's plan, built while create finishes
     bool have_last = false;  // cur_plan holds the global window order of the last train_epoch
     PinnedBuf<int> pin_i;
     PinnedBuf<double> pin_d;
@@ -237,7 +239,8 @@ struct esrnn_trainer {
     }
 
     void join_plan() {
-        if (plan_thread.joinable()) plan_thread.join();
+        if (plan_done.valid()) plan_done.wait();
+        plan_done = std::future<void>();
     }
 
     ~esrnn_trainer() {
@@ -614,8 +617,10 @@ const double* bc_table(int device) {
 
 // ------------------------------------------------------------------ plans
 // trainer.hpp:493-501: slots in first-appearance order; per slot its windows in batch order.
-void append_step(Eng* e, HostPlan& hp, const int* rows, const int* anchors, int B, std::vector<int64_t>& stamp,
-                 std::vector<int>& slot_id, int64_t step) {
+// src(i) -> {global row, anchor} of the batch's i-th window
+template <typename Src>
+void append_step(Eng* e, HostPlan& hp, const Src& src, int B, std::vector<int64_t>& stamp, std::vector<int>& slot_id,
+                 int64_t step) {
     const int wbase = static_cast<int>(hp.w_row.size());
     const int sbase = static_cast<int>(hp.slot_row.size());
     const int cbase = static_cast<int>(hp.slot_win.size());
@@ -635,7 +640,8 @@ void append_step(Eng* e, HostPlan& hp, const int* rows, const int* anchors, int 
     int* __restrict__ sid = slot_id.data();
     int nw = 0, ns = 0;
     for (int i = 0; i < B; ++i) {
-        const int r = rows[i] - row0;
+        const std::pair<int, int> ra = src(i);
+        const int r = ra.first - row0;
         if (r < 0 || r >= N) continue;
         const bool first = stp[r] != step;
         if (first) {
@@ -645,7 +651,7 @@ void append_step(Eng* e, HostPlan& hp, const int* rows, const int* anchors, int 
         }
         wfirst[nw] = first ? 1 : 0;
         wrow[nw] = r;
-        wanc[nw] = anchors[i];
+        wanc[nw] = ra.second;
         wslot[nw] = sid[r];
         ++nw;
     }
@@ -995,39 +1001,58 @@ void build_epoch_plan(Eng* e, EpochPlan& ep) {
     const int per = T - O - I + 1;
     const int64_t nw = static_cast<int64_t>(e->N_global) * per;
     ep.rng_before = e->rng.gen;
-    ep.wr.resize(nw);
-    ep.wa.resize(nw);
-    {
-        // shuffle (row, anchor) pairs together: one random access per swap
-        std::vector<uint64_t>& w = ep.wbuf;
-        w.resize(nw);
-        int64_t n = 0;
-        for (int r = 0; r < e->N_global; ++r)
-            for (int a = I - 1; a <= T - O - 1; ++a) w[n++] = (static_cast<uint64_t>(r) << 32) | static_cast<uint32_t>(a);
-        for (int64_t i = nw; i > 1; --i) {
-            const int64_t j = static_cast<int64_t>(e->rng.below(static_cast<uint64_t>(i)));
-            std::swap(w[i - 1], w[j]);
-        }
-        for (int64_t i = 0; i < nw; ++i) {
-            ep.wr[i] = static_cast<int>(w[i] >> 32);
-            ep.wa[i] = static_cast<int>(static_cast<uint32_t>(w[i]));
-        }
-    }
-    const auto p1 = clk::now();
     const int B = e->cfg.batch_size;
     const int steps = static_cast<int>((nw + B - 1) / B);
     ep.steps = steps;
-    // step-range chunks, planned in parallel (each with its own dedupe stamps)
-    const int nchunk = std::max(1, std::min(static_cast<int>(worker_pool().th.size()) + 1, steps / 6));
+    ep.n_windows = nw;
+    // (row, anchor) pairs shuffled together (one random access per swap); Rng::shuffle's
+    // draws (one per i = nw .. 2, Rng::below) generated as one block
+    std::vector<uint64_t>& w = ep.wbuf;
+    w.resize(nw);
+    std::vector<uint64_t>& rnd = ep.rnd;
+    rnd.resize(nw > 1 ? nw - 1 : 0);
+    e->rng.gen.fill(rnd.data(), rnd.size());
+    // Step-range chunks planned in parallel (each with its own dedupe stamps), pipelined
+    // with the shuffle: Fisher-Yates from the top finalises positions nw-1, nw-2, ... in
+    // turn, so task 0 shuffles and publishes `final_from` (positions >= it are final) while
+    // the other tasks plan chunks from the last one down as their windows become final.
+    const int workers = static_cast<int>(worker_pool().th.size()) + 1;
+    const int nchunk = std::max(1, std::min(steps, 64));
     ep.chunks.resize(nchunk);
     const int64_t id0 = g_stamp_id.fetch_add(steps);
     auto chunk_range = [&](int c, int& s0, int& s1) {
         s0 = static_cast<int>(static_cast<int64_t>(steps) * c / nchunk);
         s1 = static_cast<int>(static_cast<int64_t>(steps) * (c + 1) / nchunk);
     };
-    worker_pool().run(nchunk, [&](int c) {
+    std::atomic<int64_t> final_from{nw};
+    clk::time_point t_shuffled = p0;
+    worker_pool().run(nchunk + 1, [&](int task) {
+        if (task == 0) {
+            uint64_t* __restrict__ x = w.data();
+            int64_t n = 0;
+            for (int r = 0; r < e->N_global; ++r)
+                for (int a = I - 1; a <= T - O - 1; ++a) x[n++] = (static_cast<uint64_t>(r) << 32) | static_cast<uint32_t>(a);
+            constexpr int64_t kPublish = 2048;
+            for (int64_t i = nw; i > 1; --i) {
+                const int64_t j = static_cast<int64_t>((static_cast<unsigned __int128>(rnd[nw - i]) * static_cast<uint64_t>(i)) >> 64);
+                std::swap(x[i - 1], x[j]);
+                if ((i & (kPublish - 1)) == 0) final_from.store(i - 1, std::memory_order_release);
+            }
+            final_from.store(0, std::memory_order_release);
+            t_shuffled = clk::now();
+            return;
+        }
+        const int c = nchunk - task;  // last chunk first
         int s0, s1;
         chunk_range(c, s0, s1);
+        const int64_t need = static_cast<int64_t>(s0) * B;
+        while (final_from.load(std::memory_order_acquire) > need) {
+            if (workers > 2) {
+                for (int k = 0; k < 64; ++k) __builtin_ia32_pause();
+            } else {
+                std::this_thread::yield();
+            }
+        }
         HostPlan& hp = ep.chunks[c];
         const size_t wcap = static_cast<size_t>(std::min<int64_t>(nw, static_cast<int64_t>(s1 - s0) * B));
         plan_begin(hp, wcap, s1 - s0);
@@ -1037,13 +1062,21 @@ void build_epoch_plan(Eng* e, EpochPlan& ep) {
             stamp.assign(std::max(e->N, 1), -1);
             slot_id.assign(std::max(e->N, 1), 0);
         }
+        const uint64_t* x = w.data();
         for (int s = s0; s < s1; ++s) {
             const int64_t start = static_cast<int64_t>(s) * B;
             const int nb = static_cast<int>(std::min<int64_t>(nw, start + B) - start);
-            append_step(e, hp, ep.wr.data() + start, ep.wa.data() + start, nb, stamp, slot_id, id0 + s);
+            append_step(
+                e, hp,
+                [x, start](int i) {
+                    const uint64_t v = x[start + i];
+                    return std::pair<int, int>(static_cast<int>(v >> 32), static_cast<int>(static_cast<uint32_t>(v)));
+                },
+                nb, stamp, slot_id, id0 + s);
             hp.step_M.push_back(static_cast<double>(nb) * O);
         }
     });
+    const auto p1 = t_shuffled;
     const auto p2 = clk::now();
     // pack into the pinned upload buffer (device layout order), chunks in parallel
     std::vector<size_t> wb(nchunk + 1, 0), sb(nchunk + 1, 0);
@@ -1099,7 +1132,7 @@ void build_epoch_plan(Eng* e, EpochPlan& ep) {
     });
     ep.ready = true;
     if (dbg_host)
-        std::fprintf(stderr, "[esrnn host] plan: shuffle %.0f us, steps %.0f us (%d chunks), pack %.0f us\n",
+        std::fprintf(stderr, "[esrnn host] plan: draws+shuffle %.0f us, planning tail %.0f us (%d chunks), pack %.0f us\n",
                      std::chrono::duration<double, std::micro>(p1 - p0).count(),
                      std::chrono::duration<double, std::micro>(p2 - p1).count(), nchunk,
                      std::chrono::duration<double, std::micro>(clk::now() - p2).count());
@@ -1279,7 +1312,7 @@ void run_batch_impl(Eng* e, int32_t B, const int32_t* rows, const int32_t* ancho
     plan_begin(bp);
     std::vector<int64_t> stamp(std::max(e->N, 1), -1);
     std::vector<int> slot_id(std::max(e->N, 1), 0);
-    append_step(e, bp, rows, anchors, B, stamp, slot_id, 0);
+    append_step(e, bp, [&](int i) { return std::pair<int, int>(rows[i], anchors[i]); }, B, stamp, slot_id, 0);
     bp.step_M.push_back(count);
     const int Bl = static_cast<int>(bp.w_row.size());
     ensure_capacity(e, std::max(Bl, 1));
@@ -1611,38 +1644,28 @@ esrnn_status esrnn_trainer_create(const esrnn_profile* profile, const esrnn_trai
         e->in0 = I + ESRNN_NUM_CATEGORIES;
         e->L = 0;
         for (int b = 0; b < profile->n_blocks; ++b) e->L += profile->block_len[b];
-        build_layout(e.get());
-
         // network.hpp:89-116 init order on the trainer RNG (identical on every rank).  The
-        // first epoch's shuffle is the RNG's next consumer, so one helper thread draws the
-        // weights, then shuffles and plans epoch 1, while this thread sets up the device
-        // (and the NCCL communicator); the weights are uploaded once the helper has drawn them.
+        // first epoch's shuffle is the RNG's next consumer, so a helper thread draws the
+        // weights' raw numbers (one block), hands them to this thread for conversion, then
+        // shuffles and plans epoch 1 -- started first, so it overlaps the layout, device and
+        // NCCL setup below; the weights are uploaded once converted.
         e->rng = HostRng(cfg->seed);
-        e->w_host.assign(e->P, 0.0);
         e->cur_plan = plan_pool_get();
         e->next_plan = plan_pool_get();
         Eng* ep = e.get();
-        auto init_weights = [ep] {
-            const int H = ep->H;
-            const double bound = 1.0 / std::sqrt(static_cast<double>(H));
-            for (int l = 0; l < ep->L; ++l) {
-                for (int64_t i = 0; i < static_cast<int64_t>(ep->layer_in[l]) * 4 * H; ++i)
-                    ep->w_host[ep->off_win[l] + i] = ep->rng.uniform(-bound, bound);
-                for (int64_t i = 0; i < static_cast<int64_t>(H) * 4 * H; ++i)
-                    ep->w_host[ep->off_wrec[l] + i] = ep->rng.uniform(-bound, bound);
-                for (int c2 = H; c2 < 2 * H; ++c2) ep->w_host[ep->off_bias[l] + c2] = 1.0;
-            }
-            for (int64_t i = 0; i < static_cast<int64_t>(H) * H; ++i) ep->w_host[ep->off_nlw + i] = ep->rng.uniform(-bound, bound);
-            for (int64_t i = 0; i < static_cast<int64_t>(H) * ep->O; ++i)
-                ep->w_host[ep->off_outw + i] = ep->rng.uniform(-bound, bound);
-        };
-        std::promise<void> weights_drawn;
-        std::future<void> weights_ready = weights_drawn.get_future();
-        c[nc++] = clk::now();
+        // draw order: per layer W_in (in x 4H) then W_rec (H x 4H), then the head (H x H)
+        // and the adapter (H x O); biases are constants (forget chunk 1.0)
+        {
+            const int64_t H = e->H;
+            int64_t n_draw = (e->in0 + H) * 4 * H + static_cast<int64_t>(e->L - 1) * 2 * H * 4 * H + H * H + H * e->O;
+            e->w_raw.assign(n_draw, 0);
+        }
+        auto weights_drawn = std::make_shared<std::promise<void>>();
+        std::future<void> weights_ready = weights_drawn->get_future();
         if (std::max(0, T - e->O - e->I + 1) > 0) {
-            ep->plan_thread = std::thread([ep, init_weights, p = std::move(weights_drawn)]() mutable {
-                init_weights();
-                p.set_value();
+            ep->plan_done = async_runner().submit([ep, weights_drawn] {
+                ep->rng.gen.fill(ep->w_raw.data(), ep->w_raw.size());
+                weights_drawn->set_value();
                 try {
                     build_epoch_plan(ep, ep->next_plan);
                 } catch (...) {
@@ -1650,9 +1673,33 @@ esrnn_status esrnn_trainer_create(const esrnn_profile* profile, const esrnn_trai
                 }
             });
         } else {
-            init_weights();
-            weights_drawn.set_value();
+            ep->rng.gen.fill(ep->w_raw.data(), ep->w_raw.size());
+            weights_drawn->set_value();
         }
+        c[nc++] = clk::now();
+        build_layout(e.get());
+        e->w_host.assign(e->P, 0.0);
+        auto convert_weights = [ep] {
+            const int H = ep->H;
+            const double bound = 1.0 / std::sqrt(static_cast<double>(H));
+            const uint64_t* r = ep->w_raw.data();
+            // Rng::uniform(lo, hi) on each raw draw, in draw order
+            auto u = [&](int64_t off, int64_t n) {
+                double* w = ep->w_host.data() + off;
+                for (int64_t i = 0; i < n; ++i)
+                    w[i] = -bound + (bound - -bound) * (static_cast<double>(r[i] >> 11) * 0x1.0p-53);
+                r += n;
+            };
+            for (int l = 0; l < ep->L; ++l) {
+                u(ep->off_win[l], static_cast<int64_t>(ep->layer_in[l]) * 4 * H);
+                u(ep->off_wrec[l], static_cast<int64_t>(H) * 4 * H);
+                for (int c2 = H; c2 < 2 * H; ++c2) ep->w_host[ep->off_bias[l] + c2] = 1.0;
+            }
+            u(ep->off_nlw, static_cast<int64_t>(H) * H);
+            u(ep->off_outw, static_cast<int64_t>(H) * ep->O);
+            if (r != ep->w_raw.data() + ep->w_raw.size()) raise(ESRNN_ERROR, "weight init: draw count mismatch");
+            std::vector<uint64_t>().swap(ep->w_raw);
+        };
 
         int ndev = 0;
         if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
@@ -1687,6 +1734,7 @@ esrnn_status esrnn_trainer_create(const esrnn_profile* profile, const esrnn_trai
             upload_values<float>(e.get(), values, category);
         }
         weights_ready.wait();
+        convert_weights();
         c[nc++] = clk::now();
         upload_theta(e.get());
         ensure_capacity(e.get(), cfg->batch_size);
@@ -1696,7 +1744,7 @@ esrnn_status esrnn_trainer_create(const esrnn_profile* profile, const esrnn_trai
             std::fprintf(stderr, "[esrnn host] create:");
             for (int i = 1; i < nc; ++i)
                 std::fprintf(stderr, " %.0f", std::chrono::duration<double, std::micro>(c[i] - c[i - 1]).count());
-            std::fprintf(stderr, " us (setup+stream, plan thread start, alloc+values, weights wait, theta+capacity+sync)\n");
+            std::fprintf(stderr, " us (plan hand-off, layout+device+stream, nccl, alloc+values+weights, theta+capacity+sync)\n");
         }
     });
     if (st == ESRNN_OK) *out = e.release();
@@ -1843,7 +1891,7 @@ esrnn_status esrnn_trainer_get_train_state(esrnn_trainer* t, double* adam_m, dou
             // the trainer RNG before the next epoch's shuffle (the engine plans epochs ahead)
             t->join_plan();
             std::ostringstream os;
-            os << (t->next_plan.ready ? t->next_plan.rng_before : t->rng.gen);
+            os << (t->next_plan.ready ? t->next_plan.rng_before : t->rng.gen).to_std();
             const std::string txt = os.str();
             if (static_cast<int64_t>(txt.size()) + 1 > rng_cap) raise(ESRNN_SHAPE_ERROR, "train state: rng buffer too small (%zu)", txt.size() + 1);
             std::memcpy(rng_text, txt.c_str(), txt.size() + 1);
@@ -1896,7 +1944,7 @@ esrnn_status esrnn_trainer_set_train_state(esrnn_trainer* t, const double* adam_
             is >> g;
             if (is.fail()) raise(ESRNN_CHECKPOINT_ERROR, "train state: malformed rng state");
             t->join_plan();
-            t->rng.gen = g;
+            t->rng.gen = Mt64::from_std(g);
             t->next_plan.ready = false;  // re-planned from the restored RNG at the next epoch
         }
     });
@@ -1979,10 +2027,12 @@ esrnn_status esrnn_trainer_hw_state(esrnn_trainer* t, int64_t row, int64_t t_len
 }
 
 esrnn_status esrnn_trainer_last_epoch_windows(const esrnn_trainer* t, int32_t* rows, int32_t* anchors, int64_t n) {
-    const std::vector<int>& wr = t->cur_plan.wr;
-    if (!t->have_last || n != static_cast<int64_t>(wr.size())) return ESRNN_SHAPE_ERROR;
-    std::memcpy(rows, wr.data(), sizeof(int32_t) * n);
-    std::memcpy(anchors, t->cur_plan.wa.data(), sizeof(int32_t) * n);
+    if (!t->have_last || n != t->cur_plan.n_windows) return ESRNN_SHAPE_ERROR;
+    const uint64_t* w = t->cur_plan.wbuf.data();
+    for (int64_t i = 0; i < n; ++i) {
+        rows[i] = static_cast<int32_t>(w[i] >> 32);
+        anchors[i] = static_cast<int32_t>(static_cast<uint32_t>(w[i]));
+    }
     return ESRNN_OK;
 }
 

@@ -11,6 +11,8 @@
 #include <condition_variable>
 #include <cstdarg>
 #include <cstdio>
+#include <deque>
+#include <future>
 #include <functional>
 #include <list>
 #include <map>
@@ -23,6 +25,7 @@
 #include <vector>
 
 #include "esrnn_b200.h"
+#include "mt64.h"
 
 namespace esrnn_host {
 
@@ -58,7 +61,7 @@ inline thread_local std::string g_create_err;
 // ------------------------------------------------------------------ host RNG
 // matrix.hpp:173-213: std::mt19937_64 with explicit bit draws.
 struct HostRng {
-    std::mt19937_64 gen;
+    Mt64 gen;  // == std::mt19937_64, with bulk draws
     explicit HostRng(uint64_t seed) : gen(seed) {}
     double uniform() { return static_cast<double>(gen() >> 11) * 0x1.0p-53; }
     double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
@@ -245,6 +248,49 @@ inline WorkerPool& worker_pool() {
         std::max(1u, std::min(7u, std::thread::hardware_concurrency() > 1 ? std::thread::hardware_concurrency() - 1 : 1u))));
     return *p;
 }
+// Persistent helper threads for work handed off asynchronously (a trainer's first epoch
+// plan, built while its creation finishes): starting a std::thread costs ~25 us on the
+// creating thread, a hand-off here a few.
+struct AsyncRunner {
+    std::mutex mu;
+    std::condition_variable cv;
+    std::deque<std::function<void()>> q;
+    std::vector<std::thread> th;
+    explicit AsyncRunner(int n) {
+        for (int i = 0; i < n; ++i) th.emplace_back([this] { loop(); });
+    }
+    void loop() {
+        for (;;) {
+            std::function<void()> f;
+            {
+                std::unique_lock<std::mutex> lk(mu);
+                cv.wait(lk, [&] { return !q.empty(); });
+                f = std::move(q.front());
+                q.pop_front();
+            }
+            f();
+        }
+    }
+    // runs f on a helper; the future is ready when f has returned (f must not throw)
+    std::future<void> submit(std::function<void()> f) {
+        auto done = std::make_shared<std::promise<void>>();
+        std::future<void> fut = done->get_future();
+        {
+            std::lock_guard<std::mutex> g(mu);
+            q.emplace_back([f = std::move(f), done] {
+                f();
+                done->set_value();
+            });
+        }
+        cv.notify_one();
+        return fut;
+    }
+};
+inline AsyncRunner& async_runner() {
+    static AsyncRunner* r = new AsyncRunner(2);  // never destroyed (threads park in cv.wait)
+    return *r;
+}
+
 // stamp ids for slot dedupe: unique per planned step across the process (no re-init of
 // the per-row stamp arrays between steps / epochs)
 inline std::atomic<int64_t> g_stamp_id{1};

@@ -9,7 +9,7 @@ from paper_1907_03329_b200.trainer import Frequency, FrequencyProfile, TrainConf
 api = N.product_api()
 prof = FrequencyProfile.defaults(Frequency.Quarterly)
 vals, cats = api.make_synthetic(41, 1000, 88, 4, 0.05)
-cfg = TrainConfig(seed=7, batch_size=1000, precision="fp32")
+cfg = TrainConfig(seed=7, batch_size=1000, precision="fp32", max_batch_size=2048)
 
 
 def step():
