@@ -140,7 +140,8 @@ struct esrnn_trainer {
     NetLayout lay{};
     std::vector<int64_t> live_flat;   // compact index -> flat index
     std::vector<double> w_host;       // flat StackWeights mirror (dead entries live only here)
-    std::vector<uint64_t> w_raw;      // creation: the weight init's raw draws
+    PinnedBuf<uint64_t> w_raw;        // creation: the weight init's raw draws (pooled block)
+    size_t w_draws = 0;
     std::vector<int> cat_host;
     HostRng rng{0};
     std::string err;
@@ -175,6 +176,9 @@ struct esrnn_trainer {
     EpochPlan cur_plan, next_plan;
     std::future<void> plan_done;  // the first epoch's plan, built while create finishes
     bool have_last = false;  // cur_plan holds the global window order of the last train_epoch
+    DBuf<double> stage_raw;            // creation: the series block as uploaded (fp64)
+    PinnedBuf<double> stage_pin;       // creation: its pinned staging copy
+    PinnedBuf<signed char> stage_cat;  // creation: pinned category bytes
     PinnedBuf<int> pin_i;
     PinnedBuf<double> pin_d;
 
@@ -969,24 +973,27 @@ template <typename Real>
 void upload_values(Eng* e, const double* values, const int32_t* category) {
     const int N = e->N, LEN = e->LEN;
     if (N > 0) {
-        DBuf<double> raw;
+        // caller's (pageable) block -> pinned staging -> one async H2D; the staging buffers
+        // live until create's final synchronisation
+        DBuf<double>& raw = e->stage_raw;
         raw.alloc(static_cast<size_t>(N) * LEN);
-        CUDA_OK(cudaMemcpyAsync(raw.p, values + static_cast<size_t>(e->row0) * LEN, sizeof(double) * raw.n,
-                                cudaMemcpyHostToDevice, e->stream));
+        e->stage_pin.reserve(raw.n);
+        std::memcpy(e->stage_pin.p, values + static_cast<size_t>(e->row0) * LEN, sizeof(double) * raw.n);
+        CUDA_OK(cudaMemcpyAsync(raw.p, e->stage_pin.p, sizeof(double) * raw.n, cudaMemcpyHostToDevice, e->stream));
         const long long n = static_cast<long long>(N) * e->ldv;
         k_layout_values<Real><<<static_cast<int>((n + 255) / 256), 256, 0, e->stream>>>(
             raw.p, N, LEN, e->ldv, reinterpret_cast<Real*>(e->vals.p), reinterpret_cast<Real*>(e->vrm.p));
         e->launches += 1;
         CUDA_OK(cudaGetLastError());
-        std::vector<signed char> c(N, 5);
+        e->stage_cat.reserve(N);  // pinned: a pageable copy may synchronise the stream
+        signed char* c = e->stage_cat.p;
         e->cat_host.assign(N, 5);
         for (int r = 0; r < N; ++r) {
             const int v = category ? category[e->row0 + r] : -1;
             c[r] = static_cast<signed char>(v >= 0 && v < 6 ? v : 5);
             e->cat_host[r] = c[r];
         }
-        CUDA_OK(cudaMemcpyAsync(e->cat.p, c.data(), c.size(), cudaMemcpyHostToDevice, e->stream));
-        CUDA_OK(cudaStreamSynchronize(e->stream));  // raw goes back to the block cache
+        CUDA_OK(cudaMemcpyAsync(e->cat.p, c, N, cudaMemcpyHostToDevice, e->stream));
     }
 }
 
@@ -1649,6 +1656,11 @@ esrnn_status esrnn_trainer_create(const esrnn_profile* profile, const esrnn_trai
         // weights' raw numbers (one block), hands them to this thread for conversion, then
         // shuffles and plans epoch 1 -- started first, so it overlaps the layout, device and
         // NCCL setup below; the weights are uploaded once converted.
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+            raise(ESRNN_CUDA_ERROR, "no CUDA device visible: the B200 engine has no CPU fallback");
+        if (cfg->device < 0 || cfg->device >= ndev) raise(ESRNN_CUDA_ERROR, "device %d out of range", cfg->device);
+        CUDA_OK(cudaSetDevice(cfg->device));  // pinned blocks below come from this device's context
         e->rng = HostRng(cfg->seed);
         e->cur_plan = plan_pool_get();
         e->next_plan = plan_pool_get();
@@ -1658,13 +1670,15 @@ esrnn_status esrnn_trainer_create(const esrnn_profile* profile, const esrnn_trai
         {
             const int64_t H = e->H;
             int64_t n_draw = (e->in0 + H) * 4 * H + static_cast<int64_t>(e->L - 1) * 2 * H * 4 * H + H * H + H * e->O;
-            e->w_raw.assign(n_draw, 0);
+            e->w_draws = static_cast<size_t>(n_draw);
+            e->w_raw.reserve(e->w_draws);
         }
         auto weights_drawn = std::make_shared<std::promise<void>>();
         std::future<void> weights_ready = weights_drawn->get_future();
         if (std::max(0, T - e->O - e->I + 1) > 0) {
             ep->plan_done = async_runner().submit([ep, weights_drawn] {
-                ep->rng.gen.fill(ep->w_raw.data(), ep->w_raw.size());
+                cudaSetDevice(ep->cfg.device);  // the plan's pinned upload block
+                ep->rng.gen.fill(ep->w_raw.p, ep->w_draws);
                 weights_drawn->set_value();
                 try {
                     build_epoch_plan(ep, ep->next_plan);
@@ -1673,7 +1687,7 @@ esrnn_status esrnn_trainer_create(const esrnn_profile* profile, const esrnn_trai
                 }
             });
         } else {
-            ep->rng.gen.fill(ep->w_raw.data(), ep->w_raw.size());
+            ep->rng.gen.fill(ep->w_raw.p, ep->w_draws);
             weights_drawn->set_value();
         }
         c[nc++] = clk::now();
@@ -1682,7 +1696,7 @@ esrnn_status esrnn_trainer_create(const esrnn_profile* profile, const esrnn_trai
         auto convert_weights = [ep] {
             const int H = ep->H;
             const double bound = 1.0 / std::sqrt(static_cast<double>(H));
-            const uint64_t* r = ep->w_raw.data();
+            const uint64_t* r = ep->w_raw.p;
             // Rng::uniform(lo, hi) on each raw draw, in draw order
             auto u = [&](int64_t off, int64_t n) {
                 double* w = ep->w_host.data() + off;
@@ -1697,15 +1711,10 @@ esrnn_status esrnn_trainer_create(const esrnn_profile* profile, const esrnn_trai
             }
             u(ep->off_nlw, static_cast<int64_t>(H) * H);
             u(ep->off_outw, static_cast<int64_t>(H) * ep->O);
-            if (r != ep->w_raw.data() + ep->w_raw.size()) raise(ESRNN_ERROR, "weight init: draw count mismatch");
-            std::vector<uint64_t>().swap(ep->w_raw);
+            if (r != ep->w_raw.p + ep->w_draws) raise(ESRNN_ERROR, "weight init: draw count mismatch");
+            ep->w_raw.release();
         };
 
-        int ndev = 0;
-        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
-            raise(ESRNN_CUDA_ERROR, "no CUDA device visible: the B200 engine has no CPU fallback");
-        if (cfg->device < 0 || cfg->device >= ndev) raise(ESRNN_CUDA_ERROR, "device %d out of range", cfg->device);
-        CUDA_OK(cudaSetDevice(cfg->device));
         CUDA_OK(cudaDeviceGetAttribute(&g_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, cfg->device));
         CUDA_OK(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, cfg->device));
         CUDA_OK(cudaDeviceGetAttribute(&g_smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, cfg->device));
@@ -1739,6 +1748,9 @@ esrnn_status esrnn_trainer_create(const esrnn_profile* profile, const esrnn_trai
         upload_theta(e.get());
         ensure_capacity(e.get(), cfg->batch_size);
         CUDA_OK(cudaStreamSynchronize(e->stream));
+        e->stage_raw.free();
+        e->stage_pin.release();
+        e->stage_cat.release();
         c[nc++] = clk::now();
         if (dbg_host) {
             std::fprintf(stderr, "[esrnn host] create:");
