@@ -1055,7 +1055,9 @@ void build_epoch_plan(Eng* e, EpochPlan& ep) {
         const int64_t need = static_cast<int64_t>(s0) * B;
         while (final_from.load(std::memory_order_acquire) > need) {
             if (workers > 2) {
+#if defined(__x86_64__)
                 for (int k = 0; k < 64; ++k) __builtin_ia32_pause();
+#endif
             } else {
                 std::this_thread::yield();
             }

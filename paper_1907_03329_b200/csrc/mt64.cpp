@@ -40,15 +40,20 @@ __attribute__((always_inline)) inline void fill_body(Mt64& g, uint64_t* out, siz
     }
 }
 
-__attribute__((target("avx2"))) void twist_avx2(uint64_t* x) { twist_body(x); }
 void twist_generic(uint64_t* x) { twist_body(x); }
-__attribute__((target("avx2"))) void fill_avx2(Mt64& g, uint64_t* out, size_t n) { fill_body(g, out, n); }
 void fill_generic(Mt64& g, uint64_t* out, size_t n) { fill_body(g, out, n); }
-
+#if defined(__x86_64__) && !defined(ESRNN_MT64_GENERIC)
+__attribute__((target("avx2"))) void twist_avx2(uint64_t* x) { twist_body(x); }
+__attribute__((target("avx2"))) void fill_avx2(Mt64& g, uint64_t* out, size_t n) { fill_body(g, out, n); }
 bool have_avx2() {
     static const bool v = __builtin_cpu_supports("avx2");
     return v;
 }
+#else  // e.g. aarch64 hosts: the generic clone (auto-vectorised for the base ISA)
+void twist_avx2(uint64_t* x) { twist_body(x); }
+void fill_avx2(Mt64& g, uint64_t* out, size_t n) { fill_body(g, out, n); }
+bool have_avx2() { return false; }
+#endif
 
 }  // namespace
 

@@ -7,9 +7,14 @@ ROOT = Path(__file__).resolve().parent.parent
 CSRC = ROOT / "paper_1907_03329_b200" / "csrc"
 
 
-def test_mt64_matches_std(tmp_path):
+import pytest
+
+
+@pytest.mark.parametrize("variant", ["dispatch", "generic"])
+def test_mt64_matches_std(tmp_path, variant):
     exe = tmp_path / "mt64_test"
-    subprocess.run(["g++", "-std=c++17", "-O3", "-I" + str(CSRC), str(ROOT / "tests" / "cpp" / "mt64_test.cpp"),
+    extra = ["-DESRNN_MT64_GENERIC"] if variant == "generic" else []
+    subprocess.run(["g++", "-std=c++17", "-O3", *extra, "-I" + str(CSRC), str(ROOT / "tests" / "cpp" / "mt64_test.cpp"),
                     str(CSRC / "mt64.cpp"), "-o", str(exe)], check=True)
     r = subprocess.run([str(exe)], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
