@@ -913,6 +913,29 @@ void launch_step(Eng* e, const PlanDev& pv, int s, bool grads, bool update, Stat
     }
 }
 
+// Creation-time zeroing of the state buffers in one launch (instead of a cudaMemsetAsync
+// each) plus the error word reset.  blockIdx.y = span; spans start 4096-aligned (block cache).
+struct ZeroSpans {
+    static constexpr int kMax = 12;
+    unsigned char* p[kMax];
+    unsigned long long n[kMax];
+    int count;
+    int* errw;
+};
+__global__ void k_zero_spans(ZeroSpans z) {
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+        z.errw[0] = 0;
+        z.errw[1] = INT_MAX;
+    }
+    const int k = blockIdx.y;
+    if (k >= z.count) return;
+    unsigned char* p = z.p[k];
+    const unsigned long long n = z.n[k], n16 = n / 16;
+    for (unsigned long long i = blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += gridDim.x * blockDim.x)
+        reinterpret_cast<uint4*>(p)[i] = make_uint4(0, 0, 0, 0);
+    if (blockIdx.x == 0 && threadIdx.x < n - n16 * 16) p[n16 * 16 + threadIdx.x] = 0;
+}
+
 template <typename Real>
 void alloc_state(Eng* e) {
     const int N = e->N, S = e->S, LEN = e->LEN;
@@ -928,8 +951,7 @@ void alloc_state(Eng* e) {
     e->theta.alloc(r * e->lay.P_pad);
     e->mW.alloc(r * e->lay.P_pad);
     e->vW.alloc(r * e->lay.P_pad);
-    e->gbuf.alloc(r * (e->lay.P_pad + 2));
-    e->gbuf.zero(e->stream);  // padding slots of the compact vector are never written
+    e->gbuf.alloc(r * (e->lay.P_pad + 2));  // zeroed below: padding slots of the compact vector are never written
     e->red_blocks = e->lay.mat_blk0[e->lay.nmat];
     e->red_sq_part.alloc(std::max<int>(e->red_blocks, static_cast<int>((e->lay.P_pad + 255) / 256)));
     e->scal.alloc(4);
@@ -947,12 +969,20 @@ void alloc_state(Eng* e) {
         e->dbg_clk.alloc(128);
         e->dbg_clk.zero(e->stream);
     }
-    for (auto* b : {&e->ps, &e->ps_m, &e->ps_v, &e->mW, &e->vW}) b->zero(e->stream);
-    e->ps_steps.zero(e->stream);
-    e->done_ctr.zero(e->stream);
-    e->net_step.zero(e->stream);
-    const int reset[2] = {0, INT_MAX};
-    CUDA_OK(cudaMemcpyAsync(e->errw.p, reset, sizeof reset, cudaMemcpyHostToDevice, e->stream));
+    ZeroSpans z{};
+    auto add = [&](void* p, size_t bytes) {
+        z.p[z.count] = static_cast<unsigned char*>(p);
+        z.n[z.count++] = bytes;
+    };
+    add(e->gbuf.p, e->gbuf.n);
+    for (auto* b : {&e->ps, &e->ps_m, &e->ps_v, &e->mW, &e->vW}) add(b->p, b->n);
+    add(e->ps_steps.p, sizeof(int) * e->ps_steps.n);
+    add(e->done_ctr.p, sizeof(unsigned int) * e->done_ctr.n);
+    add(e->net_step.p, sizeof(long long) * e->net_step.n);
+    z.errw = e->errw.p;
+    k_zero_spans<<<dim3(32, z.count), 256, 0, e->stream>>>(z);
+    e->launches += 1;
+    CUDA_OK(cudaGetLastError());
     setup_kernel_attrs<Real>(e);
 }
 
@@ -974,7 +1004,8 @@ void upload_values(Eng* e, const double* values, const int32_t* category) {
     const int N = e->N, LEN = e->LEN;
     if (N > 0) {
         // caller's (pageable) block -> pinned staging -> one async H2D; the staging buffers
-        // live until create's final synchronisation
+        // live until create's final synchronisation (a helper-thread copy measured slower:
+        // waking it costs more than the copy)
         DBuf<double>& raw = e->stage_raw;
         raw.alloc(static_cast<size_t>(N) * LEN);
         e->stage_pin.reserve(raw.n);
