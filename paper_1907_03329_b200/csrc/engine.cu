@@ -792,7 +792,10 @@ void setup_kernel_attrs(Eng* e) {
         default: set_sc_attrs<Real, 0>(e->lay); break;
     }
     const size_t fsm = sizeof(Real) * static_cast<size_t>(e->LEN + e->S + e->I) * kScanThreads;
-    CUDA_OK(cudaFuncSetAttribute(k_forecast_scan<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
+    CUDA_OK(cudaFuncSetAttribute(k_forecast_scan<Real, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
+    CUDA_OK(cudaFuncSetAttribute(k_forecast_scan<Real, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
+    CUDA_OK(cudaFuncSetAttribute(k_forecast_scan<Real, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
+    CUDA_OK(cudaFuncSetAttribute(k_forecast_scan<Real, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
     if (stack_smem<Real>(e->lay, false) > static_cast<size_t>(g_smem_optin) ||
         finish_smem<Real>(e->lay) > static_cast<size_t>(g_smem_optin) || fsm > static_cast<size_t>(g_smem_optin))
         raise(ESRNN_CONFIG_ERROR, "profile too large for the B200 kernels' shared-memory tiles");
@@ -1437,6 +1440,24 @@ void run_batch_impl(Eng* e, int32_t B, const int32_t* rows, const int32_t* ancho
 // ------------------------------------------------------------------ forecast
 // Host outputs of one forecast pass (all nullable).  mode 0: forecast_at; 1: validate (sMAPE);
 // 2: evaluate (sMAPE + MASE + seasonal-naive scores, commands.hpp:285-338).
+// K6 scan with the season length as a template constant for the M4 profiles' S
+template <typename Real>
+void launch_forecast_scan(Eng* e, int t_len, Real* X, Real* FL, Real* FS, Real* dump_lv, Real* dump_se, int dump_row,
+                          double* score) {
+    const int sb = (e->N + kScanThreads - 1) / kScanThreads;
+    const size_t smem = sizeof(Real) * static_cast<size_t>(t_len + e->S + e->I) * kScanThreads;
+    const StateDev<Real> st = e->state<Real>();
+    auto go = [&](auto kernel) {
+        kernel<<<sb, kScanThreads, smem, e->stream>>>(st, e->lay, t_len, X, FL, FS, dump_lv, dump_se, dump_row, score);
+    };
+    switch (e->S) {
+        case 1: go(k_forecast_scan<Real, 1>); break;
+        case 4: go(k_forecast_scan<Real, 4>); break;
+        case 12: go(k_forecast_scan<Real, 12>); break;
+        default: go(k_forecast_scan<Real, 0>); break;
+    }
+}
+
 struct ScoreOut {
     double* smape = nullptr;        // [n_local]
     double* mase = nullptr;         // [n_local], NaN = undefined (std::nullopt)
@@ -1465,12 +1486,11 @@ void forecast_impl(Eng* e, int64_t drop_tail, double* out, int mode, const Score
     const NetLayout& lay = e->lay;
     CUDA_OK(cudaEventRecord(e->ev0, e->stream));
     if (N > 0) {
-        const int sb = (N + kScanThreads - 1) / kScanThreads;
         {
             Eng::KScope k(e, 6);
-            k_forecast_scan<Real><<<sb, kScanThreads, sizeof(Real) * (t_ins + S + I) * kScanThreads, e->stream>>>(
-                st, lay, t_ins, reinterpret_cast<Real*>(e->fX.p), reinterpret_cast<Real*>(e->fL.p),
-                reinterpret_cast<Real*>(e->fS.p), nullptr, nullptr, -1, mode == 2 ? e->f_score.p : nullptr);
+            launch_forecast_scan<Real>(e, t_ins, reinterpret_cast<Real*>(e->fX.p), reinterpret_cast<Real*>(e->fL.p),
+                                       reinterpret_cast<Real*>(e->fS.p), nullptr, nullptr, -1,
+                                       mode == 2 ? e->f_score.p : nullptr);
         }
         ForecastArgs fa{};
         fa.t_ins = t_ins;
@@ -1620,11 +1640,10 @@ void hw_state_impl(Eng* e, int64_t row, int64_t t_len, double* levels, double* s
         e->dump_se.alloc(r * (e->LEN + S));
     }
     StateDev<Real> st = e->state<Real>();
-    const int sb = (e->N + kScanThreads - 1) / kScanThreads;
     // the dump row's thread writes its full state; X == nullptr skips the window build
-    k_forecast_scan<Real><<<sb, kScanThreads, sizeof(Real) * (t_len + S + e->I) * kScanThreads, e->stream>>>(
-        st, e->lay, static_cast<int>(t_len), nullptr, nullptr, nullptr, reinterpret_cast<Real*>(e->dump_lv.p),
-        reinterpret_cast<Real*>(e->dump_se.p), lr, nullptr);
+    launch_forecast_scan<Real>(e, static_cast<int>(t_len), nullptr, nullptr, nullptr,
+                               reinterpret_cast<Real*>(e->dump_lv.p), reinterpret_cast<Real*>(e->dump_se.p),
+                               static_cast<int>(lr), nullptr);
     e->launches += 1;
     CUDA_OK(cudaGetLastError());
     CUDA_OK(cudaStreamSynchronize(e->stream));

@@ -27,13 +27,17 @@ __device__ __forceinline__ void stage_column(Real* ys, const Real* __restrict__ 
 
 // ------------------------------------------------------------------------------ K6
 // smem: ys [t_ins][bd] | ring [S][bd] | win [I][bd]
-template <typename Real>
+// SC > 0: the season length as a compile-time constant (1, 4, 12): the S live
+// seasonalities sit in registers and the recurrence is unrolled by S, so each step is its
+// FMA chain with the error checks folded into a select (flagged after the loop, at the
+// first failing t, as the reference throws there); SC = 0: any S, ring in shared memory.
+template <typename Real, int SC = 0>
 __global__ void __launch_bounds__(kScanThreads) k_forecast_scan(StateDev<Real> st, NetLayout lay, int t_ins, Real* X,
                                                                 Real* FL, Real* FS, Real* dump_lv, Real* dump_se,
                                                                 int dump_row, double* score) {
     using M = Math<Real>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int S = lay.S, I = lay.I, O = lay.O, in0 = lay.in0, N = st.N;
+    const int S = SC > 0 ? SC : lay.S, I = lay.I, O = lay.O, in0 = lay.in0, N = st.N;
     const int row = blockIdx.x * blockDim.x + threadIdx.x;
     if (row >= N) return;
     const int bd = blockDim.x, tid = threadIdx.x;
@@ -43,11 +47,15 @@ __global__ void __launch_bounds__(kScanThreads) k_forecast_scan(StateDev<Real> s
     for (int j = 0; j < S; ++j) cp_async_elem(ring + j * bd, st.ps + (size_t)(2 + j) * N + row);
     const Real a_raw = st.ps[row], g_raw = st.ps[N + row];
     stage_column(ys, st.vals + row, t_ins, N, bd);
-    for (int t = 0; t < t_ins; ++t)
-        if (!(ys[t * bd] > Real(0))) {
-            flag_error(st.err, kErrObs, t);
+    {
+        int bad = INT_MAX;  // first non-positive observation (a select per t, no exit branch)
+#pragma unroll 8
+        for (int t = t_ins - 1; t >= 0; --t) bad = (ys[t * bd] > Real(0)) ? bad : t;
+        if (bad != INT_MAX) {
+            flag_error(st.err, kErrObs, bad);
             return;
         }
+    }
     if (score != nullptr) {
         // mase(): in-sample seasonal-naive MAE over y[0:t_ins) (metrics.hpp:40-44); the
         // seasonal-naive forecast y[t_ins-S+(o mod S)] (metrics.hpp:52-59) scored with
@@ -83,25 +91,60 @@ __global__ void __launch_bounds__(kScanThreads) k_forecast_scan(StateDev<Real> s
     // seasonality index u is produced at step u-S; the window needs u in [t_ins-I, t_ins)
     for (int u = t_ins - I; u < S && u < t_ins; ++u)
         if (u >= 0) win[(u - (t_ins - I)) * bd] = ring[u * bd];
-    int j = 0;
-    for (int t = 0; t < t_ins; ++t) {
-        const Real yt = ys[t * bd];
-        const Real s_t = ring[j * bd];
-        const Real l = alpha * fdiv(yt, s_t) + oma * lp;
-        if (!(l > Real(0)) || !isfinite(l)) {
-            flag_error(st.err, kErrFcLevel, t);
+    if constexpr (SC > 0) {
+        Real rg[SC];
+#pragma unroll
+        for (int q = 0; q < SC; ++q) rg[q] = ring[q * bd];
+        int bad = INT_MAX;
+        for (int t0 = 0; t0 < t_ins; t0 += SC) {
+#pragma unroll
+            for (int q = 0; q < SC; ++q) {
+                const int t = t0 + q;
+                if (t < t_ins) {  // warp-uniform
+                    const Real yt = ys[t * bd];
+                    const Real s_t = rg[q];
+                    const Real l = alpha * fdiv(yt, s_t) + oma * lp;
+                    bad = (bad == INT_MAX && !(l > Real(0) && isfinite(l))) ? t : bad;
+                    const Real sn = gamma * fdiv(yt, lp) + omg * s_t;
+                    rg[q] = sn;
+                    const int uu = t + S;
+                    if (uu >= t_ins - I && uu < t_ins) win[(uu - (t_ins - I)) * bd] = sn;
+                    if (dump) {
+                        dump_lv[t] = l;
+                        dump_se[uu] = sn;
+                    }
+                    lp = l;
+                }
+            }
+        }
+        if (bad != INT_MAX) {
+            flag_error(st.err, kErrFcLevel, bad);
             return;
         }
-        const Real sn = gamma * fdiv(yt, lp) + omg * s_t;
-        ring[j * bd] = sn;
-        const int uu = t + S;
-        if (uu >= t_ins - I && uu < t_ins) win[(uu - (t_ins - I)) * bd] = sn;
-        if (dump) {
-            dump_lv[t] = l;
-            dump_se[uu] = sn;
+        // slot q holds the seasonality of the index u = q (mod S) in [t_ins, t_ins + S)
+#pragma unroll
+        for (int q = 0; q < SC; ++q) ring[q * bd] = rg[q];
+    } else {
+        int j = 0;
+        for (int t = 0; t < t_ins; ++t) {
+            const Real yt = ys[t * bd];
+            const Real s_t = ring[j * bd];
+            const Real l = alpha * fdiv(yt, s_t) + oma * lp;
+            if (!(l > Real(0)) || !isfinite(l)) {
+                flag_error(st.err, kErrFcLevel, t);
+                return;
+            }
+            const Real sn = gamma * fdiv(yt, lp) + omg * s_t;
+            ring[j * bd] = sn;
+            const int uu = t + S;
+            if (uu >= t_ins - I && uu < t_ins) win[(uu - (t_ins - I)) * bd] = sn;
+            if (dump) {
+                dump_lv[t] = l;
+                dump_se[uu] = sn;
+            }
+            lp = l;
+            j = (j + 1 == S) ? 0 : j + 1;
         }
-        lp = l;
-        j = (j + 1 == S) ? 0 : j + 1;
     }
     if (X == nullptr) return;
     const Real level = lp;
