@@ -377,3 +377,19 @@ def test_large_step_split_gradient_tiles(engine, oracle, precision, tol):
     gg2 = g2.batch_gradients(copy_batch(b))
     for name_ in go.network:
         assert np.array_equal(gg.network[name_], gg2.network[name_]), name_
+
+
+@pytest.mark.parametrize("freq", [Frequency.Yearly, Frequency.Quarterly, Frequency.Monthly])
+def test_forecast_scan_reports_first_bad_observation(engine, oracle, freq):
+    """K6 is specialised per season length (S = 1/4/12); its folded error checks must report
+    the first non-positive observation, as the reference's scan throws there."""
+    prof = FrequencyProfile.defaults(freq)
+    length = prof.min_length + 2 * prof.horizon
+    vals, cats = oracle.make_synthetic(5, 40, length, prof.seasonality_length, 0.05)
+    p = length - 2 * prof.horizon - 3
+    vals[17, p] = 0.0
+    vals[29, p + 1] = -1.0
+    for api in (engine, oracle):
+        tr = Trainer((vals, cats), prof, TrainConfig(seed=1, batch_size=64), api=api)
+        with pytest.raises(E.NumericDomainError, match=f"t={p}\\b"):
+            tr.validate()
