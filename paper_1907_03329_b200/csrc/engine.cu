@@ -180,6 +180,8 @@ struct esrnn_trainer {
     PinnedBuf<double> stage_pin;       // creation: its pinned staging copy
     PinnedBuf<signed char> stage_cat;  // creation: pinned category bytes
     PinnedBuf<int> pin_i;
+    PinnedBuf<int> pin_err;            // the error word, read back with a call's results
+    PinnedBuf<double> pin_loss;        // an epoch's per-step losses
     PinnedBuf<double> pin_d;
 
     std::shared_ptr<GraphExec> graph;  // epoch graph (shared with the process-wide cache)
@@ -365,11 +367,28 @@ void validate_config(const esrnn_profile& p, const esrnn_train_config& c) {
         raise(ESRNN_CONFIG_ERROR, "profile: window sizes unsupported by the B200 kernels");
 }
 
+// The error word's copy, enqueued with a call's results so one synchronisation covers both;
+// check_device_error() reads it after that synchronisation.
+void enqueue_error_read(Eng* e) {
+    e->pin_err.reserve(2);
+    CUDA_OK(cudaMemcpyAsync(e->pin_err.p, e->errw.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, e->stream));
+}
+
+void raise_device_error(Eng* e, const int* h);
+
+void check_device_error(Eng* e) {
+    if (e->pin_err.p[0] != 0) raise_device_error(e, e->pin_err.p);
+}
+
 void throw_device_error(Eng* e) {
     int h[2];
     CUDA_OK(cudaMemcpyAsync(h, e->errw.p, sizeof h, cudaMemcpyDeviceToHost, e->stream));
     CUDA_OK(cudaStreamSynchronize(e->stream));
-    if (h[0] == 0) return;
+    if (h[0] != 0) raise_device_error(e, h);
+}
+
+void raise_device_error(Eng* e, const int* hp) {
+    const int h[2] = {hp[0], hp[1]};
     const int reset[2] = {0, INT_MAX};
     CUDA_OK(cudaMemcpyAsync(e->errw.p, reset, sizeof reset, cudaMemcpyHostToDevice, e->stream));
     CUDA_OK(cudaStreamSynchronize(e->stream));
@@ -1281,8 +1300,10 @@ double train_epoch_impl(Eng* e) {
     // consumed in the same order as building it at the next call would)
     if (!e->profiling) build_epoch_plan(e, e->next_plan);
     if (e->profiling) e->prof_collect();
-    std::vector<double> lh(steps);
-    CUDA_OK(cudaMemcpyAsync(lh.data(), e->loss_hist.p, sizeof(double) * steps, cudaMemcpyDeviceToHost, e->stream));
+    e->pin_loss.reserve(std::max(steps, 1));
+    const double* lh = e->pin_loss.p;
+    CUDA_OK(cudaMemcpyAsync(e->pin_loss.p, e->loss_hist.p, sizeof(double) * steps, cudaMemcpyDeviceToHost, e->stream));
+    enqueue_error_read(e);
     CUDA_OK(cudaStreamSynchronize(e->stream));
     if (dbg_host) {
         const auto h4 = clk::now();
@@ -1295,7 +1316,7 @@ double train_epoch_impl(Eng* e) {
     float ms = 0.f;
     CUDA_OK(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
     e->last_ms = ms;
-    throw_device_error(e);
+    check_device_error(e);
     if (e->dbg_clk.p) {
         long long c[96];
         CUDA_OK(cudaMemcpy(c, e->dbg_clk.p, sizeof c, cudaMemcpyDeviceToHost));
@@ -1525,11 +1546,12 @@ void forecast_impl(Eng* e, int64_t drop_tail, double* out, int mode, const Score
         if (mode == 2)
             CUDA_OK(cudaMemcpyAsync(psc, e->f_score.p, sizeof(double) * nsc, cudaMemcpyDeviceToHost, e->stream));
     }
+    enqueue_error_read(e);
     CUDA_OK(cudaStreamSynchronize(e->stream));
     float ms = 0.f;
     CUDA_OK(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
     e->last_ms = ms;
-    throw_device_error(e);
+    check_device_error(e);
     if (out && N > 0) std::memcpy(out, pf, sizeof(double) * nfo);
     if (mode == 0) return;
     const double* sm = psm;
