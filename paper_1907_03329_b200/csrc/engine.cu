@@ -178,6 +178,7 @@ struct esrnn_trainer {
     bool have_last = false;  // cur_plan holds the global window order of the last train_epoch
     DBuf<double> stage_raw;            // creation: the series block as uploaded (fp64)
     PinnedBuf<double> stage_pin;       // creation: its pinned staging copy
+    PinnedBuf<double> stage_theta;     // creation: the initial compact weights, pinned
     PinnedBuf<signed char> stage_cat;  // creation: pinned category bytes
     PinnedBuf<int> pin_i;
     PinnedBuf<int> pin_err;            // the error word, read back with a call's results
@@ -568,11 +569,19 @@ void download_real(Eng* e, const void* dev, size_t n, double* dst) {
     from_real(e, tmp.data(), n, dst);
 }
 
-void upload_theta(Eng* e) {
+// stage = nullptr: synchronous (the caller's next use may follow at once); else the compact
+// vector goes through the caller's pinned staging block with no synchronisation here
+void upload_theta(Eng* e, PinnedBuf<double>* stage = nullptr) {
     std::vector<double> c(e->live_flat.size(), 0.0);
     for (size_t i = 0; i < c.size(); ++i)
         if (e->live_flat[i] >= 0) c[i] = e->w_host[e->live_flat[i]];
-    upload_real(e, e->theta.p, c.data(), c.size());
+    if (!stage) {
+        upload_real(e, e->theta.p, c.data(), c.size());
+        return;
+    }
+    stage->reserve(std::max<size_t>(c.size(), 1));
+    to_real(e, c.data(), c.size(), stage->p);
+    CUDA_OK(cudaMemcpyAsync(e->theta.p, stage->p, e->rsz * c.size(), cudaMemcpyHostToDevice, e->stream));
 }
 
 void sync_weights_from_device(Eng* e) {
@@ -1819,11 +1828,12 @@ esrnn_status esrnn_trainer_create(const esrnn_profile* profile, const esrnn_trai
         weights_ready.wait();
         convert_weights();
         c[nc++] = clk::now();
-        upload_theta(e.get());
+        upload_theta(e.get(), &e->stage_theta);
         ensure_capacity(e.get(), cfg->batch_size);
         CUDA_OK(cudaStreamSynchronize(e->stream));
         e->stage_raw.free();
         e->stage_pin.release();
+        e->stage_theta.release();
         e->stage_cat.release();
         c[nc++] = clk::now();
         if (dbg_host) {
