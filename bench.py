@@ -17,12 +17,22 @@ e2e        the same metric through the public Python API with host buffers: ever
            constructs the Trainer from host arrays (H2D of the series), trains one epoch
            (H2D of the shuffled window plan), validates and reads back the losses,
            forecasts and sMAPE (D2H); wall clock, synchronised.
-roofline   dominant kernel by device-time share, algorithmic FLOPs (SURVEY §8(d) formula)
-           per launch over its measured average launch time (CUDA events, profiling pass).
+roofline   dominant kernel by device-time share of the timed configuration (the epoch's CUDA
+           graph, programmatic dependent launch on): every CTA stamps the device global timer
+           after its dependency wait and at its end, a kernel's time per step is its latest
+           end minus its earliest start (esrnn_trainer_profile_kernels(t, 2)).  achieved =
+           algorithmic work per launch (k_tile does the stack forward and the
+           input adjoints = 2 x fwd FLOPs; k_grad_finish the weight-gradient contraction =
+           1 x fwd FLOPs; k_adam / k_forecast_scan bytes) over that time.  `kernels` lists
+           every kernel's share, time and roofline fraction.
 cpu_baseline  the reference (oracle/_ref, the reference's own headers) timed on this host,
-           1 core (it is single-threaded).  The reference arm also reports
-           all_cores_upper_bound: one reference process per usable core, each on its own
-           N/P-series shard (P separate models, so not the same training problem).
+           1 core pinned with sched_setaffinity (it is single-threaded); CPU model and build
+           flags recorded.  The reference arm also reports all_cores_upper_bound: one
+           reference process per usable core, each on its own N/P-series shard (P separate
+           models, so not the same training problem).
+
+--gpus N without a torchrun environment re-launches itself under torch.distributed.run
+with N ranks (127.0.0.1 rendezvous), one GPU per rank.
 """
 from __future__ import annotations
 
@@ -81,13 +91,35 @@ def workload(name: str, world: int):
     return freq, n, length, s, B, scaling
 
 
-def lstm_flops_per_step(prof: FrequencyProfile, B: int) -> float:
-    """live-gate LSTM FLOPs, fwd = sum_l 2*B*in_l*3H + 2BH^2 + 2BHO; bwd = 2*fwd."""
+def lstm_fwd_flops(prof: FrequencyProfile, B: int) -> float:
+    """live-gate LSTM forward FLOPs, fwd = sum_l 2*B*in_l*3H + 2BH^2 + 2BHO.
+    The step's FLOPs are 3 x fwd: k_tile does the forward and the input adjoints (2 x fwd),
+    k_grad_finish the weight-gradient contraction (1 x fwd)."""
     H, O = prof.hidden_size, prof.horizon
     in0 = prof.input_window + 6
     layers = sum(len(b) for b in prof.dilation_blocks)
-    fwd = sum(2.0 * B * (in0 if l == 0 else H) * 3 * H for l in range(layers)) + 2.0 * B * H * H + 2.0 * B * H * O
-    return 3.0 * fwd
+    return sum(2.0 * B * (in0 if l == 0 else H) * 3 * H for l in range(layers)) + 2.0 * B * H * H + 2.0 * B * H * O
+
+
+def live_params(prof: FrequencyProfile) -> int:
+    """Live shared parameters: W_in and bias over the i, g, o gates, head."""
+    H, O = prof.hidden_size, prof.horizon
+    in0 = prof.input_window + 6
+    layers = sum(len(b) for b in prof.dilation_blocks)
+    return sum(((in0 if l == 0 else H) + 1) * 3 * H for l in range(layers)) + H * H + H + H * O + O
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+REF_BUILD_FLAGS = "g++ -std=gnu++20 -O3 -march=x86-64-v4 (oracle/Makefile; the reference's Release flags, ISA pinned)"
 
 
 def scan_bytes(prof: FrequencyProfile, k: int, T: int) -> float:
@@ -195,10 +227,28 @@ def make_data(api, n, length, s, seed=41, sigma=0.05):
 
 
 # ----------------------------------------------------------------------------- CPU legs
-def time_cpu(lib_path: Path, prof, cfg: TrainConfig, vals, cats, budget_s: float):
-    """Reference / port on this host (1 thread: the reference is single-threaded).
-    Full epochs (+ validate) when an epoch fits the budget, else a bounded sample of
-    training batches through run_batch(update) extrapolated to the epoch."""
+def time_cpu(lib_path: Path, prof, cfg: TrainConfig, vals, cats, budget_s: float, warmup: int = 1):
+    """Reference / port on this host, pinned to one core (the reference is single-threaded).
+    `warmup` untimed epochs (or batches) first; then full epochs (+ validate) when an epoch
+    fits the budget, else a bounded sample of training batches through run_batch(update)
+    extrapolated to the epoch."""
+    core = None
+    old = None
+    if hasattr(os, "sched_setaffinity"):
+        old = os.sched_getaffinity(0)
+        core = max(old)
+        os.sched_setaffinity(0, {core})
+    try:
+        r = _time_cpu(lib_path, prof, cfg, vals, cats, budget_s, warmup)
+    finally:
+        if old is not None:
+            os.sched_setaffinity(0, old)
+    r.update({"pinned_core": core, "cpu_model": cpu_model(), "build": REF_BUILD_FLAGS if lib_path == REF_LIB else
+              "gcc -std=c11 -O2 (oracle/Makefile)"})
+    return r
+
+
+def _time_cpu(lib_path: Path, prof, cfg: TrainConfig, vals, cats, budget_s: float, warmup: int):
     api = N.NativeApi(lib_path)
     n = vals.shape[0]
     cfg_c = TrainConfig(**{**cfg.__dict__, "precision": "fp64", "max_batch_size": 0,
@@ -224,6 +274,9 @@ def time_cpu(lib_path: Path, prof, cfg: TrainConfig, vals, cats, budget_s: float
     times = []
     if est_epoch <= budget_s / 2:
         kind = "epochs"
+        for _ in range(warmup):
+            tr.train_epoch()
+            tr.validate()
         t_start = time.perf_counter()
         while time.perf_counter() - t_start < budget_s or not times:
             t0 = time.perf_counter()
@@ -231,9 +284,12 @@ def time_cpu(lib_path: Path, prof, cfg: TrainConfig, vals, cats, budget_s: float
             tr.validate()
             times.append(time.perf_counter() - t0)
         step_s = statistics.median(times)
-        sample = f"{len(times)} full epochs (+validate) of {n} series, median"
+        sample = f"{len(times)} full epochs (+validate) of {n} series after {warmup} untimed, median"
     else:
         kind = "batches"
+        for _ in range(warmup):
+            idx = rng.integers(0, len(w), size=cfg_c.batch_size)
+            tr.step(WindowBatch([w[i][0] for i in idx], [w[i][1] for i in idx]), update=True)
         t_start = time.perf_counter()
         nb = 0
         while time.perf_counter() - t_start < budget_s or nb == 0:
@@ -291,8 +347,21 @@ def time_cpu_all_cores(lib_path: Path, prof, cfg: TrainConfig, vals, cats, budge
 
 
 # ----------------------------------------------------------------------------- main
+def spawn_ranks(a) -> int:
+    """--gpus N outside torchrun: run this script under torch.distributed.run with N ranks."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     a = parse()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(a))
     world, rank, local = dist_setup(a.gpus)
     freq, n_total, length, s, B, scaling = workload(a.config, world)
     prof = FrequencyProfile.defaults(freq)
@@ -311,10 +380,10 @@ def main():
         api = N.NativeApi(PORT_LIB if kind == "port" else REF_LIB)
         vals, cats = make_data(api, n_total, length, s)
         cfg = TrainConfig(batch_size=min(B, 2048), seed=7, precision="fp64")
-        for _ in range(max(a.warmup, 0)):
-            pass
-        res = [time_cpu(lib, prof, cfg, vals, cats, budget_s=max(3.0, 60.0 / max(a.steps, 1)))
-               for _ in range(max(a.steps, 1))]
+        # W untimed epochs (or batches) before the first timed step, in the same process
+        res = [time_cpu(lib, prof, cfg, vals, cats, budget_s=max(3.0, 60.0 / max(a.steps, 1)),
+                        warmup=max(a.warmup, 0) if i == 0 else 0)
+               for i in range(max(a.steps, 1))]
         v = statistics.median(r["value"] for r in res)
         allc = None
         if not a.no_cpu_baseline:
@@ -324,6 +393,8 @@ def main():
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1000.0 * n_total / v, "higher_is_better": True,
             "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg_desc,
             "cpu_baseline": {"value": v, "unit": "series/s", "cores": 1, "kind": kind, "sample": res[0]["sample"],
+                             "cpu_model": res[0]["cpu_model"], "pinned_core": res[0]["pinned_core"],
+                             "host_cores": os.cpu_count(), "build": res[0]["build"],
                              "all_cores_upper_bound": allc},
             "e2e": {"value": v, "unit": "series/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
         return
@@ -374,50 +445,88 @@ def main():
     value = n_total * a.steps / (total_ms / 1000.0)
     clocks = clock.summary(local)
 
-    # per-kernel profiling pass (outside the timed region)
-    tr.profile_kernels(True)
-    tr.train_epoch()
-    tr.validate()
+    # Per-kernel time in the timed configuration (outside the timed region): the epoch graph
+    # with in-kernel global-timer spans; the forecast kernels (no graph) by CUDA events
+    tr.profile_kernels(2)
+    tr.train_epoch()  # captures the span-instrumented graph
+    tr.profile_kernels(2)  # reset
+    n_span_epochs = 3
+    for _ in range(n_span_epochs):
+        tr.train_epoch()
     kt = tr.kernel_times()
-    tr.profile_kernels(False)
-    tot = sum(ms for ms, _ in kt.values()) or 1.0
-    shares = {k: {"ms": ms, "launches": n, "share": ms / tot} for k, (ms, n) in kt.items() if n}
-    dom = max(shares, key=lambda k: shares[k]["ms"])
+    tr.profile_kernels(1)
+    tr.validate()
+    kt_fc = tr.kernel_times()
+    tr.profile_kernels(0)
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     sm_max = peaks.get("sm_max_mhz", 1965.0)
     fp32_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12
+    fma_peak = fp32_peak if a.precision == "fp32" else fp32_peak / 2
+    hbm_peak = peaks.get("hbm_gbs", 6553.9)
     T = length - 2 * prof.horizon
     per = T - prof.horizon - prof.input_window + 1
     steps_per_epoch = -(-n_total * per // B)
     B_local = B // world
-    # DRAM traffic per launch of the dominant kernel, from the committed ncu --set full capture
-    # of this workload (tools/ncu_summary.py traffic), when there is one
-    traffic = None
+    S = prof.seasonality_length
+    rb = 4 if a.precision == "fp32" else 8
+    # DRAM traffic per launch, from the committed ncu --set full capture of this workload
+    traffic = {}
     tf = ROOT / "profiles" / "ncu_traffic.json"
     if tf.exists():
         doc = json.loads(tf.read_text())
-        kname = {"tile": "k_tile", "finish": "k_grad_finish", "adam": "k_adam"}.get(dom)
-        if doc.get("config") == a.config and kname in doc.get("kernels", {}):
-            traffic = doc["kernels"][kname]
-    if dom in ("tile",):
-        flops = lstm_flops_per_step(prof, B_local)
-        avg_s = shares[dom]["ms"] / shares[dom]["launches"] / 1e3
-        achieved = flops / avg_s / 1e12
-        peak = fp32_peak if a.precision == "fp32" else fp32_peak / 2
-        roof = {"kernel": "k_tile (fused HW scan + window + LSTM fwd/bwd + pinball)", "bound": "fp32-fma",
-                "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                "peak_source": f"derived CUDA-core FP32 FMA peak: 148 SM x 128 lanes x 2 x {sm_max:.0f} MHz "
-                               f"(MEASURED_PEAKS sm_max_mhz); no tensor-core path (fp32 contract)",
-                "algorithmic_per_launch": f"{flops:.3e} FLOP (live-gate LSTM fwd+bwd, B={B_local})"}
-    else:
-        k_slots = min(n_local, B_local)
-        byts = scan_bytes(prof, k_slots, T)
-        avg_s = shares[dom]["ms"] / shares[dom]["launches"] / 1e3
-        achieved = byts / avg_s / 1e9
-        peak = peaks.get("hbm_gbs", 6553.9)
-        roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic, "peak_source": "MEASURED_PEAKS hbm_gbs (measured)",
-                "algorithmic_per_launch": f"{byts:.3e} B"}
+        if doc.get("config") == a.config and doc.get("precision", "fp32") == a.precision:
+            traffic = doc.get("kernels", {})
+    windows_local = n_local * per  # every window once per epoch
+    P_live = live_params(prof)
+    k_slots = min(n_local, B_local)
+    kern = {}
+
+    def add(name, cls, ms_tot, launches, work, unit, peak, note):
+        if not launches:
+            return
+        avg_s = ms_tot / launches / 1e3
+        ach = work / avg_s / (1e12 if unit == "TFLOP/s" else 1e9)
+        kern[name] = {"class": cls, "ms_per_step": ms_tot / (n_span_epochs if cls != "forecast" else 1),
+                      "launches_per_step": launches / (n_span_epochs if cls != "forecast" else 1),
+                      "avg_us": avg_s * 1e6, "algorithmic_per_launch": work, "achieved": ach, "unit": unit,
+                      "peak": peak, "frac": ach / peak, "work": note, "traffic": traffic.get(name)}
+
+    fwd_epoch = lstm_fwd_flops(prof, windows_local)
+    ms, n = kt["tile"]
+    add("k_tile", "train", ms, n, 2.0 * fwd_epoch / max(n / n_span_epochs, 1), "TFLOP/s", fma_peak,
+        "stack forward + input adjoints = 2 x fwd FLOPs of the step's windows (SURVEY §8(d))")
+    ms, n = kt["finish"]
+    add("k_grad_finish", "train", ms, n, fwd_epoch / max(n / n_span_epochs, 1), "TFLOP/s", fma_peak,
+        "weight-gradient contraction = 1 x fwd FLOPs (its ES reverse-scan blocks run beside it)")
+    ms, n = kt["adam"]
+    add("k_adam", "train", ms, n, rb * (7.0 * P_live + 7.0 * k_slots * (2 + S)) + 8.0 * k_slots, "GB/s", hbm_peak,
+        "SURVEY K5 bytes: 7 x (P_live + k(2+S)) Real + 8k")
+    if "finalize" in kt:
+        ms, n = kt["finalize"]
+        add("k_finalize/k_group_reduce", "train", ms, n, rb * 2.0 * P_live, "GB/s", hbm_peak, "reduced buffer in+out")
+    fmsn = kt_fc.get("forecast_scan")
+    if fmsn:
+        add("k_forecast_scan", "forecast", fmsn[0], fmsn[1], rb * (n_local * (length - 2 * prof.horizon) + n_local * (2 + S)
+                                                               + n_local * (prof.input_window + 6) + n_local * (1 + prof.horizon)),
+            "GB/s", hbm_peak, "SURVEY K6 bytes: observations to t_ins + params + window/level/seasonality outputs")
+    fmsn = kt_fc.get("forecast_tile")
+    if fmsn:
+        add("k_tile<forecast>", "forecast", fmsn[0], fmsn[1], lstm_fwd_flops(prof, n_local), "TFLOP/s", fma_peak,
+            "stack forward over every series (1 x fwd FLOPs)")
+    step_ms = sum(v["ms_per_step"] for v in kern.values())
+    for v in kern.values():
+        v["share"] = v["ms_per_step"] / step_ms if step_ms else None
+    dom = max(kern, key=lambda k: kern[k]["ms_per_step"])
+    d = kern[dom]
+    roof = {"kernel": dom, "bound": "fp32-fma" if d["unit"] == "TFLOP/s" else "hbm", "achieved": d["achieved"],
+            "peak": d["peak"], "unit": d["unit"], "frac": d["frac"], "traffic": d["traffic"],
+            "algorithmic_per_launch": d["algorithmic_per_launch"], "work": d["work"],
+            "timing": "in-graph global-timer spans (PDL on), mean over 3 epochs",
+            "peak_source": (f"derived CUDA-core FP32 FMA peak: 148 SM x 128 lanes x 2 x {sm_max:.0f} MHz "
+                            f"(MEASURED_PEAKS sm_max_mhz){'; fp64 = half' if a.precision == 'fp64' else ''}; "
+                            "no tensor-core path at these batch sizes (fp32 contract)")
+            if d["unit"] == "TFLOP/s" else "MEASURED_PEAKS hbm_gbs (measured)"}
+    shares = kern
 
     # e2e through the public API with host buffers
     e2e = None
@@ -470,7 +579,26 @@ def main():
         kind = "reference" if lib == REF_LIB else "port"
         cb = time_cpu(lib, prof, TrainConfig(batch_size=min(B, 2048), seed=7), vals, cats, a.cpu_seconds)
         cpu = {"value": cb["value"], "unit": "series/s", "cores": 1, "kind": kind, "sample": cb["sample"],
-               "host_cores": cb["host_cores"]}
+               "host_cores": cb["host_cores"], "cpu_model": cb["cpu_model"], "pinned_core": cb["pinned_core"],
+               "build": cb["build"]}
+
+    # the same step in fp64 parity mode (the reference's arithmetic), device-timed, for context
+    fp64_line = None
+    if world == 1 and a.precision == "fp32":
+        t64 = Trainer((vals, cats), prof, TrainConfig(**{**cfg.__dict__, "precision": "fp64"}), api=api)
+        for _ in range(max(1, a.warmup)):
+            t64.train_epoch()
+            t64.validate()
+        ms64 = []
+        for _ in range(max(1, a.steps)):
+            flush_l2(local)
+            t64.train_epoch()
+            m = t64.last_device_ms()
+            v64 = t64.validate()
+            ms64.append(m + t64.last_device_ms())
+        fp64_line = {"value": n_total * len(ms64) / (sum(ms64) / 1000.0), "unit": "series/s",
+                     "ms_per_step": statistics.mean(ms64), "val_smape": v64.mean_smape, "dtype": "f64"}
+        t64.close()
 
     if rank == 0:
         out = {
@@ -480,7 +608,7 @@ def main():
             "data": "synthetic (reference generator make_multiplicative_series, seed 41)", "config": cfg_desc,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
             "wall_ms_per_step": 1000.0 * statistics.mean(wall), "epoch_losses": losses,
-            "val_smape": v.mean_smape, "kernels": shares,
+            "val_smape": v.mean_smape, "kernels": shares, "fp64_engine": fp64_line,
             "speedup_vs_cpu": (value / cpu["value"]) if cpu else None,
         }
         print(json.dumps(out))

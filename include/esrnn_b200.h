@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define ESRNN_ABI_VERSION 1
+#define ESRNN_ABI_VERSION 2
 #define ESRNN_MAX_BLOCKS 8
 #define ESRNN_MAX_LAYERS 16
 #define ESRNN_NUM_CATEGORIES 6      /* data.hpp:21 kNumCategories */
@@ -56,7 +56,8 @@ typedef enum esrnn_status {
 } esrnn_status;
 
 /* Compute precision of the device path (B200 extension; the reference is fp64). */
-enum { ESRNN_FP32 = 0, ESRNN_FP64 = 1 };
+/* Zero selects fp64, the reference's arithmetic; fp32 is the opt-in performance path. */
+enum { ESRNN_FP64 = 0, ESRNN_FP32 = 1 };
 
 /* esrnn::FrequencyProfile (data.hpp:60-118).  dilation_blocks is flattened:
  * block b owns layers [sum(block_len[0..b)), +block_len[b]). */
@@ -73,8 +74,7 @@ typedef struct esrnn_profile {
 } esrnn_profile;
 
 /* esrnn::TrainConfig (trainer.hpp:22-44) plus B200 extensions at the end;
- * zero-initialised extensions reproduce the reference's behaviour except
- * `precision`, whose zero value selects the fp32 performance path. */
+ * zero-initialised extensions reproduce the reference's behaviour (precision 0 = fp64). */
 typedef struct esrnn_train_config {
     int32_t epochs;
     int32_t batch_size;
@@ -94,14 +94,32 @@ typedef struct esrnn_train_config {
     int32_t use_graphs;           /* 0 => default (on); <0 => off (debug) */
 } esrnn_train_config;
 
-/* Series-sharded data parallelism (B200 extension).  Rank r owns
- * dataset rows [floor(r*N/W), floor((r+1)*N/W)); per-series parameters live only
- * on their owner; the shared-gradient buffer is all-reduced with NCCL. */
+/* Series-sharded data parallelism (B200 extension).  Rank r owns dataset
+ * rows [floor(r*N/W), floor((r+1)*N/W)); per-series parameters live only on their owner.
+ * Per step, the shared-network gradients and the step tail (per-series squared norm, loss
+ * sum, error flag) are all-reduced, then every rank finalises the identical clip scale and
+ * Adam update.  Two transports:
+ *   - NCCL (one process per GPU): nccl_unique_id from esrnn_nccl_unique_id() on rank 0;
+ *   - an in-process group (group != NULL, from esrnn_group_create): W trainers in one
+ *     process, each driven by its own host thread, on one GPU or on peer-accessible GPUs;
+ *     the exchange is the engine's own fused reduce kernel (no NCCL).
+ * flags: ESRNN_DIST_FORCE_COLLECTIVE runs the collective step even at world_size 1 (a
+ * one-rank NCCL communicator or group): the sharded code path on a single GPU. */
+typedef struct esrnn_group esrnn_group;
+enum { ESRNN_DIST_FORCE_COLLECTIVE = 1 };
 typedef struct esrnn_dist {
     int32_t rank;
     int32_t world_size;
     uint8_t nccl_unique_id[128];  /* from esrnn_nccl_unique_id() on rank 0 */
+    /* --- ABI 2 --- */
+    int32_t flags;
+    esrnn_group* group;
 } esrnn_dist;
+
+/* In-process rank group of world_size ranks (see esrnn_dist).  Destroy after every trainer
+ * that joined it; a trainer keeps the group alive while it exists. */
+esrnn_status esrnn_group_create(int32_t world_size, esrnn_group** out);
+void esrnn_group_destroy(esrnn_group* g);
 
 /* One named network array in StackWeights::for_each_param order (network.hpp:62-74). */
 typedef struct esrnn_param_info {
@@ -146,6 +164,12 @@ esrnn_status esrnn_trainer_set_weights(esrnn_trainer* t, const double* flat, int
  * (global row numbers; must be owned).  seas_raw is n x S row-major. */
 esrnn_status esrnn_trainer_get_per_series(esrnn_trainer* t, int64_t row_begin, int64_t n,
                                           double* alpha_raw, double* gamma_raw, double* seas_raw);
+/* Collective (every rank of a sharded trainer calls it): all series' per-series parameters
+ * (Trainer::per_series_params for every i, trainer.hpp:210-211), gathered from their owners
+ * in dataset order -- what checkpoint.hpp's snapshot (:48-62) needs from a sharded run.
+ * alpha_raw, gamma_raw [n_series], seas_raw [n_series x S].  Unsharded: every row. */
+esrnn_status esrnn_trainer_gather_per_series(esrnn_trainer* t, double* alpha_raw, double* gamma_raw,
+                                             double* seas_raw);
 /* Trainer::set_per_series (trainer.hpp:434-445), same addressing. */
 esrnn_status esrnn_trainer_set_per_series(esrnn_trainer* t, int64_t row_begin, int64_t n,
                                           const double* alpha_raw, const double* gamma_raw,
@@ -251,10 +275,13 @@ esrnn_status esrnn_trainer_last_device_ms(const esrnn_trainer* t, double* ms);
 /* Number of kernels the engine launched since creation (graph nodes counted). */
 esrnn_status esrnn_trainer_kernel_launches(const esrnn_trainer* t, int64_t* n);
 
-/* Per-kernel device timing (measurement hook for bench.py's roofline).  When enabled,
+/* Per-kernel device timing (measurement hook for bench.py's roofline).  enable == 1:
  * train_epoch / run_batch / forecast launch kernels directly (no CUDA graph) with a CUDA
- * event pair around every launch on the engine stream; kernel_times returns, per kernel
- * class, the summed milliseconds and launch counts since the last reset.
+ * event pair around every launch on the engine stream.  enable == 2: train_epoch runs its
+ * CUDA graph as usual (programmatic dependent launch on) and every CTA stamps the device
+ * global timer after its dependency wait and at its end; a kernel's time per step is its
+ * latest CTA end minus its earliest CTA start.  kernel_times returns, per kernel class, the
+ * summed milliseconds and launch counts since the last reset (0 disables both).
  * Classes: 0 (unused: the training scan runs inside the tile kernel), 1 tile (scan +
  * window + stack fwd/bwd + loss), 2 finish (ES backward + weight-gradient contraction),
  * 3 (unused), 4 adam, 5 finalize, 6 forecast_scan, 7 tile (forecast). */

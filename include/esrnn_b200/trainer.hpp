@@ -34,8 +34,8 @@
 
 namespace esrnn {
 
-// TrainConfig (trainer.hpp:22-44) plus B200 extensions (defaults keep reference behaviour,
-// except precision: fp32 performance mode; set Precision::FP64 for parity mode).
+// TrainConfig (trainer.hpp:22-44) plus B200 extensions; every default keeps the reference's
+// behaviour, including fp64 arithmetic.  Precision::FP32 is the opt-in performance path.
 enum class Precision { FP32 = ESRNN_FP32, FP64 = ESRNN_FP64 };
 
 struct TrainConfig {
@@ -50,7 +50,7 @@ struct TrainConfig {
     int patience = 0;
     double min_delta = 0.0;
     // --- B200 extensions ---
-    Precision precision = Precision::FP32;
+    Precision precision = Precision::FP64;
     int max_batch_size = 0;  // 0 -> 2048 (reference cap)
     int device = 0;
     bool use_graphs = true;
@@ -182,10 +182,15 @@ struct BatchGradients {
 };
 
 // Series-sharded data parallelism (B200 extension): pass to the Trainer to run as one rank.
+// Transport: NCCL (nccl_unique_id, one process per GPU) or an in-process group (group,
+// from esrnn_group_create: one host thread per rank).  force_collective runs the
+// collective step at world_size 1 too.
 struct DistConfig {
     int rank = 0;
     int world_size = 1;
     std::array<std::uint8_t, 128> nccl_unique_id{};
+    esrnn_group* group = nullptr;
+    bool force_collective = false;
     static std::array<std::uint8_t, 128> new_unique_id() {
         std::array<std::uint8_t, 128> id{};
         detail::check(esrnn_nccl_unique_id(id.data()), nullptr);
@@ -220,6 +225,8 @@ public:
             d.rank = dist->rank;
             d.world_size = dist->world_size;
             std::memcpy(d.nccl_unique_id, dist->nccl_unique_id.data(), 128);
+            d.group = dist->group;
+            d.flags = dist->force_collective ? ESRNN_DIST_FORCE_COLLECTIVE : 0;
         }
         esrnn_trainer* h = nullptr;
         detail::check(esrnn_trainer_create(&p, &c, static_cast<std::int64_t>(series_.size()), static_cast<std::int32_t>(n),
@@ -258,14 +265,35 @@ public:
     std::size_t series_count() const { return series_.size(); }
     const SeriesRecord& series(std::size_t i) const { return series_.at(i); }
     const DatasetSplit& split(std::size_t i) const { return splits_.at(i); }
+    // A series-sharded trainer holds only its own rows' parameters: other rows are readable
+    // after the collective gather_per_series() (every rank calls it; valid until the next
+    // training call), which is what checkpoint.hpp's snapshot (:48-62) needs.
     PerSeriesParams& per_series_params(std::size_t i) {
+        check_owned(i);
         pull_params();
         tainted_rows_.insert(i);
         return params_.at(i);
     }
     const PerSeriesParams& per_series_params(std::size_t i) const {
+        check_owned(i);
         pull_params();
         return params_.at(i);
+    }
+    void gather_per_series() {
+        push();
+        const std::size_t n = series_.size();
+        const int S = profile_.seasonality_length;
+        std::vector<double> a(n), g(n), s(n * static_cast<std::size_t>(S));
+        detail::check(esrnn_trainer_gather_per_series(h_.get(), a.data(), g.data(), s.data()), h_.get());
+        for (std::size_t i = 0; i < n; ++i) {
+            PerSeriesParams& p = params_[i];
+            p.alpha_raw = a[i];
+            p.gamma_raw = g[i];
+            p.init_seasonality_raw.assign(s.begin() + static_cast<std::ptrdiff_t>(i * S),
+                                          s.begin() + static_cast<std::ptrdiff_t>((i + 1) * S));
+        }
+        params_stale_ = false;
+        gathered_ = true;
     }
     std::size_t shard_begin() const { return row_begin_; }
     std::size_t shard_end() const { return row_end_; }
@@ -684,7 +712,14 @@ private:
         }
     }
 
+    void check_owned(std::size_t i) const {
+        if (i < series_.size() && (i < row_begin_ || i >= row_end_) && !gathered_)
+            throw ContractError("per_series_params: series " + std::to_string(i) +
+                                " is owned by another rank (call gather_per_series() on every rank first)");
+    }
+
     void mark_trained() {
+        gathered_ = false;
         weights_stale_ = params_stale_ = true;
         weights_tainted_ = false;
         tainted_rows_.clear();
@@ -720,7 +755,7 @@ private:
     std::int64_t n_values_ = 0;
     mutable StackWeights weights_;
     mutable std::vector<PerSeriesParams> params_;
-    mutable bool weights_stale_ = true, params_stale_ = true, weights_tainted_ = false;
+    mutable bool weights_stale_ = true, params_stale_ = true, weights_tainted_ = false, gathered_ = false;
     std::set<std::size_t> tainted_rows_;
 };
 

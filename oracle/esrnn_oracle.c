@@ -1395,6 +1395,18 @@ esrnn_status esrnn_trainer_kernel_times(esrnn_trainer* t, double* total_ms, int6
 
 esrnn_status esrnn_release_cached_memory(void) { return ESRNN_OK; }
 
+/* Sharded-mode entry points (B200 extension): the oracle is single-process, unsharded. */
+esrnn_status esrnn_group_create(int32_t world_size, esrnn_group** out) {
+    (void)world_size;
+    *out = NULL;
+    snprintf(g_create_err, sizeof g_create_err, "oracle: no sharded mode");
+    return ESRNN_CONFIG_ERROR;
+}
+void esrnn_group_destroy(esrnn_group* g) { (void)g; }
+esrnn_status esrnn_trainer_gather_per_series(esrnn_trainer* t, double* a, double* g, double* s) {
+    return esrnn_trainer_get_per_series(t, 0, t->N, a, g, s);
+}
+
 esrnn_status esrnn_nccl_unique_id(uint8_t out[128]) {
     (void)out;
     snprintf(g_create_err, sizeof g_create_err, "oracle: no NCCL");

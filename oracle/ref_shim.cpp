@@ -544,6 +544,17 @@ esrnn_status esrnn_trainer_kernel_times(esrnn_trainer*, double* total_ms, int64_
 
 esrnn_status esrnn_release_cached_memory(void) { return ESRNN_OK; }
 
+// Sharded-mode entry points (B200 extension): the reference is single-process, unsharded.
+esrnn_status esrnn_group_create(int32_t, esrnn_group** out) {
+    *out = nullptr;
+    g_create_err = "reference shim: no sharded mode";
+    return ESRNN_CONFIG_ERROR;
+}
+void esrnn_group_destroy(esrnn_group*) {}
+esrnn_status esrnn_trainer_gather_per_series(esrnn_trainer* t, double* a, double* g, double* s) {
+    return esrnn_trainer_get_per_series(t, 0, static_cast<int64_t>(t->tr->series_count()), a, g, s);
+}
+
 esrnn_status esrnn_nccl_unique_id(uint8_t*) {
     g_create_err = "reference shim: no NCCL";
     return ESRNN_NCCL_ERROR;

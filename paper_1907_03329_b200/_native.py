@@ -19,7 +19,7 @@ from . import errors as E
 MAX_BLOCKS = 8
 MAX_LAYERS = 16
 NUM_CATEGORIES = 6
-FP32, FP64 = 0, 1
+FP64, FP32 = 0, 1
 BATCH_GRADS, BATCH_UPDATE = 1, 2
 
 PKG_DIR = Path(__file__).resolve().parent
@@ -60,8 +60,12 @@ class TrainCfg(C.Structure):
     ]
 
 
-class Dist(C.Structure):
-    _fields_ = [("rank", C.c_int32), ("world_size", C.c_int32), ("nccl_unique_id", C.c_uint8 * 128)]
+class Dist(C.Structure):  # esrnn_dist (ABI 2)
+    _fields_ = [("rank", C.c_int32), ("world_size", C.c_int32), ("nccl_unique_id", C.c_uint8 * 128),
+                ("flags", C.c_int32), ("group", C.c_void_p)]
+
+
+DIST_FORCE_COLLECTIVE = 1
 
 
 class ParamInfo(C.Structure):
@@ -142,6 +146,10 @@ class NativeApi:
         L.esrnn_trainer_profile_kernels.argtypes = [_vp, C.c_int32]
         L.esrnn_trainer_kernel_times.argtypes = [_vp, _dp, C.POINTER(C.c_int64)]
         L.esrnn_nccl_unique_id.argtypes = [C.POINTER(C.c_uint8)]
+        L.esrnn_group_create.argtypes = [C.c_int32, C.POINTER(_vp)]
+        L.esrnn_group_destroy.argtypes = [_vp]
+        L.esrnn_group_destroy.restype = None
+        L.esrnn_trainer_gather_per_series.argtypes = [_vp, _dp, _dp, _dp]
         L.esrnn_release_cached_memory.argtypes = []
         L.esrnn_make_synthetic.argtypes = [C.c_uint64, C.c_int64, C.c_int32, C.c_int32, C.c_double, _dp, _ip]
         for fn in ("esrnn_trainer_create", "esrnn_trainer_shard", "esrnn_trainer_param_count",
@@ -151,7 +159,7 @@ class NativeApi:
                    "esrnn_trainer_get_train_state", "esrnn_trainer_set_train_state", "esrnn_trainer_forward_stack",
                    "esrnn_trainer_hw_state", "esrnn_trainer_last_device_ms", "esrnn_trainer_last_epoch_windows", "esrnn_trainer_kernel_launches",
                    "esrnn_trainer_profile_kernels", "esrnn_trainer_kernel_times", "esrnn_nccl_unique_id", "esrnn_make_synthetic",
-                   "esrnn_release_cached_memory"):
+                   "esrnn_release_cached_memory", "esrnn_group_create", "esrnn_trainer_gather_per_series"):
             getattr(L, fn).restype = C.c_int
 
     @property
@@ -175,6 +183,10 @@ class NativeApi:
         """Return the engine's cached device / pinned blocks and epoch graphs to CUDA."""
         self.check(self.lib.esrnn_release_cached_memory())
 
+    def group(self, world_size: int) -> "Group":
+        """An in-process rank group (esrnn_group_create) for `world_size` sharded trainers."""
+        return Group(self, world_size)
+
     def nccl_unique_id(self) -> bytes:
         buf = (C.c_uint8 * 128)()
         self.check(self.lib.esrnn_nccl_unique_id(buf))
@@ -190,3 +202,25 @@ def product_api() -> NativeApi:
     if _PRODUCT is None:
         _PRODUCT = NativeApi(os.environ.get("ESRNN_B200_LIB", PRODUCT_LIB))
     return _PRODUCT
+
+
+class Group:
+    """esrnn_group: W series-sharded trainers in one process (one host thread each), whose
+    per-step collective is the engine's fused in-process reduce kernel instead of NCCL."""
+
+    def __init__(self, api: NativeApi, world_size: int):
+        self.api, self.world_size = api, world_size
+        h = C.c_void_p()
+        api.check(api.lib.esrnn_group_create(world_size, C.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if self.handle:
+            self.api.lib.esrnn_group_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -3,9 +3,12 @@
 
 The reference stores the profile shape, every named network array and the raw per-series
 parameters, but neither Adam state nor the trainer RNG (checkpoint.hpp:37-46), so training
-cannot resume exactly.  Files written here keep the v1 layout byte for
-byte in those fields -- the reference's load_checkpoint ignores unknown keys, so it still
-reads them -- and add:
+cannot resume exactly.  Files written here hold the same v1 fields as
+the reference's save_checkpoint, with the same values (doubles round-trip exactly) and the
+same key order (nlohmann::json objects are key-sorted, so keys are written sorted); the
+reference's load_checkpoint ignores unknown keys, so it still reads them.  Non-finite
+parameters are rejected (nlohmann would write them as null, which its own loader refuses).
+They add:
 
     "training_state": {"net_step": int, "rng": "<std::mt19937_64 text>", "epochs": int,
                        "adam": {name: {"m": [...], "v": [...]}},            # for_each_param names
@@ -42,22 +45,38 @@ class Checkpoint:  # checkpoint.hpp:37-46 (+ training_state)
     epochs: int = 0
 
 
-def snapshot(trainer: Trainer, with_training_state: bool = True, epochs: int = 0) -> Checkpoint:  # :48-62
+def snapshot(trainer: Trainer, with_training_state: bool = True, epochs: int = 0, gather=None) -> Checkpoint:  # :48-62
+    """Checkpoint of `trainer`.  A series-sharded trainer holds only its own rows'
+    per-series parameters: they are gathered from their owners by the engine's collective
+    (esrnn_trainer_gather_per_series), so EVERY rank must call snapshot.  Its exact-resume
+    state additionally needs `gather`, an all-gather of Python objects over the ranks (e.g.
+    torch.distributed.all_gather_object wrapped as ``lambda obj: list_of_all_ranks_objs``)."""
     p = trainer.profile()
-    a, g, s = trainer.per_series_arrays()
-    ids = trainer.series_ids()[trainer.row_begin:trainer.row_end]
-    per = [(i, PerSeriesParams(float(a[k]), float(g[k]), s[k].copy())) for k, i in enumerate(ids)]
+    sharded = (trainer.row_begin, trainer.row_end) != (0, trainer.series_count())
+    ids_all = trainer.series_ids()
+    if sharded:
+        a, g, s = trainer.gather_per_series_arrays()
+    else:
+        a, g, s = trainer.per_series_arrays()
+    per = [(i, PerSeriesParams(float(a[k]), float(g[k]), s[k].copy())) for k, i in enumerate(ids_all)]
     ck = Checkpoint(p.frequency.name, p.seasonality_length, p.horizon, p.input_window, p.hidden_size,
                     [list(b) for b in p.dilation_blocks], trainer.weights(), per, epochs=epochs)
     if with_training_state:
+        if sharded and gather is None:
+            raise E.CheckpointError("exact-resume state of a series-sharded trainer needs gather= (the per-series "
+                                    "Adam state of other ranks' series lives on those ranks)")
         ts = trainer.train_state()
+        ids = ids_all[trainer.row_begin:trainer.row_end]
+        ps = [{"id": i, "steps": int(ts.ps_steps[k]), "m": ts.ps_m[k].tolist(), "v": ts.ps_v[k].tolist()}
+              for k, i in enumerate(ids)]
+        if sharded:
+            parts = sorted(gather((trainer.row_begin, ps)), key=lambda x: x[0])
+            ps = [e for _, part in parts for e in part]
         adam = {}
         for n, r, c, o in trainer.param_layout:
             adam[n] = {"m": ts.adam_m[o:o + r * c].tolist(), "v": ts.adam_v[o:o + r * c].tolist()}
-        ck.training_state = {
-            "net_step": ts.net_step, "rng": ts.rng, "epochs": epochs, "adam": adam,
-            "per_series": [{"id": i, "steps": int(ts.ps_steps[k]), "m": ts.ps_m[k].tolist(),
-                            "v": ts.ps_v[k].tolist()} for k, i in enumerate(ids)]}
+        ck.training_state = {"net_step": ts.net_step, "rng": ts.rng, "epochs": epochs, "adam": adam,
+                             "per_series": ps}
     return ck
 
 
@@ -72,8 +91,12 @@ def save_checkpoint(path: str, ck: Checkpoint) -> None:  # checkpoint.hpp:64-88
     if ck.training_state is not None:
         j["training_state"] = ck.training_state
     try:
+        text = json.dumps(j, indent="\t", sort_keys=True, allow_nan=False)  # repr-exact doubles, sorted keys
+    except ValueError as e:
+        raise E.CheckpointError("checkpoint holds non-finite parameters") from e
+    try:
         with open(path, "w") as f:
-            json.dump(j, f, indent="\t")  # repr-exact doubles, like nlohmann's dump
+            f.write(text)
             f.write("\n")
     except OSError as e:
         raise E.Error(f'cannot write checkpoint "{path}"') from e

@@ -85,13 +85,18 @@ struct StateDev {
     // scratch
     Real* lv;               // [T][kcap]
     Real* se;               // [T+S][kcap]
-    Real* contrib;          // [Bcap][cwp] ES adjoint contributions per window, in slot-major
+    double* contrib;        // [Bcap][cwp] ES adjoint contributions per window, in slot-major
                             // CSR order: [0,I) input seasonalities, [I,I+O) target
-                            // seasonalities, [I+O] anchor level, [I+O+1] the anchor
+                            // seasonalities, [I+O] anchor level, [I+O+1] the anchor.
+                            // fp64 in both precisions: the ES adjoint (these contributions
+                            // and K3's reverse scan) runs in double, see finish.cuh
     int cwp;                // row stride of contrib (multiple of 4 >= I+O+2)
     Real* rowstore;         // [Bcap][rs_ld] per-window K3 operands (NetLayout rs_*)
     double* loss_part;      // [tiles]
-    Real* gbuf;             // [P_pad + 2]  (comm buffer: grads | ps sq-norm | loss sum)
+    Real* gbuf;             // [P_pad] shared-network gradients (the all-reduced buffer, sharded)
+    double* gtail;          // [4] step partials reduced with gbuf: per-series sq-norm, loss sum,
+                            // error flag (1 if this rank's error word is set), 0
+    long long* coll_seq;    // in-process group collective: calls completed (collective.cuh)
     Real* psg;              // [kcap][2+S]
     double* es_sq_part;     // [es blocks]
     double* red_sq_part;    // [weight-gradient tiles]
@@ -105,7 +110,8 @@ struct StateDev {
     const double* bc;       // [2 * bc_n] Adam bias corrections {1 - 0.9^t, 1 - 0.999^t} by step t,
                             // host std::pow like trainer.hpp:617-620 / :640-641
     long long bc_n;         // table length; both corrections are exactly 1.0 from t = bc_n on
-    int* err;               // [2] code, min t
+    int* err;               // [4] code, min t, any-rank error (sharded: set from the reduced
+                            // flag; Adam is skipped on every rank), 0
     // optional dumps (run_batch): WindowBatch matrices, step-local window order
     Real* d_inputs;
     Real* d_targets;
@@ -114,7 +120,13 @@ struct StateDev {
     double tau, lr_net, lr_ps, clip;
     int has_clip, attach;
     long long* dbg_clk;     // optional phase timestamps (ESRNN_DEBUG_CLOCKS), block 0 thread 0
+    long long* spans;       // optional in-graph kernel spans [step][kSpanKinds][2]: earliest
+                            // CTA start (after its dependency wait), latest CTA end, global
+                            // timer ns (esrnn_trainer_profile_kernels(t, 2))
 };
+
+// span kinds (the ABI's kernel classes: tile 1, finish 2, adam 4, finalize/group 5)
+enum SpanKind { kSpanTile = 0, kSpanFinish = 1, kSpanAdam = 2, kSpanReduce = 3, kSpanKinds = 4 };
 
 // Adam bias corrections of step t (StateDev::bc; exactly 1.0 past the table)
 template <typename Real>
@@ -126,7 +138,7 @@ __device__ __forceinline__ double bias_c2(const StateDev<Real>& st, long long t)
     return t < st.bc_n ? st.bc[2 * t + 1] : 1.0;
 }
 
-enum ErrCode { kErrNone = 0, kErrTrainLevel = 1, kErrObs = 2, kErrFcLevel = 3, kErrSeas = 4 };
+enum ErrCode { kErrNone = 0, kErrTrainLevel = 1, kErrObs = 2, kErrFcLevel = 3, kErrSeas = 4, kErrPeer = 5 };
 
 __device__ __forceinline__ void flag_error(int* err, int code, int t) {
     atomicMin(err + 1, t);
@@ -189,6 +201,18 @@ __device__ __forceinline__ long long gtimer() {
     do {                                                                            \
         if ((st).dbg_clk && (step) == 5 && threadIdx.x == 0)                        \
             atomicMax(reinterpret_cast<long long*>((st).dbg_clk) + 100 + (i), gtimer()); \
+    } while (0)
+
+// in-graph kernel spans: one atomic per CTA at its start (after pdl_wait) and at its end
+#define SPAN_BEGIN(st, step, kind)                                                              \
+    do {                                                                                        \
+        if ((st).spans && threadIdx.x == 0)                                                     \
+            atomicMin((st).spans + ((long long)(step) * kSpanKinds + (kind)) * 2, gtimer());    \
+    } while (0)
+#define SPAN_END(st, step, kind)                                                                \
+    do {                                                                                        \
+        if ((st).spans && threadIdx.x == 0)                                                     \
+            atomicMax((st).spans + ((long long)(step) * kSpanKinds + (kind)) * 2 + 1, gtimer()); \
     } while (0)
 
 #define DBG_CLK(st, i)                                                              \

@@ -33,6 +33,7 @@
 #include <vector>
 
 #include "esrnn_b200.h"
+#include "collective.cuh"
 #include "finish.cuh"
 #include "seqstack.cuh"
 #include "scan.cuh"
@@ -122,10 +123,100 @@ struct DevPlan {
     }
 };
 
+// In-process rank group (esrnn_group_create): W trainers in one process, one host thread
+// each, exchanging the step's partials through k_group_reduce's device slots (collective.cuh)
+// and the per-call host results (validate / evaluate totals, per-series gathers) through a
+// host barrier.  Device slots are allocated by the first rank to need them, on its device;
+// ranks on other devices reach them through peer access.
+struct LocalGroupImpl {
+    int W = 0;
+    std::mutex mu;
+    std::condition_variable cv;
+    int refs = 0;              // trainers alive in the group
+    std::vector<char> joined;  // a group serves one set of W trainers: each rank joins once
+    bool orphaned = false;     // esrnn_group_destroy called while trainers were alive
+    // device exchange (k_group_reduce)
+    int dev = -1;
+    long long stride = 0;
+    unsigned char* slots = nullptr;
+    unsigned long long* done = nullptr;
+    unsigned* ctr = nullptr;
+    // host exchange
+    long long gen = 0;
+    int arrived = 0;
+    std::vector<std::vector<unsigned char>> deposit, result;
+
+    ~LocalGroupImpl() {
+        if (dev >= 0) {
+            int d0 = 0;
+            cudaGetDevice(&d0);
+            cudaSetDevice(dev);
+            cudaFree(slots);
+            cudaFree(done);
+            cudaFree(ctr);
+            cudaSetDevice(d0);
+        }
+    }
+    // every rank deposits `n` bytes; returns all ranks' deposits, rank-major (rank order)
+    std::vector<unsigned char> exchange(int rank, const void* data, size_t n) {
+        std::unique_lock<std::mutex> lk(mu);
+        deposit[rank].assign(static_cast<const unsigned char*>(data), static_cast<const unsigned char*>(data) + n);
+        const long long my_gen = gen;
+        if (++arrived == W) {
+            std::vector<unsigned char> all;
+            for (auto& d : deposit) all.insert(all.end(), d.begin(), d.end());
+            result.assign(1, std::move(all));
+            arrived = 0;
+            ++gen;
+            cv.notify_all();
+        } else if (!cv.wait_for(lk, std::chrono::seconds(120), [&] { return gen != my_gen; })) {
+            --arrived;
+            raise(ESRNN_NCCL_ERROR, "group exchange: a rank did not arrive within 120 s");
+        }
+        return result[0];
+    }
+    // device slots for `bytes` per rank (first caller allocates; the configuration is shared)
+    void ensure_device(int device, long long bytes) {
+        std::lock_guard<std::mutex> lk(mu);
+        const long long need = (bytes + 255) / 256 * 256;
+        if (dev >= 0) {
+            if (need > stride) raise(ESRNN_CONFIG_ERROR, "group: ranks differ in configuration");
+            if (device != dev) {
+                int ok = 0;
+                CUDA_OK(cudaDeviceCanAccessPeer(&ok, device, dev));
+                if (!ok) raise(ESRNN_CUDA_ERROR, "group: device %d cannot access device %d", device, dev);
+                const cudaError_t st = cudaDeviceEnablePeerAccess(dev, 0);
+                if (st != cudaSuccess && st != cudaErrorPeerAccessAlreadyEnabled) CUDA_OK(st);
+                cudaGetLastError();
+            }
+            return;
+        }
+        dev = device;
+        stride = need;
+        CUDA_OK(cudaMalloc(&slots, 2 * static_cast<size_t>(W) * stride));
+        CUDA_OK(cudaMalloc(&done, sizeof(unsigned long long) * W));
+        CUDA_OK(cudaMalloc(&ctr, sizeof(unsigned) * 2 * W));
+        CUDA_OK(cudaMemset(done, 0, sizeof(unsigned long long) * W));
+        CUDA_OK(cudaMemset(ctr, 0, sizeof(unsigned) * 2 * W));
+        CUDA_OK(cudaDeviceSynchronize());
+    }
+};
+
+void release_group(LocalGroupImpl* g) {
+    bool del = false;
+    {
+        std::lock_guard<std::mutex> lk(g->mu);
+        del = --g->refs == 0 && g->orphaned;
+    }
+    if (del) delete g;
+}
+
 constexpr int kRows = kR;         // windows per K2 tile
 constexpr int64_t kBcSteps = 40960;  // Adam bias-correction table length (bc_table)
 
 }  // namespace
+
+struct esrnn_group : LocalGroupImpl {};
 
 struct esrnn_trainer {
     // configuration (data.hpp:60-118, trainer.hpp:22-44)
@@ -152,7 +243,12 @@ struct esrnn_trainer {
 
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // series-sharded data parallelism: the step's partials are all-reduced
+    // through NCCL (one process per GPU) or through an in-process group (esrnn_group_create)
     ncclComm_t comm = nullptr;
+    LocalGroupImpl* group = nullptr;
+    bool sharded = false;     // the collective step runs (world > 1, or forced at world 1)
+    int group_ctas = 0;       // k_group_reduce grid
 
     // device state (type-erased: Real = float or double, chosen by cfg.precision)
     DBuf<unsigned char> vals, vrm, ps, ps_m, ps_v, theta, mW, vW;
@@ -161,7 +257,8 @@ struct esrnn_trainer {
     DBuf<int> ps_steps;
     DBuf<unsigned char> lv, se, contrib, rowstore, gbuf, psg, d_inputs, d_targets, d_seas, d_levels;
     DBuf<unsigned char> fX, fL, fS, dump_lv, dump_se;
-    DBuf<double> loss_part, es_sq_part, red_sq_part, scal, loss_hist, f_out, f_smape, f_score, smape_sum;
+    DBuf<double> loss_part, es_sq_part, red_sq_part, scal, loss_hist, f_out, f_smape, f_score, smape_sum, gtail;
+    DBuf<long long> coll_seq;
     DBuf<unsigned int> done_ctr, gtile_ctr;
     DBuf<unsigned char> gpart;
     int gsplit = 1;  // K3 weight-gradient row parts per output tile (large steps)
@@ -188,8 +285,11 @@ struct esrnn_trainer {
     std::shared_ptr<GraphExec> graph;  // epoch graph (shared with the process-wide cache)
     std::string graph_key;
 
-    // per-kernel event timing (esrnn_trainer_profile_kernels)
+    // per-kernel event timing (esrnn_trainer_profile_kernels(t, 1)); in-graph global-timer
+    // spans of every step's kernels (esrnn_trainer_profile_kernels(t, 2))
     bool profiling = false;
+    bool span_mode = false;
+    DBuf<long long> spans;
     std::vector<cudaEvent_t> prof_ev;
     std::vector<int> prof_cls;
     double prof_ms[ESRNN_KERNEL_CLASSES] = {};
@@ -237,7 +337,8 @@ struct esrnn_trainer {
         };
         add(vals, vrm, ps, ps_m, ps_v, theta, mW, vW, cat, ps_steps, lv, se, contrib, rowstore, gbuf, psg, d_inputs,
             d_targets, d_seas, d_levels, fX, fL, fS, dump_lv, dump_se, loss_part, es_sq_part, red_sq_part, scal,
-            loss_hist, f_out, f_smape, f_score, smape_sum, done_ctr, gtile_ctr, gpart, net_step, dbg_clk, errw);
+            loss_hist, f_out, f_smape, f_score, smape_sum, done_ctr, gtile_ctr, gpart, net_step, dbg_clk, errw, gtail,
+            coll_seq, spans);
         for (DevPlan* d : {&epoch_plan, &batch_plan})
             add(d->w_row, d->w_anchor, d->w_slot, d->w_first, d->step_win_off, d->step_slot_off, d->slot_row,
                 d->slot_win_off, d->slot_win, d->w_csr, d->csr_anchor, d->step_M, d->mask);
@@ -256,8 +357,9 @@ struct esrnn_trainer {
         plan_pool_put(std::move(next_plan));
         if (stream) cudaStreamSynchronize(stream);  // buffers go back to the block cache below
         release_buffers();
-        graph.reset();
+        graph.reset();  // sharded trainers' graphs are never in the process cache
         if (comm) ncclCommDestroy(comm);
+        if (group) release_group(group);
         if (stream) stream_put(stream, ev0, ev1);  // idle: synchronised above
     }
 
@@ -280,11 +382,13 @@ struct esrnn_trainer {
         s.vW = reinterpret_cast<Real*>(vW.p);
         s.lv = reinterpret_cast<Real*>(lv.p);
         s.se = reinterpret_cast<Real*>(se.p);
-        s.contrib = reinterpret_cast<Real*>(contrib.p);
+        s.contrib = reinterpret_cast<double*>(contrib.p);
         s.cwp = (I + O + 2 + 3) & ~3;
         s.rowstore = reinterpret_cast<Real*>(rowstore.p);
         s.loss_part = loss_part.p;
         s.gbuf = reinterpret_cast<Real*>(gbuf.p);
+        s.gtail = gtail.p;
+        s.coll_seq = coll_seq.p;
         s.psg = reinterpret_cast<Real*>(psg.p);
         s.es_sq_part = es_sq_part.p;
         s.red_sq_part = red_sq_part.p;
@@ -309,6 +413,7 @@ struct esrnn_trainer {
         s.has_clip = cfg.has_gradient_clip ? 1 : 0;
         s.attach = cfg.attach_es_state ? 1 : 0;
         s.dbg_clk = dbg_clk.p;
+        s.spans = span_mode ? spans.p : nullptr;
         return s;
     }
 };
@@ -371,29 +476,34 @@ void validate_config(const esrnn_profile& p, const esrnn_train_config& c) {
 // The error word's copy, enqueued with a call's results so one synchronisation covers both;
 // check_device_error() reads it after that synchronisation.
 void enqueue_error_read(Eng* e) {
-    e->pin_err.reserve(2);
-    CUDA_OK(cudaMemcpyAsync(e->pin_err.p, e->errw.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, e->stream));
+    e->pin_err.reserve(4);
+    CUDA_OK(cudaMemcpyAsync(e->pin_err.p, e->errw.p, 4 * sizeof(int), cudaMemcpyDeviceToHost, e->stream));
 }
 
 void raise_device_error(Eng* e, const int* h);
 
+// The error word after a call: this rank's own error (code, first t), else -- sharded -- the
+// any-rank flag the reduced step buffers carried (every rank raises, none updated).
 void check_device_error(Eng* e) {
-    if (e->pin_err.p[0] != 0) raise_device_error(e, e->pin_err.p);
+    if (e->pin_err.p[0] != 0 || e->pin_err.p[2] != 0) raise_device_error(e, e->pin_err.p);
 }
 
 void throw_device_error(Eng* e) {
-    int h[2];
+    int h[4];
     CUDA_OK(cudaMemcpyAsync(h, e->errw.p, sizeof h, cudaMemcpyDeviceToHost, e->stream));
     CUDA_OK(cudaStreamSynchronize(e->stream));
-    if (h[0] != 0) raise_device_error(e, h);
+    if (h[0] != 0 || h[2] != 0) raise_device_error(e, h);
 }
 
 void raise_device_error(Eng* e, const int* hp) {
-    const int h[2] = {hp[0], hp[1]};
-    const int reset[2] = {0, INT_MAX};
+    const int h[3] = {hp[0], hp[1], hp[2]};
+    const int reset[4] = {0, INT_MAX, 0, 0};
     CUDA_OK(cudaMemcpyAsync(e->errw.p, reset, sizeof reset, cudaMemcpyHostToDevice, e->stream));
     CUDA_OK(cudaStreamSynchronize(e->stream));
+    if (h[0] == 0)
+        raise(ESRNN_NUMERIC_DOMAIN_ERROR, "hybrid_primer_tape: non-positive level (raised on another rank of the group)");
     switch (h[0]) {
+        case kErrPeer: raise(ESRNN_NCCL_ERROR, "group collective: rank %d did not arrive (timeout)", h[1]);
         case kErrTrainLevel: raise(ESRNN_NUMERIC_DOMAIN_ERROR, "hybrid_primer_tape: non-positive level at t=%d", h[1]);
         case kErrObs: raise(ESRNN_NUMERIC_DOMAIN_ERROR, "hybrid_primer: non-positive observation at t=%d", h[1]);
         case kErrFcLevel: raise(ESRNN_NUMERIC_DOMAIN_ERROR, "hybrid_primer: non-positive level at t=%d", h[1]);
@@ -613,7 +723,7 @@ void ensure_capacity(Eng* e, int B) {
     }
     e->lv.alloc(r * T * kc);
     e->se.alloc(r * (T + S) * kc);
-    e->contrib.alloc(r * static_cast<size_t>(B) * ((I + O + 2 + 3) & ~3));
+    e->contrib.alloc(sizeof(double) * static_cast<size_t>(B) * ((I + O + 2 + 3) & ~3));
     // row store: K2 writes every column of a live window's row; rows are read only by K3
     e->rowstore.alloc(r * static_cast<size_t>(e->tiles_cap * kRows) * e->lay.rs_ld);
     e->loss_part.alloc(e->tiles_cap);
@@ -782,13 +892,16 @@ int stack_threads(const NetLayout& lay) { return tile_threads(lay); }
 
 template <typename Real>
 size_t finish_smem(const NetLayout& lay) {
-    // lb, sb, forward l and s columns [.][bd] + one staged observation row per slot
-    // + one chunk of staged contribution rows
+    // ES blocks: level / seasonality adjoints [bd][T|1], [bd][(T+S)|1] (double), forward l and
+    // s columns [T][bd] + one staged observation row per slot (Real), one chunk of staged
+    // contribution rows (double)
     const size_t cwp = (lay.I + lay.O + 2 + 3) & ~3;
-    const size_t es = (static_cast<size_t>(4 * lay.T + lay.S + 2) + row_pad<Real>(lay.T)) * kEsSlotsPerBlock +
-                      kEsChunk * cwp;
-    const size_t gemm = static_cast<size_t>(kGBuf * kGChunk) * (kGq + kGk) + (kFinishThreads / 32) * 32 * 6;
-    return sizeof(Real) * std::max(es, gemm);
+    const size_t bd = kEsSlotsPerBlock;
+    const size_t es = sizeof(double) * bd * (static_cast<size_t>(lay.T | 1) + static_cast<size_t>((lay.T + lay.S) | 1)) +
+                      sizeof(Real) * bd * (2 * static_cast<size_t>(lay.T) + row_pad<Real>(lay.T)) +
+                      sizeof(double) * kEsChunk * cwp;
+    const size_t gemm = sizeof(Real) * (static_cast<size_t>(kGBuf * kGChunk) * (kGq + kGk) + (kFinishThreads / 32) * 32 * 6);
+    return std::max(es, gemm);
 }
 
 // The tile kernel's scans are specialised for the M4 seasonalities (S = 1, 4, 12: seasonal
@@ -913,7 +1026,7 @@ void launch_step(Eng* e, const PlanDev& pv, int s, bool grads, bool update, Stat
     }
     e->launches += 1;
     if (!grads) return;
-    const bool sharded = e->world > 1 && e->comm != nullptr;
+    const bool sharded = e->sharded;
     {
         KS k(e, 2);
         // bit 0: a last CTA finalises the step scalars (single GPU, no update: K4 does not
@@ -923,9 +1036,20 @@ void launch_step(Eng* e, const PlanDev& pv, int s, bool grads, bool update, Stat
         launch_finish<Real>(e, st, pv, s, fin, true);
     }
     e->launches += 1;
-    if (sharded) {
-        NCCL_OK(ncclAllReduce(st.gbuf, st.gbuf, lay.P_pad + 2, e->fp64 ? ncclDouble : ncclFloat, ncclSum, e->comm,
+    if (sharded && e->group) {
+        // in-process group: one fused kernel -- exchange, rank-ordered sum, finalise
+        KS k(e, 5);
+        GroupDev gd{e->group->slots, e->group->done, e->group->ctr, e->group->stride, e->world, e->rank};
+        launch_k(e, false, k_group_reduce<Real>, e->group_ctas, 256, 0, st, pv, lay, s, update ? 1 : 0, gd);
+        e->launches += 1;
+    } else if (sharded) {
+        // NCCL: the gradients (Real) and the step tail (double: per-series squared norm, loss,
+        // error flag) in one group call, then the finalisation
+        NCCL_OK(ncclGroupStart());
+        NCCL_OK(ncclAllReduce(st.gbuf, st.gbuf, lay.P_pad, e->fp64 ? ncclDouble : ncclFloat, ncclSum, e->comm,
                               e->stream));
+        NCCL_OK(ncclAllReduce(st.gtail, st.gtail, 4, ncclDouble, ncclSum, e->comm, e->stream));
+        NCCL_OK(ncclGroupEnd());
         KS k(e, 5);
         const int rb = static_cast<int>((lay.P_pad + 255) / 256);
         k_finalize<Real><<<rb, 256, 0, e->stream>>>(st, pv, lay, s, update ? 1 : 0);
@@ -957,6 +1081,8 @@ __global__ void k_zero_spans(ZeroSpans z) {
     if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
         z.errw[0] = 0;
         z.errw[1] = INT_MAX;
+        z.errw[2] = 0;
+        z.errw[3] = 0;
     }
     const int k = blockIdx.y;
     if (k >= z.count) return;
@@ -982,10 +1108,13 @@ void alloc_state(Eng* e) {
     e->theta.alloc(r * e->lay.P_pad);
     e->mW.alloc(r * e->lay.P_pad);
     e->vW.alloc(r * e->lay.P_pad);
-    e->gbuf.alloc(r * (e->lay.P_pad + 2));  // zeroed below: padding slots of the compact vector are never written
+    e->gbuf.alloc(r * e->lay.P_pad);  // zeroed below: padding slots of the compact vector are never written
+    e->gtail.alloc(4);
+    e->coll_seq.alloc(1);
     e->red_blocks = e->lay.mat_blk0[e->lay.nmat];
-    e->red_sq_part.alloc(std::max<int>(e->red_blocks, static_cast<int>((e->lay.P_pad + 255) / 256)));
+    e->red_sq_part.alloc(std::max<int>(std::max(e->red_blocks, 16), static_cast<int>((e->lay.P_pad + 255) / 256)));
     e->scal.alloc(4);
+    e->group_ctas = static_cast<int>(std::min<int64_t>(16, std::max<int64_t>(1, (e->lay.P_pad + 2047) / 2048)));
     {
         // one loss slot per training step of an epoch (make_batches, trainer.hpp:82-102)
         const int64_t nw = static_cast<int64_t>(e->N_global) * std::max(0, e->T - e->O - e->I + 1);
@@ -995,7 +1124,7 @@ void alloc_state(Eng* e) {
     }
     e->done_ctr.alloc(2);
     e->net_step.alloc(1);
-    e->errw.alloc(2);
+    e->errw.alloc(4);
     if (std::getenv("ESRNN_DEBUG_CLOCKS")) {
         e->dbg_clk.alloc(128);
         e->dbg_clk.zero(e->stream);
@@ -1006,6 +1135,8 @@ void alloc_state(Eng* e) {
         z.n[z.count++] = bytes;
     };
     add(e->gbuf.p, e->gbuf.n);
+    add(e->gtail.p, sizeof(double) * e->gtail.n);
+    add(e->coll_seq.p, sizeof(long long) * e->coll_seq.n);
     for (auto* b : {&e->ps, &e->ps_m, &e->ps_v, &e->mW, &e->vW}) add(b->p, b->n);
     add(e->ps_steps.p, sizeof(int) * e->ps_steps.n);
     add(e->done_ctr.p, sizeof(unsigned int) * e->done_ctr.n);
@@ -1255,6 +1386,15 @@ double train_epoch_impl(Eng* e) {
         e->steps_cap = steps;
     }
     const PlanDev pv = e->epoch_plan.view(false);
+    if (e->span_mode) {
+        // seed [step][kind] = {earliest start: LLONG_MAX, latest end: 0}
+        const size_t n = static_cast<size_t>(steps) * kSpanKinds * 2;
+        if (e->spans.n < n) e->spans.alloc(n);
+        std::vector<long long> seed(n);
+        for (size_t i = 0; i < n; ++i) seed[i] = (i & 1) ? 0 : LLONG_MAX;
+        CUDA_OK(cudaMemcpyAsync(e->spans.p, seed.data(), sizeof(long long) * n, cudaMemcpyHostToDevice, e->stream));
+        CUDA_OK(cudaStreamSynchronize(e->stream));
+    }
     StateDev<Real> st = e->state<Real>();
     const bool use_graph = e->cfg.use_graphs >= 0 && !e->profiling;
     if (e->dbg_clk.p) {
@@ -1269,13 +1409,15 @@ double train_epoch_impl(Eng* e) {
         key_append(key, st);
         key_append(key, pv);
         key_append(key, e->lay);
-        const long long dims[8] = {steps, e->tiles_cap, e->es_blocks, e->red_blocks, e->kcap, e->S, e->rank,
-                                   e->world};
+        const long long dims[11] = {steps, e->tiles_cap, e->es_blocks, e->red_blocks, e->kcap, e->S, e->rank,
+                                    e->world, e->gsplit, e->fp64 ? 8 : 4, e->sharded ? 1 : 0};
         key_append(key, dims);
-        key_append(key, e->comm);
         key_append(key, e->stream == nullptr);
+        // A sharded graph captures this trainer's communicator (NCCL) or group slots: it is
+        // kept by the trainer only, never shared through the process-wide cache, so it cannot
+        // outlive the communicator or be replayed by a later trainer that reuses its address.
         if (!e->graph || e->graph_key != key) {
-            e->graph = graph_cache().find(key);
+            e->graph = e->sharded ? nullptr : graph_cache().find(key);
             if (!e->graph) {
                 auto ge = std::make_shared<GraphExec>();
                 cudaGraph_t g;
@@ -1292,7 +1434,7 @@ double train_epoch_impl(Eng* e) {
                 CUDA_OK(cudaGraphDestroy(g));
                 ge->launch_nodes = static_cast<int>(e->launches - before);
                 e->launches = before;
-                graph_cache().insert(key, ge);
+                if (!e->sharded) graph_cache().insert(key, ge);
                 e->graph = ge;
             }
             e->graph_key = key;
@@ -1354,6 +1496,21 @@ double train_epoch_impl(Eng* e) {
                      sp[7] - sp[0], sp[8] - sp[0], sp[9] - sp[0]);
         std::fprintf(stderr, "[esrnn dbg] step-5 K3 ES blocks end %lld, GEMM blocks end %lld\n", sp[10] - sp[0],
                      sp[11] - sp[0]);
+    }
+    if (e->span_mode) {
+        // per kind: sum over steps of (latest CTA end - earliest CTA start)
+        const size_t n = static_cast<size_t>(steps) * kSpanKinds * 2;
+        std::vector<long long> sp(n);
+        CUDA_OK(cudaMemcpy(sp.data(), e->spans.p, sizeof(long long) * n, cudaMemcpyDeviceToHost));
+        static const int cls[kSpanKinds] = {1, 2, 4, 5};
+        for (int s = 0; s < steps; ++s)
+            for (int k = 0; k < kSpanKinds; ++k) {
+                const long long a = sp[(static_cast<size_t>(s) * kSpanKinds + k) * 2];
+                const long long b = sp[(static_cast<size_t>(s) * kSpanKinds + k) * 2 + 1];
+                if (a == LLONG_MAX || b < a) continue;
+                e->prof_ms[cls[k]] += (b - a) * 1e-6;
+                e->prof_n[cls[k]] += 1;
+            }
     }
     e->have_last = true;
     // trainer.hpp:236-242: acc += loss * count, in batch order
@@ -1426,16 +1583,16 @@ void run_batch_impl(Eng* e, int32_t B, const int32_t* rows, const int32_t* ancho
     throw_device_error(e);
     // loss: sum of tile partials (single GPU) or all-reduced sum (sharded) / M
     double lsum = 0.0;
-    if (grads && e->comm != nullptr) {
-        Real g2[2];
-        CUDA_OK(cudaMemcpy(g2, reinterpret_cast<Real*>(e->gbuf.p) + e->lay.P_pad, sizeof g2, cudaMemcpyDeviceToHost));
-        lsum = static_cast<double>(g2[1]);
+    if (grads && e->sharded) {
+        double g2[2];
+        CUDA_OK(cudaMemcpy(g2, e->gtail.p, sizeof g2, cudaMemcpyDeviceToHost));
+        lsum = g2[1];
     } else {
         const int nt = (Bl + kRows - 1) / kRows;
         std::vector<double> lp(nt);
         if (nt) CUDA_OK(cudaMemcpy(lp.data(), e->loss_part.p, sizeof(double) * nt, cudaMemcpyDeviceToHost));
         for (double v : lp) lsum += v;
-        if (e->comm != nullptr) raise(ESRNN_CONFIG_ERROR, "sharded batch_loss requires gradients (collective step)");
+        if (e->sharded) raise(ESRNN_CONFIG_ERROR, "sharded batch_loss requires gradients (collective step)");
     }
     if (loss) *loss = lsum / count;
     if (mask_count) *mask_count = count;
@@ -1486,6 +1643,44 @@ void launch_forecast_scan(Eng* e, int t_len, Real* X, Real* FL, Real* FS, Real* 
         case 12: go(k_forecast_scan<Real, 12>); break;
         default: go(k_forecast_scan<Real, 0>); break;
     }
+}
+
+// Host-level collectives of a sharded trainer (outside the step graphs): a sum of n doubles
+// in rank order, and an all-gather of equal-size byte blocks (rank-major).
+void allreduce_sum_host(Eng* e, double* v, int n) {
+    if (e->group) {
+        const std::vector<unsigned char> all = e->group->exchange(e->rank, v, sizeof(double) * n);
+        const double* a = reinterpret_cast<const double*>(all.data());
+        for (int i = 0; i < n; ++i) {
+            double s = 0.0;
+            for (int r = 0; r < e->world; ++r) s += a[static_cast<size_t>(r) * n + i];
+            v[i] = s;
+        }
+        return;
+    }
+    if (e->smape_sum.n < static_cast<size_t>(n)) e->smape_sum.alloc(n);
+    CUDA_OK(cudaMemcpy(e->smape_sum.p, v, sizeof(double) * n, cudaMemcpyHostToDevice));
+    NCCL_OK(ncclAllReduce(e->smape_sum.p, e->smape_sum.p, n, ncclDouble, ncclSum, e->comm, e->stream));
+    CUDA_OK(cudaMemcpyAsync(v, e->smape_sum.p, sizeof(double) * n, cudaMemcpyDeviceToHost, e->stream));
+    CUDA_OK(cudaStreamSynchronize(e->stream));
+}
+
+std::vector<double> allgather_host(Eng* e, const std::vector<double>& mine) {
+    if (e->group) {
+        const std::vector<unsigned char> all = e->group->exchange(e->rank, mine.data(), sizeof(double) * mine.size());
+        std::vector<double> out(all.size() / sizeof(double));
+        std::memcpy(out.data(), all.data(), all.size());
+        return out;
+    }
+    DBuf<double> d;
+    d.alloc(mine.size() * (e->world + 1));
+    double* recv = d.p + mine.size();
+    CUDA_OK(cudaMemcpy(d.p, mine.data(), sizeof(double) * mine.size(), cudaMemcpyHostToDevice));
+    NCCL_OK(ncclAllGather(d.p, recv, mine.size(), ncclDouble, e->comm, e->stream));
+    std::vector<double> out(mine.size() * e->world);
+    CUDA_OK(cudaMemcpyAsync(out.data(), recv, sizeof(double) * out.size(), cudaMemcpyDeviceToHost, e->stream));
+    CUDA_OK(cudaStreamSynchronize(e->stream));
+    return out;
 }
 
 struct ScoreOut {
@@ -1560,7 +1755,11 @@ void forecast_impl(Eng* e, int64_t drop_tail, double* out, int mode, const Score
     float ms = 0.f;
     CUDA_OK(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
     e->last_ms = ms;
-    check_device_error(e);
+    // sharded validate / evaluate: a rank's device error is raised only after the totals'
+    // collective, on every rank, so no peer waits in the collective for a rank that threw
+    const bool defer = mode != 0 && e->sharded;
+    int errw[4] = {e->pin_err.p[0], e->pin_err.p[1], e->pin_err.p[2], e->pin_err.p[3]};
+    if (!defer) check_device_error(e);
     if (out && N > 0) std::memcpy(out, pf, sizeof(double) * nfo);
     if (mode == 0) return;
     const double* sm = psm;
@@ -1581,12 +1780,14 @@ void forecast_impl(Eng* e, int64_t drop_tail, double* out, int mode, const Score
             if (!std::isnan(nm)) { tot[4] += nm; tot[5] += 1; }
         }
     }
-    if (e->comm != nullptr) {
-        if (e->smape_sum.n < 8) e->smape_sum.alloc(8);
-        CUDA_OK(cudaMemcpy(e->smape_sum.p, tot, sizeof tot, cudaMemcpyHostToDevice));
-        NCCL_OK(ncclAllReduce(e->smape_sum.p, e->smape_sum.p, 8, ncclDouble, ncclSum, e->comm, e->stream));
-        CUDA_OK(cudaMemcpyAsync(tot, e->smape_sum.p, sizeof tot, cudaMemcpyDeviceToHost, e->stream));
-        CUDA_OK(cudaStreamSynchronize(e->stream));
+    if (defer) {
+        tot[7] = errw[0] != 0 ? 1.0 : 0.0;
+        allreduce_sum_host(e, tot, 8);
+        if (errw[0] != 0) raise_device_error(e, errw);
+        if (tot[7] != 0.0) {
+            errw[0] = 0, errw[2] = 1;
+            raise_device_error(e, errw);
+        }
     }
     if (so.mean) *so.mean = tot[0] / static_cast<double>(e->N_global);
     if (so.totals)
@@ -1716,10 +1917,13 @@ esrnn_status esrnn_trainer_create(const esrnn_profile* profile, const esrnn_trai
         e->fp64 = cfg->precision == ESRNN_FP64;
         e->rsz = e->fp64 ? sizeof(double) : sizeof(float);
         e->N_global = static_cast<int>(n_series);
-        if (dist && dist->world_size > 1) {
+        const bool force = dist && (dist->flags & ESRNN_DIST_FORCE_COLLECTIVE) != 0;
+        if (dist && (dist->world_size > 1 || force)) {
             e->rank = dist->rank;
             e->world = dist->world_size;
-            if (e->rank < 0 || e->rank >= e->world) raise(ESRNN_CONFIG_ERROR, "dist: rank out of range");
+            if (e->world < 1 || e->rank < 0 || e->rank >= e->world) raise(ESRNN_CONFIG_ERROR, "dist: rank out of range");
+            if (dist->group && dist->group->W != e->world)
+                raise(ESRNN_CONFIG_ERROR, "dist: group of %d ranks, world_size %d", dist->group->W, e->world);
         }
         // contiguous row blocks
         e->row0 = static_cast<int>((static_cast<int64_t>(e->rank) * n_series) / e->world);
@@ -1803,16 +2007,28 @@ esrnn_status esrnn_trainer_create(const esrnn_profile* profile, const esrnn_trai
         CUDA_OK(cudaDeviceGetAttribute(&g_smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, cfg->device));
         stream_get(e->stream, e->ev0, e->ev1);
         c[nc++] = clk::now();
-        if (e->world > 1) {
-            // an id of 128 x 0xEE is the local-partials test mode: the shard runs its data
-            // path but skips the collective, so a test can sum per-rank partials itself
-            bool local_only = true;
-            for (int i = 0; i < 128; ++i) local_only = local_only && dist->nccl_unique_id[i] == 0xEE;
-            if (!local_only) {
-                ncclUniqueId id;
-                static_assert(sizeof(id.internal) == 128, "nccl id size");
-                std::memcpy(id.internal, dist->nccl_unique_id, 128);
-                NCCL_OK(ncclCommInitRank(&e->comm, e->world, id, e->rank));
+        if (e->world > 1 || force) {
+            if (dist->group) {
+                std::lock_guard<std::mutex> lk(dist->group->mu);
+                if (dist->group->joined.empty()) dist->group->joined.assign(dist->group->W, 0);
+                if (dist->group->joined[e->rank])
+                    raise(ESRNN_CONFIG_ERROR, "group: rank %d already joined (a group serves one set of trainers)", e->rank);
+                dist->group->joined[e->rank] = 1;
+                e->group = dist->group;
+                ++e->group->refs;
+                e->sharded = true;
+            } else {
+                // an id of 128 x 0xEE is the local-partials test mode: the shard runs its data
+                // path but skips the collective, so a test can sum per-rank partials itself
+                bool local_only = true;
+                for (int i = 0; i < 128; ++i) local_only = local_only && dist->nccl_unique_id[i] == 0xEE;
+                if (!local_only) {
+                    ncclUniqueId id;
+                    static_assert(sizeof(id.internal) == 128, "nccl id size");
+                    std::memcpy(id.internal, dist->nccl_unique_id, 128);
+                    NCCL_OK(ncclCommInitRank(&e->comm, e->world, id, e->rank));
+                    e->sharded = true;
+                }
             }
         }
 
@@ -1825,6 +2041,7 @@ esrnn_status esrnn_trainer_create(const esrnn_profile* profile, const esrnn_trai
             alloc_state<float>(e.get());
             upload_values<float>(e.get(), values, category);
         }
+        if (e->group) e->group->ensure_device(cfg->device, 32 + static_cast<long long>(e->rsz) * e->lay.P_pad);
         weights_ready.wait();
         convert_weights();
         c[nc++] = clk::now();
@@ -2143,7 +2360,8 @@ esrnn_status esrnn_trainer_kernel_launches(const esrnn_trainer* t, int64_t* n) {
 }
 
 esrnn_status esrnn_trainer_profile_kernels(esrnn_trainer* t, int32_t enable) {
-    t->profiling = enable != 0;
+    t->profiling = enable == 1;
+    t->span_mode = enable == 2;
     for (int i = 0; i < ESRNN_KERNEL_CLASSES; ++i) {
         t->prof_ms[i] = 0.0;
         t->prof_n[i] = 0;
@@ -2184,6 +2402,58 @@ esrnn_status esrnn_release_cached_memory(void) {
         c.dev.clear();
         c.host.clear();
         c.streams.clear();
+    });
+}
+
+esrnn_status esrnn_group_create(int32_t world_size, esrnn_group** out) {
+    *out = nullptr;
+    return guarded(g_create_err, [&] {
+        if (world_size < 1) raise(ESRNN_CONFIG_ERROR, "group: world_size must be >= 1");
+        esrnn_group* g = new esrnn_group();
+        g->W = world_size;
+        g->deposit.resize(world_size);
+        *out = g;
+    });
+}
+
+void esrnn_group_destroy(esrnn_group* g) {
+    if (!g) return;
+    bool del = false;
+    {
+        std::lock_guard<std::mutex> lk(g->mu);
+        g->orphaned = true;
+        del = g->refs == 0;
+    }
+    if (del) delete g;
+}
+
+esrnn_status esrnn_trainer_gather_per_series(esrnn_trainer* t, double* a, double* g, double* s) {
+    return guarded(t->err, [&] {
+        CUDA_OK(cudaSetDevice(t->cfg.device));
+        const int S = t->S, np = 2 + S;
+        // this rank's rows as [row][alpha, gamma, seas...], padded to the largest shard
+        const int64_t maxn = (static_cast<int64_t>(t->N_global) + t->world - 1) / t->world + 1;
+        std::vector<double> a0(t->N), g0(t->N), s0(static_cast<size_t>(t->N) * S);
+        ps_io(t, t->row0, t->N, a0.data(), g0.data(), s0.data(), true);
+        std::vector<double> mine(static_cast<size_t>(maxn) * np, 0.0);
+        for (int i = 0; i < t->N; ++i) {
+            mine[static_cast<size_t>(i) * np] = a0[i];
+            mine[static_cast<size_t>(i) * np + 1] = g0[i];
+            for (int j = 0; j < S; ++j) mine[static_cast<size_t>(i) * np + 2 + j] = s0[static_cast<size_t>(i) * S + j];
+        }
+        const std::vector<double> all = t->sharded ? allgather_host(t, mine) : mine;
+        const int W = t->sharded ? t->world : 1;
+        for (int r = 0; r < W; ++r) {
+            const int64_t b = t->sharded ? (static_cast<int64_t>(r) * t->N_global) / t->world : t->row0;
+            const int64_t e = t->sharded ? (static_cast<int64_t>(r + 1) * t->N_global) / t->world : t->row0 + t->N;
+            const double* src = all.data() + static_cast<size_t>(r) * maxn * np;
+            for (int64_t i = 0; i < e - b; ++i) {
+                if (a) a[b + i] = src[i * np];
+                if (g) g[b + i] = src[i * np + 1];
+                if (s)
+                    for (int j = 0; j < S; ++j) s[(b + i) * S + j] = src[i * np + 2 + j];
+            }
+        }
     });
 }
 

@@ -21,10 +21,11 @@ constexpr int kGChunk = 256;          // row-store rows staged per round
 constexpr int kGBuf = 3;              // staging ring depth (kGBuf - 1 chunks in flight)
 
 // clip scale (trainer.hpp:603-615), global Adam step and bias corrections (:617-620),
-// step loss (masked mean, autodiff.hpp:392)
+// step loss (masked mean, autodiff.hpp:392).  err_any: some rank's error word is set (the
+// reference throws before apply_updates): Adam's step does not advance anywhere.
 template <typename Real>
 __device__ void finalize_scalars(StateDev<Real>& st, const PlanDev& pl, int s, double sq, double loss_sum,
-                                 bool advance) {
+                                 bool advance, bool err_any) {
     double scale = 1.0;
     if (st.has_clip) {
         const double norm = sqrt(sq);
@@ -33,7 +34,8 @@ __device__ void finalize_scalars(StateDev<Real>& st, const PlanDev& pl, int s, d
     st.scal[0] = scale;
     st.scal[3] = loss_sum / pl.step_M[s];
     st.loss_hist[s] = loss_sum / pl.step_M[s];
-    if (advance && st.err[0] == 0) {  // only a step that applies updates advances Adam's t
+    if (err_any) st.err[2] = 1;
+    if (advance && !err_any) {  // only a step that applies updates advances Adam's t
         const long long step = ++(*st.net_step);
         st.scal[1] = bias_c1(st, step);
         st.scal[2] = bias_c2(st, step);
@@ -74,15 +76,18 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
             const int lane = tid & 31;                                         // slot lane (bd == 32)
             // window adjoints row-major per slot (odd strides: the per-slot reverse scan reads
             // them conflict-free; the per-window warp scatter writes consecutive words)
+            // The ES adjoint runs in double in both precisions (see the K2 contributions): the
+            // level and seasonality paths of a window's adjoint cancel almost exactly, so their
+            // accumulation and the reverse recursion must not round on their own
             const int ldl = T | 1, lds = (T + S) | 1;
-            Real* LB = reinterpret_cast<Real*>(smem_raw);                      // [bd][ldl] level adjoint
-            Real* SB = LB + bd * ldl;                                          // [bd][lds] seasonality adjoint
-            Real* LV = SB + bd * lds;                                          // [T][bd]   forward levels
+            double* LB = reinterpret_cast<double*>(smem_raw);                  // [bd][ldl] level adjoint
+            double* SB = LB + bd * ldl;                                        // [bd][lds] seasonality adjoint
+            Real* LV = reinterpret_cast<Real*>(SB + bd * lds);                 // [T][bd]   forward levels
             Real* SE = LV + T * bd;                                            // [T][bd]   forward seasonalities
             Real* YS = SE + T * bd;                                            // [bd][tp]  observation rows
-            Real* cbuf = YS + bd * tp;                                         // [kEsChunk][cwp]
-            Real* lb = LB + tid * ldl;
-            Real* sb = SB + tid * lds;
+            double* cbuf = reinterpret_cast<double*>(YS + bd * tp);            // [kEsChunk][cwp]
+            double* lb = LB + tid * ldl;
+            double* sb = SB + tid * lds;
             Real* lvs = LV + tid;
             Real* ses = SE + tid;
             Real* ys = YS + tid * tp;
@@ -91,12 +96,14 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
             const bool lane_ok = sl0 + lane < sl1;
             const int lrow = lane_ok ? pl.slot_row[k0 + sl0 + lane] : 0;
             constexpr int e16 = 16 / static_cast<int>(sizeof(Real));
+            constexpr int d16 = 2;  // doubles per 16-byte copy
             // observation rows are epoch constants: staged before the dependency wait
             if (lane_ok)
                 for (int ch = tid >> 5; ch * e16 < tp; ch += kFinishThreads / 32)
                     cp_async16(YS + lane * tp + ch * e16, st.vrm + (size_t)lrow * st.ldv + ch * e16);
             pdl_wait();
             DBG_SPAN_MIN(st, s, 4);
+            SPAN_BEGIN(st, s, kSpanFinish);
             Real a_raw = 0, g_raw = 0;
             Real s0[SC > 0 ? SC : 1];  // exp(seas_raw) for the output's chain rule, loaded up front
             if (mine) {
@@ -129,18 +136,18 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
             FCLK();
             for (int clo = blo; clo < bhi; clo += kEsChunk) {
                 const int chi = min(bhi, clo + kEsChunk);
-                const Real* src = st.contrib + (size_t)(clo - cb0) * cwp;
+                const double* src = st.contrib + (size_t)(clo - cb0) * cwp;
                 const int nel = (chi - clo) * cwp;
-                for (int i = tid * e16; i < nel; i += kFinishThreads * e16) cp_async16(cbuf + i, src + i);
+                for (int i = tid * d16; i < nel; i += kFinishThreads * d16) cp_async16(cbuf + i, src + i);
                 cp_async_wait_all();
                 __syncthreads();
                 FCLK();
                 for (int sl = wq; sl0 + sl < sl1 && sl < bd; sl += kFinishThreads / 32) {
                     const int w_lo = max(pl.slot_win_off[k0 + sl0 + sl], clo);
                     const int w_hi = min(pl.slot_win_off[k0 + sl0 + sl + 1], chi);
-                    Real* sbr = SB + sl * lds;
+                    double* sbr = SB + sl * lds;
                     for (int w = w_lo; w < w_hi; ++w) {
-                        const Real* c = cbuf + (w - clo) * cwp;
+                        const double* c = cbuf + (w - clo) * cwp;
                         const int a = static_cast<int>(c[nio + 1]);
                         for (int j = lane; j < nio; j += 32) sbr[a - I + 1 + j] += c[j];
                         if (lane == 0) LB[sl * ldl + a] += c[nio];
@@ -155,50 +162,59 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
             }
             FCLK();
             if (mine) {
-                const Real alpha = M::logistic_ps(a_raw);
-                const Real gamma = M::logistic_ps(g_raw);
-                const Real oma = Real(1) - alpha, omg = Real(1) - gamma;
+                // forward quantities as the forward pass computed them (Real), the adjoint
+                // recursion in double
+                const double alpha = static_cast<double>(M::logistic_ps(a_raw));
+                const double gamma = static_cast<double>(M::logistic_ps(g_raw));
+                const double oma = static_cast<double>(Real(1) - M::logistic_ps(a_raw));
+                const double omg = static_cast<double>(Real(1) - M::logistic_ps(g_raw));
                 const int row = lrow;
                 cp_async_wait_all();
                 FCLK();
-                Real l0 = 0;
-                for (int j = 0; j < S; ++j) l0 += ys[j];
-                l0 = l0 / Real(S);
-                Real abar = 0, gbar = 0, omab = 0, omgb = 0;
-                Real lbn = lb[T - 1];  // running adjoint of l[t]
+                Real l0r = 0;
+                for (int j = 0; j < S; ++j) l0r += ys[j];
+                const double l0 = static_cast<double>(l0r / Real(S));
+                double abar = 0, gbar = 0, omab = 0, omgb = 0;
+                double lbn = lb[T - 1];  // running adjoint of l[t]
+                // a / b: IEEE in fp64 mode (the reference's arithmetic); times the reciprocal
+                // (computed off the dependency chain) in fp32 mode
+                auto dv = [](double a, double b, double rb) -> double {
+                    if constexpr (sizeof(Real) == 4) return a * rb;
+                    else return a / b;
+                };
                 // one reverse step (t > 0 unless FIRST): Sb = final adjoint of s[t+S],
                 // returns the final adjoint of s[t]
-                auto step = [&](int t, Real Sb, auto first) -> Real {
+                auto step = [&](int t, double Sb, auto first) -> double {
                     constexpr bool kFirst = decltype(first)::value;
-                    const Real yt = ys[t];
-                    const Real lp = kFirst ? l0 : lvs[(t - 1) * bd];
-                    const Real s_t = ses[t * bd];
-                    const Real rlp = rcp_of(lp), rst = rcp_of(s_t);
-                    Real sbt = sb[t];
+                    const double yt = static_cast<double>(ys[t]);
+                    const double lp = kFirst ? l0 : static_cast<double>(lvs[(t - 1) * bd]);
+                    const double s_t = static_cast<double>(ses[t * bd]);
+                    const double rlp = 1.0 / lp, rst = 1.0 / s_t;
+                    double sbt = sb[t];
                     // s_{t+S} = gamma*(y/lp) + (1-gamma)*s_t
                     omgb += Sb * s_t;
                     sbt += Sb * omg;
-                    const Real d2 = fdiv_r(yt, lp, rlp);
+                    const double d2 = dv(yt, lp, rlp);
                     gbar += Sb * d2;
                     // l_t = alpha*(y/s_t) + (1-alpha)*lp
-                    const Real Lb = lbn;
+                    const double Lb = lbn;
                     omab += Lb * lp;
-                    const Real d1 = fdiv_r(yt, s_t, rst);
+                    const double d1 = dv(yt, s_t, rst);
                     abar += Lb * d1;
-                    sbt -= fdiv_r((Lb * alpha) * d1, s_t, rst);
+                    sbt -= dv((Lb * alpha) * d1, s_t, rst);
                     if constexpr (!kFirst) {
-                        const Real d2b = Sb * gamma;
-                        lbn = lb[t - 1] - fdiv_r(d2b * d2, lp, rlp) + Lb * oma;
+                        const double d2b = Sb * gamma;
+                        lbn = lb[t - 1] - dv(d2b * d2, lp, rlp) + Lb * oma;
                     }
                     return sbt;
                 };
                 using Mid = std::integral_constant<bool, false>;
                 using First = std::integral_constant<bool, true>;
-                Real sfin[SC > 0 ? SC : 1];
+                double sfin[SC > 0 ? SC : 1];
                 if constexpr (SC > 0) {
                     // register ring: rg[j] holds the final adjoint of the latest s index = j (mod S);
                     // full groups of SC steps are branch-free so consecutive steps interleave
-                    Real rg[SC];
+                    double rg[SC];
 #pragma unroll
                     for (int j = 0; j < SC; ++j) rg[j] = 0;  // s[T..T+S) receive no adjoint
                     int base = ((T - 1) / SC) * SC;
@@ -226,21 +242,21 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
                 abar -= omab;
                 gbar -= omgb;
                 Real* o = st.psg + (size_t)slot * (2 + S);
-                const Real ga = abar * alpha * (Real(1) - alpha);
-                const Real gg = gbar * gamma * (Real(1) - gamma);
+                const Real ga = static_cast<Real>(abar * alpha * oma);
+                const Real gg = static_cast<Real>(gbar * gamma * omg);
                 o[0] = ga;
                 o[1] = gg;
                 sq += static_cast<double>(ga) * ga + static_cast<double>(gg) * gg;
                 if constexpr (SC > 0) {
 #pragma unroll
                     for (int j = 0; j < SC; ++j) {
-                        const Real g = sfin[j] * M::exp_ps(s0[j]);
+                        const Real g = static_cast<Real>(sfin[j] * static_cast<double>(M::exp_ps(s0[j])));
                         o[2 + j] = g;
                         sq += static_cast<double>(g) * g;
                     }
                 } else {
                     for (int j = 0; j < S; ++j) {
-                        const Real g = sb[j] * M::exp_ps(st.ps[(2 + j) * N + row]);
+                        const Real g = static_cast<Real>(sb[j] * static_cast<double>(M::exp_ps(st.ps[(2 + j) * N + row])));
                         o[2 + j] = g;
                         sq += static_cast<double>(g) * g;
                     }
@@ -248,11 +264,13 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
             }
         } else {
             pdl_wait();
+            SPAN_BEGIN(st, s, kSpanFinish);
         }
         const double tot = block_sum(sq, red);
         if (tid == 0) st.es_sq_part[blockIdx.x] = tot;
     } else {
         pdl_wait();
+        SPAN_BEGIN(st, s, kSpanFinish);
         // ------- weight gradients: G[q][k] = sum_b A[b][q] U[b][k] over the step's windows ----
         // block -> (matrix, 16 q x 8 k output block, row part); warp w sums rows b = w (mod 8)
         // of its part in order, warps are combined in order, and for large steps (gsplit > 1
@@ -417,6 +435,7 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
     DBG_SPAN_MAX(st, s, 5);
     if (static_cast<int>(blockIdx.x) < es_blocks) DBG_SPAN_MAX(st, s, 10);
     else DBG_SPAN_MAX(st, s, 11);
+    SPAN_END(st, s, kSpanFinish);
     if (finalize & 4) {
         // single GPU, updating step: K4 derives the step scalars from the partials itself
         // (no last-CTA ticket on this kernel's tail); only a step that applies updates
@@ -448,18 +467,22 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
     ls = block_sum(ls, red);
     all = block_sum(all, red);
     if (tid != 0) return;
-    st.gbuf[lay.P_pad] = static_cast<Real>(es);
-    st.gbuf[lay.P_pad + 1] = static_cast<Real>(ls);
-    if (finalize & 1) finalize_scalars(st, pl, s, all + es, ls, (finalize & 2) != 0);
+    st.gtail[0] = es;
+    st.gtail[1] = ls;
+    st.gtail[2] = st.err[0] != 0 ? 1.0 : 0.0;
+    st.gtail[3] = 0.0;
+    if (finalize & 1) finalize_scalars(st, pl, s, all + es, ls, (finalize & 2) != 0, st.err[0] != 0);
     *st.done_ctr = 0;
     DBG_SPAN_MAX(st, s, 6);
+    SPAN_END(st, s, kSpanFinish);
 }
 
-// After the NCCL all-reduce of gbuf (sharded mode): global squared norm + scalars.
+// After the NCCL all-reduce of gbuf and gtail (sharded mode): global squared norm + scalars.
 template <typename Real>
 __global__ void __launch_bounds__(256) k_finalize(StateDev<Real> st, PlanDev pl, NetLayout lay, int s, int advance) {
     __shared__ double red[32];
     __shared__ bool last;
+    SPAN_BEGIN(st, s, kSpanReduce);
     const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     double sq = 0.0;
     if (q < lay.P_pad) {
@@ -473,15 +496,17 @@ __global__ void __launch_bounds__(256) k_finalize(StateDev<Real> st, PlanDev pl,
         last = atomicAdd(st.done_ctr + 1, 1u) == gridDim.x - 1;
     }
     __syncthreads();
+    SPAN_END(st, s, kSpanReduce);
     if (!last) return;
     __threadfence();
     double all = 0.0;
     for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) all += __ldcg(st.red_sq_part + b);
     all = block_sum(all, red);
     if (threadIdx.x != 0) return;
-    const double es = st.attach ? static_cast<double>(st.gbuf[lay.P_pad]) : 0.0;
-    finalize_scalars(st, pl, s, all + es, static_cast<double>(st.gbuf[lay.P_pad + 1]), advance != 0);
+    const double es = st.attach ? st.gtail[0] : 0.0;
+    finalize_scalars(st, pl, s, all + es, st.gtail[1], advance != 0, st.gtail[2] != 0.0);
     st.done_ctr[1] = 0;
+    SPAN_END(st, s, kSpanReduce);
 }
 
 // ------------------------------------------------------------------------------ K4
@@ -497,7 +522,8 @@ __device__ __forceinline__ void adam_update(double& theta, double& m, double& v,
 // (trainer.hpp:603-615), bias corrections at the step K3 advanced (:617-620), step loss --
 // from K3's per-block partials with the same loads, order and tree as the last-CTA
 // finalisation, so all blocks hold bit-identical values and K3 needs no serial tail;
-// block 0 publishes them.  es_blocks < 0 (sharded): k_finalize already wrote st.scal.
+// block 0 publishes them.  es_blocks < 0 (sharded): k_finalize / k_group_reduce already
+// wrote st.scal from the reduced buffers.
 template <typename Real>
 __global__ void __launch_bounds__(256) k_adam(StateDev<Real> st, PlanDev pl, NetLayout lay, int s, int es_blocks,
                                               int red_blocks, int net_blocks) {
@@ -507,6 +533,7 @@ __global__ void __launch_bounds__(256) k_adam(StateDev<Real> st, PlanDev pl, Net
     pdl_wait();
     DBG_GT(st, 6);
     DBG_SPAN_MIN(st, s, 7);
+    SPAN_BEGIN(st, s, kSpanAdam);
     const int tid = threadIdx.x;
     // this thread's Adam operands first: their L2 latency overlaps the scalar reduction
     // below.  Network blocks: one live parameter; per-series blocks (trainer.hpp:636-650):
@@ -564,8 +591,8 @@ __global__ void __launch_bounds__(256) k_adam(StateDev<Real> st, PlanDev pl, Net
             sc[1] = bias_c1(st, step);
             sc[2] = bias_c2(st, step);
             if (blockIdx.x == 0) {
-                st.gbuf[lay.P_pad] = static_cast<Real>(es);
-                st.gbuf[lay.P_pad + 1] = static_cast<Real>(ls);
+                st.gtail[0] = es;
+                st.gtail[1] = ls;
                 st.scal[0] = scale;
                 st.scal[3] = ls / pl.step_M[s];
                 st.loss_hist[s] = ls / pl.step_M[s];
@@ -581,7 +608,11 @@ __global__ void __launch_bounds__(256) k_adam(StateDev<Real> st, PlanDev pl, Net
         sc[2] = st.scal[2];
     }
     __syncthreads();
-    if (!mine || st.err[0] != 0) return;  // the reference throws before apply_updates
+    // the reference throws before apply_updates; sharded: err[2] is any rank's error
+    if (!mine || st.err[0] != 0 || st.err[2] != 0) {
+        SPAN_END(st, s, kSpanAdam);
+        return;
+    }
     double th = t0, m = m0, v = v0;
     if (net) {
         adam_update(th, m, v, static_cast<double>(g0) * sc[0], st.lr_net, sc[1], sc[2]);
@@ -596,6 +627,7 @@ __global__ void __launch_bounds__(256) k_adam(StateDev<Real> st, PlanDev pl, Net
         st.ps[e] = static_cast<Real>(th);
     }
     DBG_SPAN_MAX(st, s, 8);
+    SPAN_END(st, s, kSpanAdam);
 }
 
 }  // namespace esrnn_dev

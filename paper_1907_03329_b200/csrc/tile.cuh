@@ -437,6 +437,7 @@ __global__ void __launch_bounds__((RESIDENT || sizeof(Real) == 8) ? 512 : 384, (
         if (MODE == kTrain) {
             DBG_SPAN_MIN(st, s, 1);
             DBG_SPAN_MIN(st, s - 1, 9);
+            SPAN_BEGIN(st, s, kSpanTile);
         }
         weights_tma();
         for (int e = tid; e < nrows * np; e += NT) {
@@ -757,25 +758,29 @@ __global__ void __launch_bounds__((RESIDENT || sizeof(Real) == 8) ? 512 : 384, (
 
     // ---- ES adjoint contributions per window (Div / Mul / BroadcastCol adjoints) ----
     // written in slot-major CSR order so each slot's windows are contiguous for K3;
-    // row = [inputs (s index a-I+1..a) | targets (a+1..a+O) | level a | anchor a]
+    // row = [inputs (s index a-I+1..a) | targets (a+1..a+O) | level a | anchor a].
+    // Formed in double in both precisions: a window's seasonality and level contributions
+    // share one adjoint v and cancel almost exactly downstream (x = y / (s l) is nearly
+    // invariant under s -> c s, l -> l / c), so they must carry the same rounding of v and
+    // none of their own; K3's reverse scan continues in double
     if (st.attach) {
         // one warp per window, lanes over its I + O normalised entries; fixed-order warp sum
         const int nio = I + O;
         for (int r = warp; r < nrows; r += NW) {
-            Real* __restrict__ cr = st.contrib + (size_t)w_info[3][r] * st.cwp;
-            const Real lv = lvl[r];
-            Real acc = 0;
+            double* __restrict__ cr = st.contrib + (size_t)w_info[3][r] * st.cwp;
+            const double lv = static_cast<double>(lvl[r]);
+            double acc = 0;
             for (int j = lane; j < nio; j += 32) {
-                Real v, sv;
+                double v, sv;
                 if (j < I) {
-                    sv = s_in[r * I + j];
-                    v = UBT[j * LD + r] * XT[j * LD + r];
+                    sv = static_cast<double>(s_in[r * I + j]);
+                    v = static_cast<double>(UBT[j * LD + r]) * static_cast<double>(XT[j * LD + r]);
                 } else {
                     const int o = j - I;
-                    sv = s_out[r * ldo + o];
-                    v = -PBT[o * LD + r] * tgt[r * ldo + o];
+                    sv = static_cast<double>(s_out[r * ldo + o]);
+                    v = -(static_cast<double>(PBT[o * LD + r]) * static_cast<double>(tgt[r * ldo + o]));
                 }
-                const Real denb = -fdiv(v, sv * lv);
+                const double denb = -(v / (sv * lv));
                 cr[j] = denb * lv;
                 acc += denb * sv;
             }
@@ -783,12 +788,13 @@ __global__ void __launch_bounds__((RESIDENT || sizeof(Real) == 8) ? 512 : 384, (
             for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
             if (lane == 0) {
                 cr[nio] = acc;
-                cr[nio + 1] = static_cast<Real>(w_ancv[r]);  // exact (< 2^24)
+                cr[nio + 1] = static_cast<double>(w_ancv[r]);
             }
         }
     }
     if (MODE == kTrain) DBG_GT(st, 3);
     if (MODE == kTrain) DBG_SPAN_MAX(st, s, 2);
+    if (MODE == kTrain) SPAN_END(st, s, kSpanTile);
 }
 
 }  // namespace esrnn_dev

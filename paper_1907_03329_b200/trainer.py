@@ -111,7 +111,7 @@ class TrainConfig:  # trainer.hpp:22-44 (+ B200 extensions)
     patience: int = 0
     min_delta: float = 0.0
     # B200 extensions
-    precision: str = "fp32"          # "fp32" (performance) | "fp64" (parity mode)
+    precision: str = "fp64"          # "fp64" (reference arithmetic, default) | "fp32" (performance, opt-in)
     max_batch_size: int = 0          # 0 -> 2048 reference cap
     device: int = 0
     use_graphs: bool = True
@@ -359,7 +359,11 @@ class Trainer:
     """esrnn::Trainer (trainer.hpp:157-673) backed by a native engine handle."""
 
     def __init__(self, series, profile: FrequencyProfile, cfg: TrainConfig, *, api: N.NativeApi | None = None,
-                 dist: tuple[int, int, bytes] | None = None):
+                 dist: tuple | None = None):
+        """dist: series-sharded data parallelism (esrnn_dist), (rank, world, transport[, flags])
+        with transport the NCCL unique id (bytes, one process per GPU) or an in-process
+        `Group` (api.group(world)); flags N.DIST_FORCE_COLLECTIVE runs the collective step
+        at world 1 too."""
         self.api = api if api is not None else N.product_api()
         self._profile = profile
         self._cfg = cfg
@@ -386,7 +390,12 @@ class Trainer:
         if dist is not None:
             c_dist = N.Dist()
             c_dist.rank, c_dist.world_size = dist[0], dist[1]
-            C.memmove(c_dist.nccl_unique_id, dist[2], 128)
+            if isinstance(dist[2], N.Group):
+                c_dist.group = dist[2].handle
+                self._group = dist[2]  # the group outlives its trainers
+            else:
+                C.memmove(c_dist.nccl_unique_id, dist[2], 128)
+            c_dist.flags = dist[3] if len(dist) > 3 else 0
         h = C.c_void_p()
         p_c, cfg_c = profile.to_c(), cfg.to_c()
         self.api.check(self.api.lib.esrnn_trainer_create(
@@ -494,6 +503,14 @@ class Trainer:
         a, g, s = np.zeros(n), np.zeros(n), np.zeros((n, S))
         self._chk(self.api.lib.esrnn_trainer_get_per_series(self._h, self.row_begin, n, N.dptr(a), N.dptr(g),
                                                              N.dptr(s)))
+        return a, g, s
+
+    def gather_per_series_arrays(self):
+        """Collective on a sharded trainer (every rank calls it): every series' per-series
+        parameters, gathered from their owners in dataset order."""
+        n, S = self.series_count(), self._profile.seasonality_length
+        a, g, s = np.zeros(n), np.zeros(n), np.zeros((n, S))
+        self._chk(self.api.lib.esrnn_trainer_gather_per_series(self._h, N.dptr(a), N.dptr(g), N.dptr(s)))
         return a, g, s
 
     def set_per_series_arrays(self, a, g, s, row_begin=None):

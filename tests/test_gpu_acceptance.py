@@ -20,7 +20,7 @@ def quarterly_synthetic(api, n, seed, noise):  # acceptance.cpp:320-327
 
 def test_overfit_smoke(engine):
     vals, cats = quarterly_synthetic(engine, 4, 51, 0.0)
-    cfg = TrainConfig(batch_size=256, seed=11, learning_rate_network=5e-3)
+    cfg = TrainConfig(batch_size=256, seed=11, learning_rate_network=5e-3, precision="fp32")
     tr = Trainer((vals, cats), FrequencyProfile.defaults(Frequency.Quarterly), cfg, api=engine)
     loss, epochs = float("inf"), 0
     while epochs < 500 and not loss < 1e-2:
@@ -35,7 +35,7 @@ def test_forecast_quality_beats_seasonal_naive(engine):
     ratios = []
     for seed in (1, 2, 3):
         vals, cats = quarterly_synthetic(engine, 200, 60 + seed, 0.05)
-        cfg = TrainConfig(batch_size=256, seed=seed, learning_rate_network=3e-3, epochs=20)
+        cfg = TrainConfig(batch_size=256, seed=seed, learning_rate_network=3e-3, epochs=20, precision="fp32")
         tr = Trainer((vals, cats), prof, cfg, api=engine)
         ev0 = tr.evaluate(False)
         # seasonal_naive + smape over the validation block (metrics.hpp:17-28, :52-59)

@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 
 def _run(engine, vals, cats, seed, epochs=2):
     prof = FrequencyProfile.defaults(Frequency.Quarterly)
-    tr = Trainer((vals, cats), prof, TrainConfig(batch_size=256, seed=seed), api=engine)
+    tr = Trainer((vals, cats), prof, TrainConfig(batch_size=256, seed=seed, precision="fp32"), api=engine)
     losses = [tr.train_epoch() for _ in range(epochs)]
     v = tr.validate()
     w = np.asarray(tr.last_epoch_windows(), dtype=np.int64)

@@ -31,7 +31,7 @@ def gpu_epoch_ms(api, vals, cats, prof, B, reps=3):
     # tiny batches mean tens of thousands of steps per epoch: launch eagerly instead of
     # capturing one enormous graph
     tr = Trainer((vals, cats), prof, TrainConfig(seed=7, batch_size=B, max_batch_size=max(B, 2048),
-                                                 use_graphs=B >= 64), api=api)
+                                                 use_graphs=B >= 64, precision="fp32"), api=api)
     for _ in range(2):
         tr.train_epoch()
     ms = []
@@ -79,7 +79,7 @@ def mixed(out, epochs):
         length = prof.min_length + 2 * prof.horizon
         vals, cats = api.make_synthetic(seed, n, length, prof.seasonality_length, 0.05)
         t0 = time.perf_counter()
-        tr = Trainer((vals, cats), prof, TrainConfig(seed=7, batch_size=2048), api=api)
+        tr = Trainer((vals, cats), prof, TrainConfig(seed=7, batch_size=2048, precision="fp32"), api=api)
         dev = 0.0
         losses = []
         for _ in range(epochs):

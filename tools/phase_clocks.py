@@ -12,6 +12,6 @@ prof = FrequencyProfile.defaults(freq)
 n, B = (1000, 1000) if freq == Frequency.Quarterly else ((23000, 2048) if freq == Frequency.Yearly else (48000, 2048))
 length = prof.min_length + 2 * prof.horizon
 vals, cats = api.make_synthetic(41, n, length, prof.seasonality_length, 0.05)
-tr = Trainer((vals, cats), prof, TrainConfig(batch_size=B, seed=7, use_graphs=os.environ.get('GRAPHS') == '1', max_batch_size=max(B, 2048)), api=api)
+tr = Trainer((vals, cats), prof, TrainConfig(batch_size=B, seed=7, use_graphs=os.environ.get('GRAPHS') == '1', max_batch_size=max(B, 2048), precision='fp32'), api=api)
 for _ in range(2):
     tr.train_epoch()
