@@ -26,11 +26,23 @@
 #include <vector>
 
 #include "../esrnn_b200.h"
+#ifdef ESRNN_B200_HOST_TYPES
+// Include swap of trainer.hpp alone: the caller's tree keeps its own value types
+// (esrnn/{data,errors,holt_winters,matrix,network}.hpp of the reference) and only the
+// Trainer comes from here (tests/cpp/acceptance_overlay).
+#include <esrnn/data.hpp>
+#include <esrnn/errors.hpp>
+#include <esrnn/holt_winters.hpp>
+#include <esrnn/matrix.hpp>
+#include <esrnn/network.hpp>
+#include "status.hpp"
+#else
 #include "data.hpp"
 #include "errors.hpp"
 #include "holt_winters.hpp"
 #include "matrix.hpp"
 #include "network.hpp"
+#endif
 
 namespace esrnn {
 

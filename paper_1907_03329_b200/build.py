@@ -93,10 +93,53 @@ def build_cpp_tests() -> None:
           "-Wl,-rpath,$ORIGIN/../paper_1907_03329_b200"])
 
 
+REF_PROJ = Path("/root/reference/proj")
+
+
+def _nlohmann_dir() -> str | None:
+    """nlohmann/json 3.11.3 as vendored by cudnn_frontend in this image: the reference's
+    checkpoint.hpp / commands.hpp / report.hpp include <json.hpp> from its (absent) vendor/."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    roots = [Path(sys.prefix) / "lib" / f"python{sys.version_info.major}.{sys.version_info.minor}" / "site-packages"]
+    if spec and spec.submodule_search_locations:
+        roots += [Path(b).parent for b in spec.submodule_search_locations]
+    for r in roots:
+        d = r / "include" / "cudnn_frontend" / "thirdparty" / "nlohmann"
+        if (d / "json.hpp").exists():
+            return str(d)
+    return None
+
+
+def build_reference_acceptance() -> None:
+    """The reference's own acceptance suite (proj/tests/acceptance.cpp, criteria 1-9),
+    compiled UNMODIFIED from /root/reference with only esrnn/trainer.hpp swapped for the
+    drop-in (include overlay tests/cpp/overlay/esrnn/trainer.hpp): its Trainer calls,
+    commands.hpp's cmd_train and checkpoint.hpp then run on the B200 engine.  Built here
+    (the reference tree exists only in this container); the binary travels to the GPU box
+    in build/.  Skipped when the reference tree or nlohmann/json is absent."""
+    src = REF_PROJ / "tests" / "acceptance.cpp"
+    js = _nlohmann_dir()
+    if not src.exists() or js is None:
+        print("reference acceptance: reference tree or nlohmann/json absent, keeping prebuilt build/ref_acceptance")
+        return
+    out = BUILD / "ref_acceptance"
+    ov = ROOT / "tests" / "cpp" / "overlay"
+    deps = [src, *(REF_PROJ / "include" / "esrnn").glob("*.hpp"), *(INC / "esrnn_b200").glob("*.hpp"),
+            INC / "esrnn_b200.h", *ov.rglob("*.hpp")]
+    if not _stale(out, deps) and not _stale(out, [LIB]):
+        return
+    BUILD.mkdir(exist_ok=True)
+    _run(["g++", "-std=gnu++20", "-O2", "-I" + str(ov), "-I" + str(REF_PROJ / "include"), "-I" + str(INC),
+          "-I" + js, str(src), "-o", str(out), "-L" + str(PKG), "-lesrnn_b200",
+          "-Wl,-rpath,$ORIGIN/../paper_1907_03329_b200"])
+
+
 def build_all(force: bool = False) -> None:
     build_engine(force)
     build_oracle()
     build_cpp_tests()
+    build_reference_acceptance()
 
 
 if __name__ == "__main__":

@@ -892,13 +892,13 @@ int stack_threads(const NetLayout& lay) { return tile_threads(lay); }
 
 template <typename Real>
 size_t finish_smem(const NetLayout& lay) {
-    // ES blocks: level / seasonality adjoints [bd][T|1], [bd][(T+S)|1] (double), forward l and
-    // s columns [T][bd] + one staged observation row per slot (Real), one chunk of staged
-    // contribution rows (double)
+    // ES blocks: level / seasonality adjoints [bd][T|1], [bd][(T+S)|1], forward l and s
+    // columns [T][bd] (double), one staged observation row per slot (Real), one chunk of
+    // staged contribution rows (double)
     const size_t cwp = (lay.I + lay.O + 2 + 3) & ~3;
     const size_t bd = kEsSlotsPerBlock;
     const size_t es = sizeof(double) * bd * (static_cast<size_t>(lay.T | 1) + static_cast<size_t>((lay.T + lay.S) | 1)) +
-                      sizeof(Real) * bd * (2 * static_cast<size_t>(lay.T) + row_pad<Real>(lay.T)) +
+                      sizeof(double) * bd * 2 * static_cast<size_t>(lay.T) + sizeof(Real) * bd * row_pad<Real>(lay.T) +
                       sizeof(double) * kEsChunk * cwp;
     const size_t gemm = sizeof(Real) * (static_cast<size_t>(kGBuf * kGChunk) * (kGq + kGk) + (kFinishThreads / 32) * 32 * 6);
     return std::max(es, gemm);

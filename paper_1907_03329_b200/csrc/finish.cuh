@@ -82,14 +82,14 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
             const int ldl = T | 1, lds = (T + S) | 1;
             double* LB = reinterpret_cast<double*>(smem_raw);                  // [bd][ldl] level adjoint
             double* SB = LB + bd * ldl;                                        // [bd][lds] seasonality adjoint
-            Real* LV = reinterpret_cast<Real*>(SB + bd * lds);                 // [T][bd]   forward levels
-            Real* SE = LV + T * bd;                                            // [T][bd]   forward seasonalities
-            Real* YS = SE + T * bd;                                            // [bd][tp]  observation rows
+            double* LV = SB + bd * lds;                                        // [T][bd]   forward levels
+            double* SE = LV + T * bd;                                          // [T][bd]   forward seasonalities
+            Real* YS = reinterpret_cast<Real*>(SE + T * bd);                   // [bd][tp]  observation rows
             double* cbuf = reinterpret_cast<double*>(YS + bd * tp);            // [kEsChunk][cwp]
             double* lb = LB + tid * ldl;
             double* sb = SB + tid * lds;
-            Real* lvs = LV + tid;
-            Real* ses = SE + tid;
+            double* lvs = LV + tid;
+            double* ses = SE + tid;
             Real* ys = YS + tid * tp;
             FCLK();
             // ---- stage the forward state with the whole block (every copy in flight at once) ----
@@ -101,25 +101,63 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
             if (lane_ok)
                 for (int ch = tid >> 5; ch * e16 < tp; ch += kFinishThreads / 32)
                     cp_async16(YS + lane * tp + ch * e16, st.vrm + (size_t)lrow * st.ldv + ch * e16);
+            Real a_raw = 0, g_raw = 0;
+            Real s0[SC > 0 ? SC : 1];  // exp(seas_raw) for the output's chain rule, loaded up front
+            double l0 = 0;             // l[-1] = mean(y[0:S]) (holt_winters.hpp:247-250)
+            if constexpr (sizeof(Real) == 4) {
+                // fp32 mode: the forward levels / seasonalities the adjoint is linearised at are
+                // recomputed here in double (the reference's arithmetic) instead of taken from
+                // K2's fp32 scan.  The adjoint sums of a series' window terms cancel almost
+                // exactly (x = y/(s*l) is invariant under s -> c*s, l -> l/c except through
+                // l[-1]); linearised at fp32-rounded states the init-seasonality gradient of an
+                // S = 1 series is off by ~1e-3 of its tensor, at double states by ~1e-7.
+                // Runs before the dependency wait, overlapping K2: the per-series parameters are
+                // the previous step's K4 output (complete before K2 started), read at L2.
+                cp_async_wait_all();
+                __syncthreads();
+                if (mine) {
+                    a_raw = __ldcg(st.ps + lrow);
+                    g_raw = __ldcg(st.ps + N + lrow);
+                    const double al = Math<double>::logistic(static_cast<double>(a_raw));
+                    const double ga = Math<double>::logistic(static_cast<double>(g_raw));
+                    for (int j = 0; j < S; ++j) {
+                        const Real r = __ldcg(st.ps + (size_t)(2 + j) * N + lrow);
+                        if constexpr (SC > 0) s0[j] = r;
+                        if (j < T) ses[j * bd] = Math<double>::exp(static_cast<double>(r));
+                    }
+                    for (int j = 0; j < S; ++j) l0 += static_cast<double>(ys[j]);
+                    l0 /= S;
+                    double lp = l0;
+                    for (int t = 0; t < T; ++t) {
+                        const double yt = static_cast<double>(ys[t]), s_t = ses[t * bd];
+                        const double lv = al * (yt / s_t) + (1.0 - al) * lp;
+                        if (t + S < T) ses[(t + S) * bd] = ga * (yt / lp) + (1.0 - ga) * s_t;
+                        lvs[t * bd] = lv;
+                        lp = lv;
+                    }
+                }
+            }
             pdl_wait();
             DBG_SPAN_MIN(st, s, 4);
             SPAN_BEGIN(st, s, kSpanFinish);
-            Real a_raw = 0, g_raw = 0;
-            Real s0[SC > 0 ? SC : 1];  // exp(seas_raw) for the output's chain rule, loaded up front
-            if (mine) {
-                a_raw = st.ps[lrow];
-                g_raw = st.ps[N + lrow];
-                if constexpr (SC > 0) {
+            if constexpr (sizeof(Real) == 8) {
+                if (mine) {
+                    a_raw = st.ps[lrow];
+                    g_raw = st.ps[N + lrow];
+                    if constexpr (SC > 0) {
 #pragma unroll
-                    for (int j = 0; j < SC; ++j) s0[j] = st.ps[(size_t)(2 + j) * N + lrow];
+                        for (int j = 0; j < SC; ++j) s0[j] = st.ps[(size_t)(2 + j) * N + lrow];
+                    }
                 }
-            }
-            // forward levels / seasonalities of the block's slots: whole 16-byte pieces of the
-            // [t][kcap] rows (kcap and sl0 are multiples of kEsSlotsPerBlock)
-            for (int e = tid; e < 2 * T * (bd / e16); e += kFinishThreads) {
-                const int half = e / (T * (bd / e16)), r = e - half * T * (bd / e16);
-                const int t = r / (bd / e16), ch = r - t * (bd / e16);
-                cp_async16((half ? SE : LV) + t * bd + ch * e16, (half ? st.se : st.lv) + (size_t)t * kc + sl0 + ch * e16);
+                // forward levels / seasonalities of the block's slots from K2's fp64 scan: whole
+                // 16-byte pieces of the [t][kcap] rows (kcap and sl0 are multiples of
+                // kEsSlotsPerBlock)
+                for (int e = tid; e < 2 * T * (bd / e16); e += kFinishThreads) {
+                    const int half = e / (T * (bd / e16)), r = e - half * T * (bd / e16);
+                    const int t = r / (bd / e16), ch = r - t * (bd / e16);
+                    cp_async16(reinterpret_cast<Real*>(half ? SE : LV) + t * bd + ch * e16,
+                               (half ? st.se : st.lv) + (size_t)t * kc + sl0 + ch * e16);
+                }
             }
             // ---- window adjoints: this block's windows are one contiguous range of the
             // CSR-ordered contribution table, staged in chunks of kEsChunk rows; then one warp
@@ -162,20 +200,25 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
             }
             FCLK();
             if (mine) {
-                // forward quantities as the forward pass computed them (Real), the adjoint
-                // recursion in double
-                const double alpha = static_cast<double>(M::logistic_ps(a_raw));
-                const double gamma = static_cast<double>(M::logistic_ps(g_raw));
-                const double oma = static_cast<double>(Real(1) - M::logistic_ps(a_raw));
-                const double omg = static_cast<double>(Real(1) - M::logistic_ps(g_raw));
+                // the adjoint recursion in double, linearised at double forward states (fp64:
+                // K2's scan; fp32: the recomputation above)
+                using MD = Math<double>;
+                const double alpha = MD::logistic(static_cast<double>(a_raw));
+                const double gamma = MD::logistic(static_cast<double>(g_raw));
+                const double oma = 1.0 - alpha, omg = 1.0 - gamma;
                 const int row = lrow;
                 cp_async_wait_all();
                 FCLK();
-                Real l0r = 0;
-                for (int j = 0; j < S; ++j) l0r += ys[j];
-                const double l0 = static_cast<double>(l0r / Real(S));
+                if constexpr (sizeof(Real) == 8) {
+                    Real l0r = 0;
+                    for (int j = 0; j < S; ++j) l0r += ys[j];
+                    l0 = static_cast<double>(l0r / Real(S));
+                }
+
                 double abar = 0, gbar = 0, omab = 0, omgb = 0;
-                double lbn = lb[T - 1];  // running adjoint of l[t]
+                // the staged per-slot sums are LOG adjoints (tile.cuh): the steps below divide
+                // them by the forward states as they reach them
+                double lbn = lb[T - 1] / lvs[(T - 1) * bd];  // running adjoint of l[t]
                 // a / b: IEEE in fp64 mode (the reference's arithmetic); times the reciprocal
                 // (computed off the dependency chain) in fp32 mode
                 auto dv = [](double a, double b, double rb) -> double {
@@ -190,7 +233,7 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
                     const double lp = kFirst ? l0 : static_cast<double>(lvs[(t - 1) * bd]);
                     const double s_t = static_cast<double>(ses[t * bd]);
                     const double rlp = 1.0 / lp, rst = 1.0 / s_t;
-                    double sbt = sb[t];
+                    double sbt = dv(sb[t], s_t, rst);
                     // s_{t+S} = gamma*(y/lp) + (1-gamma)*s_t
                     omgb += Sb * s_t;
                     sbt += Sb * omg;
@@ -204,7 +247,7 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
                     sbt -= dv((Lb * alpha) * d1, s_t, rst);
                     if constexpr (!kFirst) {
                         const double d2b = Sb * gamma;
-                        lbn = lb[t - 1] - dv(d2b * d2, lp, rlp) + Lb * oma;
+                        lbn = dv(lb[t - 1], lp, rlp) - dv(d2b * d2, lp, rlp) + Lb * oma;
                     }
                     return sbt;
                 };
@@ -250,13 +293,13 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
                 if constexpr (SC > 0) {
 #pragma unroll
                     for (int j = 0; j < SC; ++j) {
-                        const Real g = static_cast<Real>(sfin[j] * static_cast<double>(M::exp_ps(s0[j])));
+                        const Real g = static_cast<Real>(sfin[j] * MD::exp(static_cast<double>(s0[j])));
                         o[2 + j] = g;
                         sq += static_cast<double>(g) * g;
                     }
                 } else {
                     for (int j = 0; j < S; ++j) {
-                        const Real g = static_cast<Real>(sb[j] * static_cast<double>(M::exp_ps(st.ps[(2 + j) * N + row])));
+                        const Real g = static_cast<Real>(sb[j] * MD::exp(static_cast<double>(st.ps[(2 + j) * N + row])));
                         o[2 + j] = g;
                         sq += static_cast<double>(g) * g;
                     }

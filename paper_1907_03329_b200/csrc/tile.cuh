@@ -330,7 +330,6 @@ template <typename Real, int MODE, bool RESIDENT, int SC>
 __global__ void __launch_bounds__((RESIDENT || sizeof(Real) == 8) ? 512 : 384, (RESIDENT || sizeof(Real) == 8) ? 1 : 2) k_tile(StateDev<Real> st, PlanDev pl, NetLayout lay_p, int s, ForecastArgs fa) {
     using M = Math<Real>;
     constexpr int R = kR, LD = ldr<Real>();
-    pdl_trigger();  // dependents may launch; they wait for this grid's completion themselves
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Real* sm = reinterpret_cast<Real*>(smem_raw);
     __shared__ double red[32];
@@ -434,6 +433,10 @@ __global__ void __launch_bounds__((RESIDENT || sizeof(Real) == 8) ? 512 : 384, (
             cp_async16(YS + r * ts.tp + c * e16, st.vrm + (size_t)w_rowv[r] * st.ldv + c * e16);
         }
         pdl_wait();
+        // dependents (K3) may launch once every tile has passed its wait: the previous
+        // step's K4 has then completed, so K3's pre-wait prologue may read the per-series
+        // parameters it wrote (K3 still waits for this grid's completion before the rest)
+        pdl_trigger();
         if (MODE == kTrain) {
             DBG_SPAN_MIN(st, s, 1);
             DBG_SPAN_MIN(st, s - 1, 9);
@@ -456,8 +459,9 @@ __global__ void __launch_bounds__((RESIDENT || sizeof(Real) == 8) ? 512 : 384, (
         }
         DBG_CLK(st, 0);
         __syncthreads();
-        // published states for K3's reverse scan: lv [T][kcap], se [T+S][kcap]
-        if (MODE == kTrain) {
+        // published states for K3's reverse scan: lv [T][kcap], se [T+S][kcap] (fp64 only:
+        // in fp32 mode K3 recomputes them in double, finish.cuh)
+        if (MODE == kTrain && sizeof(Real) == 8) {
             for (int r = warp; r < nrows; r += NW) {  // a warp per window row, lanes over t
                 const int slot = pub_slot[r];
                 if (slot < 0) continue;
@@ -470,6 +474,7 @@ __global__ void __launch_bounds__((RESIDENT || sizeof(Real) == 8) ? 512 : 384, (
     // ---- window gather + normalisation (trainer.hpp:532-566) --------------------------
     if (MODE == kForecast) {
         pdl_wait();
+        pdl_trigger();
         weights_tma();
         const Real* X = reinterpret_cast<const Real*>(fa.X);
         const Real* FL = reinterpret_cast<const Real*>(fa.lvl);
@@ -759,30 +764,29 @@ __global__ void __launch_bounds__((RESIDENT || sizeof(Real) == 8) ? 512 : 384, (
     // ---- ES adjoint contributions per window (Div / Mul / BroadcastCol adjoints) ----
     // written in slot-major CSR order so each slot's windows are contiguous for K3;
     // row = [inputs (s index a-I+1..a) | targets (a+1..a+O) | level a | anchor a].
-    // Formed in double in both precisions: a window's seasonality and level contributions
-    // share one adjoint v and cancel almost exactly downstream (x = y / (s l) is nearly
-    // invariant under s -> c s, l -> l / c), so they must carry the same rounding of v and
-    // none of their own; K3's reverse scan continues in double
+    // Stored as LOG adjoints: a normalised entry z = y / (s l) (input x or target t) with
+    // adjoint zb gives e = -zb * z, so dL/ds = e / s and dL/dl = (sum of e) / l.  A window's
+    // seasonality and level adjoints
+    // cancel almost exactly downstream (x is invariant under s -> c s, l -> l / c), so K3
+    // divides the per-slot sums by its own double forward states once, instead of this
+    // kernel dividing each term by its fp32 states (whose rounding the cancellation would
+    // amplify ~1e4x for S = 1).  Formed in double in both precisions.
     if (st.attach) {
         // one warp per window, lanes over its I + O normalised entries; fixed-order warp sum
         const int nio = I + O;
         for (int r = warp; r < nrows; r += NW) {
             double* __restrict__ cr = st.contrib + (size_t)w_info[3][r] * st.cwp;
-            const double lv = static_cast<double>(lvl[r]);
             double acc = 0;
             for (int j = lane; j < nio; j += 32) {
-                double v, sv;
+                double v;
                 if (j < I) {
-                    sv = static_cast<double>(s_in[r * I + j]);
                     v = static_cast<double>(UBT[j * LD + r]) * static_cast<double>(XT[j * LD + r]);
                 } else {
                     const int o = j - I;
-                    sv = static_cast<double>(s_out[r * ldo + o]);
                     v = -(static_cast<double>(PBT[o * LD + r]) * static_cast<double>(tgt[r * ldo + o]));
                 }
-                const double denb = -(v / (sv * lv));
-                cr[j] = denb * lv;
-                acc += denb * sv;
+                cr[j] = -v;
+                acc -= v;
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);

@@ -100,6 +100,7 @@ def test_fp32_step_within_1e4_of_reference(engine, refapi, name):
                             o.batch_gradients(WindowBatch(rows, anchors, mask=m.copy())))
             for k, v in e.items():
                 worst[k] = max(worst.get(k, 0.0), v)
+    print(name, "worst per-step errors vs reference:", {k: f"{v:.2e}" for k, v in sorted(worst.items())})
     bad = {k: v for k, v in worst.items() if v > TOL}
     assert not bad, (name, bad, max(worst.values()))
 
