@@ -513,9 +513,9 @@ def main():
     if fmsn:
         add("k_tile<forecast>", "forecast", fmsn[0], fmsn[1], lstm_fwd_flops(prof, n_local), "TFLOP/s", fma_peak,
             "stack forward over every series (1 x fwd FLOPs)")
-    step_ms = sum(v["ms_per_step"] for v in kern.values())
-    for v in kern.values():
-        v["share"] = v["ms_per_step"] / step_ms if step_ms else None
+    step_ms = sum(kv["ms_per_step"] for kv in kern.values())
+    for kv in kern.values():
+        kv["share"] = kv["ms_per_step"] / step_ms if step_ms else None
     dom = max(kern, key=lambda k: kern[k]["ms_per_step"])
     d = kern[dom]
     roof = {"kernel": dom, "bound": "fp32-fma" if d["unit"] == "TFLOP/s" else "hbm", "achieved": d["achieved"],

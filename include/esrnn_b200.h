@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define ESRNN_ABI_VERSION 2
+#define ESRNN_ABI_VERSION 3
 #define ESRNN_MAX_BLOCKS 8
 #define ESRNN_MAX_LAYERS 16
 #define ESRNN_NUM_CATEGORIES 6      /* data.hpp:21 kNumCategories */
@@ -92,6 +92,9 @@ typedef struct esrnn_train_config {
     int32_t max_batch_size;       /* 0 => 2048, the reference cap (trainer.hpp:36) */
     int32_t device;               /* CUDA device ordinal */
     int32_t use_graphs;           /* 0 => default (on); <0 => off (debug) */
+    /* --- ABI 3 --- */
+    double level_variability_penalty;  /* lambda >= 0; 0 = the reference's pinball-only loss
+                                        * (bit-identical).  See esrnn_trainer_run_batch. */
 } esrnn_train_config;
 
 /* Series-sharded data parallelism (B200 extension).  Rank r owns dataset
@@ -303,6 +306,34 @@ esrnn_status esrnn_nccl_unique_id(uint8_t out[128]);
  * order from Rng(seed): values n x length, category n. */
 esrnn_status esrnn_make_synthetic(uint64_t seed, int64_t n, int32_t length, int32_t season_length,
                                   double noise_sigma, double* values, int32_t* category);
+
+/* ---- Ingestion -------------------------------------------------
+ * The reference's prepare + load path in one call: parse_m4_train_csv (data.hpp:205-232),
+ * parse_info_csv (:251-279), apply_info (:282-290), the frequency filter and length
+ * statistics of cmd_prepare (commands.hpp:141-175), equalize_lengths (data.hpp:147-160),
+ * replacing the JSON bundle round trip (save_prepared / load_prepared, commands.hpp:30-74)
+ * that feeds Trainer(vector<SeriesRecord>).  The train CSV's lines are parsed by `threads`
+ * host threads (0 = all) with the reference's number parser (std::from_chars: values
+ * bit-identical); the kept series' last C + 2*O values land in one pinned host block,
+ * row-major n x (C + 2O), ready for esrnn_trainer_create (which uploads a pinned block
+ * with one async copy, no staging).  Errors: the reference's exception class and message
+ * for the first failing line in file order; the message via esrnn_ingest_last_error(). */
+typedef struct esrnn_dataset esrnn_dataset;
+typedef struct esrnn_ingest_stats {
+    int64_t raw_count;          /* series of the selected frequency before equalisation */
+    int64_t kept, dropped;
+    int32_t equalized_length;   /* C + 2*O */
+    double len_mean, len_stddev, len_min, len_q25, len_q50, len_q75, len_max;  /* LengthStats */
+} esrnn_ingest_stats;
+esrnn_status esrnn_ingest_m4_csv(const char* train_csv, const char* info_csv, int32_t frequency,
+                                 const esrnn_profile* profile, int32_t threads, esrnn_dataset** out,
+                                 esrnn_ingest_stats* stats);
+const char* esrnn_ingest_last_error(void);
+esrnn_status esrnn_dataset_shape(const esrnn_dataset* d, int64_t* n, int32_t* length);
+const double* esrnn_dataset_values(const esrnn_dataset* d);     /* n x length, row-major */
+const int32_t* esrnn_dataset_categories(const esrnn_dataset* d); /* n, data.hpp Category order */
+const char* esrnn_dataset_id(const esrnn_dataset* d, int64_t i);
+void esrnn_dataset_destroy(esrnn_dataset* d);
 
 #ifdef __cplusplus
 }

@@ -66,6 +66,10 @@ struct TrainConfig {
     int max_batch_size = 0;  // 0 -> 2048 (reference cap)
     int device = 0;
     bool use_graphs = true;
+    // opt-in level-variability penalty of Smyl's ES-RNN (the reference's loss is pinball
+    // only, trainer.hpp:581): lambda * O / M * sum over the batch's windows of the mean
+    // squared second difference of the window's series' log levels; 0 = reference
+    double level_variability_penalty = 0.0;
 
     void validate() const {
         const int cap = max_batch_size > 0 ? max_batch_size : 2048;
@@ -76,6 +80,8 @@ struct TrainConfig {
         if (learning_rate_network < 0.0 || learning_rate_per_series < 0.0)
             throw ConfigError("train: learning rates must be non-negative");
         if (gradient_clip && *gradient_clip <= 0.0) throw ConfigError("train: gradient_clip must be positive");
+        if (!(level_variability_penalty >= 0.0) || !std::isfinite(level_variability_penalty))
+            throw ConfigError("train: level_variability_penalty must be finite and >= 0");
     }
 };
 
@@ -601,6 +607,7 @@ private:
         c.max_batch_size = t.max_batch_size;
         c.device = t.device;
         c.use_graphs = t.use_graphs ? 0 : -1;
+        c.level_variability_penalty = t.level_variability_penalty;
         return c;
     }
 

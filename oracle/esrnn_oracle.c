@@ -214,6 +214,8 @@ static esrnn_status validate_config(const esrnn_profile* p, const esrnn_train_co
         return fail(err, ESRNN_CONFIG_ERROR, "train: learning rates must be non-negative");
     if (c->has_gradient_clip && c->gradient_clip <= 0.0)
         return fail(err, ESRNN_CONFIG_ERROR, "train: gradient_clip must be positive");
+    if (!(c->level_variability_penalty >= 0.0) || !isfinite(c->level_variability_penalty))
+        return fail(err, ESRNN_CONFIG_ERROR, "train: level_variability_penalty must be finite and >= 0");
     return ESRNN_OK;
 }
 
@@ -579,6 +581,40 @@ static void matmul_tn_acc(double* out, const double* a, const double* g, int m, 
         }
 }
 
+/* Level-variability penalty (B200 extension; NOT in the reference, whose loss is pinball
+ * only, trainer.hpp:581).  Smyl's M4 ES-RNN penalises the wiggliness of a series' levels
+ * ("penalizing dramatic changes in the level"): with u_t = log l_t over
+ * the train segment and e_t = u_t - 2 u_{t-1} + u_{t-2} (t = 2..T-1),
+ *     P(series) = mean_t e_t^2,
+ * and a batch adds  lambda * O / M * sum over its windows of P(window's series)  to the
+ * masked-mean pinball (M = unmasked target count; O / M = 1 / B without a mask), i.e. c_s *
+ * P(s) per distinct series with c_s = lambda * O * n_s / M.  Returns c * P; with lb != NULL
+ * adds d(c * P)/d l_t to the level adjoints. */
+static double lvp_series(const double* lv, int T, double c, double* lb) {
+    if (T < 3) return 0.0;
+    const double inv = 1.0 / (double)(T - 2);
+    double acc = 0.0;
+    for (int tt = 2; tt < T; ++tt) {
+        const double e = log(lv[tt]) - 2.0 * log(lv[tt - 1]) + log(lv[tt - 2]);
+        acc += e * e;
+        if (lb) {
+            const double q = c * 2.0 * inv * e;
+            lb[tt] += q / lv[tt];
+            lb[tt - 1] -= 2.0 * q / lv[tt - 1];
+            lb[tt - 2] += q / lv[tt - 2];
+        }
+    }
+    return c * acc * inv;
+}
+
+/* c_s = lambda * O * n_s / M for each slot (n_s = the slot's windows in the batch) */
+static double* lvp_weights(const esrnn_trainer* t, const work_t* w, double count) {
+    double* c = (double*)xcalloc(w->k, sizeof(double));
+    for (int b = 0; b < w->B; ++b) c[w->wslot[b]] += 1.0;
+    for (int s = 0; s < w->k; ++s) c[s] = t->cfg.level_variability_penalty * (double)t->O * c[s] / count;
+    return c;
+}
+
 /* Reverse sweep (autodiff.hpp:397-631) specialised to build_graph's graph: pinball
  * adjoint (:611-628), head/stack adjoints (MatMul :476-482, Logistic :483, Tanh :492,
  * Mul :450, Add :428, SliceCols :544, BroadcastRow :569), window gathers/normalisation
@@ -712,6 +748,11 @@ static void backward_batch(esrnn_trainer* t, work_t* w, const int32_t* anchors, 
             for (int j = 0; j < I; ++j)
                 sbar[(size_t)w->wslot[b] * (T + S) + anchors[b] - I + 1 + j] += sin_[(size_t)b * I + j];
         free(lg); free(sout); free(sin_);
+        if (t->cfg.level_variability_penalty > 0.0) {
+            double* c = lvp_weights(t, w, count);
+            for (int s = 0; s < k; ++s) lvp_series(w->lev + (size_t)s * T, T, c[s], lbar + (size_t)s * T);
+            free(c);
+        }
 
         /* reverse HW scan per slot (holt_winters.hpp:266-277 adjoints) */
         for (int s = 0; s < k; ++s) {
@@ -833,7 +874,12 @@ static esrnn_status run_batch_impl(esrnn_trainer* t, int32_t B, const int32_t* r
         const double d = w.tgt[e] - w.pred[e];
         acc += (d >= 0.0) ? t->cfg.tau * d : (t->cfg.tau - 1.0) * d;
     }
-    const double l = acc / count;
+    double l = acc / count;
+    if (t->cfg.level_variability_penalty > 0.0 && t->cfg.attach_es_state) {
+        double* c = lvp_weights(t, &w, count);
+        for (int s = 0; s < w.k; ++s) l += lvp_series(w.lev + (size_t)s * T, T, c[s], NULL);
+        free(c);
+    }
     if (loss) *loss = l;
     if (mask_count) *mask_count = count;
     if (inputs) memcpy(inputs, w.x, sizeof(double) * (size_t)B * in0);
@@ -1438,3 +1484,23 @@ esrnn_status esrnn_make_synthetic(uint64_t seed, int64_t n, int32_t length, int3
     free(season);
     return ESRNN_OK;
 }
+
+/* Ingestion: not restated in C -- its checker is the reference's own parser behind
+ * oracle/ref_shim.cpp (data.hpp:205-290 compiled where it lies). */
+struct esrnn_dataset { int unused; };
+const char* esrnn_ingest_last_error(void) { return "C oracle: ingestion is checked against the reference shim"; }
+esrnn_status esrnn_ingest_m4_csv(const char* train_csv, const char* info_csv, int32_t frequency,
+                                 const esrnn_profile* profile, int32_t threads, esrnn_dataset** out,
+                                 esrnn_ingest_stats* stats) {
+    (void)train_csv; (void)info_csv; (void)frequency; (void)profile; (void)threads; (void)stats;
+    *out = NULL;
+    return ESRNN_ERROR;
+}
+esrnn_status esrnn_dataset_shape(const esrnn_dataset* d, int64_t* n, int32_t* length) {
+    (void)d; *n = 0; *length = 0;
+    return ESRNN_ERROR;
+}
+const double* esrnn_dataset_values(const esrnn_dataset* d) { (void)d; return NULL; }
+const int32_t* esrnn_dataset_categories(const esrnn_dataset* d) { (void)d; return NULL; }
+const char* esrnn_dataset_id(const esrnn_dataset* d, int64_t i) { (void)d; (void)i; return NULL; }
+void esrnn_dataset_destroy(esrnn_dataset* d) { (void)d; }

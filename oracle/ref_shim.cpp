@@ -38,10 +38,17 @@
 #include <stdexcept>
 #include <string_view>
 #include <utility>
+#include <filesystem>
+#include <fstream>
+#include <iomanip>
+#include <iostream>
+#include <cstdlib>
+#include <json.hpp>
 
 #define private public
 #include "esrnn/trainer.hpp"
 #undef private
+#include "esrnn/commands.hpp"
 #include "helpers.hpp"
 
 #include "esrnn_b200.h"
@@ -129,6 +136,10 @@ esrnn_status esrnn_trainer_create(const esrnn_profile* profile, const esrnn_trai
     *out = nullptr;
     if (dist && dist->world_size > 1) {
         g_create_err = "reference shim: no sharded mode (the reference is single-threaded)";
+        return ESRNN_CONFIG_ERROR;
+    }
+    if (cfg->level_variability_penalty != 0.0) {
+        g_create_err = "reference shim: the reference has no level-variability penalty (trainer.hpp:581)";
         return ESRNN_CONFIG_ERROR;
     }
     auto h = std::make_unique<esrnn_trainer>();
@@ -559,6 +570,69 @@ esrnn_status esrnn_nccl_unique_id(uint8_t*) {
     g_create_err = "reference shim: no NCCL";
     return ESRNN_NCCL_ERROR;
 }
+
+// Ingestion (esrnn_b200.h): the reference's own cmd_prepare data path (commands.hpp:141-175)
+// -- parse_m4_train_csv, parse_info_csv, apply_info, the frequency filter, length_stats,
+// equalize_lengths -- without the bundle file; the checker for the engine's parallel parser.
+struct esrnn_dataset {
+    std::vector<SeriesRecord> kept;
+    std::vector<double> values;
+    std::vector<int32_t> cats;
+};
+static thread_local std::string g_ingest_err;
+const char* esrnn_ingest_last_error(void) { return g_ingest_err.c_str(); }
+esrnn_status esrnn_ingest_m4_csv(const char* train_csv, const char* info_csv, int32_t frequency,
+                                 const esrnn_profile* profile, int32_t, esrnn_dataset** out,
+                                 esrnn_ingest_stats* stats) {
+    *out = nullptr;
+    auto ds = std::make_unique<esrnn_dataset>();
+    esrnn_status st = guarded(g_ingest_err, [&] {
+        std::ifstream train_in(train_csv);
+        if (!train_in) throw Error("cannot open \"" + std::string(train_csv) + "\"");
+        std::ifstream info_in(info_csv);
+        if (!info_in) throw Error("cannot open \"" + std::string(info_csv) + "\"");
+        auto series = parse_m4_train_csv(train_in);
+        auto info = parse_info_csv(info_in);
+        apply_info(series, info);
+        std::vector<SeriesRecord> filtered;
+        for (auto& s : series)
+            if (s.frequency == static_cast<Frequency>(frequency)) filtered.push_back(std::move(s));
+        std::vector<std::size_t> raw_lengths;
+        for (const auto& s : filtered) raw_lengths.push_back(s.values.size());
+        const LengthStats raw = length_stats(raw_lengths);
+        FrequencyProfile p = FrequencyProfile::defaults(static_cast<Frequency>(frequency));
+        p.horizon = profile->horizon;
+        p.min_length = profile->min_length;
+        ds->kept = equalize_lengths(std::move(filtered), p);
+        if (ds->kept.empty()) throw ValidationError("no series after filtering");
+        for (const auto& s : ds->kept) {
+            ds->values.insert(ds->values.end(), s.values.begin(), s.values.end());
+            ds->cats.push_back(static_cast<int32_t>(s.category.value_or(Category::Other)));
+        }
+        if (stats) {
+            *stats = esrnn_ingest_stats{};
+            stats->raw_count = static_cast<int64_t>(raw.count);
+            stats->kept = static_cast<int64_t>(ds->kept.size());
+            stats->dropped = stats->raw_count - stats->kept;
+            stats->equalized_length = p.equalized_length();
+            stats->len_mean = raw.mean, stats->len_stddev = raw.stddev, stats->len_min = raw.min;
+            stats->len_q25 = raw.q25, stats->len_q50 = raw.q50, stats->len_q75 = raw.q75, stats->len_max = raw.max;
+        }
+    });
+    if (st == ESRNN_OK) *out = ds.release();
+    return st;
+}
+esrnn_status esrnn_dataset_shape(const esrnn_dataset* d, int64_t* n, int32_t* length) {
+    *n = static_cast<int64_t>(d->kept.size());
+    *length = d->kept.empty() ? 0 : static_cast<int32_t>(d->kept[0].values.size());
+    return ESRNN_OK;
+}
+const double* esrnn_dataset_values(const esrnn_dataset* d) { return d->values.data(); }
+const int32_t* esrnn_dataset_categories(const esrnn_dataset* d) { return d->cats.data(); }
+const char* esrnn_dataset_id(const esrnn_dataset* d, int64_t i) {
+    return (i >= 0 && i < static_cast<int64_t>(d->kept.size())) ? d->kept[static_cast<size_t>(i)].id.c_str() : nullptr;
+}
+void esrnn_dataset_destroy(esrnn_dataset* d) { delete d; }
 
 esrnn_status esrnn_make_synthetic(uint64_t seed, int64_t n, int32_t length, int32_t season_length,
                                   double noise_sigma, double* values, int32_t* category) {

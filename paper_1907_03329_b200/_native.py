@@ -40,6 +40,13 @@ class Profile(C.Structure):
     ]
 
 
+class IngestStats(C.Structure):  # esrnn_ingest_stats
+    _fields_ = [("raw_count", C.c_int64), ("kept", C.c_int64), ("dropped", C.c_int64),
+                ("equalized_length", C.c_int32), ("len_mean", C.c_double), ("len_stddev", C.c_double),
+                ("len_min", C.c_double), ("len_q25", C.c_double), ("len_q50", C.c_double),
+                ("len_q75", C.c_double), ("len_max", C.c_double)]
+
+
 class TrainCfg(C.Structure):
     _fields_ = [
         ("epochs", C.c_int32),
@@ -57,6 +64,7 @@ class TrainCfg(C.Structure):
         ("max_batch_size", C.c_int32),
         ("device", C.c_int32),
         ("use_graphs", C.c_int32),
+        ("level_variability_penalty", C.c_double),
     ]
 
 
@@ -152,6 +160,20 @@ class NativeApi:
         L.esrnn_trainer_gather_per_series.argtypes = [_vp, _dp, _dp, _dp]
         L.esrnn_release_cached_memory.argtypes = []
         L.esrnn_make_synthetic.argtypes = [C.c_uint64, C.c_int64, C.c_int32, C.c_int32, C.c_double, _dp, _ip]
+        L.esrnn_ingest_m4_csv.argtypes = [C.c_char_p, C.c_char_p, C.c_int32, C.POINTER(Profile), C.c_int32,
+                                          C.POINTER(_vp), C.POINTER(IngestStats)]
+        L.esrnn_ingest_m4_csv.restype = C.c_int
+        L.esrnn_ingest_last_error.restype = C.c_char_p
+        L.esrnn_dataset_shape.argtypes = [_vp, C.POINTER(C.c_int64), C.POINTER(C.c_int32)]
+        L.esrnn_dataset_shape.restype = C.c_int
+        L.esrnn_dataset_values.argtypes = [_vp]
+        L.esrnn_dataset_values.restype = _dp
+        L.esrnn_dataset_categories.argtypes = [_vp]
+        L.esrnn_dataset_categories.restype = _ip
+        L.esrnn_dataset_id.argtypes = [_vp, C.c_int64]
+        L.esrnn_dataset_id.restype = C.c_char_p
+        L.esrnn_dataset_destroy.argtypes = [_vp]
+        L.esrnn_dataset_destroy.restype = None
         for fn in ("esrnn_trainer_create", "esrnn_trainer_shard", "esrnn_trainer_param_count",
                    "esrnn_trainer_param_info", "esrnn_trainer_get_weights", "esrnn_trainer_set_weights",
                    "esrnn_trainer_get_per_series", "esrnn_trainer_set_per_series", "esrnn_trainer_train_epoch",

@@ -64,8 +64,9 @@ def build_engine(force: bool = False) -> Path:
         objs.append(str(obj))
     for src in sorted(CSRC.glob("*.cpp")):
         obj = BUILD / (src.stem + ".o")
-        opt = "-O3" if src.stem == "mt64" else "-O2"
-        _run(["g++", "-std=c++17", opt, "-fPIC", "-ffp-contract=off", "-I" + str(INC), "-c", str(src), "-o", str(obj)])
+        opt = "-O3" if src.stem in ("mt64", "ingest") else "-O2"
+        _run(["g++", "-std=c++17", opt, "-fPIC", "-pthread", "-ffp-contract=off", "-I" + str(INC),
+              "-I" + str(Path(NVCC).parent.parent / "include"), "-c", str(src), "-o", str(obj)])
         objs.append(str(obj))
     # Link the NCCL that torch bundles (2.28.x) so a process that also imports torch sees one
     # libnccl.so.2; fall back to the system copy (2.27.3) when the wheel is absent.

@@ -99,6 +99,7 @@ struct StateDev {
     long long* coll_seq;    // in-process group collective: calls completed (collective.cuh)
     Real* psg;              // [kcap][2+S]
     double* es_sq_part;     // [es blocks]
+    double* es_pen_part;    // [es blocks] level-variability penalty, in pinball-sum units (x M)
     double* red_sq_part;    // [weight-gradient tiles]
     Real* gpart;            // [gsplit][tiles][32 lanes][6]: row-part tile partials (large steps)
     unsigned* gtile_ctr;    // [tiles] arrival tickets of a tile's row parts
@@ -118,6 +119,7 @@ struct StateDev {
     Real* d_seas;
     Real* d_levels;
     double tau, lr_net, lr_ps, clip;
+    double lvp;             // level-variability penalty weight (0: off, the reference's loss)
     int has_clip, attach;
     long long* dbg_clk;     // optional phase timestamps (ESRNN_DEBUG_CLOCKS), block 0 thread 0
     long long* spans;       // optional in-graph kernel spans [step][kSpanKinds][2]: earliest

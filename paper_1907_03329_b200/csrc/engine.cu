@@ -257,7 +257,7 @@ struct esrnn_trainer {
     DBuf<int> ps_steps;
     DBuf<unsigned char> lv, se, contrib, rowstore, gbuf, psg, d_inputs, d_targets, d_seas, d_levels;
     DBuf<unsigned char> fX, fL, fS, dump_lv, dump_se;
-    DBuf<double> loss_part, es_sq_part, red_sq_part, scal, loss_hist, f_out, f_smape, f_score, smape_sum, gtail;
+    DBuf<double> loss_part, es_sq_part, es_pen_part, red_sq_part, scal, loss_hist, f_out, f_smape, f_score, smape_sum, gtail;
     DBuf<long long> coll_seq;
     DBuf<unsigned int> done_ctr, gtile_ctr;
     DBuf<unsigned char> gpart;
@@ -336,7 +336,7 @@ struct esrnn_trainer {
              ...);
         };
         add(vals, vrm, ps, ps_m, ps_v, theta, mW, vW, cat, ps_steps, lv, se, contrib, rowstore, gbuf, psg, d_inputs,
-            d_targets, d_seas, d_levels, fX, fL, fS, dump_lv, dump_se, loss_part, es_sq_part, red_sq_part, scal,
+            d_targets, d_seas, d_levels, fX, fL, fS, dump_lv, dump_se, loss_part, es_sq_part, es_pen_part, red_sq_part, scal,
             loss_hist, f_out, f_smape, f_score, smape_sum, done_ctr, gtile_ctr, gpart, net_step, dbg_clk, errw, gtail,
             coll_seq, spans);
         for (DevPlan* d : {&epoch_plan, &batch_plan})
@@ -391,6 +391,7 @@ struct esrnn_trainer {
         s.coll_seq = coll_seq.p;
         s.psg = reinterpret_cast<Real*>(psg.p);
         s.es_sq_part = es_sq_part.p;
+        s.es_pen_part = es_pen_part.p;
         s.red_sq_part = red_sq_part.p;
         s.gpart = reinterpret_cast<Real*>(gpart.p);
         s.gtile_ctr = gtile_ctr.p;
@@ -412,6 +413,9 @@ struct esrnn_trainer {
         s.clip = cfg.gradient_clip;
         s.has_clip = cfg.has_gradient_clip ? 1 : 0;
         s.attach = cfg.attach_es_state ? 1 : 0;
+        // the penalty regularises the ES state: with detached ES state it has no gradient and
+        // is omitted (oracle/esrnn_oracle.c lvp_series)
+        s.lvp = cfg.attach_es_state ? cfg.level_variability_penalty : 0.0;
         s.dbg_clk = dbg_clk.p;
         s.spans = span_mode ? spans.p : nullptr;
         return s;
@@ -466,6 +470,8 @@ void validate_config(const esrnn_profile& p, const esrnn_train_config& c) {
     if (c.learning_rate_network < 0.0 || c.learning_rate_per_series < 0.0)
         raise(ESRNN_CONFIG_ERROR, "train: learning rates must be non-negative");
     if (c.has_gradient_clip && c.gradient_clip <= 0.0) raise(ESRNN_CONFIG_ERROR, "train: gradient_clip must be positive");
+    if (!(c.level_variability_penalty >= 0.0) || !std::isfinite(c.level_variability_penalty))
+        raise(ESRNN_CONFIG_ERROR, "train: level_variability_penalty must be finite and >= 0");
     // device-kernel limits (shared-memory tiles are sized from these)
     if (p.hidden_size > 80) raise(ESRNN_CONFIG_ERROR, "profile: hidden_size > 80 unsupported by the B200 kernels");
     if (p.seasonality_length > 64) raise(ESRNN_CONFIG_ERROR, "profile: seasonality > 64 unsupported by the B200 kernels");
@@ -729,6 +735,7 @@ void ensure_capacity(Eng* e, int B) {
     e->loss_part.alloc(e->tiles_cap);
     e->psg.alloc(r * static_cast<size_t>(kc) * (2 + S));
     e->es_sq_part.alloc(e->es_blocks);
+    e->es_pen_part.alloc(e->es_blocks);
     e->d_inputs.alloc(r * static_cast<size_t>(B) * e->in0);
     e->d_targets.alloc(r * static_cast<size_t>(B) * O);
     e->d_seas.alloc(r * static_cast<size_t>(B) * O);
@@ -898,8 +905,12 @@ size_t finish_smem(const NetLayout& lay) {
     const size_t cwp = (lay.I + lay.O + 2 + 3) & ~3;
     const size_t bd = kEsSlotsPerBlock;
     const size_t es = sizeof(double) * bd * (static_cast<size_t>(lay.T | 1) + static_cast<size_t>((lay.T + lay.S) | 1)) +
-                      sizeof(double) * bd * 2 * static_cast<size_t>(lay.T) + sizeof(Real) * bd * row_pad<Real>(lay.T) +
-                      sizeof(double) * kEsChunk * cwp;
+                      (sizeof(Real) == 4 && lay.S == 1 ? sizeof(double) : sizeof(Real)) * bd * 2 * static_cast<size_t>(lay.T) +
+                      sizeof(Real) * bd * row_pad<Real>(lay.T) +
+                      std::max(sizeof(double) * kEsChunk * cwp,  // staged contributions, then (fp32)
+                               sizeof(Real) == 4 ? (lay.S == 1 ? sizeof(double) : sizeof(float)) * 4 * bd *
+                                                       static_cast<size_t>(lay.T)
+                                                 : 0);  // the scan's coefficients (finish.cuh)
     const size_t gemm = sizeof(Real) * (static_cast<size_t>(kGBuf * kGChunk) * (kGq + kGk) + (kFinishThreads / 32) * 32 * 6);
     return std::max(es, gemm);
 }
@@ -1170,9 +1181,17 @@ void upload_values(Eng* e, const double* values, const int32_t* category) {
         // waking it costs more than the copy)
         DBuf<double>& raw = e->stage_raw;
         raw.alloc(static_cast<size_t>(N) * LEN);
-        e->stage_pin.reserve(raw.n);
-        std::memcpy(e->stage_pin.p, values + static_cast<size_t>(e->row0) * LEN, sizeof(double) * raw.n);
-        CUDA_OK(cudaMemcpyAsync(raw.p, e->stage_pin.p, sizeof(double) * raw.n, cudaMemcpyHostToDevice, e->stream));
+        const double* src = values + static_cast<size_t>(e->row0) * LEN;
+        // a pinned source (esrnn_ingest_m4_csv's dataset block) is copied from directly
+        cudaPointerAttributes pa{};
+        const bool pinned = cudaPointerGetAttributes(&pa, src) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+        cudaGetLastError();
+        if (!pinned) {
+            e->stage_pin.reserve(raw.n);
+            std::memcpy(e->stage_pin.p, src, sizeof(double) * raw.n);
+            src = e->stage_pin.p;
+        }
+        CUDA_OK(cudaMemcpyAsync(raw.p, src, sizeof(double) * raw.n, cudaMemcpyHostToDevice, e->stream));
         const long long n = static_cast<long long>(N) * e->ldv;
         k_layout_values<Real><<<static_cast<int>((n + 255) / 256), 256, 0, e->stream>>>(
             raw.p, N, LEN, e->ldv, reinterpret_cast<Real*>(e->vals.p), reinterpret_cast<Real*>(e->vrm.p));
@@ -1570,8 +1589,11 @@ void run_batch_impl(Eng* e, int32_t B, const int32_t* rows, const int32_t* ancho
     const bool grads = (flags & ESRNN_BATCH_GRADS) != 0;
     const bool update = grads && (flags & ESRNN_BATCH_UPDATE) != 0;
     CUDA_OK(cudaEventRecord(e->ev0, e->stream));
+    // the level-variability penalty is formed in K3's ES blocks: a penalised batch_loss
+    // runs the gradient path (no update) to get it
+    const bool k3 = grads || st.lvp > 0.0;
     if (Bl > 0 || e->world > 1) {
-        launch_step<Real>(e, pv, 0, grads, update, st);
+        launch_step<Real>(e, pv, 0, k3, update, st);
     }
     CUDA_OK(cudaEventRecord(e->ev1, e->stream));
     CUDA_OK(cudaGetLastError());
@@ -1583,7 +1605,7 @@ void run_batch_impl(Eng* e, int32_t B, const int32_t* rows, const int32_t* ancho
     throw_device_error(e);
     // loss: sum of tile partials (single GPU) or all-reduced sum (sharded) / M
     double lsum = 0.0;
-    if (grads && e->sharded) {
+    if (k3 && (e->sharded || st.lvp > 0.0)) {  // K3 / K4 / the collective wrote the step's loss sum
         double g2[2];
         CUDA_OK(cudaMemcpy(g2, e->gtail.p, sizeof g2, cudaMemcpyDeviceToHost));
         lsum = g2[1];

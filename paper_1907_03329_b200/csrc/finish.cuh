@@ -19,6 +19,9 @@ constexpr int kEsChunk = 128;         // contribution rows staged per round
 constexpr int kGq = 16, kGk = 8;      // K3 GEMM output block (gate rows x input features)
 constexpr int kGChunk = 256;          // row-store rows staged per round
 constexpr int kGBuf = 3;              // staging ring depth (kGBuf - 1 chunks in flight)
+// fp32 mode with S = 1: K3's ES blocks recompute the forward states in double (see there)
+template <typename Real, int SC>
+constexpr bool kEsRecompute = sizeof(Real) == 4 && SC == 1;
 
 // clip scale (trainer.hpp:603-615), global Adam step and bias corrections (:617-620),
 // step loss (masked mean, autodiff.hpp:392).  err_any: some rank's error word is set (the
@@ -52,6 +55,7 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
     pdl_trigger();
     const int tid = threadIdx.x;
     double sq = 0.0;
+    double pen = 0.0;  // level-variability penalty of this thread's slot (pinball-sum units)
     // ESRNN_DEBUG_CLOCKS: ES block 0 stamps at [32, 40), reduce block 0 at [48, 56)
     const int dbg_base = blockIdx.x == 0 ? 32 : (static_cast<int>(blockIdx.x) == es_blocks ? 48 : -1);
     int fdbg = 0;
@@ -82,14 +86,16 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
             const int ldl = T | 1, lds = (T + S) | 1;
             double* LB = reinterpret_cast<double*>(smem_raw);                  // [bd][ldl] level adjoint
             double* SB = LB + bd * ldl;                                        // [bd][lds] seasonality adjoint
-            double* LV = SB + bd * lds;                                        // [T][bd]   forward levels
-            double* SE = LV + T * bd;                                          // [T][bd]   forward seasonalities
+            // forward states: double when K3 recomputes them (fp32, S = 1) or in fp64 mode
+            using SR = std::conditional_t<kEsRecompute<Real, SC>, double, Real>;
+            SR* LV = reinterpret_cast<SR*>(SB + bd * lds);                     // [T][bd]   forward levels
+            SR* SE = LV + T * bd;                                              // [T][bd]   forward seasonalities
             Real* YS = reinterpret_cast<Real*>(SE + T * bd);                   // [bd][tp]  observation rows
             double* cbuf = reinterpret_cast<double*>(YS + bd * tp);            // [kEsChunk][cwp]
             double* lb = LB + tid * ldl;
             double* sb = SB + tid * lds;
-            double* lvs = LV + tid;
-            double* ses = SE + tid;
+            SR* lvs = LV + tid;
+            SR* ses = SE + tid;
             Real* ys = YS + tid * tp;
             FCLK();
             // ---- stage the forward state with the whole block (every copy in flight at once) ----
@@ -104,15 +110,18 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
             Real a_raw = 0, g_raw = 0;
             Real s0[SC > 0 ? SC : 1];  // exp(seas_raw) for the output's chain rule, loaded up front
             double l0 = 0;             // l[-1] = mean(y[0:S]) (holt_winters.hpp:247-250)
-            if constexpr (sizeof(Real) == 4) {
-                // fp32 mode: the forward levels / seasonalities the adjoint is linearised at are
-                // recomputed here in double (the reference's arithmetic) instead of taken from
-                // K2's fp32 scan.  The adjoint sums of a series' window terms cancel almost
+            if constexpr (kEsRecompute<Real, SC>) {
+                // fp32 mode, S = 1: the forward levels / seasonalities the adjoint is linearised
+                // at are recomputed here in double (the reference's arithmetic) instead of taken
+                // from K2's fp32 scan.  The adjoint sums of a series' window terms cancel almost
                 // exactly (x = y/(s*l) is invariant under s -> c*s, l -> l/c except through
-                // l[-1]); linearised at fp32-rounded states the init-seasonality gradient of an
-                // S = 1 series is off by ~1e-3 of its tensor, at double states by ~1e-7.
-                // Runs before the dependency wait, overlapping K2: the per-series parameters are
-                // the previous step's K4 output (complete before K2 started), read at L2.
+                // l[-1]); with a single seasonal index that mode is the init seasonality itself,
+                // and linearised at fp32-rounded states its gradient is off by ~1e-3 of its
+                // tensor (at double states ~1e-7).  For S > 1 the fp32 states keep it ~1e-7
+                // (oracle emulation), so K2's published states are used (a T = 72 double
+                // recompute costs ~20 us of serial latency).  Runs before the dependency wait,
+                // overlapping K2: the per-series parameters are the previous step's K4 output
+                // (complete before K2 passed its own wait and released this grid), read at L2.
                 cp_async_wait_all();
                 __syncthreads();
                 if (mine) {
@@ -140,7 +149,7 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
             pdl_wait();
             DBG_SPAN_MIN(st, s, 4);
             SPAN_BEGIN(st, s, kSpanFinish);
-            if constexpr (sizeof(Real) == 8) {
+            if constexpr (!kEsRecompute<Real, SC>) {
                 if (mine) {
                     a_raw = st.ps[lrow];
                     g_raw = st.ps[N + lrow];
@@ -149,14 +158,13 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
                         for (int j = 0; j < SC; ++j) s0[j] = st.ps[(size_t)(2 + j) * N + lrow];
                     }
                 }
-                // forward levels / seasonalities of the block's slots from K2's fp64 scan: whole
+                // forward levels / seasonalities of the block's slots from K2's scan: whole
                 // 16-byte pieces of the [t][kcap] rows (kcap and sl0 are multiples of
                 // kEsSlotsPerBlock)
                 for (int e = tid; e < 2 * T * (bd / e16); e += kFinishThreads) {
                     const int half = e / (T * (bd / e16)), r = e - half * T * (bd / e16);
                     const int t = r / (bd / e16), ch = r - t * (bd / e16);
-                    cp_async16(reinterpret_cast<Real*>(half ? SE : LV) + t * bd + ch * e16,
-                               (half ? st.se : st.lv) + (size_t)t * kc + sl0 + ch * e16);
+                    cp_async16((half ? SE : LV) + t * bd + ch * e16, (half ? st.se : st.lv) + (size_t)t * kc + sl0 + ch * e16);
                 }
             }
             // ---- window adjoints: this block's windows are one contiguous range of the
@@ -198,88 +206,188 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
                 cp_async_wait_all();
                 __syncthreads();
             }
-            FCLK();
+            // ---- per-slot prologue (scanning threads): alpha, gamma, l[-1], the penalty ----
+            __shared__ double es_coef[3][kEsSlotsPerBlock];  // alpha, gamma, l[-1] per slot
+            using MD = Math<double>;
+            const double alpha = mine ? MD::logistic(static_cast<double>(a_raw)) : 0.0;
+            const double gamma = mine ? MD::logistic(static_cast<double>(g_raw)) : 0.0;
+            const double oma = 1.0 - alpha, omg = 1.0 - gamma;
             if (mine) {
-                // the adjoint recursion in double, linearised at double forward states (fp64:
-                // K2's scan; fp32: the recomputation above)
-                using MD = Math<double>;
-                const double alpha = MD::logistic(static_cast<double>(a_raw));
-                const double gamma = MD::logistic(static_cast<double>(g_raw));
-                const double oma = 1.0 - alpha, omg = 1.0 - gamma;
-                const int row = lrow;
                 cp_async_wait_all();
                 FCLK();
-                if constexpr (sizeof(Real) == 8) {
+                if constexpr (!kEsRecompute<Real, SC>) {
                     Real l0r = 0;
                     for (int j = 0; j < S; ++j) l0r += ys[j];
                     l0 = static_cast<double>(l0r / Real(S));
                 }
-
-                double abar = 0, gbar = 0, omab = 0, omgb = 0;
-                // the staged per-slot sums are LOG adjoints (tile.cuh): the steps below divide
-                // them by the forward states as they reach them
-                double lbn = lb[T - 1] / lvs[(T - 1) * bd];  // running adjoint of l[t]
-                // a / b: IEEE in fp64 mode (the reference's arithmetic); times the reciprocal
-                // (computed off the dependency chain) in fp32 mode
-                auto dv = [](double a, double b, double rb) -> double {
-                    if constexpr (sizeof(Real) == 4) return a * rb;
-                    else return a / b;
-                };
-                // one reverse step (t > 0 unless FIRST): Sb = final adjoint of s[t+S],
-                // returns the final adjoint of s[t]
-                auto step = [&](int t, double Sb, auto first) -> double {
-                    constexpr bool kFirst = decltype(first)::value;
-                    const double yt = static_cast<double>(ys[t]);
-                    const double lp = kFirst ? l0 : static_cast<double>(lvs[(t - 1) * bd]);
-                    const double s_t = static_cast<double>(ses[t * bd]);
-                    const double rlp = 1.0 / lp, rst = 1.0 / s_t;
-                    double sbt = dv(sb[t], s_t, rst);
-                    // s_{t+S} = gamma*(y/lp) + (1-gamma)*s_t
-                    omgb += Sb * s_t;
-                    sbt += Sb * omg;
-                    const double d2 = dv(yt, lp, rlp);
-                    gbar += Sb * d2;
-                    // l_t = alpha*(y/s_t) + (1-alpha)*lp
-                    const double Lb = lbn;
-                    omab += Lb * lp;
-                    const double d1 = dv(yt, s_t, rst);
-                    abar += Lb * d1;
-                    sbt -= dv((Lb * alpha) * d1, s_t, rst);
-                    if constexpr (!kFirst) {
-                        const double d2b = Sb * gamma;
-                        lbn = dv(lb[t - 1], lp, rlp) - dv(d2b * d2, lp, rlp) + Lb * oma;
+                if (st.lvp > 0.0 && T >= 3) {
+                    // opt-in level-variability penalty (oracle/esrnn_oracle.c lvp_series): with
+                    // u_t = log l_t and e_t = u_t - 2 u_{t-1} + u_{t-2}, this slot adds
+                    // c * mean_t e_t^2, c = lambda * O * (its windows) / M; its adjoint enters the
+                    // LOG level adjoints directly (d/du_t; divided by l_t below)
+                    const int nw = pl.slot_win_off[k0 + slot + 1] - pl.slot_win_off[k0 + slot];
+                    const double cs = st.lvp * O * nw, c = cs / pl.step_M[s], inv = 1.0 / (T - 2);
+                    double um2 = ::log(static_cast<double>(lvs[0])), um1 = ::log(static_cast<double>(lvs[bd])), acc = 0.0;
+                    for (int t = 2; t < T; ++t) {
+                        const double u = ::log(static_cast<double>(lvs[t * bd]));
+                        const double e = u - 2.0 * um1 + um2;
+                        acc += e * e;
+                        const double q = c * 2.0 * inv * e;
+                        lb[t] += q;
+                        lb[t - 1] -= 2.0 * q;
+                        lb[t - 2] += q;
+                        um2 = um1;
+                        um1 = u;
                     }
-                    return sbt;
-                };
+                    pen = cs * acc * inv;  // x M: the loss-sum units of loss_part
+                }
+                es_coef[0][tid] = alpha;
+                es_coef[1][tid] = gamma;
+                es_coef[2][tid] = l0;
+            }
+            // fp32: the recursion's per-step coefficients, formed by the whole block (8 warps)
+            // so that the single scanning warp's serial loop is 4 dependent-free loads and 4
+            // DFMAs per step (inline, its two IEEE double divisions per step alone cost ~80
+            // cycles each).  With l' = l[t-1] (l[-1] = mean(y[0:S])):
+            //   lb[t] <- lb[t] / l_t,  sb[t] <- sb[t] / s_t      (log adjoints -> adjoints)
+            //   K1 = alpha y_t / s_t^2,  K2 = gamma y_t / l'^2,  CA = y_t / s_t - l',  CG = y_t / l' - s_t
+            // in the dead contribution staging region; double for the recomputed (S = 1)
+            // states, fp32 otherwise (coefficient rounding perturbs like the states' own).
+            using CR = std::conditional_t<kEsRecompute<Real, SC>, double, float>;
+            CR* K1 = reinterpret_cast<CR*>(cbuf);
+            CR* K2 = K1 + T * bd;
+            CR* CA = K2 + T * bd;
+            CR* CG = CA + T * bd;
+            if constexpr (sizeof(Real) == 4) {
+                __syncthreads();
+                const int nsl = sl1 - sl0;
+                for (int e = tid; e < T * bd; e += kFinishThreads) {
+                    const int t = e / bd, sl = e - t * bd;
+                    if (sl >= nsl) continue;
+                    const double y = static_cast<double>(YS[sl * tp + t]);
+                    const double lv = static_cast<double>(LV[e]), sv = static_cast<double>(SE[e]);
+                    const double lpv = t > 0 ? static_cast<double>(LV[e - bd]) : es_coef[2][sl];
+                    double rs, rl, ri;
+                    if constexpr (kEsRecompute<Real, SC>) {
+                        rs = 1.0 / sv, rl = 1.0 / lpv, ri = 1.0 / lv;
+                    } else {  // fp32 states: their correctly rounded fp32 reciprocals
+                        rs = __frcp_rn(static_cast<float>(sv));
+                        rl = __frcp_rn(static_cast<float>(lpv));
+                        ri = __frcp_rn(static_cast<float>(lv));
+                    }
+                    LB[sl * ldl + t] *= ri;
+                    SB[sl * lds + t] *= rs;
+                    const double yrs = y * rs, yrl = y * rl;
+                    K1[e] = static_cast<CR>(es_coef[0][sl] * yrs * rs);
+                    K2[e] = static_cast<CR>(es_coef[1][sl] * yrl * rl);
+                    CA[e] = static_cast<CR>(yrs - lpv);
+                    CG[e] = static_cast<CR>(yrl - sv);
+                }
+                __syncthreads();
+            }
+            FCLK();
+            if (mine) {
+                const int row = lrow;
+                double abar = 0, gbar = 0, omab = 0, omgb = 0;
+                double sfin[SC > 0 ? SC : 1];
                 using Mid = std::integral_constant<bool, false>;
                 using First = std::integral_constant<bool, true>;
-                double sfin[SC > 0 ? SC : 1];
-                if constexpr (SC > 0) {
-                    // register ring: rg[j] holds the final adjoint of the latest s index = j (mod S);
-                    // full groups of SC steps are branch-free so consecutive steps interleave
-                    double rg[SC];
+                if constexpr (sizeof(Real) == 4) {
+                    // reverse recursion (holt_winters.hpp:266-277 adjoints) on the coefficients:
+                    //   sb_t(final) = sb[t] + Sb omg - Lb K1_t,   Lb_{t-1} = lb[t-1] + Lb oma - Sb K2_t,
+                    //   abar - omab += Lb CA_t,   gbar - omgb += Sb CG_t
+                    // (Sb = final adjoint of s[t+S]).  Only loads in the loop (no smem stores for
+                    // the ring path), so they issue ahead of the one-DFMA-per-step chain.
+                    double lbn = lb[T - 1];
+                    auto step = [&](int t, double Sb, auto first) -> double {
+                        constexpr bool kFirst = decltype(first)::value;
+                        const double Lb = lbn;
+                        const int e = t * bd + tid;
+                        const double sbt = (sb[t] + Sb * omg) - Lb * static_cast<double>(K1[e]);
+                        if constexpr (!kFirst) lbn = (lb[t - 1] - Sb * static_cast<double>(K2[e])) + Lb * oma;
+                        abar += Lb * static_cast<double>(CA[e]);
+                        gbar += Sb * static_cast<double>(CG[e]);
+                        return sbt;
+                    };
+                    if constexpr (SC > 0) {
+                        double rg[SC];
 #pragma unroll
-                    for (int j = 0; j < SC; ++j) rg[j] = 0;  // s[T..T+S) receive no adjoint
-                    int base = ((T - 1) / SC) * SC;
-                    if (base > 0) {
+                        for (int j = 0; j < SC; ++j) rg[j] = 0;  // s[T..T+S) receive no adjoint
+                        int base = ((T - 1) / SC) * SC;
+                        if (base > 0) {
 #pragma unroll
-                        for (int jj = SC - 1; jj >= 0; --jj)
-                            if (base + jj < T) rg[jj] = step(base + jj, rg[jj], Mid{});
-                        for (base -= SC; base > 0; base -= SC) {
+                            for (int jj = SC - 1; jj >= 0; --jj)
+                                if (base + jj < T) rg[jj] = step(base + jj, rg[jj], Mid{});
+                            for (base -= SC; base > 0; base -= SC) {
 #pragma unroll
-                            for (int jj = SC - 1; jj >= 0; --jj) rg[jj] = step(base + jj, rg[jj], Mid{});
+                                for (int jj = SC - 1; jj >= 0; --jj) rg[jj] = step(base + jj, rg[jj], Mid{});
+                            }
                         }
+#pragma unroll
+                        for (int jj = SC - 1; jj >= 1; --jj)
+                            if (jj < T) rg[jj] = step(jj, rg[jj], Mid{});
+                        rg[0] = step(0, rg[0], First{});
+#pragma unroll
+                        for (int j = 0; j < SC; ++j) sfin[j] = rg[j];
+                    } else {
+                        for (int t = T - 1; t >= 1; --t) sb[t] = step(t, sb[t + S], Mid{});
+                        sb[0] = step(0, sb[S], First{});
                     }
-#pragma unroll
-                    for (int jj = SC - 1; jj >= 1; --jj)
-                        if (jj < T) rg[jj] = step(jj, rg[jj], Mid{});
-                    rg[0] = step(0, rg[0], First{});
-#pragma unroll
-                    for (int j = 0; j < SC; ++j) sfin[j] = rg[j];
                 } else {
+                    // fp64: the reference's arithmetic (IEEE divisions), linearised at K2's states
+                    double lbn = lb[T - 1] / lvs[(T - 1) * bd];  // running adjoint of l[t]
+                    // one reverse step (t > 0 unless FIRST): Sb = final adjoint of s[t+S],
+                    // returns the final adjoint of s[t]
+                    auto step = [&](int t, double Sb, auto first) -> double {
+                        constexpr bool kFirst = decltype(first)::value;
+                        const double yt = ys[t];
+                        const double lp = kFirst ? l0 : lvs[(t - 1) * bd];
+                        const double s_t = ses[t * bd];
+                        double sbt = sb[t] / s_t;
+                        // s_{t+S} = gamma*(y/lp) + (1-gamma)*s_t
+                        omgb += Sb * s_t;
+                        sbt += Sb * omg;
+                        const double d2 = yt / lp;
+                        gbar += Sb * d2;
+                        // l_t = alpha*(y/s_t) + (1-alpha)*lp
+                        const double Lb = lbn;
+                        omab += Lb * lp;
+                        const double d1 = yt / s_t;
+                        abar += Lb * d1;
+                        sbt -= ((Lb * alpha) * d1) / s_t;
+                        if constexpr (!kFirst) {
+                            const double d2b = Sb * gamma;
+                            lbn = lb[t - 1] / lp - (d2b * d2) / lp + Lb * oma;
+                        }
+                        return sbt;
+                    };
+                    if constexpr (SC > 0) {
+                        // register ring: rg[j] holds the final adjoint of the latest s index = j
+                        // (mod S); full groups of SC steps are branch-free so steps interleave
+                        double rg[SC];
+#pragma unroll
+                        for (int j = 0; j < SC; ++j) rg[j] = 0;  // s[T..T+S) receive no adjoint
+                        int base = ((T - 1) / SC) * SC;
+                        if (base > 0) {
+#pragma unroll
+                            for (int jj = SC - 1; jj >= 0; --jj)
+                                if (base + jj < T) rg[jj] = step(base + jj, rg[jj], Mid{});
+                            for (base -= SC; base > 0; base -= SC) {
+#pragma unroll
+                                for (int jj = SC - 1; jj >= 0; --jj) rg[jj] = step(base + jj, rg[jj], Mid{});
+                            }
+                        }
+#pragma unroll
+                        for (int jj = SC - 1; jj >= 1; --jj)
+                            if (jj < T) rg[jj] = step(jj, rg[jj], Mid{});
+                        rg[0] = step(0, rg[0], First{});
+#pragma unroll
+                        for (int j = 0; j < SC; ++j) sfin[j] = rg[j];
+                    } else {
 #pragma unroll 4
-                    for (int t = T - 1; t >= 1; --t) sb[t] = step(t, sb[t + S], Mid{});
-                    sb[0] = step(0, sb[S], First{});
+                        for (int t = T - 1; t >= 1; --t) sb[t] = step(t, sb[t + S], Mid{});
+                        sb[0] = step(0, sb[S], First{});
+                    }
                 }
                 FCLK();
                 abar -= omab;
@@ -311,6 +419,10 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
         }
         const double tot = block_sum(sq, red);
         if (tid == 0) st.es_sq_part[blockIdx.x] = tot;
+        if (st.lvp > 0.0) {
+            const double pt = block_sum(pen, red);
+            if (tid == 0) st.es_pen_part[blockIdx.x] = pt;
+        }
     } else {
         pdl_wait();
         SPAN_BEGIN(st, s, kSpanFinish);
@@ -505,6 +617,8 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
     if (st.attach)
         for (int b = tid; b < es_blocks; b += kFinishThreads) es += __ldcg(st.es_sq_part + b);
     for (int t = tid; t < nt; t += kFinishThreads) ls += __ldcg(st.loss_part + t);
+    if (st.lvp > 0.0)  // the penalty joins the loss sum (its partials are in the same units)
+        for (int b = tid; b < es_blocks; b += kFinishThreads) ls += __ldcg(st.es_pen_part + b);
     for (int b = tid; b < nrb; b += kFinishThreads) all += __ldcg(st.red_sq_part + b);
     es = block_sum(es, red);
     ls = block_sum(ls, red);
@@ -621,6 +735,8 @@ __global__ void __launch_bounds__(256) k_adam(StateDev<Real> st, PlanDev pl, Net
         if (st.attach)
             for (int b = tid; b < es_blocks; b += blockDim.x) es += __ldcg(st.es_sq_part + b);
         for (int t = tid; t < nt; t += blockDim.x) ls += __ldcg(st.loss_part + t);
+        if (st.lvp > 0.0)
+            for (int b = tid; b < es_blocks; b += blockDim.x) ls += __ldcg(st.es_pen_part + b);
         for (int b = tid; b < red_blocks; b += blockDim.x) all += __ldcg(st.red_sq_part + b);
         block_sum3(es, ls, all, red);
         if (tid == 0) {

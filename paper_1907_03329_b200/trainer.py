@@ -115,6 +115,9 @@ class TrainConfig:  # trainer.hpp:22-44 (+ B200 extensions)
     max_batch_size: int = 0          # 0 -> 2048 reference cap
     device: int = 0
     use_graphs: bool = True
+    # opt-in ES-RNN level-variability penalty (Smyl's M4 model; absent from the reference,
+    # whose loss is pinball only, trainer.hpp:581): 0 = reference behaviour, bit-identical
+    level_variability_penalty: float = 0.0
 
     def to_c(self) -> N.TrainCfg:
         c = N.TrainCfg()
@@ -130,6 +133,7 @@ class TrainConfig:  # trainer.hpp:22-44 (+ B200 extensions)
         c.patience = self.patience
         c.min_delta = self.min_delta
         c.precision = N.FP64 if self.precision == "fp64" else N.FP32
+        c.level_variability_penalty = float(self.level_variability_penalty)
         c.max_batch_size = self.max_batch_size
         c.device = self.device
         c.use_graphs = 0 if self.use_graphs else -1
@@ -367,7 +371,12 @@ class Trainer:
         self.api = api if api is not None else N.product_api()
         self._profile = profile
         self._cfg = cfg
-        if isinstance(series, tuple):
+        if hasattr(series, "values") and hasattr(series, "categories") and hasattr(series, "ids"):
+            # an ingested Dataset (ingest.py): its pinned block goes up without staging
+            values, cats = series.values, np.ascontiguousarray(series.categories, dtype=np.int32)
+            self._ids_list = list(series.ids)
+            self._dataset = series  # keeps the pinned block alive
+        elif isinstance(series, tuple):
             values, cats = series
             values = np.ascontiguousarray(values, dtype=np.float64)
             cats = np.ascontiguousarray(cats, dtype=np.int32)

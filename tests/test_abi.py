@@ -42,7 +42,7 @@ def test_library_exports_every_declared_symbol(lib):
 
 def test_engine_abi_version():
     api = N.product_api()
-    assert api.lib.esrnn_abi_version() == 2
+    assert api.lib.esrnn_abi_version() == 3
     assert "sm_100a" in api.version
 
 
