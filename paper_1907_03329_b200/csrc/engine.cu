@@ -718,7 +718,8 @@ void ensure_capacity(Eng* e, int B) {
     e->kcap = (std::min(e->N > 0 ? e->N : 1, B) + kEsSlotsPerBlock - 1) / kEsSlotsPerBlock * kEsSlotsPerBlock;
     const int kc = e->kcap;
     e->tiles_cap = (B + kRows - 1) / kRows;
-    e->es_blocks = (kc + kEsSlotsPerBlock - 1) / kEsSlotsPerBlock;
+    const int es_slots = e->fp64 ? kEsSlotsPerBlock : kEsSlots32;
+    e->es_blocks = (kc + es_slots - 1) / es_slots;
     // Row parts per weight-gradient tile: at B <= 4,096 one block per tile is fastest (a
     // two-part split measured +6.8 us at cfg1); beyond, one part per 4,096 rows (<= 16)
     e->gsplit = std::max(1, std::min(16, B / 4096));
@@ -902,6 +903,21 @@ size_t finish_smem(const NetLayout& lay) {
     // ES blocks: level / seasonality adjoints [bd][T|1], [bd][(T+S)|1], forward l and s
     // columns [T][bd] (double), one staged observation row per slot (Real), one chunk of
     // staged contribution rows (double)
+    if (sizeof(Real) == 4) {
+        // es_block_fp32 (finish.cuh): adjoints [bd][T|1], [bd][(T+S)|1] (double), six [T][bd]
+        // coefficient arrays, then a scratch region: pre-wait observation rows + forward
+        // states + raw parameters, post-wait one chunk of staged contribution rows
+        const size_t bd = kEsSlots32, T = lay.T, S = lay.S;
+        const size_t ldl = T | 1, lds = (T + S) | 1;
+        const size_t cr = S == 1 ? sizeof(double) : sizeof(float);
+        const size_t cwp = (lay.I + lay.O + 2 + 3) & ~3;
+        const size_t scratch = std::max(bd * row_pad<Real>(lay.T) * sizeof(Real) + bd * (ldl + lds) * cr +
+                                            bd * (2 + S) * sizeof(Real),
+                                        sizeof(double) * kEsChunk * cwp);
+        const size_t es = sizeof(double) * bd * (ldl + lds) + 6 * T * bd * cr + sizeof(double) * bd * S + scratch;
+        const size_t gemm = sizeof(Real) * (static_cast<size_t>(kGBuf * kGChunk) * (kGq + kGk) + (kFinishThreads / 32) * 32 * 6);
+        return std::max(es, gemm);
+    }
     const size_t cwp = (lay.I + lay.O + 2 + 3) & ~3;
     const size_t bd = kEsSlotsPerBlock;
     const size_t es = sizeof(double) * bd * (static_cast<size_t>(lay.T | 1) + static_cast<size_t>((lay.T + lay.S) | 1)) +

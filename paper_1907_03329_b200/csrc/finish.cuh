@@ -14,7 +14,8 @@
 namespace esrnn_dev {
 
 constexpr int kFinishThreads = 256;
-constexpr int kEsSlotsPerBlock = 32;  // ES blocks: warp 0 owns 32 slots; all warps stage the windows
+constexpr int kEsSlotsPerBlock = 32;  // fp64 ES blocks: warp 0 owns 32 slots; all warps stage the windows
+constexpr int kEsSlots32 = 16;        // fp32 ES blocks (es_block_fp32): 16 slots, smaller shared footprint
 constexpr int kEsChunk = 128;         // contribution rows staged per round
 constexpr int kGq = 16, kGk = 8;      // K3 GEMM output block (gate rows x input features)
 constexpr int kGChunk = 256;          // row-store rows staged per round
@@ -45,6 +46,272 @@ __device__ void finalize_scalars(StateDev<Real>& st, const PlanDev& pl, int s, d
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// K3 ES block, fp32 mode: per-slot window-adjoint gather + reverse Holt-Winters adjoint for
+// kEsSlots32 slots.  Everything that does not depend on K2's output runs BEFORE the
+// dependency wait, overlapping K2 (whose tiles release this grid once they pass their own
+// wait): the observation rows, the forward scan of the slots (the tile's own hw_scan_row,
+// so the states equal K2's bit for bit; double for S = 1, see kEsRecompute), the optional
+// level-variability penalty, and the recursion's per-step coefficients.  After the wait:
+// the window log adjoints (thread per (slot, index), CSR order), their scaling by the
+// reciprocal states, the serial reverse recursion (one thread per slot: loads + 6 DFMA per
+// step, one DFMA on the dependency chain) and the per-series gradient outputs.
+// Returns the thread's squared-gradient and penalty partials.
+template <typename Real, int SC>
+__device__ __forceinline__ void es_block_fp32(StateDev<Real>& st, const PlanDev& pl, const NetLayout& lay, int s,
+                                              unsigned char* smem_raw, double& sq, double& pen) {
+    constexpr int bd = kEsSlots32;
+    const int tid = threadIdx.x;
+    auto clk = [&](int i) {
+        if (st.dbg_clk && blockIdx.x == 0 && tid == 0) st.dbg_clk[32 + i] = clock64();
+    };
+    const int k0 = pl.step_slot_off[s];
+    const int k = pl.step_slot_off[s + 1] - k0;
+    const int sl0 = blockIdx.x * bd, sl1 = min(k, sl0 + bd);
+    if (!(sl0 < sl1 && st.attach)) {  // uniform per block
+        pdl_wait();
+        SPAN_BEGIN(st, s, kSpanFinish);
+        return;
+    }
+    using CR = std::conditional_t<kEsRecompute<Real, SC>, double, float>;
+    using MD = Math<double>;
+    const int N = st.N, S = SC > 0 ? SC : lay.S, T = lay.T, I = lay.I, O = lay.O;
+    const int tp = row_pad<Real>(T), cwp = st.cwp, nsl = sl1 - sl0, np = 2 + S;
+    const int ldl = T | 1, lds = (T + S) | 1;
+    double* LB = reinterpret_cast<double*>(smem_raw);  // [bd][ldl] level (log) adjoints
+    double* SB = LB + bd * ldl;                        // [bd][lds] seasonality (log) adjoints
+    CR* K1 = reinterpret_cast<CR*>(SB + bd * lds);     // 6 x [T][bd] recursion coefficients
+    CR* K2 = K1 + T * bd;
+    CR* CA = K2 + T * bd;
+    CR* CG = CA + T * bd;
+    CR* RS = CG + T * bd;
+    CR* RI = RS + T * bd;
+    double* E0 = reinterpret_cast<double*>(RI + T * bd);  // [bd][S] exp(init seasonality raw)
+    unsigned char* X = reinterpret_cast<unsigned char*>(E0 + bd * S);  // scratch (engine.cu finish_smem)
+    Real* YS = reinterpret_cast<Real*>(X);           // pre-wait: [bd][tp] observation rows
+    CR* LVr = reinterpret_cast<CR*>(YS + bd * tp);   //           [bd][ldl] forward levels
+    CR* SEr = LVr + bd * ldl;                        //           [bd][lds] forward seasonalities
+    Real* PRM = reinterpret_cast<Real*>(SEr + bd * lds);  //      [bd][2+S] raw parameters
+    double* cbuf = reinterpret_cast<double*>(X);     // post-wait: [kEsChunk][cwp] contribution rows
+    __shared__ int woff[bd + 1];
+    __shared__ double coef[3][bd];  // alpha, gamma, l[-1] (double)
+    const int slot = sl0 + tid;
+    const bool mine = tid < nsl;
+    clk(1);
+    // ---- pre-wait: plan entries, observation rows, zeroed adjoints ----
+    constexpr int e16 = 16 / static_cast<int>(sizeof(Real));
+    const int nch = tp / e16;
+    for (int e = tid; e < nsl * nch; e += kFinishThreads) {
+        const int sl = e / nch, ch = e - sl * nch;
+        const int row = pl.slot_row[k0 + sl0 + sl];
+        cp_async16(YS + sl * tp + ch * e16, st.vrm + (size_t)row * st.ldv + ch * e16);
+    }
+    if (tid <= nsl) woff[tid] = pl.slot_win_off[k0 + sl0 + tid];
+    for (int e = tid; e < bd * (ldl + lds); e += kFinishThreads) LB[e] = 0.0;  // LB and SB are contiguous
+    const int lrow = mine ? pl.slot_row[k0 + slot] : 0;
+    // per-series parameters: the previous step's K4 output, complete before K2 passed its
+    // wait and released this grid; read at L2
+    Real* pr = PRM + tid * np;
+    if (mine)
+        for (int j = 0; j < np; ++j) pr[j] = __ldcg(st.ps + (size_t)j * N + lrow);
+    cp_async_wait_all();
+    __syncthreads();
+    clk(2);
+    // ---- pre-wait: forward states of the block's slots ----
+    if (mine) {
+        const Real* ys = YS + tid * tp;
+        double l0;
+        if constexpr (kEsRecompute<Real, SC>) {
+            // S = 1: double states (the reference's arithmetic)
+            const double al = MD::logistic(static_cast<double>(pr[0])), ga = MD::logistic(static_cast<double>(pr[1]));
+            CR* lv = LVr + tid * ldl;
+            CR* se = SEr + tid * lds;
+            for (int j = 0; j < S; ++j) se[j] = MD::exp(static_cast<double>(pr[2 + j]));
+            l0 = 0.0;
+            for (int j = 0; j < S; ++j) l0 += static_cast<double>(ys[j]);
+            l0 /= S;
+            double lp = l0;
+            for (int t = 0; t < T; ++t) {
+                const double yt = static_cast<double>(ys[t]), s_t = se[t];
+                const double l = al * (yt / s_t) + (1.0 - al) * lp;
+                se[t + S] = ga * (yt / lp) + (1.0 - ga) * s_t;
+                lv[t] = l;
+                lp = l;
+            }
+        } else {
+            // the tile's own scan: states identical to the ones K2 normalised the windows with
+            hw_scan_row<Real, SC>(ys, pr, T, S, LVr + tid * ldl, SEr + tid * lds);
+            Real l0r = 0;
+            for (int j = 0; j < S; ++j) l0r += ys[j];
+            l0 = static_cast<double>(l0r / Real(S));
+        }
+        for (int j = 0; j < S; ++j) E0[tid * S + j] = MD::exp(static_cast<double>(pr[2 + j]));
+        coef[0][tid] = MD::logistic(static_cast<double>(pr[0]));
+        coef[1][tid] = MD::logistic(static_cast<double>(pr[1]));
+        coef[2][tid] = l0;
+        if (st.lvp > 0.0 && T >= 3) {
+            // opt-in level-variability penalty (oracle/esrnn_oracle.c lvp_series): with
+            // u_t = log l_t and e_t = u_t - 2 u_{t-1} + u_{t-2}, this slot adds c * mean_t e_t^2,
+            // c = lambda * O * (its windows) / M; its adjoint enters the LOG level adjoints
+            const CR* lv = LVr + tid * ldl;
+            double* lb = LB + tid * ldl;
+            const int nw = pl.slot_win_off[k0 + slot + 1] - pl.slot_win_off[k0 + slot];
+            const double cs = st.lvp * O * nw, c = cs / pl.step_M[s], inv = 1.0 / (T - 2);
+            double um2 = ::log(static_cast<double>(lv[0])), um1 = ::log(static_cast<double>(lv[1])), acc = 0.0;
+            for (int t = 2; t < T; ++t) {
+                const double u = ::log(static_cast<double>(lv[t]));
+                const double e = u - 2.0 * um1 + um2;
+                acc += e * e;
+                const double q = c * 2.0 * inv * e;
+                lb[t] += q;
+                lb[t - 1] -= 2.0 * q;
+                lb[t - 2] += q;
+                um2 = um1;
+                um1 = u;
+            }
+            pen = cs * acc * inv;  // x M: the loss-sum units of loss_part
+        }
+    }
+    __syncthreads();
+    clk(3);
+    // ---- pre-wait: the recursion's coefficients, [t][bd] (l' = l[t-1], l[-1] = mean y[0:S])
+    //   K1 = alpha y / s^2, K2 = gamma y / l'^2, CA = y / s - l', CG = y / l' - s, RS = 1/s, RI = 1/l
+    // double for S = 1, else the correctly rounded fp32 reciprocals of the fp32 states
+    for (int e = tid; e < T * bd; e += kFinishThreads) {
+        const int t = e / bd, sl = e - t * bd;
+        if (sl >= nsl) continue;
+        const double y = static_cast<double>(YS[sl * tp + t]);
+        const CR lvc = LVr[sl * ldl + t], svc = SEr[sl * lds + t];
+        const CR lpc = t > 0 ? LVr[sl * ldl + t - 1] : static_cast<CR>(coef[2][sl]);
+        double rs, rl, ri;
+        if constexpr (kEsRecompute<Real, SC>) {
+            rs = 1.0 / svc, rl = 1.0 / lpc, ri = 1.0 / lvc;
+        } else {
+            rs = __frcp_rn(svc), rl = __frcp_rn(lpc), ri = __frcp_rn(lvc);
+        }
+        const double lpv = t > 0 ? static_cast<double>(lpc) : coef[2][sl];
+        const double yrs = y * rs, yrl = y * rl;
+        K1[e] = static_cast<CR>(coef[0][sl] * yrs * rs);
+        K2[e] = static_cast<CR>(coef[1][sl] * yrl * rl);
+        CA[e] = static_cast<CR>(yrs - lpv);
+        CG[e] = static_cast<CR>(yrl - static_cast<double>(svc));
+        RS[e] = static_cast<CR>(rs);
+        RI[e] = static_cast<CR>(ri);
+    }
+    __syncthreads();  // the scratch region becomes the contribution staging buffer
+    clk(4);
+    pdl_wait();
+    DBG_SPAN_MIN(st, s, 4);
+    SPAN_BEGIN(st, s, kSpanFinish);
+    clk(5);
+    // ---- window log adjoints (tile.cuh), chunks of kEsChunk contribution rows; thread per
+    // (slot, index u): seasonality u gets entry u - (a - I + 1) of each window whose
+    // [a - I + 1, a + O] covers u, level u the level entry of each window anchored at u ----
+    const int nio = I + O;
+    const int cb0 = pl.slot_win_off[k0];
+    const int blo = woff[0], bhi = woff[nsl];
+    for (int clo = blo; clo < bhi; clo += kEsChunk) {
+        const int chi = min(bhi, clo + kEsChunk);
+        const double* src = st.contrib + (size_t)(clo - cb0) * cwp;
+        const int nel = (chi - clo) * cwp;
+        for (int i = tid * 2; i < nel; i += kFinishThreads * 2) cp_async16(cbuf + i, src + i);
+        cp_async_wait_all();
+        __syncthreads();
+        for (int e = tid; e < nsl * T; e += kFinishThreads) {
+            const int sl = e / T, u = e - sl * T;
+            const int wl = max(woff[sl], clo), wh = min(woff[sl + 1], chi);
+            if (wl >= wh) continue;
+            double as = 0.0, al = 0.0;
+            for (int w = wl; w < wh; ++w) {
+                const double* c = cbuf + (w - clo) * cwp;
+                const int a = static_cast<int>(c[nio + 1]);
+                const int j = u - (a - I + 1);
+                if (j >= 0 && j < nio) as += c[j];
+                if (u == a) al += c[nio];
+            }
+            SB[sl * lds + u] += as;
+            LB[sl * ldl + u] += al;
+        }
+        __syncthreads();
+    }
+    clk(6);
+    // ---- log adjoints -> adjoints ----
+    for (int e = tid; e < nsl * T; e += kFinishThreads) {
+        const int sl = e / T, t = e - sl * T;
+        LB[sl * ldl + t] *= static_cast<double>(RI[t * bd + sl]);
+        SB[sl * lds + t] *= static_cast<double>(RS[t * bd + sl]);
+    }
+    __syncthreads();
+    clk(7);
+    if (!mine) return;
+    // ---- reverse recursion (holt_winters.hpp:266-277 adjoints), Sb = final adjoint of s[t+S]:
+    //   s_t: sb[t] + Sb (1-gamma) - Lb K1_t,   Lb_{t-1} = lb[t-1] + Lb (1-alpha) - Sb K2_t,
+    //   (abar - omab) += Lb CA_t,   (gbar - omgb) += Sb CG_t
+    const double alpha = coef[0][tid], gamma = coef[1][tid];
+    const double oma = 1.0 - alpha, omg = 1.0 - gamma;
+    double* lb = LB + tid * ldl;
+    double* sb = SB + tid * lds;
+    double asum = 0.0, gsum = 0.0;
+    double lbn = lb[T - 1];
+    auto step = [&](int t, double Sb, auto first) -> double {
+        constexpr bool kFirst = decltype(first)::value;
+        const double Lb = lbn;
+        const int e = t * bd + tid;
+        const double sbt = (sb[t] + Sb * omg) - Lb * static_cast<double>(K1[e]);
+        if constexpr (!kFirst) lbn = (lb[t - 1] - Sb * static_cast<double>(K2[e])) + Lb * oma;
+        asum += Lb * static_cast<double>(CA[e]);
+        gsum += Sb * static_cast<double>(CG[e]);
+        return sbt;
+    };
+    using Mid = std::integral_constant<bool, false>;
+    using First = std::integral_constant<bool, true>;
+    double sfin[SC > 0 ? SC : 1];
+    if constexpr (SC > 0) {
+        double rg[SC];
+#pragma unroll
+        for (int j = 0; j < SC; ++j) rg[j] = 0;  // s[T..T+S) receive no adjoint
+        int base = ((T - 1) / SC) * SC;
+        if (base > 0) {
+#pragma unroll
+            for (int jj = SC - 1; jj >= 0; --jj)
+                if (base + jj < T) rg[jj] = step(base + jj, rg[jj], Mid{});
+            for (base -= SC; base > 0; base -= SC) {
+#pragma unroll
+                for (int jj = SC - 1; jj >= 0; --jj) rg[jj] = step(base + jj, rg[jj], Mid{});
+            }
+        }
+#pragma unroll
+        for (int jj = SC - 1; jj >= 1; --jj)
+            if (jj < T) rg[jj] = step(jj, rg[jj], Mid{});
+        rg[0] = step(0, rg[0], First{});
+#pragma unroll
+        for (int j = 0; j < SC; ++j) sfin[j] = rg[j];
+    } else {
+        for (int t = T - 1; t >= 1; --t) sb[t] = step(t, sb[t + S], Mid{});
+        sb[0] = step(0, sb[S], First{});
+    }
+    clk(8);
+    // ---- per-series gradients: chain rule through the squashes (Logistic :483, Exp :501) ----
+    Real* o = st.psg + (size_t)slot * np;
+    const Real ga = static_cast<Real>(asum * alpha * oma);
+    const Real gg = static_cast<Real>(gsum * gamma * omg);
+    o[0] = ga;
+    o[1] = gg;
+    sq += static_cast<double>(ga) * ga + static_cast<double>(gg) * gg;
+    auto out = [&](int j, double fin) {  // (pr[] was in the scratch region: E0 holds exp(raw))
+        const Real g = static_cast<Real>(fin * E0[tid * S + j]);
+        o[2 + j] = g;
+        sq += static_cast<double>(g) * g;
+    };
+    if constexpr (SC > 0) {
+#pragma unroll
+        for (int j = 0; j < SC; ++j) out(j, sfin[j]);
+    } else {
+        for (int j = 0; j < S; ++j) out(j, sb[j]);
+    }
+    clk(9);
+}
+
 template <typename Real, int SC>
 __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> st, PlanDev pl, NetLayout lay, int s,
                                                                 int es_blocks, int finalize, int gsplit) {
@@ -66,7 +333,15 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
     FCLK();
     DBG_GT(st, 4);
     DBG_SPAN_MIN(st, s, 3);
-    if (static_cast<int>(blockIdx.x) < es_blocks) {
+    if (static_cast<int>(blockIdx.x) < es_blocks && sizeof(Real) == 4) {
+        if constexpr (sizeof(Real) == 4) es_block_fp32<Real, SC>(st, pl, lay, s, smem_raw, sq, pen);
+        const double tot = block_sum(sq, red);
+        if (tid == 0) st.es_sq_part[blockIdx.x] = tot;
+        if (st.lvp > 0.0) {
+            const double pt = block_sum(pen, red);
+            if (tid == 0) st.es_pen_part[blockIdx.x] = pt;
+        }
+    } else if (static_cast<int>(blockIdx.x) < es_blocks) {
         // ---------------- per-slot window-adjoint gather + reverse HW scan ---------------
         const int k0 = pl.step_slot_off[s];
         const int k = pl.step_slot_off[s + 1] - k0;

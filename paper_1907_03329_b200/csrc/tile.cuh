@@ -459,9 +459,10 @@ __global__ void __launch_bounds__((RESIDENT || sizeof(Real) == 8) ? 512 : 384, (
         }
         DBG_CLK(st, 0);
         __syncthreads();
-        // published states for K3's reverse scan: lv [T][kcap], se [T+S][kcap] (not for
-        // fp32 with S = 1: K3 recomputes those in double, finish.cuh kEsRecompute)
-        if (MODE == kTrain && (sizeof(Real) == 8 || SC != 1)) {
+        // published states for K3's fp64 reverse scan: lv [T][kcap], se [T+S][kcap] (fp32:
+        // K3's ES blocks rerun this scan themselves before their dependency wait,
+        // finish.cuh es_block_fp32)
+        if (MODE == kTrain && sizeof(Real) == 8) {
             for (int r = warp; r < nrows; r += NW) {  // a warp per window row, lanes over t
                 const int slot = pub_slot[r];
                 if (slot < 0) continue;
