@@ -471,7 +471,7 @@ def main():
     rb = 4 if a.precision == "fp32" else 8
     # DRAM traffic per launch, from the committed ncu --set full capture of this workload
     traffic = {}
-    tf = ROOT / "profiles" / "ncu_traffic.json"
+    tf = ROOT / "profiles" / f"ncu_traffic_{a.config}.json"
     if tf.exists():
         doc = json.loads(tf.read_text())
         if doc.get("config") == a.config and doc.get("precision", "fp32") == a.precision:

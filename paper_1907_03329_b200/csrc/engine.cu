@@ -961,11 +961,15 @@ void setup_kernel_attrs(Eng* e) {
     }
     const size_t fsm = sizeof(Real) * static_cast<size_t>(e->LEN + e->S + e->I) * kScanThreads;
     CUDA_OK(cudaFuncSetAttribute(k_forecast_scan<Real, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
-    CUDA_OK(cudaFuncSetAttribute(k_forecast_scan<Real, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
-    CUDA_OK(cudaFuncSetAttribute(k_forecast_scan<Real, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
-    CUDA_OK(cudaFuncSetAttribute(k_forecast_scan<Real, 12>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm));
+    const size_t fsm_sc = fsm + sizeof(Real) * static_cast<size_t>(e->in0 + e->O + 1) * kScanThreads;
+    CUDA_OK(cudaFuncSetAttribute(k_forecast_scan_sc<Real, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm_sc));
+    CUDA_OK(cudaFuncSetAttribute(k_forecast_scan_sc<Real, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm_sc));
+    CUDA_OK(cudaFuncSetAttribute(k_forecast_scan_sc<Real, 12, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm_sc));
+    CUDA_OK(cudaFuncSetAttribute(k_forecast_scan_sc<Real, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm_sc));
+    CUDA_OK(cudaFuncSetAttribute(k_forecast_scan_sc<Real, 4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm_sc));
+    CUDA_OK(cudaFuncSetAttribute(k_forecast_scan_sc<Real, 12, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm_sc));
     if (stack_smem<Real>(e->lay, false) > static_cast<size_t>(g_smem_optin) ||
-        finish_smem<Real>(e->lay) > static_cast<size_t>(g_smem_optin) || fsm > static_cast<size_t>(g_smem_optin))
+        finish_smem<Real>(e->lay) > static_cast<size_t>(g_smem_optin) || fsm_sc > static_cast<size_t>(g_smem_optin))
         raise(ESRNN_CONFIG_ERROR, "profile too large for the B200 kernels' shared-memory tiles");
 }
 
@@ -1672,14 +1676,16 @@ void launch_forecast_scan(Eng* e, int t_len, Real* X, Real* FL, Real* FS, Real* 
     const int sb = (e->N + kScanThreads - 1) / kScanThreads;
     const size_t smem = sizeof(Real) * static_cast<size_t>(t_len + e->S + e->I) * kScanThreads;
     const StateDev<Real> st = e->state<Real>();
-    auto go = [&](auto kernel) {
-        kernel<<<sb, kScanThreads, smem, e->stream>>>(st, e->lay, t_len, X, FL, FS, dump_lv, dump_se, dump_row, score);
+    const size_t smem_sc = smem + sizeof(Real) * static_cast<size_t>(e->in0 + e->O + 1) * kScanThreads;
+    auto go = [&](auto kernel, size_t sm) {
+        kernel<<<sb, kScanThreads, sm, e->stream>>>(st, e->lay, t_len, X, FL, FS, dump_lv, dump_se, dump_row, score);
     };
+    const bool dump = dump_row >= 0;
     switch (e->S) {
-        case 1: go(k_forecast_scan<Real, 1>); break;
-        case 4: go(k_forecast_scan<Real, 4>); break;
-        case 12: go(k_forecast_scan<Real, 12>); break;
-        default: go(k_forecast_scan<Real, 0>); break;
+        case 1: dump ? go(k_forecast_scan_sc<Real, 1, true>, smem_sc) : go(k_forecast_scan_sc<Real, 1, false>, smem_sc); break;
+        case 4: dump ? go(k_forecast_scan_sc<Real, 4, true>, smem_sc) : go(k_forecast_scan_sc<Real, 4, false>, smem_sc); break;
+        case 12: dump ? go(k_forecast_scan_sc<Real, 12, true>, smem_sc) : go(k_forecast_scan_sc<Real, 12, false>, smem_sc); break;
+        default: go(k_forecast_scan<Real, 0>, smem); break;
     }
 }
 
@@ -1864,12 +1870,35 @@ void forward_stack_impl(Eng* e, int Tq, int B, const double* inputs, double* out
     upload_real(e, w.p, e->w_host.data(), e->P);
     x.alloc(r * static_cast<size_t>(Tq) * B * e->in0);
     upload_real(e, x.p, inputs, static_cast<size_t>(Tq) * B * e->in0);
-    scratch.alloc(r * static_cast<size_t>(nblk) * SeqScratch<Real>::size(sl));
     dout.alloc(static_cast<size_t>(B) * e->O);
+    // inference (no adjoint): the shared-memory-resident kernel when a layer's weights, the
+    // (h, c) rings and the gate tile fit (seqstack.cuh k_seq_fwd_fast); the adjoint path keeps
+    // every step's activations for the reverse sweep (k_seq_forward / k_seq_backward)
+    int dmax = 1;
+    for (int l = 0; l < e->L; ++l) dmax = std::max(dmax, sl.dil[l]);
+    const size_t G = 4 * static_cast<size_t>(e->H);
+    const size_t fast_smem = r * ((static_cast<size_t>(sl.in_max) + e->H + 1) * G + static_cast<size_t>(sl.in_max) * kSeqFR +
+                                  2 * static_cast<size_t>(dmax) * e->H * kSeqFR + kSeqFR * G);
+    const bool fast = !out_bar && fast_smem <= static_cast<size_t>(g_smem_optin) && G <= 320 &&
+                      std::getenv("ESRNN_SEQ_NAIVE") == nullptr;
+    const int nfast = (B + kSeqFR - 1) / kSeqFR;
+    if (!fast) scratch.alloc(r * static_cast<size_t>(nblk) * SeqScratch<Real>::size(sl));
+    if (fast) {
+        scratch.alloc(r * static_cast<size_t>(nfast) * 3 * Tq * kSeqFR * e->H);
+        CUDA_OK(cudaFuncSetAttribute(k_seq_fwd_fast<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(fast_smem)));
+    }
     CUDA_OK(cudaEventRecord(e->ev0, e->stream));
-    k_seq_forward<Real><<<nblk, kSeqThreads, 0, e->stream>>>(sl, reinterpret_cast<const Real*>(w.p),
-                                                              reinterpret_cast<const Real*>(x.p),
-                                                              reinterpret_cast<Real*>(scratch.p), dout.p);
+    if (fast) {
+        const int nt = static_cast<int>((std::max<size_t>(G, 32) + 31) / 32 * 32);
+        k_seq_fwd_fast<Real><<<nfast, nt, fast_smem, e->stream>>>(sl, reinterpret_cast<const Real*>(w.p),
+                                                                  reinterpret_cast<const Real*>(x.p),
+                                                                  reinterpret_cast<Real*>(scratch.p), dout.p);
+    } else {
+        k_seq_forward<Real><<<nblk, kSeqThreads, 0, e->stream>>>(sl, reinterpret_cast<const Real*>(w.p),
+                                                                  reinterpret_cast<const Real*>(x.p),
+                                                                  reinterpret_cast<Real*>(scratch.p), dout.p);
+    }
     e->launches += 1;
     if (out_bar) {
         ob.alloc(r * static_cast<size_t>(B) * e->O);

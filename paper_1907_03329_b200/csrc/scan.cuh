@@ -166,4 +166,152 @@ __global__ void __launch_bounds__(kScanThreads) k_forecast_scan(StateDev<Real> s
     }
 }
 
+// ------------------------------------------------------------------------------ K6, S fixed
+// k_forecast_scan for the M4 season lengths (SC = 1, 4, 12), restructured for bandwidth:
+//  * every global input is requested up front (observation column, seasonality raws, alpha,
+//    gamma, category), then one wait;
+//  * the recurrence runs in two loops: steps whose new seasonality is not in the input window
+//    (no window stores, no checks beyond the level select), then the last steps that produce
+//    the window's seasonalities; the hw_state dump is a separate instantiation (DUMP);
+//  * the outputs (window row X, anchor level, the horizon's seasonalities) are staged in shared
+//    memory and written by the whole block: the block's rows are contiguous in X / FS / FL,
+//    so every store is coalesced (a thread's own row stores touch 32 rows per instruction).
+// smem: ys [t_ins][bd] | ring [S][bd] | win [I][bd] | ox [bd][in0] | ofs [bd][O] | ofl [bd]
+template <typename Real, int SC, bool DUMP>
+__global__ void __launch_bounds__(kScanThreads) k_forecast_scan_sc(StateDev<Real> st, NetLayout lay, int t_ins, Real* X,
+                                                                   Real* FL, Real* FS, Real* dump_lv, Real* dump_se,
+                                                                   int dump_row, double* score) {
+    using M = Math<Real>;
+    constexpr int S = SC;
+    constexpr Real kMax = sizeof(Real) == 4 ? Real(FLT_MAX) : Real(DBL_MAX);
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int I = lay.I, O = lay.O, in0 = lay.in0, N = st.N;
+    const int bd = blockDim.x, tid = threadIdx.x;
+    const int row0 = blockIdx.x * bd, nrow = min(bd, N - row0);
+    const int row = row0 + tid;
+    const bool live = tid < nrow;
+    Real* ys = reinterpret_cast<Real*>(smem_raw) + tid;
+    Real* ring = reinterpret_cast<Real*>(smem_raw) + t_ins * bd + tid;
+    Real* win = ring + S * bd;
+    Real* ox = reinterpret_cast<Real*>(smem_raw) + (t_ins + S + I) * bd;  // [bd][in0]
+    Real* ofs = ox + bd * in0;                                            // [bd][O]
+    Real* ofl = ofs + bd * O;                                             // [bd]
+    Real a_raw = 0, g_raw = 0;
+    int cat = 5;
+    if (live) {
+#pragma unroll
+        for (int j = 0; j < S; ++j) cp_async_elem(ring + j * bd, st.ps + (size_t)(2 + j) * N + row);
+#pragma unroll 8
+        for (int t = 0; t < t_ins; ++t) cp_async_elem(ys + t * bd, st.vals + (size_t)t * N + row);
+        a_raw = st.ps[row];
+        g_raw = st.ps[N + row];
+        cat = st.cat[row];
+    }
+    cp_async_wait_all();
+    bool ok = live;
+    if (live) {
+        int bad = INT_MAX;  // first non-positive observation
+#pragma unroll 8
+        for (int t = t_ins - 1; t >= 0; --t) bad = (ys[t * bd] > Real(0)) ? bad : t;
+        if (bad != INT_MAX) {
+            flag_error(st.err, kErrObs, bad);
+            ok = false;
+        }
+    }
+    if (ok && score != nullptr) {
+        // mase() denominator, seasonal-naive sMAPE / MASE (metrics.hpp:17-59)
+        double den = 0.0;
+        for (int t = S; t < t_ins; ++t)
+            den += fabs(static_cast<double>(ys[t * bd]) - static_cast<double>(ys[(t - S) * bd]));
+        den /= static_cast<double>(t_ins - S);
+        double acc = 0.0, mae = 0.0;
+        for (int o = 0; o < O; ++o) {
+            const double f = static_cast<double>(ys[(t_ins - S + o % S) * bd]);
+            const double a = static_cast<double>(st.vals[(size_t)(t_ins + o) * N + row]);
+            const double d = fabs(a) + fabs(f);
+            if (d > 0.0) acc += fabs(a - f) / d;
+            mae += fabs(a - f);
+        }
+        score[row] = den;
+        score[N + row] = 200.0 * acc / static_cast<double>(O);
+        score[2 * N + row] = den == 0.0 ? NAN : (mae / static_cast<double>(O)) / den;
+    }
+    Real lp = 0;
+    if (ok) {
+        const Real alpha = M::logistic_ps(a_raw);
+        const Real gamma = M::logistic_ps(g_raw);
+        const Real oma = Real(1) - alpha, omg = Real(1) - gamma;
+        Real rg[SC];
+#pragma unroll
+        for (int j = 0; j < S; ++j) {
+            rg[j] = M::exp_ps(ring[j * bd]);
+            if (DUMP && row == dump_row) dump_se[j] = rg[j];
+            lp += ys[j * bd];
+        }
+        lp = lp / Real(S);
+        const int w0 = t_ins - I;  // first window index; seasonality u is produced at step u - S
+        for (int u = max(w0, 0); u < S && u < t_ins; ++u) win[(u - w0) * bd] = rg[u];
+        int bad = INT_MAX;
+        auto step = [&](int t, Real& sq, bool tail) {
+            const Real yt = ys[t * bd];
+            const Real l = alpha * fdiv(yt, sq) + oma * lp;
+            bad = (bad == INT_MAX && !(l > Real(0) && l <= kMax)) ? t : bad;
+            sq = gamma * fdiv(yt, lp) + omg * sq;
+            if (tail) {
+                const int uu = t + S;
+                if (uu >= w0 && uu < t_ins) win[(uu - w0) * bd] = sq;
+            }
+            if (DUMP && row == dump_row) {
+                dump_lv[t] = l;
+                dump_se[t + S] = sq;
+            }
+            lp = l;
+        };
+        // steps t < w0 - S produce indices below the window: no stores
+        const int t_free = max(0, min(t_ins, w0 - S));
+        int t0 = 0;
+        for (; t0 + SC <= t_free; t0 += SC) {
+#pragma unroll
+            for (int q = 0; q < SC; ++q) step(t0 + q, rg[q], false);
+        }
+        for (; t0 < t_ins; t0 += SC) {
+#pragma unroll
+            for (int q = 0; q < SC; ++q)
+                if (t0 + q < t_ins) step(t0 + q, rg[q], true);  // warp-uniform
+        }
+        if (bad != INT_MAX) {
+            flag_error(st.err, kErrFcLevel, bad);
+            ok = false;
+        }
+        // slot q holds the seasonality of index u = q (mod S) in [t_ins, t_ins + S)
+        if (ok && X != nullptr) {
+            const Real level = lp;
+            for (int c = 0; c < I; ++c) {
+                const Real sv = win[c * bd];
+                if (!(sv > Real(0))) {
+                    flag_error(st.err, kErrSeas, t_ins);
+                    ok = false;
+                    break;
+                }
+                ox[tid * in0 + c] = fdiv(ys[(t_ins - I + c) * bd], level * sv);
+            }
+            for (int c = 0; c < 6; ++c) ox[tid * in0 + I + c] = (cat == c) ? Real(1) : Real(0);
+            ofl[tid] = level;
+            for (int o = 0; o < O; ++o) {  // seasonal_at(t_ins + o): ring slot (t_ins + o) mod S
+                const int slot = (t_ins + o) % S;
+                Real v = rg[0];
+#pragma unroll
+                for (int q = 1; q < SC; ++q) v = slot == q ? rg[q] : v;
+                ofs[tid * O + o] = v;
+            }
+        }
+    }
+    if (X == nullptr) return;  // (uniform) hw_state: nothing staged
+    __syncthreads();
+    // coalesced block stores of the contiguous output rows
+    for (int e = tid; e < nrow * in0; e += bd) X[(size_t)row0 * in0 + e] = ox[e];
+    for (int e = tid; e < nrow * O; e += bd) FS[(size_t)row0 * O + e] = ofs[e];
+    for (int e = tid; e < nrow; e += bd) FL[row0 + e] = ofl[e];
+}
+
 }  // namespace esrnn_dev

@@ -264,6 +264,147 @@ __global__ void __launch_bounds__(kSeqThreads) k_seq_backward(SeqLayout s, const
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// Inference forward_stack at speed: k_seq_fwd_fast.  A CTA owns kSeqFR batch rows for the
+// whole sequence; per layer its input (W_in), recurrent (W_rec) and bias weights sit in
+// shared memory, and each step is two barrier-separated phases:
+//   gates: thread j (one per gate column, 4H <= blockDim) accumulates its column for all
+//          kSeqFR rows in registers -- x_t W_in over the staged layer input, then h_{t-d}
+//          W_rec from the recurrent ring -- one shared-memory weight load feeds kSeqFR FMAs,
+//          the row values are broadcast reads ([k][row] layout, 16-byte vectors)
+//   cell:  thread per (row, unit): c = f c_{t-d} + i g, h = o tanh(c) into the (h, c) rings
+//          (depth d: slot t mod d holds step t), the layer output to the CTA's private
+//          sequence buffer (L2 resident) with the block skip added, and the next step's
+//          input staged.
+// Same summation order as k_seq_forward (x W_in, + h W_rec, + bias).  Used when no adjoint
+// is requested and the layer weights fit in shared memory (host: seq_fast_smem).
+constexpr int kSeqFR = 16;
+
+template <typename Real>
+__global__ void __launch_bounds__(320) k_seq_fwd_fast(SeqLayout s, const Real* __restrict__ W,
+                                                       const Real* __restrict__ X, Real* __restrict__ seqbuf,
+                                                       double* out) {
+    using M = Math<Real>;
+    constexpr int R = kSeqFR;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int b0 = blockIdx.x * R, nr = min(R, s.B - b0);
+    const int tid = threadIdx.x, NT = blockDim.x, H = s.H, G = 4 * H, T = s.T;
+    int dmax = 1;
+    for (int l = 0; l < s.L; ++l) dmax = max(dmax, s.dil[l]);
+    // shared layout: weights [in_max + H + 1][G] | xs [in_max][R] | hring, cring [dmax][H][R] | gates [R][G]
+    Real* Ws = reinterpret_cast<Real*>(smem_raw);
+    Real* xs = Ws + static_cast<size_t>(s.in_max + H + 1) * G;
+    Real* hr = xs + static_cast<size_t>(s.in_max) * R;
+    Real* cr = hr + static_cast<size_t>(dmax) * H * R;
+    Real* gs = cr + static_cast<size_t>(dmax) * H * R;
+    // per-CTA sequence buffers: two layer outputs in flight + the current block's input
+    const size_t TRH = static_cast<size_t>(T) * R * H;
+    Real* cur0 = seqbuf + static_cast<size_t>(blockIdx.x) * 3 * TRH;  // layer outputs l even / odd
+    Real* bin = cur0 + 2 * TRH;
+    for (int l = 0; l < s.L; ++l) {
+        const int K = s.layer_in[l], d = s.dil[l];
+        const Real* Xin = l == 0 ? nullptr : cur0 + ((l - 1) & 1) * TRH;
+        Real* Y = cur0 + (l & 1) * TRH;
+        __syncthreads();  // previous layer done with the weights / its output complete
+        const Real* Wi = W + s.w_in[l];
+        const Real* Wr = W + s.w_rec[l];
+        const Real* Bi = W + s.bias[l];
+        for (int e = tid; e < K * G; e += NT) Ws[e] = Wi[e];
+        for (int e = tid; e < H * G; e += NT) Ws[K * G + e] = Wr[e];
+        for (int e = tid; e < G; e += NT) Ws[(K + H) * G + e] = Bi[e];
+        for (int e = tid; e < 2 * d * H * R; e += NT) hr[e] = Real(0);  // h and c rings are contiguous
+        // stage x_0 as [k][row]
+        for (int e = tid; e < K * R; e += NT) {
+            const int k = e / R, r = e - k * R;
+            Real v = 0;
+            if (r < nr) v = l == 0 ? X[(static_cast<size_t>(0) * s.B + b0 + r) * s.in0 + k] : Xin[(static_cast<size_t>(0) * R + r) * H + k];
+            xs[e] = v;
+        }
+        __syncthreads();
+        for (int t = 0; t < T; ++t) {
+            // ---- gates ----
+            if (tid < G) {
+                Real acc[R], a2[R];
+#pragma unroll
+                for (int r = 0; r < R; ++r) acc[r] = 0, a2[r] = 0;
+                const Real* wcol = Ws + tid;
+                for (int k = 0; k < K; ++k) {
+                    const Real w = wcol[k * G];
+                    const Real* xk = xs + k * R;
+#pragma unroll
+                    for (int r = 0; r < R; ++r) acc[r] += xk[r] * w;
+                }
+                if (t >= d) {
+                    const Real* hp = hr + static_cast<size_t>((t - d) % d) * H * R;
+                    const Real* wrc = Ws + K * G + tid;
+                    for (int k = 0; k < H; ++k) {
+                        const Real w = wrc[k * G];
+                        const Real* hk = hp + k * R;
+#pragma unroll
+                        for (int r = 0; r < R; ++r) a2[r] += hk[r] * w;
+                    }
+                }
+                const Real b = Ws[(K + H) * G + tid];
+                const bool is_g = tid >= 2 * H && tid < 3 * H;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const Real v = (t >= d ? acc[r] + a2[r] : acc[r]) + b;
+                    gs[r * G + tid] = is_g ? M::tanh(v) : M::logistic(v);
+                }
+            }
+            __syncthreads();
+            // ---- cell, outputs, next input ----
+            const int slot = t % d;
+            for (int e = tid; e < nr * H; e += NT) {
+                const int r = e / H, j = e - r * H;
+                const Real* gt = gs + r * G;
+                const Real i = gt[j], f = gt[H + j], g = gt[2 * H + j], o = gt[3 * H + j];
+                Real* cpos = cr + (static_cast<size_t>(slot) * H + j) * R + r;  // also c_{t-d} (same slot)
+                const Real cv = (t >= d ? f * *cpos : Real(0)) + i * g;
+                const Real h = o * M::tanh(cv);
+                *cpos = cv;
+                hr[(static_cast<size_t>(slot) * H + j) * R + r] = h;
+                const size_t q = (static_cast<size_t>(t) * R + r) * H + j;
+                if (s.res_src[l] >= 0) Y[q] = h + bin[q];
+                else Y[q] = h;
+            }
+            if (t + 1 < T)
+                for (int e = tid; e < K * R; e += NT) {
+                    const int k = e / R, r = e - k * R;
+                    Real v = 0;
+                    if (r < nr)
+                        v = l == 0 ? X[(static_cast<size_t>(t + 1) * s.B + b0 + r) * s.in0 + k]
+                                   : Xin[(static_cast<size_t>(t + 1) * R + r) * H + k];
+                    xs[e] = v;
+                }
+            __syncthreads();
+        }
+        // the block skip of a later layer m adds the output of layer res_src[m] (the previous
+        // block's last layer, i.e. the block input): keep it when this layer is that source
+        bool is_src = false;
+        for (int m = l + 1; m < s.L; ++m) is_src |= s.res_src[m] == l;
+        if (is_src)
+            for (size_t e = tid; e < static_cast<size_t>(T) * R * H; e += NT) bin[e] = Y[e];
+    }
+    __syncthreads();
+    // head on the last step (network.hpp:207-209)
+    const Real* last = cur0 + ((s.L - 1) & 1) * TRH + static_cast<size_t>(T - 1) * R * H;
+    Real* z = gs;  // [R][H]
+    for (int e = tid; e < nr * H; e += NT) {
+        const int r = e / H, j = e - r * H;
+        Real acc = 0;
+        for (int k = 0; k < H; ++k) acc += last[r * H + k] * W[s.nl_w + static_cast<long long>(k) * H + j];
+        z[r * H + j] = M::tanh(acc + W[s.nl_b + j]);
+    }
+    __syncthreads();
+    for (int e = tid; e < nr * s.O; e += NT) {
+        const int r = e / s.O, o = e - r * s.O;
+        Real acc = 0;
+        for (int k = 0; k < H; ++k) acc += z[r * H + k] * W[s.out_w + static_cast<long long>(k) * s.O + o];
+        out[static_cast<long long>(b0 + r) * s.O + o] = static_cast<double>(acc + W[s.out_b + o]);
+    }
+}
+
 // weights_bar[p] = sum over CTAs b (in order) of wpart[b][p]
 template <typename Real>
 __global__ void k_seq_reduce(const Real* __restrict__ wpart, int nblk, long long P, double* out) {

@@ -130,3 +130,19 @@ def test_engine_dilation_structure(engine):
     # x_t reaches the output iff 6 - t = 2a + 3b (a, b >= 0), i.e. for every t but t = 5
     for t in range(7):
         assert np.any(xb[t] != 0) == (t != 5), t
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+@pytest.mark.parametrize("name", ["quarterly", "monthly", "yearly"])
+def test_fast_forward_stack_equals_stepwise_kernel(engine, name, precision, monkeypatch):
+    """The shared-memory-resident inference kernel (k_seq_fwd_fast) against the per-step
+    kernel the adjoint path uses (k_seq_forward), at the M4 profiles' dilations and block
+    skips, B not a multiple of the CTA's rows: same summation order, bit-identical."""
+    prof = FrequencyProfile.defaults(getattr(Frequency, name.capitalize()))
+    g = make(engine, prof, precision=precision)
+    x = seq_inputs(prof, 19, 37)
+    fast = g.forward_stack(x)
+    monkeypatch.setenv("ESRNN_SEQ_NAIVE", "1")
+    naive = g.forward_stack(x)
+    assert np.array_equal(fast, naive)

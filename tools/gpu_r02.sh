@@ -21,12 +21,14 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --c
   --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e \
   > gpurun_out/${TAG}_ncu_launch_bench.log 2>&1; echo "ncu launches rc=$?"
 for k in k_tile k_grad_finish k_adam k_forecast_scan; do
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 200 -c 1 \
+  skip=200; [ $k = k_forecast_scan ] && skip=2
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s $skip -c 1 \
     -o gpurun_out/${TAG}_cfg1_$k python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e \
     > gpurun_out/${TAG}_ncu_cfg1_$k.log 2>&1; echo "ncu cfg1 $k rc=$?"
 done
 for k in k_tile k_forecast_scan; do
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s 20 -c 1 \
+  skip=20; [ $k = k_forecast_scan ] && skip=1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s $skip -c 1 \
     -o gpurun_out/${TAG}_cfg3_$k python bench.py --config cfg3 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e \
     > gpurun_out/${TAG}_ncu_cfg3_$k.log 2>&1; echo "ncu cfg3 $k rc=$?"
 done
