@@ -634,6 +634,21 @@ const char* esrnn_dataset_id(const esrnn_dataset* d, int64_t i) {
 }
 void esrnn_dataset_destroy(esrnn_dataset* d) { delete d; }
 
+// Not in the ABI: the rest of the reference's data path after cmd_prepare's equalisation --
+// save_prepared (the JSON bundle, commands.hpp:30-47) and load_prepared (:49-74) -- timed
+// by tools/ingest_bench.py.  Returns the number of series read back, -1 on error.
+int64_t esrnn_ref_bundle_roundtrip(const esrnn_dataset* d, int32_t frequency, const char* path) {
+    try {
+        const auto f = static_cast<Frequency>(frequency);
+        const int len = d->kept.empty() ? 0 : static_cast<int>(d->kept[0].values.size());
+        save_prepared(path, f, len, d->kept);
+        return static_cast<int64_t>(load_prepared(path, f).size());
+    } catch (const std::exception& e) {
+        g_ingest_err = e.what();
+        return -1;
+    }
+}
+
 esrnn_status esrnn_make_synthetic(uint64_t seed, int64_t n, int32_t length, int32_t season_length,
                                   double noise_sigma, double* values, int32_t* category) {
     Rng rng(seed);
