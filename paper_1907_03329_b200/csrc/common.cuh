@@ -104,6 +104,8 @@ struct StateDev {
     Real* gpart;            // [gsplit][tiles][32 lanes][6]: row-part tile partials (large steps)
     unsigned* gtile_ctr;    // [tiles] arrival tickets of a tile's row parts
     int red_tiles;          // K3 weight-gradient output tiles
+    float* upart;           // [umma tiles][parts][128][64] tensor-core dW partials (fp32, large steps)
+    int umma_tiles;         // 128-row matrix slices of the tensor-core dW path
     unsigned int* done_ctr; // [2]
     double* scal;           // [4] scale, bc1, bc2, loss
     long long* net_step;

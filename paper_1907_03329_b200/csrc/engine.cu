@@ -44,6 +44,8 @@ using namespace esrnn_dev;
 using namespace esrnn_host;
 
 namespace {
+extern int g_smem_optin, g_num_sms;  // device limits (defined below, set at create)
+
 
 
 // One plan = ordered local windows + per-step slot lists + per-slot window CSR.
@@ -262,6 +264,8 @@ struct esrnn_trainer {
     DBuf<unsigned int> done_ctr, gtile_ctr;
     DBuf<unsigned char> gpart;
     int gsplit = 1;  // K3 weight-gradient row parts per output tile (large steps)
+    int umma_parts = 0, umma_tiles = 0;  // tensor-core dW path (fp32, steps >= kUmmaMinRows)
+    DBuf<unsigned char> upart;
     const double* bc_tab = nullptr;  // process-wide bias-correction table of this GPU (StateDev::bc)
     DBuf<long long> net_step;
     DBuf<long long> dbg_clk;  // ESRNN_DEBUG_CLOCKS: per-phase clock64 stamps of tile 0
@@ -336,7 +340,7 @@ struct esrnn_trainer {
              ...);
         };
         add(vals, vrm, ps, ps_m, ps_v, theta, mW, vW, cat, ps_steps, lv, se, contrib, rowstore, gbuf, psg, d_inputs,
-            d_targets, d_seas, d_levels, fX, fL, fS, dump_lv, dump_se, loss_part, es_sq_part, es_pen_part, red_sq_part, scal,
+            d_targets, d_seas, d_levels, fX, fL, fS, dump_lv, dump_se, loss_part, es_sq_part, es_pen_part, red_sq_part, scal, upart,
             loss_hist, f_out, f_smape, f_score, smape_sum, done_ctr, gtile_ctr, gpart, net_step, dbg_clk, errw, gtail,
             coll_seq, spans);
         for (DevPlan* d : {&epoch_plan, &batch_plan})
@@ -396,6 +400,8 @@ struct esrnn_trainer {
         s.gpart = reinterpret_cast<Real*>(gpart.p);
         s.gtile_ctr = gtile_ctr.p;
         s.red_tiles = red_blocks;
+        s.upart = reinterpret_cast<float*>(upart.p);
+        s.umma_tiles = umma_tiles;
         s.done_ctr = done_ctr.p;
         s.scal = scal.p;
         s.net_step = net_step.p;
@@ -724,15 +730,38 @@ void ensure_capacity(Eng* e, int B) {
     // two-part split measured +6.8 us at cfg1); beyond, one part per 4,096 rows (<= 16)
     e->gsplit = std::max(1, std::min(16, B / 4096));
     e->gpart.alloc(e->rsz * static_cast<size_t>(e->gsplit) * std::max(e->red_blocks, 1) * 32 * 6);
-    if (e->gtile_ctr.n < static_cast<size_t>(std::max(e->red_blocks, 1))) {
-        e->gtile_ctr.alloc(std::max(e->red_blocks, 1));
+    // tensor-core weight gradients (umma.cuh, finish.cuh dw_umma_block): fp32 steps of at
+    // least kUmmaMinRows windows, every matrix's K + 1 within the 64-column N tile;
+    // two blocks per SM over the matrices' 128-row tiles, parts of >= 256 rows
+    e->umma_parts = 0;
+    e->umma_tiles = 0;
+    if (!e->fp64 && B >= kUmmaMinRows && std::getenv("ESRNN_NO_UMMA") == nullptr &&
+        static_cast<size_t>(g_smem_optin) >= static_cast<size_t>(kUSmem) + 1024) {
+        bool fits = true;
+        for (int m = 0; m < e->lay.nmat; ++m) {
+            fits &= e->lay.mats[m].K + 1 <= kUN && e->lay.mats[m].a_off % 4 == 0 && e->lay.mats[m].u_off % 4 == 0;
+            e->umma_tiles += (e->lay.mats[m].Q + kUM - 1) / kUM;
+        }
+        if (fits && e->lay.rs_ld % 4 == 0) {
+            // one wave at two blocks per SM (kUSmem ~85 KB)
+            e->umma_parts = std::max(1, std::min(std::min(64, 2 * g_num_sms / e->umma_tiles), B / 256));
+            e->upart.alloc(sizeof(float) * static_cast<size_t>(e->umma_tiles) * e->umma_parts * kUM * kUN);
+        } else {
+            e->umma_tiles = 0;
+        }
+    }
+    const int ctr_n = std::max({e->red_blocks, e->umma_tiles, 1});
+    if (e->gtile_ctr.n < static_cast<size_t>(ctr_n)) {
+        e->gtile_ctr.alloc(ctr_n);
         e->gtile_ctr.zero(e->stream);
     }
     e->lv.alloc(r * T * kc);
     e->se.alloc(r * (T + S) * kc);
     e->contrib.alloc(sizeof(double) * static_cast<size_t>(B) * ((I + O + 2 + 3) & ~3));
     // row store: K2 writes every column of a live window's row; rows are read only by K3
-    e->rowstore.alloc(r * static_cast<size_t>(e->tiles_cap * kRows) * e->lay.rs_ld);
+    // (+ 256 columns: the tensor-core path reads whole 128-row / 64-column operand quads
+    // past the last matrix of the last row)
+    e->rowstore.alloc(r * (static_cast<size_t>(e->tiles_cap * kRows) * e->lay.rs_ld + 256));
     e->loss_part.alloc(e->tiles_cap);
     e->psg.alloc(r * static_cast<size_t>(kc) * (2 + S));
     e->es_sq_part.alloc(e->es_blocks);
@@ -931,6 +960,13 @@ size_t finish_smem(const NetLayout& lay) {
     return std::max(es, gemm);
 }
 
+// K3's launch smem: the tensor-core weight-gradient blocks need kUSmem (+ 1 KB alignment)
+template <typename Real>
+size_t finish_smem_launch(const NetLayout& lay, bool umma) {
+    const size_t f = finish_smem<Real>(lay);
+    return umma ? std::max(f, static_cast<size_t>(kUSmem) + 1024) : f;
+}
+
 // The tile kernel's scans are specialised for the M4 seasonalities (S = 1, 4, 12: seasonal
 // ring in registers); any other S runs the generic variant.
 template <typename Real, int MODE, int SC>
@@ -947,7 +983,7 @@ void set_sc_attrs(const NetLayout& lay) {
     set_tile_attr<Real, kTrain, SC>(lay);
     set_tile_attr<Real, kLossOnly, SC>(lay);
     CUDA_OK(cudaFuncSetAttribute(k_grad_finish<Real, SC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)finish_smem<Real>(lay)));
+                                 (int)finish_smem_launch<Real>(lay, sizeof(Real) == 4)));
 }
 
 template <typename Real>
@@ -992,8 +1028,10 @@ void launch_k(Eng* e, bool pdl, void (*kern)(KArgs...), int grid, int block, siz
 
 template <typename Real, int SC>
 void launch_finish_sc(Eng* e, const StateDev<Real>& st, const PlanDev& pv, int s, int finalize, bool pdl) {
-    launch_k(e, pdl, k_grad_finish<Real, SC>, e->es_blocks + e->red_blocks * e->gsplit, kFinishThreads,
-             finish_smem<Real>(e->lay), st, pv, e->lay, s, e->es_blocks, finalize, e->gsplit);
+    const int gemm_blocks = e->umma_parts > 0 ? e->umma_tiles * e->umma_parts : e->red_blocks * e->gsplit;
+    launch_k(e, pdl, k_grad_finish<Real, SC>, e->es_blocks + gemm_blocks, kFinishThreads,
+             finish_smem_launch<Real>(e->lay, e->umma_parts > 0), st, pv, e->lay, s, e->es_blocks, finalize, e->gsplit,
+             e->umma_parts);
 }
 template <typename Real>
 void launch_finish(Eng* e, const StateDev<Real>& st, const PlanDev& pv, int s, int finalize, bool pdl = false) {
@@ -1093,7 +1131,8 @@ void launch_step(Eng* e, const PlanDev& pv, int s, bool grads, bool update, Stat
         const int net_blocks = static_cast<int>((lay.P_pad + 255) / 256);
         const int spb = 256 / (2 + e->S);  // slots per per-series block (a thread per parameter)
         const int slot_blocks = (kc + spb - 1) / spb;
-        launch_k(e, false, k_adam<Real>, net_blocks + slot_blocks, 256, 0, st, pv, lay, s,
+        static const bool k4_pdl = std::getenv("ESRNN_K4_PDL") != nullptr;
+        launch_k(e, k4_pdl, k_adam<Real>, net_blocks + slot_blocks, 256, 0, st, pv, lay, s,
                  sharded ? -1 : e->es_blocks, e->red_blocks, net_blocks);
         e->launches += 1;
     }
@@ -1449,7 +1488,7 @@ double train_epoch_impl(Eng* e) {
         key_append(key, pv);
         key_append(key, e->lay);
         const long long dims[11] = {steps, e->tiles_cap, e->es_blocks, e->red_blocks, e->kcap, e->S, e->rank,
-                                    e->world, e->gsplit, e->fp64 ? 8 : 4, e->sharded ? 1 : 0};
+                                    e->world, e->gsplit * 256 + e->umma_parts, e->fp64 ? 8 : 4, e->sharded ? 1 : 0};
         key_append(key, dims);
         key_append(key, e->stream == nullptr);
         // A sharded graph captures this trainer's communicator (NCCL) or group slots: it is

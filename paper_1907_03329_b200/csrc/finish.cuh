@@ -10,6 +10,7 @@
 #pragma once
 #include "common.cuh"
 #include "tile.cuh"
+#include "umma.cuh"
 
 namespace esrnn_dev {
 
@@ -47,6 +48,58 @@ __device__ void finalize_scalars(StateDev<Real>& st, const PlanDev& pl, int s, d
 }
 
 // ---------------------------------------------------------------------------------------
+// K3 weight-gradient block on the tensor cores (fp32 mode, large steps; umma.cuh): block
+// gbp = (tile, part).  Tiles enumerate the matrices' 128-row slices (layer W_in^T [3H][in],
+// nl_w^T, out_w^T); part p contracts the step's rows [p*span, (p+1)*span) into a 128 x 64
+// partial (columns: the K inputs, then the bias column) in st.upart.  The last part to finish
+// a tile (ticket) sums the parts in part order -- fixed order, no float atomics -- and writes
+// the tile's gradients and bias gradients into gbuf and its squared norm into red_sq_part.
+__device__ __forceinline__ void dw_umma_block(StateDev<float>& st, const PlanDev& pl, const NetLayout& lay, int s,
+                                              int gbp, int parts, unsigned char* smem_raw, double* red) {
+    const int tile = gbp / parts, part = gbp - tile * parts;
+    int m = 0, t0 = 0;
+    for (; m < lay.nmat; ++m) {
+        const int nt = (lay.mats[m].Q + kUM - 1) / kUM;
+        if (tile < t0 + nt) break;
+        t0 += nt;
+    }
+    const MatDesc md = lay.mats[m];
+    const int mt = tile - t0;
+    const int Mv = min(kUM, md.Q - mt * kUM), Kv = md.K;
+    const int wb0 = pl.step_win_off[s];
+    const int Bstep = pl.step_win_off[s + 1] - wb0;
+    const int span = ((Bstep + parts - 1) / parts + kUK - 1) / kUK * kUK;
+    const int r0 = min(Bstep, part * span), nrows = min(Bstep, r0 + span) - r0;
+    float* mine = st.upart + (size_t)(tile * parts + part) * kUM * kUN;
+    unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    umma_partial_dw(sm, st.rowstore + md.a_off + mt * kUM, st.rowstore + md.u_off, lay.rs_ld, r0, nrows, Kv, mine);
+    __shared__ bool last_part;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last_part = atomicAdd(st.gtile_ctr + tile, 1u) == static_cast<unsigned>(parts - 1);
+    __syncthreads();
+    if (!last_part) return;
+    __threadfence();
+    if (threadIdx.x == 0) st.gtile_ctr[tile] = 0;
+    double sq = 0.0;
+    for (int e = threadIdx.x; e < Mv * (Kv + 1); e += blockDim.x) {
+        const int q = e / (Kv + 1), k = e - q * (Kv + 1);
+        float g = 0.f;
+        for (int p = 0; p < parts; ++p) g += __ldcg(st.upart + (size_t)(tile * parts + p) * kUM * kUN + q * kUN + k);
+        const int qq = mt * kUM + q;
+        if (k < Kv) st.gbuf[md.cw + (long long)qq * md.ldk + k] = g;
+        else st.gbuf[md.cb + qq] = g;
+        sq += static_cast<double>(g) * g;
+    }
+    const double tot = block_sum(sq, red);
+    if (threadIdx.x == 0) {
+        st.red_sq_part[tile] = tot;
+        if (tile == 0)  // the FFMA path's tile count is what the finalisers sum over
+            for (int i = st.umma_tiles; i < st.red_tiles; ++i) st.red_sq_part[i] = 0.0;
+    }
+}
+
+// ---------------------------------------------------------------------------------------
 // K3 ES block, fp32 mode: per-slot window-adjoint gather + reverse Holt-Winters adjoint for
 // kEsSlots32 slots.  Everything that does not depend on K2's output runs BEFORE the
 // dependency wait, overlapping K2 (whose tiles release this grid once they pass their own
@@ -59,15 +112,15 @@ __device__ void finalize_scalars(StateDev<Real>& st, const PlanDev& pl, int s, d
 // Returns the thread's squared-gradient and penalty partials.
 template <typename Real, int SC>
 __device__ __forceinline__ void es_block_fp32(StateDev<Real>& st, const PlanDev& pl, const NetLayout& lay, int s,
-                                              unsigned char* smem_raw, double& sq, double& pen) {
+                                              unsigned char* smem_raw, double& sq, double& pen, int bid) {
     constexpr int bd = kEsSlots32;
     const int tid = threadIdx.x;
     auto clk = [&](int i) {
-        if (st.dbg_clk && blockIdx.x == 0 && tid == 0) st.dbg_clk[32 + i] = clock64();
+        if (st.dbg_clk && bid == 0 && tid == 0) st.dbg_clk[32 + i] = clock64();
     };
     const int k0 = pl.step_slot_off[s];
     const int k = pl.step_slot_off[s + 1] - k0;
-    const int sl0 = blockIdx.x * bd, sl1 = min(k, sl0 + bd);
+    const int sl0 = bid * bd, sl1 = min(k, sl0 + bd);
     if (!(sl0 < sl1 && st.attach)) {  // uniform per block
         pdl_wait();
         SPAN_BEGIN(st, s, kSpanFinish);
@@ -314,7 +367,8 @@ __device__ __forceinline__ void es_block_fp32(StateDev<Real>& st, const PlanDev&
 
 template <typename Real, int SC>
 __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> st, PlanDev pl, NetLayout lay, int s,
-                                                                int es_blocks, int finalize, int gsplit) {
+                                                                int es_blocks, int finalize, int gsplit,
+                                                                int umma_parts) {
     using M = Math<Real>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ double red[32];
@@ -333,15 +387,22 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
     FCLK();
     DBG_GT(st, 4);
     DBG_SPAN_MIN(st, s, 3);
-    if (static_cast<int>(blockIdx.x) < es_blocks && sizeof(Real) == 4) {
-        if constexpr (sizeof(Real) == 4) es_block_fp32<Real, SC>(st, pl, lay, s, smem_raw, sq, pen);
+    // large (tensor-core) steps: the dW blocks take the low block indices, so the long
+    // contraction starts first and the many short ES blocks fill in around it; otherwise the
+    // ES blocks come first (they pre-compute on the SMs K2 leaves free)
+    const int ngemm = umma_parts > 0 ? static_cast<int>(gridDim.x) - es_blocks : 0;
+    const int bid = umma_parts > 0 ? (static_cast<int>(blockIdx.x) < ngemm ? es_blocks + static_cast<int>(blockIdx.x)
+                                                                           : static_cast<int>(blockIdx.x) - ngemm)
+                                   : static_cast<int>(blockIdx.x);
+    if (bid < es_blocks && sizeof(Real) == 4) {
+        if constexpr (sizeof(Real) == 4) es_block_fp32<Real, SC>(st, pl, lay, s, smem_raw, sq, pen, bid);
         const double tot = block_sum(sq, red);
-        if (tid == 0) st.es_sq_part[blockIdx.x] = tot;
+        if (tid == 0) st.es_sq_part[bid] = tot;
         if (st.lvp > 0.0) {
             const double pt = block_sum(pen, red);
-            if (tid == 0) st.es_pen_part[blockIdx.x] = pt;
+            if (tid == 0) st.es_pen_part[bid] = pt;
         }
-    } else if (static_cast<int>(blockIdx.x) < es_blocks) {
+    } else if (bid < es_blocks) {
         // ---------------- per-slot window-adjoint gather + reverse HW scan ---------------
         const int k0 = pl.step_slot_off[s];
         const int k = pl.step_slot_off[s + 1] - k0;
@@ -698,6 +759,10 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
             const double pt = block_sum(pen, red);
             if (tid == 0) st.es_pen_part[blockIdx.x] = pt;
         }
+    } else if (sizeof(Real) == 4 && umma_parts > 0) {
+        pdl_wait();
+        SPAN_BEGIN(st, s, kSpanFinish);
+        if constexpr (sizeof(Real) == 4) dw_umma_block(st, pl, lay, s, bid - es_blocks, umma_parts, smem_raw, red);
     } else {
         pdl_wait();
         SPAN_BEGIN(st, s, kSpanFinish);
@@ -863,7 +928,7 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
     }
     FCLK();
     DBG_SPAN_MAX(st, s, 5);
-    if (static_cast<int>(blockIdx.x) < es_blocks) DBG_SPAN_MAX(st, s, 10);
+    if (bid < es_blocks) DBG_SPAN_MAX(st, s, 10);
     else DBG_SPAN_MAX(st, s, 11);
     SPAN_END(st, s, kSpanFinish);
     if (finalize & 4) {

@@ -72,3 +72,16 @@ def test_cpp_header_compiles(tmp_path):
     r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-I" + str(ROOT / "include"), str(src)],
                        capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
+
+
+def test_product_library_contains_tcgen05_code():
+    """The sm_100a cubin carries the tensor-core weight-gradient path: tcgen05.mma (UTCHMMA),
+    TMEM loads (LDTM) and TMEM allocation -- checked on the built library, no GPU needed."""
+    import shutil
+    import subprocess
+    from paper_1907_03329_b200 import _native as N
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    sass = subprocess.run([exe, "-sass", str(N.PRODUCT_LIB)], capture_output=True, text=True).stdout
+    assert "UTCHMMA" in sass or "UTCMMA" in sass
+    assert "LDTM" in sass
+    assert "UTCATOMSWS" in sass  # tcgen05.alloc
