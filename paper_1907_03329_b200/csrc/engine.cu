@@ -982,8 +982,11 @@ template <typename Real, int SC>
 void set_sc_attrs(const NetLayout& lay) {
     set_tile_attr<Real, kTrain, SC>(lay);
     set_tile_attr<Real, kLossOnly, SC>(lay);
-    CUDA_OK(cudaFuncSetAttribute(k_grad_finish<Real, SC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)finish_smem_launch<Real>(lay, sizeof(Real) == 4)));
+    CUDA_OK(cudaFuncSetAttribute(k_grad_finish<Real, SC, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)finish_smem<Real>(lay)));
+    if (sizeof(Real) == 4)
+        CUDA_OK(cudaFuncSetAttribute(k_grad_finish<Real, SC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)finish_smem_launch<Real>(lay, true)));
 }
 
 template <typename Real>
@@ -1029,9 +1032,13 @@ void launch_k(Eng* e, bool pdl, void (*kern)(KArgs...), int grid, int block, siz
 template <typename Real, int SC>
 void launch_finish_sc(Eng* e, const StateDev<Real>& st, const PlanDev& pv, int s, int finalize, bool pdl) {
     const int gemm_blocks = e->umma_parts > 0 ? e->umma_tiles * e->umma_parts : e->red_blocks * e->gsplit;
-    launch_k(e, pdl, k_grad_finish<Real, SC>, e->es_blocks + gemm_blocks, kFinishThreads,
-             finish_smem_launch<Real>(e->lay, e->umma_parts > 0), st, pv, e->lay, s, e->es_blocks, finalize, e->gsplit,
-             e->umma_parts);
+    if (e->umma_parts > 0)
+        launch_k(e, pdl, k_grad_finish<Real, SC, true>, e->es_blocks + gemm_blocks, kFinishThreads,
+                 finish_smem_launch<Real>(e->lay, true), st, pv, e->lay, s, e->es_blocks, finalize, e->gsplit,
+                 e->umma_parts);
+    else
+        launch_k(e, pdl, k_grad_finish<Real, SC, false>, e->es_blocks + gemm_blocks, kFinishThreads,
+                 finish_smem<Real>(e->lay), st, pv, e->lay, s, e->es_blocks, finalize, e->gsplit, 0);
 }
 template <typename Real>
 void launch_finish(Eng* e, const StateDev<Real>& st, const PlanDev& pv, int s, int finalize, bool pdl = false) {

@@ -365,10 +365,13 @@ __device__ __forceinline__ void es_block_fp32(StateDev<Real>& st, const PlanDev&
     clk(9);
 }
 
-template <typename Real, int SC>
+// UMMA: the tensor-core weight-gradient instantiation (large fp32 steps); the small-step
+// kernel is compiled without that code (it changes the ES path's register allocation)
+template <typename Real, int SC, bool UMMA>
 __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> st, PlanDev pl, NetLayout lay, int s,
                                                                 int es_blocks, int finalize, int gsplit,
-                                                                int umma_parts) {
+                                                                int umma_parts_arg) {
+    const int umma_parts = UMMA ? umma_parts_arg : 0;
     using M = Math<Real>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ double red[32];
@@ -759,10 +762,10 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
             const double pt = block_sum(pen, red);
             if (tid == 0) st.es_pen_part[blockIdx.x] = pt;
         }
-    } else if (sizeof(Real) == 4 && umma_parts > 0) {
+    } else if (UMMA && sizeof(Real) == 4) {
         pdl_wait();
         SPAN_BEGIN(st, s, kSpanFinish);
-        if constexpr (sizeof(Real) == 4) dw_umma_block(st, pl, lay, s, bid - es_blocks, umma_parts, smem_raw, red);
+        if constexpr (UMMA && sizeof(Real) == 4) dw_umma_block(st, pl, lay, s, bid - es_blocks, umma_parts, smem_raw, red);
     } else {
         pdl_wait();
         SPAN_BEGIN(st, s, kSpanFinish);
