@@ -1058,7 +1058,9 @@ void launch_tile_sc(Eng* e, int grid, const StateDev<Real>& st, const PlanDev& p
     // Resident weights (one TMA copy, one CTA per SM) win while the grid is about one wave;
     // from two waves on, per-layer staging lets two fp32 CTAs share an SM and hide each
     // other's phase latencies (measured: B=4,096 tile -15%, B=48,000 -18%; cfg1 +40%).
-    const bool two_waves = sizeof(Real) == 4 && grid >= 2 * g_num_sms &&
+    static const int stage_min = std::getenv("ESRNN_TILE_STAGED_MIN") ? std::atoi(std::getenv("ESRNN_TILE_STAGED_MIN"))
+                                                                       : 2 * g_num_sms;
+    const bool two_waves = sizeof(Real) == 4 && grid >= stage_min &&
                            2 * (stack_smem<Real>(lay, false) + 1024) <= static_cast<size_t>(g_smem_per_sm);
     if (stack_resident<Real>(lay) && !two_waves)
         launch_k(e, pdl, k_tile<Real, MODE, true, SC>, grid, nt, stack_smem<Real>(lay, true), st, pv, lay, s, fa);
@@ -1923,9 +1925,10 @@ void forward_stack_impl(Eng* e, int Tq, int B, const double* inputs, double* out
     int dmax = 1;
     for (int l = 0; l < e->L; ++l) dmax = std::max(dmax, sl.dil[l]);
     const size_t G = 4 * static_cast<size_t>(e->H);
-    const size_t fast_smem = r * ((static_cast<size_t>(sl.in_max) + e->H + 1) * G + static_cast<size_t>(sl.in_max) * kSeqFR +
+    const size_t fast_smem = r * ((static_cast<size_t>(sl.in_max) + e->H + 1) * G + 2 * static_cast<size_t>(sl.in_max) * kSeqFR +
                                   2 * static_cast<size_t>(dmax) * e->H * kSeqFR + kSeqFR * G);
-    const bool fast = !out_bar && fast_smem <= static_cast<size_t>(g_smem_optin) && G <= 320 &&
+    const bool fast = !out_bar && fast_smem <= static_cast<size_t>(g_smem_optin) &&
+                      kSeqSplit * ((G + 31) / 32 * 32) <= 1024 &&
                       std::getenv("ESRNN_SEQ_NAIVE") == nullptr;
     const int nfast = (B + kSeqFR - 1) / kSeqFR;
     if (!fast) scratch.alloc(r * static_cast<size_t>(nblk) * SeqScratch<Real>::size(sl));
@@ -1936,7 +1939,7 @@ void forward_stack_impl(Eng* e, int Tq, int B, const double* inputs, double* out
     }
     CUDA_OK(cudaEventRecord(e->ev0, e->stream));
     if (fast) {
-        const int nt = static_cast<int>((std::max<size_t>(G, 32) + 31) / 32 * 32);
+        const int nt = kSeqSplit * static_cast<int>((std::max<size_t>(G, 32) + 31) / 32 * 32);
         k_seq_fwd_fast<Real><<<nfast, nt, fast_smem, e->stream>>>(sl, reinterpret_cast<const Real*>(w.p),
                                                                   reinterpret_cast<const Real*>(x.p),
                                                                   reinterpret_cast<Real*>(scratch.p), dout.p);

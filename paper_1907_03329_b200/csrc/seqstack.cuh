@@ -268,10 +268,10 @@ __global__ void __launch_bounds__(kSeqThreads) k_seq_backward(SeqLayout s, const
 // Inference forward_stack at speed: k_seq_fwd_fast.  A CTA owns kSeqFR batch rows for the
 // whole sequence; per layer its input (W_in), recurrent (W_rec) and bias weights sit in
 // shared memory, and each step is two barrier-separated phases:
-//   gates: thread j (one per gate column, 4H <= blockDim) accumulates its column for all
-//          kSeqFR rows in registers -- x_t W_in over the staged layer input, then h_{t-d}
-//          W_rec from the recurrent ring -- one shared-memory weight load feeds kSeqFR FMAs,
-//          the row values are broadcast reads ([k][row] layout, 16-byte vectors)
+//   gates: kSeqSplit threads per gate column (4H <= 256) each accumulate the column for a
+//          quarter of the kSeqFR rows in registers -- x_t W_in over the staged layer input, then h_{t-d}
+//          W_rec from the recurrent ring -- one shared-memory weight load feeds kSeqFR/2
+//          FMAs, the row values are broadcast reads ([k][row] layout, 16-byte vectors)
 //   cell:  thread per (row, unit): c = f c_{t-d} + i g, h = o tanh(c) into the (h, c) rings
 //          (depth d: slot t mod d holds step t), the layer output to the CTA's private
 //          sequence buffer (L2 resident) with the block skip added, and the next step's
@@ -279,9 +279,10 @@ __global__ void __launch_bounds__(kSeqThreads) k_seq_backward(SeqLayout s, const
 // Same summation order as k_seq_forward (x W_in, + h W_rec, + bias).  Used when no adjoint
 // is requested and the layer weights fit in shared memory (host: seq_fast_smem).
 constexpr int kSeqFR = 16;
+constexpr int kSeqSplit = 4;  // threads per gate column in the gate phase
 
 template <typename Real>
-__global__ void __launch_bounds__(320) k_seq_fwd_fast(SeqLayout s, const Real* __restrict__ W,
+__global__ void __launch_bounds__(1024) k_seq_fwd_fast(SeqLayout s, const Real* __restrict__ W,
                                                        const Real* __restrict__ X, Real* __restrict__ seqbuf,
                                                        double* out) {
     using M = Math<Real>;
@@ -291,10 +292,10 @@ __global__ void __launch_bounds__(320) k_seq_fwd_fast(SeqLayout s, const Real* _
     const int tid = threadIdx.x, NT = blockDim.x, H = s.H, G = 4 * H, T = s.T;
     int dmax = 1;
     for (int l = 0; l < s.L; ++l) dmax = max(dmax, s.dil[l]);
-    // shared layout: weights [in_max + H + 1][G] | xs [in_max][R] | hring, cring [dmax][H][R] | gates [R][G]
+    // shared layout: weights [in_max + H + 1][G] | xs [2][in_max][R] | hring, cring [dmax][H][R] | gates [R][G]
     Real* Ws = reinterpret_cast<Real*>(smem_raw);
     Real* xs = Ws + static_cast<size_t>(s.in_max + H + 1) * G;
-    Real* hr = xs + static_cast<size_t>(s.in_max) * R;
+    Real* hr = xs + 2 * static_cast<size_t>(s.in_max) * R;
     Real* cr = hr + static_cast<size_t>(dmax) * H * R;
     Real* gs = cr + static_cast<size_t>(dmax) * H * R;
     // per-CTA sequence buffers: two layer outputs in flight + the current block's input
@@ -313,43 +314,62 @@ __global__ void __launch_bounds__(320) k_seq_fwd_fast(SeqLayout s, const Real* _
         for (int e = tid; e < H * G; e += NT) Ws[K * G + e] = Wr[e];
         for (int e = tid; e < G; e += NT) Ws[(K + H) * G + e] = Bi[e];
         for (int e = tid; e < 2 * d * H * R; e += NT) hr[e] = Real(0);  // h and c rings are contiguous
-        // stage x_0 as [k][row]
-        for (int e = tid; e < K * R; e += NT) {
-            const int k = e / R, r = e - k * R;
-            Real v = 0;
-            if (r < nr) v = l == 0 ? X[(static_cast<size_t>(0) * s.B + b0 + r) * s.in0 + k] : Xin[(static_cast<size_t>(0) * R + r) * H + k];
-            xs[e] = v;
-        }
+        // x_t as [k][row] in buffer t & 1, copied asynchronously one step ahead (rows past
+        // the batch stay zero: the buffers are cleared per layer)
+        auto stage_x = [&](int t) {
+            Real* dst = xs + static_cast<size_t>(t & 1) * s.in_max * R;
+            for (int e = tid; e < K * nr; e += NT) {
+                const int k = e / nr, r = e - k * nr;
+                const Real* src = l == 0 ? X + (static_cast<size_t>(t) * s.B + b0 + r) * s.in0 + k
+                                         : Xin + (static_cast<size_t>(t) * R + r) * H + k;
+                cp_async_elem(dst + k * R + r, src);
+            }
+            cp_async_commit();
+        };
+        for (int e = tid; e < 2 * s.in_max * R; e += NT) xs[e] = Real(0);
+        __syncthreads();
+        stage_x(0);
+        cp_async_wait_all();
         __syncthreads();
         for (int t = 0; t < T; ++t) {
+            const Real* xcur = xs + static_cast<size_t>(t & 1) * s.in_max * R;
+            if (t + 1 < T) stage_x(t + 1);  // lands during this step's two phases
             // ---- gates ----
-            if (tid < G) {
-                Real acc[R], a2[R];
+            // kSeqSplit threads per gate column, each over R / kSeqSplit rows: more warps to
+            // hide the shared-memory latency of the k loops (one CTA per SM holds the weights)
+            const int Gp = (G + 31) & ~31;
+            const int col = tid % Gp, half = tid / Gp;
+            if (col < G && half < kSeqSplit) {
+                constexpr int RH = R / kSeqSplit;
+                Real acc[RH], a2[RH];
 #pragma unroll
-                for (int r = 0; r < R; ++r) acc[r] = 0, a2[r] = 0;
-                const Real* wcol = Ws + tid;
-                for (int k = 0; k < K; ++k) {
+                for (int r = 0; r < RH; ++r) acc[r] = 0, a2[r] = 0;
+                const Real* wcol = Ws + col;
+                const Real* xh = xcur + half * RH;
+#pragma unroll 4
+                for (int k = 0; k < K; ++k) {  // unrolled: the next k's loads issue under these FMAs
                     const Real w = wcol[k * G];
-                    const Real* xk = xs + k * R;
+                    const Real* xk = xh + k * R;
 #pragma unroll
-                    for (int r = 0; r < R; ++r) acc[r] += xk[r] * w;
+                    for (int r = 0; r < RH; ++r) acc[r] += xk[r] * w;
                 }
                 if (t >= d) {
-                    const Real* hp = hr + static_cast<size_t>((t - d) % d) * H * R;
-                    const Real* wrc = Ws + K * G + tid;
+                    const Real* hp = hr + static_cast<size_t>((t - d) % d) * H * R + half * RH;
+                    const Real* wrc = Ws + K * G + col;
+#pragma unroll 4
                     for (int k = 0; k < H; ++k) {
                         const Real w = wrc[k * G];
                         const Real* hk = hp + k * R;
 #pragma unroll
-                        for (int r = 0; r < R; ++r) a2[r] += hk[r] * w;
+                        for (int r = 0; r < RH; ++r) a2[r] += hk[r] * w;
                     }
                 }
-                const Real b = Ws[(K + H) * G + tid];
-                const bool is_g = tid >= 2 * H && tid < 3 * H;
+                const Real b = Ws[(K + H) * G + col];
+                const bool is_g = col >= 2 * H && col < 3 * H;
 #pragma unroll
-                for (int r = 0; r < R; ++r) {
+                for (int r = 0; r < RH; ++r) {
                     const Real v = (t >= d ? acc[r] + a2[r] : acc[r]) + b;
-                    gs[r * G + tid] = is_g ? M::tanh(v) : M::logistic(v);
+                    gs[(half * RH + r) * G + col] = is_g ? M::tanh(v) : M::logistic(v);
                 }
             }
             __syncthreads();
@@ -368,15 +388,7 @@ __global__ void __launch_bounds__(320) k_seq_fwd_fast(SeqLayout s, const Real* _
                 if (s.res_src[l] >= 0) Y[q] = h + bin[q];
                 else Y[q] = h;
             }
-            if (t + 1 < T)
-                for (int e = tid; e < K * R; e += NT) {
-                    const int k = e / R, r = e - k * R;
-                    Real v = 0;
-                    if (r < nr)
-                        v = l == 0 ? X[(static_cast<size_t>(t + 1) * s.B + b0 + r) * s.in0 + k]
-                                   : Xin[(static_cast<size_t>(t + 1) * R + r) * H + k];
-                    xs[e] = v;
-                }
+            cp_async_wait_all();
             __syncthreads();
         }
         // the block skip of a later layer m adds the output of layer res_src[m] (the previous
