@@ -26,12 +26,18 @@ for k in k_tile k_grad_finish k_adam k_forecast_scan; do
     -o gpurun_out/${TAG}_cfg1_$k python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e \
     > gpurun_out/${TAG}_ncu_cfg1_$k.log 2>&1; echo "ncu cfg1 $k rc=$?"
 done
-for k in k_tile k_forecast_scan; do
+for k in k_tile k_grad_finish k_adam k_forecast_scan; do
   skip=20; [ $k = k_forecast_scan ] && skip=1
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k -s $skip -c 1 \
     -o gpurun_out/${TAG}_cfg3_$k python bench.py --config cfg3 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e \
     > gpurun_out/${TAG}_ncu_cfg3_$k.log 2>&1; echo "ncu cfg3 $k rc=$?"
 done
+# the tensor-core weight-gradient blocks at the sweep end (B = 48,000)
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_grad_finish -s 3 -c 1 \
+  -o gpurun_out/${TAG}_sweep48000_k_grad_finish python bench.py --config sweep48000 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e \
+  > gpurun_out/${TAG}_ncu_sweep.log 2>&1; echo "ncu sweep48000 k_grad_finish rc=$?"
+python tools/ncu_summary.py full gpurun_out/${TAG}_sweep48000_*.ncu-rep > gpurun_out/${TAG}_ncu_full_sweep48000.txt 2>&1
+timeout 600 python bench.py --config sweep48000 --no-cpu-baseline --no-e2e > gpurun_out/${TAG}_bench_sweep48000.json 2>/dev/null
 # summaries on the box (the reps exceed gpurun's 64 MiB return limit); keep only k_tile's rep
 python tools/ncu_summary.py full gpurun_out/${TAG}_cfg1_*.ncu-rep > gpurun_out/${TAG}_ncu_full_cfg1.txt 2>&1
 python tools/ncu_summary.py full gpurun_out/${TAG}_cfg3_*.ncu-rep > gpurun_out/${TAG}_ncu_full_cfg3.txt 2>&1
@@ -39,6 +45,6 @@ python tools/ncu_summary.py traffic gpurun_out/${TAG}_ncu_traffic_cfg1.json cfg1
 python tools/ncu_summary.py traffic gpurun_out/${TAG}_ncu_traffic_cfg3.json cfg3 gpurun_out/${TAG}_cfg3_*.ncu-rep > /dev/null 2>&1
 python tools/ncu_summary.py launches gpurun_out/${TAG}_launches.csv > gpurun_out/${TAG}_launches.txt 2>&1
 rm -f gpurun_out/${TAG}_cfg1_k_grad_finish.ncu-rep gpurun_out/${TAG}_cfg1_k_adam.ncu-rep gpurun_out/${TAG}_cfg1_k_forecast_scan.ncu-rep \
-      gpurun_out/${TAG}_cfg3_*.ncu-rep gpurun_out/${TAG}_launches.csv
+      gpurun_out/${TAG}_cfg3_*.ncu-rep gpurun_out/${TAG}_sweep48000_*.ncu-rep gpurun_out/${TAG}_launches.csv
 du -sh gpurun_out
 for f in gpurun_out/${TAG}_bench_*.json; do echo "== $f"; tail -1 $f | cut -c1-400; done
