@@ -735,7 +735,8 @@ void ensure_capacity(Eng* e, int B) {
     // two blocks per SM over the matrices' 128-row tiles, parts of >= 256 rows
     e->umma_parts = 0;
     e->umma_tiles = 0;
-    if (!e->fp64 && B >= kUmmaMinRows && std::getenv("ESRNN_NO_UMMA") == nullptr &&
+    static const int umma_min = std::getenv("ESRNN_UMMA_MIN") ? std::atoi(std::getenv("ESRNN_UMMA_MIN")) : kUmmaMinRows;
+    if (!e->fp64 && B >= umma_min && std::getenv("ESRNN_NO_UMMA") == nullptr &&
         static_cast<size_t>(g_smem_optin) >= static_cast<size_t>(kUSmem) + 1024) {
         bool fits = true;
         for (int m = 0; m < e->lay.nmat; ++m) {

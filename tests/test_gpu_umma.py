@@ -1,4 +1,4 @@
-"""The tensor-core weight-gradient path (K3 on steps of >= 8,192 windows, fp32): tcgen05.mma
+"""The tensor-core weight-gradient path (K3 on steps of >= 4,096 windows, fp32): tcgen05.mma
 kind::tf32 with a 3xTF32 split (csrc/umma.cuh, finish.cuh dw_umma_block), against the fp64
 oracle at the north-star 1e-4 (pinball kinks masked on both sides, as in
 test_gpu_fp32_contract.py), against the CUDA-core path (ESRNN_NO_UMMA), and for determinism.
