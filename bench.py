@@ -489,7 +489,8 @@ def main():
         kern[name] = {"class": cls, "ms_per_step": ms_tot / (n_span_epochs if cls != "forecast" else 1),
                       "launches_per_step": launches / (n_span_epochs if cls != "forecast" else 1),
                       "avg_us": avg_s * 1e6, "algorithmic_per_launch": work, "achieved": ach, "unit": unit,
-                      "peak": peak, "frac": ach / peak, "work": note, "traffic": traffic.get(name)}
+                      "peak": peak, "frac": ach / peak, "work": note,
+                      "traffic": traffic.get(name, traffic.get(name + "_sc"))}
 
     fwd_epoch = lstm_fwd_flops(prof, windows_local)
     ms, n = kt["tile"]

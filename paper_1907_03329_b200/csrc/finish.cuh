@@ -406,273 +406,150 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
             if (tid == 0) st.es_pen_part[bid] = pt;
         }
     } else if (bid < es_blocks) {
-        // ---------------- per-slot window-adjoint gather + reverse HW scan ---------------
-        const int k0 = pl.step_slot_off[s];
-        const int k = pl.step_slot_off[s + 1] - k0;
-        const int sl0 = blockIdx.x * kEsSlotsPerBlock;
-        const int sl1 = min(k, sl0 + kEsSlotsPerBlock);
-        if (sl0 < sl1 && st.attach) {  // uniform per block
-            const int N = st.N, S = SC > 0 ? SC : lay.S, T = lay.T, I = lay.I, O = lay.O, kc = st.kcap;
-            const int bd = kEsSlotsPerBlock, tp = row_pad<Real>(T), cwp = st.cwp;
-            const int slot = sl0 + tid;
-            const bool mine = tid < bd && slot < sl1;
-            const int lane = tid & 31;                                         // slot lane (bd == 32)
-            // window adjoints row-major per slot (odd strides: the per-slot reverse scan reads
-            // them conflict-free; the per-window warp scatter writes consecutive words)
-            // The ES adjoint runs in double in both precisions (see the K2 contributions): the
-            // level and seasonality paths of a window's adjoint cancel almost exactly, so their
-            // accumulation and the reverse recursion must not round on their own
-            const int ldl = T | 1, lds = (T + S) | 1;
-            double* LB = reinterpret_cast<double*>(smem_raw);                  // [bd][ldl] level adjoint
-            double* SB = LB + bd * ldl;                                        // [bd][lds] seasonality adjoint
-            // forward states: double when K3 recomputes them (fp32, S = 1) or in fp64 mode
-            using SR = std::conditional_t<kEsRecompute<Real, SC>, double, Real>;
-            SR* LV = reinterpret_cast<SR*>(SB + bd * lds);                     // [T][bd]   forward levels
-            SR* SE = LV + T * bd;                                              // [T][bd]   forward seasonalities
-            Real* YS = reinterpret_cast<Real*>(SE + T * bd);                   // [bd][tp]  observation rows
-            double* cbuf = reinterpret_cast<double*>(YS + bd * tp);            // [kEsChunk][cwp]
-            double* lb = LB + tid * ldl;
-            double* sb = SB + tid * lds;
-            SR* lvs = LV + tid;
-            SR* ses = SE + tid;
-            Real* ys = YS + tid * tp;
-            FCLK();
-            // ---- stage the forward state with the whole block (every copy in flight at once) ----
-            const bool lane_ok = sl0 + lane < sl1;
-            const int lrow = lane_ok ? pl.slot_row[k0 + sl0 + lane] : 0;
-            constexpr int e16 = 16 / static_cast<int>(sizeof(Real));
-            constexpr int d16 = 2;  // doubles per 16-byte copy
-            // observation rows are epoch constants: staged before the dependency wait
-            if (lane_ok)
-                for (int ch = tid >> 5; ch * e16 < tp; ch += kFinishThreads / 32)
-                    cp_async16(YS + lane * tp + ch * e16, st.vrm + (size_t)lrow * st.ldv + ch * e16);
-            Real a_raw = 0, g_raw = 0;
-            Real s0[SC > 0 ? SC : 1];  // exp(seas_raw) for the output's chain rule, loaded up front
-            double l0 = 0;             // l[-1] = mean(y[0:S]) (holt_winters.hpp:247-250)
-            if constexpr (kEsRecompute<Real, SC>) {
-                // fp32 mode, S = 1: the forward levels / seasonalities the adjoint is linearised
-                // at are recomputed here in double (the reference's arithmetic) instead of taken
-                // from K2's fp32 scan.  The adjoint sums of a series' window terms cancel almost
-                // exactly (x = y/(s*l) is invariant under s -> c*s, l -> l/c except through
-                // l[-1]); with a single seasonal index that mode is the init seasonality itself,
-                // and linearised at fp32-rounded states its gradient is off by ~1e-3 of its
-                // tensor (at double states ~1e-7).  For S > 1 the fp32 states keep it ~1e-7
-                // (oracle emulation), so K2's published states are used (a T = 72 double
-                // recompute costs ~20 us of serial latency).  Runs before the dependency wait,
-                // overlapping K2: the per-series parameters are the previous step's K4 output
-                // (complete before K2 passed its own wait and released this grid), read at L2.
-                cp_async_wait_all();
-                __syncthreads();
-                if (mine) {
-                    a_raw = __ldcg(st.ps + lrow);
-                    g_raw = __ldcg(st.ps + N + lrow);
-                    const double al = Math<double>::logistic(static_cast<double>(a_raw));
-                    const double ga = Math<double>::logistic(static_cast<double>(g_raw));
-                    for (int j = 0; j < S; ++j) {
-                        const Real r = __ldcg(st.ps + (size_t)(2 + j) * N + lrow);
-                        if constexpr (SC > 0) s0[j] = r;
-                        if (j < T) ses[j * bd] = Math<double>::exp(static_cast<double>(r));
-                    }
-                    for (int j = 0; j < S; ++j) l0 += static_cast<double>(ys[j]);
-                    l0 /= S;
-                    double lp = l0;
-                    for (int t = 0; t < T; ++t) {
-                        const double yt = static_cast<double>(ys[t]), s_t = ses[t * bd];
-                        const double lv = al * (yt / s_t) + (1.0 - al) * lp;
-                        if (t + S < T) ses[(t + S) * bd] = ga * (yt / lp) + (1.0 - ga) * s_t;
-                        lvs[t * bd] = lv;
-                        lp = lv;
-                    }
-                }
-            }
-            pdl_wait();
-            DBG_SPAN_MIN(st, s, 4);
-            SPAN_BEGIN(st, s, kSpanFinish);
-            if constexpr (!kEsRecompute<Real, SC>) {
-                if (mine) {
-                    a_raw = st.ps[lrow];
-                    g_raw = st.ps[N + lrow];
-                    if constexpr (SC > 0) {
-#pragma unroll
-                        for (int j = 0; j < SC; ++j) s0[j] = st.ps[(size_t)(2 + j) * N + lrow];
-                    }
-                }
-                // forward levels / seasonalities of the block's slots from K2's scan: whole
-                // 16-byte pieces of the [t][kcap] rows (kcap and sl0 are multiples of
-                // kEsSlotsPerBlock)
-                for (int e = tid; e < 2 * T * (bd / e16); e += kFinishThreads) {
-                    const int half = e / (T * (bd / e16)), r = e - half * T * (bd / e16);
-                    const int t = r / (bd / e16), ch = r - t * (bd / e16);
-                    cp_async16((half ? SE : LV) + t * bd + ch * e16, (half ? st.se : st.lv) + (size_t)t * kc + sl0 + ch * e16);
-                }
-            }
-            // ---- window adjoints: this block's windows are one contiguous range of the
-            // CSR-ordered contribution table, staged in chunks of kEsChunk rows; then one warp
-            // per slot adds the slot's windows in CSR order, lanes over the window's
-            // contiguous run of seasonality indices [a-I+1, a+O] ----
-            const int cb0 = pl.slot_win_off[k0];
-            const int blo = pl.slot_win_off[k0 + sl0], bhi = pl.slot_win_off[k0 + sl1];
-            const int nio = I + O;
-            const int wq = tid >> 5;
-            for (int sl = wq; sl < bd; sl += kFinishThreads / 32) {
-                for (int t = lane; t < lds; t += 32) SB[sl * lds + t] = 0;
-                for (int t = lane; t < ldl; t += 32) LB[sl * ldl + t] = 0;
-            }
-            FCLK();
-            for (int clo = blo; clo < bhi; clo += kEsChunk) {
-                const int chi = min(bhi, clo + kEsChunk);
-                const double* src = st.contrib + (size_t)(clo - cb0) * cwp;
-                const int nel = (chi - clo) * cwp;
-                for (int i = tid * d16; i < nel; i += kFinishThreads * d16) cp_async16(cbuf + i, src + i);
-                cp_async_wait_all();
-                __syncthreads();
+        if constexpr (sizeof(Real) == 8) {  // (fp32 ES blocks: es_block_fp32 above)
+            // ---------------- per-slot window-adjoint gather + reverse HW scan ---------------
+            const int k0 = pl.step_slot_off[s];
+            const int k = pl.step_slot_off[s + 1] - k0;
+            const int sl0 = blockIdx.x * kEsSlotsPerBlock;
+            const int sl1 = min(k, sl0 + kEsSlotsPerBlock);
+            if (sl0 < sl1 && st.attach) {  // uniform per block
+                const int N = st.N, S = SC > 0 ? SC : lay.S, T = lay.T, I = lay.I, O = lay.O, kc = st.kcap;
+                const int bd = kEsSlotsPerBlock, tp = row_pad<Real>(T), cwp = st.cwp;
+                const int slot = sl0 + tid;
+                const bool mine = tid < bd && slot < sl1;
+                const int lane = tid & 31;                                         // slot lane (bd == 32)
+                // window adjoints row-major per slot (odd strides: the per-slot reverse scan reads
+                // them conflict-free; the per-window warp scatter writes consecutive words)
+                // The ES adjoint runs in double in both precisions (see the K2 contributions): the
+                // level and seasonality paths of a window's adjoint cancel almost exactly, so their
+                // accumulation and the reverse recursion must not round on their own
+                const int ldl = T | 1, lds = (T + S) | 1;
+                double* LB = reinterpret_cast<double*>(smem_raw);                  // [bd][ldl] level adjoint
+                double* SB = LB + bd * ldl;                                        // [bd][lds] seasonality adjoint
+                Real* LV = reinterpret_cast<Real*>(SB + bd * lds);                 // [T][bd]   forward levels
+                Real* SE = LV + T * bd;                                            // [T][bd]   forward seasonalities
+                Real* YS = reinterpret_cast<Real*>(SE + T * bd);                   // [bd][tp]  observation rows
+                double* cbuf = reinterpret_cast<double*>(YS + bd * tp);            // [kEsChunk][cwp]
+                double* lb = LB + tid * ldl;
+                double* sb = SB + tid * lds;
+                Real* lvs = LV + tid;
+                Real* ses = SE + tid;
+                Real* ys = YS + tid * tp;
                 FCLK();
-                for (int sl = wq; sl0 + sl < sl1 && sl < bd; sl += kFinishThreads / 32) {
-                    const int w_lo = max(pl.slot_win_off[k0 + sl0 + sl], clo);
-                    const int w_hi = min(pl.slot_win_off[k0 + sl0 + sl + 1], chi);
-                    double* sbr = SB + sl * lds;
-                    for (int w = w_lo; w < w_hi; ++w) {
-                        const double* c = cbuf + (w - clo) * cwp;
-                        const int a = static_cast<int>(c[nio + 1]);
-                        for (int j = lane; j < nio; j += 32) sbr[a - I + 1 + j] += c[j];
-                        if (lane == 0) LB[sl * ldl + a] += c[nio];
-                        __syncwarp();
-                    }
-                }
-                __syncthreads();
-            }
-            if (blo == bhi) {  // no windows (cannot happen for a slot in the step; kept total)
-                cp_async_wait_all();
-                __syncthreads();
-            }
-            // ---- per-slot prologue (scanning threads): alpha, gamma, l[-1], the penalty ----
-            __shared__ double es_coef[3][kEsSlotsPerBlock];  // alpha, gamma, l[-1] per slot
-            using MD = Math<double>;
-            const double alpha = mine ? MD::logistic(static_cast<double>(a_raw)) : 0.0;
-            const double gamma = mine ? MD::logistic(static_cast<double>(g_raw)) : 0.0;
-            const double oma = 1.0 - alpha, omg = 1.0 - gamma;
-            if (mine) {
-                cp_async_wait_all();
-                FCLK();
-                if constexpr (!kEsRecompute<Real, SC>) {
-                    Real l0r = 0;
-                    for (int j = 0; j < S; ++j) l0r += ys[j];
-                    l0 = static_cast<double>(l0r / Real(S));
-                }
-                if (st.lvp > 0.0 && T >= 3) {
-                    // opt-in level-variability penalty (oracle/esrnn_oracle.c lvp_series): with
-                    // u_t = log l_t and e_t = u_t - 2 u_{t-1} + u_{t-2}, this slot adds
-                    // c * mean_t e_t^2, c = lambda * O * (its windows) / M; its adjoint enters the
-                    // LOG level adjoints directly (d/du_t; divided by l_t below)
-                    const int nw = pl.slot_win_off[k0 + slot + 1] - pl.slot_win_off[k0 + slot];
-                    const double cs = st.lvp * O * nw, c = cs / pl.step_M[s], inv = 1.0 / (T - 2);
-                    double um2 = ::log(static_cast<double>(lvs[0])), um1 = ::log(static_cast<double>(lvs[bd])), acc = 0.0;
-                    for (int t = 2; t < T; ++t) {
-                        const double u = ::log(static_cast<double>(lvs[t * bd]));
-                        const double e = u - 2.0 * um1 + um2;
-                        acc += e * e;
-                        const double q = c * 2.0 * inv * e;
-                        lb[t] += q;
-                        lb[t - 1] -= 2.0 * q;
-                        lb[t - 2] += q;
-                        um2 = um1;
-                        um1 = u;
-                    }
-                    pen = cs * acc * inv;  // x M: the loss-sum units of loss_part
-                }
-                es_coef[0][tid] = alpha;
-                es_coef[1][tid] = gamma;
-                es_coef[2][tid] = l0;
-            }
-            // fp32: the recursion's per-step coefficients, formed by the whole block (8 warps)
-            // so that the single scanning warp's serial loop is 4 dependent-free loads and 4
-            // DFMAs per step (inline, its two IEEE double divisions per step alone cost ~80
-            // cycles each).  With l' = l[t-1] (l[-1] = mean(y[0:S])):
-            //   lb[t] <- lb[t] / l_t,  sb[t] <- sb[t] / s_t      (log adjoints -> adjoints)
-            //   K1 = alpha y_t / s_t^2,  K2 = gamma y_t / l'^2,  CA = y_t / s_t - l',  CG = y_t / l' - s_t
-            // in the dead contribution staging region; double for the recomputed (S = 1)
-            // states, fp32 otherwise (coefficient rounding perturbs like the states' own).
-            using CR = std::conditional_t<kEsRecompute<Real, SC>, double, float>;
-            CR* K1 = reinterpret_cast<CR*>(cbuf);
-            CR* K2 = K1 + T * bd;
-            CR* CA = K2 + T * bd;
-            CR* CG = CA + T * bd;
-            if constexpr (sizeof(Real) == 4) {
-                __syncthreads();
-                const int nsl = sl1 - sl0;
-                for (int e = tid; e < T * bd; e += kFinishThreads) {
-                    const int t = e / bd, sl = e - t * bd;
-                    if (sl >= nsl) continue;
-                    const double y = static_cast<double>(YS[sl * tp + t]);
-                    const double lv = static_cast<double>(LV[e]), sv = static_cast<double>(SE[e]);
-                    const double lpv = t > 0 ? static_cast<double>(LV[e - bd]) : es_coef[2][sl];
-                    double rs, rl, ri;
-                    if constexpr (kEsRecompute<Real, SC>) {
-                        rs = 1.0 / sv, rl = 1.0 / lpv, ri = 1.0 / lv;
-                    } else {  // fp32 states: their correctly rounded fp32 reciprocals
-                        rs = __frcp_rn(static_cast<float>(sv));
-                        rl = __frcp_rn(static_cast<float>(lpv));
-                        ri = __frcp_rn(static_cast<float>(lv));
-                    }
-                    LB[sl * ldl + t] *= ri;
-                    SB[sl * lds + t] *= rs;
-                    const double yrs = y * rs, yrl = y * rl;
-                    K1[e] = static_cast<CR>(es_coef[0][sl] * yrs * rs);
-                    K2[e] = static_cast<CR>(es_coef[1][sl] * yrl * rl);
-                    CA[e] = static_cast<CR>(yrs - lpv);
-                    CG[e] = static_cast<CR>(yrl - sv);
-                }
-                __syncthreads();
-            }
-            FCLK();
-            if (mine) {
-                const int row = lrow;
-                double abar = 0, gbar = 0, omab = 0, omgb = 0;
-                double sfin[SC > 0 ? SC : 1];
-                using Mid = std::integral_constant<bool, false>;
-                using First = std::integral_constant<bool, true>;
-                if constexpr (sizeof(Real) == 4) {
-                    // reverse recursion (holt_winters.hpp:266-277 adjoints) on the coefficients:
-                    //   sb_t(final) = sb[t] + Sb omg - Lb K1_t,   Lb_{t-1} = lb[t-1] + Lb oma - Sb K2_t,
-                    //   abar - omab += Lb CA_t,   gbar - omgb += Sb CG_t
-                    // (Sb = final adjoint of s[t+S]).  Only loads in the loop (no smem stores for
-                    // the ring path), so they issue ahead of the one-DFMA-per-step chain.
-                    double lbn = lb[T - 1];
-                    auto step = [&](int t, double Sb, auto first) -> double {
-                        constexpr bool kFirst = decltype(first)::value;
-                        const double Lb = lbn;
-                        const int e = t * bd + tid;
-                        const double sbt = (sb[t] + Sb * omg) - Lb * static_cast<double>(K1[e]);
-                        if constexpr (!kFirst) lbn = (lb[t - 1] - Sb * static_cast<double>(K2[e])) + Lb * oma;
-                        abar += Lb * static_cast<double>(CA[e]);
-                        gbar += Sb * static_cast<double>(CG[e]);
-                        return sbt;
-                    };
-                    if constexpr (SC > 0) {
-                        double rg[SC];
+                // ---- stage the forward state with the whole block (every copy in flight at once) ----
+                const bool lane_ok = sl0 + lane < sl1;
+                const int lrow = lane_ok ? pl.slot_row[k0 + sl0 + lane] : 0;
+                constexpr int e16 = 16 / static_cast<int>(sizeof(Real));
+                constexpr int d16 = 2;  // doubles per 16-byte copy
+                // observation rows are epoch constants: staged before the dependency wait
+                if (lane_ok)
+                    for (int ch = tid >> 5; ch * e16 < tp; ch += kFinishThreads / 32)
+                        cp_async16(YS + lane * tp + ch * e16, st.vrm + (size_t)lrow * st.ldv + ch * e16);
+                Real a_raw = 0, g_raw = 0;
+                Real s0[SC > 0 ? SC : 1];  // exp(seas_raw) for the output's chain rule, loaded up front
+                double l0 = 0;             // l[-1] = mean(y[0:S]) (holt_winters.hpp:247-250)
+                pdl_wait();
+                DBG_SPAN_MIN(st, s, 4);
+                SPAN_BEGIN(st, s, kSpanFinish);
+                {
+                    if (mine) {
+                        a_raw = st.ps[lrow];
+                        g_raw = st.ps[N + lrow];
+                        if constexpr (SC > 0) {
 #pragma unroll
-                        for (int j = 0; j < SC; ++j) rg[j] = 0;  // s[T..T+S) receive no adjoint
-                        int base = ((T - 1) / SC) * SC;
-                        if (base > 0) {
-#pragma unroll
-                            for (int jj = SC - 1; jj >= 0; --jj)
-                                if (base + jj < T) rg[jj] = step(base + jj, rg[jj], Mid{});
-                            for (base -= SC; base > 0; base -= SC) {
-#pragma unroll
-                                for (int jj = SC - 1; jj >= 0; --jj) rg[jj] = step(base + jj, rg[jj], Mid{});
-                            }
+                            for (int j = 0; j < SC; ++j) s0[j] = st.ps[(size_t)(2 + j) * N + lrow];
                         }
-#pragma unroll
-                        for (int jj = SC - 1; jj >= 1; --jj)
-                            if (jj < T) rg[jj] = step(jj, rg[jj], Mid{});
-                        rg[0] = step(0, rg[0], First{});
-#pragma unroll
-                        for (int j = 0; j < SC; ++j) sfin[j] = rg[j];
-                    } else {
-                        for (int t = T - 1; t >= 1; --t) sb[t] = step(t, sb[t + S], Mid{});
-                        sb[0] = step(0, sb[S], First{});
                     }
-                } else {
+                    // forward levels / seasonalities of the block's slots from K2's scan: whole
+                    // 16-byte pieces of the [t][kcap] rows (kcap and sl0 are multiples of
+                    // kEsSlotsPerBlock)
+                    for (int e = tid; e < 2 * T * (bd / e16); e += kFinishThreads) {
+                        const int half = e / (T * (bd / e16)), r = e - half * T * (bd / e16);
+                        const int t = r / (bd / e16), ch = r - t * (bd / e16);
+                        cp_async16((half ? SE : LV) + t * bd + ch * e16, (half ? st.se : st.lv) + (size_t)t * kc + sl0 + ch * e16);
+                    }
+                }
+                // ---- window adjoints: this block's windows are one contiguous range of the
+                // CSR-ordered contribution table, staged in chunks of kEsChunk rows; then one warp
+                // per slot adds the slot's windows in CSR order, lanes over the window's
+                // contiguous run of seasonality indices [a-I+1, a+O] ----
+                const int cb0 = pl.slot_win_off[k0];
+                const int blo = pl.slot_win_off[k0 + sl0], bhi = pl.slot_win_off[k0 + sl1];
+                const int nio = I + O;
+                const int wq = tid >> 5;
+                for (int sl = wq; sl < bd; sl += kFinishThreads / 32) {
+                    for (int t = lane; t < lds; t += 32) SB[sl * lds + t] = 0;
+                    for (int t = lane; t < ldl; t += 32) LB[sl * ldl + t] = 0;
+                }
+                FCLK();
+                for (int clo = blo; clo < bhi; clo += kEsChunk) {
+                    const int chi = min(bhi, clo + kEsChunk);
+                    const double* src = st.contrib + (size_t)(clo - cb0) * cwp;
+                    const int nel = (chi - clo) * cwp;
+                    for (int i = tid * d16; i < nel; i += kFinishThreads * d16) cp_async16(cbuf + i, src + i);
+                    cp_async_wait_all();
+                    __syncthreads();
+                    FCLK();
+                    for (int sl = wq; sl0 + sl < sl1 && sl < bd; sl += kFinishThreads / 32) {
+                        const int w_lo = max(pl.slot_win_off[k0 + sl0 + sl], clo);
+                        const int w_hi = min(pl.slot_win_off[k0 + sl0 + sl + 1], chi);
+                        double* sbr = SB + sl * lds;
+                        for (int w = w_lo; w < w_hi; ++w) {
+                            const double* c = cbuf + (w - clo) * cwp;
+                            const int a = static_cast<int>(c[nio + 1]);
+                            for (int j = lane; j < nio; j += 32) sbr[a - I + 1 + j] += c[j];
+                            if (lane == 0) LB[sl * ldl + a] += c[nio];
+                            __syncwarp();
+                        }
+                    }
+                    __syncthreads();
+                }
+                if (blo == bhi) {  // no windows (cannot happen for a slot in the step; kept total)
+                    cp_async_wait_all();
+                    __syncthreads();
+                }
+                // ---- per-slot prologue (scanning threads): alpha, gamma, l[-1], the penalty ----
+                using MD = Math<double>;
+                const double alpha = mine ? MD::logistic(static_cast<double>(a_raw)) : 0.0;
+                const double gamma = mine ? MD::logistic(static_cast<double>(g_raw)) : 0.0;
+                const double oma = 1.0 - alpha, omg = 1.0 - gamma;
+                if (mine) {
+                    cp_async_wait_all();
+                    FCLK();
+                    {
+                        Real l0r = 0;
+                        for (int j = 0; j < S; ++j) l0r += ys[j];
+                        l0 = static_cast<double>(l0r / Real(S));
+                    }
+                    if (st.lvp > 0.0 && T >= 3) {
+                        // opt-in level-variability penalty (oracle/esrnn_oracle.c lvp_series): with
+                        // u_t = log l_t and e_t = u_t - 2 u_{t-1} + u_{t-2}, this slot adds
+                        // c * mean_t e_t^2, c = lambda * O * (its windows) / M; its adjoint enters the
+                        // LOG level adjoints directly (d/du_t; divided by l_t below)
+                        const int nw = pl.slot_win_off[k0 + slot + 1] - pl.slot_win_off[k0 + slot];
+                        const double cs = st.lvp * O * nw, c = cs / pl.step_M[s], inv = 1.0 / (T - 2);
+                        double um2 = ::log(static_cast<double>(lvs[0])), um1 = ::log(static_cast<double>(lvs[bd])), acc = 0.0;
+                        for (int t = 2; t < T; ++t) {
+                            const double u = ::log(static_cast<double>(lvs[t * bd]));
+                            const double e = u - 2.0 * um1 + um2;
+                            acc += e * e;
+                            const double q = c * 2.0 * inv * e;
+                            lb[t] += q;
+                            lb[t - 1] -= 2.0 * q;
+                            lb[t - 2] += q;
+                            um2 = um1;
+                            um1 = u;
+                        }
+                        pen = cs * acc * inv;  // x M: the loss-sum units of loss_part
+                    }
+                }
+                FCLK();
+                if (mine) {
+                    const int row = lrow;
+                    double abar = 0, gbar = 0, omab = 0, omgb = 0;
+                    double sfin[SC > 0 ? SC : 1];
+                    using Mid = std::integral_constant<bool, false>;
+                    using First = std::integral_constant<bool, true>;
                     // fp64: the reference's arithmetic (IEEE divisions), linearised at K2's states
                     double lbn = lb[T - 1] / lvs[(T - 1) * bd];  // running adjoint of l[t]
                     // one reverse step (t > 0 unless FIRST): Sb = final adjoint of s[t+S],
@@ -727,40 +604,40 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
                         for (int t = T - 1; t >= 1; --t) sb[t] = step(t, sb[t + S], Mid{});
                         sb[0] = step(0, sb[S], First{});
                     }
-                }
-                FCLK();
-                abar -= omab;
-                gbar -= omgb;
-                Real* o = st.psg + (size_t)slot * (2 + S);
-                const Real ga = static_cast<Real>(abar * alpha * oma);
-                const Real gg = static_cast<Real>(gbar * gamma * omg);
-                o[0] = ga;
-                o[1] = gg;
-                sq += static_cast<double>(ga) * ga + static_cast<double>(gg) * gg;
-                if constexpr (SC > 0) {
+                    FCLK();
+                    abar -= omab;
+                    gbar -= omgb;
+                    Real* o = st.psg + (size_t)slot * (2 + S);
+                    const Real ga = static_cast<Real>(abar * alpha * oma);
+                    const Real gg = static_cast<Real>(gbar * gamma * omg);
+                    o[0] = ga;
+                    o[1] = gg;
+                    sq += static_cast<double>(ga) * ga + static_cast<double>(gg) * gg;
+                    if constexpr (SC > 0) {
 #pragma unroll
-                    for (int j = 0; j < SC; ++j) {
-                        const Real g = static_cast<Real>(sfin[j] * MD::exp(static_cast<double>(s0[j])));
-                        o[2 + j] = g;
-                        sq += static_cast<double>(g) * g;
-                    }
-                } else {
-                    for (int j = 0; j < S; ++j) {
-                        const Real g = static_cast<Real>(sb[j] * MD::exp(static_cast<double>(st.ps[(2 + j) * N + row])));
-                        o[2 + j] = g;
-                        sq += static_cast<double>(g) * g;
+                        for (int j = 0; j < SC; ++j) {
+                            const Real g = static_cast<Real>(sfin[j] * MD::exp(static_cast<double>(s0[j])));
+                            o[2 + j] = g;
+                            sq += static_cast<double>(g) * g;
+                        }
+                    } else {
+                        for (int j = 0; j < S; ++j) {
+                            const Real g = static_cast<Real>(sb[j] * MD::exp(static_cast<double>(st.ps[(2 + j) * N + row])));
+                            o[2 + j] = g;
+                            sq += static_cast<double>(g) * g;
+                        }
                     }
                 }
+            } else {
+                pdl_wait();
+                SPAN_BEGIN(st, s, kSpanFinish);
             }
-        } else {
-            pdl_wait();
-            SPAN_BEGIN(st, s, kSpanFinish);
-        }
-        const double tot = block_sum(sq, red);
-        if (tid == 0) st.es_sq_part[blockIdx.x] = tot;
-        if (st.lvp > 0.0) {
-            const double pt = block_sum(pen, red);
-            if (tid == 0) st.es_pen_part[blockIdx.x] = pt;
+            const double tot = block_sum(sq, red);
+            if (tid == 0) st.es_sq_part[blockIdx.x] = tot;
+            if (st.lvp > 0.0) {
+                const double pt = block_sum(pen, red);
+                if (tid == 0) st.es_pen_part[blockIdx.x] = pt;
+            }
         }
     } else if (UMMA && sizeof(Real) == 4) {
         pdl_wait();
