@@ -33,3 +33,9 @@ tr.set_train_state(ts)
 x = np.random.default_rng(0).uniform(-1, 1, (3, 4, prof.input_window + 6))
 out, wb, xb = tr.forward_stack(x, np.ones((4, prof.horizon)))
 print("stack", float(out.sum()), float(xb.sum()))
+# round 2: the inference forward_stack kernel (shared-memory-resident layer weights) and, with
+# a penalty, the penalised ES path
+print("stack-fast", float(tr.forward_stack(x).sum()))
+tp = Trainer((vals, cats), prof, TrainConfig(seed=7, precision=prec, batch_size=bs, max_batch_size=max(bs, 2048),
+                                             level_variability_penalty=2.0), api=eng)
+print("penalised epoch", tp.train_epoch())
