@@ -1920,49 +1920,82 @@ void forward_stack_impl(Eng* e, int Tq, int B, const double* inputs, double* out
     x.alloc(r * static_cast<size_t>(Tq) * B * e->in0);
     upload_real(e, x.p, inputs, static_cast<size_t>(Tq) * B * e->in0);
     dout.alloc(static_cast<size_t>(B) * e->O);
-    // inference (no adjoint): the shared-memory-resident kernel when a layer's weights, the
-    // (h, c) rings and the gate tile fit (seqstack.cuh k_seq_fwd_fast); the adjoint path keeps
-    // every step's activations for the reverse sweep (k_seq_forward / k_seq_backward)
+    // the shared-memory-resident kernels (seqstack.cuh k_seq_fwd_fast / k_seq_bwd_fast) when a
+    // layer's weights, the (h, c) rings and the step tiles fit; else the stepwise kernels that
+    // keep every activation in a per-4-row scratch (k_seq_forward / k_seq_backward)
     int dmax = 1;
     for (int l = 0; l < e->L; ++l) dmax = std::max(dmax, sl.dil[l]);
     const size_t G = 4 * static_cast<size_t>(e->H);
     const size_t fast_smem = r * ((static_cast<size_t>(sl.in_max) + e->H + 1) * G + 2 * static_cast<size_t>(sl.in_max) * kSeqFR +
                                   2 * static_cast<size_t>(dmax) * e->H * kSeqFR + kSeqFR * G);
-    const bool fast = !out_bar && fast_smem <= static_cast<size_t>(g_smem_optin) &&
-                      kSeqSplit * ((G + 31) / 32 * 32) <= 1024 &&
-                      std::getenv("ESRNN_SEQ_NAIVE") == nullptr;
+    const size_t bwd_smem = r * ((static_cast<size_t>(sl.in_max) + e->H) * G + kSeqFR * G +
+                                 2 * static_cast<size_t>(dmax) * e->H * kSeqFR +
+                                 (static_cast<size_t>(sl.in_max) + e->H) * kSeqFR);
+    const bool naive_env = std::getenv("ESRNN_SEQ_NAIVE") != nullptr;
+    const bool fast_fwd = fast_smem <= static_cast<size_t>(g_smem_optin) && kSeqSplit * ((G + 31) / 32 * 32) <= 1024 &&
+                          !naive_env;
+    const bool fast_bwd = fast_fwd && sizeof(Real) == 4 && bwd_smem <= static_cast<size_t>(g_smem_optin) &&
+                          (static_cast<size_t>(sl.in_max) + e->H + 1) * G <= static_cast<size_t>(kSeqBwdAcc) * kSeqBwdThreads;
+    const bool fast = out_bar ? fast_bwd : fast_fwd;
     const int nfast = (B + kSeqFR - 1) / kSeqFR;
     if (!fast) scratch.alloc(r * static_cast<size_t>(nblk) * SeqScratch<Real>::size(sl));
+    DBuf<unsigned char> dcurbuf;
     if (fast) {
-        scratch.alloc(r * static_cast<size_t>(nfast) * 3 * Tq * kSeqFR * e->H);
-        CUDA_OK(cudaFuncSetAttribute(k_seq_fwd_fast<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(fast_smem)));
+        if (out_bar) {
+            scratch.alloc(r * static_cast<size_t>(nfast) * SeqSave<Real>::per_cta(sl));
+            dcurbuf.alloc(r * static_cast<size_t>(nfast) * e->L * Tq * kSeqFR * e->H);
+            CUDA_OK(cudaFuncSetAttribute(k_seq_fwd_fast<Real, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(fast_smem)));
+            CUDA_OK(cudaFuncSetAttribute(k_seq_bwd_fast<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(bwd_smem)));
+        } else {
+            scratch.alloc(r * static_cast<size_t>(nfast) * 3 * Tq * kSeqFR * e->H);
+            CUDA_OK(cudaFuncSetAttribute(k_seq_fwd_fast<Real, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(fast_smem)));
+        }
     }
     CUDA_OK(cudaEventRecord(e->ev0, e->stream));
-    if (fast) {
-        const int nt = kSeqSplit * static_cast<int>((std::max<size_t>(G, 32) + 31) / 32 * 32);
-        k_seq_fwd_fast<Real><<<nfast, nt, fast_smem, e->stream>>>(sl, reinterpret_cast<const Real*>(w.p),
-                                                                  reinterpret_cast<const Real*>(x.p),
-                                                                  reinterpret_cast<Real*>(scratch.p), dout.p);
+    const int nt = kSeqSplit * static_cast<int>((std::max<size_t>(G, 32) + 31) / 32 * 32);
+    if (fast && !out_bar) {
+        k_seq_fwd_fast<Real, false><<<nfast, nt, fast_smem, e->stream>>>(
+            sl, reinterpret_cast<const Real*>(w.p), reinterpret_cast<const Real*>(x.p), reinterpret_cast<Real*>(scratch.p),
+            dout.p);
+        e->launches += 1;
+    } else if (fast) {
+        k_seq_fwd_fast<Real, true><<<nfast, nt, fast_smem, e->stream>>>(
+            sl, reinterpret_cast<const Real*>(w.p), reinterpret_cast<const Real*>(x.p), reinterpret_cast<Real*>(scratch.p),
+            dout.p);
+        ob.alloc(r * static_cast<size_t>(B) * e->O);
+        upload_real(e, ob.p, out_bar, static_cast<size_t>(B) * e->O);
+        wpart.alloc(r * static_cast<size_t>(nfast) * e->P);
+        if (xbar) xb.alloc(r * static_cast<size_t>(Tq) * B * e->in0);
+        k_seq_bwd_fast<Real><<<nfast, kSeqBwdThreads, bwd_smem, e->stream>>>(
+            sl, reinterpret_cast<const Real*>(w.p), reinterpret_cast<const Real*>(x.p), reinterpret_cast<Real*>(scratch.p),
+            reinterpret_cast<Real*>(dcurbuf.p), reinterpret_cast<const Real*>(ob.p), reinterpret_cast<Real*>(wpart.p),
+            xbar ? reinterpret_cast<Real*>(xb.p) : nullptr);
+        dwbar.alloc(e->P);
+        k_seq_reduce<Real><<<static_cast<int>((e->P + 255) / 256), 256, 0, e->stream>>>(
+            reinterpret_cast<const Real*>(wpart.p), nfast, e->P, dwbar.p);
+        e->launches += 3;
     } else {
         k_seq_forward<Real><<<nblk, kSeqThreads, 0, e->stream>>>(sl, reinterpret_cast<const Real*>(w.p),
                                                                   reinterpret_cast<const Real*>(x.p),
                                                                   reinterpret_cast<Real*>(scratch.p), dout.p);
-    }
-    e->launches += 1;
-    if (out_bar) {
-        ob.alloc(r * static_cast<size_t>(B) * e->O);
-        upload_real(e, ob.p, out_bar, static_cast<size_t>(B) * e->O);
-        wpart.alloc(r * static_cast<size_t>(nblk) * e->P);
-        if (xbar) xb.alloc(r * static_cast<size_t>(Tq) * B * e->in0);
-        k_seq_backward<Real><<<nblk, kSeqThreads, 0, e->stream>>>(
-            sl, reinterpret_cast<const Real*>(w.p), reinterpret_cast<const Real*>(x.p),
-            reinterpret_cast<Real*>(scratch.p), reinterpret_cast<const Real*>(ob.p), reinterpret_cast<Real*>(wpart.p),
-            xbar ? reinterpret_cast<Real*>(xb.p) : nullptr);
-        dwbar.alloc(e->P);
-        k_seq_reduce<Real><<<static_cast<int>((e->P + 255) / 256), 256, 0, e->stream>>>(
-            reinterpret_cast<const Real*>(wpart.p), nblk, e->P, dwbar.p);
-        e->launches += 2;
+        e->launches += 1;
+        if (out_bar) {
+            ob.alloc(r * static_cast<size_t>(B) * e->O);
+            upload_real(e, ob.p, out_bar, static_cast<size_t>(B) * e->O);
+            wpart.alloc(r * static_cast<size_t>(nblk) * e->P);
+            if (xbar) xb.alloc(r * static_cast<size_t>(Tq) * B * e->in0);
+            k_seq_backward<Real><<<nblk, kSeqThreads, 0, e->stream>>>(
+                sl, reinterpret_cast<const Real*>(w.p), reinterpret_cast<const Real*>(x.p),
+                reinterpret_cast<Real*>(scratch.p), reinterpret_cast<const Real*>(ob.p), reinterpret_cast<Real*>(wpart.p),
+                xbar ? reinterpret_cast<Real*>(xb.p) : nullptr);
+            dwbar.alloc(e->P);
+            k_seq_reduce<Real><<<static_cast<int>((e->P + 255) / 256), 256, 0, e->stream>>>(
+                reinterpret_cast<const Real*>(wpart.p), nblk, e->P, dwbar.p);
+            e->launches += 2;
+        }
     }
     CUDA_OK(cudaEventRecord(e->ev1, e->stream));
     CUDA_OK(cudaGetLastError());

@@ -281,7 +281,29 @@ __global__ void __launch_bounds__(kSeqThreads) k_seq_backward(SeqLayout s, const
 constexpr int kSeqFR = 16;
 constexpr int kSeqSplit = 4;  // threads per gate column in the gate phase
 
+// Saved activations of the fast path for its adjoint (k_seq_bwd_fast), per CTA of kSeqFR rows:
+// gates [L][T][R][4H] (post-activation i f g o), c / h (the cell state and the recurrent
+// output) / cur (the layer output incl. the block skip) [L][T][R][H]
 template <typename Real>
+struct SeqSave {
+    Real *gates, *cst, *hraw, *cur;
+    __host__ __device__ static long long per_cta(const SeqLayout& s) {
+        return static_cast<long long>(s.L) * s.T * kSeqFR * (4LL * s.H + 3LL * s.H);
+    }
+    __device__ static SeqSave at(Real* base, const SeqLayout& s) {
+        const long long LTR = static_cast<long long>(s.L) * s.T * kSeqFR;
+        SeqSave v;
+        Real* p = base + static_cast<long long>(blockIdx.x) * per_cta(s);
+        v.gates = p, p += LTR * 4 * s.H;
+        v.cst = p, p += LTR * s.H;
+        v.hraw = p, p += LTR * s.H;
+        v.cur = p;
+        return v;
+    }
+};
+
+// SAVE: also keep every step's activations (SeqSave in seqbuf) for the adjoint kernel
+template <typename Real, bool SAVE>
 __global__ void __launch_bounds__(1024) k_seq_fwd_fast(SeqLayout s, const Real* __restrict__ W,
                                                        const Real* __restrict__ X, Real* __restrict__ seqbuf,
                                                        double* out) {
@@ -299,13 +321,17 @@ __global__ void __launch_bounds__(1024) k_seq_fwd_fast(SeqLayout s, const Real* 
     Real* cr = hr + static_cast<size_t>(dmax) * H * R;
     Real* gs = cr + static_cast<size_t>(dmax) * H * R;
     // per-CTA sequence buffers: two layer outputs in flight + the current block's input
+    // (SAVE: every layer's output kept, the block input read in place)
     const size_t TRH = static_cast<size_t>(T) * R * H;
-    Real* cur0 = seqbuf + static_cast<size_t>(blockIdx.x) * 3 * TRH;  // layer outputs l even / odd
-    Real* bin = cur0 + 2 * TRH;
+    SeqSave<Real> sv{};
+    if constexpr (SAVE) sv = SeqSave<Real>::at(seqbuf, s);
+    Real* cur0 = SAVE ? sv.cur : seqbuf + static_cast<size_t>(blockIdx.x) * 3 * TRH;  // layer outputs
+    Real* bin = SAVE ? nullptr : cur0 + 2 * TRH;
     for (int l = 0; l < s.L; ++l) {
         const int K = s.layer_in[l], d = s.dil[l];
-        const Real* Xin = l == 0 ? nullptr : cur0 + ((l - 1) & 1) * TRH;
-        Real* Y = cur0 + (l & 1) * TRH;
+        const Real* Xin = l == 0 ? nullptr : cur0 + (SAVE ? (l - 1) : ((l - 1) & 1)) * TRH;
+        Real* Y = cur0 + (SAVE ? l : (l & 1)) * TRH;
+        if constexpr (SAVE) bin = s.res_src[l] >= 0 ? cur0 + s.res_src[l] * TRH : nullptr;
         __syncthreads();  // previous layer done with the weights / its output complete
         const Real* Wi = W + s.w_in[l];
         const Real* Wr = W + s.w_rec[l];
@@ -369,7 +395,10 @@ __global__ void __launch_bounds__(1024) k_seq_fwd_fast(SeqLayout s, const Real* 
 #pragma unroll
                 for (int r = 0; r < RH; ++r) {
                     const Real v = (t >= d ? acc[r] + a2[r] : acc[r]) + b;
-                    gs[(half * RH + r) * G + col] = is_g ? M::tanh(v) : M::logistic(v);
+                    const Real a = is_g ? M::tanh(v) : M::logistic(v);
+                    gs[(half * RH + r) * G + col] = a;
+                    if constexpr (SAVE)
+                        if (half * RH + r < nr) sv.gates[((static_cast<size_t>(l) * T + t) * R + half * RH + r) * G + col] = a;
                 }
             }
             __syncthreads();
@@ -385,6 +414,10 @@ __global__ void __launch_bounds__(1024) k_seq_fwd_fast(SeqLayout s, const Real* 
                 *cpos = cv;
                 hr[(static_cast<size_t>(slot) * H + j) * R + r] = h;
                 const size_t q = (static_cast<size_t>(t) * R + r) * H + j;
+                if constexpr (SAVE) {
+                    sv.cst[l * TRH + q] = cv;
+                    sv.hraw[l * TRH + q] = h;
+                }
                 if (s.res_src[l] >= 0) Y[q] = h + bin[q];
                 else Y[q] = h;
             }
@@ -393,14 +426,16 @@ __global__ void __launch_bounds__(1024) k_seq_fwd_fast(SeqLayout s, const Real* 
         }
         // the block skip of a later layer m adds the output of layer res_src[m] (the previous
         // block's last layer, i.e. the block input): keep it when this layer is that source
-        bool is_src = false;
-        for (int m = l + 1; m < s.L; ++m) is_src |= s.res_src[m] == l;
-        if (is_src)
-            for (size_t e = tid; e < static_cast<size_t>(T) * R * H; e += NT) bin[e] = Y[e];
+        if constexpr (!SAVE) {
+            bool is_src = false;
+            for (int m = l + 1; m < s.L; ++m) is_src |= s.res_src[m] == l;
+            if (is_src)
+                for (size_t e = tid; e < static_cast<size_t>(T) * R * H; e += NT) bin[e] = Y[e];
+        }
     }
     __syncthreads();
     // head on the last step (network.hpp:207-209)
-    const Real* last = cur0 + ((s.L - 1) & 1) * TRH + static_cast<size_t>(T - 1) * R * H;
+    const Real* last = cur0 + (SAVE ? s.L - 1 : ((s.L - 1) & 1)) * TRH + static_cast<size_t>(T - 1) * R * H;
     Real* z = gs;  // [R][H]
     for (int e = tid; e < nr * H; e += NT) {
         const int r = e / H, j = e - r * H;
@@ -414,6 +449,207 @@ __global__ void __launch_bounds__(1024) k_seq_fwd_fast(SeqLayout s, const Real* 
         Real acc = 0;
         for (int k = 0; k < H; ++k) acc += z[r * H + k] * W[s.out_w + static_cast<long long>(k) * s.O + o];
         out[static_cast<long long>(b0 + r) * s.O + o] = static_cast<double>(acc + W[s.out_b + o]);
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Adjoint of the fast forward (k_seq_fwd_fast<SAVE>): k_seq_bwd_fast, a CTA per kSeqFR rows,
+// the reverse sweep of k_seq_backward's graph with a layer's W_in / W_rec in shared memory.
+// Per step (reverse): cell adjoints (thread per (row, unit)) into the pre-activation adjoints
+// dpre [R][4H] and the (h, c) recurrent-adjoint rings; then, per thread, the input and
+// recurrent adjoints (thread per (input feature, row quarter): a dot over 4H with the
+// feature's weight row) and its share of the weight gradients, accumulated in registers over
+// the layer's steps (thread-owned (feature, gate column) entries; reverse-step, row-ascending
+// order as k_seq_backward).  dcur [L][T][R][H] (the adjoint of every layer output) lives in a
+// CTA-private global buffer; per-CTA weight-gradient partials are reduced by k_seq_reduce.
+constexpr int kSeqBwdThreads = 1024;
+constexpr int kSeqBwdAcc = 24;  // weight-gradient entries per thread ((in_max + H + 1) * 4H <= 24 * 1024)
+
+template <typename Real>
+__global__ void __launch_bounds__(kSeqBwdThreads) k_seq_bwd_fast(SeqLayout s, const Real* __restrict__ W,
+                                                                  const Real* __restrict__ X, Real* __restrict__ seqbuf,
+                                                                  Real* __restrict__ dcurbuf,
+                                                                  const Real* __restrict__ obar, Real* __restrict__ wpart,
+                                                                  Real* __restrict__ xbar) {
+    using M = Math<Real>;
+    constexpr int R = kSeqFR;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int b0 = blockIdx.x * R, nr = min(R, s.B - b0);
+    const int tid = threadIdx.x, NT = blockDim.x, H = s.H, G = 4 * H, T = s.T, O = s.O;
+    int dmax = 1;
+    for (int l = 0; l < s.L; ++l) dmax = max(dmax, s.dil[l]);
+    // shared: Wi [in_max][G] | Wr [H][G] | dpre [R][G] | dh, dc rings [dmax][H][R] | xs, hs [in_max][R], [H][R]
+    Real* Wi = reinterpret_cast<Real*>(smem_raw);
+    Real* Wr = Wi + static_cast<size_t>(s.in_max) * G;
+    Real* dp = Wr + static_cast<size_t>(H) * G;
+    Real* dhr = dp + static_cast<size_t>(R) * G;
+    Real* dcr = dhr + static_cast<size_t>(dmax) * H * R;
+    Real* xs = dcr + static_cast<size_t>(dmax) * H * R;
+    Real* hs = xs + static_cast<size_t>(s.in_max) * R;
+    const SeqSave<Real> sv = SeqSave<Real>::at(seqbuf, s);
+    const size_t TRH = static_cast<size_t>(T) * R * H;
+    Real* dcur = dcurbuf + static_cast<size_t>(blockIdx.x) * s.L * TRH;
+    Real* wp = wpart + static_cast<long long>(blockIdx.x) * s.P;
+    for (size_t e = tid; e < static_cast<size_t>(s.L) * TRH; e += NT) dcur[e] = Real(0);
+    // ---- head: out = z out_w + out_b, z = tanh(last nl_w + nl_b) (z recomputed) ----
+    const Real* last = sv.cur + static_cast<size_t>(s.L - 1) * TRH + static_cast<size_t>(T - 1) * R * H;
+    Real* z = dp;            // [R][H]
+    Real* dzp = dp + R * H;  // [R][H]
+    for (int e = tid; e < nr * H; e += NT) {
+        const int r = e / H, j = e - r * H;
+        Real acc = 0;
+        for (int k = 0; k < H; ++k) acc += last[r * H + k] * W[s.nl_w + static_cast<long long>(k) * H + j];
+        z[r * H + j] = M::tanh(acc + W[s.nl_b + j]);
+    }
+    __syncthreads();
+    const Real* ob = obar + static_cast<long long>(b0) * O;
+    for (int e = tid; e < H * O + O; e += NT) {
+        Real acc = 0;
+        if (e < H * O) {
+            const int k = e / O, o = e - k * O;
+            for (int r = 0; r < nr; ++r) acc += z[r * H + k] * ob[r * O + o];
+            wp[s.out_w + e] = acc;
+        } else {
+            for (int r = 0; r < nr; ++r) acc += ob[r * O + (e - H * O)];
+            wp[s.out_b + (e - H * O)] = acc;
+        }
+    }
+    for (int e = tid; e < nr * H; e += NT) {
+        const int r = e / H, k = e - r * H;
+        Real acc = 0;
+        for (int o = 0; o < O; ++o) acc += ob[r * O + o] * W[s.out_w + static_cast<long long>(k) * O + o];
+        const Real zz = z[r * H + k];
+        dzp[r * H + k] = acc * (Real(1) - zz * zz);
+    }
+    __syncthreads();
+    for (int e = tid; e < H * H + H; e += NT) {
+        Real acc = 0;
+        if (e < H * H) {
+            const int k = e / H, j = e - k * H;
+            for (int r = 0; r < nr; ++r) acc += last[r * H + k] * dzp[r * H + j];
+            wp[s.nl_w + e] = acc;
+        } else {
+            for (int r = 0; r < nr; ++r) acc += dzp[r * H + (e - H * H)];
+            wp[s.nl_b + (e - H * H)] = acc;
+        }
+    }
+    Real* dlast = dcur + static_cast<size_t>(s.L - 1) * TRH + static_cast<size_t>(T - 1) * R * H;
+    for (int e = tid; e < nr * H; e += NT) {
+        const int r = e / H, k = e - r * H;
+        Real acc = 0;
+        for (int j = 0; j < H; ++j) acc += dzp[r * H + j] * W[s.nl_w + static_cast<long long>(k) * H + j];
+        dlast[r * H + k] = acc;
+    }
+    __syncthreads();
+    // ---- layers in reverse ----
+    for (int l = s.L - 1; l >= 0; --l) {
+        const int K = s.layer_in[l], d = s.dil[l];
+        Real* dcl = dcur + static_cast<size_t>(l) * TRH;
+        // block skip: its source receives the layer output's adjoint too
+        if (s.res_src[l] >= 0) {
+            Real* dsrc = dcur + static_cast<size_t>(s.res_src[l]) * TRH;
+            for (size_t e = tid; e < TRH; e += NT) dsrc[e] += dcl[e];
+        }
+        for (int e = tid; e < K * G; e += NT) Wi[e] = W[s.w_in[l] + e];
+        for (int e = tid; e < H * G; e += NT) Wr[e] = W[s.w_rec[l] + e];
+        for (int e = tid; e < 2 * d * H * R; e += NT) dhr[e] = Real(0);  // dh and dc rings are contiguous
+        for (int e = tid; e < (s.in_max + H) * R; e += NT) xs[e] = Real(0);
+        // weight-gradient accumulators: entry q = tid + i * NT of the layer's (K + H + 1) x G block
+        // (rows: input features, recurrent features, bias)
+        const int nq = (K + H + 1) * G;
+        Real acc[kSeqBwdAcc];
+#pragma unroll
+        for (int i = 0; i < kSeqBwdAcc; ++i) acc[i] = 0;
+        const Real* Xin = l == 0 ? nullptr : sv.cur + static_cast<size_t>(l - 1) * TRH;
+        __syncthreads();
+        for (int t = T - 1; t >= 0; --t) {
+            const int slot = t % d;
+            // ---- phase 1: cell adjoints (Mul / Tanh / Logistic / Add adjoints of lstm_cell) and
+            // the step's layer input / recurrent input staged for the weight gradients ----
+            for (int e = tid; e < nr * H; e += NT) {
+                const int r = e / H, j = e - r * H;
+                const size_t q = (static_cast<size_t>(l) * T + t) * R + r;
+                const Real* gt = sv.gates + q * G;
+                const Real i = gt[j], f = gt[H + j], g = gt[2 * H + j], o = gt[3 * H + j];
+                const Real tc = M::tanh(sv.cst[q * H + j]);
+                Real* dhp = dhr + (static_cast<size_t>(slot) * H + j) * R + r;
+                Real* dcp = dcr + (static_cast<size_t>(slot) * H + j) * R + r;
+                const Real dh = dcl[(static_cast<size_t>(t) * R + r) * H + j] + *dhp;
+                const Real dc = *dcp + dh * o * (Real(1) - tc * tc);
+                Real df = 0;
+                if (t >= d) {
+                    df = dc * sv.cst[(q - static_cast<size_t>(d) * R) * H + j];
+                    *dcp = dc * f;  // the adjoint of c_{t-d} (read at step t - d, same slot)
+                } else {
+                    *dcp = Real(0);
+                }
+                Real* dr = dp + r * G;
+                dr[j] = dc * g * i * (Real(1) - i);
+                dr[H + j] = df * f * (Real(1) - f);
+                dr[2 * H + j] = dc * i * (Real(1) - g * g);
+                dr[3 * H + j] = dh * tc * o * (Real(1) - o);
+            }
+            for (int e = tid; e < K * nr; e += NT) {
+                const int k = e / nr, r = e - k * nr;
+                xs[k * R + r] = l == 0 ? X[(static_cast<size_t>(t) * s.B + b0 + r) * s.in0 + k]
+                                       : Xin[(static_cast<size_t>(t) * R + r) * H + k];
+            }
+            for (int e = tid; e < H * nr; e += NT) {
+                const int k = e / nr, r = e - k * nr;
+                hs[k * R + r] = t >= d ? sv.hraw[(static_cast<size_t>(l) * T + t - d) * R * H + r * H + k] : Real(0);
+            }
+            __syncthreads();
+            // ---- phase 2: input adjoint of step t, recurrent adjoint of h_{t-d}, weight grads ----
+            const int kmax = K > H ? K : H;
+            for (int e = tid; e < kmax * nr; e += NT) {
+                const int k = e / nr, r = e - k * nr;
+                const Real* dr = dp + r * G;
+                if (k < K) {
+                    Real a = 0;
+                    const Real* wrow = Wi + k * G;
+                    for (int j = 0; j < G; ++j) a += dr[j] * wrow[j];
+                    if (l > 0) dcur[static_cast<size_t>(l - 1) * TRH + (static_cast<size_t>(t) * R + r) * H + k] += a;
+                    else if (xbar) xbar[(static_cast<size_t>(t) * s.B + b0 + r) * s.in0 + k] = a;
+                }
+                if (k < H) {
+                    Real a = 0;
+                    if (t >= d) {
+                        const Real* wrow = Wr + k * G;
+                        for (int j = 0; j < G; ++j) a += dr[j] * wrow[j];
+                    }
+                    dhr[(static_cast<size_t>(slot) * H + k) * R + r] = a;  // for step t - d (same slot)
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < kSeqBwdAcc; ++i) {
+                const int q = tid + i * NT;
+                if (q < nq) {
+                    const int k = q / G, j = q - k * G;
+                    Real a = acc[i];
+                    if (k < K) {
+                        for (int r = 0; r < nr; ++r) a += xs[k * R + r] * dp[r * G + j];
+                    } else if (k < K + H) {
+                        if (t >= d)
+                            for (int r = 0; r < nr; ++r) a += hs[(k - K) * R + r] * dp[r * G + j];
+                    } else {
+                        for (int r = 0; r < nr; ++r) a += dp[r * G + j];
+                    }
+                    acc[i] = a;
+                }
+            }
+            __syncthreads();
+        }
+#pragma unroll
+        for (int i = 0; i < kSeqBwdAcc; ++i) {
+            const int q = tid + i * NT;
+            if (q < nq) {
+                const int k = q / G, j = q - k * G;
+                if (k < K) wp[s.w_in[l] + static_cast<long long>(k) * G + j] = acc[i];
+                else if (k < K + H) wp[s.w_rec[l] + static_cast<long long>(k - K) * G + j] = acc[i];
+                else wp[s.bias[l] + j] = acc[i];
+            }
+        }
+        __syncthreads();
     }
 }
 

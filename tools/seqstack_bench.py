@@ -48,6 +48,7 @@ def main():
         for T in (16, 32, 72):
             x = np.random.default_rng(T).uniform(0.5, 1.5, size=(T, B, prof.input_window + 6))
             res = {}
+            ob = np.random.default_rng(T + 1).normal(size=(B, prof.horizon))
             for mode in ("fast", "naive"):
                 if mode == "naive":
                     os.environ["ESRNN_SEQ_NAIVE"] = "1"
@@ -58,7 +59,12 @@ def main():
                 for _ in range(5):
                     out = tr.forward_stack(x)
                     ms.append(tr.last_device_ms())
-                res[mode] = (float(np.median(ms)), out)
+                tr.forward_stack(x, ob)  # warm-up of the adjoint path
+                msb = []
+                for _ in range(3):
+                    tr.forward_stack(x, ob)
+                    msb.append(tr.last_device_ms())
+                res[mode] = (float(np.median(ms)), out, float(np.median(msb)))
             os.environ.pop("ESRNN_SEQ_NAIVE", None)
             f = flops(prof, T, B)
             fast_ms, naive_ms = res["fast"][0], res["naive"][0]
@@ -66,7 +72,10 @@ def main():
             row = {"frequency": freq.name, "T": T, "B": B, "H": prof.hidden_size, "precision": prec,
                    "fast_ms": fast_ms, "naive_ms": naive_ms, "speedup": naive_ms / fast_ms,
                    "gflop": f / 1e9, "fast_tflops": f / fast_ms / 1e9, "frac_ffma_peak": f / fast_ms / 1e9 / peak,
-                   "max_abs_diff_fast_vs_naive": diff}
+                   "max_abs_diff_fast_vs_naive": diff,
+                   "fwd_bwd_fast_ms": res["fast"][2], "fwd_bwd_naive_ms": res["naive"][2],
+                   "fwd_bwd_speedup": res["naive"][2] / res["fast"][2],
+                   "fwd_bwd_frac_ffma_peak": 3 * f / res["fast"][2] / 1e9 / peak}
             rows.append(row)
             print(json.dumps(row), file=sys.stderr, flush=True)
         tr.close()
