@@ -92,6 +92,8 @@ struct StateDev {
                             // and K3's reverse scan) runs in double, see finish.cuh
     int cwp;                // row stride of contrib (multiple of 4 >= I+O+2)
     Real* rowstore;         // [Bcap][rs_ld] per-window K3 operands (NetLayout rs_*)
+    const void* tm_rs;      // two CUtensorMaps (global memory) over the row store for K3's GEMM
+                            // staging: [0] box kGq x kGChunk (A columns), [1] kGk x kGChunk (U)
     double* loss_part;      // [tiles]
     Real* gbuf;             // [P_pad] shared-network gradients (the all-reduced buffer, sharded)
     double* gtail;          // [4] step partials reduced with gbuf: per-series sq-norm, loss sum,
@@ -219,6 +221,22 @@ __device__ __forceinline__ long long gtimer() {
             atomicMax((st).spans + ((long long)(step) * kSpanKinds + (kind)) * 2 + 1, gtimer()); \
     } while (0)
 
+// step-5 per-tile spans of k_tile (entry, after the dependency wait, end): dbg_clk[128 + 3 tile + j]
+constexpr int kDbgTiles = 8192;
+#define DBG_TILE(st, step, tile, j)                                                 \
+    do {                                                                            \
+        if ((st).dbg_clk && (step) == 5 && threadIdx.x == 0 && (tile) < kDbgTiles)  \
+            (st).dbg_clk[128 + 3 * (tile) + (j)] = gtimer();                        \
+    } while (0)
+
+// step-5 per-block spans of k_grad_finish (after the dependency wait, end): dbg_clk[128 + 3 kDbgTiles + 2 bid + j]
+constexpr int kDbgK3 = 4096;
+#define DBG_K3(st, step, bid, j)                                                    \
+    do {                                                                            \
+        if ((st).dbg_clk && (step) == 5 && threadIdx.x == 0 && (bid) < kDbgK3)      \
+            (st).dbg_clk[128 + 3 * kDbgTiles + 2 * (bid) + (j)] = gtimer();         \
+    } while (0)
+
 #define DBG_CLK(st, i)                                                              \
     do {                                                                            \
         if ((st).dbg_clk && blockIdx.x == 0 && threadIdx.x == 0 && _dbg < 64) (st).dbg_clk[_dbg] = clock64(); \
@@ -251,6 +269,15 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                      smem_addr(dst)),
                  "l"(src), "r"(bytes), "r"(smem_addr(bar))
                  : "memory");
+}
+// 2-D tensor copy global -> shared (TMA), box origin (x = column, y = row) in elements;
+// the tensor map lives in global memory (64-byte aligned)
+__device__ __forceinline__ void tma2d_g2s(void* dst, const void* tmap, int x, int y, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            smem_addr(dst)),
+        "l"(tmap), "r"(x), "r"(y), "r"(smem_addr(bar))
+        : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
     unsigned ok = 0;

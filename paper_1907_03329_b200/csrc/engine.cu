@@ -5,6 +5,7 @@
 // all arithmetic of the training step, forecast and validation runs in the sm_100a
 // kernels of kernels.cuh.  There is no CPU compute fallback: without a CUDA device the
 // create call fails with ESRNN_CUDA_ERROR.
+#include <cuda.h>  // CUtensorMap (the encoder is reached through cudaGetDriverEntryPoint)
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -257,6 +258,7 @@ struct esrnn_trainer {
     int ldv = 0;  // row stride of the row-major value copy (16-byte multiple)
     DBuf<signed char> cat;
     DBuf<int> ps_steps;
+    DBuf<unsigned char> tm_rs;  // K3 GEMM staging tensor maps over the row store (2 x 128 B)
     DBuf<unsigned char> lv, se, contrib, rowstore, gbuf, psg, d_inputs, d_targets, d_seas, d_levels;
     DBuf<unsigned char> fX, fL, fS, dump_lv, dump_se;
     DBuf<double> loss_part, es_sq_part, es_pen_part, red_sq_part, scal, loss_hist, f_out, f_smape, f_score, smape_sum, gtail;
@@ -339,7 +341,7 @@ struct esrnn_trainer {
              }(bs)),
              ...);
         };
-        add(vals, vrm, ps, ps_m, ps_v, theta, mW, vW, cat, ps_steps, lv, se, contrib, rowstore, gbuf, psg, d_inputs,
+        add(vals, vrm, ps, ps_m, ps_v, theta, mW, vW, cat, ps_steps, lv, se, contrib, tm_rs, rowstore, gbuf, psg, d_inputs,
             d_targets, d_seas, d_levels, fX, fL, fS, dump_lv, dump_se, loss_part, es_sq_part, es_pen_part, red_sq_part, scal, upart,
             loss_hist, f_out, f_smape, f_score, smape_sum, done_ctr, gtile_ctr, gpart, net_step, dbg_clk, errw, gtail,
             coll_seq, spans);
@@ -389,6 +391,7 @@ struct esrnn_trainer {
         s.contrib = reinterpret_cast<double*>(contrib.p);
         s.cwp = (I + O + 2 + 3) & ~3;
         s.rowstore = reinterpret_cast<Real*>(rowstore.p);
+        s.tm_rs = tm_rs.p;
         s.loss_part = loss_part.p;
         s.gbuf = reinterpret_cast<Real*>(gbuf.p);
         s.gtail = gtail.p;
@@ -714,6 +717,8 @@ void sync_weights_from_device(Eng* e) {
 }
 
 // ------------------------------------------------------------------ capacity
+void encode_rowstore_maps(Eng* e, int rsz);  // defined with the kernel attributes below
+
 void ensure_capacity(Eng* e, int B) {
     if (B <= e->Bcap) return;
     const int S = e->S, T = e->T, I = e->I, O = e->O;
@@ -763,6 +768,7 @@ void ensure_capacity(Eng* e, int B) {
     // (+ 256 columns: the tensor-core path reads whole 128-row / 64-column operand quads
     // past the last matrix of the last row)
     e->rowstore.alloc(r * (static_cast<size_t>(e->tiles_cap * kRows) * e->lay.rs_ld + 256));
+    encode_rowstore_maps(e, static_cast<int>(r));
     e->loss_part.alloc(e->tiles_cap);
     e->psg.alloc(r * static_cast<size_t>(kc) * (2 + S));
     e->es_sq_part.alloc(e->es_blocks);
@@ -968,15 +974,60 @@ size_t finish_smem_launch(const NetLayout& lay, bool umma) {
     return umma ? std::max(f, static_cast<size_t>(kUSmem) + 1024) : f;
 }
 
+// K3's GEMM staging tensor maps (finish.cuh): the row store as a 2-D [rows][rs_ld] tensor of
+// Real, boxes of kGChunk rows x kGq (A) / kGk (U) columns, no swizzle, zero fill past the end.
+using TensorMapEncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                       const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                       CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+void encode_rowstore_maps(Eng* e, int rsz) {
+    static TensorMapEncodeFn enc = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        CUDA_OK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || !fn) raise(ESRNN_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+        return reinterpret_cast<TensorMapEncodeFn>(fn);
+    }();
+    alignas(64) CUtensorMap maps[2];
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(e->lay.rs_ld), static_cast<cuuint64_t>(e->tiles_cap) * kRows};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(e->lay.rs_ld) * rsz};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUtensorMapDataType dt = rsz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+    for (int i = 0; i < 2; ++i) {
+        const cuuint32_t box[2] = {static_cast<cuuint32_t>(i == 0 ? kGq : kGk), static_cast<cuuint32_t>(kGChunk)};
+        const CUresult r = enc(&maps[i], dt, 2, e->rowstore.p, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) raise(ESRNN_CUDA_ERROR, "row-store tensor map encoding failed (%d)", static_cast<int>(r));
+    }
+    e->tm_rs.alloc(sizeof maps);
+    CUDA_OK(cudaMemcpyAsync(e->tm_rs.p, maps, sizeof maps, cudaMemcpyHostToDevice, e->stream));
+    CUDA_OK(cudaStreamSynchronize(e->stream));  // `maps` is a stack buffer
+}
+
+// Every kernel of the step prefers the maximum shared-memory carveout.  Under programmatic
+// dependent launch the next kernel's CTAs are placed on SMs still running the previous
+// kernel's blocks; an SM configured for a small-smem kernel (K4, 1 KB) cannot take a K2
+// tile (133 KB at cfg1) until it drains and reconfigures, so those tiles launched late and
+// passed their dependency wait up to 2.4 us after the first (ESRNN_NO_CARVEOUT=1 restores
+// the driver's default choice).
+template <typename K>
+void max_carveout(K* kern) {
+    static const bool off = std::getenv("ESRNN_NO_CARVEOUT") != nullptr;
+    if (!off) CUDA_OK(cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+}
+
 // The tile kernel's scans are specialised for the M4 seasonalities (S = 1, 4, 12: seasonal
 // ring in registers); any other S runs the generic variant.
 template <typename Real, int MODE, int SC>
 void set_tile_attr(const NetLayout& lay) {
-    if (stack_resident<Real>(lay))
+    if (stack_resident<Real>(lay)) {
         CUDA_OK(cudaFuncSetAttribute(k_tile<Real, MODE, true, SC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)stack_smem<Real>(lay, true)));
+        max_carveout(k_tile<Real, MODE, true, SC>);
+    }
     CUDA_OK(cudaFuncSetAttribute(k_tile<Real, MODE, false, SC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)stack_smem<Real>(lay, false)));
+    max_carveout(k_tile<Real, MODE, false, SC>);
 }
 
 template <typename Real, int SC>
@@ -985,14 +1036,20 @@ void set_sc_attrs(const NetLayout& lay) {
     set_tile_attr<Real, kLossOnly, SC>(lay);
     CUDA_OK(cudaFuncSetAttribute(k_grad_finish<Real, SC, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)finish_smem<Real>(lay)));
-    if (sizeof(Real) == 4)
+    max_carveout(k_grad_finish<Real, SC, false>);
+    if (sizeof(Real) == 4) {
         CUDA_OK(cudaFuncSetAttribute(k_grad_finish<Real, SC, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)finish_smem_launch<Real>(lay, true)));
+        max_carveout(k_grad_finish<Real, SC, true>);
+    }
 }
 
 template <typename Real>
 void setup_kernel_attrs(Eng* e) {
     set_tile_attr<Real, kForecast, 0>(e->lay);
+    max_carveout(k_adam<Real>);
+    max_carveout(k_finalize<Real>);
+    max_carveout(k_group_reduce<Real>);
     switch (e->S) {
         case 1: set_sc_attrs<Real, 1>(e->lay); break;
         case 4: set_sc_attrs<Real, 4>(e->lay); break;
@@ -1206,7 +1263,7 @@ void alloc_state(Eng* e) {
     e->net_step.alloc(1);
     e->errw.alloc(4);
     if (std::getenv("ESRNN_DEBUG_CLOCKS")) {
-        e->dbg_clk.alloc(128);
+        e->dbg_clk.alloc(128 + 3 * kDbgTiles + 2 * kDbgK3);  // + per-tile step-5 spans of k_tile
         e->dbg_clk.zero(e->stream);
     }
     ZeroSpans z{};
@@ -1568,7 +1625,8 @@ double train_epoch_impl(Eng* e) {
         for (int i = 33; i < 48 && c[i] > 0; ++i) std::fprintf(stderr, " %lld", c[i] - c[i - 1]);
         std::fprintf(stderr, "\n[esrnn dbg] grad_finish reduce block0:");
         for (int i = 49; i < 64 && c[i] > 0; ++i) std::fprintf(stderr, " %lld", c[i] - c[i - 1]);
-        std::fprintf(stderr, "\n[esrnn dbg] reduce block0 start - ES block0 start: %lld\n", c[48] - c[32]);
+        std::fprintf(stderr, "\n[esrnn dbg] ES block0 first chunk landed %lld cycles after the wait\n", c[42] - c[37]);
+        std::fprintf(stderr, "[esrnn dbg] reduce block0 start - ES block0 start: %lld\n", c[48] - c[32]);
         std::fprintf(stderr, "[esrnn dbg] scan block0:");
         for (int i = 65; i < 80 && c[i] > 0; ++i) std::fprintf(stderr, " %lld", c[i] - c[i - 1]);
         std::fprintf(stderr, "\n[esrnn dbg] timeline ns (scan0 start, scan0 end, stack0 start, stack0 end, "
@@ -1584,6 +1642,38 @@ double train_epoch_impl(Eng* e) {
                      sp[7] - sp[0], sp[8] - sp[0], sp[9] - sp[0]);
         std::fprintf(stderr, "[esrnn dbg] step-5 K3 ES blocks end %lld, GEMM blocks end %lld\n", sp[10] - sp[0],
                      sp[11] - sp[0]);
+        std::vector<long long> tc(3 * kDbgTiles);
+        CUDA_OK(cudaMemcpy(tc.data(), e->dbg_clk.p + 128, sizeof(long long) * tc.size(), cudaMemcpyDeviceToHost));
+        std::vector<long long> ent, st0, en0, du;
+        for (int t = 0; t < kDbgTiles; ++t)
+            if (tc[3 * t + 1] > 0) {
+                ent.push_back(tc[3 * t] - sp[0]);
+                st0.push_back(tc[3 * t + 1] - sp[0]);
+                en0.push_back(tc[3 * t + 2] - sp[0]);
+                du.push_back(tc[3 * t + 2] - tc[3 * t + 1]);
+            }
+        auto q = [](std::vector<long long> v, double f) {
+            std::sort(v.begin(), v.end());
+            return v.empty() ? 0LL : v[std::min(v.size() - 1, static_cast<size_t>(f * v.size()))];
+        };
+        std::fprintf(stderr, "[esrnn dbg] step-5 tiles %zu: entry min/med/max %lld %lld %lld | waited %lld %lld %lld | end %lld %lld %lld | "
+                             "duration %lld %lld %lld\n", du.size(), q(ent, 0), q(ent, 0.5), q(ent, 1), q(st0, 0), q(st0, 0.5), q(st0, 1), q(en0, 0),
+                     q(en0, 0.5), q(en0, 1), q(du, 0), q(du, 0.5), q(du, 1));
+        std::vector<long long> kc(2 * kDbgK3);
+        CUDA_OK(cudaMemcpy(kc.data(), e->dbg_clk.p + 128 + 3 * kDbgTiles, sizeof(long long) * kc.size(),
+                           cudaMemcpyDeviceToHost));
+        for (int kind = 0; kind < 2; ++kind) {
+            std::vector<long long> a, b, d;
+            for (int i = 0; i < kDbgK3; ++i)
+                if (kc[2 * i] > 0 && ((i < e->es_blocks) == (kind == 0))) {
+                    a.push_back(kc[2 * i] - sp[0]);
+                    b.push_back(kc[2 * i + 1] - sp[0]);
+                    d.push_back(kc[2 * i + 1] - kc[2 * i]);
+                }
+            std::fprintf(stderr, "[esrnn dbg] step-5 K3 %s blocks %zu: waited min/med/max %lld %lld %lld | end %lld %lld %lld | "
+                                 "duration %lld %lld %lld\n", kind == 0 ? "ES" : "GEMM", a.size(), q(a, 0), q(a, 0.5),
+                         q(a, 1), q(b, 0), q(b, 0.5), q(b, 1), q(d, 0), q(d, 0.5), q(d, 1));
+        }
     }
     if (e->span_mode) {
         // per kind: sum over steps of (latest CTA end - earliest CTA start)

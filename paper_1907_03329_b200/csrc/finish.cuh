@@ -16,7 +16,7 @@ namespace esrnn_dev {
 
 constexpr int kFinishThreads = 256;
 constexpr int kEsSlotsPerBlock = 32;  // fp64 ES blocks: warp 0 owns 32 slots; all warps stage the windows
-constexpr int kEsSlots32 = 16;        // fp32 ES blocks (es_block_fp32): 16 slots, smaller shared footprint
+constexpr int kEsSlots32 = 8;         // fp32 ES blocks (es_block_fp32): 8 slots (measured against 16: see DESIGN perf log)
 constexpr int kEsChunk = 128;         // contribution rows staged per round
 constexpr int kGq = 16, kGk = 8;      // K3 GEMM output block (gate rows x input features)
 constexpr int kGChunk = 256;          // row-store rows staged per round
@@ -256,45 +256,62 @@ __device__ __forceinline__ void es_block_fp32(StateDev<Real>& st, const PlanDev&
     pdl_wait();
     DBG_SPAN_MIN(st, s, 4);
     SPAN_BEGIN(st, s, kSpanFinish);
+    DBG_K3(st, s, bid, 0);
     clk(5);
-    // ---- window log adjoints (tile.cuh), chunks of kEsChunk contribution rows; thread per
-    // (slot, index u): seasonality u gets entry u - (a - I + 1) of each window whose
-    // [a - I + 1, a + O] covers u, level u the level entry of each window anchored at u ----
+    // ---- window log adjoints (tile.cuh), chunks of kEsChunk contribution rows; a warp per
+    // slot, lanes over the index u: seasonality u gets entry u - (a - I + 1) of each window
+    // whose [a - I + 1, a + O] covers u, level u the level entry of each window anchored at
+    // u.  The last chunk also turns the log adjoints into adjoints (x 1/s, x 1/l) in the same
+    // pass ((sum + chunk) * r: the operations of a separate scaling pass, one barrier fewer) ----
     const int nio = I + O;
     const int cb0 = pl.slot_win_off[k0];
     const int blo = woff[0], bhi = woff[nsl];
+    const int lane = tid & 31, wq = tid >> 5;
+    constexpr int kW = kFinishThreads / 32;
     for (int clo = blo; clo < bhi; clo += kEsChunk) {
         const int chi = min(bhi, clo + kEsChunk);
+        const bool lastc = chi == bhi;
         const double* src = st.contrib + (size_t)(clo - cb0) * cwp;
         const int nel = (chi - clo) * cwp;
         for (int i = tid * 2; i < nel; i += kFinishThreads * 2) cp_async16(cbuf + i, src + i);
         cp_async_wait_all();
         __syncthreads();
-        for (int e = tid; e < nsl * T; e += kFinishThreads) {
-            const int sl = e / T, u = e - sl * T;
+        if (clo == blo) clk(10);  // first chunk landed (dbg_clk[42])
+        for (int sl = wq; sl < nsl; sl += kW) {  // warp-uniform
             const int wl = max(woff[sl], clo), wh = min(woff[sl + 1], chi);
-            if (wl >= wh) continue;
-            double as = 0.0, al = 0.0;
-            for (int w = wl; w < wh; ++w) {
-                const double* c = cbuf + (w - clo) * cwp;
-                const int a = static_cast<int>(c[nio + 1]);
-                const int j = u - (a - I + 1);
-                if (j >= 0 && j < nio) as += c[j];
-                if (u == a) al += c[nio];
+            if (wl >= wh && !lastc) continue;
+            double* sbr = SB + sl * lds;
+            double* lbr = LB + sl * ldl;
+            for (int u = lane; u < T; u += 32) {
+                if (wl < wh) {
+                    double as = 0.0, al = 0.0;
+                    for (int w = wl; w < wh; ++w) {
+                        const double* c = cbuf + (w - clo) * cwp;
+                        const int a = static_cast<int>(c[nio + 1]);
+                        const int j = u - (a - I + 1);
+                        if (j >= 0 && j < nio) as += c[j];
+                        if (u == a) al += c[nio];
+                    }
+                    sbr[u] += as;
+                    lbr[u] += al;
+                }
+                if (lastc) {
+                    lbr[u] *= static_cast<double>(RI[u * bd + sl]);
+                    sbr[u] *= static_cast<double>(RS[u * bd + sl]);
+                }
             }
-            SB[sl * lds + u] += as;
-            LB[sl * ldl + u] += al;
         }
         __syncthreads();
     }
     clk(6);
-    // ---- log adjoints -> adjoints ----
-    for (int e = tid; e < nsl * T; e += kFinishThreads) {
-        const int sl = e / T, t = e - sl * T;
-        LB[sl * ldl + t] *= static_cast<double>(RI[t * bd + sl]);
-        SB[sl * lds + t] *= static_cast<double>(RS[t * bd + sl]);
+    if (blo == bhi) {  // no windows (cannot happen for a slot in the step; kept total)
+        for (int sl = wq; sl < nsl; sl += kW)
+            for (int t = lane; t < T; t += 32) {
+                LB[sl * ldl + t] *= static_cast<double>(RI[t * bd + sl]);
+                SB[sl * lds + t] *= static_cast<double>(RS[t * bd + sl]);
+            }
+        __syncthreads();
     }
-    __syncthreads();
     clk(7);
     if (!mine) return;
     // ---- reverse recursion (holt_winters.hpp:266-277 adjoints), Sb = final adjoint of s[t+S]:
@@ -646,6 +663,8 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
     } else {
         pdl_wait();
         SPAN_BEGIN(st, s, kSpanFinish);
+        DBG_K3(st, s, bid, 0);
+        FCLK();
         // ------- weight gradients: G[q][k] = sum_b A[b][q] U[b][k] over the step's windows ----
         // block -> (matrix, 16 q x 8 k output block, row part); warp w sums rows b = w (mod 8)
         // of its part in order, warps are combined in order, and for large steps (gsplit > 1
@@ -670,33 +689,36 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
         Real* As = reinterpret_cast<Real*>(smem_raw);       // [kGBuf][kGChunk][kGq]
         Real* Us = As + kGBuf * kGChunk * kGq;               // [kGBuf][kGChunk][kGk]
         Real* Rd = Us + kGBuf * kGChunk * kGk;               // [8 warps][32 lanes][6]
-        constexpr int e16 = 16 / static_cast<int>(sizeof(Real));
-        constexpr int ca = kGq / e16, cu = kGk / e16;
-        const int rs_ld = lay.rs_ld;
-        // one cp.async group per chunk (possibly empty, so the group count stays uniform)
+        // chunk staging by TMA: two 2-D tensor copies per chunk (the A and U column boxes of
+        // kGChunk rows), completion on the buffer's mbarrier.  (16-byte cp.async of the
+        // scattered row segments kept the SM's load pipeline busy ~1.5k cycles per chunk and
+        // stalled the co-resident ES blocks' shared-memory traffic behind it.)  Rows past the
+        // step's end are staged but never summed; rows past the allocation read as zeros.
+        __shared__ __align__(8) uint64_t gbar[kGBuf];
+        if (tid == 0) {
+#pragma unroll
+            for (int b = 0; b < kGBuf; ++b) mbar_init(&gbar[b], 1);
+        }
+        __syncthreads();
+        const int nch = (Bl + kGChunk - 1) / kGChunk;
+        const void* tmA = st.tm_rs;
+        const void* tmU = static_cast<const unsigned char*>(st.tm_rs) + 128;
         auto stage = [&](int c) {
-            const int c0 = c * kGChunk, buf = c % kGBuf;
-            const int nb = min(kGChunk, Bl - c0);
-            for (int i = tid; i < nb * (ca + cu); i += kFinishThreads) {
-                const int row = i / (ca + cu), part = i - row * (ca + cu);
-                const Real* src = st.rowstore + (size_t)(r0 + c0 + row) * rs_ld;
-                if (part < ca)
-                    cp_async16(As + (buf * kGChunk + row) * kGq + part * e16, src + md.a_off + q0 + part * e16);
-                else
-                    cp_async16(Us + (buf * kGChunk + row) * kGk + (part - ca) * e16,
-                               src + md.u_off + k0 + (part - ca) * e16);
-            }
-            cp_async_commit();
+            if (tid != 0 || c >= nch) return;
+            const int buf = c % kGBuf;
+            fence_proxy_async_smem();  // the buffer's previous generic reads before the async writes
+            mbar_expect_tx(&gbar[buf], static_cast<unsigned>(sizeof(Real) * kGChunk * (kGq + kGk)));
+            tma2d_g2s(As + buf * kGChunk * kGq, tmA, md.a_off + q0, r0 + c * kGChunk, &gbar[buf]);
+            tma2d_g2s(Us + buf * kGChunk * kGk, tmU, md.u_off + k0, r0 + c * kGChunk, &gbar[buf]);
         };
         Real acc[2][2] = {{0, 0}, {0, 0}}, bacc[2] = {0, 0};
-        const int nch = (Bl + kGChunk - 1) / kGChunk;
         // kGBuf - 1 chunks in flight ahead of the one being summed
 #pragma unroll
         for (int c = 0; c < kGBuf - 1; ++c) stage(c);
         for (int c = 0; c < nch; ++c) {
-            stage(c + kGBuf - 1);  // empty group past the end
-            cp_async_wait<kGBuf - 1>();
-            __syncthreads();
+            stage(c + kGBuf - 1);
+            mbar_wait(&gbar[c % kGBuf], static_cast<unsigned>((c / kGBuf) & 1));
+            if (c == 0) FCLK();
             const int nb = min(kGChunk, Bl - c * kGChunk);
             const Real* Ab = As + (c % kGBuf) * kGChunk * kGq + 2 * qp;
             const Real* Ub = Us + (c % kGBuf) * kGChunk * kGk + 2 * kp;
@@ -742,7 +764,7 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
             }
             __syncthreads();  // buffer c % kGBuf is restaged next round
         }
-        cp_async_wait<0>();
+        FCLK();
         Real* rd = Rd + (warp * 32 + lane) * 6;
         rd[0] = acc[0][0];
         rd[1] = acc[0][1];
@@ -807,6 +829,7 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
         if (tid == 0 && writer) st.red_sq_part[gb] = tot;
     }
     FCLK();
+    DBG_K3(st, s, bid, 1);
     DBG_SPAN_MAX(st, s, 5);
     if (bid < es_blocks) DBG_SPAN_MAX(st, s, 10);
     else DBG_SPAN_MAX(st, s, 11);

@@ -373,6 +373,7 @@ __global__ void __launch_bounds__((RESIDENT || sizeof(Real) == 8) ? 512 : 384, (
     int _dbg = 0;
     if (MODE == kTrain) DBG_GT(st, 2);
     if (MODE == kTrain) DBG_SPAN_MIN(st, s, 0);
+    if (MODE == kTrain) DBG_TILE(st, s, tile, 0);
     DBG_CLK(st, 0);
     // row store of this tile's windows (K3 operands): [b][rs_ld], b = step-local window
     Real* __restrict__ rs = (MODE == kTrain) ? st.rowstore + (size_t)(tile * R) * lay.rs_ld : nullptr;
@@ -441,6 +442,7 @@ __global__ void __launch_bounds__((RESIDENT || sizeof(Real) == 8) ? 512 : 384, (
             DBG_SPAN_MIN(st, s, 1);
             DBG_SPAN_MIN(st, s - 1, 9);
             SPAN_BEGIN(st, s, kSpanTile);
+            DBG_TILE(st, s, tile, 1);
         }
         weights_tma();
         for (int e = tid; e < nrows * np; e += NT) {
@@ -800,6 +802,7 @@ __global__ void __launch_bounds__((RESIDENT || sizeof(Real) == 8) ? 512 : 384, (
     if (MODE == kTrain) DBG_GT(st, 3);
     if (MODE == kTrain) DBG_SPAN_MAX(st, s, 2);
     if (MODE == kTrain) SPAN_END(st, s, kSpanTile);
+    if (MODE == kTrain) DBG_TILE(st, s, tile, 2);
 }
 
 }  // namespace esrnn_dev
