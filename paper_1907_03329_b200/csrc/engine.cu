@@ -935,7 +935,7 @@ bool stack_resident(const NetLayout& lay) {
 int stack_threads(const NetLayout& lay) { return tile_threads(lay); }
 
 template <typename Real>
-size_t finish_smem(const NetLayout& lay) {
+size_t finish_smem(const NetLayout& lay, int ring = kGBuf) {
     // ES blocks: level / seasonality adjoints [bd][T|1], [bd][(T+S)|1], forward l and s
     // columns [T][bd] (double), one staged observation row per slot (Real), one chunk of
     // staged contribution rows (double)
@@ -951,7 +951,7 @@ size_t finish_smem(const NetLayout& lay) {
                                             bd * (2 + S) * sizeof(Real),
                                         sizeof(double) * kEsChunk * cwp);
         const size_t es = sizeof(double) * bd * (ldl + lds) + 6 * T * bd * cr + sizeof(double) * bd * S + scratch;
-        const size_t gemm = sizeof(Real) * (static_cast<size_t>(kGBuf * kGChunk) * (kGq + kGk) + (kFinishThreads / 32) * 32 * 6);
+        const size_t gemm = sizeof(Real) * (static_cast<size_t>(ring * kGChunk) * (kGq + kGk) + (kFinishThreads / 32) * 32 * 6);
         return std::max(es, gemm);
     }
     const size_t cwp = (lay.I + lay.O + 2 + 3) & ~3;
@@ -963,7 +963,7 @@ size_t finish_smem(const NetLayout& lay) {
                                sizeof(Real) == 4 ? (lay.S == 1 ? sizeof(double) : sizeof(float)) * 4 * bd *
                                                        static_cast<size_t>(lay.T)
                                                  : 0);  // the scan's coefficients (finish.cuh)
-    const size_t gemm = sizeof(Real) * (static_cast<size_t>(kGBuf * kGChunk) * (kGq + kGk) + (kFinishThreads / 32) * 32 * 6);
+    const size_t gemm = sizeof(Real) * (static_cast<size_t>(ring * kGChunk) * (kGq + kGk) + (kFinishThreads / 32) * 32 * 6);
     return std::max(es, gemm);
 }
 
@@ -1087,16 +1087,27 @@ void launch_k(Eng* e, bool pdl, void (*kern)(KArgs...), int grid, int block, siz
     CUDA_OK(cudaLaunchKernelEx(&lc, kern, std::forward<Args>(args)...));
 }
 
+// K3's GEMM staging ring: 3 buffers (2 chunks in flight) while the grid fits one wave at two
+// blocks per SM; beyond that 2 buffers, so the smaller blocks fit four per SM and the GEMM blocks
+// are not queued behind the ES blocks (measured: cfg1 ring 3 0.63M vs ring 2 0.57M series/s;
+// cfg3 ring 2 52.3 vs ring 3 55.3 ms per epoch + validate)
+int finish_ring(const Eng* e, int blocks) {
+    static const int forced = std::getenv("ESRNN_GEMM_RING") ? std::atoi(std::getenv("ESRNN_GEMM_RING")) : 0;
+    if (forced == 2 || forced == 3) return forced;
+    return blocks > 2 * g_num_sms ? 2 : 3;
+}
+
 template <typename Real, int SC>
 void launch_finish_sc(Eng* e, const StateDev<Real>& st, const PlanDev& pv, int s, int finalize, bool pdl) {
     const int gemm_blocks = e->umma_parts > 0 ? e->umma_tiles * e->umma_parts : e->red_blocks * e->gsplit;
+    const int ring = finish_ring(e, e->es_blocks + gemm_blocks);
     if (e->umma_parts > 0)
         launch_k(e, pdl, k_grad_finish<Real, SC, true>, e->es_blocks + gemm_blocks, kFinishThreads,
                  finish_smem_launch<Real>(e->lay, true), st, pv, e->lay, s, e->es_blocks, finalize, e->gsplit,
-                 e->umma_parts);
+                 e->umma_parts, 3);
     else
         launch_k(e, pdl, k_grad_finish<Real, SC, false>, e->es_blocks + gemm_blocks, kFinishThreads,
-                 finish_smem<Real>(e->lay), st, pv, e->lay, s, e->es_blocks, finalize, e->gsplit, 0);
+                 finish_smem<Real>(e->lay, ring), st, pv, e->lay, s, e->es_blocks, finalize, e->gsplit, 0, ring);
 }
 template <typename Real>
 void launch_finish(Eng* e, const StateDev<Real>& st, const PlanDev& pv, int s, int finalize, bool pdl = false) {

@@ -20,7 +20,8 @@ constexpr int kEsSlots32 = 8;         // fp32 ES blocks (es_block_fp32): 8 slots
 constexpr int kEsChunk = 128;         // contribution rows staged per round
 constexpr int kGq = 16, kGk = 8;      // K3 GEMM output block (gate rows x input features)
 constexpr int kGChunk = 256;          // row-store rows staged per round
-constexpr int kGBuf = 3;              // staging ring depth (kGBuf - 1 chunks in flight)
+constexpr int kGBuf = 3;              // staging ring depth, maximum (ring - 1 chunks in flight; the
+                                      // launch picks 3 or 2, engine.cu finish_ring)
 // fp32 mode with S = 1: K3's ES blocks recompute the forward states in double (see there)
 template <typename Real, int SC>
 constexpr bool kEsRecompute = sizeof(Real) == 4 && SC == 1;
@@ -387,7 +388,7 @@ __device__ __forceinline__ void es_block_fp32(StateDev<Real>& st, const PlanDev&
 template <typename Real, int SC, bool UMMA>
 __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> st, PlanDev pl, NetLayout lay, int s,
                                                                 int es_blocks, int finalize, int gsplit,
-                                                                int umma_parts_arg) {
+                                                                int umma_parts_arg, int nring) {
     const int umma_parts = UMMA ? umma_parts_arg : 0;
     using M = Math<Real>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -686,9 +687,9 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
         const int Bl = min(Bstep, r0 + span) - r0;
         const int lane = tid & 31, warp = tid >> 5;
         const int qp = lane >> 2, kp = lane & 3;
-        Real* As = reinterpret_cast<Real*>(smem_raw);       // [kGBuf][kGChunk][kGq]
-        Real* Us = As + kGBuf * kGChunk * kGq;               // [kGBuf][kGChunk][kGk]
-        Real* Rd = Us + kGBuf * kGChunk * kGk;               // [8 warps][32 lanes][6]
+        Real* As = reinterpret_cast<Real*>(smem_raw);       // [nring][kGChunk][kGq]
+        Real* Us = As + nring * kGChunk * kGq;               // [nring][kGChunk][kGk]
+        Real* Rd = Us + nring * kGChunk * kGk;               // [8 warps][32 lanes][6]
         // chunk staging by TMA: two 2-D tensor copies per chunk (the A and U column boxes of
         // kGChunk rows), completion on the buffer's mbarrier.  (16-byte cp.async of the
         // scattered row segments kept the SM's load pipeline busy ~1.5k cycles per chunk and
@@ -697,7 +698,8 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
         __shared__ __align__(8) uint64_t gbar[kGBuf];
         if (tid == 0) {
 #pragma unroll
-            for (int b = 0; b < kGBuf; ++b) mbar_init(&gbar[b], 1);
+            for (int b = 0; b < kGBuf; ++b)
+                if (b < nring) mbar_init(&gbar[b], 1);
         }
         __syncthreads();
         const int nch = (Bl + kGChunk - 1) / kGChunk;
@@ -705,23 +707,22 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
         const void* tmU = static_cast<const unsigned char*>(st.tm_rs) + 128;
         auto stage = [&](int c) {
             if (tid != 0 || c >= nch) return;
-            const int buf = c % kGBuf;
+            const int buf = c % nring;
             fence_proxy_async_smem();  // the buffer's previous generic reads before the async writes
             mbar_expect_tx(&gbar[buf], static_cast<unsigned>(sizeof(Real) * kGChunk * (kGq + kGk)));
             tma2d_g2s(As + buf * kGChunk * kGq, tmA, md.a_off + q0, r0 + c * kGChunk, &gbar[buf]);
             tma2d_g2s(Us + buf * kGChunk * kGk, tmU, md.u_off + k0, r0 + c * kGChunk, &gbar[buf]);
         };
         Real acc[2][2] = {{0, 0}, {0, 0}}, bacc[2] = {0, 0};
-        // kGBuf - 1 chunks in flight ahead of the one being summed
-#pragma unroll
-        for (int c = 0; c < kGBuf - 1; ++c) stage(c);
+        // nring - 1 chunks in flight ahead of the one being summed
+        for (int c = 0; c < nring - 1; ++c) stage(c);
         for (int c = 0; c < nch; ++c) {
-            stage(c + kGBuf - 1);
-            mbar_wait(&gbar[c % kGBuf], static_cast<unsigned>((c / kGBuf) & 1));
+            stage(c + nring - 1);
+            mbar_wait(&gbar[c % nring], static_cast<unsigned>((c / nring) & 1));
             if (c == 0) FCLK();
             const int nb = min(kGChunk, Bl - c * kGChunk);
-            const Real* Ab = As + (c % kGBuf) * kGChunk * kGq + 2 * qp;
-            const Real* Ub = Us + (c % kGBuf) * kGChunk * kGk + 2 * kp;
+            const Real* Ab = As + (c % nring) * kGChunk * kGq + 2 * qp;
+            const Real* Ub = Us + (c % nring) * kGChunk * kGk + 2 * kp;
 #pragma unroll 8
             for (int b = warp; b < nb; b += kFinishThreads / 32) {
                 Real a0, a1, u0, u1;
@@ -762,7 +763,7 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
                     bacc[1] += a1;
                 }
             }
-            __syncthreads();  // buffer c % kGBuf is restaged next round
+            __syncthreads();  // buffer c % nring is restaged next round
         }
         FCLK();
         Real* rd = Rd + (warp * 32 + lane) * 6;
