@@ -272,7 +272,7 @@ struct esrnn_trainer {
     DBuf<long long> net_step;
     DBuf<long long> dbg_clk;  // ESRNN_DEBUG_CLOCKS: per-phase clock64 stamps of tile 0
     DBuf<int> errw;
-    int Bcap = 0, kcap = 0, tiles_cap = 0, es_blocks = 0, red_blocks = 0, steps_cap = 0;
+    int Bcap = 0, kcap = 0, tiles_cap = 0, es_bd = 16, es_blocks = 0, red_blocks = 0, steps_cap = 0;
     bool pdl = std::getenv("ESRNN_NO_PDL") == nullptr;  // programmatic dependent launch between step kernels
 
     DevPlan epoch_plan, batch_plan;
@@ -729,7 +729,13 @@ void ensure_capacity(Eng* e, int B) {
     e->kcap = (std::min(e->N > 0 ? e->N : 1, B) + kEsSlotsPerBlock - 1) / kEsSlotsPerBlock * kEsSlotsPerBlock;
     const int kc = e->kcap;
     e->tiles_cap = (B + kRows - 1) / kRows;
-    const int es_slots = e->fp64 ? kEsSlotsPerBlock : kEsSlots32;
+    // fp32 ES blocks: 8 slots while that keeps them within four per SM (shorter per-block gather,
+    // more blocks overlapping K2: cfg1 -8% step, cfg3 -5%); 16 for large steps (B = 48,000:
+    // 8 slots measured 24.5 vs 20.7 ms per epoch)
+    e->es_bd = e->fp64 ? kEsSlotsPerBlock : ((kc + 7) / 8 <= 4 * g_num_sms ? 8 : kEsSlots32);
+    if (const char* v = std::getenv("ESRNN_ES_SLOTS"); v && !e->fp64 && (std::atoi(v) == 8 || std::atoi(v) == 16))
+        e->es_bd = std::atoi(v);
+    const int es_slots = e->es_bd;
     e->es_blocks = (kc + es_slots - 1) / es_slots;
     // Row parts per weight-gradient tile: at B <= 4,096 one block per tile is fastest (a
     // two-part split measured +6.8 us at cfg1); beyond, one part per 4,096 rows (<= 16)
@@ -935,7 +941,7 @@ bool stack_resident(const NetLayout& lay) {
 int stack_threads(const NetLayout& lay) { return tile_threads(lay); }
 
 template <typename Real>
-size_t finish_smem(const NetLayout& lay, int ring = kGBuf) {
+size_t finish_smem(const NetLayout& lay, int ring = kGBuf, int es_bd = kEsSlots32) {
     // ES blocks: level / seasonality adjoints [bd][T|1], [bd][(T+S)|1], forward l and s
     // columns [T][bd] (double), one staged observation row per slot (Real), one chunk of
     // staged contribution rows (double)
@@ -943,7 +949,7 @@ size_t finish_smem(const NetLayout& lay, int ring = kGBuf) {
         // es_block_fp32 (finish.cuh): adjoints [bd][T|1], [bd][(T+S)|1] (double), six [T][bd]
         // coefficient arrays, then a scratch region: pre-wait observation rows + forward
         // states + raw parameters, post-wait one chunk of staged contribution rows
-        const size_t bd = kEsSlots32, T = lay.T, S = lay.S;
+        const size_t bd = es_bd, T = lay.T, S = lay.S;
         const size_t ldl = T | 1, lds = (T + S) | 1;
         const size_t cr = S == 1 ? sizeof(double) : sizeof(float);
         const size_t cwp = (lay.I + lay.O + 2 + 3) & ~3;
@@ -1101,13 +1107,14 @@ template <typename Real, int SC>
 void launch_finish_sc(Eng* e, const StateDev<Real>& st, const PlanDev& pv, int s, int finalize, bool pdl) {
     const int gemm_blocks = e->umma_parts > 0 ? e->umma_tiles * e->umma_parts : e->red_blocks * e->gsplit;
     const int ring = finish_ring(e, e->es_blocks + gemm_blocks);
+    const int bd = e->es_bd;
     if (e->umma_parts > 0)
         launch_k(e, pdl, k_grad_finish<Real, SC, true>, e->es_blocks + gemm_blocks, kFinishThreads,
                  finish_smem_launch<Real>(e->lay, true), st, pv, e->lay, s, e->es_blocks, finalize, e->gsplit,
-                 e->umma_parts, 3);
+                 e->umma_parts, 3, bd);
     else
         launch_k(e, pdl, k_grad_finish<Real, SC, false>, e->es_blocks + gemm_blocks, kFinishThreads,
-                 finish_smem<Real>(e->lay, ring), st, pv, e->lay, s, e->es_blocks, finalize, e->gsplit, 0, ring);
+                 finish_smem<Real>(e->lay, ring, bd), st, pv, e->lay, s, e->es_blocks, finalize, e->gsplit, 0, ring, bd);
 }
 template <typename Real>
 void launch_finish(Eng* e, const StateDev<Real>& st, const PlanDev& pv, int s, int finalize, bool pdl = false) {

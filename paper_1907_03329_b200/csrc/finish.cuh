@@ -16,8 +16,9 @@ namespace esrnn_dev {
 
 constexpr int kFinishThreads = 256;
 constexpr int kEsSlotsPerBlock = 32;  // fp64 ES blocks: warp 0 owns 32 slots; all warps stage the windows
-constexpr int kEsSlots32 = 8;         // fp32 ES blocks (es_block_fp32): 8 slots (measured against 16: see DESIGN perf log)
-constexpr int kEsChunk = 128;         // contribution rows staged per round
+constexpr int kEsSlots32 = 16;        // fp32 ES blocks (es_block_fp32): at most 16 slots; the launch picks
+                                      // 8 or 16 (engine.cu es_slots_fp32)
+constexpr int kEsChunk = 64;          // contribution rows staged per round (64: K3 fits four blocks per SM at Monthly)
 constexpr int kGq = 16, kGk = 8;      // K3 GEMM output block (gate rows x input features)
 constexpr int kGChunk = 256;          // row-store rows staged per round
 constexpr int kGBuf = 3;              // staging ring depth, maximum (ring - 1 chunks in flight; the
@@ -113,8 +114,7 @@ __device__ __forceinline__ void dw_umma_block(StateDev<float>& st, const PlanDev
 // Returns the thread's squared-gradient and penalty partials.
 template <typename Real, int SC>
 __device__ __forceinline__ void es_block_fp32(StateDev<Real>& st, const PlanDev& pl, const NetLayout& lay, int s,
-                                              unsigned char* smem_raw, double& sq, double& pen, int bid) {
-    constexpr int bd = kEsSlots32;
+                                              unsigned char* smem_raw, double& sq, double& pen, int bid, int bd) {
     const int tid = threadIdx.x;
     auto clk = [&](int i) {
         if (st.dbg_clk && bid == 0 && tid == 0) st.dbg_clk[32 + i] = clock64();
@@ -147,8 +147,8 @@ __device__ __forceinline__ void es_block_fp32(StateDev<Real>& st, const PlanDev&
     CR* SEr = LVr + bd * ldl;                        //           [bd][lds] forward seasonalities
     Real* PRM = reinterpret_cast<Real*>(SEr + bd * lds);  //      [bd][2+S] raw parameters
     double* cbuf = reinterpret_cast<double*>(X);     // post-wait: [kEsChunk][cwp] contribution rows
-    __shared__ int woff[bd + 1];
-    __shared__ double coef[3][bd];  // alpha, gamma, l[-1] (double)
+    __shared__ int woff[kEsSlots32 + 1];
+    __shared__ double coef[3][kEsSlots32];  // alpha, gamma, l[-1] (double)
     const int slot = sl0 + tid;
     const bool mine = tid < nsl;
     clk(1);
@@ -231,8 +231,9 @@ __device__ __forceinline__ void es_block_fp32(StateDev<Real>& st, const PlanDev&
     // ---- pre-wait: the recursion's coefficients, [t][bd] (l' = l[t-1], l[-1] = mean y[0:S])
     //   K1 = alpha y / s^2, K2 = gamma y / l'^2, CA = y / s - l', CG = y / l' - s, RS = 1/s, RI = 1/l
     // double for S = 1, else the correctly rounded fp32 reciprocals of the fp32 states
+    const int bsh = bd == 16 ? 4 : 3;  // bd is 8 or 16
     for (int e = tid; e < T * bd; e += kFinishThreads) {
-        const int t = e / bd, sl = e - t * bd;
+        const int t = e >> bsh, sl = e - (t << bsh);
         if (sl >= nsl) continue;
         const double y = static_cast<double>(YS[sl * tp + t]);
         const CR lvc = LVr[sl * ldl + t], svc = SEr[sl * lds + t];
@@ -388,7 +389,7 @@ __device__ __forceinline__ void es_block_fp32(StateDev<Real>& st, const PlanDev&
 template <typename Real, int SC, bool UMMA>
 __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> st, PlanDev pl, NetLayout lay, int s,
                                                                 int es_blocks, int finalize, int gsplit,
-                                                                int umma_parts_arg, int nring) {
+                                                                int umma_parts_arg, int nring, int es_bd) {
     const int umma_parts = UMMA ? umma_parts_arg : 0;
     using M = Math<Real>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -416,7 +417,7 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
                                                                            : static_cast<int>(blockIdx.x) - ngemm)
                                    : static_cast<int>(blockIdx.x);
     if (bid < es_blocks && sizeof(Real) == 4) {
-        if constexpr (sizeof(Real) == 4) es_block_fp32<Real, SC>(st, pl, lay, s, smem_raw, sq, pen, bid);
+        if constexpr (sizeof(Real) == 4) es_block_fp32<Real, SC>(st, pl, lay, s, smem_raw, sq, pen, bid, es_bd);
         const double tot = block_sum(sq, red);
         if (tid == 0) st.es_sq_part[bid] = tot;
         if (st.lvp > 0.0) {
