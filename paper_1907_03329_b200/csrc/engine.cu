@@ -1704,6 +1704,10 @@ double train_epoch_impl(Eng* e) {
                 const long long a = sp[(static_cast<size_t>(s) * kSpanKinds + k) * 2];
                 const long long b = sp[(static_cast<size_t>(s) * kSpanKinds + k) * 2 + 1];
                 if (a == LLONG_MAX || b < a) continue;
+                static const bool dump = std::getenv("ESRNN_SPAN_DUMP") != nullptr;
+                if (dump)
+                    std::fprintf(stderr, "[esrnn span] step %d kind %d start %lld len %lld\n", s, k,
+                                 a - sp[0], b - a);
                 e->prof_ms[cls[k]] += (b - a) * 1e-6;
                 e->prof_n[cls[k]] += 1;
             }
