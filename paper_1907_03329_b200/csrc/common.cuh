@@ -47,6 +47,8 @@ struct NetLayout {
     int rs_h[kMaxLayers], rs_pr[kMaxLayers];
     int nmat;                      // L + 2 (layers, nl head, out head)
     int mat_blk0[kMaxMats + 1];    // prefix of K3 GEMM blocks per matrix
+    int mat_wblk0[kMaxMats + 1];   // prefix of K3 q-strip blocks (kWq rows of G) per matrix
+    int wkp_in0, wkp_h;            // q-strip U boxes: in0 / H rounded up to 4 columns
     MatDesc mats[kMaxMats];
 };
 
@@ -106,6 +108,7 @@ struct StateDev {
     Real* gpart;            // [gsplit][tiles][32 lanes][6]: row-part tile partials (large steps)
     unsigned* gtile_ctr;    // [tiles] arrival tickets of a tile's row parts
     int red_tiles;          // K3 weight-gradient output tiles
+    int gemm_wide;          // 1: K3 weight gradients by q-strip blocks (finish.cuh dw_wide_block)
     float* upart;           // [umma tiles][parts][128][64] tensor-core dW partials (fp32, large steps)
     int umma_tiles;         // 128-row matrix slices of the tensor-core dW path
     unsigned int* done_ctr; // [2]

@@ -266,6 +266,7 @@ struct esrnn_trainer {
     DBuf<unsigned int> done_ctr, gtile_ctr;
     DBuf<unsigned char> gpart;
     int gsplit = 1;  // K3 weight-gradient row parts per output tile (large steps)
+    bool wide = false;  // K3 weight gradients by q-strip blocks (finish.cuh dw_wide_block)
     int umma_parts = 0, umma_tiles = 0;  // tensor-core dW path (fp32, steps >= kUmmaMinRows)
     DBuf<unsigned char> upart;
     const double* bc_tab = nullptr;  // process-wide bias-correction table of this GPU (StateDev::bc)
@@ -403,6 +404,7 @@ struct esrnn_trainer {
         s.gpart = reinterpret_cast<Real*>(gpart.p);
         s.gtile_ctr = gtile_ctr.p;
         s.red_tiles = red_blocks;
+        s.gemm_wide = wide ? 1 : 0;
         s.upart = reinterpret_cast<float*>(upart.p);
         s.umma_tiles = umma_tiles;
         s.done_ctr = done_ctr.p;
@@ -657,10 +659,14 @@ void build_layout(Eng* e) {
     lay.mats[lay.L] = MatDesc{lay.rs_zb, H, lay.rs_h[lay.L - 1], H, lay.ldkh, 0, lay.c_nlw, lay.c_nlb};
     lay.mats[lay.L + 1] = MatDesc{lay.rs_pb, O, lay.rs_z, H, lay.ldkh, 0, lay.c_outw, lay.c_outb};
     lay.mat_blk0[0] = 0;
+    lay.mat_wblk0[0] = 0;
     for (int m = 0; m < lay.nmat; ++m) {
         const MatDesc& d = lay.mats[m];
         lay.mat_blk0[m + 1] = lay.mat_blk0[m] + ((d.Q + kGq - 1) / kGq) * ((d.K + kGk - 1) / kGk);
+        lay.mat_wblk0[m + 1] = lay.mat_wblk0[m] + (d.Q + kWq - 1) / kWq;
     }
+    lay.wkp_in0 = (lay.layer_in[0] + 3) & ~3;
+    lay.wkp_h = (H + 3) & ~3;
 }
 
 // ------------------------------------------------------------------ conversions
@@ -737,10 +743,7 @@ void ensure_capacity(Eng* e, int B) {
         e->es_bd = std::atoi(v);
     const int es_slots = e->es_bd;
     e->es_blocks = (kc + es_slots - 1) / es_slots;
-    // Row parts per weight-gradient tile: at B <= 4,096 one block per tile is fastest (a
-    // two-part split measured +6.8 us at cfg1); beyond, one part per 4,096 rows (<= 16)
-    e->gsplit = std::max(1, std::min(16, B / 4096));
-    e->gpart.alloc(e->rsz * static_cast<size_t>(e->gsplit) * std::max(e->red_blocks, 1) * 32 * 6);
+
     // tensor-core weight gradients (umma.cuh, finish.cuh dw_umma_block): fp32 steps of at
     // least kUmmaMinRows windows, every matrix's K + 1 within the 64-column N tile;
     // two blocks per SM over the matrices' 128-row tiles, parts of >= 256 rows
@@ -761,6 +764,27 @@ void ensure_capacity(Eng* e, int B) {
         } else {
             e->umma_tiles = 0;
         }
+    }
+    // weight-gradient contraction without the tensor cores: the 16 x 8 output tiles.  The
+    // q-strip blocks (finish.cuh dw_wide_block: each row-store row read once per 32 rows of G,
+    // parts combined in order by the last to arrive) are opt-in, ESRNN_GEMM_WIDE=1: measured
+    // slower (cfg1 1.60 -> 2.70 ms, cfg3 52.7 -> 66.7 ms per epoch + validate; the last part's
+    // combine serialises its loads behind its stores, and a part's publish + ticket costs more
+    // than the re-reads it saves at these row counts)
+    e->wide = false;
+    if (!e->fp64 && e->umma_parts == 0 && std::max(e->lay.wkp_in0, e->lay.wkp_h) <= kWkMax) {
+        const char* v = std::getenv("ESRNN_GEMM_WIDE");
+        e->wide = v && std::atoi(v) == 1;
+    }
+    e->red_blocks = e->wide ? e->lay.mat_wblk0[e->lay.nmat] : e->lay.mat_blk0[e->lay.nmat];
+    if (e->wide) {
+        e->gsplit = std::max(1, std::min(8, B / 128));
+        e->gpart.alloc(e->rsz * static_cast<size_t>(e->gsplit) * std::max(e->red_blocks, 1) * kWq * (kWkMax + 1));
+    } else {
+        // Row parts per 16 x 8 tile: at B <= 4,096 one block per tile is fastest (a two-part
+        // split measured +6.8 us at cfg1); beyond, one part per 4,096 rows (<= 16)
+        e->gsplit = std::max(1, std::min(16, B / 4096));
+        e->gpart.alloc(e->rsz * static_cast<size_t>(e->gsplit) * std::max(e->red_blocks, 1) * 32 * 6);
     }
     const int ctr_n = std::max({e->red_blocks, e->umma_tiles, 1});
     if (e->gtile_ctr.n < static_cast<size_t>(ctr_n)) {
@@ -941,7 +965,7 @@ bool stack_resident(const NetLayout& lay) {
 int stack_threads(const NetLayout& lay) { return tile_threads(lay); }
 
 template <typename Real>
-size_t finish_smem(const NetLayout& lay, int ring = kGBuf, int es_bd = kEsSlots32) {
+size_t finish_smem(const NetLayout& lay, int ring = kGBuf, int es_bd = kEsSlots32, bool wide = false) {
     // ES blocks: level / seasonality adjoints [bd][T|1], [bd][(T+S)|1], forward l and s
     // columns [T][bd] (double), one staged observation row per slot (Real), one chunk of
     // staged contribution rows (double)
@@ -958,7 +982,8 @@ size_t finish_smem(const NetLayout& lay, int ring = kGBuf, int es_bd = kEsSlots3
                                         sizeof(double) * kEsChunk * cwp);
         const size_t es = sizeof(double) * bd * (ldl + lds) + 6 * T * bd * cr + sizeof(double) * bd * S + scratch;
         const size_t gemm = sizeof(Real) * (static_cast<size_t>(ring * kGChunk) * (kGq + kGk) + (kFinishThreads / 32) * 32 * 6);
-        return std::max(es, gemm);
+        const size_t wgemm = sizeof(float) * ring * kWr * static_cast<size_t>(kWq + std::max(lay.wkp_in0, lay.wkp_h));
+        return std::max(es, wide ? wgemm : gemm);
     }
     const size_t cwp = (lay.I + lay.O + 2 + 3) & ~3;
     const size_t bd = kEsSlotsPerBlock;
@@ -993,13 +1018,15 @@ void encode_rowstore_maps(Eng* e, int rsz) {
         if (q != cudaDriverEntryPointSuccess || !fn) raise(ESRNN_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
         return reinterpret_cast<TensorMapEncodeFn>(fn);
     }();
-    alignas(64) CUtensorMap maps[2];
+    alignas(64) CUtensorMap maps[5];  // 16 x 8 tiles: A, U; q-strips: A, U (in0), U (H)
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(e->lay.rs_ld), static_cast<cuuint64_t>(e->tiles_cap) * kRows};
     const cuuint64_t strides[1] = {static_cast<cuuint64_t>(e->lay.rs_ld) * rsz};
     const cuuint32_t estr[2] = {1, 1};
     const CUtensorMapDataType dt = rsz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
-    for (int i = 0; i < 2; ++i) {
-        const cuuint32_t box[2] = {static_cast<cuuint32_t>(i == 0 ? kGq : kGk), static_cast<cuuint32_t>(kGChunk)};
+    for (int i = 0; i < 5; ++i) {
+        const int bx = i == 0 ? kGq : i == 1 ? kGk : i == 2 ? kWq : i == 3 ? e->lay.wkp_in0 : e->lay.wkp_h;
+        const cuuint32_t box[2] = {static_cast<cuuint32_t>(std::min(bx, 256)),
+                                   static_cast<cuuint32_t>(i < 2 ? kGChunk : kWr)};
         const CUresult r = enc(&maps[i], dt, 2, e->rowstore.p, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -1114,7 +1141,8 @@ void launch_finish_sc(Eng* e, const StateDev<Real>& st, const PlanDev& pv, int s
                  e->umma_parts, 3, bd);
     else
         launch_k(e, pdl, k_grad_finish<Real, SC, false>, e->es_blocks + gemm_blocks, kFinishThreads,
-                 finish_smem<Real>(e->lay, ring, bd), st, pv, e->lay, s, e->es_blocks, finalize, e->gsplit, 0, ring, bd);
+                 finish_smem<Real>(e->lay, ring, bd, e->wide), st, pv, e->lay, s, e->es_blocks, finalize, e->gsplit, 0,
+                 ring, bd);
 }
 template <typename Real>
 void launch_finish(Eng* e, const StateDev<Real>& st, const PlanDev& pv, int s, int finalize, bool pdl = false) {

@@ -21,6 +21,8 @@ constexpr int kEsSlots32 = 16;        // fp32 ES blocks (es_block_fp32): at most
 constexpr int kEsChunk = 64;          // contribution rows staged per round (64: K3 fits four blocks per SM at Monthly)
 constexpr int kGq = 16, kGk = 8;      // K3 GEMM output block (gate rows x input features)
 constexpr int kGChunk = 256;          // row-store rows staged per round
+constexpr int kWq = 32, kWr = 64;      // q-strip GEMM: G rows per block, row-store rows per chunk
+constexpr int kWkMax = 64;             // q-strip GEMM: K (+ padding) at most (else the 16 x 8 tiles)
 constexpr int kGBuf = 3;              // staging ring depth, maximum (ring - 1 chunks in flight; the
                                       // launch picks 3 or 2, engine.cu finish_ring)
 // fp32 mode with S = 1: K3's ES blocks recompute the forward states in double (see there)
@@ -384,6 +386,156 @@ __device__ __forceinline__ void es_block_fp32(StateDev<Real>& st, const PlanDev&
     clk(9);
 }
 
+// ---------------------------------------------------------------------------------------
+// K3 weight gradients by q-strips (fp32): block gbp = (strip, part), strip = kWq rows q of one
+// matrix's G = A^T U over ALL its K columns, part = a contiguous range of the step's rows.
+// Each row-store row is read once per strip (the 16 x 8 tiles read A K/8 times and U Q/16
+// times: 15.7 MB of L2 reads per cfg1 step, 57 MB at cfg3), chunks of kWr rows by two TMA
+// tensor copies.  Thread t owns G[4 qq .. 4 qq + 3][2 kk, 2 kk + 1] (qq = t % 8, kk = t / 8)
+// and the bias sums of its 4 rows (kk == 0), summing its part's rows in order; parts are
+// combined in part order by the last part to arrive (ticket) -- fixed order, no atomics on
+// values.  Returns this thread's squared-gradient contribution (writer block only).
+__device__ __forceinline__ double dw_wide_block(StateDev<float>& st, const PlanDev& pl, const NetLayout& lay, int s,
+                                               int gbp, int gsplit, unsigned char* smem_raw, int nring,
+                                               bool& writer) {
+    const int tid = threadIdx.x;
+    writer = true;
+    const int gb = gbp / gsplit, part = gbp - gb * gsplit;
+    int m = 0;
+    while (m + 1 < lay.nmat && gb >= lay.mat_wblk0[m + 1]) ++m;
+    const MatDesc md = lay.mats[m];
+    const int q0 = (gb - lay.mat_wblk0[m]) * kWq;
+    const bool uin0 = md.K == lay.layer_in[0] && m == 0;
+    const int kp = uin0 ? lay.wkp_in0 : lay.wkp_h;  // U box columns
+    const int wb0 = pl.step_win_off[s];
+    const int Bstep = pl.step_win_off[s + 1] - wb0;
+    const int span = ((Bstep + gsplit - 1) / gsplit + kWr - 1) / kWr * kWr;
+    const int r0 = min(Bstep, part * span);
+    const int Bl = min(Bstep, r0 + span) - r0;
+    const int nch = (Bl + kWr - 1) / kWr;
+    const int kmax = max(lay.wkp_in0, lay.wkp_h);
+    float* As = reinterpret_cast<float*>(smem_raw);  // [nring][kWr][kWq]
+    float* Us = As + nring * kWr * kWq;              // [nring][kWr][kp] (buffer stride kmax)
+    __shared__ __align__(8) uint64_t wbar[kGBuf];
+    __shared__ bool wlast;
+    if (tid == 0)
+        for (int b = 0; b < nring; ++b) mbar_init(&wbar[b], 1);
+    __syncthreads();
+    const unsigned char* tmb = static_cast<const unsigned char*>(st.tm_rs);
+    const void* tmA = tmb + 2 * 128;
+    const void* tmU = tmb + (uin0 ? 3 : 4) * 128;
+    auto stage = [&](int c) {
+        if (tid != 0 || c >= nch) return;
+        const int buf = c % nring;
+        fence_proxy_async_smem();
+        mbar_expect_tx(&wbar[buf], static_cast<unsigned>(sizeof(float) * kWr * (kWq + kp)));
+        tma2d_g2s(As + buf * kWr * kWq, tmA, md.a_off + q0, r0 + c * kWr, &wbar[buf]);
+        tma2d_g2s(Us + buf * kWr * kmax, tmU, md.u_off, r0 + c * kWr, &wbar[buf]);
+    };
+    const int qq = tid & 7, kk = tid >> 3;
+    const bool act = 2 * kk < kp;  // compute threads (kk == 0 also forms the bias sums)
+    float acc[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}}, bacc[4] = {0, 0, 0, 0};
+    for (int c = 0; c < nring - 1; ++c) stage(c);
+    for (int c = 0; c < nch; ++c) {
+        stage(c + nring - 1);
+        mbar_wait(&wbar[c % nring], static_cast<unsigned>((c / nring) & 1));
+        const int nb = min(kWr, Bl - c * kWr);
+        const float* Ab = As + (c % nring) * kWr * kWq + 4 * qq;
+        const float* Ub = Us + (c % nring) * kWr * kmax + 2 * kk;
+        if (act) {
+#pragma unroll 4
+            for (int b = 0; b < nb; ++b) {
+                const float4 a = *reinterpret_cast<const float4*>(Ab + b * kWq);
+                const float2 u = *reinterpret_cast<const float2*>(Ub + b * kp);
+                // paired FMAs (FFMA2): bit-identical to the scalar form
+                asm("{ .reg .b64 p0, p1, p2, p3, u, a0, a1, a2, a3;\n\t"
+                    "mov.b64 u, {%8, %9};\n\t"
+                    "mov.b64 a0, {%10, %10};\n\t"
+                    "mov.b64 a1, {%11, %11};\n\t"
+                    "mov.b64 a2, {%12, %12};\n\t"
+                    "mov.b64 a3, {%13, %13};\n\t"
+                    "mov.b64 p0, {%0, %1};\n\t"
+                    "mov.b64 p1, {%2, %3};\n\t"
+                    "mov.b64 p2, {%4, %5};\n\t"
+                    "mov.b64 p3, {%6, %7};\n\t"
+                    "fma.rn.f32x2 p0, a0, u, p0;\n\t"
+                    "fma.rn.f32x2 p1, a1, u, p1;\n\t"
+                    "fma.rn.f32x2 p2, a2, u, p2;\n\t"
+                    "fma.rn.f32x2 p3, a3, u, p3;\n\t"
+                    "mov.b64 {%0, %1}, p0;\n\t"
+                    "mov.b64 {%2, %3}, p1;\n\t"
+                    "mov.b64 {%4, %5}, p2;\n\t"
+                    "mov.b64 {%6, %7}, p3; }"
+                    : "+f"(acc[0][0]), "+f"(acc[0][1]), "+f"(acc[1][0]), "+f"(acc[1][1]), "+f"(acc[2][0]),
+                      "+f"(acc[2][1]), "+f"(acc[3][0]), "+f"(acc[3][1])
+                    : "f"(u.x), "f"(u.y), "f"(a.x), "f"(a.y), "f"(a.z), "f"(a.w));
+                if (kk == 0) {
+                    bacc[0] += a.x;
+                    bacc[1] += a.y;
+                    bacc[2] += a.z;
+                    bacc[3] += a.w;
+                }
+            }
+        }
+        __syncthreads();  // buffer c % nring is restaged next round
+    }
+    // this part's strip: [kWq][kWkMax + 1] (column kWkMax: bias), parts combined in order
+    constexpr int ld = kWkMax + 1;
+    double sq = 0.0;
+    auto emit = [&](int i, int j, float g) {  // G[q0 + 4 qq + i][2 kk + j] (j == 2: bias)
+        const int q = q0 + 4 * qq + i;
+        if (q >= md.Q) return;
+        if (j < 2) {
+            const int k = 2 * kk + j;
+            if (k >= md.K) return;
+            st.gbuf[md.cw + (long long)q * md.ldk + k] = g;
+        } else {
+            st.gbuf[md.cb + q] = g;
+        }
+        sq += static_cast<double>(g) * g;
+    };
+    if (gsplit == 1) {
+        if (act)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                emit(i, 0, acc[i][0]);
+                emit(i, 1, acc[i][1]);
+                if (kk == 0) emit(i, 2, bacc[i]);
+            }
+        return sq;
+    }
+    float* mine = st.gpart + ((size_t)gb * gsplit + part) * kWq * ld;
+    if (act)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            mine[(4 * qq + i) * ld + 2 * kk] = acc[i][0];
+            mine[(4 * qq + i) * ld + 2 * kk + 1] = acc[i][1];
+            if (kk == 0) mine[(4 * qq + i) * ld + kWkMax] = bacc[i];
+        }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) wlast = atomicAdd(st.gtile_ctr + gb, 1u) == static_cast<unsigned>(gsplit - 1);
+    __syncthreads();
+    writer = wlast;
+    if (!wlast) return 0.0;
+    __threadfence();
+    if (tid == 0) st.gtile_ctr[gb] = 0;
+    if (act) {
+        const float* base = st.gpart + (size_t)gb * gsplit * kWq * ld;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                if (j == 2 && kk != 0) continue;
+                const int col = j < 2 ? 2 * kk + j : kWkMax;
+                float g = 0.f;
+                for (int p = 0; p < gsplit; ++p) g += __ldcg(base + (size_t)p * kWq * ld + (4 * qq + i) * ld + col);
+                emit(i, j, g);
+            }
+    }
+    return sq;
+}
+
 // UMMA: the tensor-core weight-gradient instantiation (large fp32 steps); the small-step
 // kernel is compiled without that code (it changes the ES path's register allocation)
 template <typename Real, int SC, bool UMMA>
@@ -662,6 +814,17 @@ __global__ void __launch_bounds__(kFinishThreads) k_grad_finish(StateDev<Real> s
         pdl_wait();
         SPAN_BEGIN(st, s, kSpanFinish);
         if constexpr (UMMA && sizeof(Real) == 4) dw_umma_block(st, pl, lay, s, bid - es_blocks, umma_parts, smem_raw, red);
+    } else if (sizeof(Real) == 4 && st.gemm_wide) {
+        pdl_wait();
+        SPAN_BEGIN(st, s, kSpanFinish);
+        DBG_K3(st, s, bid, 0);
+        if constexpr (sizeof(Real) == 4) {
+            const int gbp = bid - es_blocks;
+            bool writer = true;
+            sq = dw_wide_block(st, pl, lay, s, gbp, gsplit, smem_raw, nring, writer);
+            const double tot = block_sum(sq, red);
+            if (tid == 0 && writer) st.red_sq_part[gbp / gsplit] = tot;
+        }
     } else {
         pdl_wait();
         SPAN_BEGIN(st, s, kSpanFinish);
