@@ -264,7 +264,7 @@ def test_sharded_partials_sum_to_full_batch(engine, oracle, world, precision):
     """Series-sharded ranks on one GPU (local-partials mode: the data path of every rank
     runs, the collective is summed here): the per-rank partial loss / shared gradients add
     up to the single-GPU step; per-series gradients stay with their owner."""
-    from paper_1907_03329_b200.sharding import LOCAL_PARTIALS_ID, shard_range
+    from sharding_helpers import LOCAL_PARTIALS_ID, shard_range
     prof, vals, cats = dataset(oracle, "monthly", 10, 4)
     cfg = TrainConfig(seed=7, batch_size=64, precision=precision)
     full = Trainer((vals, cats), prof, cfg, api=engine)

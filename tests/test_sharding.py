@@ -22,7 +22,7 @@ ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 sys.path.insert(0, str(ROOT / "tests"))
 
-from paper_1907_03329_b200.sharding import local_windows, shard_range, slots_first_appearance  # noqa: E402
+from sharding_helpers import local_windows, shard_range, slots_first_appearance  # noqa: E402
 
 
 def _free_port():
