@@ -950,6 +950,12 @@ template <typename Real>
 size_t stack_smem(const NetLayout& lay, bool resident) {
     return sizeof(Real) * TileSmem::make<Real>(lay, resident).total;
 }
+// two tiles per CTA sharing the resident weights (k_tile<..., NG = 2>)
+template <typename Real>
+size_t stack_smem2(const NetLayout& lay) {
+    const TileSmem t = TileSmem::make<Real>(lay, true);
+    return sizeof(Real) * (static_cast<size_t>(t.total) + (t.total - t.wsize));
+}
 
 // Resident mode keeps every live weight in shared memory for the whole tile (one TMA
 // bulk copy); larger fp64 networks stage one layer at a time.
@@ -1061,6 +1067,13 @@ void set_tile_attr(const NetLayout& lay) {
     CUDA_OK(cudaFuncSetAttribute(k_tile<Real, MODE, false, SC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)stack_smem<Real>(lay, false)));
     max_carveout(k_tile<Real, MODE, false, SC>);
+    if constexpr (sizeof(Real) == 4 && MODE != kForecast) {
+        if (stack_resident<Real>(lay) && stack_smem2<Real>(lay) + 1024 <= static_cast<size_t>(g_smem_optin)) {
+            CUDA_OK(cudaFuncSetAttribute(k_tile<Real, MODE, true, SC, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)stack_smem2<Real>(lay)));
+            max_carveout(k_tile<Real, MODE, true, SC, 2>);
+        }
+    }
 }
 
 template <typename Real, int SC>
@@ -1166,6 +1179,18 @@ void launch_tile_sc(Eng* e, int grid, const StateDev<Real>& st, const PlanDev& p
                                                                        : 2 * g_num_sms;
     const bool two_waves = sizeof(Real) == 4 && grid >= stage_min &&
                            2 * (stack_smem<Real>(lay, false) + 1024) <= static_cast<size_t>(g_smem_per_sm);
+    if constexpr (sizeof(Real) == 4 && MODE != kForecast) {
+        // more than one wave at one resident tile per SM: two tiles per CTA on one weight copy
+        // when they fit (ESRNN_TILE_G2=0 disables)
+        const char* g2v = std::getenv("ESRNN_TILE_G2");  // read per launch (graph capture / eager steps)
+        const bool g2_off = g2v && std::atoi(g2v) == 0;
+        if (!g2_off && stack_resident<Real>(lay) && grid > g_num_sms && 2 * nt <= 768 &&
+            stack_smem2<Real>(lay) + 1024 <= static_cast<size_t>(g_smem_optin)) {
+            launch_k(e, pdl, k_tile<Real, MODE, true, SC, 2>, (grid + 1) / 2, 2 * nt, stack_smem2<Real>(lay), st, pv,
+                     lay, s, fa);
+            return;
+        }
+    }
     if (stack_resident<Real>(lay) && !two_waves)
         launch_k(e, pdl, k_tile<Real, MODE, true, SC>, grid, nt, stack_smem<Real>(lay, true), st, pv, lay, s, fa);
     else

@@ -326,26 +326,47 @@ __device__ __forceinline__ int hw_scan_row(const Real* __restrict__ ys, const Re
 
 // RESIDENT: all weights in shared memory, one CTA per SM; staged fp32 tiles (weights one
 // layer at a time) fit two CTAs per SM, so their register budget is capped accordingly.
-template <typename Real, int MODE, bool RESIDENT, int SC>
-__global__ void __launch_bounds__((RESIDENT || sizeof(Real) == 8) ? 512 : 384, (RESIDENT || sizeof(Real) == 8) ? 1 : 2) k_tile(StateDev<Real> st, PlanDev pl, NetLayout lay_p, int s, ForecastArgs fa) {
+// NG = 2 (fp32, resident): two tiles per CTA, one group of warps each, sharing ONE resident copy
+// of the weights (one TMA copy per CTA); each group synchronises on its own named barrier.
+// Two Quarterly tiles fit one SM this way (77 KB of weights + 2 x 56 KB) where two CTAs of one
+// tile each (2 x 133 KB) do not, so multi-wave steps run two tiles per SM without the staged
+// variant's per-layer weight copies.
+template <typename Real, int MODE, bool RESIDENT, int SC, int NG = 1>
+__global__ void __launch_bounds__(NG == 2 ? 768 : ((RESIDENT || sizeof(Real) == 8) ? 512 : 384),
+                                  (NG == 2 || RESIDENT || sizeof(Real) == 8) ? 1 : 2)
+    k_tile(StateDev<Real> st, PlanDev pl, NetLayout lay_p, int s, ForecastArgs fa) {
     using M = Math<Real>;
     constexpr int R = kR, LD = ldr<Real>();
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    Real* sm = reinterpret_cast<Real*>(smem_raw);
-    __shared__ double red[32];
+    __shared__ double red_all[NG][32];
     __shared__ __align__(8) uint64_t wbar;
     __shared__ NetLayout lay_s;  // read with dynamic layer indices in every phase
-    if (threadIdx.x == 0) lay_s = lay_p;
+    if (threadIdx.x == 0) {
+        lay_s = lay_p;
+        if (NG > 1 && RESIDENT) mbar_init(&wbar, 1);  // before any group can wait on it
+    }
     __syncthreads();
     const NetLayout& lay = lay_s;
-    const int tid = threadIdx.x, NT = blockDim.x, lane = tid & 31, warp = tid >> 5, NW = NT >> 5;
+    const int NT = static_cast<int>(blockDim.x) / NG, grp = static_cast<int>(threadIdx.x) / NT;
+    const int tid = static_cast<int>(threadIdx.x) - grp * NT, lane = tid & 31, warp = tid >> 5, NW = NT >> 5;
+    double* red = red_all[grp];
+    // the group's barrier (named barrier 1 + grp over its NT threads); the whole CTA for NG = 1
+    auto gsync = [&]() {
+        if constexpr (NG == 1) {
+            __syncthreads();
+        } else {
+            asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(NT) : "memory");
+        }
+    };
     const TileSmem ts = TileSmem::make<Real>(lay, RESIDENT);
     const int H = lay.H, O = lay.O, I = lay.I, in0 = lay.in0, L = lay.L, G = 3 * H;
     const int ldo = lay.ldo, ldkh = lay.ldkh;
-    const int tile = blockIdx.x;
+    const int tile = static_cast<int>(blockIdx.x) * NG + grp;
     const Real* __restrict__ th = st.theta;
+    Real* smw = reinterpret_cast<Real*>(smem_raw);
+    Real* sm = smw + grp * (ts.total - ts.wsize);  // this group's tile region (offsets past the weights)
 
-    Real* wsm = sm + ts.w;
+    Real* wsm = smw + ts.w;
     Real* XT = sm + ts.xt;
     Real* HT = sm + ts.ht;
     Real* GT = sm + ts.gt;
@@ -380,7 +401,8 @@ __global__ void __launch_bounds__((RESIDENT || sizeof(Real) == 8) ? 512 : 384, (
     // the tile's windows' plan entries (epoch constants), one load per thread, all in flight:
     // series row, anchor, publishing slot (-1 unless the window is its slot's first), CSR
     // position, category
-    __shared__ int w_info[5][kR];
+    __shared__ int w_info_all[NG][5][kR];
+    auto& w_info = w_info_all[grp];
     if (MODE != kForecast) {
         if (tid < 4 * R) {
             const int q = tid / R, r = tid - q * R;
@@ -394,7 +416,7 @@ __global__ void __launch_bounds__((RESIDENT || sizeof(Real) == 8) ? 512 : 384, (
             }
             w_info[q][r] = v;
         }
-        __syncthreads();
+        gsync();
         if (tid < nrows) w_info[4][tid] = st.cat[w_info[0][tid]];
     }
     const int* w_rowv = w_info[0];
@@ -405,8 +427,8 @@ __global__ void __launch_bounds__((RESIDENT || sizeof(Real) == 8) ? 512 : 384, (
     // ---- weights: TMA bulk copy of the compact parameter vector (resident mode), issued
     // once the previous step's Adam has completed (after pdl_wait) ----
     auto weights_tma = [&]() {
-        if (!(RESIDENT && tid == 0)) return;
-        mbar_init(&wbar, 1);
+        if (!(RESIDENT && tid == 0 && grp == 0)) return;
+        if (NG == 1) mbar_init(&wbar, 1);
         const unsigned total = static_cast<unsigned>(lay.P_pad * sizeof(Real));
         mbar_expect_tx(&wbar, total);
         constexpr unsigned kChunk = 32768;
@@ -450,7 +472,7 @@ __global__ void __launch_bounds__((RESIDENT || sizeof(Real) == 8) ? 512 : 384, (
             cp_async_elem(PSM + r * np + c, st.ps + (size_t)c * st.N + w_rowv[r]);
         }
         cp_async_wait_all();
-        __syncthreads();
+        gsync();
         DBG_CLK(st, 0);
         // the tile holding a slot's first window (batch order) publishes the slot's states
         const int* pub_slot = w_info[2];
@@ -460,7 +482,7 @@ __global__ void __launch_bounds__((RESIDENT || sizeof(Real) == 8) ? 512 : 384, (
             if (bad != INT_MAX) flag_error(st.err, kErrTrainLevel, bad);
         }
         DBG_CLK(st, 0);
-        __syncthreads();
+        gsync();
         // published states for K3's fp64 reverse scan: lv [T][kcap], se [T+S][kcap] (fp32:
         // K3's ES blocks rerun this scan themselves before their dependency wait,
         // finish.cuh es_block_fp32)
@@ -539,7 +561,7 @@ __global__ void __launch_bounds__((RESIDENT || sizeof(Real) == 8) ? 512 : 384, (
             }
         }
     }
-    __syncthreads();
+    gsync();
     DBG_CLK(st, 1);
     if (MODE != kForecast && st.d_inputs != nullptr) {
         const int base = tile * R;
@@ -562,7 +584,7 @@ __global__ void __launch_bounds__((RESIDENT || sizeof(Real) == 8) ? 512 : 384, (
         const Real* U = l == 0 ? XT : HT + (l - 1) * H * LD;
         if (!RESIDENT) {
             stage_segment(wsm, th + lay.cw[l], lay.cb[l] - lay.cw[l] + G);
-            __syncthreads();
+            gsync();
         }
         const Real* WT = RESIDENT ? wsm + lay.cw[l] : wsm;
         const Real* bias = RESIDENT ? wsm + lay.cb[l] : wsm + (lay.cb[l] - lay.cw[l]);
@@ -593,14 +615,14 @@ __global__ void __launch_bounds__((RESIDENT || sizeof(Real) == 8) ? 512 : 384, (
                 if (rs && rf < nrows) rs[rf * lay.rs_ld + lay.rs_h[l] + hh] = h;
             }
         }
-        __syncthreads();
+        gsync();
         DBG_CLK(st, 2);
     }
     // head (network.hpp:207-209): z = tanh(h nl_w + nl_b); pred = z out_w + out_b
     const Real* cur = HT + (L - 1) * H * LD;
     if (!RESIDENT) {
         stage_segment(wsm, th + lay.c_nlw, lay.P_pad - lay.c_nlw);
-        __syncthreads();
+        gsync();
     }
     const long long hb0 = RESIDENT ? 0 : lay.c_nlw;
     const Real* nlwT = wsm + (lay.c_nlw - hb0);
@@ -619,7 +641,7 @@ __global__ void __launch_bounds__((RESIDENT || sizeof(Real) == 8) ? 512 : 384, (
             if (rs && rf < nrows) rs[rf * lay.rs_ld + lay.rs_z + hh] = z;
         }
     }
-    __syncthreads();
+    gsync();
     // adapter output, fused with the masked pinball (autodiff.hpp:384-392) and its adjoint
     // (:620-626): the lane owning (output oo, row rf) forms its loss term and pred_bar
     double lsum = 0.0;
@@ -654,7 +676,7 @@ __global__ void __launch_bounds__((RESIDENT || sizeof(Real) == 8) ? 512 : 384, (
         for (int o = 16; o > 0; o >>= 1) lsum += __shfl_down_sync(0xffffffffu, lsum, o);
         if (lane == 0) red[warp] = lsum;
     }
-    __syncthreads();
+    gsync();
     DBG_CLK(st, 3);
     if (MODE == kForecast) {
         for (int e = tid; e < nrows * O; e += NT) {
@@ -662,7 +684,7 @@ __global__ void __launch_bounds__((RESIDENT || sizeof(Real) == 8) ? 512 : 384, (
             fa.out[(size_t)(tile * R + r) * O + o] = static_cast<double>(PT[o * LD + r] * lvl[r] * s_out[r * ldo + o]);
         }
         if (fa.validate) {
-            __syncthreads();
+            gsync();
             // sMAPE (metrics.hpp:17-28) and MASE (:33-49) against the held-out block
             // y[t_ins : t_ins+O) (validate: the validation block; evaluate: the test block)
             for (int r = tid; r < nrows; r += NT) {
@@ -707,7 +729,7 @@ __global__ void __launch_bounds__((RESIDENT || sizeof(Real) == 8) ? 512 : 384, (
             if (rs && r < nrows) rs[r * lay.rs_ld + lay.rs_zb + k] = zb;
         }
     }
-    __syncthreads();
+    gsync();
     DBG_CLK(st, 5);
     // h_bar of layer l comes from the product of the layer above (or the head); the lane that
     // owns (row, unit) forms the gate adjoints of layer l right away
@@ -751,17 +773,17 @@ __global__ void __launch_bounds__((RESIDENT || sizeof(Real) == 8) ? 512 : 384, (
         if (l < 0) break;
         // next product: layer l's input adjoint through W^T_l
         if (!RESIDENT) {
-            __syncthreads();
+            gsync();
             stage_segment(wsm, th + lay.cw[l], lay.cb[l] - lay.cw[l]);
         }
-        __syncthreads();
+        gsync();
         DBG_CLK(st, 6);
         AT = PR;
         WA = RESIDENT ? wsm + lay.cw[l] : wsm;
         lda = lay.ldk[l];
         QA = G;
     }
-    __syncthreads();
+    gsync();
     DBG_CLK(st, 7);
 
     // ---- ES adjoint contributions per window (Div / Mul / BroadcastCol adjoints) ----

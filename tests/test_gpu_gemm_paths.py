@@ -43,3 +43,20 @@ def test_q_strip_and_tile_gemm_meet_contract_and_agree(engine, oracle, monkeypat
         assert tensor_err(gw.network[k], gt.network[k]) < 1e-5, k
         assert np.array_equal(gw.network[k], gw2.network[k]), k  # fixed summation order
     assert gw.loss == gt.loss
+
+
+def test_two_tile_ctas_are_bit_identical(engine, oracle, monkeypatch):
+    """k_tile<..., NG = 2> (two tiles per CTA on one resident weight copy, chosen for multi-wave
+    fp32 steps) runs the same per-tile arithmetic as one tile per CTA: bit-identical epochs."""
+    prof, vals, cats = dataset(oracle, "quarterly", 400, 29)
+    kw = dict(precision="fp32", batch_size=2048, seed=7, use_graphs=True)
+    out = []
+    for g2 in ("1", "0"):
+        monkeypatch.setenv("ESRNN_TILE_G2", g2)
+        tr = Trainer((vals, cats), prof, TrainConfig(**kw), api=engine)
+        losses = [tr.train_epoch() for _ in range(2)]
+        out.append((losses, tr.weights(), tr.validate().mean_smape))
+    assert out[0][0] == out[1][0]
+    for k in out[0][1]:
+        assert np.array_equal(out[0][1][k], out[1][1][k]), k
+    assert out[0][2] == out[1][2]
