@@ -1184,7 +1184,11 @@ void launch_tile_sc(Eng* e, int grid, const StateDev<Real>& st, const PlanDev& p
         // when they fit (ESRNN_TILE_G2=0 disables)
         const char* g2v = std::getenv("ESRNN_TILE_G2");  // read per launch (graph capture / eager steps)
         const bool g2_off = g2v && std::atoi(g2v) == 0;
-        if (!g2_off && stack_resident<Real>(lay) && grid > g_num_sms && 2 * nt <= 768 &&
+        // only where two one-tile CTAs cannot share an SM (Yearly's can: there NG = 2 measured
+        // 0.94 -> 1.05 ms per cfg2 epoch)
+        const bool two_ctas_fit = 2 * (stack_smem<Real>(lay, true) + 1024) <= static_cast<size_t>(g_smem_per_sm) &&
+                                  2 * nt * 128 <= 65536;
+        if (!g2_off && !two_ctas_fit && stack_resident<Real>(lay) && grid > g_num_sms && 2 * nt <= 768 &&
             stack_smem2<Real>(lay) + 1024 <= static_cast<size_t>(g_smem_optin)) {
             launch_k(e, pdl, k_tile<Real, MODE, true, SC, 2>, (grid + 1) / 2, 2 * nt, stack_smem2<Real>(lay), st, pv,
                      lay, s, fa);
