@@ -196,7 +196,7 @@ __device__ __forceinline__ void es_block_fp32(StateDev<Real>& st, const PlanDev&
             }
         } else {
             // the tile's own scan: states identical to the ones K2 normalised the windows with
-            hw_scan_row<Real, SC>(ys, pr, T, S, LVr + tid * ldl, SEr + tid * lds);
+            hw_scan_row<Real, SC, false>(ys, pr, T, S, LVr + tid * ldl, SEr + tid * lds);  // K2 flags bad levels
             Real l0r = 0;
             for (int j = 0; j < S; ++j) l0r += ys[j];
             l0 = static_cast<double>(l0r / Real(S));

@@ -258,7 +258,9 @@ __device__ __forceinline__ void cell_adjoint(Real hb, Real i, Real g, Real o, Re
 // s_{t+S} = g*y_t/l_{t-1} + (1-g)*s_t.  ys: the staged row; lv[t], se[t] out (shared).
 // SC > 0: the last S seasonalities live in a register ring; SC == 0: se[] is the ring.
 // Returns the first step with a non-positive / non-finite level, INT_MAX if none.
-template <typename Real, int SC>
+// CHECK = false: no level check in the serial loop (K3 reruns the scan K2 already checked;
+// returns INT_MAX).
+template <typename Real, int SC, bool CHECK = true>
 __device__ __forceinline__ int hw_scan_row(const Real* __restrict__ ys, const Real* __restrict__ pr, int T, int S,
                                            Real* __restrict__ lv, Real* __restrict__ se) {
     using M = Math<Real>;
@@ -281,8 +283,10 @@ __device__ __forceinline__ int hw_scan_row(const Real* __restrict__ ys, const Re
         // l depends on l_{t-1} through one FMA; the reciprocals feed steps S later
         auto step = [&](int t, Real& sj, Real yt) {
             const Real l = alpha * (yt * rcp_of(sj)) + oma * lp;
-            const bool ok = (l > Real(0)) & (l <= kMax);
-            bad = min(bad, ok ? INT_MAX : t);
+            if constexpr (CHECK) {
+                const bool ok = (l > Real(0)) & (l <= kMax);
+                bad = min(bad, ok ? INT_MAX : t);
+            }
             sj = gamma * (yt * rcp_of(lp)) + omg * sj;
             se[t + SC] = sj;
             lv[t] = l;
@@ -314,8 +318,10 @@ __device__ __forceinline__ int hw_scan_row(const Real* __restrict__ ys, const Re
             const Real yt = ys[t];
             const Real s_t = se[t];
             const Real l = alpha * fdiv(yt, s_t) + oma * lp;
-            const bool ok = (l > Real(0)) & (l <= kMax);
-            bad = min(bad, ok ? INT_MAX : t);
+            if constexpr (CHECK) {
+                const bool ok = (l > Real(0)) & (l <= kMax);
+                bad = min(bad, ok ? INT_MAX : t);
+            }
             se[t + S] = gamma * fdiv(yt, lp) + omg * s_t;
             lv[t] = l;
             lp = l;
@@ -706,12 +712,17 @@ __global__ void __launch_bounds__(NG == 2 ? 768 : ((RESIDENT || sizeof(Real) == 
         }
         return;
     }
-    if (tid == 0) {
+    // the tile's loss partial (fixed warp order): kLossOnly now; kTrain at the end, by the last
+    // warp (idle in the final per-window phase), off warp 0's backward critical path
+    auto loss_partial = [&]() {
         double ltot = 0.0;
         for (int w = 0; w < NW; ++w) ltot += red[w];
         st.loss_part[tile] = ltot;
+    };
+    if (MODE == kLossOnly) {
+        if (tid == 0) loss_partial();
+        return;
     }
-    if (MODE == kLossOnly) return;
     DBG_CLK(st, 4);
 
     // ---- backward: input adjoints, each fused with the epilogue of the layer below ----
@@ -821,6 +832,7 @@ __global__ void __launch_bounds__(NG == 2 ? 768 : ((RESIDENT || sizeof(Real) == 
             }
         }
     }
+    if (MODE == kTrain && warp == NW - 1 && lane == 0) loss_partial();
     if (MODE == kTrain) DBG_GT(st, 3);
     if (MODE == kTrain) DBG_SPAN_MAX(st, s, 2);
     if (MODE == kTrain) SPAN_END(st, s, kSpanTile);
