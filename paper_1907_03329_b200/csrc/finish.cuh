@@ -1095,13 +1095,11 @@ __global__ void __launch_bounds__(256) k_adam(StateDev<Real> st, PlanDev pl, Net
     __shared__ double red[96];
     __shared__ double sc[3];
     pdl_trigger();
-    pdl_wait();
-    DBG_GT(st, 6);
-    DBG_SPAN_MIN(st, s, 7);
-    SPAN_BEGIN(st, s, kSpanAdam);
     const int tid = threadIdx.x;
-    // this thread's Adam operands first: their L2 latency overlaps the scalar reduction
-    // below.  Network blocks: one live parameter; per-series blocks (trainer.hpp:636-650):
+    // this thread's Adam operands first: m, v and the parameter (no kernel of this step writes
+    // them before this one) before the dependency wait -- under programmatic dependent launch
+    // (ESRNN_K4_PDL) their latency overlaps K3's tail -- then the gradient after it; their L2
+    // latency overlaps the scalar reduction below.  Network blocks: one live parameter; per-series blocks (trainer.hpp:636-650):
     // one (slot, parameter), a slot's 2+S threads in one block so its step counter is read
     // before it is advanced.
     const bool net = static_cast<int>(blockIdx.x) < net_blocks;
@@ -1114,7 +1112,7 @@ __global__ void __launch_bounds__(256) k_adam(StateDev<Real> st, PlanDev pl, Net
     double c1 = 1.0, c2 = 1.0;
     if (net) {
         mine = q < lay.P_pad;
-        if (mine) g0 = st.gbuf[q], m0 = st.mW[q], v0 = st.vW[q], t0 = st.theta[q];
+        if (mine) m0 = st.mW[q], v0 = st.vW[q], t0 = st.theta[q];
     } else if (st.attach) {
         const int spb = static_cast<int>(blockDim.x) / np;
         const int k0 = pl.step_slot_off[s];
@@ -1127,11 +1125,16 @@ __global__ void __launch_bounds__(256) k_adam(StateDev<Real> st, PlanDev pl, Net
             row = pl.slot_row[k0 + slot];
             steps = st.ps_steps[row] + 1;
             e = (size_t)j * N + row;
-            g0 = st.psg[(size_t)slot * np + j], m0 = st.ps_m[e], v0 = st.ps_v[e], t0 = st.ps[e];
+            m0 = st.ps_m[e], v0 = st.ps_v[e], t0 = st.ps[e];
             c1 = bias_c1(st, steps);
             c2 = bias_c2(st, steps);
         }
     }
+    pdl_wait();
+    DBG_GT(st, 6);
+    DBG_SPAN_MIN(st, s, 7);
+    SPAN_BEGIN(st, s, kSpanAdam);
+    if (mine) g0 = net ? st.gbuf[q] : st.psg[(size_t)slot * np + j];
     if (es_blocks >= 0) {
         // single GPU: the step scalars from K3's partials -- clip scale (trainer.hpp:603-615),
         // bias corrections at the step K3 advanced (:617-620), step loss -- with the same
