@@ -708,8 +708,13 @@ class Trainer:
     KERNEL_CLASSES = ("unused0", "tile", "finish", "unused3", "adam", "finalize", "forecast_scan",
                       "forecast_tile")
 
-    def profile_kernels(self, enable: bool) -> None:
-        self._chk(self.api.lib.esrnn_trainer_profile_kernels(self._h, 1 if enable else 0))
+    def profile_kernels(self, mode: int) -> None:
+        """0: off; 1 (or True): per-kernel CUDA events, eager launches without PDL; 2: in-graph
+        global-timer spans of every step's kernels (graph + PDL, the timed configuration)."""
+        mode = int(mode)
+        if mode not in (0, 1, 2):
+            raise ValueError(f"profile_kernels mode must be 0, 1 or 2, got {mode}")
+        self._chk(self.api.lib.esrnn_trainer_profile_kernels(self._h, mode))
 
     def kernel_times(self) -> dict:
         ms = np.zeros(8)
