@@ -34,3 +34,29 @@ def test_time_cpu_all_cores_bound():
     assert 1 <= r["cores"] <= 4  # n // 4 shards at most
     assert r["value"] > 0 and np.isfinite(r["value"])
     assert "not the same training problem" in r["note"]
+
+
+def test_profile_kernels_passes_the_mode_through():
+    """bench.py asks for mode 2 (in-graph spans, PDL on); a bool mapping once turned it into
+    mode 1 (eager launches with CUDA events), so the reported kernel times were eager-mode."""
+    from paper_1907_03329_b200.trainer import Trainer
+
+    calls = []
+
+    class Lib:
+        def esrnn_trainer_profile_kernels(self, h, mode):
+            calls.append(mode)
+            return 0
+
+    class Api:
+        lib = Lib()
+
+    t = Trainer.__new__(Trainer)
+    t.api, t._h = Api(), None
+    t._chk = lambda rc: None
+    for m in (0, 1, 2, True, False):
+        t.profile_kernels(m)
+    assert calls == [0, 1, 2, 1, 0]
+    import pytest
+    with pytest.raises(ValueError):
+        t.profile_kernels(3)
