@@ -109,6 +109,7 @@ struct StateDev {
     unsigned* gtile_ctr;    // [tiles] arrival tickets of a tile's row parts
     int red_tiles;          // K3 weight-gradient output tiles
     int gemm_wide;          // 1: K3 weight gradients by q-strip blocks (finish.cuh dw_wide_block)
+    int tile_trigger_early; // 1: K2 releases K3 right after its wait (ESRNN_TILE_TRIGGER_EARLY)
     float* upart;           // [umma tiles][parts][128][64] tensor-core dW partials (fp32, large steps)
     int umma_tiles;         // 128-row matrix slices of the tensor-core dW path
     unsigned int* done_ctr; // [2]

@@ -405,6 +405,7 @@ struct esrnn_trainer {
         s.gtile_ctr = gtile_ctr.p;
         s.red_tiles = red_blocks;
         s.gemm_wide = wide ? 1 : 0;
+        s.tile_trigger_early = std::getenv("ESRNN_TILE_TRIGGER_EARLY") ? 1 : 0;
         s.upart = reinterpret_cast<float*>(upart.p);
         s.umma_tiles = umma_tiles;
         s.done_ctr = done_ctr.p;

@@ -464,8 +464,10 @@ __global__ void __launch_bounds__(NG == 2 ? 768 : ((RESIDENT || sizeof(Real) == 
         pdl_wait();
         // dependents (K3) may launch once every tile has passed its wait: the previous
         // step's K4 has then completed, so K3's pre-wait prologue may read the per-series
-        // parameters it wrote (K3 still waits for this grid's completion before the rest)
-        pdl_trigger();
+        // parameters it wrote (K3 still waits for this grid's completion before the rest).
+        // kTrain triggers after the forward pass instead (below), so K3's pre-wait work
+        // shares the SMs with the backward half only
+        if (MODE != kTrain || st.tile_trigger_early) pdl_trigger();
         if (MODE == kTrain) {
             DBG_SPAN_MIN(st, s, 1);
             DBG_SPAN_MIN(st, s - 1, 9);
@@ -624,6 +626,7 @@ __global__ void __launch_bounds__(NG == 2 ? 768 : ((RESIDENT || sizeof(Real) == 
         gsync();
         DBG_CLK(st, 2);
     }
+    if (MODE == kTrain && !st.tile_trigger_early) pdl_trigger();
     // head (network.hpp:207-209): z = tanh(h nl_w + nl_b); pred = z out_w + out_b
     const Real* cur = HT + (L - 1) * H * LD;
     if (!RESIDENT) {
